@@ -1,0 +1,324 @@
+#!/usr/bin/env python
+"""bench.py -- DAMAS on the wavelet-compressed grid, batched over frequency bins, on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--impl ours|reference]
+                  [--scaling weak|strong]
+
+One *step* = one pass of the whole hot path (S1..S8 of SURVEY §8(a): steering, fp64 DAS,
+fp64 wavelet threshold + compaction, PSF on the kept points, Gauss-Seidel sweeps, embed)
+over one band of synthetic input (BASELINE.json configs[2] = cfg3: 64 mics, 101x101 grid,
+256 bins 0.5-10 kHz, ~5% kept, 1000 sweeps) already resident in HBM.  The timed region is
+bracketed by barrier + cuda.synchronize, each step timed with CUDA events on the stream the
+library launches on, and the L2 is flushed (256 MiB write) between timed steps.
+
+Multi-GPU (torchrun, one rank per GPU, NCCL): bins are independent.  --scaling weak
+(default): every rank solves its own 256-bin band (per-rank seed), no data-path collective.
+--scaling strong: the 256 bins are strided over ranks and the maps are gathered once with
+all_gather_into_tensor at the end (inside the timed region).  Time = max over ranks.
+
+--impl reference: the fp64 CPU oracle (oracle/) as it stands, on this host's cores, timed
+on a bounded strided sample of the same workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "DAMAS freq-bins/s and PSF-stream HBM GB/s (compressed grid) at 1/2/4/8 B200"
+UNIT = "freq-bins/s"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d.get("hbm_gbs", 6650.0)), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def workload_desc(cfg):
+    kept = {"cfg2": "~10%", "cfg3": "~5%", "cfg5": "~8%"}.get(cfg.name, "full grid" if cfg.full_grid else "")
+    return (f"{cfg.name}: {cfg.m} mics ({cfg.aperture} m spiral), {cfg.n}x{cfg.n} grid (S={cfg.S}), "
+            f"{cfg.n_bins} bins {cfg.f_lo:g}-{cfg.f_hi:g} Hz, "
+            f"{'exact' if cfg.csm == 'exact' else f'{cfg.snapshots}-snapshot {cfg.snr_db:g} dB'} CSM, "
+            f"eps={cfg.epsilon} ({kept} kept), {cfg.sweeps} sweeps")
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        smax = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------ reference arm
+def run_reference(args, cfg):
+    import oracle
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cores = os.cpu_count() or 1
+    nb = args.ref_bins or max(4, min(16, cores))
+    bins = synth.strided_bins(cfg.n_bins, nb)
+    band = synth.make_band(cfg, bins=bins)
+    oracle.build()
+    times = []
+    for it in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        oracle.solve_band_cfg(band, n_threads=cores)
+        dt = time.perf_counter() - t0
+        if it >= args.warmup:
+            times.append(dt)
+    ms = 1000.0 * float(np.mean(times))
+    value = len(bins) / (ms / 1000.0)
+    sample = f"{len(bins)} strided bins of {cfg.n_bins} (full {cfg.sweeps} sweeps each), fp64 oracle, pthread pool"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_desc(cfg), "bins_per_step": len(bins)},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline(cfg, budget_bins=None):
+    """The oracle as it stands on the host cores, on a bounded strided sample."""
+    import oracle
+    cores = os.cpu_count() or 1
+    nb = budget_bins or max(4, min(16, cores))
+    bins = synth.strided_bins(cfg.n_bins, nb)
+    band = synth.make_band(cfg, bins=bins)
+    oracle.build()
+    t0 = time.perf_counter()
+    oracle.solve_band_cfg(band, n_threads=cores)
+    dt = time.perf_counter() - t0
+    return {"value": len(bins) / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{len(bins)} strided bins of {cfg.n_bins}, full {cfg.sweeps} sweeps, {dt:.1f} s wall"}
+
+
+# ------------------------------------------------------------------------------ our arm
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1608_05179_b200 import Context, Geometry
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+
+    # inputs: weak = own full band per rank (seed = rank); strong = strided shard of one band
+    if args.scaling == "weak" or world == 1:
+        band = synth.make_band(cfg, seed=rank)
+    else:
+        band = synth.make_band(cfg, bins=list(range(rank, cfg.n_bins, world)))
+    K = len(band.freqs)
+    geom = Geometry(band.mic_xyz, cfg.n, cfg.side_len, cfg.z0, cfg.c0, cfg.cx, cfg.cy)
+    csm_dev = torch.from_numpy(band.csm).to(dev)
+    ctx = Context(dev.index)
+    ctx.set_timing(True)
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    S = cfg.S
+    kmax = math.ceil(cfg.n_bins / world)
+    gather_x = None
+    if args.scaling == "strong" and world > 1:
+        gather_x = torch.empty((world, kmax, S), dtype=torch.float32, device=dev)
+        pad_x = torch.zeros((kmax, S), dtype=torch.float32, device=dev)
+
+    def step():
+        out = ctx.solve_band(geom, band.freqs, csm_dev, cfg.epsilon, cfg.sweeps, cfg.eps_mode,
+                             full_grid=cfg.full_grid, stream=stream)
+        if gather_x is not None:
+            pad_x[:K].copy_(out["x_map"])
+            dist.all_gather_into_tensor(gather_x, pad_x)
+        return out
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    clocks = ClockSampler(dev.index)
+    clocks.start()
+    ms_steps, st_list = [], []
+    for it in range(args.steps):
+        flush.zero_()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ms_steps.append(e0.elapsed_time(e1))
+        st_list.append(ctx.stats())
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clk = clocks.stop()
+
+    ms = float(np.mean(ms_steps))
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    total_bins = (K * world) if args.scaling == "weak" else cfg.n_bins
+    value = total_bins / (ms / 1000.0)
+
+    # roofline of the dominant kernel (GS sweep stream), per launch, CUDA-event timed
+    st = st_list[-1]
+    gs_ms = float(np.mean([s["ms_gs"] for s in st_list]))
+    algo_bytes = st["gs_bytes"]
+    achieved = algo_bytes / (gs_ms / 1000.0) / 1e9
+    peak, peak_src = load_peaks()
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "gs_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(cfg.name)
+        except Exception:
+            traffic = None
+    launches = int(sum(s["launches"] for s in st_list))
+
+    # e2e through the C ABI with host buffers (pinned), copies inside the timed region
+    csm_host = torch.from_numpy(band.csm).pin_memory()
+    h_out = {"n_keep": torch.empty(K, dtype=torch.int32).pin_memory(),
+             "keep_idx": torch.empty((K, S), dtype=torch.int32).pin_memory(),
+             "x_map": torch.empty((K, S), dtype=torch.float32).pin_memory(), "b_map": None}
+    ctx.solve_band_host(geom, band.freqs, csm_host, cfg.epsilon, cfg.sweeps, cfg.eps_mode, cfg.full_grid,
+                        out=h_out, stream=stream)
+    e2e_ms = []
+    for it in range(args.steps):
+        flush.zero_()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ctx.solve_band_host(geom, band.freqs, csm_host, cfg.epsilon, cfg.sweeps, cfg.eps_mode, cfg.full_grid,
+                            out=h_out, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        e2e_ms.append(e0.elapsed_time(e1))
+    ems = float(np.mean(e2e_ms))
+    if world > 1:
+        t = torch.tensor([ems], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ems = float(t.item())
+    e2e_value = ((K * world) if args.scaling == "weak" else cfg.n_bins) / (ems / 1000.0)
+    h2d = band.csm.nbytes
+    d2h = K * 4 + K * S * 4 + K * S * 4
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(cfg, args.ref_bins)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": args.scaling if world > 1 else "weak", "vs_baseline": None,
+            "dtype": "f32 (PSF + Gauss-Seidel); f64 (DAS map + wavelet threshold)", "data": "synthetic",
+            "config": {"workload": workload_desc(cfg), "bins_per_gpu": K, "parallelism": f"bins-dp{world}",
+                       "l2_flush": "256 MiB write between timed steps", "inputs": "CSMs resident in HBM"},
+            "psf_stream_gbs": achieved,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "gs_kernel",
+                         "algorithmic_bytes_per_launch": algo_bytes, "kernel_ms": gs_ms, "peak_source": peak_src},
+            "stage_ms": {"das": float(np.mean([s["ms_das"] for s in st_list])),
+                         "compress": float(np.mean([s["ms_compress"] for s in st_list])),
+                         "psf": float(np.mean([s["ms_psf"] for s in st_list])), "gs": gs_ms,
+                         "total_events": float(np.mean([s["ms_total"] for s in st_list]))},
+            "sum_keep": int(st["sum_keep"]), "mean_keep_frac": st["sum_keep"] / (K * S),
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": ems},
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--ref-bins", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    cfg = synth.CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

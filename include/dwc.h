@@ -1,0 +1,176 @@
+/*
+ * dwc.h -- C ABI of the B200-native DAMAS-on-wavelet-compressed-grid library.
+ *
+ * One data-parallel hot path (Ma & Liu, arXiv 1608.05179, /root/reference/PAPER.md):
+ * for every frequency bin of a band
+ *   S1 steering vectors            Eq. 3-4, 7
+ *   S2 DAS map b = diag(E^H C E)/M^2   Eq. 2
+ *   S3/S4 wavelet detail + threshold   Alg. 1, Eq. 15-22
+ *   S5 PSF on the kept points A = |E^H E|^2/M^2   Eq. 9-12, 23
+ *   S6 restrict b                  Eq. 23
+ *   S7 non-negative Gauss-Seidel   Eq. 13-14
+ *   S8 embed the solution on the full grid
+ * Readings of ambiguous passages are listed in DESIGN.md ("Readings" R1..R18).
+ *
+ * Conventions (all entry points):
+ *  - Every size is int32 and explicit; every struct is POD.
+ *  - "dev" pointers are CUDA device pointers on the context's device (e.g. torch
+ *    tensors); "host" pointers are ordinary host memory, read/written only during the
+ *    call.  The caller owns every buffer passed in; the library never frees or retains a
+ *    caller pointer after the call returns.
+ *  - Work is enqueued on `cuda_stream` (a cudaStream_t; NULL = legacy default stream).
+ *    Unless stated, calls return after enqueueing (results valid once the stream reaches
+ *    that point).  dwc_solve_band performs exactly one internal device->host read (the
+ *    kept-point counts, to size the PSF storage) and otherwise stays asynchronous.
+ *  - Argument validation happens on the host before any launch.  On failure the call
+ *    returns a negative dwc_status and dwc_last_error() describes it; no output is
+ *    written in that case, except DWC_ENUMERIC detected on device (outputs undefined).
+ *  - A context is used by one host thread at a time.  Different devices need different
+ *    contexts.
+ *  - Scan grid node s = row*n + col sits at x = cx - L/2 + col*dx, y = cy - L/2 + row*dx,
+ *    z = z0, dx = L/(n-1) (reading R17).
+ *  - A CSM is m*m complex128, row-major, C[i][j] at (i*m + j), interleaved (re, im)
+ *    (Eq. 1).  Only its Hermitian part affects the map (reading R3).
+ */
+#ifndef DWC_H
+#define DWC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define DWC_API __attribute__((visibility("default")))
+#else
+#define DWC_API
+#endif
+
+typedef struct dwc_ctx dwc_ctx; /* opaque; one per CUDA device */
+
+typedef enum {
+    DWC_OK = 0,
+    DWC_EINVAL = -1,     /* invalid argument (sizes, geometry, eps <= 0, sweeps < 1, NULL) */
+    DWC_ESINGULAR = -2,  /* a scan-grid node coincides with a microphone */
+    DWC_ENUMERIC = -3,   /* non-finite CSM/map value or A_ii <= 0 */
+    DWC_ENOMEM = -4,     /* device or pinned-host allocation failed */
+    DWC_ECUDA = -5,      /* CUDA runtime failure (message from the runtime) */
+    DWC_ESTATE = -6      /* wrong device / unsupported device (needs sm_100) */
+} dwc_status;
+
+/* Microphone array (Fig. 1 origin at the array centre). */
+typedef struct {
+    int32_t m;              /* number of microphones M, 2 <= m <= DWC_MAX_MICS */
+    const double *mic_xyz;  /* host, m*3 metres, (x, y, z) per microphone */
+    double c0;              /* speed of sound (m/s), > 0 */
+} dwc_array;
+
+/* Scan plane parallel to the array at distance z0. */
+typedef struct {
+    int32_t n;        /* nodes per side N >= 2, S = n*n */
+    double side_len;  /* L > 0 (m); dx = L/(n-1) */
+    double z0;        /* plane distance (m), > 0 */
+    double cx, cy;    /* plane centre (m) */
+} dwc_grid;
+
+/* Compression threshold and solver controls. */
+typedef struct {
+    double epsilon;   /* > 0; relative (eps * max|b|) or absolute */
+    int32_t eps_mode; /* 0 = relative, 1 = absolute (reading R6) */
+    int32_t sweeps;   /* Gauss-Seidel sweeps >= 1 from x0 = 0 */
+    int32_t flags;    /* DWC_FULL_GRID: keep every node (the paper's "original grid") */
+} dwc_params;
+
+#define DWC_FULL_GRID 1
+#define DWC_MAX_MICS 512
+
+/* Create / destroy a context on CUDA device `device`.  The device must be sm_100
+ * (B200).  dwc_destroy frees the context's workspace pool. */
+DWC_API dwc_status dwc_create(int device, dwc_ctx **out);
+DWC_API dwc_status dwc_destroy(dwc_ctx *ctx);
+
+/* ---- the batched hot path (S0..S8) ------------------------------------------------
+ * n_bins >= 1 frequency bins; freq_hz host[n_bins] (> 0).
+ * csm      dev  n_bins*m*m complex128 (interleaved), bin k at k*m*m.
+ * n_keep   dev  int32[n_bins]          (out) S~_k = number of kept nodes (>= |G^0|).
+ * keep_idx dev  int32[n_bins*S]        (out) kept node indices of bin k, ascending, at k*S;
+ *                                            entries n_keep[k]..S-1 are -1.
+ * x_map    dev  float[n_bins*S]        (out) DAMAS source-power descriptors on the full
+ *                                            grid after `sweeps` sweeps; 0 off the kept set.
+ * b_map    dev  double[n_bins*S]       (out, nullable) the DAS map of every bin.
+ * warn     host uint32[n_bins]         (out, nullable) bit0: dx/B > 0.2 at that bin
+ *                                      (Eq. 24 beamwidth).
+ * Errors: DWC_EINVAL, DWC_ESINGULAR, DWC_ENUMERIC, DWC_ENOMEM, DWC_ECUDA. */
+DWC_API dwc_status dwc_solve_band(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid,
+                          const dwc_params *p, int32_t n_bins, const double *freq_hz,
+                          const double *csm, int32_t *n_keep, int32_t *keep_idx,
+                          float *x_map, double *b_map, uint32_t *warn, void *cuda_stream);
+
+/* Same computation with HOST buffers (csm, n_keep, keep_idx, x_map, b_map all host; b_map
+ * nullable).  The host<->device copies are part of the call, which returns when the
+ * outputs are in host memory.  Page-locked (pinned) host buffers make the copies
+ * asynchronous DMA; pageable buffers work but are staged by the CUDA runtime. */
+DWC_API dwc_status dwc_solve_band_host(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid,
+                               const dwc_params *p, int32_t n_bins, const double *freq_hz,
+                               const double *csm, int32_t *n_keep, int32_t *keep_idx,
+                               float *x_map, double *b_map, uint32_t *warn, void *cuda_stream);
+
+/* ---- stage entry points (parity tests feed identical inputs to GPU and oracle) ---- */
+
+/* S1: normalised steering vectors e_s = sqrt(M) g_s/||g_s|| of n_pts nodes (reading R1).
+ * idx dev int32[n_pts]; E dev complex128 [n_pts][m] interleaved (out). */
+DWC_API dwc_status dwc_steer(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, double freq_hz,
+                     int32_t n_pts, const int32_t *idx, double *E, void *cuda_stream);
+
+/* S2: DAS maps b_k(s) = Re(e_s^H C_k e_s)/M^2 in fp64.  csm dev as in dwc_solve_band;
+ * b_map dev double[n_bins*S] (out). */
+DWC_API dwc_status dwc_das(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, int32_t n_bins,
+                   const double *freq_hz, const double *csm, double *b_map, void *cuda_stream);
+
+/* S3+S4: wavelet details in fp64 (no FMA contraction, reading R7 stencil) and threshold;
+ * b_map dev double[n_bins*S]; n_keep/keep_idx as in dwc_solve_band (out);
+ * level dev uint8[n_bins*S] (out, nullable): resolution level of each node (Eq. 15). */
+DWC_API dwc_status dwc_compress(dwc_ctx *ctx, const dwc_grid *grid, const dwc_params *p,
+                        int32_t n_bins, const double *b_map, int32_t *n_keep,
+                        int32_t *keep_idx, uint8_t *level, void *cuda_stream);
+
+/* S5: PSF matrix on n_keep nodes, A[i][j] = |e_i^H e_j|^2/M^2, fp32 accurate.
+ * keep_idx dev int32[n_keep]; A dev float[n_keep*n_keep] row-major (out). */
+DWC_API dwc_status dwc_psf(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, double freq_hz,
+                   int32_t n_keep, const int32_t *keep_idx, float *A, void *cuda_stream);
+
+/* S7: `sweeps` forward projected Gauss-Seidel sweeps from x0 = 0 on one system.
+ * A dev float[n*n] row-major (A_ii > 0), b dev double[n], x dev float[n] (out). */
+DWC_API dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int32_t sweeps,
+                  float *x, void *cuda_stream);
+
+/* ---- diagnostics ------------------------------------------------------------------ */
+
+/* Per-call statistics of the last dwc_solve_band / dwc_solve_band_host on this context.
+ * Stage times are measured with CUDA events on the call's stream only when timing is
+ * enabled (dwc_set_timing); reading them synchronises on those events. */
+typedef struct {
+    int32_t n_bins;
+    int64_t sum_keep;         /* sum_k S~_k */
+    double sum_keep_sq;       /* sum_k S~_k^2 */
+    double gs_bytes;          /* sum_k sweeps * bytes of A~_k as streamed by the GS kernel */
+    double psf_flops;         /* real flops of the PSF Gram (8*M*S~^2 per bin, full square) */
+    double das_flops;         /* real flops of the DAS quadratic forms (8*M^2*S per bin) */
+    int32_t launches;         /* kernels launched by the call */
+    float ms_total;           /* event time of the whole call (timing on) */
+    float ms_das, ms_compress, ms_psf, ms_gs; /* per-stage event times (timing on) */
+} dwc_stats;
+
+DWC_API dwc_status dwc_set_timing(dwc_ctx *ctx, int enable);
+DWC_API dwc_status dwc_get_stats(dwc_ctx *ctx, dwc_stats *out);
+
+DWC_API const char *dwc_last_error(void);            /* thread-local; valid until the next call */
+DWC_API size_t dwc_workspace_bytes(const dwc_ctx *ctx);
+DWC_API const char *dwc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DWC_H */

@@ -1,0 +1,579 @@
+// dwc_api.cu -- host side of the C ABI (include/dwc.h): validation, workspace pool,
+// per-call layout of the compressed systems, LPT schedule, stage orchestration, stats.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "dwc_internal.cuh"
+
+using namespace dwc;
+
+namespace {
+
+thread_local std::string g_err;
+
+dwc_status fail(dwc_status s, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+};
+
+struct PinBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+};
+
+enum FlagBits { kFlagNonFinite = 1, kFlagSingular = 4 };
+
+}  // namespace
+
+struct dwc_ctx {
+    int device = 0;
+    int num_sms = 148;
+    size_t total_bytes = 0;
+    DevBuf mic, freq, dist, amp, herm, bint, xplanes, bt, A, lay, order, counter, tiles, flag,
+        csm_h, nk_h, keep_h, xmap_h, bmap_h, gs_x, gs_b;
+    PinBuf stage, readback;
+    size_t stage_off = 0;
+    cudaEvent_t stage_done = nullptr;
+    int geo_m = -1, geo_n = -1;
+    bool timing = false;
+    cudaEvent_t ev[8] = {};
+    dwc_stats stats{};
+    bool stats_events_valid = false;
+};
+
+namespace {
+
+#define CU(call)                                                                       \
+    do {                                                                               \
+        cudaError_t e_ = (call);                                                       \
+        if (e_ != cudaSuccess)                                                         \
+            return fail(e_ == cudaErrorMemoryAllocation ? DWC_ENOMEM : DWC_ECUDA,      \
+                        "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+    } while (0)
+
+#define LAUNCH(expr)                                                                   \
+    do {                                                                               \
+        int n_ = (expr);                                                               \
+        if (n_ < 0) {                                                                  \
+            cudaError_t e_ = cudaGetLastError();                                       \
+            return fail(DWC_ECUDA, "launch %s: %s", #expr, cudaGetErrorString(e_));   \
+        }                                                                              \
+        launches += n_;                                                                \
+    } while (0)
+
+dwc_status ensure(dwc_ctx *ctx, DevBuf &b, size_t bytes) {
+    if (bytes <= b.bytes) return DWC_OK;
+    bytes = std::max(bytes, b.bytes + b.bytes / 4);  // grow geometrically
+    if (b.p) {
+        CU(cudaDeviceSynchronize());
+        CU(cudaFree(b.p));
+        ctx->total_bytes -= b.bytes;
+        b.p = nullptr;
+        b.bytes = 0;
+    }
+    cudaError_t e = cudaMalloc(&b.p, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(DWC_ENOMEM, "device allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
+    }
+    b.bytes = bytes;
+    ctx->total_bytes += bytes;
+    return DWC_OK;
+}
+
+dwc_status ensure_pin(PinBuf &b, size_t bytes) {
+    if (bytes <= b.bytes) return DWC_OK;
+    bytes = std::max(bytes, (size_t)64 << 10);
+    if (b.p) CU(cudaFreeHost(b.p));
+    b.p = nullptr;
+    b.bytes = 0;
+    cudaError_t e = cudaMallocHost(&b.p, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(DWC_ENOMEM, "pinned allocation of %zu bytes failed", bytes);
+    }
+    b.bytes = bytes;
+    return DWC_OK;
+}
+
+// Staging of small host arrays into device buffers through a pinned bump buffer.  The
+// buffer is reused only after the previous call's copies completed (event).
+dwc_status stage_begin(dwc_ctx *ctx, size_t need) {
+    CU(cudaEventSynchronize(ctx->stage_done));
+    dwc_status s = ensure_pin(ctx->stage, need + 4096);
+    if (s) return s;
+    ctx->stage_off = 0;
+    return DWC_OK;
+}
+
+dwc_status stage_upload(dwc_ctx *ctx, void *dst, const void *src, size_t bytes, cudaStream_t st) {
+    if (bytes == 0) return DWC_OK;
+    size_t off = (ctx->stage_off + 255) & ~(size_t)255;
+    if (off + bytes > ctx->stage.bytes) return fail(DWC_ECUDA, "internal: staging overflow");
+    char *p = (char *)ctx->stage.p + off;
+    memcpy(p, src, bytes);
+    CU(cudaMemcpyAsync(dst, p, bytes, cudaMemcpyHostToDevice, st));
+    ctx->stage_off = off + bytes;
+    return DWC_OK;
+}
+
+dwc_status stage_end(dwc_ctx *ctx, cudaStream_t st) {
+    CU(cudaEventRecord(ctx->stage_done, st));
+    return DWC_OK;
+}
+
+bool finite(double v) { return std::isfinite(v); }
+
+dwc_status check_ctx(dwc_ctx *ctx) {
+    if (!ctx) return fail(DWC_EINVAL, "ctx is NULL");
+    int cur = -1;
+    CU(cudaGetDevice(&cur));
+    if (cur != ctx->device) CU(cudaSetDevice(ctx->device));
+    return DWC_OK;
+}
+
+dwc_status check_array(const dwc_array *a) {
+    if (!a) return fail(DWC_EINVAL, "array is NULL");
+    if (a->m < 2 || a->m > DWC_MAX_MICS) return fail(DWC_EINVAL, "m = %d outside [2, %d]", a->m, DWC_MAX_MICS);
+    if (!a->mic_xyz) return fail(DWC_EINVAL, "mic_xyz is NULL");
+    if (!(a->c0 > 0.0) || !finite(a->c0)) return fail(DWC_EINVAL, "c0 must be > 0 and finite");
+    for (int i = 0; i < 3 * a->m; i++)
+        if (!finite(a->mic_xyz[i])) return fail(DWC_EINVAL, "mic_xyz[%d] is not finite", i);
+    return DWC_OK;
+}
+
+dwc_status check_grid(const dwc_grid *g) {
+    if (!g) return fail(DWC_EINVAL, "grid is NULL");
+    if (g->n < 2 || g->n > 46340) return fail(DWC_EINVAL, "n = %d outside [2, 46340]", g->n);
+    if (!(g->side_len > 0.0) || !finite(g->side_len)) return fail(DWC_EINVAL, "side_len must be > 0");
+    if (!(g->z0 > 0.0) || !finite(g->z0)) return fail(DWC_EINVAL, "z0 must be > 0");
+    if (!finite(g->cx) || !finite(g->cy)) return fail(DWC_EINVAL, "plane centre not finite");
+    return DWC_OK;
+}
+
+dwc_status check_params(const dwc_params *p) {
+    if (!p) return fail(DWC_EINVAL, "params is NULL");
+    if (!(p->epsilon > 0.0) || !finite(p->epsilon)) return fail(DWC_EINVAL, "epsilon must be > 0");
+    if (p->eps_mode != 0 && p->eps_mode != 1) return fail(DWC_EINVAL, "eps_mode must be 0 or 1");
+    if (p->sweeps < 1) return fail(DWC_EINVAL, "sweeps must be >= 1");
+    if (p->flags & ~DWC_FULL_GRID) return fail(DWC_EINVAL, "unknown flags 0x%x", p->flags);
+    return DWC_OK;
+}
+
+dwc_status check_freqs(int n_bins, const double *f) {
+    if (n_bins < 1) return fail(DWC_EINVAL, "n_bins must be >= 1");
+    if (!f) return fail(DWC_EINVAL, "freq_hz is NULL");
+    for (int k = 0; k < n_bins; k++)
+        if (!(f[k] > 0.0) || !finite(f[k])) return fail(DWC_EINVAL, "freq_hz[%d] must be > 0", k);
+    return DWC_OK;
+}
+
+Geo make_geo(dwc_ctx *ctx, const dwc_array *a, const dwc_grid *g) {
+    Geo G;
+    G.m = a->m;
+    G.n = g->n;
+    G.S = g->n * g->n;
+    G.L = g->side_len;
+    G.z0 = g->z0;
+    G.cx = g->cx;
+    G.cy = g->cy;
+    G.dx = g->side_len / (double)(g->n - 1);
+    G.c0 = a->c0;
+    G.mic = (const double *)ctx->mic.p;
+    return G;
+}
+
+// Upload mic + frequencies, build the steering tables.  Returns the launch count via *launches.
+dwc_status prepare_geometry(dwc_ctx *ctx, const dwc_array *a, const dwc_grid *g, int n_freq,
+                            const double *freq, Geo &G, int &launches, cudaStream_t st) {
+    dwc_status s;
+    const size_t S = (size_t)g->n * g->n;
+    if ((s = ensure(ctx, ctx->mic, sizeof(double) * 3 * a->m))) return s;
+    if ((s = ensure(ctx, ctx->freq, sizeof(double) * std::max(n_freq, 1)))) return s;
+    if ((s = ensure(ctx, ctx->dist, sizeof(double) * a->m * S))) return s;
+    if ((s = ensure(ctx, ctx->amp, sizeof(double) * a->m * S))) return s;
+    if ((s = ensure(ctx, ctx->flag, 64))) return s;
+    if ((s = stage_begin(ctx, sizeof(double) * (3 * a->m + n_freq) + 1024))) return s;
+    if ((s = stage_upload(ctx, ctx->mic.p, a->mic_xyz, sizeof(double) * 3 * a->m, st))) return s;
+    if (n_freq > 0 && (s = stage_upload(ctx, ctx->freq.p, freq, sizeof(double) * n_freq, st))) return s;
+    if ((s = stage_end(ctx, st))) return s;
+    CU(cudaMemsetAsync(ctx->flag.p, 0, 64, st));
+    G = make_geo(ctx, a, g);
+    LAUNCH(launch_geom_tables(G, (double *)ctx->dist.p, (double *)ctx->amp.p, (int *)ctx->flag.p, st));
+    return DWC_OK;
+}
+
+void ev(dwc_ctx *ctx, int i, cudaStream_t st) {
+    if (ctx->timing) cudaEventRecord(ctx->ev[i], st);
+}
+
+// The batched path on device buffers.
+dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, const dwc_params *p,
+                          int n_bins, const double *freq, const double *csm, int32_t *n_keep,
+                          int32_t *keep_idx, float *x_map, double *b_map, uint32_t *warn,
+                          cudaStream_t st) {
+    dwc_status s;
+    int launches = 0;
+    const int M = arr->m, n = grid->n;
+    const int S = n * n;
+    ev(ctx, 0, st);
+    Geo G;
+    if ((s = prepare_geometry(ctx, arr, grid, n_bins, freq, G, launches, st))) return s;
+    // S2 DAS on the Hermitian part of each CSM
+    if ((s = ensure(ctx, ctx->herm, sizeof(double) * 2 * (size_t)n_bins * M * M))) return s;
+    double *b = b_map;
+    if (!b) {
+        if ((s = ensure(ctx, ctx->bint, sizeof(double) * (size_t)n_bins * S))) return s;
+        b = (double *)ctx->bint.p;
+    }
+    LAUNCH(launch_hermitize(M, n_bins, csm, (double *)ctx->herm.p, st));
+    LAUNCH(launch_das(G, (double *)ctx->dist.p, (double *)ctx->amp.p, n_bins, (double *)ctx->freq.p,
+                      (double *)ctx->herm.p, b, st));
+    ev(ctx, 1, st);
+    // S3+S4
+    LAUNCH(launch_compress(n, n_bins, b, p->epsilon, p->eps_mode, (p->flags & DWC_FULL_GRID) ? 1 : 0,
+                           n_keep, keep_idx, nullptr, (int *)ctx->flag.p, st));
+    ev(ctx, 2, st);
+    // the single device->host read: kept counts (+ error flags)
+    if ((s = ensure_pin(ctx->readback, sizeof(int32_t) * (n_bins + 16)))) return s;
+    int32_t *hk = (int32_t *)ctx->readback.p;
+    CU(cudaMemcpyAsync(hk, n_keep, sizeof(int32_t) * n_bins, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(hk + n_bins, ctx->flag.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    const int flags = hk[n_bins];
+    if (flags & kFlagSingular) return fail(DWC_ESINGULAR, "a scan-grid node coincides with a microphone");
+    if (flags & kFlagNonFinite) return fail(DWC_ENUMERIC, "non-finite value in the CSM / DAS map");
+    // host layout of the compressed systems
+    std::vector<BinLayout> lay(n_bins);
+    int64_t a_off = 0, v_off = 0;
+    int max_sp = 0;
+    double sum_sq = 0.0;
+    int64_t sum_k = 0;
+    for (int k = 0; k < n_bins; k++) {
+        const int nk = hk[k];
+        const int sp = (nk + 31) & ~31;
+        lay[k] = {nk, sp, a_off, v_off};
+        a_off += (int64_t)sp * sp;
+        v_off += sp;
+        max_sp = std::max(max_sp, sp);
+        sum_sq += (double)nk * nk;
+        sum_k += nk;
+    }
+    if (max_sp * 4 + 20 * 1024 > 227 * 1024)
+        return fail(DWC_EINVAL, "compressed grid of %d points exceeds the on-chip x capacity", max_sp);
+    std::vector<int32_t> order(n_bins);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b2) { return hk[a] > hk[b2]; });
+    std::vector<int4> tiles;
+    for (int k = 0; k < n_bins; k++) {
+        const int T = (lay[k].sp + 63) / 64;
+        for (int I = 0; I < T; I++)
+            for (int J = I; J < T; J++) tiles.push_back(make_int4(k, I, J, 0));
+    }
+    if ((s = ensure(ctx, ctx->lay, sizeof(BinLayout) * n_bins))) return s;
+    if ((s = ensure(ctx, ctx->order, sizeof(int32_t) * n_bins))) return s;
+    if ((s = ensure(ctx, ctx->tiles, sizeof(int4) * std::max<size_t>(tiles.size(), 1)))) return s;
+    if ((s = ensure(ctx, ctx->counter, 64))) return s;
+    if ((s = ensure(ctx, ctx->xplanes, sizeof(float) * 2 * M * (size_t)v_off))) return s;
+    if ((s = ensure(ctx, ctx->bt, sizeof(float) * (size_t)v_off))) return s;
+    if ((s = ensure(ctx, ctx->A, sizeof(float) * (size_t)a_off))) return s;
+    if ((s = stage_begin(ctx, sizeof(BinLayout) * n_bins + sizeof(int32_t) * n_bins +
+                                  sizeof(int4) * tiles.size() + 4096))) return s;
+    if ((s = stage_upload(ctx, ctx->lay.p, lay.data(), sizeof(BinLayout) * n_bins, st))) return s;
+    if ((s = stage_upload(ctx, ctx->order.p, order.data(), sizeof(int32_t) * n_bins, st))) return s;
+    if ((s = stage_upload(ctx, ctx->tiles.p, tiles.data(), sizeof(int4) * tiles.size(), st))) return s;
+    if ((s = stage_end(ctx, st))) return s;
+    ev(ctx, 3, st);
+    // S5 (+S6)
+    LAUNCH(launch_steer_kept(G, (double *)ctx->dist.p, (double *)ctx->amp.p, n_bins, (double *)ctx->freq.p,
+                             (BinLayout *)ctx->lay.p, keep_idx, b, (float *)ctx->xplanes.p,
+                             (float *)ctx->bt.p, max_sp, st));
+    LAUNCH(launch_gram(M, (int)tiles.size(), (int4 *)ctx->tiles.p, (BinLayout *)ctx->lay.p,
+                       (float *)ctx->xplanes.p, (float *)ctx->A.p, st));
+    ev(ctx, 4, st);
+    // S7 + S8
+    CU(cudaMemsetAsync(x_map, 0, sizeof(float) * (size_t)n_bins * S, st));
+    CU(cudaMemsetAsync(ctx->counter.p, 0, 64, st));
+    ev(ctx, 5, st);
+    LAUNCH(launch_gs(n_bins, (BinLayout *)ctx->lay.p, max_sp, (int32_t *)ctx->order.p, (int *)ctx->counter.p,
+                     (float *)ctx->A.p, (float *)ctx->bt.p, p->sweeps, nullptr, x_map, keep_idx, S,
+                     ctx->num_sms, st));
+    ev(ctx, 6, st);
+    // warnings (host, Eq. 24)
+    if (warn) {
+        double rmax = 0.0;
+        for (int i = 0; i < M; i++)
+            rmax = std::max(rmax, sqrt(arr->mic_xyz[3 * i] * arr->mic_xyz[3 * i] +
+                                       arr->mic_xyz[3 * i + 1] * arr->mic_xyz[3 * i + 1]));
+        const double phi = atan(grid->side_len / (2.0 * grid->z0));
+        const double dx = grid->side_len / (double)(n - 1);
+        for (int k = 0; k < n_bins; k++) {
+            const double cp = cos(phi);
+            const double B = 1.22 * grid->z0 * arr->c0 / (cp * cp * cp * 2.0 * rmax * freq[k]);
+            warn[k] = (dx / B > 0.2) ? 1u : 0u;
+        }
+    }
+    dwc_stats &stt = ctx->stats;
+    stt = dwc_stats{};
+    stt.n_bins = n_bins;
+    stt.sum_keep = sum_k;
+    stt.sum_keep_sq = sum_sq;
+    stt.gs_bytes = 4.0 * sum_sq * p->sweeps;
+    stt.psf_flops = 8.0 * M * sum_sq;
+    stt.das_flops = 8.0 * (double)M * M * S * n_bins;
+    stt.launches = launches;
+    ctx->stats_events_valid = ctx->timing;
+    return DWC_OK;
+}
+
+}  // namespace
+
+// =====================================================================================
+extern "C" {
+
+const char *dwc_version(void) { return "dwc 0.1 (sm_100a)"; }
+
+const char *dwc_last_error(void) { return g_err.c_str(); }
+
+size_t dwc_workspace_bytes(const dwc_ctx *ctx) { return ctx ? ctx->total_bytes : 0; }
+
+dwc_status dwc_create(int device, dwc_ctx **out) {
+    if (!out) return fail(DWC_EINVAL, "out is NULL");
+    *out = nullptr;
+    int count = 0;
+    CU(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) return fail(DWC_EINVAL, "device %d not present (%d devices)", device, count);
+    cudaDeviceProp prop;
+    CU(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10 || prop.minor != 0)
+        return fail(DWC_ESTATE, "device %d is sm_%d%d; this library is built for sm_100a (B200)", device,
+                    prop.major, prop.minor);
+    CU(cudaSetDevice(device));
+    dwc_ctx *c = new dwc_ctx();
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    if (cudaEventCreateWithFlags(&c->stage_done, cudaEventDisableTiming) != cudaSuccess) {
+        delete c;
+        return fail(DWC_ECUDA, "event creation failed");
+    }
+    for (auto &e : c->ev) cudaEventCreate(&e);
+    *out = c;
+    return DWC_OK;
+}
+
+dwc_status dwc_destroy(dwc_ctx *ctx) {
+    if (!ctx) return DWC_OK;
+    cudaSetDevice(ctx->device);
+    cudaDeviceSynchronize();
+    DevBuf *bufs[] = {&ctx->mic, &ctx->freq, &ctx->dist, &ctx->amp, &ctx->herm, &ctx->bint, &ctx->xplanes,
+                      &ctx->bt, &ctx->A, &ctx->lay, &ctx->order, &ctx->counter, &ctx->tiles, &ctx->flag,
+                      &ctx->csm_h, &ctx->nk_h, &ctx->keep_h, &ctx->xmap_h, &ctx->bmap_h, &ctx->gs_x, &ctx->gs_b};
+    for (DevBuf *b : bufs)
+        if (b->p) cudaFree(b->p);
+    if (ctx->stage.p) cudaFreeHost(ctx->stage.p);
+    if (ctx->readback.p) cudaFreeHost(ctx->readback.p);
+    if (ctx->stage_done) cudaEventDestroy(ctx->stage_done);
+    for (auto &e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    delete ctx;
+    return DWC_OK;
+}
+
+dwc_status dwc_set_timing(dwc_ctx *ctx, int enable) {
+    if (!ctx) return fail(DWC_EINVAL, "ctx is NULL");
+    ctx->timing = enable != 0;
+    return DWC_OK;
+}
+
+dwc_status dwc_get_stats(dwc_ctx *ctx, dwc_stats *out) {
+    if (!ctx || !out) return fail(DWC_EINVAL, "NULL argument");
+    dwc_stats s = ctx->stats;
+    if (ctx->stats_events_valid) {
+        CU(cudaEventSynchronize(ctx->ev[6]));
+        cudaEventElapsedTime(&s.ms_total, ctx->ev[0], ctx->ev[6]);
+        cudaEventElapsedTime(&s.ms_das, ctx->ev[0], ctx->ev[1]);
+        cudaEventElapsedTime(&s.ms_compress, ctx->ev[1], ctx->ev[2]);
+        cudaEventElapsedTime(&s.ms_psf, ctx->ev[3], ctx->ev[4]);
+        cudaEventElapsedTime(&s.ms_gs, ctx->ev[5], ctx->ev[6]);
+    }
+    *out = s;
+    return DWC_OK;
+}
+
+dwc_status dwc_solve_band(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, const dwc_params *p,
+                          int32_t n_bins, const double *freq_hz, const double *csm, int32_t *n_keep,
+                          int32_t *keep_idx, float *x_map, double *b_map, uint32_t *warn,
+                          void *cuda_stream) {
+    dwc_status s;
+    if ((s = check_ctx(ctx)) || (s = check_array(arr)) || (s = check_grid(grid)) || (s = check_params(p)) ||
+        (s = check_freqs(n_bins, freq_hz)))
+        return s;
+    if (!csm || !n_keep || !keep_idx || !x_map) return fail(DWC_EINVAL, "NULL device buffer");
+    return solve_band_dev(ctx, arr, grid, p, n_bins, freq_hz, csm, n_keep, keep_idx, x_map, b_map, warn,
+                          (cudaStream_t)cuda_stream);
+}
+
+dwc_status dwc_solve_band_host(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid,
+                               const dwc_params *p, int32_t n_bins, const double *freq_hz,
+                               const double *csm, int32_t *n_keep, int32_t *keep_idx, float *x_map,
+                               double *b_map, uint32_t *warn, void *cuda_stream) {
+    dwc_status s;
+    if ((s = check_ctx(ctx)) || (s = check_array(arr)) || (s = check_grid(grid)) || (s = check_params(p)) ||
+        (s = check_freqs(n_bins, freq_hz)))
+        return s;
+    if (!csm || !n_keep || !keep_idx || !x_map) return fail(DWC_EINVAL, "NULL host buffer");
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    const size_t S = (size_t)grid->n * grid->n, M = arr->m;
+    const size_t csm_b = sizeof(double) * 2 * M * M * n_bins;
+    if ((s = ensure(ctx, ctx->csm_h, csm_b)) || (s = ensure(ctx, ctx->nk_h, sizeof(int32_t) * n_bins)) ||
+        (s = ensure(ctx, ctx->keep_h, sizeof(int32_t) * S * n_bins)) ||
+        (s = ensure(ctx, ctx->xmap_h, sizeof(float) * S * n_bins)))
+        return s;
+    if (b_map && (s = ensure(ctx, ctx->bmap_h, sizeof(double) * S * n_bins))) return s;
+    CU(cudaMemcpyAsync(ctx->csm_h.p, csm, csm_b, cudaMemcpyHostToDevice, st));
+    s = solve_band_dev(ctx, arr, grid, p, n_bins, freq_hz, (double *)ctx->csm_h.p, (int32_t *)ctx->nk_h.p,
+                       (int32_t *)ctx->keep_h.p, (float *)ctx->xmap_h.p,
+                       b_map ? (double *)ctx->bmap_h.p : nullptr, warn, st);
+    if (s) return s;
+    CU(cudaMemcpyAsync(n_keep, ctx->nk_h.p, sizeof(int32_t) * n_bins, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(keep_idx, ctx->keep_h.p, sizeof(int32_t) * S * n_bins, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(x_map, ctx->xmap_h.p, sizeof(float) * S * n_bins, cudaMemcpyDeviceToHost, st));
+    if (b_map) CU(cudaMemcpyAsync(b_map, ctx->bmap_h.p, sizeof(double) * S * n_bins, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    return DWC_OK;
+}
+
+dwc_status dwc_steer(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, double freq_hz,
+                     int32_t n_pts, const int32_t *idx, double *E, void *cuda_stream) {
+    dwc_status s;
+    if ((s = check_ctx(ctx)) || (s = check_array(arr)) || (s = check_grid(grid)) || (s = check_freqs(1, &freq_hz)))
+        return s;
+    if (n_pts < 0 || (n_pts > 0 && (!idx || !E))) return fail(DWC_EINVAL, "bad n_pts / NULL buffer");
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    int launches = 0;
+    Geo G;
+    if ((s = prepare_geometry(ctx, arr, grid, 1, &freq_hz, G, launches, st))) return s;
+    LAUNCH(launch_steer(G, (double *)ctx->dist.p, (double *)ctx->amp.p, (double *)ctx->freq.p, n_pts, idx, E, st));
+    return DWC_OK;
+}
+
+dwc_status dwc_das(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, int32_t n_bins,
+                   const double *freq_hz, const double *csm, double *b_map, void *cuda_stream) {
+    dwc_status s;
+    if ((s = check_ctx(ctx)) || (s = check_array(arr)) || (s = check_grid(grid)) || (s = check_freqs(n_bins, freq_hz)))
+        return s;
+    if (!csm || !b_map) return fail(DWC_EINVAL, "NULL device buffer");
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    int launches = 0;
+    Geo G;
+    if ((s = prepare_geometry(ctx, arr, grid, n_bins, freq_hz, G, launches, st))) return s;
+    if ((s = ensure(ctx, ctx->herm, sizeof(double) * 2 * (size_t)n_bins * arr->m * arr->m))) return s;
+    LAUNCH(launch_hermitize(arr->m, n_bins, csm, (double *)ctx->herm.p, st));
+    LAUNCH(launch_das(G, (double *)ctx->dist.p, (double *)ctx->amp.p, n_bins, (double *)ctx->freq.p,
+                      (double *)ctx->herm.p, b_map, st));
+    return DWC_OK;
+}
+
+dwc_status dwc_compress(dwc_ctx *ctx, const dwc_grid *grid, const dwc_params *p, int32_t n_bins,
+                        const double *b_map, int32_t *n_keep, int32_t *keep_idx, uint8_t *level,
+                        void *cuda_stream) {
+    dwc_status s;
+    if ((s = check_ctx(ctx)) || (s = check_grid(grid)) || (s = check_params(p))) return s;
+    if (n_bins < 1) return fail(DWC_EINVAL, "n_bins must be >= 1");
+    if (!b_map || !n_keep || !keep_idx) return fail(DWC_EINVAL, "NULL device buffer");
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    int launches = 0;
+    if ((s = ensure(ctx, ctx->flag, 64))) return s;
+    LAUNCH(launch_compress(grid->n, n_bins, b_map, p->epsilon, p->eps_mode, (p->flags & DWC_FULL_GRID) ? 1 : 0,
+                           n_keep, keep_idx, level, (int *)ctx->flag.p, st));
+    return DWC_OK;
+}
+
+dwc_status dwc_psf(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, double freq_hz,
+                   int32_t n_keep, const int32_t *keep_idx, float *A, void *cuda_stream) {
+    dwc_status s;
+    if ((s = check_ctx(ctx)) || (s = check_array(arr)) || (s = check_grid(grid)) || (s = check_freqs(1, &freq_hz)))
+        return s;
+    const int S = grid->n * grid->n;
+    if (n_keep < 1 || n_keep > S) return fail(DWC_EINVAL, "n_keep = %d outside [1, S]", n_keep);
+    if (!keep_idx || !A) return fail(DWC_EINVAL, "NULL device buffer");
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    int launches = 0;
+    Geo G;
+    if ((s = prepare_geometry(ctx, arr, grid, 1, &freq_hz, G, launches, st))) return s;
+    const int sp = (n_keep + 31) & ~31;
+    BinLayout lay{n_keep, sp, 0, 0};
+    std::vector<int4> tiles;
+    const int T = (sp + 63) / 64;
+    for (int I = 0; I < T; I++)
+        for (int J = I; J < T; J++) tiles.push_back(make_int4(0, I, J, 0));
+    if ((s = ensure(ctx, ctx->lay, sizeof(BinLayout))) || (s = ensure(ctx, ctx->tiles, sizeof(int4) * tiles.size())) ||
+        (s = ensure(ctx, ctx->xplanes, sizeof(float) * 2 * arr->m * (size_t)sp)) ||
+        (s = ensure(ctx, ctx->bt, sizeof(float) * sp)) || (s = ensure(ctx, ctx->A, sizeof(float) * (size_t)sp * sp)))
+        return s;
+    if ((s = stage_begin(ctx, sizeof(BinLayout) + sizeof(int4) * tiles.size() + 1024))) return s;
+    if ((s = stage_upload(ctx, ctx->lay.p, &lay, sizeof(BinLayout), st))) return s;
+    if ((s = stage_upload(ctx, ctx->tiles.p, tiles.data(), sizeof(int4) * tiles.size(), st))) return s;
+    if ((s = stage_end(ctx, st))) return s;
+    LAUNCH(launch_steer_kept(G, (double *)ctx->dist.p, (double *)ctx->amp.p, 1, (double *)ctx->freq.p,
+                             (BinLayout *)ctx->lay.p, keep_idx, nullptr, (float *)ctx->xplanes.p,
+                             (float *)ctx->bt.p, sp, st));
+    LAUNCH(launch_gram(arr->m, (int)tiles.size(), (int4 *)ctx->tiles.p, (BinLayout *)ctx->lay.p,
+                       (float *)ctx->xplanes.p, (float *)ctx->A.p, st));
+    CU(cudaMemcpy2DAsync(A, sizeof(float) * n_keep, ctx->A.p, sizeof(float) * sp, sizeof(float) * n_keep, n_keep,
+                         cudaMemcpyDeviceToDevice, st));
+    return DWC_OK;
+}
+
+dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int32_t sweeps, float *x,
+                  void *cuda_stream) {
+    dwc_status s;
+    if ((s = check_ctx(ctx))) return s;
+    if (n < 1) return fail(DWC_EINVAL, "n must be >= 1");
+    if (sweeps < 1) return fail(DWC_EINVAL, "sweeps must be >= 1");
+    if (!A || !b || !x) return fail(DWC_EINVAL, "NULL device buffer");
+    const int sp = (n + 31) & ~31;
+    if (sp * 4 + 20 * 1024 > 227 * 1024) return fail(DWC_EINVAL, "n = %d exceeds the on-chip x capacity", n);
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    int launches = 0;
+    BinLayout lay{n, sp, 0, 0};
+    int32_t order0 = 0;
+    if ((s = ensure(ctx, ctx->lay, sizeof(BinLayout))) || (s = ensure(ctx, ctx->order, sizeof(int32_t))) ||
+        (s = ensure(ctx, ctx->counter, 64)) || (s = ensure(ctx, ctx->gs_b, sizeof(float) * sp)) ||
+        (s = ensure(ctx, ctx->gs_x, sizeof(float) * (size_t)sp * sp)))
+        return s;
+    if ((s = stage_begin(ctx, 1024))) return s;
+    if ((s = stage_upload(ctx, ctx->lay.p, &lay, sizeof(BinLayout), st))) return s;
+    if ((s = stage_upload(ctx, ctx->order.p, &order0, sizeof(int32_t), st))) return s;
+    if ((s = stage_end(ctx, st))) return s;
+    float *Ap = (float *)ctx->gs_x.p;
+    CU(cudaMemsetAsync(Ap, 0, sizeof(float) * (size_t)sp * sp, st));
+    CU(cudaMemcpy2DAsync(Ap, sizeof(float) * sp, A, sizeof(float) * n, sizeof(float) * n, n,
+                         cudaMemcpyDeviceToDevice, st));
+    CU(cudaMemsetAsync(ctx->gs_b.p, 0, sizeof(float) * sp, st));
+    LAUNCH(launch_f64_to_f32(b, (float *)ctx->gs_b.p, n, st));
+    CU(cudaMemsetAsync(ctx->counter.p, 0, 64, st));
+    LAUNCH(launch_gs(1, (BinLayout *)ctx->lay.p, sp, (int32_t *)ctx->order.p, (int *)ctx->counter.p, Ap,
+                     (float *)ctx->gs_b.p, sweeps, x, nullptr, nullptr, 0, ctx->num_sms, st));
+    return DWC_OK;
+}
+
+}  // extern "C"

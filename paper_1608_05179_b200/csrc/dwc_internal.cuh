@@ -1,0 +1,77 @@
+// dwc_internal.cuh -- internal declarations of the B200 (sm_100a) implementation behind
+// include/dwc.h.  Nothing here is visible through the C ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/dwc.h"
+
+namespace dwc {
+
+// Scan-grid + array geometry as the kernels see it (all fp64, device pointers).
+struct Geo {
+    int m;          // microphones
+    int n;          // nodes per side
+    int S;          // n*n
+    double L, z0, cx, cy, dx, c0;
+    const double *mic;  // dev m*3
+};
+
+__host__ __device__ inline double node_x(const Geo &g, int c) { return g.cx - g.L / 2.0 + (double)c * g.dx; }
+__host__ __device__ inline double node_y(const Geo &g, int r) { return g.cy - g.L / 2.0 + (double)r * g.dx; }
+
+constexpr double kTwoPi = 6.283185307179586476925286766559;
+
+// ---- launchers (each returns the number of kernels it launched, or -1 on launch error)
+
+// Frequency-independent steering tables: dist[m][s] = |r_s - r_m| and
+// amp[m][s] = sqrt(M) / (dist * ||g_s||) with ||g_s||^2 = sum_m 1/dist^2 (reading R1).
+// Sets *singular (dev int) to 1 when some distance is 0.
+int launch_geom_tables(const Geo &g, double *dist, double *amp, int *flag, cudaStream_t st);
+
+// S1 for a list of nodes: E[pt][m] complex128 interleaved.
+int launch_steer(const Geo &g, const double *dist, const double *amp, const double *freq,
+                 int n_pts, const int32_t *idx, double *E, cudaStream_t st);
+
+// Hermitian part of the CSMs (reading R3), into H (dev, same layout).
+int launch_hermitize(int M, int n_bins, const double *csm, double *H, cudaStream_t st);
+
+// S2: b[k][s] for n_bins bins; freq dev[n_bins]; csm dev.
+int launch_das(const Geo &g, const double *dist, const double *amp, int n_bins,
+               const double *freq, const double *csm, double *b, cudaStream_t st);
+
+// S3+S4: compaction of kept nodes.  flag (dev int): bit 1 set when b has a non-finite value.
+int launch_compress(int n, int n_bins, const double *b, double eps, int eps_mode, int full_grid,
+                    int32_t *n_keep, int32_t *keep_idx, uint8_t *level, int *flag,
+                    cudaStream_t st);
+
+// Per-bin layout of the compressed systems, built on the host after n_keep is known.
+struct BinLayout {
+    int32_t nk;       // S~
+    int32_t sp;       // padded size (multiple of 32)
+    int64_t a_off;    // float offset of A~_k (sp*sp dense row-major)
+    int64_t v_off;    // float offset of per-bin vectors (sp entries) and of the E planes / sp
+};
+
+// S5 part 1: kept steering planes X[k] = [Re E~; Im E~] as fp32 (2m rows x sp cols) and
+// bt[k][i] = b[k][keep[i]] (S6, fp32), zero padded to sp.
+// b may be NULL (bt then untouched).  Grid spans max_sp columns.
+int launch_steer_kept(const Geo &g, const double *dist, const double *amp, int n_bins,
+                      const double *freq, const BinLayout *lay, const int32_t *keep_idx,
+                      const double *b, float *xplanes, float *bt, int max_sp, cudaStream_t st);
+
+// S5 part 2: A~_k = |E~^H E~|^2 / M^2 (dense, both triangles written) over a list of
+// 64x64 upper tile pairs (bin, I, J, -).
+int launch_gram(int m, int n_tiles, const int4 *tiles, const BinLayout *lay_dev,
+                const float *xplanes, float *A, cudaStream_t st);
+
+// fp64 -> fp32 copy (dwc_gs right-hand side).
+int launch_f64_to_f32(const double *src, float *dst, int n, cudaStream_t st);
+
+// S7+S8: Gauss-Seidel sweeps, LPT-ordered persistent kernel; writes x_out (per bin at
+// v_off, nullable) and scatters into x_map[k*S + keep[i]] (nullable).
+int launch_gs(int n_bins, const BinLayout *lay_dev, int max_sp, const int32_t *order,
+              int *counter, const float *A, const float *bt, int sweeps, float *x_out,
+              float *x_map, const int32_t *keep_idx, int S, int num_sms, cudaStream_t st);
+
+}  // namespace dwc

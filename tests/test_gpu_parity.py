@@ -1,0 +1,326 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle, element by
+element on the same seeded inputs (north_star tolerances):
+  keep set bit-exact; b and A within 1e-5 relative L2; x_map within 1e-3 relative L2;
+  integrated power within 1e-3."""
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL_B = 1e-5
+TOL_A = 1e-5
+TOL_X = 1e-3
+TOL_P = 1e-3
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    den = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (den if den > 0 else 1.0)
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+@pytest.fixture(scope="module")
+def ctx(torch_cuda):
+    from paper_1608_05179_b200 import Context
+    c = Context(0)
+    yield c
+    c.close()
+
+
+def geom_of(band):
+    from paper_1608_05179_b200 import Geometry
+    cfg = band.cfg
+    return Geometry(band.mic_xyz, cfg.n, cfg.side_len, cfg.z0, cfg.c0, cfg.cx, cfg.cy)
+
+
+def oracle_args(g):
+    return (g.mic_xyz, g.c0, g.n, g.side_len, g.z0, g.cx, g.cy)
+
+
+def small_geom(m=16, n=13, arms=2):
+    from paper_1608_05179_b200 import Geometry
+    return Geometry(synth.spiral_array(m, 0.6, arms), n, 1.2, 0.9, 343.0, 0.03, -0.02)
+
+
+# ---------------------------------------------------------------------------- S1
+def test_steer_parity(ctx, torch_cuda, oracle_lib):
+    torch = torch_cuda
+    g = small_geom()
+    idx = np.array([0, 1, 5, 77, g.S - 1], dtype=np.int32)
+    E = ctx.steer(g, 4321.0, torch.from_numpy(idx).cuda()).cpu().numpy()
+    ref = oracle_lib.steering(*oracle_args(g), 4321.0, idx)
+    assert np.max(np.abs(E - ref)) < 1e-12
+
+
+# ---------------------------------------------------------------------------- S2
+@pytest.mark.parametrize("cfgname", ["cfg1", "cfg2"])
+def test_das_parity(ctx, torch_cuda, oracle_lib, cfgname):
+    torch = torch_cuda
+    band = synth.make_band(cfgname)
+    g = geom_of(band)
+    b = ctx.das(g, band.freqs, torch.from_numpy(band.csm).cuda()).cpu().numpy()
+    for k in range(len(band.freqs)):
+        ref = oracle_lib.das(*oracle_args(g), band.freqs[k], band.csm[k])
+        assert rel_l2(b[k], ref) < 1e-12          # fp64 both sides (<< the 1e-5 bar)
+        assert rel_l2(b[k], ref) < TOL_B
+
+
+@pytest.mark.parametrize("m", [2, 13, 64, 128])
+def test_das_odd_sizes_and_non_hermitian(ctx, torch_cuda, oracle_lib, m):
+    """Ragged mic counts (chunk tails) and a non-Hermitian CSM: only its Hermitian part
+    matters (reading R3), so GPU == oracle's full quadratic form."""
+    torch = torch_cuda
+    from paper_1608_05179_b200 import Geometry
+    rng = np.random.default_rng(m)
+    g = Geometry(rng.uniform(-0.4, 0.4, size=(m, 3)) * [1, 1, 0], 9, 1.0, 1.0, 343.0)
+    C = rng.standard_normal((2, m, m)) + 1j * rng.standard_normal((2, m, m))
+    freqs = np.array([900.0, 7300.0])
+    b = ctx.das(g, freqs, torch.from_numpy(C).cuda()).cpu().numpy()
+    for k in range(2):
+        ref = oracle_lib.das(*oracle_args(g), freqs[k], C[k])
+        assert np.max(np.abs(b[k] - ref)) < 1e-12 * np.max(np.abs(ref))
+
+
+# ---------------------------------------------------------------------------- S3/S4
+def _compress_both(ctx, torch, g, bmaps, eps, mode=0, full=False):
+    nk, keep, lev = ctx.compress(g, torch.from_numpy(np.ascontiguousarray(bmaps)).cuda(), eps, mode, full,
+                                 want_level=True)
+    nk, keep, lev = nk.cpu().numpy(), keep.cpu().numpy(), lev.cpu().numpy()
+    import oracle as orc
+    for k in range(bmaps.shape[0]):
+        rk, rlev, _, _ = orc.compress(g.n, bmaps[k], eps, mode, full)
+        assert nk[k] == len(rk)
+        assert np.array_equal(keep[k, : nk[k]], rk)
+        assert np.all(keep[k, nk[k]:] == -1)
+        assert np.array_equal(lev[k], rlev)
+    return nk
+
+
+def test_compress_bit_exact_on_oracle_maps(ctx, torch_cuda, oracle_lib):
+    """Stage test (i): the same fp64 b into both compressors -> identical keep sets."""
+    torch = torch_cuda
+    band = synth.make_band("cfg2")
+    g = geom_of(band)
+    bm = np.stack([oracle_lib.das(*oracle_args(g), f, c) for f, c in zip(band.freqs, band.csm)])
+    for eps in [band.cfg.epsilon, 0.001, 0.05, 0.3]:
+        _compress_both(ctx, torch, g, bm, eps)
+    # absolute mode, full grid
+    _compress_both(ctx, torch, g, bm, 0.01 * bm.max(), mode=1)
+    nk = _compress_both(ctx, torch, g, bm, 0.5, full=True)
+    assert np.all(nk == g.S)
+
+
+@pytest.mark.parametrize("n", [2, 3, 5, 6, 8, 17, 33, 64, 101])
+def test_compress_edge_grids(ctx, torch_cuda, n):
+    """Dyadic and non-dyadic N, tiny grids, random maps with ties, constant and zero maps."""
+    torch = torch_cuda
+    from paper_1608_05179_b200 import Geometry
+    g = Geometry(np.zeros((2, 3)), n, 1.0, 1.0)
+    rng = np.random.default_rng(n)
+    maps = [rng.random(n * n), np.full(n * n, 2.5), np.zeros(n * n),
+            np.round(rng.random(n * n) * 4) / 4]          # many exact ties at |d| == eps_eff
+    bm = np.stack(maps)
+    for eps in [0.125, 0.25, 0.01]:
+        _compress_both(ctx, torch, g, bm, eps)
+    _compress_both(ctx, torch, g, bm, 0.25, mode=1)
+
+
+# ---------------------------------------------------------------------------- S5
+@pytest.mark.parametrize("cfgname,bin_", [("cfg1", 0), ("cfg2", 0), ("cfg2", 7), ("cfg3", 200)])
+def test_psf_parity_on_oracle_keep(ctx, torch_cuda, oracle_lib, cfgname, bin_):
+    torch = torch_cuda
+    band = synth.make_band(cfgname, bins=[bin_])
+    g = geom_of(band)
+    f = band.freqs[0]
+    b = oracle_lib.das(*oracle_args(g), f, band.csm[0])
+    keep, *_ = oracle_lib.compress(g.n, b, band.cfg.epsilon)
+    A = ctx.psf(g, f, torch.from_numpy(keep).cuda()).cpu().numpy()
+    ref = oracle_lib.psf(*oracle_args(g), f, keep)
+    assert rel_l2(A, ref) < TOL_A
+    assert np.max(np.abs(A - A.T)) == 0.0
+    assert np.max(np.abs(np.diag(A) - 1)) < 1e-5
+
+
+@pytest.mark.parametrize("nk", [1, 2, 31, 32, 33, 64, 65, 130])
+def test_psf_ragged_sizes(ctx, torch_cuda, oracle_lib, nk):
+    torch = torch_cuda
+    g = small_geom(24, 15, 3)
+    keep = np.sort(np.random.default_rng(nk).choice(g.S, size=nk, replace=False)).astype(np.int32)
+    A = ctx.psf(g, 5100.0, torch.from_numpy(keep).cuda()).cpu().numpy()
+    ref = oracle_lib.psf(*oracle_args(g), 5100.0, keep)
+    assert rel_l2(A, ref) < TOL_A
+
+
+# ---------------------------------------------------------------------------- S7
+def test_gs_identity_and_scalar(ctx, torch_cuda):
+    torch = torch_cuda
+    b = np.array([0.5, -1.0, 2.0, 0.0, 3.0])
+    x = ctx.gs(torch.eye(5, dtype=torch.float32).cuda(), torch.from_numpy(b).cuda(), 1).cpu().numpy()
+    assert np.array_equal(x, np.maximum(b, 0).astype(np.float32))
+    x = ctx.gs(torch.tensor([[4.0]]).cuda(), torch.tensor([3.0], dtype=torch.float64).cuda(), 3).cpu().numpy()
+    assert x[0] == 0.75
+
+
+@pytest.mark.parametrize("nk,sweeps", [(2, 7), (31, 50), (32, 50), (33, 50), (97, 200), (300, 1000),
+                                       (1000, 100)])
+def test_gs_parity_on_oracle_system(ctx, torch_cuda, oracle_lib, nk, sweeps):
+    """GS on the oracle's own A~ (rounded to fp32) and b~: ragged sizes around the 32-row
+    block and multi-block systems."""
+    torch = torch_cuda
+    band = synth.make_band("cfg3", bins=[150])
+    g = geom_of(band)
+    f = band.freqs[0]
+    b = oracle_lib.das(*oracle_args(g), f, band.csm[0])
+    order = np.argsort(-b)[:nk]
+    keep = np.sort(order).astype(np.int32)
+    A = oracle_lib.psf(*oracle_args(g), f, keep)
+    bt = b[keep]
+    ref = oracle_lib.gs(A, bt, sweeps)
+    x = ctx.gs(torch.from_numpy(A.astype(np.float32)).cuda(), torch.from_numpy(bt).cuda(), sweeps).cpu().numpy()
+    assert x.min() >= 0
+    assert rel_l2(x, ref) < TOL_X
+    assert abs(x.sum() - ref.sum()) < TOL_P * ref.sum()
+
+
+# ---------------------------------------------------------------------------- end to end
+def _e2e(ctx, torch, oracle_lib, band, sweeps=None, full=False, check_b=True):
+    cfg = band.cfg
+    g = geom_of(band)
+    sw = sweeps or cfg.sweeps
+    out = ctx.solve_band(g, band.freqs, torch.from_numpy(band.csm).cuda(), cfg.epsilon, sw, cfg.eps_mode,
+                         full_grid=full, want_b=True)
+    nk = out["n_keep"].cpu().numpy()
+    keep = out["keep_idx"].cpu().numpy()
+    x = out["x_map"].cpu().numpy()
+    bm = out["b_map"].cpu().numpy()
+    rnk, rkeep, rx, rb = oracle_lib.solve_band_cfg(band, sweeps=sw, full_grid=full)
+    for k in range(len(band.freqs)):
+        assert rel_l2(bm[k], rb[k]) < TOL_B
+        assert nk[k] == rnk[k], (k, nk[k], rnk[k])
+        assert np.array_equal(keep[k], rkeep[k])
+        assert rel_l2(x[k], rx[k]) < TOL_X, (k, rel_l2(x[k], rx[k]))
+        assert abs(x[k].sum() - rx[k].sum()) <= TOL_P * rx[k].sum()
+        assert x[k].min() >= 0
+    return out
+
+
+def test_e2e_cfg1_compressed_and_full(ctx, torch_cuda, oracle_lib):
+    band = synth.make_band("cfg1")
+    _e2e(ctx, torch_cuda, oracle_lib, band)
+    _e2e(ctx, torch_cuda, oracle_lib, band, full=True)
+
+
+def test_e2e_cfg2_all_bins(ctx, torch_cuda, oracle_lib):
+    _e2e(ctx, torch_cuda, oracle_lib, synth.make_band("cfg2"))
+
+
+def test_e2e_cfg3_strided_bins(ctx, torch_cuda, oracle_lib):
+    band = synth.make_band("cfg3", bins=synth.strided_bins(256, 6))
+    _e2e(ctx, torch_cuda, oracle_lib, band)
+
+
+def test_e2e_full_grid_m128(ctx, torch_cuda, oracle_lib):
+    """Full-grid mode (cfg4's 128-mic array, exact CSM) on a 31x31 grid the oracle can
+    build the dense S x S PSF for; several 32-row blocks and a ragged tail (961 = 30*32+1)."""
+    import dataclasses
+    cfg = dataclasses.replace(synth.CONFIGS["cfg4"], n=31, n_bins=3)
+    band = synth.make_band(cfg)
+    _e2e(ctx, torch_cuda, oracle_lib, band, sweeps=60, full=True)
+
+
+def test_e2e_cfg5_strided_bins_few_sweeps(ctx, torch_cuda, oracle_lib):
+    """cfg5 geometry (M=128, 201x201 grid, 10 dB SNR) on two low bins, 20 sweeps."""
+    band = synth.make_band("cfg5", bins=[10, 120])
+    _e2e(ctx, torch_cuda, oracle_lib, band, sweeps=20)
+
+
+def test_full_size_cfg3_sampled(ctx, torch_cuda, oracle_lib):
+    """BASELINE configs[2] at full size in the bench's launch configuration (all 256 bins in
+    one call); the oracle recomputes a strided sample of 8 bins one by one."""
+    torch = torch_cuda
+    cfg = synth.CONFIGS["cfg3"]
+    band = synth.make_band(cfg)
+    g = geom_of(band)
+    out = ctx.solve_band(g, band.freqs, torch.from_numpy(band.csm).cuda(), cfg.epsilon, cfg.sweeps)
+    nk = out["n_keep"].cpu().numpy()
+    keep = out["keep_idx"].cpu().numpy()
+    x = out["x_map"].cpu().numpy()
+    sample = synth.strided_bins(256, 8)
+    sub = synth.make_band(cfg, bins=sample)
+    rnk, rkeep, rx, _ = oracle_lib.solve_band_cfg(sub)
+    for j, k in enumerate(sample):
+        assert nk[k] == rnk[j] and np.array_equal(keep[k], rkeep[j])
+        assert rel_l2(x[k], rx[j]) < TOL_X
+        assert abs(x[k].sum() - rx[j].sum()) <= TOL_P * rx[j].sum()
+
+
+def test_host_api_equals_device_api_and_deterministic(ctx, torch_cuda):
+    torch = torch_cuda
+    band = synth.make_band("cfg2", bins=[1, 4, 6])
+    g = geom_of(band)
+    cfg = band.cfg
+    d1 = ctx.solve_band(g, band.freqs, torch.from_numpy(band.csm).cuda(), cfg.epsilon, 200, want_b=True)
+    d2 = ctx.solve_band(g, band.freqs, torch.from_numpy(band.csm).cuda(), cfg.epsilon, 200, want_b=True)
+    h = ctx.solve_band_host(g, band.freqs, torch.from_numpy(band.csm).pin_memory(), cfg.epsilon, 200, want_b=True)
+    for key in ["n_keep", "keep_idx", "x_map", "b_map"]:
+        a = d1[key].cpu()
+        assert torch.equal(a, d2[key].cpu())
+        assert torch.equal(a, h[key])
+
+
+def test_shard_invariance(ctx, torch_cuda):
+    """Per-bin outputs do not depend on which other bins share the call (the property the
+    multi-GPU strided sharding relies on): bins solved in a batch == bins solved alone."""
+    torch = torch_cuda
+    band = synth.make_band("cfg2")
+    g = geom_of(band)
+    cfg = band.cfg
+    full = ctx.solve_band(g, band.freqs, torch.from_numpy(band.csm).cuda(), cfg.epsilon, 300)
+    for k in [0, 3, 7]:
+        one = ctx.solve_band(g, band.freqs[k:k + 1], torch.from_numpy(band.csm[k:k + 1]).cuda(), cfg.epsilon, 300)
+        assert torch.equal(one["x_map"][0], full["x_map"][k])
+        assert torch.equal(one["keep_idx"][0], full["keep_idx"][k])
+
+
+def test_errors(ctx, torch_cuda):
+    torch = torch_cuda
+    from paper_1608_05179_b200 import DwcError, Geometry
+    band = synth.make_band("cfg1")
+    g = geom_of(band)
+    csm = torch.from_numpy(band.csm).cuda()
+    with pytest.raises(DwcError) as e:
+        ctx.solve_band(g, band.freqs, csm, -1.0, 10)
+    assert e.value.code == -1
+    with pytest.raises(DwcError) as e:
+        ctx.solve_band(g, band.freqs, csm, 0.1, 0)
+    assert e.value.code == -1
+    with pytest.raises(DwcError) as e:
+        ctx.solve_band(g, -band.freqs, csm, 0.1, 10)
+    assert e.value.code == -1
+    bad = Geometry(g.mic_xyz, 1, 1.0, 1.0)
+    with pytest.raises(DwcError):
+        ctx.solve_band(bad, band.freqs, torch.zeros((1, 16, 16), dtype=torch.complex128).cuda(), 0.1, 10)
+    nan = csm.clone()
+    nan[0, 0, 0] = float("nan")
+    with pytest.raises(DwcError) as e:
+        ctx.solve_band(g, band.freqs, nan, 0.1, 10)
+    assert e.value.code == -3
+    # a grid node on a microphone -> singular
+    mic = np.array([[0.0, 0.0, 1.0], [0.2, 0.1, 0.0]])
+    gs = Geometry(mic, 3, 1.0, 1.0)
+    with pytest.raises(DwcError) as e:
+        ctx.solve_band(gs, [1000.0], torch.eye(2, dtype=torch.complex128).reshape(1, 2, 2).cuda(), 0.1, 5)
+    assert e.value.code == -2
+    # the context still works after errors
+    ctx.solve_band(g, band.freqs, csm, 0.1, 5)
