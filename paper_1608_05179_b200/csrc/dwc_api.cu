@@ -47,7 +47,7 @@ struct dwc_ctx {
     int device = 0;
     int num_sms = 148;
     size_t total_bytes = 0;
-    DevBuf mic, freq, dist, amp, herm, bint, xplanes, bt, A, lay, order, counter, tiles, flag,
+    DevBuf mic, freq, dist, amp, herm, bint, xplanes, bt, A, lay, order, counter, tiles, flag, items,
         csm_h, nk_h, keep_h, xmap_h, bmap_h, gs_x, gs_b;
     PinBuf stage, readback;
     size_t stage_off = 0;
@@ -221,6 +221,34 @@ dwc_status prepare_geometry(dwc_ctx *ctx, const dwc_array *a, const dwc_grid *g,
     return DWC_OK;
 }
 
+// Work items of the GS cluster kernel: bins in descending S~ order, grouped by their
+// per-bin CTA count g (batch independent): one g=4 bin, two g=2 bins or four g=1 bins per
+// item; items stay in descending-work order (LPT).
+std::vector<int> build_gs_items(const std::vector<int32_t> &order, const int32_t *nk) {
+    const int cl = gs_cluster_size(), w = gs_item_ints();
+    std::vector<int> items;
+    std::vector<int> cur;
+    int cur_g = 0;
+    auto flush = [&]() {
+        if (cur.empty()) return;
+        items.push_back(cur_g);
+        for (int q = 0; q < cl; q++) items.push_back(q < (int)cur.size() ? cur[q] : -1);
+        for (int q = cl + 1; q < w; q++) items.push_back(-1);
+        cur.clear();
+    };
+    for (int b : order) {
+        const int g = gs_group_size(nk[b]);
+        if (g != cur_g) {
+            flush();
+            cur_g = g;
+        }
+        cur.push_back(b);
+        if ((int)cur.size() == cl / g) flush();
+    }
+    flush();
+    return items;
+}
+
 void ev(dwc_ctx *ctx, int i, cudaStream_t st) {
     if (ctx->timing) cudaEventRecord(ctx->ev[i], st);
 }
@@ -277,11 +305,13 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
         sum_sq += (double)nk * nk;
         sum_k += nk;
     }
-    if (max_sp * 4 + 20 * 1024 > 227 * 1024)
+    if (gs_smem_bytes(max_sp) > 227 * 1024)
         return fail(DWC_EINVAL, "compressed grid of %d points exceeds the on-chip x capacity", max_sp);
     std::vector<int32_t> order(n_bins);
     std::iota(order.begin(), order.end(), 0);
     std::stable_sort(order.begin(), order.end(), [&](int a, int b2) { return hk[a] > hk[b2]; });
+    std::vector<int> items = build_gs_items(order, hk);
+    const int n_items = (int)items.size() / gs_item_ints();
     std::vector<int4> tiles;
     for (int k = 0; k < n_bins; k++) {
         const int T = (lay[k].sp + 63) / 64;
@@ -289,32 +319,32 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
             for (int J = I; J < T; J++) tiles.push_back(make_int4(k, I, J, 0));
     }
     if ((s = ensure(ctx, ctx->lay, sizeof(BinLayout) * n_bins))) return s;
-    if ((s = ensure(ctx, ctx->order, sizeof(int32_t) * n_bins))) return s;
+    if ((s = ensure(ctx, ctx->items, sizeof(int) * items.size()))) return s;
     if ((s = ensure(ctx, ctx->tiles, sizeof(int4) * std::max<size_t>(tiles.size(), 1)))) return s;
     if ((s = ensure(ctx, ctx->counter, 64))) return s;
-    if ((s = ensure(ctx, ctx->xplanes, sizeof(float) * 2 * M * (size_t)v_off))) return s;
-    if ((s = ensure(ctx, ctx->bt, sizeof(float) * (size_t)v_off))) return s;
+    if ((s = ensure(ctx, ctx->xplanes, sizeof(double) * 2 * M * (size_t)v_off))) return s;
+    if ((s = ensure(ctx, ctx->bt, sizeof(double) * (size_t)v_off))) return s;
     if ((s = ensure(ctx, ctx->A, sizeof(float) * (size_t)a_off))) return s;
-    if ((s = stage_begin(ctx, sizeof(BinLayout) * n_bins + sizeof(int32_t) * n_bins +
+    if ((s = stage_begin(ctx, sizeof(BinLayout) * n_bins + sizeof(int) * items.size() +
                                   sizeof(int4) * tiles.size() + 4096))) return s;
     if ((s = stage_upload(ctx, ctx->lay.p, lay.data(), sizeof(BinLayout) * n_bins, st))) return s;
-    if ((s = stage_upload(ctx, ctx->order.p, order.data(), sizeof(int32_t) * n_bins, st))) return s;
+    if ((s = stage_upload(ctx, ctx->items.p, items.data(), sizeof(int) * items.size(), st))) return s;
     if ((s = stage_upload(ctx, ctx->tiles.p, tiles.data(), sizeof(int4) * tiles.size(), st))) return s;
     if ((s = stage_end(ctx, st))) return s;
     ev(ctx, 3, st);
     // S5 (+S6)
     LAUNCH(launch_steer_kept(G, (double *)ctx->dist.p, (double *)ctx->amp.p, n_bins, (double *)ctx->freq.p,
-                             (BinLayout *)ctx->lay.p, keep_idx, b, (float *)ctx->xplanes.p,
-                             (float *)ctx->bt.p, max_sp, st));
+                             (BinLayout *)ctx->lay.p, keep_idx, b, (double *)ctx->xplanes.p,
+                             (double *)ctx->bt.p, max_sp, st));
     LAUNCH(launch_gram(M, (int)tiles.size(), (int4 *)ctx->tiles.p, (BinLayout *)ctx->lay.p,
-                       (float *)ctx->xplanes.p, (float *)ctx->A.p, st));
+                       (double *)ctx->xplanes.p, (float *)ctx->A.p, st));
     ev(ctx, 4, st);
     // S7 + S8
     CU(cudaMemsetAsync(x_map, 0, sizeof(float) * (size_t)n_bins * S, st));
     CU(cudaMemsetAsync(ctx->counter.p, 0, 64, st));
     ev(ctx, 5, st);
-    LAUNCH(launch_gs(n_bins, (BinLayout *)ctx->lay.p, max_sp, (int32_t *)ctx->order.p, (int *)ctx->counter.p,
-                     (float *)ctx->A.p, (float *)ctx->bt.p, p->sweeps, nullptr, x_map, keep_idx, S,
+    LAUNCH(launch_gs(n_items, (int *)ctx->items.p, (BinLayout *)ctx->lay.p, max_sp, (int *)ctx->counter.p,
+                     (float *)ctx->A.p, (double *)ctx->bt.p, p->sweeps, nullptr, x_map, keep_idx, S,
                      ctx->num_sms, st));
     ev(ctx, 6, st);
     // warnings (host, Eq. 24)
@@ -385,7 +415,7 @@ dwc_status dwc_destroy(dwc_ctx *ctx) {
     cudaDeviceSynchronize();
     DevBuf *bufs[] = {&ctx->mic, &ctx->freq, &ctx->dist, &ctx->amp, &ctx->herm, &ctx->bint, &ctx->xplanes,
                       &ctx->bt, &ctx->A, &ctx->lay, &ctx->order, &ctx->counter, &ctx->tiles, &ctx->flag,
-                      &ctx->csm_h, &ctx->nk_h, &ctx->keep_h, &ctx->xmap_h, &ctx->bmap_h, &ctx->gs_x, &ctx->gs_b};
+                      &ctx->items, &ctx->csm_h, &ctx->nk_h, &ctx->keep_h, &ctx->xmap_h, &ctx->bmap_h, &ctx->gs_x, &ctx->gs_b};
     for (DevBuf *b : bufs)
         if (b->p) cudaFree(b->p);
     if (ctx->stage.p) cudaFreeHost(ctx->stage.p);
@@ -526,20 +556,19 @@ dwc_status dwc_psf(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, dou
     for (int I = 0; I < T; I++)
         for (int J = I; J < T; J++) tiles.push_back(make_int4(0, I, J, 0));
     if ((s = ensure(ctx, ctx->lay, sizeof(BinLayout))) || (s = ensure(ctx, ctx->tiles, sizeof(int4) * tiles.size())) ||
-        (s = ensure(ctx, ctx->xplanes, sizeof(float) * 2 * arr->m * (size_t)sp)) ||
-        (s = ensure(ctx, ctx->bt, sizeof(float) * sp)) || (s = ensure(ctx, ctx->A, sizeof(float) * (size_t)sp * sp)))
+        (s = ensure(ctx, ctx->xplanes, sizeof(double) * 2 * arr->m * (size_t)sp)) ||
+        (s = ensure(ctx, ctx->bt, sizeof(double) * sp)) || (s = ensure(ctx, ctx->A, sizeof(float) * (size_t)sp * sp)))
         return s;
     if ((s = stage_begin(ctx, sizeof(BinLayout) + sizeof(int4) * tiles.size() + 1024))) return s;
     if ((s = stage_upload(ctx, ctx->lay.p, &lay, sizeof(BinLayout), st))) return s;
     if ((s = stage_upload(ctx, ctx->tiles.p, tiles.data(), sizeof(int4) * tiles.size(), st))) return s;
     if ((s = stage_end(ctx, st))) return s;
     LAUNCH(launch_steer_kept(G, (double *)ctx->dist.p, (double *)ctx->amp.p, 1, (double *)ctx->freq.p,
-                             (BinLayout *)ctx->lay.p, keep_idx, nullptr, (float *)ctx->xplanes.p,
-                             (float *)ctx->bt.p, sp, st));
+                             (BinLayout *)ctx->lay.p, keep_idx, nullptr, (double *)ctx->xplanes.p,
+                             (double *)ctx->bt.p, sp, st));
     LAUNCH(launch_gram(arr->m, (int)tiles.size(), (int4 *)ctx->tiles.p, (BinLayout *)ctx->lay.p,
-                       (float *)ctx->xplanes.p, (float *)ctx->A.p, st));
-    CU(cudaMemcpy2DAsync(A, sizeof(float) * n_keep, ctx->A.p, sizeof(float) * sp, sizeof(float) * n_keep, n_keep,
-                         cudaMemcpyDeviceToDevice, st));
+                       (double *)ctx->xplanes.p, (float *)ctx->A.p, st));
+    LAUNCH(launch_tile_convert(0, n_keep, sp, (float *)ctx->A.p, A, st));
     return DWC_OK;
 }
 
@@ -551,28 +580,29 @@ dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int3
     if (sweeps < 1) return fail(DWC_EINVAL, "sweeps must be >= 1");
     if (!A || !b || !x) return fail(DWC_EINVAL, "NULL device buffer");
     const int sp = (n + 31) & ~31;
-    if (sp * 4 + 20 * 1024 > 227 * 1024) return fail(DWC_EINVAL, "n = %d exceeds the on-chip x capacity", n);
+    if (gs_smem_bytes(sp) > 227 * 1024) return fail(DWC_EINVAL, "n = %d exceeds the on-chip x capacity", n);
     cudaStream_t st = (cudaStream_t)cuda_stream;
     int launches = 0;
     BinLayout lay{n, sp, 0, 0};
-    int32_t order0 = 0;
-    if ((s = ensure(ctx, ctx->lay, sizeof(BinLayout))) || (s = ensure(ctx, ctx->order, sizeof(int32_t))) ||
-        (s = ensure(ctx, ctx->counter, 64)) || (s = ensure(ctx, ctx->gs_b, sizeof(float) * sp)) ||
+    std::vector<int32_t> order{0};
+    int32_t nk0 = n;
+    std::vector<int> items = build_gs_items(order, &nk0);
+    if ((s = ensure(ctx, ctx->lay, sizeof(BinLayout))) || (s = ensure(ctx, ctx->items, sizeof(int) * items.size())) ||
+        (s = ensure(ctx, ctx->counter, 64)) || (s = ensure(ctx, ctx->gs_b, sizeof(double) * sp)) ||
         (s = ensure(ctx, ctx->gs_x, sizeof(float) * (size_t)sp * sp)))
         return s;
-    if ((s = stage_begin(ctx, 1024))) return s;
+    if ((s = stage_begin(ctx, 1024 + sizeof(int) * items.size()))) return s;
     if ((s = stage_upload(ctx, ctx->lay.p, &lay, sizeof(BinLayout), st))) return s;
-    if ((s = stage_upload(ctx, ctx->order.p, &order0, sizeof(int32_t), st))) return s;
+    if ((s = stage_upload(ctx, ctx->items.p, items.data(), sizeof(int) * items.size(), st))) return s;
     if ((s = stage_end(ctx, st))) return s;
     float *Ap = (float *)ctx->gs_x.p;
-    CU(cudaMemsetAsync(Ap, 0, sizeof(float) * (size_t)sp * sp, st));
-    CU(cudaMemcpy2DAsync(Ap, sizeof(float) * sp, A, sizeof(float) * n, sizeof(float) * n, n,
-                         cudaMemcpyDeviceToDevice, st));
-    CU(cudaMemsetAsync(ctx->gs_b.p, 0, sizeof(float) * sp, st));
-    LAUNCH(launch_f64_to_f32(b, (float *)ctx->gs_b.p, n, st));
+    LAUNCH(launch_tile_convert(1, n, sp, A, Ap, st));
+    CU(cudaMemsetAsync(ctx->gs_b.p, 0, sizeof(double) * sp, st));
+    CU(cudaMemcpyAsync(ctx->gs_b.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     CU(cudaMemsetAsync(ctx->counter.p, 0, 64, st));
-    LAUNCH(launch_gs(1, (BinLayout *)ctx->lay.p, sp, (int32_t *)ctx->order.p, (int *)ctx->counter.p, Ap,
-                     (float *)ctx->gs_b.p, sweeps, x, nullptr, nullptr, 0, ctx->num_sms, st));
+    LAUNCH(launch_gs((int)items.size() / gs_item_ints(), (int *)ctx->items.p, (BinLayout *)ctx->lay.p, sp,
+                     (int *)ctx->counter.p, Ap, (double *)ctx->gs_b.p, sweeps, x, nullptr, nullptr, 0, ctx->num_sms,
+                     st));
     return DWC_OK;
 }
 

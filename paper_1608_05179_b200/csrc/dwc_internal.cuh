@@ -53,25 +53,38 @@ struct BinLayout {
     int64_t v_off;    // float offset of per-bin vectors (sp entries) and of the E planes / sp
 };
 
-// S5 part 1: kept steering planes X[k] = [Re E~; Im E~] as fp32 (2m rows x sp cols) and
-// bt[k][i] = b[k][keep[i]] (S6, fp32), zero padded to sp.
+// S5 part 1: kept steering planes X[k] = [Re E~; Im E~] in fp64 (2m rows x sp cols) and
+// bt[k][i] = b[k][keep[i]] (S6, fp64), zero padded to sp.
 // b may be NULL (bt then untouched).  Grid spans max_sp columns.
 int launch_steer_kept(const Geo &g, const double *dist, const double *amp, int n_bins,
                       const double *freq, const BinLayout *lay, const int32_t *keep_idx,
-                      const double *b, float *xplanes, float *bt, int max_sp, cudaStream_t st);
+                      const double *b, double *xplanes, double *bt, int max_sp, cudaStream_t st);
 
 // S5 part 2: A~_k = |E~^H E~|^2 / M^2 (dense, both triangles written) over a list of
 // 64x64 upper tile pairs (bin, I, J, -).
 int launch_gram(int m, int n_tiles, const int4 *tiles, const BinLayout *lay_dev,
-                const float *xplanes, float *A, cudaStream_t st);
+                const double *xplanes, float *A, cudaStream_t st);
 
-// fp64 -> fp32 copy (dwc_gs right-hand side).
-int launch_f64_to_f32(const double *src, float *dst, int n, cudaStream_t st);
 
-// S7+S8: Gauss-Seidel sweeps, LPT-ordered persistent kernel; writes x_out (per bin at
-// v_off, nullable) and scatters into x_map[k*S + keep[i]] (nullable).
-int launch_gs(int n_bins, const BinLayout *lay_dev, int max_sp, const int32_t *order,
-              int *counter, const float *A, const float *bt, int sweeps, float *x_out,
-              float *x_map, const int32_t *keep_idx, int S, int num_sms, cudaStream_t st);
+// S5 storage layout of A~_k (shared by the Gram epilogue and the GS kernel): 32x32 fp32
+// tiles, column-major inside a tile, row-block-major; T = sp/32; element (i, j) at
+//   a_off + ((i/32)*T + j/32)*1024 + (j%32)*32 + (i%32).
+__host__ __device__ inline size_t tiled_index(int T, int i, int j) {
+    return ((size_t)(i >> 5) * T + (j >> 5)) * 1024 + (size_t)(j & 31) * 32 + (i & 31);
+}
+
+// dense row-major n x n <-> tiled sp x sp (zero padded) conversions (stage entry points).
+int launch_tile_convert(int to_tiled, int n, int sp, const float *src, float *dst, cudaStream_t st);
+
+// S7+S8: Gauss-Seidel sweeps, persistent cluster kernel over LPT-ordered work items
+// (gs_item_ints() ints each: g, bin[4]); writes x_out (per bin at v_off, nullable) and
+// scatters into x_map[k*S + keep[i]] (nullable).
+size_t gs_smem_bytes(int max_sp);
+int gs_cluster_size();
+int gs_item_ints();
+int gs_group_size(int nk);
+int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_sp, int *counter, const float *A,
+              const double *bt, int sweeps, float *x_out, float *x_map, const int32_t *keep_idx, int S,
+              int num_sms, cudaStream_t st);
 
 }  // namespace dwc

@@ -149,7 +149,7 @@ def test_psf_parity_on_oracle_keep(ctx, torch_cuda, oracle_lib, cfgname, bin_):
     ref = oracle_lib.psf(*oracle_args(g), f, keep)
     assert rel_l2(A, ref) < TOL_A
     assert np.max(np.abs(A - A.T)) == 0.0
-    assert np.max(np.abs(np.diag(A) - 1)) < 1e-5
+    assert np.max(np.abs(np.diag(A) - 1)) < 1e-6
 
 
 @pytest.mark.parametrize("nk", [1, 2, 31, 32, 33, 64, 65, 130])
