@@ -47,7 +47,7 @@ struct dwc_ctx {
     int device = 0;
     int num_sms = 148;
     size_t total_bytes = 0;
-    DevBuf mic, freq, dist, amp, herm, bint, xplanes, bt, A, lay, order, counter, tiles, flag, items,
+    DevBuf mic, freq, dist, amp, herm, bint, xplanes, bt, A, lay, order, counter, tiles, flag, items, packets,
         csm_h, nk_h, keep_h, xmap_h, bmap_h, gs_x, gs_b;
     PinBuf stage, readback;
     size_t stage_off = 0;
@@ -325,6 +325,7 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
     if ((s = ensure(ctx, ctx->xplanes, sizeof(double) * 2 * M * (size_t)v_off))) return s;
     if ((s = ensure(ctx, ctx->bt, sizeof(double) * (size_t)v_off))) return s;
     if ((s = ensure(ctx, ctx->A, sizeof(float) * (size_t)a_off))) return s;
+    if ((s = ensure(ctx, ctx->packets, (size_t)gs_packet_bytes() * (size_t)(v_off / 32)))) return s;
     if ((s = stage_begin(ctx, sizeof(BinLayout) * n_bins + sizeof(int) * items.size() +
                                   sizeof(int4) * tiles.size() + 4096))) return s;
     if ((s = stage_upload(ctx, ctx->lay.p, lay.data(), sizeof(BinLayout) * n_bins, st))) return s;
@@ -343,8 +344,10 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
     CU(cudaMemsetAsync(x_map, 0, sizeof(float) * (size_t)n_bins * S, st));
     CU(cudaMemsetAsync(ctx->counter.p, 0, 64, st));
     ev(ctx, 5, st);
+    LAUNCH(launch_gs_prep(n_bins, max_sp, (BinLayout *)ctx->lay.p, (float *)ctx->A.p, (double *)ctx->bt.p,
+                          ctx->packets.p, st));
     LAUNCH(launch_gs(n_items, (int *)ctx->items.p, (BinLayout *)ctx->lay.p, max_sp, (int *)ctx->counter.p,
-                     (float *)ctx->A.p, (double *)ctx->bt.p, p->sweeps, nullptr, x_map, keep_idx, S,
+                     (float *)ctx->A.p, ctx->packets.p, p->sweeps, nullptr, x_map, keep_idx, S,
                      ctx->num_sms, st));
     ev(ctx, 6, st);
     // warnings (host, Eq. 24)
@@ -415,7 +418,7 @@ dwc_status dwc_destroy(dwc_ctx *ctx) {
     cudaDeviceSynchronize();
     DevBuf *bufs[] = {&ctx->mic, &ctx->freq, &ctx->dist, &ctx->amp, &ctx->herm, &ctx->bint, &ctx->xplanes,
                       &ctx->bt, &ctx->A, &ctx->lay, &ctx->order, &ctx->counter, &ctx->tiles, &ctx->flag,
-                      &ctx->items, &ctx->csm_h, &ctx->nk_h, &ctx->keep_h, &ctx->xmap_h, &ctx->bmap_h, &ctx->gs_x, &ctx->gs_b};
+                      &ctx->items, &ctx->packets, &ctx->csm_h, &ctx->nk_h, &ctx->keep_h, &ctx->xmap_h, &ctx->bmap_h, &ctx->gs_x, &ctx->gs_b};
     for (DevBuf *b : bufs)
         if (b->p) cudaFree(b->p);
     if (ctx->stage.p) cudaFreeHost(ctx->stage.p);
@@ -589,7 +592,8 @@ dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int3
     std::vector<int> items = build_gs_items(order, &nk0);
     if ((s = ensure(ctx, ctx->lay, sizeof(BinLayout))) || (s = ensure(ctx, ctx->items, sizeof(int) * items.size())) ||
         (s = ensure(ctx, ctx->counter, 64)) || (s = ensure(ctx, ctx->gs_b, sizeof(double) * sp)) ||
-        (s = ensure(ctx, ctx->gs_x, sizeof(float) * (size_t)sp * sp)))
+        (s = ensure(ctx, ctx->gs_x, sizeof(float) * (size_t)sp * sp)) ||
+        (s = ensure(ctx, ctx->packets, (size_t)gs_packet_bytes() * (size_t)(sp / 32))))
         return s;
     if ((s = stage_begin(ctx, 1024 + sizeof(int) * items.size()))) return s;
     if ((s = stage_upload(ctx, ctx->lay.p, &lay, sizeof(BinLayout), st))) return s;
@@ -600,8 +604,9 @@ dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int3
     CU(cudaMemsetAsync(ctx->gs_b.p, 0, sizeof(double) * sp, st));
     CU(cudaMemcpyAsync(ctx->gs_b.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     CU(cudaMemsetAsync(ctx->counter.p, 0, 64, st));
+    LAUNCH(launch_gs_prep(1, sp, (BinLayout *)ctx->lay.p, Ap, (double *)ctx->gs_b.p, ctx->packets.p, st));
     LAUNCH(launch_gs((int)items.size() / gs_item_ints(), (int *)ctx->items.p, (BinLayout *)ctx->lay.p, sp,
-                     (int *)ctx->counter.p, Ap, (double *)ctx->gs_b.p, sweeps, x, nullptr, nullptr, 0, ctx->num_sms,
+                     (int *)ctx->counter.p, Ap, ctx->packets.p, sweeps, x, nullptr, nullptr, 0, ctx->num_sms,
                      st));
     return DWC_OK;
 }

@@ -84,7 +84,13 @@ int gs_cluster_size();
 int gs_item_ints();
 int gs_group_size(int nk);
 int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_sp, int *counter, const float *A,
-              const double *bt, int sweeps, float *x_out, float *x_map, const int32_t *keep_idx, int S,
+              const void *packets, int sweeps, float *x_out, float *x_map, const int32_t *keep_idx, int S,
               int num_sms, cudaStream_t st);
+
+// Per-block solver packets (1/A_ii, within-group scaled coefficients, b~ block) for the GS
+// kernel: gs_packet_bytes() bytes per 32-row block, bin k's packets at v_off/32.
+int gs_packet_bytes();
+int launch_gs_prep(int n_bins, int max_sp, const BinLayout *lay_dev, const float *A, const double *bt,
+                   void *packets, cudaStream_t st);
 
 }  // namespace dwc

@@ -34,6 +34,8 @@
 //  * g depends on S~ only (host), so a bin's result is bit-identical whatever else is in
 //    the batch (and on however many GPUs the band is sharded); items run largest first.
 #include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -44,9 +46,20 @@ namespace dwc {
 constexpr int kCl = 4;             // cluster size
 constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
-constexpr int kCons = kWarps - 2;  // consumer warps (2..7)
+constexpr int kCons = kWarps - 3;  // consumer warps (3..7)
 constexpr int kStages = 16;        // ring depth (4 KB tiles)
 constexpr int kTile = 1024;        // floats per tile
+constexpr int kStg = 4;            // solver tiles (L, D) prefetched this many steps ahead
+
+// Per-block solver packet (precomputed once per bin by gs_prep_kernel, staged with L/D):
+// invd[r] = 1/A_rr (0 for padding rows), wg[L][0..5] = within-group A[r][t]/A[r][r] for
+// lane L's rows r = 4L+i' > t = 4L+i  (order: 10 20 30 21 31 32), b~ of the block in fp64.
+struct __align__(16) GsPacket {
+    float invd[32];
+    float wg[8][8];
+    double b[32];
+};
+constexpr int kPacketBytes = (int)sizeof(GsPacket);
 
 struct GsItem {
     int g;          // CTAs per bin: 1, 2 or 4
@@ -55,13 +68,13 @@ struct GsItem {
 
 struct __align__(128) GsSmem {
     float ring[kStages][kTile];
-    float stg[2][2][kTile];            // [buf][0 = L tile, 1 = D tile]
-    float pw[2][kCons][32];            // consumer partials (double-buffered by step)
-    float pr[2][kCl][32];              // sub-group partials (leader)
+    float stg[kStg][2][kTile];         // [step % kStg][0 = L tile, 1 = D tile]
+    GsPacket pk[kStg];                 // solver packet of the staged block
+    float pr[2][kCl][kCons][32];       // leader: partial row sums of every consumer warp of the sub-group
     unsigned long long full[kStages], empty[kStages];
-    unsigned long long stg_full[2], stg_empty[2];
-    unsigned long long pready[2];      // leader: g*32 arrivals per step
-    unsigned long long xr[2];          // every CTA: 32 arrivals per solver step
+    unsigned long long stg_full[kStg], stg_empty[kStg];
+    unsigned long long pready[2];      // leader: 1 arrival + g*kCons*128 tx bytes per step
+    unsigned long long xr[2];          // leader: solver arrival; others: 1 arrival + 128 tx
     int item;
 };
 
@@ -115,6 +128,28 @@ __device__ __forceinline__ void st_remote_f32(uint32_t raddr, float v) {
 __device__ __forceinline__ void st_remote_s32(uint32_t raddr, int v) {
     asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(raddr), "r"(v) : "memory");
 }
+// shared::cta -> shared::cluster (another CTA) bulk copy, completing on the remote mbarrier
+__device__ __forceinline__ void bulk_s2s(uint32_t dst_cluster, const void *src, uint32_t bytes, uint32_t bar_cluster) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst_cluster),
+        "r"(smem_u32(src)), "r"(bytes), "r"(bar_cluster)
+        : "memory");
+}
+// st.async: register -> another CTA's shared memory, completing tx bytes on its mbarrier
+__device__ __forceinline__ void st_async_v4(uint32_t raddr, float4 v, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(raddr),
+                 "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(rbar)
+                 : "memory");
+}
+__device__ __forceinline__ void st_async_f32(uint32_t raddr, float v, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f32 [%0], %1, [%2];" ::"r"(raddr), "f"(v),
+                 "r"(rbar)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 // Consumer: acc[q] (rows 4*rq+q) += sum over columns c = cq + 4i of tile[c][4rq+q] * x[c].
@@ -137,9 +172,9 @@ __device__ __forceinline__ void tile_dot(const float *__restrict__ tile, const f
 // tile (kn,kx) (L, for the solver) and (kn,kn) (D, solver + its old-x product).
 __global__ void __launch_bounds__(kThreads, 2)
 gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout *__restrict__ lay,
-                  int *__restrict__ counter, const float *__restrict__ A, const double *__restrict__ bt,
+                  int *__restrict__ counter, const float *__restrict__ A, const GsPacket *__restrict__ packets,
                   int sweeps, float *__restrict__ x_out, float *__restrict__ x_map,
-                  const int32_t *__restrict__ keep_idx, int S) {
+                  const int32_t *__restrict__ keep_idx, int S, unsigned long long *__restrict__ prof) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     GsSmem &sh = *reinterpret_cast<GsSmem *>(smem_raw);
     float *xs = reinterpret_cast<float *>(smem_raw + sizeof(GsSmem));
@@ -166,7 +201,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
         const int sp = L.sp, nk = L.nk, T = sp >> 5;
         const int total = (bin >= 0) ? sweeps * T : 0;
         const float *Ab = A + L.a_off;
-        const double *btb = bt + L.v_off;
+        const GsPacket *pkb = packets + (L.v_off >> 5);
 
         for (int i = tid; i < sp; i += kThreads) xs[i] = 0.f;
         if (tid == 0) {
@@ -174,30 +209,25 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 mbar_init(&sh.full[i], 1);
                 mbar_init(&sh.empty[i], 1);
             }
-            for (int b = 0; b < 2; b++) {
+            for (int b = 0; b < kStg; b++) {
                 mbar_init(&sh.stg_full[b], 1);
-                mbar_init(&sh.stg_empty[b], 2);
-                mbar_init(&sh.pready[b], (uint32_t)g * 32);
-                mbar_init(&sh.xr[b], 32);
+                mbar_init(&sh.stg_empty[b], 3);   // solver, L-product warp, D-product warp
+            }
+            for (int b = 0; b < 2; b++) {
+                mbar_init(&sh.pready[b], 1);
+                mbar_init(&sh.xr[b], 1);
             }
             fence_mbar_init();
         }
         cluster_sync();
 
         if (wid == 1) {
-            // ================= TMA producer (one lane) =================
+            // ================= stream producer (one lane): this CTA's tiles of each row block
             if (lane == 0) {
                 uint32_t seq = 0;
                 for (int s = 0; s < total; s++) {
                     const int kn = s % T, kx = (s + T - 1) % T;
                     const float *rowb = Ab + (size_t)kn * T * kTile;
-                    if (is_leader) {
-                        const int b = s & 1;
-                        mbar_wait(&sh.stg_empty[b], ((s >> 1) & 1) ^ 1);
-                        mbar_expect_tx(&sh.stg_full[b], 2 * kTile * 4);
-                        bulk_g2s(sh.stg[b][0], rowb + (size_t)kx * kTile, kTile * 4, &sh.stg_full[b]);
-                        bulk_g2s(sh.stg[b][1], rowb + (size_t)kn * kTile, kTile * 4, &sh.stg_full[b]);
-                    }
                     for (int J = rg; J < T; J += g) {
                         if (J == kx || J == kn) continue;
                         const uint32_t slot = seq % kStages;
@@ -208,105 +238,251 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                     }
                 }
             }
+        } else if (wid == 4) {
+            // ================= staging producer (leader, one lane): L = (kn,kx), D = (kn,kn)
+            // (warp 4 shares the solver's SM sub-partition; it is mostly asleep in try_wait)
+            if (is_leader && lane == 0) {
+                for (int s = 0; s < total; s++) {
+                    const int kn = s % T, kx = (s + T - 1) % T, sl = s % kStg;
+                    const float *rowb = Ab + (size_t)kn * T * kTile;
+                    mbar_wait(&sh.stg_empty[sl], ((s / kStg) & 1) ^ 1);
+                    mbar_expect_tx(&sh.stg_full[sl], 2 * kTile * 4 + kPacketBytes);
+                    bulk_g2s(sh.stg[sl][0], rowb + (size_t)kx * kTile, kTile * 4, &sh.stg_full[sl]);
+                    bulk_g2s(sh.stg[sl][1], rowb + (size_t)kn * kTile, kTile * 4, &sh.stg_full[sl]);
+                    bulk_g2s(&sh.pk[sl], pkb + kn, kPacketBytes, &sh.stg_full[sl]);
+                }
+            }
         } else if (wid >= 2) {
-            // ================= consumers =================
-            const int c = wid - 2;
+            // ================= consumers: P_s = A[I_kn, J != kx] x_J  +  A[I_kn, I_kx] x_kx^old
+            // warps 2,3,5,6,7 (none on the solver's sub-partition 0).  In the leader, consumer 4
+            // computes the staged L product (old x; the solver adds the increment of the block
+            // it is solving) and consumer 3 the in-block D product; the stream tiles go to the
+            // others.  Every warp sends its 32 partial row sums to the leader with st.async.
+            const int c = (wid < 4) ? wid - 2 : wid - 3;
             const int rq = lane & 7, cq = lane >> 3;
+            const int n_sw = is_leader ? kCons - 2 : kCons;   // warps taking stream tiles
+            const bool do_L = is_leader && c == kCons - 1, do_D = is_leader && c == kCons - 2;
             uint32_t seq = 0;
-            const uint32_t pr_base = smem_u32(&sh.pr[0][0][0]);
+            const bool skip_dot = prof && prof[15];
+            const bool pf = prof && blockIdx.x == 0 && c == 0 && lane == 0;
+            unsigned long long tA = 0, cw_x = 0, cw_full = 0, c_comp = 0, c_red = 0;
             for (int s = 0; s < total; s++) {
                 const int kn = s % T, kx = (s + T - 1) % T;
-                if (s >= 2) mbar_wait(&sh.xr[s & 1], ((s - 2) >> 1) & 1);
-                float acc[4] = {0.f, 0.f, 0.f, 0.f};
-                int i = 0;
-                for (int J = rg; J < T; J += g) {
-                    if (J == kx || J == kn) continue;
-                    if (i == c) {
-                        const uint32_t slot = seq % kStages;
-                        mbar_wait(&sh.full[slot], (seq / kStages) & 1);
-                        tile_dot(sh.ring[slot], xs + 32 * J, rq, cq, acc);
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive_local(&sh.empty[slot]);
-                    }
-                    i = (i + 1 == kCons) ? 0 : i + 1;
-                    seq++;
+                if (pf) tA = clock64();
+                if (s >= 2) {
+                    if (!is_leader && c == 0 && lane == 0) mbar_expect_tx(&sh.xr[s & 1], 128);
+                    mbar_wait(&sh.xr[s & 1], ((s - 2) >> 1) & 1);
                 }
-                if (is_leader && c == kCons - 1) {
-                    const int b = s & 1;
-                    mbar_wait(&sh.stg_full[b], (s >> 1) & 1);
-                    if (T >= 2) tile_dot(sh.stg[b][1], xs + 32 * kn, rq, cq, acc);
+                // arm P-ready for this step only now: x of solver step s-2 being published implies
+                // that step consumed P_{s-2}, i.e. the previous phase of this barrier completed
+                if (is_leader && c == 0 && lane == 0)
+                    mbar_expect_tx(&sh.pready[s & 1], (uint32_t)(g * kCons * 128));
+                if (pf) { const unsigned long long t = clock64(); cw_x += t - tA; tA = t; }
+                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+                if (do_L || do_D) {
+                    const int b = s % kStg;
+                    if (do_L && s + 1 < total) mbar_wait(&sh.stg_full[(s + 1) % kStg], ((s + 1) / kStg) & 1);
+                    mbar_wait(&sh.stg_full[b], (s / kStg) & 1);
+                    if (do_L) tile_dot(sh.stg[b][0], xs + 32 * kx, rq, cq, acc);
+                    else if (T >= 2) tile_dot(sh.stg[b][1], xs + 32 * kn, rq, cq, acc);
                     __syncwarp();
                     if (lane == 0) mbar_arrive_local(&sh.stg_empty[b]);
+                    // stream-tile bookkeeping: these warps take none, but keep seq in step
+                    for (int J = rg; J < T; J += g) seq += (J != kx && J != kn);
+                } else {
+                    int i = 0;
+                    for (int J = rg; J < T; J += g) {
+                        if (J == kx || J == kn) continue;
+                        if (i == c) {
+                            const uint32_t slot = seq % kStages;
+                            mbar_wait(&sh.full[slot], (seq / kStages) & 1);
+                            if (pf) { const unsigned long long t = clock64(); cw_full += t - tA; tA = t; }
+                            if (!skip_dot) tile_dot(sh.ring[slot], xs + 32 * J, rq, cq, acc);
+                            if (pf) { const unsigned long long t = clock64(); c_comp += t - tA; tA = t; }
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive_local(&sh.empty[slot]);
+                        }
+                        i = (i + 1 == n_sw) ? 0 : i + 1;
+                        seq++;
+                    }
                 }
-                // reduce over the 4 column groups: every lane then holds rows 4rq..4rq+3
+                // reduce over the 4 column groups: lanes (rq, cq) then hold rows 4rq..4rq+3
 #pragma unroll
                 for (int q = 0; q < 4; q++) {
                     acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], 8);
                     acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], 16);
                 }
                 if (cq == 0)
-                    *reinterpret_cast<float4 *>(&sh.pw[s & 1][c][4 * rq]) = make_float4(acc[0], acc[1], acc[2], acc[3]);
-                named_bar(1, kCons * 32);
-                if (c == 0) {
-                    float v = 0.f;
-#pragma unroll
-                    for (int w = 0; w < kCons; w++) v += sh.pw[s & 1][w][lane];
-                    const uint32_t off = (uint32_t)((((s & 1) * kCl + rg) * 32 + lane) * 4);
-                    st_remote_f32(mapa(pr_base + off, leader), v);
-                    mbar_arrive_remote(mapa(smem_u32(&sh.pready[s & 1]), leader));
+                    st_async_v4(mapa(smem_u32(&sh.pr[s & 1][rg][c][4 * rq]), leader),
+                                make_float4(acc[0], acc[1], acc[2], acc[3]), mapa(smem_u32(&sh.pready[s & 1]), leader));
+                if (pf) { const unsigned long long t = clock64(); c_red += t - tA; tA = t; }
+            }
+            if (!is_leader && c == 0 && total > 0) {
+                // the last two x blocks the leader pushes are not needed here: wait for them so
+                // no async store lands after this item (barriers are re-initialised per item)
+                for (int s = total; s < total + 2; s++) {
+                    if (s < 2) continue;
+                    if (lane == 0) mbar_expect_tx(&sh.xr[s & 1], 128);
+                    mbar_wait(&sh.xr[s & 1], ((s - 2) >> 1) & 1);
                 }
+            }
+            if (pf) {
+                prof[5] = cw_x; prof[6] = cw_full; prof[7] = c_comp; prof[8] = c_red; prof[9] = total;
             }
         } else if (is_leader && total > 0) {
             // ================= solver (warp 0 of the leader) =================
-            float xprev = 0.f;
-            double bnext = btb[lane];
+            // Lane l: group L = l & 7 (rows 4L..4L+3), role = l >> 3.  Role 0 (lanes 0-7) solves
+            // the current block; role 1 (lanes 8-15) executes the same instruction stream on the
+            // next block's sub-diagonal tile, accumulating A[I_{k+1}, I_k] delta_k (lres); roles
+            // 2,3 mirror role 0.  x_k^new is published (xs + x-ready) only once P_{k+1} has
+            // arrived, so the stream warps read x_k^old for their share of that product.
+            const int L4 = 4 * (lane & 7);
+            const bool role1 = (lane >> 3) == 1;
             const uint32_t xs_base = smem_u32(xs);
-            for (int j = 0; j < total; j++) {
-                const int k = j % T, b = j & 1, row0 = 32 * k;
-                const double bk = bnext;
-                bnext = btb[32 * ((j + 1) % T) + lane];
-                mbar_wait(&sh.pready[b], (j >> 1) & 1);
-                mbar_wait(&sh.stg_full[b], (j >> 1) & 1);
-                float acc = 0.f;
-                for (int q = 0; q < g; q++) acc += sh.pr[b][q][lane];
-                const float *Lt = sh.stg[b][0];
-                float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll
-                for (int t = 0; t < 32; t += 4) {
-                    a0 = fmaf(Lt[(t + 0) * 32 + lane], __shfl_sync(0xffffffffu, xprev, t + 0), a0);
-                    a1 = fmaf(Lt[(t + 1) * 32 + lane], __shfl_sync(0xffffffffu, xprev, t + 1), a1);
-                    a2 = fmaf(Lt[(t + 2) * 32 + lane], __shfl_sync(0xffffffffu, xprev, t + 2), a2);
-                    a3 = fmaf(Lt[(t + 3) * 32 + lane], __shfl_sync(0xffffffffu, xprev, t + 3), a3);
+            float xprev[4] = {0.f, 0.f, 0.f, 0.f};
+            float lres[4] = {0.f, 0.f, 0.f, 0.f};
+            float invd[4], xo[4], wg10, wg20, wg30, wg21, wg31, wg32;
+            double bk[4];
+            int prev_row0 = -1;
+            const bool pf = prof && blockIdx.x == 0 && lane == 0;
+            unsigned long long tA = 0, w_p = 0, w_s = 0, c_set = 0, c_rec = 0, c_bc = 0, c_pub = 0, c_post = 0;
+            auto publish = [&](int jj, int r0) {
+                // x of solver step jj (block at r0) -> own xs + x-ready; bulk copies to the others
+                const float4 xv = make_float4(xprev[0], xprev[1], xprev[2], xprev[3]);
+                if (lane < 8) {
+                    *reinterpret_cast<float4 *>(xs + r0 + L4) = xv;
+                    const uint32_t xa = xs_base + (uint32_t)(r0 + L4) * 4;
+                    const uint32_t xra = smem_u32(&sh.xr[jj & 1]);
+                    for (int q = 1; q < g; q++) st_async_v4(mapa(xa, leader + q), xv, mapa(xra, leader + q));
                 }
-                acc += (a0 + a1) + (a2 + a3);
-                // residual in fp64 against the fp64 b~ (an fp32 b~ would shift the fixed point)
-                const double r = (double)acc - bk;
-                const float *Dt = sh.stg[b][1];
-                const float dii = Dt[lane * 32 + lane];
-                const float invd = (row0 + lane < nk) ? 1.0f / dii : 0.f;
-                float w = (float)(-r * (double)invd);
-                float xo = xs[row0 + lane];
-                float dp[32];
-#pragma unroll
-                for (int t = 0; t < 32; t++) dp[t] = Dt[t * 32 + lane] * invd;
-#pragma unroll
-                for (int t = 0; t < 32; t++) {
-                    const float cand = fmaxf(w, -xo);
-                    const float d = __shfl_sync(0xffffffffu, cand, t);
-                    w = fmaf(-dp[t], d, w);
-                    xo = (lane == t) ? xo + d : xo;
-                }
-                xprev = xo;
                 __syncwarp();
-                if (lane == 0) mbar_arrive_local(&sh.stg_empty[b]);
-                // broadcast the new block to every CTA of the sub-group (self included)
-                const uint32_t xa = xs_base + (uint32_t)(row0 + lane) * 4;
-                const uint32_t xra = smem_u32(&sh.xr[b]);
-                for (int q = 0; q < g; q++) {
-                    st_remote_f32(mapa(xa, leader + q), xo);
-                    mbar_arrive_remote(mapa(xra, leader + q));
+                if (lane == 0) mbar_arrive_local(&sh.xr[jj & 1]);
+            };
+            // per-block operands of the own rows from the staged packet (+ x^old)
+            auto prepare = [&](int jj) {
+                const GsPacket &P = sh.pk[jj % kStg];
+                const float4 iv = *reinterpret_cast<const float4 *>(&P.invd[L4]);
+                invd[0] = iv.x; invd[1] = iv.y; invd[2] = iv.z; invd[3] = iv.w;
+                const float4 w0 = *reinterpret_cast<const float4 *>(&P.wg[L4 >> 2][0]);
+                const float4 w1 = *reinterpret_cast<const float4 *>(&P.wg[L4 >> 2][4]);
+                wg10 = w0.x; wg20 = w0.y; wg30 = w0.z; wg21 = w0.w; wg31 = w1.x; wg32 = w1.y;
+                const double2 b01 = *reinterpret_cast<const double2 *>(&P.b[L4]);
+                const double2 b23 = *reinterpret_cast<const double2 *>(&P.b[L4 + 2]);
+                bk[0] = b01.x; bk[1] = b01.y; bk[2] = b23.x; bk[3] = b23.y;
+                if (T == 1) {
+#pragma unroll
+                    for (int i = 0; i < 4; i++) xo[i] = xprev[i];
+                } else {
+                    const float4 v = *reinterpret_cast<const float4 *>(xs + 32 * (jj % T) + L4);
+                    xo[0] = v.x; xo[1] = v.y; xo[2] = v.z; xo[3] = v.w;
                 }
+            };
+            mbar_wait(&sh.stg_full[0], 0);
+            prepare(0);
+            // operands of the next block, loaded ahead of the recurrence (latency hidden)
+            float n_invd[4], n_xo[4], n_wg[6];
+            double n_bk[4];
+            auto fetch_next = [&](int jj) {
+                const GsPacket &P = sh.pk[jj % kStg];
+                const float4 iv = *reinterpret_cast<const float4 *>(&P.invd[L4]);
+                n_invd[0] = iv.x; n_invd[1] = iv.y; n_invd[2] = iv.z; n_invd[3] = iv.w;
+                const float4 w0 = *reinterpret_cast<const float4 *>(&P.wg[L4 >> 2][0]);
+                const float4 w1 = *reinterpret_cast<const float4 *>(&P.wg[L4 >> 2][4]);
+                n_wg[0] = w0.x; n_wg[1] = w0.y; n_wg[2] = w0.z; n_wg[3] = w0.w; n_wg[4] = w1.x; n_wg[5] = w1.y;
+                const double2 b01 = *reinterpret_cast<const double2 *>(&P.b[L4]);
+                const double2 b23 = *reinterpret_cast<const double2 *>(&P.b[L4 + 2]);
+                n_bk[0] = b01.x; n_bk[1] = b01.y; n_bk[2] = b23.x; n_bk[3] = b23.y;
+                const float4 v = *reinterpret_cast<const float4 *>(xs + 32 * (jj % T) + L4);
+                n_xo[0] = v.x; n_xo[1] = v.y; n_xo[2] = v.z; n_xo[3] = v.w;
+            };
+            for (int j = 0; j < total; j++) {
+                const int k = j % T, b = j & 1, row0 = 32 * k, sl = j % kStg, sl1 = (j + 1) % kStg;
+                const bool has_next = (j + 1 < total);
+                if (pf) tA = clock64();
+                const float *Dt = sh.stg[sl][1];
+                // role 1 streams the next block's L tile; with no next step it re-reads Dt (unused)
+                const float *tp = (role1 && has_next) ? sh.stg[sl1][0] : Dt;
+                // ---- critical path: P_k -> publish x_{k-1} -> residual -> recurrence
+                mbar_wait(&sh.pready[b], (j >> 1) & 1);
+                if (pf) { const unsigned long long t = clock64(); w_p += t - tA; tA = t; }
+                if (prev_row0 >= 0) publish(j - 1, prev_row0);
+                if (pf) { const unsigned long long t = clock64(); c_pub += t - tA; tA = t; }
+                float ac[4];
+                {
+                    float a[4] = {lres[0], lres[1], lres[2], lres[3]};
+                    for (int q = 0; q < g; q++) {
+#pragma unroll
+                        for (int w = 0; w < kCons; w++) {
+                            const float4 v = *reinterpret_cast<const float4 *>(&sh.pr[b][q][w][L4]);
+                            a[0] += v.x; a[1] += v.y; a[2] += v.z; a[3] += v.w;
+                        }
+                    }
+#pragma unroll
+                    for (int i = 0; i < 4; i++) {
+                        // residual in fp64 against the fp64 b~ (an fp32 b~ would shift the fixed point)
+                        const float r = (float)((double)a[i] - bk[i]);
+                        ac[i] = role1 ? 0.f : r;
+                    }
+                }
+                if (has_next) fetch_next(j + 1);   // slot j+1 is complete: the P_j producer waited on it
+                if (pf) { const unsigned long long t = clock64(); c_set += t - tA; tA = t; }
+#pragma unroll
+                for (int G = 0; G < 8; G++) {
+                    const float m = (lane == G) ? 1.f : 0.f;
+                    // rows 4G..4G+3, sequential inside lane G, on temporaries
+                    const float c0 = fmaxf(-ac[0] * invd[0], -xo[0]);
+                    const float d0 = __shfl_sync(0xffffffffu, c0, G);
+                    float u1 = fmaf(-wg10, c0, -ac[1] * invd[1]);
+                    float u2 = fmaf(-wg20, c0, -ac[2] * invd[2]);
+                    float u3 = fmaf(-wg30, c0, -ac[3] * invd[3]);
+                    const float c1 = fmaxf(u1, -xo[1]);
+                    const float d1 = __shfl_sync(0xffffffffu, c1, G);
+                    u2 = fmaf(-wg21, c1, u2);
+                    u3 = fmaf(-wg31, c1, u3);
+                    const float c2 = fmaxf(u2, -xo[2]);
+                    const float d2 = __shfl_sync(0xffffffffu, c2, G);
+                    u3 = fmaf(-wg32, c2, u3);
+                    const float c3 = fmaxf(u3, -xo[3]);
+                    const float d3 = __shfl_sync(0xffffffffu, c3, G);
+                    xo[0] = fmaf(m, c0, xo[0]);
+                    xo[1] = fmaf(m, c1, xo[1]);
+                    xo[2] = fmaf(m, c2, xo[2]);
+                    xo[3] = fmaf(m, c3, xo[3]);
+                    // role 0: residuals of later lanes' rows; role 1: next block's lres
+                    const float dg[4] = {d0, d1, d2, d3};
+#pragma unroll
+                    for (int i = 0; i < 4; i++) {
+                        const float4 v = *reinterpret_cast<const float4 *>(tp + (4 * G + i) * 32 + L4);
+                        ac[0] = fmaf(v.x, dg[i], ac[0]);
+                        ac[1] = fmaf(v.y, dg[i], ac[1]);
+                        ac[2] = fmaf(v.z, dg[i], ac[2]);
+                        ac[3] = fmaf(v.w, dg[i], ac[3]);
+                    }
+                }
+                if (pf) { asm volatile("" ::"f"(xo[3])); const unsigned long long t = clock64(); c_rec += t - tA; tA = t; }
+                // role-1 accumulators (lanes 8-15) -> lres of lanes 0-7
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    lres[i] = __shfl_sync(0xffffffffu, ac[i], (lane & 7) + 8);
+                    xprev[i] = xo[i];
+                }
+                prev_row0 = row0;
+                __syncwarp();
+                if (lane == 0) mbar_arrive_local(&sh.stg_empty[sl]);
+                if (pf) { const unsigned long long t = clock64(); c_post += t - tA; tA = t; }
+                if (has_next) {
+#pragma unroll
+                    for (int i = 0; i < 4; i++) {
+                        invd[i] = n_invd[i];
+                        bk[i] = n_bk[i];
+                        xo[i] = (T == 1) ? xprev[i] : n_xo[i];
+                    }
+                    wg10 = n_wg[0]; wg20 = n_wg[1]; wg30 = n_wg[2]; wg21 = n_wg[3]; wg31 = n_wg[4]; wg32 = n_wg[5];
+                }
+                if (pf) { const unsigned long long t = clock64(); c_bc += t - tA; tA = t; }
             }
+            publish(total - 1, prev_row0);
+            if (pf) { prof[0] = w_p; prof[1] = w_s; prof[2] = c_set; prof[3] = c_rec; prof[4] = c_bc; prof[10] = c_pub; prof[11] = c_post; }
         }
         __syncthreads();
         // ---- output (leader): x~ and the embedded full-grid map (S8)
@@ -319,6 +495,45 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
         }
         cluster_sync();
     }
+}
+
+// Solver packets: one per (bin, block); reads the diagonal tile of A~ and b~.
+__global__ void gs_prep_kernel(const BinLayout *__restrict__ lay, const float *__restrict__ A,
+                               const double *__restrict__ bt, GsPacket *__restrict__ packets) {
+    const int bin = blockIdx.y;
+    const BinLayout L = lay[bin];
+    const int T = L.sp >> 5, k = blockIdx.x, r = threadIdx.x;
+    if (k >= T) return;
+    const float *D = A + L.a_off + ((size_t)k * T + k) * kTile;   // tile (k,k), [c][r]
+    GsPacket &P = packets[(L.v_off >> 5) + k];
+    const int row = 32 * k + r;
+    const float inv = (row < L.nk) ? __frcp_rn(D[r * 32 + r]) : 0.f;
+    P.invd[r] = inv;
+    P.b[r] = bt[L.v_off + row];
+    __shared__ float sinv[32];
+    sinv[r] = inv;
+    __syncwarp();
+    if (r < 8) {
+        const int q = 4 * r;   // rows q+i', columns q+i, i < i'
+        const float *c0 = D + (q + 0) * 32, *c1 = D + (q + 1) * 32, *c2 = D + (q + 2) * 32;
+        P.wg[r][0] = c0[q + 1] * sinv[q + 1];
+        P.wg[r][1] = c0[q + 2] * sinv[q + 2];
+        P.wg[r][2] = c0[q + 3] * sinv[q + 3];
+        P.wg[r][3] = c1[q + 2] * sinv[q + 2];
+        P.wg[r][4] = c1[q + 3] * sinv[q + 3];
+        P.wg[r][5] = c2[q + 3] * sinv[q + 3];
+        P.wg[r][6] = 0.f;
+        P.wg[r][7] = 0.f;
+    }
+}
+
+int gs_packet_bytes() { return kPacketBytes; }
+
+int launch_gs_prep(int n_bins, int max_sp, const BinLayout *lay_dev, const float *A, const double *bt,
+                   void *packets, cudaStream_t st) {
+    dim3 grid(max_sp >> 5, n_bins);
+    gs_prep_kernel<<<grid, 32, 0, st>>>(lay_dev, A, bt, (GsPacket *)packets);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
 // Layout conversions for the stage entry points: dense row-major n x n <-> tiled.
@@ -354,8 +569,20 @@ int gs_item_ints() { return (int)(sizeof(GsItem) / sizeof(int)); }
 int gs_group_size(int nk) { return nk >= 768 ? 4 : (nk >= 384 ? 2 : 1); }
 
 int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_sp, int *counter, const float *A,
-              const double *bt, int sweeps, float *x_out, float *x_map, const int32_t *keep_idx, int S,
+              const void *packets, int sweeps, float *x_out, float *x_map, const int32_t *keep_idx, int S,
               int num_sms, cudaStream_t st) {
+    // DWC_GS_PROFILE=1: clock64 breakdown of the first CTA's solver / consumer warp (stderr).
+    static const bool profile = getenv("DWC_GS_PROFILE") != nullptr;
+    unsigned long long *prof = nullptr;
+    if (profile) {
+        cudaMalloc(&prof, 16 * sizeof(unsigned long long));
+        cudaMemsetAsync(prof, 0, 16 * sizeof(unsigned long long), st);
+        if (getenv("DWC_GS_SKIP_STREAM_DOT")) {   // experiment: consumers skip the tile dots
+            unsigned long long one = 1;
+            cudaMemcpyAsync(prof + 15, &one, sizeof one, cudaMemcpyHostToDevice, st);
+            cudaStreamSynchronize(st);
+        }
+    }
     const size_t smem = gs_smem_bytes(max_sp);
     cudaFuncSetAttribute(gs_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaLaunchConfig_t cfg = {};
@@ -379,7 +606,19 @@ int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_s
     if (n_clusters < 1) n_clusters = 1;
     cfg.gridDim = dim3(n_clusters * kCl);
     cudaError_t e = cudaLaunchKernelEx(&cfg, gs_cluster_kernel, n_items, (const GsItem *)items, lay_dev, counter, A,
-                                       bt, sweeps, x_out, x_map, keep_idx, S);
+                                       (const GsPacket *)packets, sweeps, x_out, x_map, keep_idx, S, prof);
+    if (profile) {
+        unsigned long long h[16];
+        cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        const double n = h[9] ? (double)h[9] : 1.0;
+        fprintf(stderr,
+                "[gs-prof] steps=%llu grid=%d | solver cyc/step: wait_P %.0f wait_stg %.0f publish %.0f resid %.0f recur %.0f post %.0f prep %.0f"
+                " | consumer0: wait_x %.0f wait_tile %.0f compute %.0f reduce+send %.0f\n",
+                h[9], n_clusters * kCl, h[0] / n, h[1] / n, h[10] / n, (h[2] - h[10]) / n, h[3] / n, h[11] / n,
+                (h[4] - h[11]) / n, h[5] / n, h[6] / n, h[7] / n, h[8] / n);
+        cudaFree(prof);
+    }
     return e == cudaSuccess ? 1 : -1;
 }
 
