@@ -47,17 +47,21 @@ constexpr int kCl = 4;             // cluster size
 constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
 constexpr int kCons = kWarps - 3;  // consumer warps (3..7)
-constexpr int kStages = 16;        // ring depth (4 KB tiles)
+constexpr int kChunk = 4;          // tiles per ring slot (one contiguous bulk copy)
+constexpr int kRing = 4;           // ring slots
 constexpr int kTile = 1024;        // floats per tile
 constexpr int kStg = 4;            // solver tiles (L, D) prefetched this many steps ahead
 
 // Per-block solver packet (precomputed once per bin by gs_prep_kernel, staged with L/D):
 // invd[r] = 1/A_rr (0 for padding rows), wg[L][0..5] = within-group A[r][t]/A[r][r] for
-// lane L's rows r = 4L+i' > t = 4L+i  (order: 10 20 30 21 31 32), b~ of the block in fp64.
+// lane L's rows r = 4L+i' > t = 4L+i  (order: 10 20 30 21 31 32), and b~ of the block as an
+// fp32 pair b = bhi + blo (the residual (acc - bhi) - blo keeps b~'s fp64 accuracy: an fp32
+// b~ would shift the fixed point the sweeps converge to).
 struct __align__(16) GsPacket {
     float invd[32];
     float wg[8][8];
-    double b[32];
+    float bhi[32];
+    float blo[32];
 };
 constexpr int kPacketBytes = (int)sizeof(GsPacket);
 
@@ -67,11 +71,11 @@ struct GsItem {
 };
 
 struct __align__(128) GsSmem {
-    float ring[kStages][kTile];
+    float ring[kRing][kChunk][kTile];
     float stg[kStg][2][kTile];         // [step % kStg][0 = L tile, 1 = D tile]
     GsPacket pk[kStg];                 // solver packet of the staged block
     float pr[2][kCl][kCons][32];       // leader: partial row sums of every consumer warp of the sub-group
-    unsigned long long full[kStages], empty[kStages];
+    unsigned long long full[kRing], empty[kRing];
     unsigned long long stg_full[kStg], stg_empty[kStg];
     unsigned long long pready[2];      // leader: 1 arrival + g*kCons*128 tx bytes per step
     unsigned long long xr[2];          // leader: solver arrival; others: 1 arrival + 128 tx
@@ -152,6 +156,19 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
+// Next contiguous run of stream tiles at or after cur (skipping kx, kn), at most kChunk long.
+__device__ __forceinline__ bool next_chunk(int &cur, int hi, int kx, int kn, int &j0, int &nt) {
+    while (cur < hi && (cur == kx || cur == kn)) cur++;
+    if (cur >= hi) return false;
+    j0 = cur;
+    nt = 0;
+    while (cur < hi && cur != kx && cur != kn && nt < kChunk) {
+        cur++;
+        nt++;
+    }
+    return true;
+}
+
 // Consumer: acc[q] (rows 4*rq+q) += sum over columns c = cq + 4i of tile[c][4rq+q] * x[c].
 __device__ __forceinline__ void tile_dot(const float *__restrict__ tile, const float *__restrict__ xcol, int rq,
                                          int cq, float acc[4]) {
@@ -201,13 +218,16 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
         const int sp = L.sp, nk = L.nk, T = sp >> 5;
         const int total = (bin >= 0) ? sweeps * T : 0;
         const float *Ab = A + L.a_off;
+        // this CTA's contiguous range of tile columns (stream tiles: J in [c_lo, c_hi), J != kx, kn)
+        const int c_lo = (T * rg) / g, c_hi = (T * (rg + 1)) / g;
         const GsPacket *pkb = packets + (L.v_off >> 5);
 
         for (int i = tid; i < sp; i += kThreads) xs[i] = 0.f;
         if (tid == 0) {
-            for (int i = 0; i < kStages; i++) {
+            const int n_sw = is_leader ? kCons - 2 : kCons;
+            for (int i = 0; i < kRing; i++) {
                 mbar_init(&sh.full[i], 1);
-                mbar_init(&sh.empty[i], 1);
+                mbar_init(&sh.empty[i], (uint32_t)n_sw);   // every stream warp releases every chunk
             }
             for (int b = 0; b < kStg; b++) {
                 mbar_init(&sh.stg_full[b], 1);
@@ -225,18 +245,25 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
             // ================= stream producer (one lane): this CTA's tiles of each row block
             if (lane == 0) {
                 uint32_t seq = 0;
+                const bool ppf = prof && blockIdx.x == 0;
+                unsigned long long t0 = 0, p_wait = 0, p_issue = 0;
                 for (int s = 0; s < total; s++) {
                     const int kn = s % T, kx = (s + T - 1) % T;
                     const float *rowb = Ab + (size_t)kn * T * kTile;
-                    for (int J = rg; J < T; J += g) {
-                        if (J == kx || J == kn) continue;
-                        const uint32_t slot = seq % kStages;
-                        mbar_wait(&sh.empty[slot], ((seq / kStages) & 1) ^ 1);
-                        mbar_expect_tx(&sh.full[slot], kTile * 4);
-                        bulk_g2s(sh.ring[slot], rowb + (size_t)J * kTile, kTile * 4, &sh.full[slot]);
+                    int cur = c_lo;
+                    int j0, nt;
+                    while (next_chunk(cur, c_hi, kx, kn, j0, nt)) {
+                        const uint32_t slot = seq % kRing;
+                        if (ppf) t0 = clock64();
+                        mbar_wait(&sh.empty[slot], ((seq / kRing) & 1) ^ 1);
+                        if (ppf) { const unsigned long long t = clock64(); p_wait += t - t0; t0 = t; }
+                        mbar_expect_tx(&sh.full[slot], (uint32_t)nt * kTile * 4);
+                        bulk_g2s(sh.ring[slot][0], rowb + (size_t)j0 * kTile, (uint32_t)nt * kTile * 4, &sh.full[slot]);
+                        if (ppf) { const unsigned long long t = clock64(); p_issue += t - t0; }
                         seq++;
                     }
                 }
+                if (ppf) { prof[12] = p_wait; prof[13] = p_issue; prof[14] = seq; }
             }
         } else if (wid == 4) {
             // ================= staging producer (leader, one lane): L = (kn,kx), D = (kn,kn)
@@ -264,6 +291,16 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
             const bool do_L = is_leader && c == kCons - 1, do_D = is_leader && c == kCons - 2;
             uint32_t seq = 0;
             const bool skip_dot = prof && prof[15];
+            // leader, D warp: forward x of solver step jj to the sub-group's other CTAs (st.async
+            // completes 128 bytes on their x-ready barrier)
+            auto push_x = [&](int jj) {
+                if (g > 1 && lane < 8) {
+                    const int r0 = 32 * (jj % T) + 4 * lane;
+                    const float4 xv = *reinterpret_cast<const float4 *>(xs + r0);
+                    const uint32_t xa = smem_u32(xs + r0), xra = smem_u32(&sh.xr[jj & 1]);
+                    for (int q = 1; q < g; q++) st_async_v4(mapa(xa, leader + q), xv, mapa(xra, leader + q));
+                }
+            };
             const bool pf = prof && blockIdx.x == 0 && c == 0 && lane == 0;
             unsigned long long tA = 0, cw_x = 0, cw_full = 0, c_comp = 0, c_red = 0;
             for (int s = 0; s < total; s++) {
@@ -272,6 +309,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 if (s >= 2) {
                     if (!is_leader && c == 0 && lane == 0) mbar_expect_tx(&sh.xr[s & 1], 128);
                     mbar_wait(&sh.xr[s & 1], ((s - 2) >> 1) & 1);
+                    if (do_D) push_x(s - 2);
                 }
                 // arm P-ready for this step only now: x of solver step s-2 being published implies
                 // that step consumed P_{s-2}, i.e. the previous phase of this barrier completed
@@ -287,22 +325,19 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                     else if (T >= 2) tile_dot(sh.stg[b][1], xs + 32 * kn, rq, cq, acc);
                     __syncwarp();
                     if (lane == 0) mbar_arrive_local(&sh.stg_empty[b]);
-                    // stream-tile bookkeeping: these warps take none, but keep seq in step
-                    for (int J = rg; J < T; J += g) seq += (J != kx && J != kn);
+                    // these warps take no stream tiles
                 } else {
-                    int i = 0;
-                    for (int J = rg; J < T; J += g) {
-                        if (J == kx || J == kn) continue;
-                        if (i == c) {
-                            const uint32_t slot = seq % kStages;
-                            mbar_wait(&sh.full[slot], (seq / kStages) & 1);
-                            if (pf) { const unsigned long long t = clock64(); cw_full += t - tA; tA = t; }
-                            if (!skip_dot) tile_dot(sh.ring[slot], xs + 32 * J, rq, cq, acc);
-                            if (pf) { const unsigned long long t = clock64(); c_comp += t - tA; tA = t; }
-                            __syncwarp();
-                            if (lane == 0) mbar_arrive_local(&sh.empty[slot]);
-                        }
-                        i = (i + 1 == n_sw) ? 0 : i + 1;
+                    // chunks of this step: tile t of a chunk goes to stream warp t mod n_sw
+                    int cur = c_lo, j0, nt;
+                    while (next_chunk(cur, c_hi, kx, kn, j0, nt)) {
+                        const uint32_t slot = seq % kRing;
+                        mbar_wait(&sh.full[slot], (seq / kRing) & 1);
+                        if (pf) { const unsigned long long t = clock64(); cw_full += t - tA; tA = t; }
+                        for (int t = c; t < nt; t += n_sw)
+                            if (!skip_dot) tile_dot(sh.ring[slot][t], xs + 32 * (j0 + t), rq, cq, acc);
+                        if (pf) { const unsigned long long t = clock64(); c_comp += t - tA; tA = t; }
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_local(&sh.empty[slot]);
                         seq++;
                     }
                 }
@@ -316,6 +351,14 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                     st_async_v4(mapa(smem_u32(&sh.pr[s & 1][rg][c][4 * rq]), leader),
                                 make_float4(acc[0], acc[1], acc[2], acc[3]), mapa(smem_u32(&sh.pready[s & 1]), leader));
                 if (pf) { const unsigned long long t = clock64(); c_red += t - tA; tA = t; }
+            }
+            if (do_D) {
+                // the solver's last two blocks (steps total-2, total-1)
+                for (int s = total; s < total + 2; s++) {
+                    if (s < 2) continue;
+                    mbar_wait(&sh.xr[s & 1], ((s - 2) >> 1) & 1);
+                    push_x(s - 2);
+                }
             }
             if (!is_leader && c == 0 && total > 0) {
                 // the last two x blocks the leader pushes are not needed here: wait for them so
@@ -338,23 +381,17 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
             // arrived, so the stream warps read x_k^old for their share of that product.
             const int L4 = 4 * (lane & 7);
             const bool role1 = (lane >> 3) == 1;
-            const uint32_t xs_base = smem_u32(xs);
             float xprev[4] = {0.f, 0.f, 0.f, 0.f};
             float lres[4] = {0.f, 0.f, 0.f, 0.f};
             float invd[4], xo[4], wg10, wg20, wg30, wg21, wg31, wg32;
-            double bk[4];
+            float bhi[4], blo[4];
             int prev_row0 = -1;
             const bool pf = prof && blockIdx.x == 0 && lane == 0;
             unsigned long long tA = 0, w_p = 0, w_s = 0, c_set = 0, c_rec = 0, c_bc = 0, c_pub = 0, c_post = 0;
             auto publish = [&](int jj, int r0) {
                 // x of solver step jj (block at r0) -> own xs + x-ready; bulk copies to the others
-                const float4 xv = make_float4(xprev[0], xprev[1], xprev[2], xprev[3]);
-                if (lane < 8) {
-                    *reinterpret_cast<float4 *>(xs + r0 + L4) = xv;
-                    const uint32_t xa = xs_base + (uint32_t)(r0 + L4) * 4;
-                    const uint32_t xra = smem_u32(&sh.xr[jj & 1]);
-                    for (int q = 1; q < g; q++) st_async_v4(mapa(xa, leader + q), xv, mapa(xra, leader + q));
-                }
+                // local only: the leader's D-product warp pushes the block to the other CTAs
+                if (lane < 8) *reinterpret_cast<float4 *>(xs + r0 + L4) = make_float4(xprev[0], xprev[1], xprev[2], xprev[3]);
                 __syncwarp();
                 if (lane == 0) mbar_arrive_local(&sh.xr[jj & 1]);
             };
@@ -366,9 +403,10 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 const float4 w0 = *reinterpret_cast<const float4 *>(&P.wg[L4 >> 2][0]);
                 const float4 w1 = *reinterpret_cast<const float4 *>(&P.wg[L4 >> 2][4]);
                 wg10 = w0.x; wg20 = w0.y; wg30 = w0.z; wg21 = w0.w; wg31 = w1.x; wg32 = w1.y;
-                const double2 b01 = *reinterpret_cast<const double2 *>(&P.b[L4]);
-                const double2 b23 = *reinterpret_cast<const double2 *>(&P.b[L4 + 2]);
-                bk[0] = b01.x; bk[1] = b01.y; bk[2] = b23.x; bk[3] = b23.y;
+                const float4 bh = *reinterpret_cast<const float4 *>(&P.bhi[L4]);
+                const float4 bl = *reinterpret_cast<const float4 *>(&P.blo[L4]);
+                bhi[0] = bh.x; bhi[1] = bh.y; bhi[2] = bh.z; bhi[3] = bh.w;
+                blo[0] = bl.x; blo[1] = bl.y; blo[2] = bl.z; blo[3] = bl.w;
                 if (T == 1) {
 #pragma unroll
                     for (int i = 0; i < 4; i++) xo[i] = xprev[i];
@@ -380,8 +418,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
             mbar_wait(&sh.stg_full[0], 0);
             prepare(0);
             // operands of the next block, loaded ahead of the recurrence (latency hidden)
-            float n_invd[4], n_xo[4], n_wg[6];
-            double n_bk[4];
+            float n_invd[4], n_xo[4], n_wg[6], n_bhi[4], n_blo[4];
             auto fetch_next = [&](int jj) {
                 const GsPacket &P = sh.pk[jj % kStg];
                 const float4 iv = *reinterpret_cast<const float4 *>(&P.invd[L4]);
@@ -389,9 +426,10 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 const float4 w0 = *reinterpret_cast<const float4 *>(&P.wg[L4 >> 2][0]);
                 const float4 w1 = *reinterpret_cast<const float4 *>(&P.wg[L4 >> 2][4]);
                 n_wg[0] = w0.x; n_wg[1] = w0.y; n_wg[2] = w0.z; n_wg[3] = w0.w; n_wg[4] = w1.x; n_wg[5] = w1.y;
-                const double2 b01 = *reinterpret_cast<const double2 *>(&P.b[L4]);
-                const double2 b23 = *reinterpret_cast<const double2 *>(&P.b[L4 + 2]);
-                n_bk[0] = b01.x; n_bk[1] = b01.y; n_bk[2] = b23.x; n_bk[3] = b23.y;
+                const float4 bh = *reinterpret_cast<const float4 *>(&P.bhi[L4]);
+                const float4 bl = *reinterpret_cast<const float4 *>(&P.blo[L4]);
+                n_bhi[0] = bh.x; n_bhi[1] = bh.y; n_bhi[2] = bh.z; n_bhi[3] = bh.w;
+                n_blo[0] = bl.x; n_blo[1] = bl.y; n_blo[2] = bl.z; n_blo[3] = bl.w;
                 const float4 v = *reinterpret_cast<const float4 *>(xs + 32 * (jj % T) + L4);
                 n_xo[0] = v.x; n_xo[1] = v.y; n_xo[2] = v.z; n_xo[3] = v.w;
             };
@@ -419,8 +457,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                     }
 #pragma unroll
                     for (int i = 0; i < 4; i++) {
-                        // residual in fp64 against the fp64 b~ (an fp32 b~ would shift the fixed point)
-                        const float r = (float)((double)a[i] - bk[i]);
+                        const float r = (a[i] - bhi[i]) - blo[i];   // residual against b~ = bhi + blo
                         ac[i] = role1 ? 0.f : r;
                     }
                 }
@@ -474,7 +511,8 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
 #pragma unroll
                     for (int i = 0; i < 4; i++) {
                         invd[i] = n_invd[i];
-                        bk[i] = n_bk[i];
+                        bhi[i] = n_bhi[i];
+                        blo[i] = n_blo[i];
                         xo[i] = (T == 1) ? xprev[i] : n_xo[i];
                     }
                     wg10 = n_wg[0]; wg20 = n_wg[1]; wg30 = n_wg[2]; wg21 = n_wg[3]; wg31 = n_wg[4]; wg32 = n_wg[5];
@@ -509,7 +547,10 @@ __global__ void gs_prep_kernel(const BinLayout *__restrict__ lay, const float *_
     const int row = 32 * k + r;
     const float inv = (row < L.nk) ? __frcp_rn(D[r * 32 + r]) : 0.f;
     P.invd[r] = inv;
-    P.b[r] = bt[L.v_off + row];
+    const double bv = bt[L.v_off + row];
+    const float bh = (float)bv;
+    P.bhi[r] = bh;
+    P.blo[r] = (float)(bv - (double)bh);
     __shared__ float sinv[32];
     sinv[r] = inv;
     __syncwarp();
@@ -617,6 +658,8 @@ int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_s
                 " | consumer0: wait_x %.0f wait_tile %.0f compute %.0f reduce+send %.0f\n",
                 h[9], n_clusters * kCl, h[0] / n, h[1] / n, h[10] / n, (h[2] - h[10]) / n, h[3] / n, h[11] / n,
                 (h[4] - h[11]) / n, h[5] / n, h[6] / n, h[7] / n, h[8] / n);
+        fprintf(stderr, "[gs-prof] producer: chunks=%llu (%.1f/step) wait_empty %.0f issue %.0f cyc/chunk\n", h[14],
+                h[14] / n, h[14] ? (double)h[12] / h[14] : 0.0, h[14] ? (double)h[13] / h[14] : 0.0);
         cudaFree(prof);
     }
     return e == cudaSuccess ? 1 : -1;
