@@ -108,7 +108,8 @@ def run_reference(args, cfg):
     if rank != 0:
         return 0
     cores = os.cpu_count() or 1
-    nb = args.ref_bins or max(4, min(16, cores))
+    # each step: a bounded strided sample (~4 bins per core, a few seconds on the box)
+    nb = args.ref_bins or min(cfg.n_bins, 4 * cores)
     bins = synth.strided_bins(cfg.n_bins, nb)
     band = synth.make_band(cfg, bins=bins)
     oracle.build()
@@ -136,7 +137,8 @@ def cpu_baseline(cfg, budget_bins=None):
     """The oracle as it stands on the host cores, on a bounded strided sample."""
     import oracle
     cores = os.cpu_count() or 1
-    nb = budget_bins or max(4, min(16, cores))
+    # bounded sample sized for ~10-30 s of CPU work on the box (cfg3: 256 bins ~ 13 s on 16 cores)
+    nb = budget_bins or min(cfg.n_bins, 16 * cores)
     bins = synth.strided_bins(cfg.n_bins, nb)
     band = synth.make_band(cfg, bins=bins)
     oracle.build()
