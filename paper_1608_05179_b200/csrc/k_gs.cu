@@ -156,18 +156,37 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-// Next contiguous run of stream tiles at or after cur (skipping kx, kn), at most kChunk long.
-__device__ __forceinline__ bool next_chunk(int &cur, int hi, int kx, int kn, int &j0, int &nt) {
-    while (cur < hi && (cur == kx || cur == kn)) cur++;
-    if (cur >= hi) return false;
-    j0 = cur;
-    nt = 0;
-    while (cur < hi && cur != kx && cur != kn && nt < kChunk) {
-        cur++;
-        nt++;
+// Stream chunks of one step for the CTA column range [lo, hi): columns J != kx, kn as
+// contiguous runs of at most kChunk tiles.  If column kl = (kn-2) mod T -- the only block
+// whose x comes from the solver step just published -- is in the range, the order is rotated
+// so that kl is the very last tile: all other tiles can be consumed before that x arrives.
+struct ChunkIter {
+    int lo, hi, kx, kn, kl, cur, stop;
+    bool wrapped;
+    __device__ ChunkIter(int lo_, int hi_, int kx_, int kn_, int kl_) : lo(lo_), hi(hi_), kx(kx_), kn(kn_), kl(kl_) {
+        const bool rot = (kl >= lo && kl < hi && kl != kx && kl != kn);
+        cur = rot ? kl + 1 : lo;
+        stop = hi;
+        wrapped = !rot;
     }
-    return true;
-}
+    __device__ bool next(int &j0, int &nt) {
+        for (;;) {
+            while (cur < stop && (cur == kx || cur == kn)) cur++;
+            if (cur < stop) break;
+            if (wrapped) return false;
+            wrapped = true;            // second part of the rotation: [lo, kl]
+            cur = lo;
+            stop = kl + 1;
+        }
+        j0 = cur;
+        nt = 0;
+        while (cur < stop && cur != kx && cur != kn && nt < kChunk) {
+            cur++;
+            nt++;
+        }
+        return true;
+    }
+};
 
 // Consumer: acc[q] (rows 4*rq+q) += sum over columns c = cq + 4i of tile[c][4rq+q] * x[c].
 __device__ __forceinline__ void tile_dot(const float *__restrict__ tile, const float *__restrict__ xcol, int rq,
@@ -250,9 +269,9 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 for (int s = 0; s < total; s++) {
                     const int kn = s % T, kx = (s + T - 1) % T;
                     const float *rowb = Ab + (size_t)kn * T * kTile;
-                    int cur = c_lo;
+                    ChunkIter it(c_lo, c_hi, kx, kn, (s + T - 2) % T);
                     int j0, nt;
-                    while (next_chunk(cur, c_hi, kx, kn, j0, nt)) {
+                    while (it.next(j0, nt)) {
                         const uint32_t slot = seq % kRing;
                         if (ppf) t0 = clock64();
                         mbar_wait(&sh.empty[slot], ((seq / kRing) & 1) ^ 1);
@@ -304,37 +323,50 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
             const bool pf = prof && blockIdx.x == 0 && c == 0 && lane == 0;
             unsigned long long tA = 0, cw_x = 0, cw_full = 0, c_comp = 0, c_red = 0;
             for (int s = 0; s < total; s++) {
-                const int kn = s % T, kx = (s + T - 1) % T;
+                const int kn = s % T, kx = (s + T - 1) % T, kl = (s + T - 2) % T;
                 if (pf) tA = clock64();
-                if (s >= 2) {
-                    if (!is_leader && c == 0 && lane == 0) mbar_expect_tx(&sh.xr[s & 1], 128);
-                    mbar_wait(&sh.xr[s & 1], ((s - 2) >> 1) & 1);
-                    if (do_D) push_x(s - 2);
-                }
-                // arm P-ready for this step only now: x of solver step s-2 being published implies
-                // that step consumed P_{s-2}, i.e. the previous phase of this barrier completed
-                if (is_leader && c == 0 && lane == 0)
-                    mbar_expect_tx(&sh.pready[s & 1], (uint32_t)(g * kCons * 128));
+                // x of solver step s-3 (every column except kl = block of step s-2).  Observing it
+                // also guarantees the solver consumed P_{s-2}, so this step's partials cannot land
+                // in the previous phase of P-ready[s&1].  At s = 2 that guarantee needs x of step 0
+                // (published only after P_0 was consumed).
+                // Non-leader: arm x-ready for solver step s-2 first (its previous phase, step s-4,
+                // was observed by this warp at step s-1), since the waits below may target it.
+                if (!is_leader && c == 0 && lane == 0 && s >= 2) mbar_expect_tx(&sh.xr[s & 1], 128);
+                if (s >= 3) mbar_wait(&sh.xr[(s - 3) & 1], ((s - 3) >> 1) & 1);
+                else if (s == 2) mbar_wait(&sh.xr[0], 0);
+                // leader: arm this step's P-ready (its previous phase, step s-2, is complete)
+                if (is_leader && c == 0 && lane == 0) mbar_expect_tx(&sh.pready[s & 1], (uint32_t)(g * kCons * 128));
                 if (pf) { const unsigned long long t = clock64(); cw_x += t - tA; tA = t; }
                 float acc[4] = {0.f, 0.f, 0.f, 0.f};
                 if (do_L || do_D) {
                     const int b = s % kStg;
                     if (do_L && s + 1 < total) mbar_wait(&sh.stg_full[(s + 1) % kStg], ((s + 1) / kStg) & 1);
                     mbar_wait(&sh.stg_full[b], (s / kStg) & 1);
+                    // L: x_kx^old (last updated at step s-1-T); D: x_kn^old (step s-T).  With T <= 2
+                    // those may be step s-2.
+                    if (T <= 2 && s >= 2) mbar_wait(&sh.xr[s & 1], ((s - 2) >> 1) & 1);
                     if (do_L) tile_dot(sh.stg[b][0], xs + 32 * kx, rq, cq, acc);
                     else if (T >= 2) tile_dot(sh.stg[b][1], xs + 32 * kn, rq, cq, acc);
                     __syncwarp();
                     if (lane == 0) mbar_arrive_local(&sh.stg_empty[b]);
-                    // these warps take no stream tiles
+                    if (do_D && s >= 2) {
+                        // forward x of solver step s-2 to the sub-group's other CTAs
+                        if (T > 2) mbar_wait(&sh.xr[s & 1], ((s - 2) >> 1) & 1);
+                        push_x(s - 2);
+                    }
                 } else {
-                    // chunks of this step: tile t of a chunk goes to stream warp t mod n_sw
-                    int cur = c_lo, j0, nt;
-                    while (next_chunk(cur, c_hi, kx, kn, j0, nt)) {
+                    // chunks of this step: tile t of a chunk goes to stream warp t mod n_sw; the
+                    // tile of column kl (last in the order) waits for x of solver step s-2
+                    ChunkIter it(c_lo, c_hi, kx, kn, kl);
+                    int j0, nt;
+                    while (it.next(j0, nt)) {
                         const uint32_t slot = seq % kRing;
                         mbar_wait(&sh.full[slot], (seq / kRing) & 1);
                         if (pf) { const unsigned long long t = clock64(); cw_full += t - tA; tA = t; }
-                        for (int t = c; t < nt; t += n_sw)
+                        for (int t = c; t < nt; t += n_sw) {
+                            if (j0 + t == kl && s >= 2) mbar_wait(&sh.xr[s & 1], ((s - 2) >> 1) & 1);
                             if (!skip_dot) tile_dot(sh.ring[slot][t], xs + 32 * (j0 + t), rq, cq, acc);
+                        }
                         if (pf) { const unsigned long long t = clock64(); c_comp += t - tA; tA = t; }
                         __syncwarp();
                         if (lane == 0) mbar_arrive_local(&sh.empty[slot]);
@@ -361,12 +393,12 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 }
             }
             if (!is_leader && c == 0 && total > 0) {
-                // the last two x blocks the leader pushes are not needed here: wait for them so
-                // no async store lands after this item (barriers are re-initialised per item)
-                for (int s = total; s < total + 2; s++) {
-                    if (s < 2) continue;
-                    if (lane == 0) mbar_expect_tx(&sh.xr[s & 1], 128);
-                    mbar_wait(&sh.xr[s & 1], ((s - 2) >> 1) & 1);
+                // observe every remaining x-ready phase (steps total-3 .. total-1; the last two are
+                // armed here) so no async store lands after this item: barriers are re-initialised
+                for (int j = total - 3; j < total; j++) {
+                    if (j < 0) continue;
+                    if (j >= total - 2 && lane == 0) mbar_expect_tx(&sh.xr[j & 1], 128);
+                    mbar_wait(&sh.xr[j & 1], (j >> 1) & 1);
                 }
             }
             if (pf) {
