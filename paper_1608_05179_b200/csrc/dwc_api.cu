@@ -39,6 +39,15 @@ struct PinBuf {
     size_t bytes = 0;
 };
 
+// PSF output tiles (bin, I, J) of 128 rows x 64 columns that touch the upper triangle of the
+// sp x sp system (the kernel writes each computed entry and its mirror).
+void append_psf_tiles(std::vector<int4> &tiles, int bin, int sp) {
+    const int TR = dwc::psf_tile_rows(), TC = dwc::psf_tile_cols();
+    for (int I = 0; I * TR < sp; I++)
+        for (int J = 0; J * TC < sp; J++)
+            if (J * TC + TC - 1 >= I * TR) tiles.push_back(make_int4(bin, I, J, 0));
+}
+
 enum FlagBits { kFlagNonFinite = 1, kFlagSingular = 4 };
 
 }  // namespace
@@ -47,7 +56,7 @@ struct dwc_ctx {
     int device = 0;
     int num_sms = 148;
     size_t total_bytes = 0;
-    DevBuf mic, freq, dist, amp, herm, bint, xplanes, bt, A, lay, order, counter, tiles, flag, items, packets,
+    DevBuf mic, freq, dist, amp, herm, bint, opa, opb, rsc, bt, A, lay, order, counter, tiles, flag, items, packets,
         csm_h, nk_h, keep_h, xmap_h, bmap_h, gs_x, gs_b;
     PinBuf stage, readback;
     size_t stage_off = 0;
@@ -291,17 +300,21 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
     if (flags & kFlagNonFinite) return fail(DWC_ENUMERIC, "non-finite value in the CSM / DAS map");
     // host layout of the compressed systems
     std::vector<BinLayout> lay(n_bins);
-    int64_t a_off = 0, v_off = 0;
-    int max_sp = 0;
+    int64_t a_off = 0, v_off = 0, r_off = 0;
+    int max_sp = 0, max_rp = 0;
     double sum_sq = 0.0;
     int64_t sum_k = 0;
+    const int TR = psf_tile_rows();
     for (int k = 0; k < n_bins; k++) {
         const int nk = hk[k];
         const int sp = (nk + 31) & ~31;
-        lay[k] = {nk, sp, a_off, v_off};
+        const int rp = (nk + TR - 1) / TR * TR;
+        lay[k] = {nk, sp, a_off, v_off, rp, 0, r_off};
         a_off += (int64_t)sp * sp;
         v_off += sp;
+        r_off += rp;
         max_sp = std::max(max_sp, sp);
+        max_rp = std::max(max_rp, rp);
         sum_sq += (double)nk * nk;
         sum_k += nk;
     }
@@ -313,16 +326,14 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
     std::vector<int> items = build_gs_items(order, hk);
     const int n_items = (int)items.size() / gs_item_ints();
     std::vector<int4> tiles;
-    for (int k = 0; k < n_bins; k++) {
-        const int T = (lay[k].sp + 63) / 64;
-        for (int I = 0; I < T; I++)
-            for (int J = I; J < T; J++) tiles.push_back(make_int4(k, I, J, 0));
-    }
+    for (int k = 0; k < n_bins; k++) append_psf_tiles(tiles, k, lay[k].sp);
     if ((s = ensure(ctx, ctx->lay, sizeof(BinLayout) * n_bins))) return s;
     if ((s = ensure(ctx, ctx->items, sizeof(int) * items.size()))) return s;
     if ((s = ensure(ctx, ctx->tiles, sizeof(int4) * std::max<size_t>(tiles.size(), 1)))) return s;
     if ((s = ensure(ctx, ctx->counter, 64))) return s;
-    if ((s = ensure(ctx, ctx->xplanes, sizeof(double) * 2 * M * (size_t)v_off))) return s;
+    if ((s = ensure(ctx, ctx->opa, psf_opa_bytes(M, r_off))) || (s = ensure(ctx, ctx->opb, psf_opb_bytes(M, r_off))) ||
+        (s = ensure(ctx, ctx->rsc, sizeof(double) * (size_t)r_off)))
+        return s;
     if ((s = ensure(ctx, ctx->bt, sizeof(double) * (size_t)v_off))) return s;
     if ((s = ensure(ctx, ctx->A, sizeof(float) * (size_t)a_off))) return s;
     if ((s = ensure(ctx, ctx->packets, (size_t)gs_packet_bytes() * (size_t)(v_off / 32)))) return s;
@@ -334,11 +345,10 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
     if ((s = stage_end(ctx, st))) return s;
     ev(ctx, 3, st);
     // S5 (+S6)
-    LAUNCH(launch_steer_kept(G, (double *)ctx->dist.p, (double *)ctx->amp.p, n_bins, (double *)ctx->freq.p,
-                             (BinLayout *)ctx->lay.p, keep_idx, b, (double *)ctx->xplanes.p,
-                             (double *)ctx->bt.p, max_sp, st));
-    LAUNCH(launch_gram(M, (int)tiles.size(), (int4 *)ctx->tiles.p, (BinLayout *)ctx->lay.p,
-                       (double *)ctx->xplanes.p, (float *)ctx->A.p, st));
+    LAUNCH(launch_psf(G, (double *)ctx->dist.p, (double *)ctx->amp.p, n_bins, (double *)ctx->freq.p,
+                      (BinLayout *)ctx->lay.p, keep_idx, b, max_rp, (int)tiles.size(), (int4 *)ctx->tiles.p,
+                      (int8_t *)ctx->opa.p, (int8_t *)ctx->opb.p, (double *)ctx->rsc.p, (double *)ctx->bt.p,
+                      (float *)ctx->A.p, st));
     ev(ctx, 4, st);
     // S7 + S8
     CU(cudaMemsetAsync(x_map, 0, sizeof(float) * (size_t)n_bins * S, st));
@@ -416,7 +426,7 @@ dwc_status dwc_destroy(dwc_ctx *ctx) {
     if (!ctx) return DWC_OK;
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();
-    DevBuf *bufs[] = {&ctx->mic, &ctx->freq, &ctx->dist, &ctx->amp, &ctx->herm, &ctx->bint, &ctx->xplanes,
+    DevBuf *bufs[] = {&ctx->mic, &ctx->freq, &ctx->dist, &ctx->amp, &ctx->herm, &ctx->bint, &ctx->opa, &ctx->opb, &ctx->rsc,
                       &ctx->bt, &ctx->A, &ctx->lay, &ctx->order, &ctx->counter, &ctx->tiles, &ctx->flag,
                       &ctx->items, &ctx->packets, &ctx->csm_h, &ctx->nk_h, &ctx->keep_h, &ctx->xmap_h, &ctx->bmap_h, &ctx->gs_x, &ctx->gs_b};
     for (DevBuf *b : bufs)
@@ -553,24 +563,23 @@ dwc_status dwc_psf(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, dou
     Geo G;
     if ((s = prepare_geometry(ctx, arr, grid, 1, &freq_hz, G, launches, st))) return s;
     const int sp = (n_keep + 31) & ~31;
-    BinLayout lay{n_keep, sp, 0, 0};
+    const int rp = (n_keep + psf_tile_rows() - 1) / psf_tile_rows() * psf_tile_rows();
+    BinLayout lay{n_keep, sp, 0, 0, rp, 0, 0};
     std::vector<int4> tiles;
-    const int T = (sp + 63) / 64;
-    for (int I = 0; I < T; I++)
-        for (int J = I; J < T; J++) tiles.push_back(make_int4(0, I, J, 0));
+    append_psf_tiles(tiles, 0, sp);
     if ((s = ensure(ctx, ctx->lay, sizeof(BinLayout))) || (s = ensure(ctx, ctx->tiles, sizeof(int4) * tiles.size())) ||
-        (s = ensure(ctx, ctx->xplanes, sizeof(double) * 2 * arr->m * (size_t)sp)) ||
-        (s = ensure(ctx, ctx->bt, sizeof(double) * sp)) || (s = ensure(ctx, ctx->A, sizeof(float) * (size_t)sp * sp)))
+        (s = ensure(ctx, ctx->opa, psf_opa_bytes(arr->m, rp))) || (s = ensure(ctx, ctx->opb, psf_opb_bytes(arr->m, rp))) ||
+        (s = ensure(ctx, ctx->rsc, sizeof(double) * rp)) || (s = ensure(ctx, ctx->bt, sizeof(double) * sp)) ||
+        (s = ensure(ctx, ctx->A, sizeof(float) * (size_t)sp * sp)))
         return s;
     if ((s = stage_begin(ctx, sizeof(BinLayout) + sizeof(int4) * tiles.size() + 1024))) return s;
     if ((s = stage_upload(ctx, ctx->lay.p, &lay, sizeof(BinLayout), st))) return s;
     if ((s = stage_upload(ctx, ctx->tiles.p, tiles.data(), sizeof(int4) * tiles.size(), st))) return s;
     if ((s = stage_end(ctx, st))) return s;
-    LAUNCH(launch_steer_kept(G, (double *)ctx->dist.p, (double *)ctx->amp.p, 1, (double *)ctx->freq.p,
-                             (BinLayout *)ctx->lay.p, keep_idx, nullptr, (double *)ctx->xplanes.p,
-                             (double *)ctx->bt.p, sp, st));
-    LAUNCH(launch_gram(arr->m, (int)tiles.size(), (int4 *)ctx->tiles.p, (BinLayout *)ctx->lay.p,
-                       (double *)ctx->xplanes.p, (float *)ctx->A.p, st));
+    LAUNCH(launch_psf(G, (double *)ctx->dist.p, (double *)ctx->amp.p, 1, (double *)ctx->freq.p,
+                      (BinLayout *)ctx->lay.p, keep_idx, nullptr, rp, (int)tiles.size(), (int4 *)ctx->tiles.p,
+                      (int8_t *)ctx->opa.p, (int8_t *)ctx->opb.p, (double *)ctx->rsc.p, (double *)ctx->bt.p,
+                      (float *)ctx->A.p, st));
     LAUNCH(launch_tile_convert(0, n_keep, sp, (float *)ctx->A.p, A, st));
     return DWC_OK;
 }

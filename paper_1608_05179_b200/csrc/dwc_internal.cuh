@@ -50,21 +50,24 @@ struct BinLayout {
     int32_t nk;       // S~
     int32_t sp;       // padded size (multiple of 32)
     int64_t a_off;    // float offset of A~_k (sp*sp dense row-major)
-    int64_t v_off;    // float offset of per-bin vectors (sp entries) and of the E planes / sp
+    int64_t v_off;    // offset of per-bin vectors (sp entries)
+    int32_t rp;       // S~ padded to the PSF tile rows (128)
+    int32_t pad_;
+    int64_t r_off;    // row offset of the bin's PSF operand digits and row scales
 };
 
-// S5 part 1: kept steering planes X[k] = [Re E~; Im E~] in fp64 (2m rows x sp cols) and
-// bt[k][i] = b[k][keep[i]] (S6, fp64), zero padded to sp.
-// b may be NULL (bt then untouched).  Grid spans max_sp columns.
-int launch_steer_kept(const Geo &g, const double *dist, const double *amp, int n_bins,
-                      const double *freq, const BinLayout *lay, const int32_t *keep_idx,
-                      const double *b, double *xplanes, double *bt, int max_sp, cudaStream_t st);
-
-// S5 part 2: A~_k = |E~^H E~|^2 / M^2 (dense, both triangles written) over a list of
-// 64x64 upper tile pairs (bin, I, J, -).
-int launch_gram(int m, int n_tiles, const int4 *tiles, const BinLayout *lay_dev,
-                const double *xplanes, float *A, cudaStream_t st);
-
+// S5 + S6 on the tensor cores (k_psf.cu): int8 digit operands of the kept steering vectors
+// (opA: psf_opa_bytes, opB: psf_opb_bytes for sum rp rows; rsc: sum rp doubles), b~ = b[keep]
+// into bt (fp64, zero padded to sp; skipped when b is NULL), then A~_k over the (bin, I, J)
+// list of 128x64 output tiles touching the upper triangle, both triangles written.
+int psf_kp(int m);
+size_t psf_opa_bytes(int m, int64_t rows);
+size_t psf_opb_bytes(int m, int64_t rows);
+int psf_tile_rows();
+int psf_tile_cols();
+int launch_psf(const Geo &g, const double *dist, const double *amp, int n_bins, const double *freq,
+               const BinLayout *lay, const int32_t *keep_idx, const double *b, int max_rp, int n_tiles,
+               const int4 *tiles, int8_t *opA, int8_t *opB, double *rsc, double *bt, float *A, cudaStream_t st);
 
 // S5 storage layout of A~_k (shared by the Gram epilogue and the GS kernel): 32x32 fp32
 // tiles, column-major inside a tile, row-block-major; T = sp/32; element (i, j) at

@@ -1,135 +1,288 @@
-// k_psf.cu -- S5 PSF matrix on the compressed grid (+ S6 restriction of b).
+// k_psf.cu -- S5 PSF matrix on the compressed grid (+ S6 restriction of b), on the
+// 5th-generation tensor cores (tcgen05.mma kind::i8, accumulators in TMEM).
 //
 // Eq. 9-12 restricted by Eq. 23, reading R1:
 //   A~_ij = |e_i^H e_j|^2 / M^2  over the kept nodes i, j.
-// Real-GEMM decomposition of the complex Gram G = E~^H E~ with X = Re E~, Y = Im E~:
-//   Re G = X^T X + Y^T Y,   Im G = X^T Y - Y^T X,   A = (Re G^2 + Im G^2) / M^2.
-// G is Hermitian, so A is symmetric: only tile pairs I <= J are computed and mirrored.
+// Real-GEMM form of the complex Gram G = E~^H E~: with the per-node real vectors
+//   X_i = [Re e_i ; Im e_i]  and  Z_i = [-Im e_i ; Re e_i]   (length 2M),
+//   Re G_ij = X_i . X_j,   Im G_ij = Z_i . X_j,   A = (Re G^2 + Im G^2) / M^2.
 //
-// steer_kept_kernel: kept steering planes (fp64 phases and sincos), and b~ = b[keep] (S6,
-// kept in fp64: rounding b~ to fp32 perturbs the system the sweeps converge to).
-// gram_kernel: fp64 accumulation, 64x64 tiles, K = m in chunks of 16 staged in shared
-// memory; the |G|^2/M^2 epilogue rounds once to fp32 and stores the tiled layout the GS
-// kernel streams (dwc_internal.cuh tiled_index).  Measured on the configs, an fp32
-// accumulated Gram leaves |A - A_oracle| ~ 2e-7 (rel. L2), which GS amplifies ~10^3-10^4x
-// in ill-conditioned low-frequency bins (map error > 1e-3); fp64 accumulation gives the
-// correctly rounded fp32 A (~1e-8).  Only I <= J tiles are computed and entries with
-// j >= i are written together with their mirror, so A is exactly symmetric.
+// Precision: GS amplifies errors of A~ 10^3-10^4x in ill-conditioned bins, so
+// A~ must be fp32-accurate -- an fp32-accumulated Gram (|dA| ~ 2e-7) already fails the 1e-3 map
+// tolerance, and so does 3-pass TF32 with fp32 accumulation.  The Gram therefore runs as an
+// exact integer product: every row X_i (and Z_i) is scaled by a power of two 2^q_i and split
+// into kSl = 4 signed int8 digits, v 2^q = sum_s a_s 128^-(s+1) + rho, |rho| <= 2^-29, computed
+// exactly in fp64.  The digit products P_st = D_s^T D_t are exact int32 sums on the tensor
+// cores; the pairs with s + t = w share accumulator w (w = 0..3, pairs with s + t > 3 are
+// below the residual and dropped), so Re G and Im G take 4 accumulators each:
+//   G_ij = 2^-(q_i + q_j + 35) * (acc_0 2^21 + acc_1 2^14 + acc_2 2^7 + acc_3)   (int64, exact)
+// The epilogue squares in fp64 and rounds A once to fp32: |dA| <~ 1e-8, the accuracy of the
+// correctly rounded fp64 A.  G is computed exactly (integer), so A_ij and A_ji are bitwise
+// equal and only output tiles touching the upper triangle are computed (the rest mirrored).
+//
+// Kernels
+//  psf_slice_kernel  one warp per kept node: fp64 steering (sincos of k d, amplitude table),
+//                    power-of-two row scale, int8 digits of X and Z written directly in the
+//                    tensor-core operand layout; b~ = b[keep] (S6, fp64).
+//  psf_tc_kernel     one CTA per 128 x 64 output tile (bin, I, J): warp 0 streams the K steps
+//                    (32 bytes of K per step: 32 KB of A digits, 8 KB of B digits, two bulk
+//                    copies) into a 4-deep shared-memory ring; one thread of warp 1 issues the
+//                    20 MMAs (128x64x32, int8 -> s32) per step into 8 TMEM accumulators
+//                    (512 columns); warps 2-5 read TMEM and write A~ in the GS tile layout
+//                    (dwc_internal.cuh tiled_index), both (i, j) and the mirror (j, i).
+//
+// Operand layout (per bin; rp = nk rounded up to 128 rows, kp = 2M rounded up to 32 bytes):
+//   A side (8 matrices mt = X_0..X_3, Z_0..Z_3), byte of (mt, row r, k):
+//     (k/32)*(rp*256) + (r/8)*2048 + mt*256 + ((k/16)%2)*128 + (r%8)*16 + k%16
+//   B side (4 matrices t = X_0..X_3):
+//     (k/32)*(rp*128) + (r/8)*1024 + t*256 + ((k/16)%2)*128 + (r%8)*16 + k%16
+// so a 128-row A tile (64-row B tile) of one K step is a single contiguous 32 KB (8 KB) block,
+// and in shared memory each matrix is the canonical K-major no-swizzle UMMA layout with
+// LBO = 128 B and SBO = 2048 B (A) / 1024 B (B).
 #include <math.h>
 
 #include "dwc_internal.cuh"
+#include "sm100.cuh"
 
 namespace dwc {
 
-__global__ void steer_kept_kernel(Geo g, const double *__restrict__ dist, const double *__restrict__ amp,
-                                  const double *__restrict__ freq, const BinLayout *__restrict__ lay,
-                                  const int32_t *__restrict__ keep_idx, const double *__restrict__ b,
-                                  double *__restrict__ xplanes, double *__restrict__ bt) {
+using namespace sm100;
+
+constexpr int kSl = 4;                     // int8 digits per value
+constexpr int kTM = 128;                   // output tile rows (MMA M)
+constexpr int kTN = 64;                    // output tile cols (MMA N)
+constexpr int kAMat = 2 * kSl;             // X_s, Z_s
+constexpr int kBMat = kSl;                 // X_t
+constexpr int kABytes = kTM * 32 * kAMat;  // 32 KB per K step
+constexpr int kBBytes = kTN * 32 * kBMat;  //  8 KB per K step
+constexpr int kNS = 4;                     // ring depth
+constexpr int kTmemCols = 2 * kSl * kTN;   // 8 accumulators x 64 columns = 512
+constexpr int kPsfThreads = 192;
+
+__host__ __device__ inline size_t opa_index(int rp, int mt, int r, int k) {
+    return (size_t)(k >> 5) * ((size_t)rp * 256) + (size_t)(r >> 3) * 2048 + mt * 256 + ((k >> 4) & 1) * 128 +
+           (r & 7) * 16 + (k & 15);
+}
+__host__ __device__ inline size_t opb_index(int rp, int t, int r, int k) {
+    return (size_t)(k >> 5) * ((size_t)rp * 128) + (size_t)(r >> 3) * 1024 + t * 256 + ((k >> 4) & 1) * 128 +
+           (r & 7) * 16 + (k & 15);
+}
+
+// exact int8 digits of v in [-127/128, 127/128]: v = sum_s a[s] 128^-(s+1) + rho
+__device__ __forceinline__ void digits(double v, int a[kSl]) {
+#pragma unroll
+    for (int s = 0; s < kSl; s++) {
+        v *= 128.0;                // exact
+        const double d = rint(v);  // |d| <= 127 for s = 0, <= 64 after
+        a[s] = (int)d;
+        v -= d;                    // exact (fraction of a double)
+    }
+}
+
+__global__ void __launch_bounds__(256)
+psf_slice_kernel(Geo g, const double *__restrict__ dist, const double *__restrict__ amp,
+                 const double *__restrict__ freq, const BinLayout *__restrict__ lay,
+                 const int32_t *__restrict__ keep_idx, const double *__restrict__ b, int kp,
+                 int8_t *__restrict__ opA, int8_t *__restrict__ opB, double *__restrict__ rsc,
+                 double *__restrict__ bt) {
     const int bin = blockIdx.y;
     const BinLayout L = lay[bin];
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= L.sp) return;
+    const int lane = threadIdx.x & 31;
+    const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (r >= L.rp) return;
     const int M = g.m;
-    double *X = xplanes + L.v_off * 2 * M;
-    if (i < L.nk) {
-        const int s = keep_idx[(size_t)bin * g.S + i];
+    int8_t *A = opA + (size_t)L.r_off * kp * kAMat;
+    int8_t *B = opB + (size_t)L.r_off * kp * kBMat;
+    if (r < L.nk) {
+        const int s = keep_idx[(size_t)bin * g.S + r];
+        // power-of-two row scale from the amplitude bound |Re e|, |Im e| <= amp
+        double amax = 0.0;
+        for (int m = lane; m < M; m += 32) amax = fmax(amax, amp[(size_t)m * g.S + s]);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+        int e;
+        const double f = frexp(amax, &e);         // amax = f 2^e, f in [0.5, 1)
+        const int q = (f > 127.0 / 128.0) ? -e - 1 : -e;  // |v| 2^q <= 127/128
         const double k = kTwoPi * freq[bin] / g.c0;
-        for (int m = 0; m < M; m++) {
+        for (int m = lane; m < M; m += 32) {
             const double d = dist[(size_t)m * g.S + s], a = amp[(size_t)m * g.S + s];
             double sn, cs;
             sincos(k * d, &sn, &cs);
-            X[(size_t)m * L.sp + i] = a * cs;
-            X[(size_t)(M + m) * L.sp + i] = -(a * sn);
+            int dr[kSl], di[kSl];
+            digits(ldexp(a * cs, q), dr);
+            digits(ldexp(-(a * sn), q), di);
+#pragma unroll
+            for (int t = 0; t < kSl; t++) {
+                A[opa_index(L.rp, t, r, m)] = (int8_t)dr[t];            // X_t = [Re; Im]
+                A[opa_index(L.rp, t, r, M + m)] = (int8_t)di[t];
+                A[opa_index(L.rp, kSl + t, r, m)] = (int8_t)(-di[t]);   // Z_t = [-Im; Re]
+                A[opa_index(L.rp, kSl + t, r, M + m)] = (int8_t)dr[t];
+                B[opb_index(L.rp, t, r, m)] = (int8_t)dr[t];
+                B[opb_index(L.rp, t, r, M + m)] = (int8_t)di[t];
+            }
         }
-        if (b) bt[L.v_off + i] = b[(size_t)bin * g.S + s];
+        for (int kk = 2 * M + lane; kk < kp; kk += 32) {
+#pragma unroll
+            for (int t = 0; t < kSl; t++) {
+                A[opa_index(L.rp, t, r, kk)] = 0;
+                A[opa_index(L.rp, kSl + t, r, kk)] = 0;
+                B[opb_index(L.rp, t, r, kk)] = 0;
+            }
+        }
+        if (lane == 0) {
+            rsc[L.r_off + r] = ldexp(1.0, -2 * q - 35);
+            if (b) bt[L.v_off + r] = b[(size_t)bin * g.S + s];
+        }
     } else {
-        for (int m = 0; m < 2 * M; m++) X[(size_t)m * L.sp + i] = 0.0;
-        if (b) bt[L.v_off + i] = 0.0;
+        for (int kk = lane; kk < kp; kk += 32) {
+#pragma unroll
+            for (int t = 0; t < kSl; t++) {
+                A[opa_index(L.rp, t, r, kk)] = 0;
+                A[opa_index(L.rp, kSl + t, r, kk)] = 0;
+                B[opb_index(L.rp, t, r, kk)] = 0;
+            }
+        }
+        if (lane == 0) {
+            rsc[L.r_off + r] = 0.0;
+            if (b && r < L.sp) bt[L.v_off + r] = 0.0;
+        }
     }
 }
 
-int launch_steer_kept(const Geo &g, const double *dist, const double *amp, int n_bins,
-                      const double *freq, const BinLayout *lay, const int32_t *keep_idx,
-                      const double *b, double *xplanes, double *bt, int max_sp, cudaStream_t st) {
-    dim3 grid((max_sp + 127) / 128, n_bins);
-    steer_kept_kernel<<<grid, 128, 0, st>>>(g, dist, amp, freq, lay, keep_idx, b, xplanes, bt);
-    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
-}
+struct __align__(1024) PsfSmem {
+    int8_t a[kNS][kABytes];
+    int8_t b[kNS][kBBytes];
+    unsigned long long full[kNS], empty[kNS], tmem_full;
+    uint32_t tmem_base;
+};
 
-// ------------------------------------------------------------------------------------
-constexpr int kGT = 64;   // output tile
-constexpr int kGK = 16;   // K chunk
+__global__ void __launch_bounds__(kPsfThreads, 1)
+psf_tc_kernel(int M, int kp, const int4 *__restrict__ tiles, const BinLayout *__restrict__ lay,
+              const int8_t *__restrict__ opA, const int8_t *__restrict__ opB, const double *__restrict__ rsc,
+              float *__restrict__ Aout) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    PsfSmem &sm = *reinterpret_cast<PsfSmem *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int4 tl = tiles[blockIdx.x];  // (bin, I: 128-row block, J: 64-col block)
+    const BinLayout L = lay[tl.x];
+    const int nkc = kp >> 5;
 
-__global__ void __launch_bounds__(256)
-gram_kernel(int M, const int4 *__restrict__ tiles, const BinLayout *__restrict__ lay,
-            const double *__restrict__ xplanes, float *__restrict__ A) {
-    __shared__ double sXi[kGK][kGT], sYi[kGK][kGT], sXj[kGK][kGT], sYj[kGK][kGT];
-    const int4 t = tiles[blockIdx.x];  // (bin, I, J, -)
-    const BinLayout L = lay[t.x];
-    const int i0 = t.y * kGT, j0 = t.z * kGT;
-    const double *X = xplanes + L.v_off * 2 * M;
-    const double *Y = X + (size_t)M * L.sp;
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 16 x 16 threads, 4x4 each
-    double re[4][4], im[4][4];
-#pragma unroll
-    for (int a = 0; a < 4; a++)
-#pragma unroll
-        for (int c = 0; c < 4; c++) re[a][c] = im[a][c] = 0.0;
-    for (int m0 = 0; m0 < M; m0 += kGK) {
-        for (int e = threadIdx.x; e < kGK * kGT; e += 256) {
-            const int kk = e / kGT, col = e % kGT;
-            const int m = m0 + kk;
-            const bool okm = m < M;
-            const int ci = i0 + col, cj = j0 + col;
-            sXi[kk][col] = (okm && ci < L.sp) ? X[(size_t)m * L.sp + ci] : 0.0;
-            sYi[kk][col] = (okm && ci < L.sp) ? Y[(size_t)m * L.sp + ci] : 0.0;
-            sXj[kk][col] = (okm && cj < L.sp) ? X[(size_t)m * L.sp + cj] : 0.0;
-            sYj[kk][col] = (okm && cj < L.sp) ? Y[(size_t)m * L.sp + cj] : 0.0;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kNS; i++) {
+            mbar_init(&sm.full[i], 1);
+            mbar_init(&sm.empty[i], 1);
         }
-        __syncthreads();
-#pragma unroll
-        for (int kk = 0; kk < kGK; kk++) {
-            double xi[4], yi[4], xj[4], yj[4];
-#pragma unroll
-            for (int a = 0; a < 4; a++) {
-                xi[a] = sXi[kk][ty * 4 + a];
-                yi[a] = sYi[kk][ty * 4 + a];
-                xj[a] = sXj[kk][tx * 4 + a];
-                yj[a] = sYj[kk][tx * 4 + a];
-            }
-#pragma unroll
-            for (int a = 0; a < 4; a++)
-#pragma unroll
-                for (int c = 0; c < 4; c++) {
-                    re[a][c] = fma(xi[a], xj[c], re[a][c]);
-                    re[a][c] = fma(yi[a], yj[c], re[a][c]);
-                    im[a][c] = fma(xi[a], yj[c], im[a][c]);
-                    im[a][c] = fma(-yi[a], xj[c], im[a][c]);
-                }
-        }
-        __syncthreads();
+        mbar_init(&sm.tmem_full, 1);
+        fence_mbar_init();
     }
-    const double m2 = (double)M * (double)M;
-    float *Ab = A + L.a_off;
-    const int T = L.sp >> 5;
-#pragma unroll
-    for (int a = 0; a < 4; a++)
-#pragma unroll
-        for (int c = 0; c < 4; c++) {
-            const int i = i0 + ty * 4 + a, j = j0 + tx * 4 + c;
-            if (i < L.sp && j < L.sp && j >= i) {
-                const float v = (float)((re[a][c] * re[a][c] + im[a][c] * im[a][c]) / m2);
-                Ab[tiled_index(T, i, j)] = v;
-                if (j != i) Ab[tiled_index(T, j, i)] = v;
+    if (warp == 1) tmem_alloc(&sm.tmem_base, kTmemCols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = sm.tmem_base;
+
+    if (warp == 0) {
+        if (lane == 0) {  // producer: one K step = one 32 KB A block + one 8 KB B block
+            const int8_t *ga = opA + (size_t)L.r_off * kp * kAMat + (size_t)tl.y * (kTM / 8) * 2048;
+            const int8_t *gb = opB + (size_t)L.r_off * kp * kBMat + (size_t)tl.z * (kTN / 8) * 1024;
+            for (int kc = 0; kc < nkc; kc++) {
+                const int st = kc % kNS;
+                if (kc >= kNS) mbar_wait(&sm.empty[st], ((kc / kNS) - 1) & 1);
+                mbar_expect_tx(&sm.full[st], kABytes + kBBytes);
+                bulk_g2s(sm.a[st], ga + (size_t)kc * L.rp * 256, kABytes, &sm.full[st]);
+                bulk_g2s(sm.b[st], gb + (size_t)kc * L.rp * 128, kBBytes, &sm.full[st]);
             }
         }
+    } else if (warp == 1) {
+        if (lane == 0) {  // MMA issuer
+            constexpr uint32_t idesc = idesc_i8(kTM, kTN);
+            for (int kc = 0; kc < nkc; kc++) {
+                const int st = kc % kNS;
+                mbar_wait(&sm.full[st], (kc / kNS) & 1);
+                tc_fence_after();
+                const uint32_t sa = smem_u32(sm.a[st]), sb = smem_u32(sm.b[st]);
+#pragma unroll
+                for (int p = 0; p < 2; p++)
+#pragma unroll
+                    for (int s = 0; s < kSl; s++)
+#pragma unroll
+                        for (int t = 0; t + s < kSl; t++) {
+                            const uint64_t ad = smem_desc(sa + (p * kSl + s) * 256, 128, 2048);
+                            const uint64_t bd = smem_desc(sb + t * 256, 128, 1024);
+                            mma_i8(tmem + (uint32_t)((p * kSl + s + t) * kTN), ad, bd, idesc,
+                                   (kc > 0 || s > 0) ? 1u : 0u);
+                        }
+                mma_commit(&sm.empty[st]);  // frees the ring slot when these MMAs complete
+            }
+            mma_commit(&sm.tmem_full);
+        }
+    } else {
+        // epilogue: warp w reads TMEM lanes 32*(w%4) .. +31 (= tile rows)
+        const int q = warp & 3;
+        const int il = q * 32 + lane;
+        const int i = tl.y * kTM + il;
+        const int T = L.sp >> 5;
+        const bool row_ok = i < L.sp;
+        const double ri = row_ok ? rsc[L.r_off + i] : 0.0;
+        const double inv_m2 = 1.0 / ((double)M * (double)M);
+        float *Ab = Aout + L.a_off;
+        mbar_wait(&sm.tmem_full, 0);
+        tc_fence_after();
+        for (int jc = 0; jc < kTN; jc += 8) {
+            __syncwarp();
+            int32_t acc[2 * kSl][8];
+#pragma unroll
+            for (int a = 0; a < 2 * kSl; a++)
+                tmem_ld8(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * kTN + jc), acc[a]);
+            tmem_ld_wait();
+            const int j0 = tl.z * kTN + jc;
+            if (!row_ok || j0 >= L.sp) continue;  // sp is a multiple of 32: all 8 columns valid
+            float v[8];
+#pragma unroll
+            for (int c = 0; c < 8; c++) {
+                const long long gre = ((long long)acc[0][c] << 21) + ((long long)acc[1][c] << 14) +
+                                      ((long long)acc[2][c] << 7) + (long long)acc[3][c];
+                const long long gim = ((long long)acc[4][c] << 21) + ((long long)acc[5][c] << 14) +
+                                      ((long long)acc[6][c] << 7) + (long long)acc[7][c];
+                const double dre = (double)gre, dim = (double)gim;
+                const double sq = dre * dre + dim * dim;
+                v[c] = (float)(sq * ri * rsc[L.r_off + j0 + c] * inv_m2);
+            }
+#pragma unroll
+            for (int c = 0; c < 8; c++) Ab[tiled_index(T, i, j0 + c)] = v[c];  // coalesced over lanes
+            float4 *mir = reinterpret_cast<float4 *>(Ab + tiled_index(T, j0, i));  // (j0..j0+7, i): contiguous
+            mir[0] = make_float4(v[0], v[1], v[2], v[3]);
+            mir[1] = make_float4(v[4], v[5], v[6], v[7]);
+        }
+        tc_fence_before();
+    }
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem, kTmemCols);
 }
 
-int launch_gram(int m, int n_tiles, const int4 *tiles, const BinLayout *lay_dev,
-                const double *xplanes, float *A, cudaStream_t st) {
-    if (n_tiles <= 0) return 0;
-    gram_kernel<<<n_tiles, 256, 0, st>>>(m, tiles, lay_dev, xplanes, A);
-    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+int psf_kp(int m) { return ((2 * m + 31) / 32) * 32; }
+size_t psf_opa_bytes(int m, int64_t rows) { return (size_t)rows * psf_kp(m) * kAMat; }
+size_t psf_opb_bytes(int m, int64_t rows) { return (size_t)rows * psf_kp(m) * kBMat; }
+int psf_tile_rows() { return kTM; }
+int psf_tile_cols() { return kTN; }
+
+int launch_psf(const Geo &g, const double *dist, const double *amp, int n_bins, const double *freq,
+               const BinLayout *lay, const int32_t *keep_idx, const double *b, int max_rp, int n_tiles,
+               const int4 *tiles, int8_t *opA, int8_t *opB, double *rsc, double *bt, float *A, cudaStream_t st) {
+    const int kp = psf_kp(g.m);
+    dim3 grid((max_rp + 7) / 8, n_bins);
+    psf_slice_kernel<<<grid, 256, 0, st>>>(g, dist, amp, freq, lay, keep_idx, b, kp, opA, opB, rsc, bt);
+    if (cudaPeekAtLastError() != cudaSuccess) return -1;
+    if (n_tiles <= 0) return 1;
+    const size_t smem = sizeof(PsfSmem) + 1024;
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(psf_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return -1;
+        attr = true;
+    }
+    psf_tc_kernel<<<n_tiles, kPsfThreads, smem, st>>>(g.m, kp, tiles, lay, opA, opB, rsc, A);
+    return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
 }
 
 }  // namespace dwc

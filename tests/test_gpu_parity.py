@@ -148,18 +148,26 @@ def test_psf_parity_on_oracle_keep(ctx, torch_cuda, oracle_lib, cfgname, bin_):
     A = ctx.psf(g, f, torch.from_numpy(keep).cuda()).cpu().numpy()
     ref = oracle_lib.psf(*oracle_args(g), f, keep)
     assert rel_l2(A, ref) < TOL_A
+    assert rel_l2(A, ref) < 1e-7          # fp32-accurate (the fp64 PSF rounded to fp32)
     assert np.max(np.abs(A - A.T)) == 0.0
     assert np.max(np.abs(np.diag(A) - 1)) < 1e-6
 
 
-@pytest.mark.parametrize("nk", [1, 2, 31, 32, 33, 64, 65, 130])
-def test_psf_ragged_sizes(ctx, torch_cuda, oracle_lib, nk):
+@pytest.mark.parametrize("m,n,nk", [(24, 15, 1), (24, 15, 2), (24, 15, 31), (24, 15, 32), (24, 15, 33),
+                                    (24, 15, 64), (24, 15, 65), (24, 15, 127), (24, 15, 128), (24, 15, 129),
+                                    (24, 15, 200), (13, 15, 100), (5, 15, 40), (128, 21, 300), (128, 21, 441)])
+def test_psf_ragged_sizes(ctx, torch_cuda, oracle_lib, m, n, nk):
+    """Ragged S~ (one tile, tile edges, several 128x64 tiles + tail) and odd M (K padding)."""
     torch = torch_cuda
-    g = small_geom(24, 15, 3)
+    g = small_geom(m, n, 3 if m % 3 == 0 else 1)
     keep = np.sort(np.random.default_rng(nk).choice(g.S, size=nk, replace=False)).astype(np.int32)
     A = ctx.psf(g, 5100.0, torch.from_numpy(keep).cuda()).cpu().numpy()
     ref = oracle_lib.psf(*oracle_args(g), 5100.0, keep)
     assert rel_l2(A, ref) < TOL_A
+    # the int8-digit tensor-core Gram is exact to ~1e-9: A is the fp64 PSF rounded to fp32
+    assert rel_l2(A, ref) < 1e-7
+    assert np.max(np.abs(A - ref)) <= 2.0 ** -23
+    assert np.array_equal(A, A.T)
 
 
 # ---------------------------------------------------------------------------- S7
