@@ -13,6 +13,10 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
                  "-I", os.path.join(HERE, "..", "include"), "-Xptxas", "-v"]
+# DWC_NVCC_EXTRA: extra nvcc flags for experiments (e.g. -DGS_KSTG=4); DWC_LIB: output path
+COMMON += os.environ.get("DWC_NVCC_EXTRA", "").split()
+LIB = os.environ.get("DWC_LIB", LIB)
+BUILD = os.environ.get("DWC_BUILD_DIR", BUILD)
 SOURCES = {
     "dwc_api.cu": [],
     "k_das.cu": [],

@@ -301,16 +301,18 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
     // host layout of the compressed systems
     std::vector<BinLayout> lay(n_bins);
     int64_t a_off = 0, v_off = 0, r_off = 0;
-    int max_sp = 0, max_rp = 0;
-    double sum_sq = 0.0;
+    int max_sp = 0, max_rp = 0, ystride = 0;
+    double sum_sq = 0.0, sum_sym = 0.0;
     int64_t sum_k = 0;
     const int TR = psf_tile_rows();
     for (int k = 0; k < n_bins; k++) {
         const int nk = hk[k];
         const int sp = (nk + 31) & ~31;
         const int rp = (nk + TR - 1) / TR * TR;
-        lay[k] = {nk, sp, a_off, v_off, rp, 0, r_off};
-        a_off += (int64_t)sp * sp;
+        lay[k] = {nk, sp, a_off, v_off, rp, gs_group_size(nk), r_off};
+        a_off += sym_tiles(sp / 32) * 1024;
+        ystride = std::max(ystride, gs_ystride(nk));
+        sum_sym += (double)nk * (nk + 1) / 2.0;
         v_off += sp;
         r_off += rp;
         max_sp = std::max(max_sp, sp);
@@ -318,7 +320,7 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
         sum_sq += (double)nk * nk;
         sum_k += nk;
     }
-    if (gs_smem_bytes(max_sp) > 227 * 1024)
+    if (gs_smem_bytes(max_sp, ystride) > 227 * 1024)
         return fail(DWC_EINVAL, "compressed grid of %d points exceeds the on-chip x capacity", max_sp);
     std::vector<int32_t> order(n_bins);
     std::iota(order.begin(), order.end(), 0);
@@ -356,7 +358,7 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
     ev(ctx, 5, st);
     LAUNCH(launch_gs_prep(n_bins, max_sp, (BinLayout *)ctx->lay.p, (float *)ctx->A.p, (double *)ctx->bt.p,
                           ctx->packets.p, st));
-    LAUNCH(launch_gs(n_items, (int *)ctx->items.p, (BinLayout *)ctx->lay.p, max_sp, (int *)ctx->counter.p,
+    LAUNCH(launch_gs(n_items, (int *)ctx->items.p, (BinLayout *)ctx->lay.p, max_sp, ystride, (int *)ctx->counter.p,
                      (float *)ctx->A.p, ctx->packets.p, p->sweeps, nullptr, x_map, keep_idx, S,
                      ctx->num_sms, st));
     ev(ctx, 6, st);
@@ -379,7 +381,7 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
     stt.n_bins = n_bins;
     stt.sum_keep = sum_k;
     stt.sum_keep_sq = sum_sq;
-    stt.gs_bytes = 4.0 * sum_sq * p->sweeps;
+    stt.gs_bytes = 4.0 * sum_sym * p->sweeps;   // the symmetric-packed A~ (fp32) once per sweep
     stt.psf_flops = 8.0 * M * sum_sq;
     stt.das_flops = 8.0 * (double)M * M * S * n_bins;
     stt.launches = launches;
@@ -564,13 +566,13 @@ dwc_status dwc_psf(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, dou
     if ((s = prepare_geometry(ctx, arr, grid, 1, &freq_hz, G, launches, st))) return s;
     const int sp = (n_keep + 31) & ~31;
     const int rp = (n_keep + psf_tile_rows() - 1) / psf_tile_rows() * psf_tile_rows();
-    BinLayout lay{n_keep, sp, 0, 0, rp, 0, 0};
+    BinLayout lay{n_keep, sp, 0, 0, rp, gs_group_size(n_keep), 0};
     std::vector<int4> tiles;
     append_psf_tiles(tiles, 0, sp);
     if ((s = ensure(ctx, ctx->lay, sizeof(BinLayout))) || (s = ensure(ctx, ctx->tiles, sizeof(int4) * tiles.size())) ||
         (s = ensure(ctx, ctx->opa, psf_opa_bytes(arr->m, rp))) || (s = ensure(ctx, ctx->opb, psf_opb_bytes(arr->m, rp))) ||
         (s = ensure(ctx, ctx->rsc, sizeof(double) * rp)) || (s = ensure(ctx, ctx->bt, sizeof(double) * sp)) ||
-        (s = ensure(ctx, ctx->A, sizeof(float) * (size_t)sp * sp)))
+        (s = ensure(ctx, ctx->A, sizeof(float) * 1024 * (size_t)sym_tiles(sp / 32))))
         return s;
     if ((s = stage_begin(ctx, sizeof(BinLayout) + sizeof(int4) * tiles.size() + 1024))) return s;
     if ((s = stage_upload(ctx, ctx->lay.p, &lay, sizeof(BinLayout), st))) return s;
@@ -580,7 +582,7 @@ dwc_status dwc_psf(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, dou
                       (BinLayout *)ctx->lay.p, keep_idx, nullptr, rp, (int)tiles.size(), (int4 *)ctx->tiles.p,
                       (int8_t *)ctx->opa.p, (int8_t *)ctx->opb.p, (double *)ctx->rsc.p, (double *)ctx->bt.p,
                       (float *)ctx->A.p, st));
-    LAUNCH(launch_tile_convert(0, n_keep, sp, (float *)ctx->A.p, A, st));
+    LAUNCH(launch_tile_convert(0, n_keep, sp, lay.g, (float *)ctx->A.p, A, st));
     return DWC_OK;
 }
 
@@ -592,16 +594,17 @@ dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int3
     if (sweeps < 1) return fail(DWC_EINVAL, "sweeps must be >= 1");
     if (!A || !b || !x) return fail(DWC_EINVAL, "NULL device buffer");
     const int sp = (n + 31) & ~31;
-    if (gs_smem_bytes(sp) > 227 * 1024) return fail(DWC_EINVAL, "n = %d exceeds the on-chip x capacity", n);
+    if (gs_smem_bytes(sp, gs_ystride(n)) > 227 * 1024)
+        return fail(DWC_EINVAL, "n = %d exceeds the on-chip x capacity", n);
     cudaStream_t st = (cudaStream_t)cuda_stream;
     int launches = 0;
-    BinLayout lay{n, sp, 0, 0};
+    BinLayout lay{n, sp, 0, 0, 0, gs_group_size(n), 0};
     std::vector<int32_t> order{0};
     int32_t nk0 = n;
     std::vector<int> items = build_gs_items(order, &nk0);
     if ((s = ensure(ctx, ctx->lay, sizeof(BinLayout))) || (s = ensure(ctx, ctx->items, sizeof(int) * items.size())) ||
         (s = ensure(ctx, ctx->counter, 64)) || (s = ensure(ctx, ctx->gs_b, sizeof(double) * sp)) ||
-        (s = ensure(ctx, ctx->gs_x, sizeof(float) * (size_t)sp * sp)) ||
+        (s = ensure(ctx, ctx->gs_x, sizeof(float) * 1024 * (size_t)sym_tiles(sp / 32))) ||
         (s = ensure(ctx, ctx->packets, (size_t)gs_packet_bytes() * (size_t)(sp / 32))))
         return s;
     if ((s = stage_begin(ctx, 1024 + sizeof(int) * items.size()))) return s;
@@ -609,12 +612,13 @@ dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int3
     if ((s = stage_upload(ctx, ctx->items.p, items.data(), sizeof(int) * items.size(), st))) return s;
     if ((s = stage_end(ctx, st))) return s;
     float *Ap = (float *)ctx->gs_x.p;
-    LAUNCH(launch_tile_convert(1, n, sp, A, Ap, st));
+    LAUNCH(launch_tile_convert(1, n, sp, lay.g, A, Ap, st));
     CU(cudaMemsetAsync(ctx->gs_b.p, 0, sizeof(double) * sp, st));
     CU(cudaMemcpyAsync(ctx->gs_b.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     CU(cudaMemsetAsync(ctx->counter.p, 0, 64, st));
     LAUNCH(launch_gs_prep(1, sp, (BinLayout *)ctx->lay.p, Ap, (double *)ctx->gs_b.p, ctx->packets.p, st));
     LAUNCH(launch_gs((int)items.size() / gs_item_ints(), (int *)ctx->items.p, (BinLayout *)ctx->lay.p, sp,
+                     gs_ystride(n),
                      (int *)ctx->counter.p, Ap, ctx->packets.p, sweeps, x, nullptr, nullptr, 0, ctx->num_sms,
                      st));
     return DWC_OK;

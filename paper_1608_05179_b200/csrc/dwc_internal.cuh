@@ -49,10 +49,10 @@ int launch_compress(int n, int n_bins, const double *b, double eps, int eps_mode
 struct BinLayout {
     int32_t nk;       // S~
     int32_t sp;       // padded size (multiple of 32)
-    int64_t a_off;    // float offset of A~_k (sp*sp dense row-major)
+    int64_t a_off;    // float offset of A~_k (sym_tiles(sp/32) tiles of 1024 floats)
     int64_t v_off;    // offset of per-bin vectors (sp entries)
     int32_t rp;       // S~ padded to the PSF tile rows (128)
-    int32_t pad_;
+    int32_t g;        // GS CTAs per bin (gs_group_size(nk)); fixes the tile order of A~_k
     int64_t r_off;    // row offset of the bin's PSF operand digits and row scales
 };
 
@@ -69,26 +69,56 @@ int launch_psf(const Geo &g, const double *dist, const double *amp, int n_bins, 
                const BinLayout *lay, const int32_t *keep_idx, const double *b, int max_rp, int n_tiles,
                const int4 *tiles, int8_t *opA, int8_t *opB, double *rsc, double *bt, float *A, cudaStream_t st);
 
-// S5 storage layout of A~_k (shared by the Gram epilogue and the GS kernel): 32x32 fp32
-// tiles, column-major inside a tile, row-block-major; T = sp/32; element (i, j) at
-//   a_off + ((i/32)*T + j/32)*1024 + (j%32)*32 + (i%32).
-__host__ __device__ inline size_t tiled_index(int T, int i, int j) {
-    return ((size_t)(i >> 5) * T + (j >> 5)) * 1024 + (size_t)(j & 31) * 32 + (i & 31);
+// S5 storage layout of A~_k (written by the PSF epilogue, streamed by the GS kernel).
+// A~ is symmetric (reading R1), so only one triangle is stored.  32x32 fp32 tiles, column-major
+// inside a tile (element (32I+r, 32J+c) at [c*32 + r]); T = sp/32 tile rows; g = CTAs the GS
+// kernel gives the bin (gs_group_size); tile indices relative to the bin's base a_off/1024:
+//   D_k = A[k][k]              at k                        (T tiles)
+//   L_k = A[k][(k-1) mod T]    at T + k                    (T tiles; the solver's sub-diagonal)
+//   U(I,J) = A[I][J], J > I    at 2T + row_base(I) + pos   (T(T-1)/2 tiles)
+// Row I's U tiles are grouped by owner CTA o = J mod g and ascending in J inside a group, so
+// the tiles a GS CTA streams from one row block are one contiguous run.
+__host__ __device__ inline int sym_cnt(int x, int o, int g) { return x >= o ? (x - o) / g + 1 : 0; }
+__host__ __device__ inline int sym_row_base(int T, int I) { return I * (T - 1) - I * (I - 1) / 2; }
+__host__ __device__ inline int sym_run_len(int T, int g, int I, int o) {
+    return sym_cnt(T - 1, o, g) - sym_cnt(I, o, g);
 }
+__host__ __device__ inline int sym_run_start(int T, int g, int I, int o) {
+    int s = 0;
+    for (int q = 0; q < o; q++) s += sym_run_len(T, g, I, q);
+    return 2 * T + sym_row_base(T, I) + s;
+}
+// first J > I owned by o
+__host__ __device__ inline int sym_run_j0(int g, int I, int o) { return I + 1 + ((o - (I + 1) % g) + g) % g; }
+__host__ __device__ inline int sym_u_tile(int T, int g, int I, int J) {
+    const int o = J % g;
+    return sym_run_start(T, g, I, o) + (sym_cnt(J - 1, o, g) - sym_cnt(I, o, g));
+}
+// stored tiles holding block (a, b) of A~ (up to two: U(0,T-1) is also L_0; for T = 1, D_0 = L_0)
+__host__ __device__ inline int sym_targets(int T, int g, int a, int b, int t[2]) {
+    int n = 0;
+    if (a == b) t[n++] = a;
+    else if (b > a) t[n++] = sym_u_tile(T, g, a, b);
+    if (b == (a + T - 1) % T) t[n++] = T + a;
+    return n;
+}
+__host__ __device__ inline int64_t sym_tiles(int T) { return (int64_t)T * (T - 1) / 2 + 2 * (int64_t)T; }
 
-// dense row-major n x n <-> tiled sp x sp (zero padded) conversions (stage entry points).
-int launch_tile_convert(int to_tiled, int n, int sp, const float *src, float *dst, cudaStream_t st);
+// dense row-major n x n <-> symmetric tile layout (zero padded to sp; g as above) for the
+// stage entry points.  to_sym reads the upper triangle of src only.
+int launch_tile_convert(int to_sym, int n, int sp, int g, const float *src, float *dst, cudaStream_t st);
 
 // S7+S8: Gauss-Seidel sweeps, persistent cluster kernel over LPT-ordered work items
 // (gs_item_ints() ints each: g, bin[4]); writes x_out (per bin at v_off, nullable) and
 // scatters into x_map[k*S + keep[i]] (nullable).
-size_t gs_smem_bytes(int max_sp);
+size_t gs_smem_bytes(int max_sp, int ystride);
+int gs_ystride(int nk);
 int gs_cluster_size();
 int gs_item_ints();
 int gs_group_size(int nk);
-int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_sp, int *counter, const float *A,
-              const void *packets, int sweeps, float *x_out, float *x_map, const int32_t *keep_idx, int S,
-              int num_sms, cudaStream_t st);
+int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_sp, int ystride, int *counter,
+              const float *A, const void *packets, int sweeps, float *x_out, float *x_map, const int32_t *keep_idx,
+              int S, int num_sms, cudaStream_t st);
 
 // Per-block solver packets (1/A_ii, within-group scaled coefficients, b~ block) for the GS
 // kernel: gs_packet_bytes() bytes per 32-row block, bin k's packets at v_off/32.

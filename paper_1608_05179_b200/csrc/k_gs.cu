@@ -50,7 +50,10 @@ constexpr int kCons = kWarps - 3;  // consumer warps (3..7)
 constexpr int kChunk = 4;          // tiles per ring slot (one contiguous bulk copy)
 constexpr int kRing = 4;           // ring slots
 constexpr int kTile = 1024;        // floats per tile
-constexpr int kStg = 4;            // solver tiles (L, D) prefetched this many steps ahead
+#ifndef GS_KSTG
+#define GS_KSTG 3
+#endif
+constexpr int kStg = GS_KSTG;            // solver tiles (L, D) prefetched this many steps ahead
 
 // Per-block solver packet (precomputed once per bin by gs_prep_kernel, staged with L/D):
 // invd[r] = 1/A_rr (0 for padding rows), wg[L][0..5] = within-group A[r][t]/A[r][r] for
@@ -156,37 +159,37 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-// Stream chunks of one step for the CTA column range [lo, hi): columns J != kx, kn as
-// contiguous runs of at most kChunk tiles.  If column kl = (kn-2) mod T -- the only block
-// whose x comes from the solver step just published -- is in the range, the order is rotated
-// so that kl is the very last tile: all other tiles can be consumed before that x arrives.
-struct ChunkIter {
-    int lo, hi, kx, kn, kl, cur, stop;
-    bool wrapped;
-    __device__ ChunkIter(int lo_, int hi_, int kx_, int kn_, int kl_) : lo(lo_), hi(hi_), kx(kx_), kn(kn_), kl(kl_) {
-        const bool rot = (kl >= lo && kl < hi && kl != kx && kl != kn);
-        cur = rot ? kl + 1 : lo;
-        stop = hi;
-        wrapped = !rot;
-    }
-    __device__ bool next(int &j0, int &nt) {
-        for (;;) {
-            while (cur < stop && (cur == kx || cur == kn)) cur++;
-            if (cur < stop) break;
-            if (wrapped) return false;
-            wrapped = true;            // second part of the rotation: [lo, kl]
-            cur = lo;
-            stop = kl + 1;
-        }
-        j0 = cur;
-        nt = 0;
-        while (cur < stop && cur != kx && cur != kn && nt < kChunk) {
-            cur++;
-            nt++;
-        }
-        return true;
-    }
+// The stream tiles of one step (row block kn) for CTA rg of a g-CTA sub-group, in ring order:
+// three contiguous runs of the symmetric layout (dwc_internal.cuh), each cut into chunks of
+// <= kChunk tiles:
+//  seg 0  row use      U(kn, J), J > kn, J = rg mod g (minus J = T-1 = kx when kn = 0), x_J old
+//  seg 1  scatter      U(kn-3, J)^T x_{kn-3}^new for J >= kn (kn >= 3): J = kn into P_kn, J > kn
+//                      into the warp's y_J (the lower part of row J, consumed at step J)
+//  seg 2  pull         U(kn-2, kn)^T x_{kn-2}^new (kn >= 2, kn owned): x of the solver step but
+//                      one, so it is last
+// A[kn, kn-1] (L) and A[kn, kn] (D) are staged for the leader's solver / L / D warps.
+// The runs are computed once per work item into shared memory (seg_table) so the per-step cost
+// on the critical path is three LDS.128.
+struct __align__(16) Seg {
+    int t0, len, j0, pad;   // first tile (bin-relative), tiles, J of the first tile
 };
+__device__ Seg seg_run(int T, int g, int rg, int kn, int seg) {
+    Seg r{0, 0, 0, 0};
+    if (seg == 0 || seg == 1) {
+        const int I = (seg == 0) ? kn : kn - 3;
+        if (I < 0) return r;
+        int len = sym_run_len(T, g, I, rg), st = sym_run_start(T, g, I, rg), j = sym_run_j0(g, I, rg);
+        if (seg == 0) {
+            if (kn == 0 && len > 0 && j + g * (len - 1) == T - 1) len--;
+        } else {
+            while (len > 0 && j < kn) { j += g; st++; len--; }
+        }
+        r.t0 = st; r.len = len; r.j0 = j;
+    } else if (kn >= 2 && kn % g == rg) {
+        r.t0 = sym_u_tile(T, g, kn - 2, kn); r.len = 1; r.j0 = kn;
+    }
+    return r;
+}
 
 // Consumer: acc[q] (rows 4*rq+q) += sum over columns c = cq + 4i of tile[c][4rq+q] * x[c].
 __device__ __forceinline__ void tile_dot(const float *__restrict__ tile, const float *__restrict__ xcol, int rq,
@@ -203,6 +206,27 @@ __device__ __forceinline__ void tile_dot(const float *__restrict__ tile, const f
     }
 }
 
+// Consumer, transposed tile: acc[q] (output 4*rq+q = tile column) += sum over the tile rows r
+// of lane (rq, cq)'s 4-row chunks b = (rq + cq + 4i) mod 8 of tile[4rq+q][r] * x[r] (rotation
+// keeps each quarter-warp on 8 distinct 16-byte bank groups); the reduction over cq is the
+// same as tile_dot's.
+__device__ __forceinline__ void tile_tdot(const float *__restrict__ tile, const float *__restrict__ xcol, int rq,
+                                          int cq, float acc[4]) {
+#pragma unroll
+    for (int i = 0; i < 2; i++) {
+        const int r0 = 4 * ((rq + cq + 4 * i) & 7);
+        const float4 xv = *reinterpret_cast<const float4 *>(xcol + r0);
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const float4 v = *reinterpret_cast<const float4 *>(tile + (4 * rq + q) * 32 + r0);
+            acc[q] = fmaf(v.x, xv.x, acc[q]);
+            acc[q] = fmaf(v.y, xv.y, acc[q]);
+            acc[q] = fmaf(v.z, xv.z, acc[q]);
+            acc[q] = fmaf(v.w, xv.w, acc[q]);
+        }
+    }
+}
+
 // Stream step s computes P for block kn = s mod T excluding kx = (s-1) mod T.  Stream tiles
 // of sub-group rank rg: J in [0,T), J mod g == rg, J != kx, J != kn.  The leader also stages
 // tile (kn,kx) (L, for the solver) and (kn,kn) (D, solver + its old-x product).
@@ -210,10 +234,13 @@ __global__ void __launch_bounds__(kThreads, 2)
 gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout *__restrict__ lay,
                   int *__restrict__ counter, const float *__restrict__ A, const GsPacket *__restrict__ packets,
                   int sweeps, float *__restrict__ x_out, float *__restrict__ x_map,
-                  const int32_t *__restrict__ keep_idx, int S, unsigned long long *__restrict__ prof) {
+                  const int32_t *__restrict__ keep_idx, int S, int xcap, int ystride,
+                  unsigned long long *__restrict__ prof) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     GsSmem &sh = *reinterpret_cast<GsSmem *>(smem_raw);
     float *xs = reinterpret_cast<float *>(smem_raw + sizeof(GsSmem));
+    float *ys = xs + xcap;   // per stream warp: y_J (lower part of row J) for the owned J, J/g-indexed
+    Seg *segt = reinterpret_cast<Seg *>(ys + kCons * ystride);   // [kn][3] runs of this CTA
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint32_t crank = cluster_rank();
 
@@ -227,21 +254,21 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
         const int item = sh.item;
         if (item >= n_items) break;
         const GsItem IT = items[item];
-        const int g = IT.g;
+        const int g = IT.g, lg = g >> 1;   // g in {1, 2, 4}
         const int sg = (int)crank / g, rg = (int)crank % g;
         const uint32_t leader = (uint32_t)(sg * g);
         const bool is_leader = (rg == 0);
         const int bin = IT.bin[sg];
-        BinLayout L = {0, 0, 0, 0};
+        BinLayout L = {0, 0, 0, 0, 0, 0, 0};
         if (bin >= 0) L = lay[bin];
         const int sp = L.sp, nk = L.nk, T = sp >> 5;
         const int total = (bin >= 0) ? sweeps * T : 0;
         const float *Ab = A + L.a_off;
-        // this CTA's contiguous range of tile columns (stream tiles: J in [c_lo, c_hi), J != kx, kn)
-        const int c_lo = (T * rg) / g, c_hi = (T * (rg + 1)) / g;
         const GsPacket *pkb = packets + (L.v_off >> 5);
 
         for (int i = tid; i < sp; i += kThreads) xs[i] = 0.f;
+        for (int i = tid; i < kCons * ystride; i += kThreads) ys[i] = 0.f;
+        for (int i = tid; i < 3 * T; i += kThreads) segt[i] = seg_run(T, g, rg, i / 3, i % 3);
         if (tid == 0) {
             const int n_sw = is_leader ? kCons - 2 : kCons;
             for (int i = 0; i < kRing; i++) {
@@ -267,17 +294,16 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 const bool ppf = prof && blockIdx.x == 0;
                 unsigned long long t0 = 0, p_wait = 0, p_issue = 0;
                 for (int s = 0; s < total; s++) {
-                    const int kn = s % T, kx = (s + T - 1) % T;
-                    const float *rowb = Ab + (size_t)kn * T * kTile;
-                    ChunkIter it(c_lo, c_hi, kx, kn, (s + T - 2) % T);
-                    int j0, nt;
-                    while (it.next(j0, nt)) {
+                    const Seg *sd = segt + 3 * (s % T);
+                    for (int sg = 0; sg < 3; sg++)
+                    for (int off = 0; off < sd[sg].len; off += kChunk) {
+                        const int tt = sd[sg].t0 + off, nt = min(kChunk, sd[sg].len - off);
                         const uint32_t slot = seq % kRing;
                         if (ppf) t0 = clock64();
                         mbar_wait(&sh.empty[slot], ((seq / kRing) & 1) ^ 1);
                         if (ppf) { const unsigned long long t = clock64(); p_wait += t - t0; t0 = t; }
                         mbar_expect_tx(&sh.full[slot], (uint32_t)nt * kTile * 4);
-                        bulk_g2s(sh.ring[slot][0], rowb + (size_t)j0 * kTile, (uint32_t)nt * kTile * 4, &sh.full[slot]);
+                        bulk_g2s(sh.ring[slot][0], Ab + (size_t)tt * kTile, (uint32_t)nt * kTile * 4, &sh.full[slot]);
                         if (ppf) { const unsigned long long t = clock64(); p_issue += t - t0; }
                         seq++;
                     }
@@ -289,12 +315,11 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
             // (warp 4 shares the solver's SM sub-partition; it is mostly asleep in try_wait)
             if (is_leader && lane == 0) {
                 for (int s = 0; s < total; s++) {
-                    const int kn = s % T, kx = (s + T - 1) % T, sl = s % kStg;
-                    const float *rowb = Ab + (size_t)kn * T * kTile;
+                    const int kn = s % T, sl = s % kStg;
                     mbar_wait(&sh.stg_empty[sl], ((s / kStg) & 1) ^ 1);
                     mbar_expect_tx(&sh.stg_full[sl], 2 * kTile * 4 + kPacketBytes);
-                    bulk_g2s(sh.stg[sl][0], rowb + (size_t)kx * kTile, kTile * 4, &sh.stg_full[sl]);
-                    bulk_g2s(sh.stg[sl][1], rowb + (size_t)kn * kTile, kTile * 4, &sh.stg_full[sl]);
+                    bulk_g2s(sh.stg[sl][0], Ab + (size_t)(T + kn) * kTile, kTile * 4, &sh.stg_full[sl]);   // L_kn
+                    bulk_g2s(sh.stg[sl][1], Ab + (size_t)kn * kTile, kTile * 4, &sh.stg_full[sl]);         // D_kn
                     bulk_g2s(&sh.pk[sl], pkb + kn, kPacketBytes, &sh.stg_full[sl]);
                 }
             }
@@ -355,22 +380,61 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                         push_x(s - 2);
                     }
                 } else {
-                    // chunks of this step: tile t of a chunk goes to stream warp t mod n_sw; the
-                    // tile of column kl (last in the order) waits for x of solver step s-2
-                    ChunkIter it(c_lo, c_hi, kx, kn, kl);
-                    int j0, nt;
-                    while (it.next(j0, nt)) {
-                        const uint32_t slot = seq % kRing;
-                        mbar_wait(&sh.full[slot], (seq / kRing) & 1);
-                        if (pf) { const unsigned long long t = clock64(); cw_full += t - tA; tA = t; }
-                        for (int t = c; t < nt; t += n_sw) {
-                            if (j0 + t == kl && s >= 2) mbar_wait(&sh.xr[s & 1], ((s - 2) >> 1) & 1);
-                            if (!skip_dot) tile_dot(sh.ring[slot][t], xs + 32 * (j0 + t), rq, cq, acc);
+                    // chunks of this step (seg_table): the step's i-th tile goes to stream warp i mod n_sw
+                    float *yw = ys + c * ystride;
+                    const Seg *sd = segt + 3 * kn;
+                    // the lower part of row kn this warp accumulated from earlier steps' scatters
+                    if ((kn & (g - 1)) == rg && cq == 0) {
+                        float4 *yp = reinterpret_cast<float4 *>(yw + (kn >> lg) * 32 + 4 * rq);
+                        const float4 o = *yp;
+                        acc[0] += o.x; acc[1] += o.y; acc[2] += o.z; acc[3] += o.w;
+                        *yp = make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+                    int first = c;   // index (within the next chunk) of this warp's first tile
+                    for (int sg = 0; sg < 3; sg++) {
+                        const Seg sr = sd[sg];
+                        const float *xsrc = xs + 32 * (sg == 1 ? kn - 3 : kn - 2);   // transposed uses
+                        for (int off = 0; off < sr.len; off += kChunk) {
+                            const int nt = min(kChunk, sr.len - off);
+                            const uint32_t slot = seq % kRing;
+                            mbar_wait(&sh.full[slot], (seq / kRing) & 1);
+                            if (pf) { const unsigned long long t = clock64(); cw_full += t - tA; tA = t; }
+                            int t = first;
+                            for (; t < nt && !skip_dot; t += n_sw) {
+                                const int J = sr.j0 + g * (off + t);
+                                const float *tile = sh.ring[slot][t];
+                                if (sg == 0) {
+                                    // the tile of column kl (kn <= 1 only) needs x of solver step s-2
+                                    if (J == kl && s >= 2) mbar_wait(&sh.xr[s & 1], ((s - 2) >> 1) & 1);
+                                    tile_dot(tile, xs + 32 * J, rq, cq, acc);
+                                    continue;
+                                }
+                                if (sg == 2) mbar_wait(&sh.xr[s & 1], ((s - 2) >> 1) & 1);   // x_{kn-2}: step s-2
+                                float y4[4] = {0.f, 0.f, 0.f, 0.f};
+                                tile_tdot(tile, xsrc, rq, cq, y4);
+                                if (J == kn) {
+#pragma unroll
+                                    for (int q = 0; q < 4; q++) acc[q] += y4[q];
+                                } else {
+#pragma unroll
+                                    for (int q = 0; q < 4; q++) {
+                                        y4[q] += __shfl_xor_sync(0xffffffffu, y4[q], 8);
+                                        y4[q] += __shfl_xor_sync(0xffffffffu, y4[q], 16);
+                                    }
+                                    if (cq == 0) {
+                                        float4 *yp = reinterpret_cast<float4 *>(yw + (J >> lg) * 32 + 4 * rq);
+                                        float4 o = *yp;
+                                        o.x += y4[0]; o.y += y4[1]; o.z += y4[2]; o.w += y4[3];
+                                        *yp = o;
+                                    }
+                                }
+                            }
+                            first = t - nt;
+                            if (pf) { const unsigned long long t = clock64(); c_comp += t - tA; tA = t; }
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive_local(&sh.empty[slot]);
+                            seq++;
                         }
-                        if (pf) { const unsigned long long t = clock64(); c_comp += t - tA; tA = t; }
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive_local(&sh.empty[slot]);
-                        seq++;
                     }
                 }
                 // reduce over the 4 column groups: lanes (rq, cq) then hold rows 4rq..4rq+3
@@ -574,7 +638,7 @@ __global__ void gs_prep_kernel(const BinLayout *__restrict__ lay, const float *_
     const BinLayout L = lay[bin];
     const int T = L.sp >> 5, k = blockIdx.x, r = threadIdx.x;
     if (k >= T) return;
-    const float *D = A + L.a_off + ((size_t)k * T + k) * kTile;   // tile (k,k), [c][r]
+    const float *D = A + L.a_off + (size_t)k * kTile;   // D_k = tile (k,k), [c][r]
     GsPacket &P = packets[(L.v_off >> 5) + k];
     const int row = 32 * k + r;
     const float inv = (row < L.nk) ? __frcp_rn(D[r * 32 + r]) : 0.f;
@@ -609,30 +673,44 @@ int launch_gs_prep(int n_bins, int max_sp, const BinLayout *lay_dev, const float
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
-// Layout conversions for the stage entry points: dense row-major n x n <-> tiled.
-__global__ void tile_convert_kernel(int to_tiled, int n, int sp, const float *__restrict__ src,
+// Layout conversions for the stage entry points: dense row-major n x n <-> symmetric tiles.
+// to_sym: every (i, j) of the padded sp x sp matrix writes the stored tiles of its block with
+// the upper-triangle value src[min(i,j)][max(i,j)] (0 outside n).
+__global__ void tile_convert_kernel(int to_sym, int n, int sp, int g, const float *__restrict__ src,
                                     float *__restrict__ dst) {
     const int T = sp >> 5;
     const long total = (long)sp * sp;
     for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
-        const int tile = (int)(e >> 10), w = (int)(e & 1023);
-        const int I = tile / T, J = tile - (tile / T) * T, c = w >> 5, r = w & 31;
-        const int i = 32 * I + r, j = 32 * J + c;
-        if (to_tiled)
-            dst[e] = (i < n && j < n) ? src[(size_t)i * n + j] : 0.f;
-        else if (i < n && j < n)
-            dst[(size_t)i * n + j] = src[e];
+        const int i = (int)(e / sp), j = (int)(e - (long)(e / sp) * sp);
+        const int lo = min(i, j), hi = max(i, j);
+        if (to_sym) {
+            const float v = (hi < n) ? src[(size_t)lo * n + hi] : 0.f;
+            int t[2];
+            const int nt = sym_targets(T, g, i >> 5, j >> 5, t);
+            for (int u = 0; u < nt; u++) dst[(size_t)t[u] * kTile + (j & 31) * 32 + (i & 31)] = v;
+        } else if (i < n && j < n) {
+            const int tl = (lo >> 5) == (hi >> 5) ? (lo >> 5) : sym_u_tile(T, g, lo >> 5, hi >> 5);
+            dst[(size_t)i * n + j] = src[(size_t)tl * kTile + (hi & 31) * 32 + (lo & 31)];
+        }
     }
 }
 
-int launch_tile_convert(int to_tiled, int n, int sp, const float *src, float *dst, cudaStream_t st) {
+int launch_tile_convert(int to_sym, int n, int sp, int g, const float *src, float *dst, cudaStream_t st) {
     long total = (long)sp * sp;
     int blocks = (int)std::min<long>((total + 255) / 256, 148L * 32);
-    tile_convert_kernel<<<blocks, 256, 0, st>>>(to_tiled, n, sp, src, dst);
+    tile_convert_kernel<<<blocks, 256, 0, st>>>(to_sym, n, sp, g, src, dst);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
-size_t gs_smem_bytes(int max_sp) { return sizeof(GsSmem) + (size_t)max_sp * 4; }
+size_t gs_smem_bytes(int max_sp, int ystride) {
+    return sizeof(GsSmem) + (size_t)max_sp * 4 + (size_t)kCons * ystride * 4 + sizeof(Seg) * 3 * (size_t)(max_sp / 32);
+}
+
+// floats of y per stream warp: 32 per owned column block (ceil(T/g))
+int gs_ystride(int nk) {
+    const int T = (nk + 31) / 32, g = gs_group_size(nk);
+    return (T + g - 1) / g * 32;
+}
 
 int gs_cluster_size() { return kCl; }
 
@@ -641,7 +719,8 @@ int gs_item_ints() { return (int)(sizeof(GsItem) / sizeof(int)); }
 // CTAs per bin from S~ alone (batch-independent => bit-identical per-bin results).
 int gs_group_size(int nk) { return nk >= 768 ? 4 : (nk >= 384 ? 2 : 1); }
 
-int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_sp, int *counter, const float *A,
+int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_sp, int ystride, int *counter,
+              const float *A,
               const void *packets, int sweeps, float *x_out, float *x_map, const int32_t *keep_idx, int S,
               int num_sms, cudaStream_t st) {
     // DWC_GS_PROFILE=1: clock64 breakdown of the first CTA's solver / consumer warp (stderr).
@@ -656,7 +735,7 @@ int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_s
             cudaStreamSynchronize(st);
         }
     }
-    const size_t smem = gs_smem_bytes(max_sp);
+    const size_t smem = gs_smem_bytes(max_sp, ystride);
     cudaFuncSetAttribute(gs_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
@@ -679,7 +758,8 @@ int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_s
     if (n_clusters < 1) n_clusters = 1;
     cfg.gridDim = dim3(n_clusters * kCl);
     cudaError_t e = cudaLaunchKernelEx(&cfg, gs_cluster_kernel, n_items, (const GsItem *)items, lay_dev, counter, A,
-                                       (const GsPacket *)packets, sweeps, x_out, x_map, keep_idx, S, prof);
+                                       (const GsPacket *)packets, sweeps, x_out, x_map, keep_idx, S, max_sp, ystride,
+                                       prof);
     if (profile) {
         unsigned long long h[16];
         cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, st);

@@ -29,7 +29,7 @@
 //                    copies) into a 4-deep shared-memory ring; one thread of warp 1 issues the
 //                    20 MMAs (128x64x32, int8 -> s32) per step into 8 TMEM accumulators
 //                    (512 columns); warps 2-5 read TMEM and write A~ in the GS tile layout
-//                    (dwc_internal.cuh tiled_index), both (i, j) and the mirror (j, i).
+//                    (symmetric tile layout, dwc_internal.cuh), from (i, j) and the mirror (j, i).
 //
 // Operand layout (per bin; rp = nk rounded up to 128 rows, kp = 2M rounded up to 32 bytes):
 //   A side (8 matrices mt = X_0..X_3, Z_0..Z_3), byte of (mt, row r, k):
@@ -248,11 +248,20 @@ psf_tc_kernel(int M, int kp, const int4 *__restrict__ tiles, const BinLayout *__
                 const double sq = dre * dre + dim * dim;
                 v[c] = (float)(sq * ri * rsc[L.r_off + j0 + c] * inv_m2);
             }
+            // direct (i, j0..j0+7): coalesced over lanes; mirror (j0..j0+7, i): two float4 per lane
+            int td[2], tm[2];
+            const int nd = sym_targets(T, L.g, i >> 5, j0 >> 5, td);
+            const int nm = sym_targets(T, L.g, j0 >> 5, i >> 5, tm);
+            for (int u = 0; u < nd; u++) {
+                float *dst = Ab + (size_t)td[u] * 1024 + (i & 31);
 #pragma unroll
-            for (int c = 0; c < 8; c++) Ab[tiled_index(T, i, j0 + c)] = v[c];  // coalesced over lanes
-            float4 *mir = reinterpret_cast<float4 *>(Ab + tiled_index(T, j0, i));  // (j0..j0+7, i): contiguous
-            mir[0] = make_float4(v[0], v[1], v[2], v[3]);
-            mir[1] = make_float4(v[4], v[5], v[6], v[7]);
+                for (int c = 0; c < 8; c++) dst[((j0 + c) & 31) * 32] = v[c];
+            }
+            for (int u = 0; u < nm; u++) {
+                float4 *mir = reinterpret_cast<float4 *>(Ab + (size_t)tm[u] * 1024 + (i & 31) * 32 + (j0 & 31));
+                mir[0] = make_float4(v[0], v[1], v[2], v[3]);
+                mir[1] = make_float4(v[4], v[5], v[6], v[7]);
+            }
         }
         tc_fence_before();
     }

@@ -12,7 +12,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdwc.so")
+LIB_PATH = os.environ.get("DWC_LIB", os.path.join(_HERE, "libdwc.so"))   # override: experiments only
 
 DWC_FULL_GRID = 1
 STATUS = {0: "DWC_OK", -1: "DWC_EINVAL", -2: "DWC_ESINGULAR", -3: "DWC_ENUMERIC",
