@@ -73,9 +73,10 @@ int launch_psf(const Geo &g, const double *dist, const double *amp, int n_bins, 
 // A~ is symmetric (reading R1), so only one triangle is stored.  32x32 fp32 tiles, column-major
 // inside a tile (element (32I+r, 32J+c) at [c*32 + r]); T = sp/32 tile rows; g = CTAs the GS
 // kernel gives the bin (gs_group_size); tile indices relative to the bin's base a_off/1024:
-//   D_k = A[k][k]              at k                        (T tiles)
-//   L_k = A[k][(k-1) mod T]    at T + k                    (T tiles; the solver's sub-diagonal)
-//   U(I,J) = A[I][J], J > I    at 2T + row_base(I) + pos   (T(T-1)/2 tiles)
+//   D_k  = A[k][k]             at k                        (T tiles)
+//   L_k  = A[k][(k-1) mod T]   at T + k                    (T tiles; first sub-diagonal)
+//   LL_k = A[k][(k-2) mod T]   at 2T + k                   (T tiles; second sub-diagonal)
+//   U(I,J) = A[I][J], J > I    at 3T + row_base(I) + pos   (T(T-1)/2 tiles)
 // Row I's U tiles are grouped by owner CTA o = J mod g and ascending in J inside a group, so
 // the tiles a GS CTA streams from one row block are one contiguous run.
 __host__ __device__ inline int sym_cnt(int x, int o, int g) { return x >= o ? (x - o) / g + 1 : 0; }
@@ -86,7 +87,7 @@ __host__ __device__ inline int sym_run_len(int T, int g, int I, int o) {
 __host__ __device__ inline int sym_run_start(int T, int g, int I, int o) {
     int s = 0;
     for (int q = 0; q < o; q++) s += sym_run_len(T, g, I, q);
-    return 2 * T + sym_row_base(T, I) + s;
+    return 3 * T + sym_row_base(T, I) + s;
 }
 // first J > I owned by o
 __host__ __device__ inline int sym_run_j0(int g, int I, int o) { return I + 1 + ((o - (I + 1) % g) + g) % g; }
@@ -94,15 +95,17 @@ __host__ __device__ inline int sym_u_tile(int T, int g, int I, int J) {
     const int o = J % g;
     return sym_run_start(T, g, I, o) + (sym_cnt(J - 1, o, g) - sym_cnt(I, o, g));
 }
-// stored tiles holding block (a, b) of A~ (up to two: U(0,T-1) is also L_0; for T = 1, D_0 = L_0)
-__host__ __device__ inline int sym_targets(int T, int g, int a, int b, int t[2]) {
+// stored tiles holding block (a, b) of A~ (up to three: U(0,T-1) is also L_0, U(0,T-2) also
+// LL_0, ...; for T <= 2 the L / LL copies coincide with D or U)
+__host__ __device__ inline int sym_targets(int T, int g, int a, int b, int t[3]) {
     int n = 0;
     if (a == b) t[n++] = a;
     else if (b > a) t[n++] = sym_u_tile(T, g, a, b);
     if (b == (a + T - 1) % T) t[n++] = T + a;
+    if (b == (a + 2 * T - 2) % T) t[n++] = 2 * T + a;
     return n;
 }
-__host__ __device__ inline int64_t sym_tiles(int T) { return (int64_t)T * (T - 1) / 2 + 2 * (int64_t)T; }
+__host__ __device__ inline int64_t sym_tiles(int T) { return (int64_t)T * (T - 1) / 2 + 3 * (int64_t)T; }
 
 // dense row-major n x n <-> symmetric tile layout (zero padded to sp; g as above) for the
 // stage entry points.  to_sym reads the upper triangle of src only.

@@ -47,7 +47,7 @@ constexpr int kCl = 4;             // cluster size
 constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
 constexpr int kCons = kWarps - 3;  // consumer warps (3..7)
-constexpr int kChunk = 4;          // tiles per ring slot (one contiguous bulk copy)
+constexpr int kChunk = 3;          // tiles per ring slot (one contiguous bulk copy)
 constexpr int kRing = 4;           // ring slots
 constexpr int kTile = 1024;        // floats per tile
 #ifndef GS_KSTG
@@ -75,7 +75,7 @@ struct GsItem {
 
 struct __align__(128) GsSmem {
     float ring[kRing][kChunk][kTile];
-    float stg[kStg][2][kTile];         // [step % kStg][0 = L tile, 1 = D tile]
+    float stg[kStg][3][kTile];         // [step j % kStg]: L_j, D_j, LL_{j+2} (row blocks mod T)
     GsPacket pk[kStg];                 // solver packet of the staged block
     float pr[2][kCl][kCons][32];       // leader: partial row sums of every consumer warp of the sub-group
     unsigned long long full[kRing], empty[kRing];
@@ -160,34 +160,33 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 // The stream tiles of one step (row block kn) for CTA rg of a g-CTA sub-group, in ring order:
-// three contiguous runs of the symmetric layout (dwc_internal.cuh), each cut into chunks of
+// two contiguous runs of the symmetric layout (dwc_internal.cuh), each cut into chunks of
 // <= kChunk tiles:
-//  seg 0  row use      U(kn, J), J > kn, J = rg mod g (minus J = T-1 = kx when kn = 0), x_J old
+//  seg 0  row use      U(kn, J), J > kn, J = rg mod g, x_J old -- minus J = (kn-1) mod T and
+//                      (kn-2) mod T (kn <= 1), which are L_kn / LL_kn
 //  seg 1  scatter      U(kn-3, J)^T x_{kn-3}^new for J >= kn (kn >= 3): J = kn into P_kn, J > kn
 //                      into the warp's y_J (the lower part of row J, consumed at step J)
-//  seg 2  pull         U(kn-2, kn)^T x_{kn-2}^new (kn >= 2, kn owned): x of the solver step but
-//                      one, so it is last
-// A[kn, kn-1] (L) and A[kn, kn] (D) are staged for the leader's solver / L / D warps.
+// The first and second sub-diagonal blocks A[kn, kn-1] = L_kn and A[kn, kn-2] = LL_kn are done
+// by the leader: its L warp multiplies them with the old x (LL one step early) and the solver
+// adds their increments while it solves blocks kn-1 / kn-2.  So the stream needs only x of solver
+// step s-3 and older, and runs up to two steps ahead of the solver.
 // The runs are computed once per work item into shared memory (seg_table) so the per-step cost
-// on the critical path is three LDS.128.
+// is two LDS.128.
 struct __align__(16) Seg {
     int t0, len, j0, pad;   // first tile (bin-relative), tiles, J of the first tile
 };
 __device__ Seg seg_run(int T, int g, int rg, int kn, int seg) {
     Seg r{0, 0, 0, 0};
-    if (seg == 0 || seg == 1) {
-        const int I = (seg == 0) ? kn : kn - 3;
-        if (I < 0) return r;
-        int len = sym_run_len(T, g, I, rg), st = sym_run_start(T, g, I, rg), j = sym_run_j0(g, I, rg);
-        if (seg == 0) {
-            if (kn == 0 && len > 0 && j + g * (len - 1) == T - 1) len--;
-        } else {
-            while (len > 0 && j < kn) { j += g; st++; len--; }
-        }
-        r.t0 = st; r.len = len; r.j0 = j;
-    } else if (kn >= 2 && kn % g == rg) {
-        r.t0 = sym_u_tile(T, g, kn - 2, kn); r.len = 1; r.j0 = kn;
+    const int I = (seg == 0) ? kn : kn - 3;
+    if (I < 0) return r;
+    int len = sym_run_len(T, g, I, rg), st = sym_run_start(T, g, I, rg), j = sym_run_j0(g, I, rg);
+    if (seg == 0) {
+        const int kx = (kn + T - 1) % T, kl = (kn + T - 2) % T;
+        while (len > 0 && (j + g * (len - 1) == kx || j + g * (len - 1) == kl)) len--;
+    } else {
+        while (len > 0 && j < kn) { j += g; st++; len--; }
     }
+    r.t0 = st; r.len = len; r.j0 = j;
     return r;
 }
 
@@ -240,7 +239,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
     GsSmem &sh = *reinterpret_cast<GsSmem *>(smem_raw);
     float *xs = reinterpret_cast<float *>(smem_raw + sizeof(GsSmem));
     float *ys = xs + xcap;   // per stream warp: y_J (lower part of row J) for the owned J, J/g-indexed
-    Seg *segt = reinterpret_cast<Seg *>(ys + kCons * ystride);   // [kn][3] runs of this CTA
+    Seg *segt = reinterpret_cast<Seg *>(ys + kCons * ystride);   // [kn][2] runs of this CTA
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint32_t crank = cluster_rank();
 
@@ -268,7 +267,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
 
         for (int i = tid; i < sp; i += kThreads) xs[i] = 0.f;
         for (int i = tid; i < kCons * ystride; i += kThreads) ys[i] = 0.f;
-        for (int i = tid; i < 3 * T; i += kThreads) segt[i] = seg_run(T, g, rg, i / 3, i % 3);
+        for (int i = tid; i < 2 * T; i += kThreads) segt[i] = seg_run(T, g, rg, i >> 1, i & 1);
         if (tid == 0) {
             const int n_sw = is_leader ? kCons - 2 : kCons;
             for (int i = 0; i < kRing; i++) {
@@ -294,8 +293,8 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 const bool ppf = prof && blockIdx.x == 0;
                 unsigned long long t0 = 0, p_wait = 0, p_issue = 0;
                 for (int s = 0; s < total; s++) {
-                    const Seg *sd = segt + 3 * (s % T);
-                    for (int sg = 0; sg < 3; sg++)
+                    const Seg *sd = segt + 2 * (s % T);
+                    for (int sg = 0; sg < 2; sg++)
                     for (int off = 0; off < sd[sg].len; off += kChunk) {
                         const int tt = sd[sg].t0 + off, nt = min(kChunk, sd[sg].len - off);
                         const uint32_t slot = seq % kRing;
@@ -317,24 +316,28 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 for (int s = 0; s < total; s++) {
                     const int kn = s % T, sl = s % kStg;
                     mbar_wait(&sh.stg_empty[sl], ((s / kStg) & 1) ^ 1);
-                    mbar_expect_tx(&sh.stg_full[sl], 2 * kTile * 4 + kPacketBytes);
+                    mbar_expect_tx(&sh.stg_full[sl], 3 * kTile * 4 + kPacketBytes);
                     bulk_g2s(sh.stg[sl][0], Ab + (size_t)(T + kn) * kTile, kTile * 4, &sh.stg_full[sl]);   // L_kn
                     bulk_g2s(sh.stg[sl][1], Ab + (size_t)kn * kTile, kTile * 4, &sh.stg_full[sl]);         // D_kn
+                    bulk_g2s(sh.stg[sl][2], Ab + (size_t)(2 * T + (kn + 2) % T) * kTile, kTile * 4,
+                             &sh.stg_full[sl]);                                                      // LL_{kn+2}
                     bulk_g2s(&sh.pk[sl], pkb + kn, kPacketBytes, &sh.stg_full[sl]);
                 }
             }
         } else if (wid >= 2) {
-            // ================= consumers: P_s = A[I_kn, J != kx] x_J  +  A[I_kn, I_kx] x_kx^old
+            // ================= consumers: P_s = sum over J != kn of A[I_kn, I_J] x_J (old x for the
+            // blocks being solved: the solver adds their increments)
             // warps 2,3,5,6,7 (none on the solver's sub-partition 0).  In the leader, consumer 4
-            // computes the staged L product (old x; the solver adds the increment of the block
-            // it is solving) and consumer 3 the in-block D product; the stream tiles go to the
-            // others.  Every warp sends its 32 partial row sums to the leader with st.async.
+            // computes L_kn x_kx^old (+ LL_kn x_{kn-2}^old, computed one step early as LL_{kn+1} x_kx^old)
+            // and consumer 3 the in-block D product; the stream tiles (SegIter) go to the others.
+            // Every warp sends its 32 partial row sums to the leader with st.async.
             const int c = (wid < 4) ? wid - 2 : wid - 3;
             const int rq = lane & 7, cq = lane >> 3;
             const int n_sw = is_leader ? kCons - 2 : kCons;   // warps taking stream tiles
             const bool do_L = is_leader && c == kCons - 1, do_D = is_leader && c == kCons - 2;
             uint32_t seq = 0;
             const bool skip_dot = prof && prof[15];
+            float lcarry[4] = {0.f, 0.f, 0.f, 0.f};   // L warp: LL_{kn+1} x_kx^old for the next step
             // leader, D warp: forward x of solver step jj to the sub-group's other CTAs (st.async
             // completes 128 bytes on their x-ready barrier)
             auto push_x = [&](int jj) {
@@ -348,12 +351,11 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
             const bool pf = prof && blockIdx.x == 0 && c == 0 && lane == 0;
             unsigned long long tA = 0, cw_x = 0, cw_full = 0, c_comp = 0, c_red = 0;
             for (int s = 0; s < total; s++) {
-                const int kn = s % T, kx = (s + T - 1) % T, kl = (s + T - 2) % T;
+                const int kn = s % T, kx = (s + T - 1) % T;
                 if (pf) tA = clock64();
-                // x of solver step s-3 (every column except kl = block of step s-2).  Observing it
-                // also guarantees the solver consumed P_{s-2}, so this step's partials cannot land
-                // in the previous phase of P-ready[s&1].  At s = 2 that guarantee needs x of step 0
-                // (published only after P_0 was consumed).
+                // x of solver step s-3 (the newest any stream tile needs).  The solver publishes it
+                // only after it consumed P_{s-2}, so this step's partials cannot land in the
+                // previous phase of P-ready[s&1].  At s = 2 that guarantee needs x of step 0.
                 // Non-leader: arm x-ready for solver step s-2 first (its previous phase, step s-4,
                 // was observed by this warp at step s-1), since the waits below may target it.
                 if (!is_leader && c == 0 && lane == 0 && s >= 2) mbar_expect_tx(&sh.xr[s & 1], 128);
@@ -365,24 +367,28 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 float acc[4] = {0.f, 0.f, 0.f, 0.f};
                 if (do_L || do_D) {
                     const int b = s % kStg;
-                    if (do_L && s + 1 < total) mbar_wait(&sh.stg_full[(s + 1) % kStg], ((s + 1) / kStg) & 1);
                     mbar_wait(&sh.stg_full[b], (s / kStg) & 1);
                     // L: x_kx^old (last updated at step s-1-T); D: x_kn^old (step s-T).  With T <= 2
                     // those may be step s-2.
                     if (T <= 2 && s >= 2) mbar_wait(&sh.xr[s & 1], ((s - 2) >> 1) & 1);
-                    if (do_L) tile_dot(sh.stg[b][0], xs + 32 * kx, rq, cq, acc);
-                    else if (T >= 2) tile_dot(sh.stg[b][1], xs + 32 * kn, rq, cq, acc);
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive_local(&sh.stg_empty[b]);
-                    if (do_D && s >= 2) {
-                        // forward x of solver step s-2 to the sub-group's other CTAs
-                        if (T > 2) mbar_wait(&sh.xr[s & 1], ((s - 2) >> 1) & 1);
-                        push_x(s - 2);
+                    if (do_L) {
+                        // L_kn x_kx^old + the carried LL_kn x_{kn-2}^old; then LL_{kn+1} x_kx^old
+                        // (tile staged at step s-1) for the next step, while x_kx is still old
+#pragma unroll
+                        for (int q = 0; q < 4; q++) { acc[q] = lcarry[q]; lcarry[q] = 0.f; }
+                        tile_dot(sh.stg[b][0], xs + 32 * kx, rq, cq, acc);
+                        if (T >= 3 && s >= 1) tile_dot(sh.stg[(s - 1) % kStg][2], xs + 32 * kx, rq, cq, lcarry);
+                        __syncwarp();
+                        if (lane == 0 && s >= 1) mbar_arrive_local(&sh.stg_empty[(s - 1) % kStg]);
+                    } else {
+                        if (T >= 2) tile_dot(sh.stg[b][1], xs + 32 * kn, rq, cq, acc);
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_local(&sh.stg_empty[b]);
                     }
                 } else {
                     // chunks of this step (seg_table): the step's i-th tile goes to stream warp i mod n_sw
                     float *yw = ys + c * ystride;
-                    const Seg *sd = segt + 3 * kn;
+                    const Seg *sd = segt + 2 * kn;
                     // the lower part of row kn this warp accumulated from earlier steps' scatters
                     if ((kn & (g - 1)) == rg && cq == 0) {
                         float4 *yp = reinterpret_cast<float4 *>(yw + (kn >> lg) * 32 + 4 * rq);
@@ -391,9 +397,9 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                         *yp = make_float4(0.f, 0.f, 0.f, 0.f);
                     }
                     int first = c;   // index (within the next chunk) of this warp's first tile
-                    for (int sg = 0; sg < 3; sg++) {
+                    for (int sg = 0; sg < 2; sg++) {
                         const Seg sr = sd[sg];
-                        const float *xsrc = xs + 32 * (sg == 1 ? kn - 3 : kn - 2);   // transposed uses
+                        const float *xsrc = xs + 32 * (kn - 3);   // scatter: x_{kn-3}^new
                         for (int off = 0; off < sr.len; off += kChunk) {
                             const int nt = min(kChunk, sr.len - off);
                             const uint32_t slot = seq % kRing;
@@ -404,12 +410,9 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                                 const int J = sr.j0 + g * (off + t);
                                 const float *tile = sh.ring[slot][t];
                                 if (sg == 0) {
-                                    // the tile of column kl (kn <= 1 only) needs x of solver step s-2
-                                    if (J == kl && s >= 2) mbar_wait(&sh.xr[s & 1], ((s - 2) >> 1) & 1);
                                     tile_dot(tile, xs + 32 * J, rq, cq, acc);
                                     continue;
                                 }
-                                if (sg == 2) mbar_wait(&sh.xr[s & 1], ((s - 2) >> 1) & 1);   // x_{kn-2}: step s-2
                                 float y4[4] = {0.f, 0.f, 0.f, 0.f};
                                 tile_tdot(tile, xsrc, rq, cq, y4);
                                 if (J == kn) {
@@ -446,6 +449,12 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 if (cq == 0)
                     st_async_v4(mapa(smem_u32(&sh.pr[s & 1][rg][c][4 * rq]), leader),
                                 make_float4(acc[0], acc[1], acc[2], acc[3]), mapa(smem_u32(&sh.pready[s & 1]), leader));
+                if (do_D && s >= 2) {
+                    // forward x of solver step s-2 to the sub-group's other CTAs (they need it from
+                    // their step s+1 on); after this step's partial so P_s never waits for it
+                    if (T > 2) mbar_wait(&sh.xr[s & 1], ((s - 2) >> 1) & 1);
+                    push_x(s - 2);
+                }
                 if (pf) { const unsigned long long t = clock64(); c_red += t - tA; tA = t; }
             }
             if (do_D) {
@@ -472,13 +481,16 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
             // ================= solver (warp 0 of the leader) =================
             // Lane l: group L = l & 7 (rows 4L..4L+3), role = l >> 3.  Role 0 (lanes 0-7) solves
             // the current block; role 1 (lanes 8-15) executes the same instruction stream on the
-            // next block's sub-diagonal tile, accumulating A[I_{k+1}, I_k] delta_k (lres); roles
-            // 2,3 mirror role 0.  x_k^new is published (xs + x-ready) only once P_{k+1} has
-            // arrived, so the stream warps read x_k^old for their share of that product.
+            // next block's sub-diagonal tile, accumulating A[I_{k+1}, I_k] delta_k (lres, used at
+            // the next step); role 2 (lanes 16-23) on LL_{k+2} = A[I_{k+2}, I_k], accumulating
+            // A[I_{k+2}, I_k] delta_k (used two steps later); role 3 mirrors role 0.  x_k^new is
+            // published (xs + x-ready) only once P_{k+1} has arrived, so the L warp reads x_k^old.
             const int L4 = 4 * (lane & 7);
-            const bool role1 = (lane >> 3) == 1;
+            const bool role1 = (lane >> 3) == 1, role2 = (lane >> 3) == 2;
             float xprev[4] = {0.f, 0.f, 0.f, 0.f};
             float lres[4] = {0.f, 0.f, 0.f, 0.f};
+            float ll0[4] = {0.f, 0.f, 0.f, 0.f}, ll1[4] = {0.f, 0.f, 0.f, 0.f};   // LL increments by step parity
+            const bool use_ll = T >= 3;
             float invd[4], xo[4], wg10, wg20, wg30, wg21, wg31, wg32;
             float bhi[4], blo[4];
             int prev_row0 = -1;
@@ -534,30 +546,38 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 const bool has_next = (j + 1 < total);
                 if (pf) tA = clock64();
                 const float *Dt = sh.stg[sl][1];
-                // role 1 streams the next block's L tile; with no next step it re-reads Dt (unused)
-                const float *tp = (role1 && has_next) ? sh.stg[sl1][0] : Dt;
-                // ---- critical path: P_k -> publish x_{k-1} -> residual -> recurrence
+                // role 1 streams the next block's L tile (with no next step it re-reads Dt, unused),
+                // role 2 the LL tile staged with this step
+                const float *tp = (role1 && has_next) ? sh.stg[sl1][0] : (role2 ? sh.stg[sl][2] : Dt);
+                // ---- critical path: P_k -> residual -> publish x_{k-1} -> recurrence
                 mbar_wait(&sh.pready[b], (j >> 1) & 1);
                 if (pf) { const unsigned long long t = clock64(); w_p += t - tA; tA = t; }
-                if (prev_row0 >= 0) publish(j - 1, prev_row0);
-                if (pf) { const unsigned long long t = clock64(); c_pub += t - tA; tA = t; }
                 float ac[4];
                 {
-                    float a[4] = {lres[0], lres[1], lres[2], lres[3]};
-                    for (int q = 0; q < g; q++) {
-#pragma unroll
-                        for (int w = 0; w < kCons; w++) {
-                            const float4 v = *reinterpret_cast<const float4 *>(&sh.pr[b][q][w][L4]);
-                            a[0] += v.x; a[1] += v.y; a[2] += v.z; a[3] += v.w;
-                        }
+                    // the g*kCons partials, a quarter per lane group, then summed across groups
+                    float a[4] = {0.f, 0.f, 0.f, 0.f};
+                    const float *prb = &sh.pr[b][0][0][0];
+                    for (int idx = lane >> 3; idx < g * kCons; idx += 4) {
+                        const float4 v = *reinterpret_cast<const float4 *>(prb + idx * 32 + L4);
+                        a[0] += v.x; a[1] += v.y; a[2] += v.z; a[3] += v.w;
                     }
 #pragma unroll
                     for (int i = 0; i < 4; i++) {
+                        a[i] += __shfl_xor_sync(0xffffffffu, a[i], 8);
+                        a[i] += __shfl_xor_sync(0xffffffffu, a[i], 16);
+                        a[i] += lres[i];
+                        if (use_ll) a[i] += (j & 1) ? ll1[i] : ll0[i];
                         const float r = (a[i] - bhi[i]) - blo[i];   // residual against b~ = bhi + blo
-                        ac[i] = role1 ? 0.f : r;
+                        ac[i] = (role1 || role2) ? 0.f : r;
                     }
                 }
-                if (has_next) fetch_next(j + 1);   // slot j+1 is complete: the P_j producer waited on it
+                // partials of P_j are consumed: x of step j-1 may now release the stream warps
+                if (prev_row0 >= 0) publish(j - 1, prev_row0);
+                if (pf) { const unsigned long long t = clock64(); c_pub += t - tA; tA = t; }
+                if (has_next) {
+                    mbar_wait(&sh.stg_full[sl1], ((j + 1) / kStg) & 1);
+                    fetch_next(j + 1);
+                }
                 if (pf) { const unsigned long long t = clock64(); c_set += t - tA; tA = t; }
 #pragma unroll
                 for (int G = 0; G < 8; G++) {
@@ -593,10 +613,14 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                     }
                 }
                 if (pf) { asm volatile("" ::"f"(xo[3])); const unsigned long long t = clock64(); c_rec += t - tA; tA = t; }
-                // role-1 accumulators (lanes 8-15) -> lres of lanes 0-7
+                // role-1 accumulators (lanes 8-15) -> lres; role-2 (lanes 16-23) -> LL increment of
+                // step j+2 (same parity slot as this step's, already consumed)
 #pragma unroll
                 for (int i = 0; i < 4; i++) {
                     lres[i] = __shfl_sync(0xffffffffu, ac[i], (lane & 7) + 8);
+                    const float v = __shfl_sync(0xffffffffu, ac[i], (lane & 7) + 16);
+                    if (j & 1) ll1[i] = v;
+                    else ll0[i] = v;
                     xprev[i] = xo[i];
                 }
                 prev_row0 = row0;
@@ -703,7 +727,7 @@ int launch_tile_convert(int to_sym, int n, int sp, int g, const float *src, floa
 }
 
 size_t gs_smem_bytes(int max_sp, int ystride) {
-    return sizeof(GsSmem) + (size_t)max_sp * 4 + (size_t)kCons * ystride * 4 + sizeof(Seg) * 3 * (size_t)(max_sp / 32);
+    return sizeof(GsSmem) + (size_t)max_sp * 4 + (size_t)kCons * ystride * 4 + sizeof(Seg) * 2 * (size_t)(max_sp / 32);
 }
 
 // floats of y per stream warp: 32 per owned column block (ceil(T/g))
@@ -766,9 +790,9 @@ int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_s
         cudaStreamSynchronize(st);
         const double n = h[9] ? (double)h[9] : 1.0;
         fprintf(stderr,
-                "[gs-prof] steps=%llu grid=%d | solver cyc/step: wait_P %.0f wait_stg %.0f publish %.0f resid %.0f recur %.0f post %.0f prep %.0f"
+                "[gs-prof] steps=%llu grid=%d | solver cyc/step: wait_P %.0f wait_stg %.0f sum+publish %.0f fetch %.0f recur %.0f post %.0f prep %.0f"
                 " | consumer0: wait_x %.0f wait_tile %.0f compute %.0f reduce+send %.0f\n",
-                h[9], n_clusters * kCl, h[0] / n, h[1] / n, h[10] / n, (h[2] - h[10]) / n, h[3] / n, h[11] / n,
+                h[9], n_clusters * kCl, h[0] / n, h[1] / n, h[10] / n, h[2] / n, h[3] / n, h[11] / n,
                 (h[4] - h[11]) / n, h[5] / n, h[6] / n, h[7] / n, h[8] / n);
         fprintf(stderr, "[gs-prof] producer: chunks=%llu (%.1f/step) wait_empty %.0f issue %.0f cyc/chunk\n", h[14],
                 h[14] / n, h[14] ? (double)h[12] / h[14] : 0.0, h[14] ? (double)h[13] / h[14] : 0.0);

@@ -249,7 +249,7 @@ psf_tc_kernel(int M, int kp, const int4 *__restrict__ tiles, const BinLayout *__
                 v[c] = (float)(sq * ri * rsc[L.r_off + j0 + c] * inv_m2);
             }
             // direct (i, j0..j0+7): coalesced over lanes; mirror (j0..j0+7, i): two float4 per lane
-            int td[2], tm[2];
+            int td[3], tm[3];
             const int nd = sym_targets(T, L.g, i >> 5, j0 >> 5, td);
             const int nm = sym_targets(T, L.g, j0 >> 5, i >> 5, tm);
             for (int u = 0; u < nd; u++) {
