@@ -205,25 +205,22 @@ __device__ __forceinline__ void tile_dot(const float *__restrict__ tile, const f
     }
 }
 
-// Consumer, transposed tile: acc[q] (output 4*rq+q = tile column) += sum over the tile rows r
-// of lane (rq, cq)'s 4-row chunks b = (rq + cq + 4i) mod 8 of tile[4rq+q][r] * x[r] (rotation
-// keeps each quarter-warp on 8 distinct 16-byte bank groups); the reduction over cq is the
-// same as tile_dot's.
-__device__ __forceinline__ void tile_tdot(const float *__restrict__ tile, const float *__restrict__ xcol, int rq,
-                                          int cq, float acc[4]) {
+// Consumer, transposed tile: returns, in lane o, (U^T x)[o] = sum_r tile[o][r] x[r] -- the whole
+// column o of the column-major tile, read as 8 float4 in the lane-rotated order (k + o) mod 8 so
+// every quarter-warp touches 8 distinct 16-byte bank groups (x likewise).  No cross-lane reduction.
+__device__ __forceinline__ float tile_tdot(const float *__restrict__ tile, const float *__restrict__ x, int lane) {
+    float t = 0.f;
 #pragma unroll
-    for (int i = 0; i < 2; i++) {
-        const int r0 = 4 * ((rq + cq + 4 * i) & 7);
-        const float4 xv = *reinterpret_cast<const float4 *>(xcol + r0);
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-            const float4 v = *reinterpret_cast<const float4 *>(tile + (4 * rq + q) * 32 + r0);
-            acc[q] = fmaf(v.x, xv.x, acc[q]);
-            acc[q] = fmaf(v.y, xv.y, acc[q]);
-            acc[q] = fmaf(v.z, xv.z, acc[q]);
-            acc[q] = fmaf(v.w, xv.w, acc[q]);
-        }
+    for (int k = 0; k < 8; k++) {
+        const int r0 = 4 * ((k + lane) & 7);
+        const float4 v = *reinterpret_cast<const float4 *>(tile + lane * 32 + r0);
+        const float4 xv = *reinterpret_cast<const float4 *>(x + r0);
+        t = fmaf(v.x, xv.x, t);
+        t = fmaf(v.y, xv.y, t);
+        t = fmaf(v.z, xv.z, t);
+        t = fmaf(v.w, xv.w, t);
     }
+    return t;
 }
 
 // Stream step s computes P for block kn = s mod T excluding kx = (s-1) mod T.  Stream tiles
@@ -292,8 +289,8 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 uint32_t seq = 0;
                 const bool ppf = prof && blockIdx.x == 0;
                 unsigned long long t0 = 0, p_wait = 0, p_issue = 0;
-                for (int s = 0; s < total; s++) {
-                    const Seg *sd = segt + 2 * (s % T);
+                for (int s = 0, kn = 0; s < total; s++, kn = (kn + 1 == T) ? 0 : kn + 1) {
+                    const Seg *sd = segt + 2 * kn;
                     for (int sg = 0; sg < 2; sg++)
                     for (int off = 0; off < sd[sg].len; off += kChunk) {
                         const int tt = sd[sg].t0 + off, nt = min(kChunk, sd[sg].len - off);
@@ -313,13 +310,14 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
             // ================= staging producer (leader, one lane): L = (kn,kx), D = (kn,kn)
             // (warp 4 shares the solver's SM sub-partition; it is mostly asleep in try_wait)
             if (is_leader && lane == 0) {
-                for (int s = 0; s < total; s++) {
-                    const int kn = s % T, sl = s % kStg;
+                for (int s = 0, kn = 0, sl = 0; s < total;
+                     s++, kn = (kn + 1 == T) ? 0 : kn + 1, sl = (sl + 1 == kStg) ? 0 : sl + 1) {
+                    const int kn2 = (kn + 2 >= T) ? kn + 2 - T : kn + 2;   // (mod T again for T < 2)
                     mbar_wait(&sh.stg_empty[sl], ((s / kStg) & 1) ^ 1);
                     mbar_expect_tx(&sh.stg_full[sl], 3 * kTile * 4 + kPacketBytes);
                     bulk_g2s(sh.stg[sl][0], Ab + (size_t)(T + kn) * kTile, kTile * 4, &sh.stg_full[sl]);   // L_kn
                     bulk_g2s(sh.stg[sl][1], Ab + (size_t)kn * kTile, kTile * 4, &sh.stg_full[sl]);         // D_kn
-                    bulk_g2s(sh.stg[sl][2], Ab + (size_t)(2 * T + (kn + 2) % T) * kTile, kTile * 4,
+                    bulk_g2s(sh.stg[sl][2], Ab + (size_t)(2 * T + kn2 % T) * kTile, kTile * 4,
                              &sh.stg_full[sl]);                                                      // LL_{kn+2}
                     bulk_g2s(&sh.pk[sl], pkb + kn, kPacketBytes, &sh.stg_full[sl]);
                 }
@@ -350,8 +348,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
             };
             const bool pf = prof && blockIdx.x == 0 && c == 0 && lane == 0;
             unsigned long long tA = 0, cw_x = 0, cw_full = 0, c_comp = 0, c_red = 0;
-            for (int s = 0; s < total; s++) {
-                const int kn = s % T, kx = (s + T - 1) % T;
+            for (int s = 0, kn = 0, kx = T - 1; s < total; s++, kx = kn, kn = (kn + 1 == T) ? 0 : kn + 1) {
                 if (pf) tA = clock64();
                 // x of solver step s-3 (the newest any stream tile needs).  The solver publishes it
                 // only after it consumed P_{s-2}, so this step's partials cannot land in the
@@ -365,6 +362,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 if (is_leader && c == 0 && lane == 0) mbar_expect_tx(&sh.pready[s & 1], (uint32_t)(g * kCons * 128));
                 if (pf) { const unsigned long long t = clock64(); cw_x += t - tA; tA = t; }
                 float acc[4] = {0.f, 0.f, 0.f, 0.f};
+                float acc_t = 0.f;   // row `lane` of P_kn from transposed tiles and y
                 if (do_L || do_D) {
                     const int b = s % kStg;
                     mbar_wait(&sh.stg_full[b], (s / kStg) & 1);
@@ -390,16 +388,15 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                     float *yw = ys + c * ystride;
                     const Seg *sd = segt + 2 * kn;
                     // the lower part of row kn this warp accumulated from earlier steps' scatters
-                    if ((kn & (g - 1)) == rg && cq == 0) {
-                        float4 *yp = reinterpret_cast<float4 *>(yw + (kn >> lg) * 32 + 4 * rq);
-                        const float4 o = *yp;
-                        acc[0] += o.x; acc[1] += o.y; acc[2] += o.z; acc[3] += o.w;
-                        *yp = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if ((kn & (g - 1)) == rg) {
+                        float *yp = yw + (kn >> lg) * 32 + lane;
+                        acc_t += *yp;
+                        *yp = 0.f;
                     }
+                    const float *x3 = xs + 32 * (kn - 3);   // scatter: x_{kn-3}^new
                     int first = c;   // index (within the next chunk) of this warp's first tile
                     for (int sg = 0; sg < 2; sg++) {
                         const Seg sr = sd[sg];
-                        const float *xsrc = xs + 32 * (kn - 3);   // scatter: x_{kn-3}^new
                         for (int off = 0; off < sr.len; off += kChunk) {
                             const int nt = min(kChunk, sr.len - off);
                             const uint32_t slot = seq % kRing;
@@ -411,24 +408,12 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                                 const float *tile = sh.ring[slot][t];
                                 if (sg == 0) {
                                     tile_dot(tile, xs + 32 * J, rq, cq, acc);
-                                    continue;
-                                }
-                                float y4[4] = {0.f, 0.f, 0.f, 0.f};
-                                tile_tdot(tile, xsrc, rq, cq, y4);
-                                if (J == kn) {
-#pragma unroll
-                                    for (int q = 0; q < 4; q++) acc[q] += y4[q];
                                 } else {
-#pragma unroll
-                                    for (int q = 0; q < 4; q++) {
-                                        y4[q] += __shfl_xor_sync(0xffffffffu, y4[q], 8);
-                                        y4[q] += __shfl_xor_sync(0xffffffffu, y4[q], 16);
-                                    }
-                                    if (cq == 0) {
-                                        float4 *yp = reinterpret_cast<float4 *>(yw + (J >> lg) * 32 + 4 * rq);
-                                        float4 o = *yp;
-                                        o.x += y4[0]; o.y += y4[1]; o.z += y4[2]; o.w += y4[3];
-                                        *yp = o;
+                                    const float v = tile_tdot(tile, x3, lane);
+                                    if (J == kn) {
+                                        acc_t += v;
+                                    } else {
+                                        yw[(J >> lg) * 32 + lane] += v;
                                     }
                                 }
                             }
@@ -440,11 +425,13 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                         }
                     }
                 }
-                // reduce over the 4 column groups: lanes (rq, cq) then hold rows 4rq..4rq+3
+                // reduce over the 4 column groups: lanes (rq, cq) then hold rows 4rq..4rq+3; add the
+                // per-lane (row = lane) transposed / y contributions
 #pragma unroll
                 for (int q = 0; q < 4; q++) {
                     acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], 8);
                     acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], 16);
+                    acc[q] += __shfl_sync(0xffffffffu, acc_t, 4 * rq + q);
                 }
                 if (cq == 0)
                     st_async_v4(mapa(smem_u32(&sh.pr[s & 1][rg][c][4 * rq]), leader),
@@ -527,7 +514,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
             prepare(0);
             // operands of the next block, loaded ahead of the recurrence (latency hidden)
             float n_invd[4], n_xo[4], n_wg[6], n_bhi[4], n_blo[4];
-            auto fetch_next = [&](int jj) {
+            auto fetch_next = [&](int jj, int kk) {
                 const GsPacket &P = sh.pk[jj % kStg];
                 const float4 iv = *reinterpret_cast<const float4 *>(&P.invd[L4]);
                 n_invd[0] = iv.x; n_invd[1] = iv.y; n_invd[2] = iv.z; n_invd[3] = iv.w;
@@ -538,11 +525,13 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 const float4 bl = *reinterpret_cast<const float4 *>(&P.blo[L4]);
                 n_bhi[0] = bh.x; n_bhi[1] = bh.y; n_bhi[2] = bh.z; n_bhi[3] = bh.w;
                 n_blo[0] = bl.x; n_blo[1] = bl.y; n_blo[2] = bl.z; n_blo[3] = bl.w;
-                const float4 v = *reinterpret_cast<const float4 *>(xs + 32 * (jj % T) + L4);
+                const float4 v = *reinterpret_cast<const float4 *>(xs + 32 * kk + L4);
                 n_xo[0] = v.x; n_xo[1] = v.y; n_xo[2] = v.z; n_xo[3] = v.w;
             };
-            for (int j = 0; j < total; j++) {
-                const int k = j % T, b = j & 1, row0 = 32 * k, sl = j % kStg, sl1 = (j + 1) % kStg;
+            for (int j = 0, k = 0, sl = 0; j < total;
+                 j++, k = (k + 1 == T) ? 0 : k + 1, sl = (sl + 1 == kStg) ? 0 : sl + 1) {
+                const int b = j & 1, row0 = 32 * k, sl1 = (sl + 1 == kStg) ? 0 : sl + 1;
+                const int kn1 = (k + 1 == T) ? 0 : k + 1;   // next block
                 const bool has_next = (j + 1 < total);
                 if (pf) tA = clock64();
                 const float *Dt = sh.stg[sl][1];
@@ -557,9 +546,17 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                     // the g*kCons partials, a quarter per lane group, then summed across groups
                     float a[4] = {0.f, 0.f, 0.f, 0.f};
                     const float *prb = &sh.pr[b][0][0][0];
-                    for (int idx = lane >> 3; idx < g * kCons; idx += 4) {
-                        const float4 v = *reinterpret_cast<const float4 *>(prb + idx * 32 + L4);
-                        a[0] += v.x; a[1] += v.y; a[2] += v.z; a[3] += v.w;
+                    const int np = g * kCons;
+                    float4 v[(kCl * kCons + 3) / 4];
+#pragma unroll
+                    for (int it = 0; it < (kCl * kCons + 3) / 4; it++) {   // all loads in flight at once
+                        const int idx = (lane >> 3) + 4 * it;
+                        v[it] = (idx < np) ? *reinterpret_cast<const float4 *>(prb + idx * 32 + L4)
+                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+#pragma unroll
+                    for (int it = 0; it < (kCl * kCons + 3) / 4; it++) {
+                        a[0] += v[it].x; a[1] += v[it].y; a[2] += v[it].z; a[3] += v[it].w;
                     }
 #pragma unroll
                     for (int i = 0; i < 4; i++) {
@@ -576,7 +573,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 if (pf) { const unsigned long long t = clock64(); c_pub += t - tA; tA = t; }
                 if (has_next) {
                     mbar_wait(&sh.stg_full[sl1], ((j + 1) / kStg) & 1);
-                    fetch_next(j + 1);
+                    fetch_next(j + 1, kn1);
                 }
                 if (pf) { const unsigned long long t = clock64(); c_set += t - tA; tA = t; }
 #pragma unroll
