@@ -275,7 +275,7 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
     Geo G;
     if ((s = prepare_geometry(ctx, arr, grid, n_bins, freq, G, launches, st))) return s;
     // S2 DAS on the Hermitian part of each CSM
-    if ((s = ensure(ctx, ctx->herm, sizeof(double) * 2 * (size_t)n_bins * M * M))) return s;
+    if ((s = ensure(ctx, ctx->herm, sizeof(double) * 2 * (size_t)n_bins * das_mpad(M) * das_mpad(M)))) return s;
     double *b = b_map;
     if (!b) {
         if ((s = ensure(ctx, ctx->bint, sizeof(double) * (size_t)n_bins * S))) return s;
@@ -530,7 +530,8 @@ dwc_status dwc_das(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, int
     int launches = 0;
     Geo G;
     if ((s = prepare_geometry(ctx, arr, grid, n_bins, freq_hz, G, launches, st))) return s;
-    if ((s = ensure(ctx, ctx->herm, sizeof(double) * 2 * (size_t)n_bins * arr->m * arr->m))) return s;
+    if ((s = ensure(ctx, ctx->herm, sizeof(double) * 2 * (size_t)n_bins * das_mpad(arr->m) * das_mpad(arr->m))))
+        return s;
     LAUNCH(launch_hermitize(arr->m, n_bins, csm, (double *)ctx->herm.p, st));
     LAUNCH(launch_das(G, (double *)ctx->dist.p, (double *)ctx->amp.p, n_bins, (double *)ctx->freq.p,
                       (double *)ctx->herm.p, b_map, st));

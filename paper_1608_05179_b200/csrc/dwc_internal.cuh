@@ -33,12 +33,14 @@ int launch_geom_tables(const Geo &g, double *dist, double *amp, int *flag, cudaS
 int launch_steer(const Geo &g, const double *dist, const double *amp, const double *freq,
                  int n_pts, const int32_t *idx, double *E, cudaStream_t st);
 
-// Hermitian part of the CSMs (reading R3), into H (dev, same layout).
+// Half-Hermitian part of the CSMs (reading R3), zero padded to das_mpad(M): H (dev) holds
+// n_bins * Mp * Mp complex128 (upper triangle of (C + C^H)/2, diagonal halved).
+int das_mpad(int M);
 int launch_hermitize(int M, int n_bins, const double *csm, double *H, cudaStream_t st);
 
-// S2: b[k][s] for n_bins bins; freq dev[n_bins]; csm dev.
+// S2: b[k][s] for n_bins bins; freq dev[n_bins]; csm_half = launch_hermitize's output.
 int launch_das(const Geo &g, const double *dist, const double *amp, int n_bins,
-               const double *freq, const double *csm, double *b, cudaStream_t st);
+               const double *freq, const double *csm_half, double *b, cudaStream_t st);
 
 // S3+S4: compaction of kept nodes.  flag (dev int): bit 1 set when b has a non-finite value.
 int launch_compress(int n, int n_bins, const double *b, double eps, int eps_mode, int full_grid,

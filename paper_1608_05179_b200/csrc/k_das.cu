@@ -4,14 +4,10 @@
 //   e_ms = sqrt(M) * exp(-j k d_ms) / (d_ms * ||g_s||),  ||g_s||^2 = sum_m 1/d_ms^2,
 // split into a frequency-independent amplitude table amp[m][s] = sqrt(M)/(d_ms ||g_s||)
 // and distance table dist[m][s] (both fp64, s fastest -> coalesced), computed once per
-// call, and the per-bin phase k*d_ms evaluated with fp64 sincos inside the consumers.
+// call, and the per-bin phase k*d_ms evaluated with fp64 sincospi inside the consumers.
 //
-// S2 (Eq. 2): b_s = Re(e_s^H C e_s) / M^2 in fp64, never forming E^H C E.
-// Hermitian form (reading R3): b = sum_m C_mm |e_m|^2 + 2 Re sum_{m<n} conj(e_m) C_mn e_n,
-// half the flops of the full quadratic form.  One CTA = P scan points x TSUB threads per
-// point (256 threads); the P steering columns live in shared memory ([m][p], conflict-free);
-// each thread holds an 8-column chunk of e_n in registers and streams rows m of C through
-// L1 as warp-uniform broadcast loads.  fp64 CUDA-core bound (B200 has no faster fp64 path).
+// S2 (Eq. 2): b_s = Re(e_s^H C e_s) / M^2 in fp64, never forming E^H C E
+// (das_kernel below: triangular register-blocked GEMM on the half-Hermitian CSM).
 #include <math.h>
 
 #include "dwc_internal.cuh"
@@ -49,16 +45,19 @@ int launch_geom_tables(const Geo &g, double *dist, double *amp, int *flag, cudaS
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
-__device__ __forceinline__ double2 steer_elem(double d, double a, double k) {
+// e = a exp(-j k d) with the phase in half-turns, kpi = k / pi = 2 f / c0: sincospi reduces
+// its argument exactly (subtract the nearest integer) -- cheaper than sincos' Cody-Waite
+// reduction, same ~1e-16 relative accuracy of e.
+__device__ __forceinline__ double2 steer_elem(double d, double a, double kpi) {
     double sn, cs;
-    sincos(k * d, &sn, &cs);
+    sincospi(kpi * d, &sn, &cs);
     return make_double2(a * cs, -(a * sn));
 }
 
 __global__ void steer_kernel(Geo g, const double *__restrict__ dist, const double *__restrict__ amp,
                              const double *__restrict__ freq, int n_pts,
                              const int32_t *__restrict__ idx, double2 *__restrict__ E) {
-    const double k = kTwoPi * freq[0] / g.c0;
+    const double k = 2.0 * freq[0] / g.c0;   // half-turns per metre
     const int total = n_pts * g.m;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
         const int pt = t / g.m, m = t - (t / g.m) * g.m;
@@ -78,8 +77,19 @@ int launch_steer(const Geo &g, const double *dist, const double *amp, const doub
 }
 
 // ------------------------------------------------------------------------------------
+// S2 as a register-blocked triangular complex GEMM.  With the half-Hermitian matrix
+//   Ch[m][n] = H[m][n] (n > m),  H[m][m] / 2 (n = m),  0 (n < m),   H = (C + C^H)/2,
+// b_s = 2 Re(e_s^H Ch e_s) / M^2 -- the Hermitian form at half the flops.  A CTA = P scan points
+// of one bin (P = 64, or 32 when Mp > 64); their steering vectors Es[n][p] (Mp x P complex,
+// Mp = M rounded up to 8, zero rows beyond M) in shared memory.  Warp w owns the row-group
+// pairs (q, G-1-q), q = w, w+8, ... (G = Mp/4 groups of 4 rows), paired so every warp has the
+// same triangular work, and stages those 8 rows of Ch in its own shared-memory slice.  Lane l
+// owns points l (+32).  Per n a thread reads 8 row entries (broadcast LDS.128) and e_n of its
+// points and does 8 or 16 complex MACs; W = Ch e stays in registers; the epilogue reduces
+// Re(conj(e_m) W_m) over the rows and the warps in fixed order (deterministic).  fp64 CUDA
+// cores (B200 DFMA and DMMA peak are the same, ~36 TFLOP/s measured).
 constexpr int kDasThreads = 256;
-constexpr int kNch = 8;  // n-chunk held in registers
+constexpr int kDasWarps = kDasThreads / 32;
 
 __device__ __forceinline__ void cmac(double2 &acc, double2 a, double2 b) {  // acc += a*b
     acc.x = fma(a.x, b.x, acc.x);
@@ -87,136 +97,144 @@ __device__ __forceinline__ void cmac(double2 &acc, double2 a, double2 b) {  // a
     acc.y = fma(a.x, b.y, acc.y);
     acc.y = fma(a.y, b.x, acc.y);
 }
-__device__ __forceinline__ void cjmac(double2 &acc, double2 a, double2 b) {  // acc += conj(a)*b
-    acc.x = fma(a.x, b.x, acc.x);
-    acc.x = fma(a.y, b.y, acc.x);
-    acc.y = fma(a.x, b.y, acc.y);
-    acc.y = fma(-a.y, b.x, acc.y);
-}
 
-// One chunk c of 8 columns: returns 2*Re(sum_{m<n, n in chunk} conj(e_m) C_mn e_n)
-// + sum_{n in chunk} C_nn |e_n|^2 for the thread's point.
-__device__ __forceinline__ double das_chunk(const double2 *__restrict__ C, int M, int c,
-                                            const double2 *__restrict__ Es, int P, int p) {
-    const int n0 = c * kNch;
-    double2 en[kNch];
-#pragma unroll
-    for (int j = 0; j < kNch; j++) en[j] = (n0 + j < M) ? Es[(n0 + j) * P + p] : make_double2(0.0, 0.0);
-    double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
-    const bool full = (n0 + kNch <= M);
-    // rows strictly above the chunk
+int das_mpad(int M) { return (M + 7) / 8 * 8; }
+
+template <int PPL, bool kBoth>
+__device__ __forceinline__ void das_rows(const double2 *__restrict__ Cw, const double2 *__restrict__ Es, int Mp,
+                                         int n0, int n1, int lane, double2 Wa[4][PPL], double2 Wb[4][PPL]) {
+    constexpr int P = 32 * PPL;
 #pragma unroll 2
-    for (int m = 0; m < n0; m++) {
-        const double2 em = Es[m * P + p];
-        const double2 *row = C + (size_t)m * M + n0;
-        double2 t0 = make_double2(0.0, 0.0), t1 = make_double2(0.0, 0.0);
-        if (full) {
+    for (int n = n0; n < n1; n++) {
+        double2 e[PPL];
 #pragma unroll
-            for (int j = 0; j < kNch; j += 2) {
-                cmac(t0, __ldg(row + j), en[j]);
-                cmac(t1, __ldg(row + j + 1), en[j + 1]);
+        for (int j = 0; j < PPL; j++) e[j] = Es[n * P + lane + 32 * j];
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+            const double2 c = Cw[r * Mp + n];
+#pragma unroll
+            for (int j = 0; j < PPL; j++) cmac(Wa[r][j], c, e[j]);
+        }
+        if (kBoth) {
+#pragma unroll
+            for (int r = 0; r < 4; r++) {
+                const double2 c = Cw[(4 + r) * Mp + n];
+#pragma unroll
+                for (int j = 0; j < PPL; j++) cmac(Wb[r][j], c, e[j]);
             }
-        } else {
-#pragma unroll
-            for (int j = 0; j < kNch; j++)
-                if (n0 + j < M) cmac(t0, __ldg(row + j), en[j]);
-        }
-        t0.x += t1.x;
-        t0.y += t1.y;
-        if (m & 1) cjmac(acc1, em, t0); else cjmac(acc0, em, t0);
-    }
-    // pairs inside the chunk (a < b) and the diagonal
-    double diag = 0.0;
-#pragma unroll
-    for (int a = 0; a < kNch; a++) {
-        if (n0 + a < M) {
-            const double2 *row = C + (size_t)(n0 + a) * M + n0;
-            const double2 caa = __ldg(row + a);
-            diag = fma(caa.x, en[a].x * en[a].x + en[a].y * en[a].y, diag);
-            double2 t = make_double2(0.0, 0.0);
-#pragma unroll
-            for (int b = a + 1; b < kNch; b++)
-                if (n0 + b < M) cmac(t, __ldg(row + b), en[b]);
-            cjmac(acc0, en[a], t);
         }
     }
-    return 2.0 * (acc0.x + acc1.x) + diag;
 }
 
-__global__ void __launch_bounds__(kDasThreads)
+template <int PPL>
+__global__ void __launch_bounds__(kDasThreads, 1)
 das_kernel(Geo g, const double *__restrict__ dist, const double *__restrict__ amp,
-           const double *__restrict__ freq, const double2 *__restrict__ csm,
-           double *__restrict__ b, int P) {
-    extern __shared__ double2 Es[];  // [M][P]
-    __shared__ double part[kDasThreads];
+           const double *__restrict__ freq, const double2 *__restrict__ Ch, int Mp, double *__restrict__ b) {
+    constexpr int P = 32 * PPL;
+    extern __shared__ double2 smem_d2[];
+    double2 *Es = smem_d2;                       // [Mp][P]
+    double2 *Cw = smem_d2 + (size_t)Mp * P;      // [warp][8 rows][Mp]
+    __shared__ double part[kDasWarps][P];
     const int M = g.m;
     const int bin = blockIdx.y;
     const int s0 = blockIdx.x * P;
-    const double k = kTwoPi * freq[bin] / g.c0;
-    for (int t = threadIdx.x; t < M * P; t += kDasThreads) {
-        const int m = t / P, p = t - (t / P) * P;
+    const double k = 2.0 * freq[bin] / g.c0;   // half-turns per metre
+    for (int t = threadIdx.x; t < Mp * P; t += kDasThreads) {
+        const int m = t / P, p = t % P;
         const int s = s0 + p;
-        double2 e = make_double2(0.0, 0.0);
-        if (s < g.S) e = steer_elem(dist[(size_t)m * g.S + s], amp[(size_t)m * g.S + s], k);
-        Es[t] = e;
+        Es[t] = (m < M && s < g.S) ? steer_elem(dist[(size_t)m * g.S + s], amp[(size_t)m * g.S + s], k)
+                                   : make_double2(0.0, 0.0);
     }
     __syncthreads();
-    const int p = threadIdx.x % P, sub = threadIdx.x / P, tsub = kDasThreads / P;
-    const double2 *C = csm + (size_t)bin * M * M;
-    const int NC = (M + kNch - 1) / kNch;
-    double acc = 0.0;
-    for (int q = sub; q < (NC + 1) / 2; q += tsub) {
-        acc += das_chunk(C, M, q, Es, P, p);
-        if (NC - 1 - q != q) acc += das_chunk(C, M, NC - 1 - q, Es, P, p);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int G = Mp / 4;
+    const double2 *C = Ch + (size_t)bin * Mp * Mp;
+    double2 *cw = Cw + (size_t)w * 8 * Mp;
+    double acc[PPL];
+#pragma unroll
+    for (int j = 0; j < PPL; j++) acc[j] = 0.0;
+    for (int qa = w; qa < G / 2; qa += kDasWarps) {
+        const int qb = G - 1 - qa;
+        __syncwarp();
+        for (int t = lane; t < 8 * Mp; t += 32) {   // rows 4qa..4qa+3, 4qb..4qb+3 of Ch
+            const int r = t / Mp, n = t - (t / Mp) * Mp;
+            const int m = (r < 4) ? 4 * qa + r : 4 * qb + r - 4;
+            cw[t] = __ldg(C + (size_t)m * Mp + n);
+        }
+        __syncwarp();
+        double2 Wa[4][PPL], Wb[4][PPL];
+#pragma unroll
+        for (int r = 0; r < 4; r++)
+#pragma unroll
+            for (int j = 0; j < PPL; j++) Wa[r][j] = Wb[r][j] = make_double2(0.0, 0.0);
+        das_rows<PPL, false>(cw, Es, Mp, 4 * qa, 4 * qb, lane, Wa, Wb);   // only rows of qa reach n < 4 qb
+        das_rows<PPL, true>(cw, Es, Mp, 4 * qb, Mp, lane, Wa, Wb);
+#pragma unroll
+        for (int r = 0; r < 4; r++)
+#pragma unroll
+            for (int j = 0; j < PPL; j++) {
+                const double2 ea = Es[(4 * qa + r) * P + lane + 32 * j], eb = Es[(4 * qb + r) * P + lane + 32 * j];
+                acc[j] += ea.x * Wa[r][j].x + ea.y * Wa[r][j].y + eb.x * Wb[r][j].x + eb.y * Wb[r][j].y;
+            }
     }
-    part[threadIdx.x] = acc;
+#pragma unroll
+    for (int j = 0; j < PPL; j++) part[w][lane + 32 * j] = acc[j];
     __syncthreads();
-    if (sub == 0 && s0 + p < g.S) {
-        double v = part[p];
-        for (int j = 1; j < tsub; j++) v += part[j * P + p];
-        b[(size_t)bin * g.S + s0 + p] = v / ((double)M * (double)M);
+    if (threadIdx.x < P && s0 + (int)threadIdx.x < g.S) {
+        double v = 0.0;
+#pragma unroll
+        for (int q = 0; q < kDasWarps; q++) v += part[q][threadIdx.x];
+        b[(size_t)bin * g.S + s0 + threadIdx.x] = 2.0 * v / ((double)M * (double)M);
     }
 }
 
-// Hermitian part H = (C + C^H)/2 of every bin's CSM (reading R3).  For an exactly
-// Hermitian input this is the identity bit for bit.
-__global__ void hermitize_kernel(int M, long total, const double2 *__restrict__ C,
-                                 double2 *__restrict__ H) {
+// Half-Hermitian, zero-padded CSM Ch (Mp x Mp per bin) from the input C (reading R3: only the
+// Hermitian part H = (C + C^H)/2 enters Re(e^H C e)).
+__global__ void hermitize_kernel(int M, int Mp, long total, const double2 *__restrict__ C,
+                                 double2 *__restrict__ Ch) {
     for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total; t += (long)gridDim.x * blockDim.x) {
-        const long bin = t / ((long)M * M);
-        const int r = (int)(t - bin * M * M);
-        const int i = r / M, j = r - (r / M) * M;
-        const double2 a = C[t];
-        const double2 b = C[bin * M * M + (long)j * M + i];
-        H[t] = make_double2((a.x + b.x) * 0.5, (a.y - b.y) * 0.5);
+        const long bin = t / ((long)Mp * Mp);
+        const int r = (int)(t - bin * Mp * Mp);
+        const int i = r / Mp, j = r - (r / Mp) * Mp;
+        double2 v = make_double2(0.0, 0.0);
+        if (i < M && j < M && j >= i) {
+            const double2 a = C[bin * M * M + (long)i * M + j];
+            const double2 c = C[bin * M * M + (long)j * M + i];
+            v = make_double2((a.x + c.x) * 0.5, (a.y - c.y) * 0.5);
+            if (j == i) v = make_double2(v.x * 0.5, 0.0);
+        }
+        Ch[t] = v;
     }
 }
 
 int launch_hermitize(int M, int n_bins, const double *csm, double *H, cudaStream_t st) {
-    long total = (long)n_bins * M * M;
+    const int Mp = das_mpad(M);
+    long total = (long)n_bins * Mp * Mp;
     int blocks = (int)((total + 255) / 256);
     if (blocks > 148 * 16) blocks = 148 * 16;
-    hermitize_kernel<<<blocks, 256, 0, st>>>(M, total, (const double2 *)csm, (double2 *)H);
+    hermitize_kernel<<<blocks, 256, 0, st>>>(M, Mp, total, (const double2 *)csm, (double2 *)H);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
-int das_points_per_cta(int M) {
-    int P = 128;
-    while (P > 16 && P * M > 4096) P >>= 1;
-    return P;
-}
-
 int launch_das(const Geo &g, const double *dist, const double *amp, int n_bins,
-               const double *freq, const double *csm, double *b, cudaStream_t st) {
-    const int P = das_points_per_cta(g.m);
-    const size_t smem = (size_t)16 * g.m * P;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(das_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-        attr_set = true;
+               const double *freq, const double *csm_half, double *b, cudaStream_t st) {
+    const int Mp = das_mpad(g.m);
+    const int P = (Mp <= 64) ? 64 : 32;
+    const size_t smem = (size_t)16 * Mp * (P + 8 * kDasWarps);
+    if (smem > 220 * 1024) return -1;
+    static size_t attr2 = 0, attr1 = 0;
+    size_t &attr = (P == 64) ? attr2 : attr1;
+    if (smem > attr) {
+        const cudaError_t e = (P == 64) ? cudaFuncSetAttribute(das_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                                        : cudaFuncSetAttribute(das_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return -1;
+        attr = smem;
     }
     dim3 grid((g.S + P - 1) / P, n_bins);
-    das_kernel<<<grid, kDasThreads, smem, st>>>(g, dist, amp, freq, (const double2 *)csm, b, P);
+    if (P == 64)
+        das_kernel<2><<<grid, kDasThreads, smem, st>>>(g, dist, amp, freq, (const double2 *)csm_half, Mp, b);
+    else
+        das_kernel<1><<<grid, kDasThreads, smem, st>>>(g, dist, amp, freq, (const double2 *)csm_half, Mp, b);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

@@ -21,7 +21,7 @@
 // equal and only output tiles touching the upper triangle are computed (the rest mirrored).
 //
 // Kernels
-//  psf_slice_kernel  one warp per kept node: fp64 steering (sincos of k d, amplitude table),
+//  psf_slice_kernel  one warp per kept node: fp64 steering (sincospi of k d / pi, amplitude table),
 //                    power-of-two row scale, int8 digits of X and Z written directly in the
 //                    tensor-core operand layout; b~ = b[keep] (S6, fp64).
 //  psf_tc_kernel     one CTA per 128 x 64 output tile (bin, I, J): warp 0 streams the K steps
@@ -103,11 +103,11 @@ psf_slice_kernel(Geo g, const double *__restrict__ dist, const double *__restric
         int e;
         const double f = frexp(amax, &e);         // amax = f 2^e, f in [0.5, 1)
         const int q = (f > 127.0 / 128.0) ? -e - 1 : -e;  // |v| 2^q <= 127/128
-        const double k = kTwoPi * freq[bin] / g.c0;
+        const double kpi = 2.0 * freq[bin] / g.c0;   // k / pi: phase in half-turns
         for (int m = lane; m < M; m += 32) {
             const double d = dist[(size_t)m * g.S + s], a = amp[(size_t)m * g.S + s];
             double sn, cs;
-            sincos(k * d, &sn, &cs);
+            sincospi(kpi * d, &sn, &cs);
             int dr[kSl], di[kSl];
             digits(ldexp(a * cs, q), dr);
             digits(ldexp(-(a * sn), q), di);
