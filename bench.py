@@ -155,6 +155,7 @@ def run_ours(args, cfg):
     import torch.distributed as dist
 
     from paper_1608_05179_b200 import Context, Geometry
+    from paper_1608_05179_b200.band_parallel import gather_band, shard_bins
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -169,7 +170,7 @@ def run_ours(args, cfg):
     if args.scaling == "weak" or world == 1:
         band = synth.make_band(cfg, seed=rank)
     else:
-        band = synth.make_band(cfg, bins=list(range(rank, cfg.n_bins, world)))
+        band = synth.make_band(cfg, bins=shard_bins(cfg.n_bins, rank, world))
     K = len(band.freqs)
     geom = Geometry(band.mic_xyz, cfg.n, cfg.side_len, cfg.z0, cfg.c0, cfg.cx, cfg.cy)
     csm_dev = torch.from_numpy(band.csm).to(dev)
@@ -178,18 +179,15 @@ def run_ours(args, cfg):
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     S = cfg.S
-    kmax = math.ceil(cfg.n_bins / world)
-    gather_x = None
-    if args.scaling == "strong" and world > 1:
-        gather_x = torch.empty((world, kmax, S), dtype=torch.float32, device=dev)
-        pad_x = torch.zeros((kmax, S), dtype=torch.float32, device=dev)
+    strong = args.scaling == "strong" and world > 1
 
     def step():
         out = ctx.solve_band(geom, band.freqs, csm_dev, cfg.epsilon, cfg.sweeps, cfg.eps_mode,
                              full_grid=cfg.full_grid, stream=stream)
-        if gather_x is not None:
-            pad_x[:K].copy_(out["x_map"])
-            dist.all_gather_into_tensor(gather_x, pad_x)
+        if strong:
+            # the one collective: maps + keep bitmasks + counts, all ranks
+            mask = ctx.keep_mask(out["n_keep"], out["keep_idx"], stream=stream)
+            out["gathered"] = gather_band(out["x_map"], out["n_keep"], mask, cfg.n_bins)
         return out
 
     for _ in range(args.warmup):

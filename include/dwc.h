@@ -142,9 +142,25 @@ DWC_API dwc_status dwc_psf(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *g
                    int32_t n_keep, const int32_t *keep_idx, float *A, void *cuda_stream);
 
 /* S7: `sweeps` forward projected Gauss-Seidel sweeps from x0 = 0 on one system.
- * A dev float[n*n] row-major (A_ii > 0), b dev double[n], x dev float[n] (out). */
+ * A dev float[n*n] row-major, symmetric (as A~ is, reading R1) with A_ii > 0: only the upper
+ * triangle (j >= i) is read, the lower one is taken as its transpose.
+ * b dev double[n], x dev float[n] (out). */
 DWC_API dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int32_t sweeps,
                   float *x, void *cuda_stream);
+
+/* ---- multi-GPU gather helpers --------------------------------------- */
+
+/* Keep set -> bitmask: for each of n_bins bins, mask holds W = ceil(S/32) uint32 words; bit
+ * (s % 32) of word s/32 is set iff node s is in the bin's keep list.  n_keep dev int32[n_bins],
+ * keep_idx dev int32[n_bins*S] ascending (as dwc_solve_band writes it), mask dev
+ * uint32[n_bins*W] (out).  The bitmask is what the ranks all-gather (S/8 bytes per bin
+ * instead of 4 S).  Errors: DWC_EINVAL (S < 1, n_bins < 0, NULL), DWC_ECUDA. */
+DWC_API dwc_status dwc_keep_mask(dwc_ctx *ctx, int32_t n_bins, int32_t S, const int32_t *n_keep,
+                                 const int32_t *keep_idx, uint32_t *mask, void *cuda_stream);
+
+/* Bitmask -> keep set: the inverse of dwc_keep_mask (ascending list, -1 padded to S). */
+DWC_API dwc_status dwc_keep_unmask(dwc_ctx *ctx, int32_t n_bins, int32_t S, const uint32_t *mask,
+                                   int32_t *n_keep, int32_t *keep_idx, void *cuda_stream);
 
 /* ---- diagnostics ------------------------------------------------------------------ */
 
@@ -155,7 +171,8 @@ typedef struct {
     int32_t n_bins;
     int64_t sum_keep;         /* sum_k S~_k */
     double sum_keep_sq;       /* sum_k S~_k^2 */
-    double gs_bytes;          /* sum_k sweeps * bytes of A~_k as streamed by the GS kernel */
+    double gs_bytes;          /* sum_k sweeps * 2 S~_k (S~_k + 1): the symmetric-packed fp32 A~_k
+                                 once per sweep (algorithmic bytes of the GS stream) */
     double psf_flops;         /* real flops of the PSF Gram (8*M*S~^2 per bin, full square) */
     double das_flops;         /* real flops of the DAS quadratic forms (8*M^2*S per bin) */
     int32_t launches;         /* kernels launched by the call */

@@ -23,6 +23,7 @@ SOURCES = {
     "k_compress.cu": ["--fmad=false"],   # the fp64 threshold arithmetic must not contract
     "k_psf.cu": [],
     "k_gs.cu": [],
+    "k_keep.cu": [],
 }
 
 

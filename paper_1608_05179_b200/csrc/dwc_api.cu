@@ -625,4 +625,28 @@ dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int3
     return DWC_OK;
 }
 
+dwc_status dwc_keep_mask(dwc_ctx *ctx, int32_t n_bins, int32_t S, const int32_t *n_keep, const int32_t *keep_idx,
+                         uint32_t *mask, void *cuda_stream) {
+    dwc_status s;
+    if ((s = check_ctx(ctx))) return s;
+    if (S < 1 || n_bins < 0) return fail(DWC_EINVAL, "S = %d, n_bins = %d", S, n_bins);
+    if (n_bins == 0) return DWC_OK;
+    if (!n_keep || !keep_idx || !mask) return fail(DWC_EINVAL, "NULL device buffer");
+    int launches = 0;
+    LAUNCH(launch_keep_mask(n_bins, S, n_keep, keep_idx, mask, (cudaStream_t)cuda_stream));
+    return DWC_OK;
+}
+
+dwc_status dwc_keep_unmask(dwc_ctx *ctx, int32_t n_bins, int32_t S, const uint32_t *mask, int32_t *n_keep,
+                           int32_t *keep_idx, void *cuda_stream) {
+    dwc_status s;
+    if ((s = check_ctx(ctx))) return s;
+    if (S < 1 || n_bins < 0) return fail(DWC_EINVAL, "S = %d, n_bins = %d", S, n_bins);
+    if (n_bins == 0) return DWC_OK;
+    if (!n_keep || !keep_idx || !mask) return fail(DWC_EINVAL, "NULL device buffer");
+    int launches = 0;
+    LAUNCH(launch_keep_unmask(n_bins, S, mask, n_keep, keep_idx, (cudaStream_t)cuda_stream));
+    return DWC_OK;
+}
+
 }  // extern "C"

@@ -131,4 +131,10 @@ int gs_packet_bytes();
 int launch_gs_prep(int n_bins, int max_sp, const BinLayout *lay_dev, const float *A, const double *bt,
                    void *packets, cudaStream_t st);
 
+// Keep-set bitmasks (k_keep.cu): ceil(S/32) uint32 words per bin.
+int launch_keep_mask(int n_bins, int S, const int32_t *n_keep, const int32_t *keep_idx, uint32_t *mask,
+                     cudaStream_t st);
+int launch_keep_unmask(int n_bins, int S, const uint32_t *mask, int32_t *n_keep, int32_t *keep_idx,
+                       cudaStream_t st);
+
 }  // namespace dwc

@@ -70,6 +70,8 @@ def lib() -> C.CDLL:
         L.dwc_compress.argtypes = [P, gp, pp, i32, P, P, P, P, P]
         L.dwc_psf.argtypes = [P, ap, gp, d, i32, P, P, P]
         L.dwc_gs.argtypes = [P, i32, P, P, i32, P, P]
+        L.dwc_keep_mask.argtypes = [P, i32, i32, P, P, P, P]
+        L.dwc_keep_unmask.argtypes = [P, i32, i32, P, P, P, P]
         L.dwc_set_timing.argtypes = [P, C.c_int]
         L.dwc_get_stats.argtypes = [P, C.POINTER(Stats)]
         L.dwc_last_error.restype = C.c_char_p
@@ -77,7 +79,8 @@ def lib() -> C.CDLL:
         L.dwc_workspace_bytes.argtypes = [P]
         L.dwc_workspace_bytes.restype = C.c_size_t
         for name in ("dwc_create", "dwc_destroy", "dwc_solve_band", "dwc_solve_band_host", "dwc_steer",
-                     "dwc_das", "dwc_compress", "dwc_psf", "dwc_gs", "dwc_set_timing", "dwc_get_stats"):
+                     "dwc_das", "dwc_compress", "dwc_psf", "dwc_gs", "dwc_keep_mask", "dwc_keep_unmask",
+                     "dwc_set_timing", "dwc_get_stats"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -259,6 +262,29 @@ class Context:
         _check(lib().dwc_gs(self._h, n, _dev(A, torch.float32, "A"), _dev(b, torch.float64, "b"), int(sweeps),
                             _dev(x, torch.float32, "x"), _stream(stream)))
         return x
+
+    # ---- multi-GPU gather helpers ----------------------------------------------------------
+    def keep_mask(self, n_keep, keep_idx, stream=None):
+        """Keep lists [K, S] (ascending, -1 padded) -> bitmask words [K, ceil(S/32)] (int32
+        tensor holding the uint32 bit patterns: bit s%32 of word s/32)."""
+        import torch
+        K, S = keep_idx.shape
+        mask = torch.empty((K, (S + 31) // 32), dtype=torch.int32, device=keep_idx.device)
+        _check(lib().dwc_keep_mask(self._h, K, S, _dev(n_keep, torch.int32, "n_keep"),
+                                   _dev(keep_idx, torch.int32, "keep_idx"), _dev(mask, torch.int32, "mask"),
+                                   _stream(stream)))
+        return mask
+
+    def keep_unmask(self, mask, S: int, stream=None):
+        """Inverse of keep_mask: (n_keep [K], keep_idx [K, S] ascending, -1 padded)."""
+        import torch
+        K = mask.shape[0]
+        n_keep = torch.empty(K, dtype=torch.int32, device=mask.device)
+        keep_idx = torch.empty((K, S), dtype=torch.int32, device=mask.device)
+        _check(lib().dwc_keep_unmask(self._h, K, int(S), _dev(mask, torch.int32, "mask"),
+                                     _dev(n_keep, torch.int32, "n_keep"), _dev(keep_idx, torch.int32, "keep_idx"),
+                                     _stream(stream)))
+        return n_keep, keep_idx
 
     # ---- diagnostics --------------------------------------------------------------------
     def set_timing(self, enable: bool = True):
