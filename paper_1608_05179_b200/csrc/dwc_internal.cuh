@@ -79,9 +79,34 @@ int launch_psf(const Geo &g, const double *dist, const double *amp, int n_bins, 
 //   L_k  = A[k][(k-1) mod T]   at T + k                    (T tiles; first sub-diagonal)
 //   LL_k = A[k][(k-2) mod T]   at 2T + k                   (T tiles; second sub-diagonal)
 //   U(I,J) = A[I][J], J > I    at 3T + row_base(I) + pos   (T(T-1)/2 tiles)
-// Row I's U tiles are grouped by owner CTA o = J mod g and ascending in J inside a group, so
-// the tiles a GS CTA streams from one row block are one contiguous run.
-__host__ __device__ inline int sym_cnt(int x, int o, int g) { return x >= o ? (x - o) / g + 1 : 0; }
+// Row I's U tiles are grouped by owner CTA o = own_of(g, J) and ascending in J inside a group,
+// so the tiles a GS CTA streams from one row block are one contiguous run.  Ownership is a
+// periodic pattern weighted by the CTAs' stream warps: the sub-group leader (owner 0) runs the
+// solver, L and D warps and streams with 3 warps, the others with 5, so for g = 4 the leader
+// owns 3 of every 18 column blocks (period 0123123 0123123 0123, 5 each for 1..3), for g = 2 3
+// of every 8 (01101101).
+__host__ __device__ inline int own_period(int g) { return g == 4 ? 18 : (g == 2 ? 8 : 1); }
+__host__ __device__ inline int own_weight(int g, int o) { return g == 4 ? (o == 0 ? 3 : 5) : (g == 2 ? (o == 0 ? 3 : 5) : 1); }
+__host__ __device__ inline int own_of(int g, int J) {
+    if (g == 4) return (int)((0xE4E7939E4ull >> (2 * (J % 18))) & 3ull);   // 0,1,2,3,1,2,3,0,1,2,3,1,2,3,0,1,2,3
+    if (g == 2) return (0xB6u >> (J % 8)) & 1u;                                // 0,1,1,0,1,1,0,1
+    return 0;
+}
+// number of J in [0, x] owned by o
+__host__ __device__ inline int sym_cnt(int x, int o, int g) {
+    if (x < 0) return 0;
+    const int P = own_period(g), full = (x + 1) / P, rem = (x + 1) - full * P;
+    int c = full * own_weight(g, o);
+    for (int r = 0; r < rem; r++) c += (own_of(g, r) == o);
+    return c;
+}
+// the idx-th (0-based) J owned by o
+__host__ __device__ inline int own_nth(int g, int o, int idx) {
+    const int P = own_period(g), w = own_weight(g, o);
+    int k = idx % w, J = (idx / w) * P;
+    for (int r = 0;; r++)
+        if (own_of(g, r) == o && k-- == 0) return J + r;
+}
 __host__ __device__ inline int sym_row_base(int T, int I) { return I * (T - 1) - I * (I - 1) / 2; }
 __host__ __device__ inline int sym_run_len(int T, int g, int I, int o) {
     return sym_cnt(T - 1, o, g) - sym_cnt(I, o, g);
@@ -91,10 +116,8 @@ __host__ __device__ inline int sym_run_start(int T, int g, int I, int o) {
     for (int q = 0; q < o; q++) s += sym_run_len(T, g, I, q);
     return 3 * T + sym_row_base(T, I) + s;
 }
-// first J > I owned by o
-__host__ __device__ inline int sym_run_j0(int g, int I, int o) { return I + 1 + ((o - (I + 1) % g) + g) % g; }
 __host__ __device__ inline int sym_u_tile(int T, int g, int I, int J) {
-    const int o = J % g;
+    const int o = own_of(g, J);
     return sym_run_start(T, g, I, o) + (sym_cnt(J - 1, o, g) - sym_cnt(I, o, g));
 }
 // stored tiles holding block (a, b) of A~ (up to three: U(0,T-1) is also L_0, U(0,T-2) also

@@ -49,6 +49,10 @@ constexpr int kThreads = kWarps * 32;
 constexpr int kCons = kWarps - 3;  // consumer warps (3..7)
 constexpr int kChunk = 3;          // tiles per ring slot (one contiguous bulk copy)
 constexpr int kRing = 4;           // ring slots
+#ifndef GS_PF
+#define GS_PF 4
+#endif
+constexpr int kPf = GS_PF;         // L2 prefetch distance of the stream runs, in steps
 constexpr int kTile = 1024;        // floats per tile
 #ifndef GS_KSTG
 #define GS_KSTG 3
@@ -73,12 +77,14 @@ struct GsItem {
     int bin[kCl];   // bins of the sub-groups (-1 = idle)
 };
 
+static_assert(kChunk == 3, "a staging slot (L, D, LL) doubles as one stream ring slot");
 struct __align__(128) GsSmem {
-    float ring[kRing][kChunk][kTile];
-    float stg[kStg][3][kTile];         // [step j % kStg]: L_j, D_j, LL_{j+2} (row blocks mod T)
+    // stream ring slots 0..kRing-1; slots kRing..kRing+kStg-1 are the leader's staging slots
+    // ([step j % kStg]: L_j, D_j, LL_{j+2}) and extra stream slots in the other CTAs
+    float ring[kRing + kStg][kChunk][kTile];
     GsPacket pk[kStg];                 // solver packet of the staged block
     float pr[2][kCl][kCons][32];       // leader: partial row sums of every consumer warp of the sub-group
-    unsigned long long full[kRing], empty[kRing];
+    unsigned long long full[kRing + kStg], empty[kRing + kStg];
     unsigned long long stg_full[kStg], stg_empty[kStg];
     unsigned long long pready[2];      // leader: 1 arrival + g*kCons*128 tx bytes per step
     unsigned long long xr[2];          // leader: solver arrival; others: 1 arrival + 128 tx
@@ -153,6 +159,10 @@ __device__ __forceinline__ void st_async_f32(uint32_t raddr, float v, uint32_t r
                  "r"(rbar)
                  : "memory");
 }
+// L2 prefetch of a global range (no shared-memory destination, no completion tracking)
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -173,20 +183,24 @@ __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.syn
 // The runs are computed once per work item into shared memory (seg_table) so the per-step cost
 // is two LDS.128.
 struct __align__(16) Seg {
-    int t0, len, j0, pad;   // first tile (bin-relative), tiles, J of the first tile
-};
+    int t0, len, j0, ord0;   // first tile (bin-relative), tiles, J of the first tile, its ordinal
+};                           // among the CTA's owned column blocks (own_nth)
 __device__ Seg seg_run(int T, int g, int rg, int kn, int seg) {
     Seg r{0, 0, 0, 0};
     const int I = (seg == 0) ? kn : kn - 3;
     if (I < 0) return r;
-    int len = sym_run_len(T, g, I, rg), st = sym_run_start(T, g, I, rg), j = sym_run_j0(g, I, rg);
+    int len = sym_run_len(T, g, I, rg), st = sym_run_start(T, g, I, rg), ord = sym_cnt(I, rg, g);
     if (seg == 0) {
         const int kx = (kn + T - 1) % T, kl = (kn + T - 2) % T;
-        while (len > 0 && (j + g * (len - 1) == kx || j + g * (len - 1) == kl)) len--;
+        while (len > 0) {
+            const int jl = own_nth(g, rg, ord + len - 1);
+            if (jl != kx && jl != kl) break;
+            len--;
+        }
     } else {
-        while (len > 0 && j < kn) { j += g; st++; len--; }
+        while (len > 0 && own_nth(g, rg, ord) < kn) { ord++; st++; len--; }
     }
-    r.t0 = st; r.len = len; r.j0 = j;
+    r.t0 = st; r.len = len; r.j0 = len > 0 ? own_nth(g, rg, ord) : 0; r.ord0 = ord;
     return r;
 }
 
@@ -237,6 +251,8 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
     float *xs = reinterpret_cast<float *>(smem_raw + sizeof(GsSmem));
     float *ys = xs + xcap;   // per stream warp: y_J (lower part of row J) for the owned J, J/g-indexed
     Seg *segt = reinterpret_cast<Seg *>(ys + kCons * ystride);   // [kn][2] runs of this CTA
+    int *ownJ = reinterpret_cast<int *>(segt + 2 * (xcap / 32));  // ordinal -> owned column block J
+    int *ordOf = ownJ + (xcap / 32);                             // J -> ordinal (-1: not owned)
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint32_t crank = cluster_rank();
 
@@ -250,10 +266,11 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
         const int item = sh.item;
         if (item >= n_items) break;
         const GsItem IT = items[item];
-        const int g = IT.g, lg = g >> 1;   // g in {1, 2, 4}
+        const int g = IT.g;   // 1, 2 or 4
         const int sg = (int)crank / g, rg = (int)crank % g;
         const uint32_t leader = (uint32_t)(sg * g);
         const bool is_leader = (rg == 0);
+        const int nring = is_leader ? kRing : kRing + kStg;   // non-leaders stream into the staging slots too
         const int bin = IT.bin[sg];
         BinLayout L = {0, 0, 0, 0, 0, 0, 0};
         if (bin >= 0) L = lay[bin];
@@ -265,9 +282,15 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
         for (int i = tid; i < sp; i += kThreads) xs[i] = 0.f;
         for (int i = tid; i < kCons * ystride; i += kThreads) ys[i] = 0.f;
         for (int i = tid; i < 2 * T; i += kThreads) segt[i] = seg_run(T, g, rg, i >> 1, i & 1);
+        for (int J = tid; J < T; J += kThreads) {
+            const bool mine = own_of(g, J) == rg;
+            const int o = sym_cnt(J - 1, rg, g);
+            ordOf[J] = mine ? o : -1;
+            if (mine) ownJ[o] = J;
+        }
         if (tid == 0) {
             const int n_sw = is_leader ? kCons - 2 : kCons;
-            for (int i = 0; i < kRing; i++) {
+            for (int i = 0; i < kRing + kStg; i++) {
                 mbar_init(&sh.full[i], 1);
                 mbar_init(&sh.empty[i], (uint32_t)n_sw);   // every stream warp releases every chunk
             }
@@ -286,22 +309,31 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
         if (wid == 1) {
             // ================= stream producer (one lane): this CTA's tiles of each row block
             if (lane == 0) {
-                uint32_t seq = 0;
-                const bool ppf = prof && blockIdx.x == 0;
+                uint32_t seq = 0, slot = 0, ph = 0;
+                const bool ppf = prof && item == 0 && crank == 0;   // item 0 = the largest bin (LPT)
                 unsigned long long t0 = 0, p_wait = 0, p_issue = 0;
-                for (int s = 0, kn = 0; s < total; s++, kn = (kn + 1 == T) ? 0 : kn + 1) {
+                // the row runs of step s + kPf are prefetched into L2 while step s is copied into the
+                // ring: the ring then only has to cover L2 latency, not HBM latency
+                for (int s = 0, kn = 0, kp = kPf % T; s < total;
+                     s++, kn = (kn + 1 == T) ? 0 : kn + 1, kp = (kp + 1 == T) ? 0 : kp + 1) {
+                    if (s + kPf < total) {
+                        const Seg *sp = segt + 2 * kp;
+                        for (int sg = 0; sg < 2; sg++)
+                            if (sp[sg].len > 0)
+                                bulk_prefetch_l2(Ab + (size_t)sp[sg].t0 * kTile, (uint32_t)sp[sg].len * kTile * 4);
+                    }
                     const Seg *sd = segt + 2 * kn;
                     for (int sg = 0; sg < 2; sg++)
                     for (int off = 0; off < sd[sg].len; off += kChunk) {
                         const int tt = sd[sg].t0 + off, nt = min(kChunk, sd[sg].len - off);
-                        const uint32_t slot = seq % kRing;
                         if (ppf) t0 = clock64();
-                        mbar_wait(&sh.empty[slot], ((seq / kRing) & 1) ^ 1);
+                        mbar_wait(&sh.empty[slot], ph ^ 1);
                         if (ppf) { const unsigned long long t = clock64(); p_wait += t - t0; t0 = t; }
                         mbar_expect_tx(&sh.full[slot], (uint32_t)nt * kTile * 4);
                         bulk_g2s(sh.ring[slot][0], Ab + (size_t)tt * kTile, (uint32_t)nt * kTile * 4, &sh.full[slot]);
                         if (ppf) { const unsigned long long t = clock64(); p_issue += t - t0; }
                         seq++;
+                        if (++slot == (uint32_t)nring) { slot = 0; ph ^= 1; }
                     }
                 }
                 if (ppf) { prof[12] = p_wait; prof[13] = p_issue; prof[14] = seq; }
@@ -315,9 +347,9 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                     const int kn2 = (kn + 2 >= T) ? kn + 2 - T : kn + 2;   // (mod T again for T < 2)
                     mbar_wait(&sh.stg_empty[sl], ((s / kStg) & 1) ^ 1);
                     mbar_expect_tx(&sh.stg_full[sl], 3 * kTile * 4 + kPacketBytes);
-                    bulk_g2s(sh.stg[sl][0], Ab + (size_t)(T + kn) * kTile, kTile * 4, &sh.stg_full[sl]);   // L_kn
-                    bulk_g2s(sh.stg[sl][1], Ab + (size_t)kn * kTile, kTile * 4, &sh.stg_full[sl]);         // D_kn
-                    bulk_g2s(sh.stg[sl][2], Ab + (size_t)(2 * T + kn2 % T) * kTile, kTile * 4,
+                    bulk_g2s(sh.ring[kRing + sl][0], Ab + (size_t)(T + kn) * kTile, kTile * 4, &sh.stg_full[sl]);   // L_kn
+                    bulk_g2s(sh.ring[kRing + sl][1], Ab + (size_t)kn * kTile, kTile * 4, &sh.stg_full[sl]);         // D_kn
+                    bulk_g2s(sh.ring[kRing + sl][2], Ab + (size_t)(2 * T + kn2 % T) * kTile, kTile * 4,
                              &sh.stg_full[sl]);                                                      // LL_{kn+2}
                     bulk_g2s(&sh.pk[sl], pkb + kn, kPacketBytes, &sh.stg_full[sl]);
                 }
@@ -333,8 +365,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
             const int rq = lane & 7, cq = lane >> 3;
             const int n_sw = is_leader ? kCons - 2 : kCons;   // warps taking stream tiles
             const bool do_L = is_leader && c == kCons - 1, do_D = is_leader && c == kCons - 2;
-            uint32_t seq = 0;
-            const bool skip_dot = prof && prof[15];
+            uint32_t slot = 0, ph = 0;
             float lcarry[4] = {0.f, 0.f, 0.f, 0.f};   // L warp: LL_{kn+1} x_kx^old for the next step
             // leader, D warp: forward x of solver step jj to the sub-group's other CTAs (st.async
             // completes 128 bytes on their x-ready barrier)
@@ -346,7 +377,9 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                     for (int q = 1; q < g; q++) st_async_v4(mapa(xa, leader + q), xv, mapa(xra, leader + q));
                 }
             };
-            const bool pf = prof && blockIdx.x == 0 && c == 0 && lane == 0;
+            // profile item 0 (the largest bin): consumer 0 of the leader and of cluster rank 1
+            const bool pf = prof && item == 0 && c == 0 && lane == 0 && crank <= 1;
+            unsigned long long *pc = prof + (crank == 0 ? 5 : 16);
             unsigned long long tA = 0, cw_x = 0, cw_full = 0, c_comp = 0, c_red = 0;
             for (int s = 0, kn = 0, kx = T - 1; s < total; s++, kx = kn, kn = (kn + 1 == T) ? 0 : kn + 1) {
                 if (pf) tA = clock64();
@@ -374,12 +407,12 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                         // (tile staged at step s-1) for the next step, while x_kx is still old
 #pragma unroll
                         for (int q = 0; q < 4; q++) { acc[q] = lcarry[q]; lcarry[q] = 0.f; }
-                        tile_dot(sh.stg[b][0], xs + 32 * kx, rq, cq, acc);
-                        if (T >= 3 && s >= 1) tile_dot(sh.stg[(s - 1) % kStg][2], xs + 32 * kx, rq, cq, lcarry);
+                        tile_dot(sh.ring[kRing + b][0], xs + 32 * kx, rq, cq, acc);
+                        if (T >= 3 && s >= 1) tile_dot(sh.ring[kRing + (s - 1) % kStg][2], xs + 32 * kx, rq, cq, lcarry);
                         __syncwarp();
                         if (lane == 0 && s >= 1) mbar_arrive_local(&sh.stg_empty[(s - 1) % kStg]);
                     } else {
-                        if (T >= 2) tile_dot(sh.stg[b][1], xs + 32 * kn, rq, cq, acc);
+                        if (T >= 2) tile_dot(sh.ring[kRing + b][1], xs + 32 * kn, rq, cq, acc);
                         __syncwarp();
                         if (lane == 0) mbar_arrive_local(&sh.stg_empty[b]);
                     }
@@ -388,8 +421,8 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                     float *yw = ys + c * ystride;
                     const Seg *sd = segt + 2 * kn;
                     // the lower part of row kn this warp accumulated from earlier steps' scatters
-                    if ((kn & (g - 1)) == rg) {
-                        float *yp = yw + (kn >> lg) * 32 + lane;
+                    if (ordOf[kn] >= 0) {
+                        float *yp = yw + ordOf[kn] * 32 + lane;
                         acc_t += *yp;
                         *yp = 0.f;
                     }
@@ -399,12 +432,13 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                         const Seg sr = sd[sg];
                         for (int off = 0; off < sr.len; off += kChunk) {
                             const int nt = min(kChunk, sr.len - off);
-                            const uint32_t slot = seq % kRing;
-                            mbar_wait(&sh.full[slot], (seq / kRing) & 1);
+                            // every warp observes and releases every chunk (parity-tracked barriers: no
+                            // warp may fall a ring lap behind or run one ahead)
+                            mbar_wait(&sh.full[slot], ph);
                             if (pf) { const unsigned long long t = clock64(); cw_full += t - tA; tA = t; }
                             int t = first;
-                            for (; t < nt && !skip_dot; t += n_sw) {
-                                const int J = sr.j0 + g * (off + t);
+                            for (; t < nt; t += n_sw) {
+                                const int ord = sr.ord0 + off + t, J = ownJ[ord];
                                 const float *tile = sh.ring[slot][t];
                                 if (sg == 0) {
                                     tile_dot(tile, xs + 32 * J, rq, cq, acc);
@@ -413,7 +447,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                                     if (J == kn) {
                                         acc_t += v;
                                     } else {
-                                        yw[(J >> lg) * 32 + lane] += v;
+                                        yw[ord * 32 + lane] += v;
                                     }
                                 }
                             }
@@ -421,7 +455,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                             if (pf) { const unsigned long long t = clock64(); c_comp += t - tA; tA = t; }
                             __syncwarp();
                             if (lane == 0) mbar_arrive_local(&sh.empty[slot]);
-                            seq++;
+                            if (++slot == (uint32_t)nring) { slot = 0; ph ^= 1; }
                         }
                     }
                 }
@@ -462,7 +496,8 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 }
             }
             if (pf) {
-                prof[5] = cw_x; prof[6] = cw_full; prof[7] = c_comp; prof[8] = c_red; prof[9] = total;
+                pc[0] = cw_x; pc[1] = cw_full; pc[2] = c_comp; pc[3] = c_red;
+                if (crank == 0) prof[9] = total;
             }
         } else if (is_leader && total > 0) {
             // ================= solver (warp 0 of the leader) =================
@@ -481,7 +516,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
             float invd[4], xo[4], wg10, wg20, wg30, wg21, wg31, wg32;
             float bhi[4], blo[4];
             int prev_row0 = -1;
-            const bool pf = prof && blockIdx.x == 0 && lane == 0;
+            const bool pf = prof && item == 0 && lane == 0;
             unsigned long long tA = 0, w_p = 0, w_s = 0, c_set = 0, c_rec = 0, c_bc = 0, c_pub = 0, c_post = 0;
             auto publish = [&](int jj, int r0) {
                 // x of solver step jj (block at r0) -> own xs + x-ready; bulk copies to the others
@@ -534,10 +569,10 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 const int kn1 = (k + 1 == T) ? 0 : k + 1;   // next block
                 const bool has_next = (j + 1 < total);
                 if (pf) tA = clock64();
-                const float *Dt = sh.stg[sl][1];
+                const float *Dt = sh.ring[kRing + sl][1];
                 // role 1 streams the next block's L tile (with no next step it re-reads Dt, unused),
                 // role 2 the LL tile staged with this step
-                const float *tp = (role1 && has_next) ? sh.stg[sl1][0] : (role2 ? sh.stg[sl][2] : Dt);
+                const float *tp = (role1 && has_next) ? sh.ring[kRing + sl1][0] : (role2 ? sh.ring[kRing + sl][2] : Dt);
                 // ---- critical path: P_k -> residual -> publish x_{k-1} -> recurrence
                 mbar_wait(&sh.pready[b], (j >> 1) & 1);
                 if (pf) { const unsigned long long t = clock64(); w_p += t - tA; tA = t; }
@@ -579,35 +614,39 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
 #pragma unroll
                 for (int G = 0; G < 8; G++) {
                     const float m = (lane == G) ? 1.f : 0.f;
-                    // rows 4G..4G+3, sequential inside lane G, on temporaries
-                    const float c0 = fmaxf(-ac[0] * invd[0], -xo[0]);
-                    const float d0 = __shfl_sync(0xffffffffu, c0, G);
-                    float u1 = fmaf(-wg10, c0, -ac[1] * invd[1]);
-                    float u2 = fmaf(-wg20, c0, -ac[2] * invd[2]);
-                    float u3 = fmaf(-wg30, c0, -ac[3] * invd[3]);
+                    // this group's 4 tile columns (role 0/3: D, role 1: L_{k+1}, role 2: LL_{k+2})
+                    float4 v[4];
+#pragma unroll
+                    for (int i = 0; i < 4; i++) v[i] = *reinterpret_cast<const float4 *>(tp + (4 * G + i) * 32 + L4);
+                    // rows 4G..4G+3, sequential inside lane G, on temporaries taken before this
+                    // group's updates; every delta is broadcast and applied to all lanes' residuals
+                    // as soon as it is known (only the last one is on the path to the next group)
+                    const float w0 = -ac[0] * invd[0], w1 = -ac[1] * invd[1], w2 = -ac[2] * invd[2],
+                                w3 = -ac[3] * invd[3];
+                    auto apply = [&](const float4 &t, float d) {
+                        ac[0] = fmaf(t.x, d, ac[0]);
+                        ac[1] = fmaf(t.y, d, ac[1]);
+                        ac[2] = fmaf(t.z, d, ac[2]);
+                        ac[3] = fmaf(t.w, d, ac[3]);
+                    };
+                    const float c0 = fmaxf(w0, -xo[0]);
+                    apply(v[0], __shfl_sync(0xffffffffu, c0, G));
+                    float u1 = fmaf(-wg10, c0, w1);
+                    float u2 = fmaf(-wg20, c0, w2);
+                    float u3 = fmaf(-wg30, c0, w3);
                     const float c1 = fmaxf(u1, -xo[1]);
-                    const float d1 = __shfl_sync(0xffffffffu, c1, G);
+                    apply(v[1], __shfl_sync(0xffffffffu, c1, G));
                     u2 = fmaf(-wg21, c1, u2);
                     u3 = fmaf(-wg31, c1, u3);
                     const float c2 = fmaxf(u2, -xo[2]);
-                    const float d2 = __shfl_sync(0xffffffffu, c2, G);
+                    apply(v[2], __shfl_sync(0xffffffffu, c2, G));
                     u3 = fmaf(-wg32, c2, u3);
                     const float c3 = fmaxf(u3, -xo[3]);
-                    const float d3 = __shfl_sync(0xffffffffu, c3, G);
+                    apply(v[3], __shfl_sync(0xffffffffu, c3, G));
                     xo[0] = fmaf(m, c0, xo[0]);
                     xo[1] = fmaf(m, c1, xo[1]);
                     xo[2] = fmaf(m, c2, xo[2]);
                     xo[3] = fmaf(m, c3, xo[3]);
-                    // role 0: residuals of later lanes' rows; role 1: next block's lres
-                    const float dg[4] = {d0, d1, d2, d3};
-#pragma unroll
-                    for (int i = 0; i < 4; i++) {
-                        const float4 v = *reinterpret_cast<const float4 *>(tp + (4 * G + i) * 32 + L4);
-                        ac[0] = fmaf(v.x, dg[i], ac[0]);
-                        ac[1] = fmaf(v.y, dg[i], ac[1]);
-                        ac[2] = fmaf(v.z, dg[i], ac[2]);
-                        ac[3] = fmaf(v.w, dg[i], ac[3]);
-                    }
                 }
                 if (pf) { asm volatile("" ::"f"(xo[3])); const unsigned long long t = clock64(); c_rec += t - tA; tA = t; }
                 // role-1 accumulators (lanes 8-15) -> lres; role-2 (lanes 16-23) -> LL increment of
@@ -724,13 +763,16 @@ int launch_tile_convert(int to_sym, int n, int sp, int g, const float *src, floa
 }
 
 size_t gs_smem_bytes(int max_sp, int ystride) {
-    return sizeof(GsSmem) + (size_t)max_sp * 4 + (size_t)kCons * ystride * 4 + sizeof(Seg) * 2 * (size_t)(max_sp / 32);
+    return sizeof(GsSmem) + (size_t)max_sp * 4 + (size_t)kCons * ystride * 4 + sizeof(Seg) * 2 * (size_t)(max_sp / 32) +
+           2 * sizeof(int) * (size_t)(max_sp / 32);
 }
 
-// floats of y per stream warp: 32 per owned column block (ceil(T/g))
+// floats of y per stream warp: 32 per owned column block
 int gs_ystride(int nk) {
     const int T = (nk + 31) / 32, g = gs_group_size(nk);
-    return (T + g - 1) / g * 32;
+    int mx = 0;
+    for (int o = 0; o < g; o++) mx = std::max(mx, sym_cnt(T - 1, o, g));
+    return mx * 32;
 }
 
 int gs_cluster_size() { return kCl; }
@@ -748,13 +790,8 @@ int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_s
     static const bool profile = getenv("DWC_GS_PROFILE") != nullptr;
     unsigned long long *prof = nullptr;
     if (profile) {
-        cudaMalloc(&prof, 16 * sizeof(unsigned long long));
-        cudaMemsetAsync(prof, 0, 16 * sizeof(unsigned long long), st);
-        if (getenv("DWC_GS_SKIP_STREAM_DOT")) {   // experiment: consumers skip the tile dots
-            unsigned long long one = 1;
-            cudaMemcpyAsync(prof + 15, &one, sizeof one, cudaMemcpyHostToDevice, st);
-            cudaStreamSynchronize(st);
-        }
+        cudaMalloc(&prof, 32 * sizeof(unsigned long long));
+        cudaMemsetAsync(prof, 0, 32 * sizeof(unsigned long long), st);
     }
     const size_t smem = gs_smem_bytes(max_sp, ystride);
     cudaFuncSetAttribute(gs_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -782,7 +819,7 @@ int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_s
                                        (const GsPacket *)packets, sweeps, x_out, x_map, keep_idx, S, max_sp, ystride,
                                        prof);
     if (profile) {
-        unsigned long long h[16];
+        unsigned long long h[32];
         cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, st);
         cudaStreamSynchronize(st);
         const double n = h[9] ? (double)h[9] : 1.0;
@@ -793,6 +830,8 @@ int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_s
                 (h[4] - h[11]) / n, h[5] / n, h[6] / n, h[7] / n, h[8] / n);
         fprintf(stderr, "[gs-prof] producer: chunks=%llu (%.1f/step) wait_empty %.0f issue %.0f cyc/chunk\n", h[14],
                 h[14] / n, h[14] ? (double)h[12] / h[14] : 0.0, h[14] ? (double)h[13] / h[14] : 0.0);
+        fprintf(stderr, "[gs-prof] rank-1 consumer0: wait_x %.0f wait_tile %.0f compute %.0f reduce+send %.0f\n",
+                h[16] / n, h[17] / n, h[18] / n, h[19] / n);
         cudaFree(prof);
     }
     return e == cudaSuccess ? 1 : -1;
