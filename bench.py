@@ -183,7 +183,7 @@ def run_ours(args, cfg):
 
     def step():
         out = ctx.solve_band(geom, band.freqs, csm_dev, cfg.epsilon, cfg.sweeps, cfg.eps_mode,
-                             full_grid=cfg.full_grid, stream=stream)
+                             full_grid=cfg.full_grid, order=args.order, stream=stream)
         if strong:
             # the one collective: maps + keep bitmasks + counts, all ranks
             mask = ctx.keep_mask(out["n_keep"], out["keep_idx"], stream=stream)
@@ -244,7 +244,7 @@ def run_ours(args, cfg):
              "keep_idx": torch.empty((K, S), dtype=torch.int32).pin_memory(),
              "x_map": torch.empty((K, S), dtype=torch.float32).pin_memory(), "b_map": None}
     ctx.solve_band_host(geom, band.freqs, csm_host, cfg.epsilon, cfg.sweeps, cfg.eps_mode, cfg.full_grid,
-                        out=h_out, stream=stream)
+                        out=h_out, stream=stream, order=args.order)
     e2e_ms = []
     for it in range(args.steps):
         flush.zero_()
@@ -255,7 +255,7 @@ def run_ours(args, cfg):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         ctx.solve_band_host(geom, band.freqs, csm_host, cfg.epsilon, cfg.sweeps, cfg.eps_mode, cfg.full_grid,
-                            out=h_out, stream=stream)
+                            out=h_out, stream=stream, order=args.order)
         e1.record(stream)
         torch.cuda.synchronize(dev)
         e2e_ms.append(e0.elapsed_time(e1))
@@ -277,7 +277,8 @@ def run_ours(args, cfg):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": args.scaling if world > 1 else "weak", "vs_baseline": None,
             "dtype": "f32 (PSF + Gauss-Seidel); f64 (DAS map + wavelet threshold)", "data": "synthetic",
-            "config": {"workload": workload_desc(cfg), "bins_per_gpu": K, "parallelism": f"bins-dp{world}",
+            "config": {"workload": workload_desc(cfg), "bins_per_gpu": K,
+                       "predictor": "cubic (R19)" if args.order == 3 else "linear (R7)", "parallelism": f"bins-dp{world}",
                        "l2_flush": "256 MiB write between timed steps", "inputs": "CSMs resident in HBM"},
             "psf_stream_gbs": achieved,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -311,6 +312,8 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--ref-bins", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--order", type=int, default=1, choices=[1, 3],
+                    help="S3 predictor: 1 linear (reading R7, default), 3 cubic (R19)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

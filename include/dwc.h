@@ -80,10 +80,15 @@ typedef struct {
     double epsilon;   /* > 0; relative (eps * max|b|) or absolute */
     int32_t eps_mode; /* 0 = relative, 1 = absolute (reading R6) */
     int32_t sweeps;   /* Gauss-Seidel sweeps >= 1 from x0 = 0 */
-    int32_t flags;    /* DWC_FULL_GRID: keep every node (the paper's "original grid") */
+    int32_t flags;    /* DWC_FULL_GRID: keep every node (the paper's "original grid"); DWC_CUBIC */
 } dwc_params;
 
 #define DWC_FULL_GRID 1
+/* DWC_CUBIC: 4-point (cubic, Deslauriers-Dubuc family) interpolating predictor in S3 instead
+ * of the linear one (reading R19): Lagrange interpolation through
+ * the 4 nearest coarse nodes, linear rule where fewer than 4 are in reach.  Changes only the
+ * compressed index set (and so everything downstream). */
+#define DWC_CUBIC 2
 #define DWC_MAX_MICS 512
 
 /* Create / destroy a context on CUDA device `device`.  The device must be sm_100

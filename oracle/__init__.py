@@ -49,8 +49,8 @@ def lib():
         _lib.or_steering.argtypes = geo + [d, i, _P, _P]
         _lib.or_das.argtypes = geo + [d, _P, _P]
         _lib.or_max_level.argtypes = [i]
-        _lib.or_wavelet_details.argtypes = [i, _P, _P, _P]
-        _lib.or_compress.argtypes = [i, _P, d, i, i, _P, _P, _P, _P]
+        _lib.or_wavelet_details.argtypes = [i, _P, _P, _P, i]
+        _lib.or_compress.argtypes = [i, _P, d, i, i, _P, _P, _P, _P, i]
         _lib.or_psf.argtypes = geo + [d, i, _P, _P]
         _lib.or_gs.argtypes = [i, _P, _P, i, _P]
         _lib.or_solve_bin.argtypes = geo + [d, _P, d, i, i, i, _P, _P, _P, _P]
@@ -120,15 +120,16 @@ def max_level(n: int) -> int:
     return lib().or_max_level(int(n))
 
 
-def wavelet_details(n: int, b) -> Tuple[np.ndarray, np.ndarray]:
+def wavelet_details(n: int, b, order: int = 1) -> Tuple[np.ndarray, np.ndarray]:
+    """order 1: linear predictor (R7); 3: 4-point cubic predictor (R19)."""
     b = _f64(b)
     d = np.zeros(n * n)
     lv = np.zeros(n * n, dtype=np.uint8)
-    _chk(lib().or_wavelet_details(int(n), _p(b), _p(d), _p(lv)), "wavelet_details")
+    _chk(lib().or_wavelet_details(int(n), _p(b), _p(d), _p(lv), int(order)), "wavelet_details")
     return d, lv
 
 
-def compress(n: int, b, eps: float, eps_mode: int = 0, full_grid: bool = False):
+def compress(n: int, b, eps: float, eps_mode: int = 0, full_grid: bool = False, order: int = 1):
     """-> (keep int32 ascending, level uint8[S], d fp64[S], eps_eff)."""
     b = _f64(b)
     keep = np.zeros(n * n, dtype=np.int32)
@@ -136,7 +137,7 @@ def compress(n: int, b, eps: float, eps_mode: int = 0, full_grid: bool = False):
     d = np.zeros(n * n)
     ee = np.zeros(1)
     nk = _chk(lib().or_compress(int(n), _p(b), float(eps), int(eps_mode), int(full_grid),
-                                _p(keep), _p(lv), _p(d), _p(ee)), "compress")
+                                _p(keep), _p(lv), _p(d), _p(ee), int(order)), "compress")
     return keep[:nk].copy(), lv, d, float(ee[0])
 
 
@@ -156,7 +157,11 @@ def gs(A, b, sweeps: int) -> np.ndarray:
     return x
 
 
-def solve_bin(mic, c0, n, L, z0, cx, cy, freq, csm, eps, eps_mode, sweeps, full_grid=False):
+def _flags(full_grid, order):
+    return (1 if full_grid else 0) | (2 if order == 3 else 0)
+
+
+def solve_bin(mic, c0, n, L, z0, cx, cy, freq, csm, eps, eps_mode, sweeps, full_grid=False, order=1):
     """-> (keep, x_map fp64[S], b fp64[S])."""
     mic, g = _geo(mic, c0, n, L, z0, cx, cy)
     csm = np.ascontiguousarray(csm, dtype=np.complex128)
@@ -166,12 +171,12 @@ def solve_bin(mic, c0, n, L, z0, cx, cy, freq, csm, eps, eps_mode, sweeps, full_
     x = np.zeros(S)
     b = np.zeros(S)
     _chk(lib().or_solve_bin(*g, float(freq), _p(csm), float(eps), int(eps_mode), int(sweeps),
-                            int(full_grid), _p(nk), _p(keep), _p(x), _p(b)), "solve_bin")
+                            _flags(full_grid, order), _p(nk), _p(keep), _p(x), _p(b)), "solve_bin")
     return keep[: nk[0]].copy(), x, b
 
 
 def solve_band(mic, c0, n, L, z0, cx, cy, freqs, csm, eps, eps_mode, sweeps,
-               full_grid=False, n_threads: Optional[int] = None):
+               full_grid=False, n_threads: Optional[int] = None, order: int = 1):
     """Batched S0..S8 over K bins on a pthread pool.
     -> (n_keep int32[K], keep int32[K,S] (-1 padded), x_map fp64[K,S], b fp64[K,S])."""
     mic, g = _geo(mic, c0, n, L, z0, cx, cy)
@@ -186,16 +191,16 @@ def solve_band(mic, c0, n, L, z0, cx, cy, freqs, csm, eps, eps_mode, sweeps,
     if n_threads is None:
         n_threads = os.cpu_count() or 1
     _chk(lib().or_solve_band(*g, K, _p(freqs), _p(csm), float(eps), int(eps_mode), int(sweeps),
-                             int(full_grid), _p(nk), _p(keep), _p(x), _p(b), int(n_threads)),
+                             _flags(full_grid, order), _p(nk), _p(keep), _p(x), _p(b), int(n_threads)),
          "solve_band")
     return nk, keep, x, b
 
 
 def solve_band_cfg(band, n_threads: Optional[int] = None, sweeps: Optional[int] = None,
-                   full_grid: Optional[bool] = None, eps: Optional[float] = None):
+                   full_grid: Optional[bool] = None, eps: Optional[float] = None, order: int = 1):
     """Convenience: run the oracle on a synth.Band."""
     cfg = band.cfg
     return solve_band(band.mic_xyz, cfg.c0, cfg.n, cfg.side_len, cfg.z0, cfg.cx, cfg.cy,
                       band.freqs, band.csm, cfg.epsilon if eps is None else eps, cfg.eps_mode,
                       cfg.sweeps if sweeps is None else sweeps,
-                      cfg.full_grid if full_grid is None else full_grid, n_threads)
+                      cfg.full_grid if full_grid is None else full_grid, n_threads, order)

@@ -176,14 +176,40 @@ static int taps_1d(int i, int h, int n, int *pos, double *w) {
     return 1;
 }
 
+/* 1-D taps of the 4-point (cubic) interpolating wavelet, SURVEY §8(f) NEXT-1 (PAPER.md:228
+ * cites the Deslauriers-Dubuc interpolating family; reading R19 in DESIGN.md): Lagrange
+ * interpolation at i through the 4 nearest coarse points i + k h, k odd.  Interior
+ * {-3,-1,1,3}: (-1, 9, 9, -1)/16; left edge {-1,1,3,5}: (5, 15, -5, 1)/16; right edge
+ * {-5,-3,-1,1}: (1, -5, 15, 5)/16; past the last coarse point {-7,-5,-3,-1}:
+ * (-5, 21, -35, 35)/16; taps in ascending position.  Fewer than 4 coarse points in reach:
+ * the linear rule (R7).                                                       */
+static int taps_1d_cubic(int i, int h, int n, int *pos, double *w) {
+    int H = 2 * h;
+    if (i % H == 0) { pos[0] = i; w[0] = 1.0; return 1; }
+    static const int off[4][4] = {{-3, -1, 1, 3}, {-1, 1, 3, 5}, {-5, -3, -1, 1}, {-7, -5, -3, -1}};
+    static const double wt[4][4] = {{-1.0, 9.0, 9.0, -1.0}, {5.0, 15.0, -5.0, 1.0},
+                                    {1.0, -5.0, 15.0, 5.0}, {-5.0, 21.0, -35.0, 35.0}};
+    int set = -1;
+    if (i - 3 * h >= 0 && i + 3 * h <= n - 1) set = 0;
+    else if (i - 3 * h < 0 && i + 5 * h <= n - 1) set = 1;
+    else if (i + h <= n - 1 && i + 3 * h > n - 1 && i - 5 * h >= 0) set = 2;
+    else if (i + h > n - 1 && i - 7 * h >= 0) set = 3;
+    if (set < 0) return taps_1d(i, h, n, pos, w);
+    for (int k = 0; k < 4; k++) {
+        pos[k] = i + off[set][k] * h;
+        w[k] = wt[set][k] / 16.0;   /* exact */
+    }
+    return 4;
+}
+
 /* Interpolated value at (r,c) from level-j values of b (fine stride h).
  * Tensor product "interpolate rows then column" (R7):
- * t_a = sum_b w_b * b[r_a][c_b] (along x), pred = sum_a w_a * t_a.          */
-static double interp_2d(const double *b, int n, int r, int c, int h) {
-    int rp[2], cp[2];
-    double rw[2], cw[2];
-    int nr = taps_1d(r, h, n, rp, rw);
-    int nc = taps_1d(c, h, n, cp, cw);
+ * t_a = sum_b w_b * b[r_a][c_b] (along x), pred = sum_a w_a * t_a, sums left to right. */
+static double interp_2d(const double *b, int n, int r, int c, int h, int order) {
+    int rp[4], cp[4];
+    double rw[4], cw[4];
+    int nr = order == 3 ? taps_1d_cubic(r, h, n, rp, rw) : taps_1d(r, h, n, rp, rw);
+    int nc = order == 3 ? taps_1d_cubic(c, h, n, cp, cw) : taps_1d(c, h, n, cp, cw);
     double pred = 0.0;
     for (int a = 0; a < nr; a++) {
         double t = 0.0;
@@ -198,9 +224,9 @@ static double interp_2d(const double *b, int n, int r, int c, int h) {
 }
 
 /* Detail coefficients d = b - interp (Eq. 22) for every point of every level
- * > 0, and the level of every node.  d[s] = 0 on G^0.                        */
-int or_wavelet_details(int n, const double *b, double *d, uint8_t *level) {
-    if (n < 2) return OR_EINVAL;
+ * > 0, and the level of every node.  d[s] = 0 on G^0.  order: 1 linear (R7), 3 cubic (R19). */
+int or_wavelet_details(int n, const double *b, double *d, uint8_t *level, int order) {
+    if (n < 2 || (order != 1 && order != 3)) return OR_EINVAL;
     int J = or_max_level(n);
     int S = n * n;
     for (int s = 0; s < S; s++) { d[s] = 0.0; if (level) level[s] = 0; }
@@ -210,7 +236,7 @@ int or_wavelet_details(int n, const double *b, double *d, uint8_t *level) {
         for (int r = 0; r < n; r += h)
             for (int c = 0; c < n; c += h) {
                 if (r % H == 0 && c % H == 0) continue;   /* in G^j already */
-                double pred = interp_2d(b, n, r, c, h);   /* Alg. 1 line 5 */
+                double pred = interp_2d(b, n, r, c, h, order);   /* Alg. 1 line 5 */
                 d[(size_t)r * n + c] = b[(size_t)r * n + c] - pred;
                 if (level) level[(size_t)r * n + c] = (uint8_t)(j + 1);
             }
@@ -222,13 +248,13 @@ int or_wavelet_details(int n, const double *b, double *d, uint8_t *level) {
  * eps_mode 1: eps_eff = eps (absolute).  full_grid != 0: keep everything.
  * Returns n_keep (> 0) or a negative error.                                   */
 int or_compress(int n, const double *b, double eps, int eps_mode, int full_grid,
-                int *keep, uint8_t *level, double *d_out, double *eps_eff_out) {
+                int *keep, uint8_t *level, double *d_out, double *eps_eff_out, int order) {
     if (n < 2 || !(eps > 0.0)) return OR_EINVAL;
     int S = n * n;
     double *d = d_out ? d_out : (double *)malloc(sizeof(double) * (size_t)S);
     uint8_t *lv = level ? level : (uint8_t *)malloc((size_t)S);
     if (!d || !lv) return OR_ENOMEM;
-    int rc = or_wavelet_details(n, b, d, lv);
+    int rc = or_wavelet_details(n, b, d, lv, order);
     double maxabs = 0.0;
     for (int s = 0; s < S; s++) {
         double a = fabs(b[s]);
@@ -308,10 +334,11 @@ int or_gs(int nk, const double *A, const double *b, int sweeps, double *x) {
 
 /* ------------------------------------------------------------------------ */
 /* One bin, S1..S8.  keep (S ints) ascending, first n_keep valid.  x_map (S)
- * is the source power on the full grid, zero off the kept set (S8).          */
+ * is the source power on the full grid, zero off the kept set (S8).
+ * flags: bit 0 full grid (keep every node), bit 1 cubic predictor (R19).      */
 int or_solve_bin(int m, const double *mic, double c0, int n, double L, double z0,
                  double cx, double cy, double freq, const double *csm,
-                 double eps, int eps_mode, int sweeps, int full_grid,
+                 double eps, int eps_mode, int sweeps, int flags,
                  int *n_keep, int *keep, double *x_map, double *b_map) {
     int S = n * n;
     double *b = b_map ? b_map : (double *)malloc(sizeof(double) * (size_t)S);
@@ -320,7 +347,7 @@ int or_solve_bin(int m, const double *mic, double c0, int n, double L, double z0
     int nk = 0;
     double *A = NULL, *bt = NULL, *xt = NULL;
     if (rc == OR_OK) {
-        nk = or_compress(n, b, eps, eps_mode, full_grid, keep, NULL, NULL, NULL);
+        nk = or_compress(n, b, eps, eps_mode, flags & 1, keep, NULL, NULL, NULL, (flags & 2) ? 3 : 1);
         if (nk < 0) rc = nk;
     }
     if (rc == OR_OK) {
@@ -351,7 +378,7 @@ int or_solve_bin(int m, const double *mic, double c0, int n, double L, double z0
 typedef struct {
     int m; const double *mic; double c0; int n; double L, z0, cx, cy;
     int K; const double *freq; const double *csm;
-    double eps; int eps_mode, sweeps, full_grid;
+    double eps; int eps_mode, sweeps, flags;
     int *n_keep, *keep; double *x_map, *b_map;
     int next; int rc; pthread_mutex_t mu;
 } band_job;
@@ -366,7 +393,7 @@ static void *band_worker(void *arg) {
         if (k >= jb->K) break;
         int rc = or_solve_bin(jb->m, jb->mic, jb->c0, jb->n, jb->L, jb->z0, jb->cx, jb->cy,
                               jb->freq[k], jb->csm + (size_t)2 * jb->m * jb->m * k,
-                              jb->eps, jb->eps_mode, jb->sweeps, jb->full_grid,
+                              jb->eps, jb->eps_mode, jb->sweeps, jb->flags,
                               jb->n_keep + k, jb->keep + (size_t)S * k,
                               jb->x_map + (size_t)S * k,
                               jb->b_map ? jb->b_map + (size_t)S * k : NULL);
@@ -381,13 +408,13 @@ static void *band_worker(void *arg) {
 
 int or_solve_band(int m, const double *mic, double c0, int n, double L, double z0,
                   double cx, double cy, int K, const double *freq, const double *csm,
-                  double eps, int eps_mode, int sweeps, int full_grid,
+                  double eps, int eps_mode, int sweeps, int flags,
                   int *n_keep, int *keep, double *x_map, double *b_map, int n_threads) {
     if (K < 1) return OR_OK;
     if (n_threads < 1) n_threads = 1;
     if (n_threads > K) n_threads = K;
     band_job jb = {m, mic, c0, n, L, z0, cx, cy, K, freq, csm, eps, eps_mode, sweeps,
-                   full_grid, n_keep, keep, x_map, b_map, 0, OR_OK, PTHREAD_MUTEX_INITIALIZER};
+                   flags, n_keep, keep, x_map, b_map, 0, OR_OK, PTHREAD_MUTEX_INITIALIZER};
     pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)n_threads);
     if (!th) return OR_ENOMEM;
     for (int t = 0; t < n_threads; t++) pthread_create(&th[t], NULL, band_worker, &jb);

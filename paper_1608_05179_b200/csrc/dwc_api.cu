@@ -183,7 +183,7 @@ dwc_status check_params(const dwc_params *p) {
     if (!(p->epsilon > 0.0) || !finite(p->epsilon)) return fail(DWC_EINVAL, "epsilon must be > 0");
     if (p->eps_mode != 0 && p->eps_mode != 1) return fail(DWC_EINVAL, "eps_mode must be 0 or 1");
     if (p->sweeps < 1) return fail(DWC_EINVAL, "sweeps must be >= 1");
-    if (p->flags & ~DWC_FULL_GRID) return fail(DWC_EINVAL, "unknown flags 0x%x", p->flags);
+    if (p->flags & ~(DWC_FULL_GRID | DWC_CUBIC)) return fail(DWC_EINVAL, "unknown flags 0x%x", p->flags);
     return DWC_OK;
 }
 
@@ -286,7 +286,7 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
                       (double *)ctx->herm.p, b, st));
     ev(ctx, 1, st);
     // S3+S4
-    LAUNCH(launch_compress(n, n_bins, b, p->epsilon, p->eps_mode, (p->flags & DWC_FULL_GRID) ? 1 : 0,
+    LAUNCH(launch_compress(n, n_bins, b, p->epsilon, p->eps_mode, (p->flags & DWC_FULL_GRID) ? 1 : 0, (p->flags & DWC_CUBIC) ? 3 : 1,
                            n_keep, keep_idx, nullptr, (int *)ctx->flag.p, st));
     ev(ctx, 2, st);
     // the single device->host read: kept counts (+ error flags)
@@ -548,7 +548,7 @@ dwc_status dwc_compress(dwc_ctx *ctx, const dwc_grid *grid, const dwc_params *p,
     cudaStream_t st = (cudaStream_t)cuda_stream;
     int launches = 0;
     if ((s = ensure(ctx, ctx->flag, 64))) return s;
-    LAUNCH(launch_compress(grid->n, n_bins, b_map, p->epsilon, p->eps_mode, (p->flags & DWC_FULL_GRID) ? 1 : 0,
+    LAUNCH(launch_compress(grid->n, n_bins, b_map, p->epsilon, p->eps_mode, (p->flags & DWC_FULL_GRID) ? 1 : 0, (p->flags & DWC_CUBIC) ? 3 : 1,
                            n_keep, keep_idx, level, (int *)ctx->flag.p, st));
     return DWC_OK;
 }

@@ -42,9 +42,10 @@ int launch_hermitize(int M, int n_bins, const double *csm, double *H, cudaStream
 int launch_das(const Geo &g, const double *dist, const double *amp, int n_bins,
                const double *freq, const double *csm_half, double *b, cudaStream_t st);
 
-// S3+S4: compaction of kept nodes.  flag (dev int): bit 1 set when b has a non-finite value.
+// S3+S4: compaction of kept nodes.  order 1: linear predictor (R7), 3: cubic (R19).
+// flag (dev int): bit 1 set when b has a non-finite value.
 int launch_compress(int n, int n_bins, const double *b, double eps, int eps_mode, int full_grid,
-                    int32_t *n_keep, int32_t *keep_idx, uint8_t *level, int *flag,
+                    int order, int32_t *n_keep, int32_t *keep_idx, uint8_t *level, int *flag,
                     cudaStream_t st);
 
 // Per-bin layout of the compressed systems, built on the host after n_keep is known.

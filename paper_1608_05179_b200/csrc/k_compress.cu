@@ -5,7 +5,8 @@
 // independent and the whole transform is ONE pass over the grid: node (r,c) belongs to
 // level l = J - min(v2(r), v2(c), J) (v2 = 2-adic valuation, v2(0) = inf); its detail is
 // b - interp(b on G^(l-1)) with the linear stencil of reading R7 (interior midpoint, right
-// edge linear extrapolation, else constant).  All arithmetic is fp64 with explicit
+// edge linear extrapolation, else constant) or the 4-point cubic stencil of reading R19
+// (DWC_CUBIC; Lagrange through the 4 nearest coarse nodes, linear fallback).  All arithmetic is fp64 with explicit
 // round-to-nearest intrinsics (no FMA contraction) in exactly the order of the oracle's
 // definition, so the same b gives the same keep set bit for bit.
 //
@@ -36,30 +37,55 @@ __device__ __forceinline__ int taps1d(int i, int h, int n, int *pos, double *w) 
     return 1;
 }
 
+// 1-D taps of the 4-point predictor (reading R19), ascending positions; weights k/16 exact.
+__device__ __forceinline__ int taps1d_cubic(int i, int h, int n, int *pos, double *w) {
+    const int H = 2 * h;
+    if (i % H == 0) { pos[0] = i; w[0] = 1.0; return 1; }
+    int o0, o1, o2, o3;
+    double w0, w1, w2, w3;
+    if (i - 3 * h >= 0 && i + 3 * h <= n - 1) {
+        o0 = -3; o1 = -1; o2 = 1; o3 = 3; w0 = -1.0; w1 = 9.0; w2 = 9.0; w3 = -1.0;
+    } else if (i - 3 * h < 0 && i + 5 * h <= n - 1) {
+        o0 = -1; o1 = 1; o2 = 3; o3 = 5; w0 = 5.0; w1 = 15.0; w2 = -5.0; w3 = 1.0;
+    } else if (i + h <= n - 1 && i + 3 * h > n - 1 && i - 5 * h >= 0) {
+        o0 = -5; o1 = -3; o2 = -1; o3 = 1; w0 = 1.0; w1 = -5.0; w2 = 15.0; w3 = 5.0;
+    } else if (i + h > n - 1 && i - 7 * h >= 0) {
+        o0 = -7; o1 = -5; o2 = -3; o3 = -1; w0 = -5.0; w1 = 21.0; w2 = -35.0; w3 = 35.0;
+    } else {
+        return taps1d(i, h, n, pos, w);
+    }
+    pos[0] = i + o0 * h; pos[1] = i + o1 * h; pos[2] = i + o2 * h; pos[3] = i + o3 * h;
+    w[0] = w0 / 16.0; w[1] = w1 / 16.0; w[2] = w2 / 16.0; w[3] = w3 / 16.0;
+    return 4;
+}
+
 __device__ __forceinline__ int level_of(int r, int c, int J) {
     const int vr = r == 0 ? J : min(__ffs(r) - 1, J);
     const int vc = c == 0 ? J : min(__ffs(c) - 1, J);
     return J - min(vr, vc);
 }
 
-// detail d = b - pred at a level >= 1 node; t_a = sum_q w_q * b[r_a][c_q], pred = sum_a w_a t_a
+// detail d = b - pred at a level >= 1 node; t_a = sum_q w_q * b[r_a][c_q], pred = sum_a w_a t_a,
+// both sums left to right, every product and sum rounded (the oracle's order)
+template <int kOrder>
 __device__ __forceinline__ double detail_at(const double *__restrict__ b, int n, int r, int c,
                                             int lev, int J) {
     const int h = 1 << (J - lev);
-    int rp[2], cp[2];
-    double rw[2], cw[2];
-    const int nr = taps1d(r, h, n, rp, rw);
-    const int nc = taps1d(c, h, n, cp, cw);
+    int rp[4], cp[4];
+    double rw[4], cw[4];
+    const int nr = kOrder == 3 ? taps1d_cubic(r, h, n, rp, rw) : taps1d(r, h, n, rp, rw);
+    const int nc = kOrder == 3 ? taps1d_cubic(c, h, n, cp, cw) : taps1d(c, h, n, cp, cw);
     double pred = 0.0;
     for (int a = 0; a < nr; a++) {
         double t = __dmul_rn(cw[0], b[(size_t)rp[a] * n + cp[0]]);
-        if (nc == 2) t = __dadd_rn(t, __dmul_rn(cw[1], b[(size_t)rp[a] * n + cp[1]]));
+        for (int q = 1; q < nc; q++) t = __dadd_rn(t, __dmul_rn(cw[q], b[(size_t)rp[a] * n + cp[q]]));
         const double v = __dmul_rn(rw[a], t);
         pred = (a == 0) ? v : __dadd_rn(pred, v);
     }
     return __dsub_rn(b[(size_t)r * n + c], pred);
 }
 
+template <int kOrder>
 __global__ void __launch_bounds__(kCmpThreads)
 compress_kernel(int n, const double *__restrict__ bmaps, double eps, int eps_mode, int full_grid,
                 int32_t *__restrict__ n_keep, int32_t *__restrict__ keep_idx,
@@ -105,7 +131,7 @@ compress_kernel(int n, const double *__restrict__ bmaps, double eps, int eps_mod
             const int lev = level_of(r, c, J);
             if (level) level[(size_t)bin * S + s] = (uint8_t)lev;
             if (full_grid || lev == 0) kp = true;
-            else if (!degenerate) kp = fabs(detail_at(b, n, r, c, lev, J)) >= eps_eff;
+            else if (!degenerate) kp = fabs(detail_at<kOrder>(b, n, r, c, lev, J)) >= eps_eff;
         }
         const unsigned bal = __ballot_sync(0xffffffffu, kp);
         if (lane == 0) wcount[warp] = __popc(bal);
@@ -130,10 +156,14 @@ compress_kernel(int n, const double *__restrict__ bmaps, double eps, int eps_mod
 }
 
 int launch_compress(int n, int n_bins, const double *b, double eps, int eps_mode, int full_grid,
-                    int32_t *n_keep, int32_t *keep_idx, uint8_t *level, int *flag,
+                    int order, int32_t *n_keep, int32_t *keep_idx, uint8_t *level, int *flag,
                     cudaStream_t st) {
-    compress_kernel<<<n_bins, kCmpThreads, 0, st>>>(n, b, eps, eps_mode, full_grid, n_keep,
-                                                     keep_idx, level, flag);
+    if (order == 3)
+        compress_kernel<3><<<n_bins, kCmpThreads, 0, st>>>(n, b, eps, eps_mode, full_grid, n_keep, keep_idx, level,
+                                                            flag);
+    else
+        compress_kernel<1><<<n_bins, kCmpThreads, 0, st>>>(n, b, eps, eps_mode, full_grid, n_keep, keep_idx, level,
+                                                            flag);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

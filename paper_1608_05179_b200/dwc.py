@@ -15,6 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("DWC_LIB", os.path.join(_HERE, "libdwc.so"))   # override: experiments only
 
 DWC_FULL_GRID = 1
+DWC_CUBIC = 2
 STATUS = {0: "DWC_OK", -1: "DWC_EINVAL", -2: "DWC_ESINGULAR", -3: "DWC_ENUMERIC",
           -4: "DWC_ENOMEM", -5: "DWC_ECUDA", -6: "DWC_ESTATE"}
 
@@ -120,6 +121,12 @@ class Geometry:
         return Grid(int(self.n), float(self.side_len), float(self.z0), float(self.cx), float(self.cy))
 
 
+def _flags(full_grid: bool, order: int) -> int:
+    if order not in (1, 3):
+        raise ValueError("order must be 1 (linear predictor) or 3 (cubic)")
+    return (DWC_FULL_GRID if full_grid else 0) | (DWC_CUBIC if order == 3 else 0)
+
+
 def _stream(stream) -> int:
     import torch
     s = torch.cuda.current_stream() if stream is None else stream
@@ -158,7 +165,7 @@ class Context:
 
     # ---- hot path ---------------------------------------------------------------
     def solve_band(self, geom: Geometry, freqs: Sequence[float], csm, epsilon: float, sweeps: int,
-                   eps_mode: int = 0, full_grid: bool = False, want_b: bool = False, out=None,
+                   eps_mode: int = 0, full_grid: bool = False, want_b: bool = False, out=None, order: int = 1,
                    stream=None):
         """Batched S0..S8 on device tensors.  csm: cuda complex128 [K,M,M].
         Returns dict(n_keep int32[K], keep_idx int32[K,S], x_map float32[K,S], b_map, warn)."""
@@ -175,7 +182,7 @@ class Context:
                    "b_map": torch.empty((K, S), dtype=torch.float64, device=dev) if want_b else None}
         warn = np.zeros(K, dtype=np.uint32)
         arr, grid = geom.c_array(), geom.c_grid()
-        prm = Params(float(epsilon), int(eps_mode), int(sweeps), DWC_FULL_GRID if full_grid else 0)
+        prm = Params(float(epsilon), int(eps_mode), int(sweeps), _flags(full_grid, order))
         _check(lib().dwc_solve_band(
             self._h, C.byref(arr), C.byref(grid), C.byref(prm), K, freqs.ctypes.data,
             _dev(csm, torch.complex128, "csm"), _dev(out["n_keep"], torch.int32, "n_keep"),
@@ -186,7 +193,7 @@ class Context:
         return out
 
     def solve_band_host(self, geom: Geometry, freqs, csm, epsilon: float, sweeps: int, eps_mode: int = 0,
-                        full_grid: bool = False, want_b: bool = False, out=None, stream=None):
+                        full_grid: bool = False, want_b: bool = False, out=None, stream=None, order: int = 1):
         """Same as solve_band with host buffers (numpy or CPU tensors, pinned or not); the
         host<->device copies happen inside the C call, which returns when results are on the host."""
         import torch
@@ -202,7 +209,7 @@ class Context:
                    "b_map": torch.empty((K, S), dtype=torch.float64) if want_b else None}
         warn = np.zeros(K, dtype=np.uint32)
         arr, grid = geom.c_array(), geom.c_grid()
-        prm = Params(float(epsilon), int(eps_mode), int(sweeps), DWC_FULL_GRID if full_grid else 0)
+        prm = Params(float(epsilon), int(eps_mode), int(sweeps), _flags(full_grid, order))
         csm = csm.contiguous()
         _check(lib().dwc_solve_band_host(
             self._h, C.byref(arr), C.byref(grid), C.byref(prm), K, freqs.ctypes.data, csm.data_ptr(),
@@ -231,7 +238,7 @@ class Context:
                              _dev(csm, torch.complex128, "csm"), _dev(b, torch.float64, "b"), _stream(stream)))
         return b
 
-    def compress(self, geom: Geometry, b_map, epsilon: float, eps_mode: int = 0, full_grid: bool = False,
+    def compress(self, geom: Geometry, b_map, epsilon: float, eps_mode: int = 0, full_grid: bool = False, order: int = 1,
                  want_level: bool = False, stream=None):
         import torch
         K = b_map.shape[0]
@@ -239,7 +246,7 @@ class Context:
         keep = torch.empty((K, geom.S), dtype=torch.int32, device=b_map.device)
         lev = torch.empty((K, geom.S), dtype=torch.uint8, device=b_map.device) if want_level else None
         grid = geom.c_grid()
-        prm = Params(float(epsilon), int(eps_mode), 1, DWC_FULL_GRID if full_grid else 0)
+        prm = Params(float(epsilon), int(eps_mode), 1, _flags(full_grid, order))
         _check(lib().dwc_compress(self._h, C.byref(grid), C.byref(prm), K, _dev(b_map, torch.float64, "b_map"),
                                   _dev(nk, torch.int32, "n_keep"), _dev(keep, torch.int32, "keep_idx"),
                                   _dev(lev, torch.uint8, "level") if lev is not None else None, _stream(stream)))

@@ -93,13 +93,13 @@ def test_das_odd_sizes_and_non_hermitian(ctx, torch_cuda, oracle_lib, m):
 
 
 # ---------------------------------------------------------------------------- S3/S4
-def _compress_both(ctx, torch, g, bmaps, eps, mode=0, full=False):
+def _compress_both(ctx, torch, g, bmaps, eps, mode=0, full=False, order=1):
     nk, keep, lev = ctx.compress(g, torch.from_numpy(np.ascontiguousarray(bmaps)).cuda(), eps, mode, full,
-                                 want_level=True)
+                                 order=order, want_level=True)
     nk, keep, lev = nk.cpu().numpy(), keep.cpu().numpy(), lev.cpu().numpy()
     import oracle as orc
     for k in range(bmaps.shape[0]):
-        rk, rlev, _, _ = orc.compress(g.n, bmaps[k], eps, mode, full)
+        rk, rlev, _, _ = orc.compress(g.n, bmaps[k], eps, mode, full, order=order)
         assert nk[k] == len(rk)
         assert np.array_equal(keep[k, : nk[k]], rk)
         assert np.all(keep[k, nk[k]:] == -1)
@@ -121,8 +121,21 @@ def test_compress_bit_exact_on_oracle_maps(ctx, torch_cuda, oracle_lib):
     assert np.all(nk == g.S)
 
 
-@pytest.mark.parametrize("n", [2, 3, 5, 6, 8, 17, 33, 64, 101])
-def test_compress_edge_grids(ctx, torch_cuda, n):
+@pytest.mark.parametrize("order", [1, 3])
+def test_compress_cubic_bit_exact_on_oracle_maps(ctx, torch_cuda, oracle_lib, order):
+    """NEXT-1: the cubic (4-point) predictor, same stage protocol (bit-exact keep sets)."""
+    torch = torch_cuda
+    for cfgname in ("cfg1", "cfg2"):
+        band = synth.make_band(cfgname)
+        g = geom_of(band)
+        bm = np.stack([oracle_lib.das(*oracle_args(g), f, c) for f, c in zip(band.freqs, band.csm)])
+        for eps in [band.cfg.epsilon, 0.002, 0.05]:
+            _compress_both(ctx, torch, g, bm, eps, order=order)
+
+
+@pytest.mark.parametrize("order", [1, 3])
+@pytest.mark.parametrize("n", [2, 3, 5, 6, 8, 17, 20, 33, 64, 101])
+def test_compress_edge_grids(ctx, torch_cuda, n, order):
     """Dyadic and non-dyadic N, tiny grids, random maps with ties, constant and zero maps."""
     torch = torch_cuda
     from paper_1608_05179_b200 import Geometry
@@ -132,8 +145,8 @@ def test_compress_edge_grids(ctx, torch_cuda, n):
             np.round(rng.random(n * n) * 4) / 4]          # many exact ties at |d| == eps_eff
     bm = np.stack(maps)
     for eps in [0.125, 0.25, 0.01]:
-        _compress_both(ctx, torch, g, bm, eps)
-    _compress_both(ctx, torch, g, bm, 0.25, mode=1)
+        _compress_both(ctx, torch, g, bm, eps, order=order)
+    _compress_both(ctx, torch, g, bm, 0.25, mode=1, order=order)
 
 
 # ---------------------------------------------------------------------------- S5
@@ -202,17 +215,17 @@ def test_gs_parity_on_oracle_system(ctx, torch_cuda, oracle_lib, nk, sweeps):
 
 
 # ---------------------------------------------------------------------------- end to end
-def _e2e(ctx, torch, oracle_lib, band, sweeps=None, full=False, check_b=True):
+def _e2e(ctx, torch, oracle_lib, band, sweeps=None, full=False, check_b=True, order=1):
     cfg = band.cfg
     g = geom_of(band)
     sw = sweeps or cfg.sweeps
     out = ctx.solve_band(g, band.freqs, torch.from_numpy(band.csm).cuda(), cfg.epsilon, sw, cfg.eps_mode,
-                         full_grid=full, want_b=True)
+                         full_grid=full, want_b=True, order=order)
     nk = out["n_keep"].cpu().numpy()
     keep = out["keep_idx"].cpu().numpy()
     x = out["x_map"].cpu().numpy()
     bm = out["b_map"].cpu().numpy()
-    rnk, rkeep, rx, rb = oracle_lib.solve_band_cfg(band, sweeps=sw, full_grid=full)
+    rnk, rkeep, rx, rb = oracle_lib.solve_band_cfg(band, sweeps=sw, full_grid=full, order=order)
     for k in range(len(band.freqs)):
         assert rel_l2(bm[k], rb[k]) < TOL_B
         assert nk[k] == rnk[k], (k, nk[k], rnk[k])
@@ -231,6 +244,11 @@ def test_e2e_cfg1_compressed_and_full(ctx, torch_cuda, oracle_lib):
 
 def test_e2e_cfg2_all_bins(ctx, torch_cuda, oracle_lib):
     _e2e(ctx, torch_cuda, oracle_lib, synth.make_band("cfg2"))
+
+
+def test_e2e_cfg2_cubic_predictor(ctx, torch_cuda, oracle_lib):
+    """NEXT-1 end to end: the cubic predictor changes the kept set; every tolerance holds."""
+    _e2e(ctx, torch_cuda, oracle_lib, synth.make_band("cfg2"), order=3)
 
 
 def test_e2e_cfg3_strided_bins(ctx, torch_cuda, oracle_lib):

@@ -165,3 +165,114 @@ def test_eq19_error_bound(oracle_lib):
             pred = itp(np.stack([rr, cc], axis=1).astype(float))
             rec[rr, cc] = np.where(kept[rr, cc], b[rr, cc], pred)
         assert np.max(np.abs(rec - b)) <= 10 * ee
+
+
+# ---------------------------------------------------------------------------------------
+# NEXT-1: the 4-point (cubic, Deslauriers-Dubuc family)
+# interpolating predictor, reading R19.
+
+def _coarse_counts(n, J):
+    """Per-axis number of G^j nodes (multiples of 2^(J-j) in [0, n-1])."""
+    return [(n - 1) // (1 << (J - j)) + 1 for j in range(J + 1)]
+
+
+@pytest.mark.parametrize("n", [21, 50, 81, 101])
+def test_cubic_reproduces_bicubic_maps(oracle_lib, n):
+    """4-point Lagrange interpolation is exact for cubics: details vanish exactly at every
+    level whose coarse lattice has >= 4 nodes per axis (integer bicubic map: all values,
+    weights k/16 and partial sums are exact in fp64).  Bilinear maps vanish everywhere
+    (the linear fallback of the coarsest levels is exact for them too)."""
+    J = oracle_lib.max_level(n)
+    r, c = np.meshgrid(np.arange(n, dtype=float), np.arange(n, dtype=float), indexing="ij")
+    b = (2 * c ** 3 - 3 * c ** 2 + c - 7) * (r ** 3 + 5 * r - 2)
+    d, lv = oracle_lib.wavelet_details(n, b.ravel(), order=3)
+    cnt = _coarse_counts(n, J)
+    full = [l for l in range(1, J + 1) if cnt[l - 1] >= 4]
+    assert full, "test grid too small"
+    for l in full:
+        assert np.all(d[lv == l] == 0.0), (n, l)
+    lo = [l for l in range(1, J + 1) if cnt[l - 1] < 4]
+    assert any(np.any(d[lv == l] != 0.0) for l in lo)   # the linear fallback is not exact for cubics
+    bl = 7.0 + 3.0 * r - 5.0 * c + 2.0 * r * c
+    d2, _ = oracle_lib.wavelet_details(n, bl.ravel(), order=3)
+    assert np.all(d2 == 0.0)
+
+
+def _lagrange_1d(f, i, h, n):
+    """Independent route: numpy.polyfit through the 4 nearest coarse nodes (the node choice
+    is reading R19; the weights come from the library fit), or None when fewer than 4."""
+    cand = [i + k * h for k in (-7, -5, -3, -1, 1, 3, 5, 7) if 0 <= i + k * h <= n - 1]
+    if len(cand) < 4:
+        return None
+    near = sorted(sorted(cand, key=lambda p: (abs(p - i), p))[:4])
+    # R19 prefers the symmetric set, then the set shifted away from the nearer boundary
+    xs = np.array(near, dtype=float) - i
+    return lambda vals: np.polyval(np.polyfit(xs, vals, 3), 0.0), near
+
+
+@pytest.mark.parametrize("n", [13, 21, 40])
+def test_cubic_details_match_polyfit(oracle_lib, n):
+    """On random maps the cubic details equal b - (tensor 4-point polynomial fit: rows
+    first, then the column) to 1e-9, at every node where both axes have 4 coarse nodes."""
+    rng = np.random.default_rng(n)
+    b = rng.standard_normal((n, n))
+    d, lv = oracle_lib.wavelet_details(n, b.ravel(), order=3)
+    d = d.reshape(n, n)
+    lv = lv.reshape(n, n)
+    J = oracle_lib.max_level(n)
+    checked = 0
+    for r in range(n):
+        for c in range(n):
+            l = int(lv[r, c])
+            if l == 0:
+                continue
+            h = 1 << (J - l)
+            on_r, on_c = r % (2 * h) == 0, c % (2 * h) == 0
+            fr = None if on_r else _lagrange_1d(None, r, h, n)
+            fc = None if on_c else _lagrange_1d(None, c, h, n)
+            if (not on_r and fr is None) or (not on_c and fc is None):
+                continue
+            rows = [r] if on_r else fr[1]
+            cols = [c] if on_c else fc[1]
+            t = [b[rr, c] if on_c else fc[0](b[rr, cols]) for rr in rows]
+            pred = t[0] if on_r else fr[0](np.array(t))
+            assert abs(d[r, c] - (b[r, c] - pred)) < 1e-9, (n, r, c)
+            checked += 1
+    assert checked > n * n // 4
+
+
+def test_cubic_edge_weights_closed_form(oracle_lib):
+    """One-sided 4-point weights (R19) at each edge of a 1-D-varying map: a single unit
+    spike at coarse node p gives detail -w_p at the fine node (Lagrange basis values)."""
+    n = 21   # J = 4; finest level h = 1, coarse stride 2
+    cases = {  # fine node i -> {coarse node: weight}
+        1: {0: 5 / 16, 2: 15 / 16, 4: -5 / 16, 6: 1 / 16},        # left edge {-1,1,3,5}
+        9: {6: -1 / 16, 8: 9 / 16, 10: 9 / 16, 12: -1 / 16},      # interior
+        19: {14: 1 / 16, 16: -5 / 16, 18: 15 / 16, 20: 5 / 16},   # right edge {-5,-3,-1,1}
+    }
+    for i, wts in cases.items():
+        for p, w in wts.items():
+            b = np.zeros((n, n))
+            b[:, p] = 1.0                       # constant along rows: the row rule is exact
+            d, _ = oracle_lib.wavelet_details(n, b.ravel(), order=3)
+            assert d.reshape(n, n)[0, i] == -w, (i, p)
+    # extrapolation past the last coarse node {-7,-5,-3,-1}: N = 20 -> node 19 (h = 1)
+    n = 20
+    for p, w in {12: -5 / 16, 14: 21 / 16, 16: -35 / 16, 18: 35 / 16}.items():
+        b = np.zeros((n, n))
+        b[:, p] = 1.0
+        d, _ = oracle_lib.wavelet_details(n, b.ravel(), order=3)
+        assert d.reshape(n, n)[0, 19] == -w, p
+
+
+def test_cubic_keeps_fewer_points_on_smooth_maps(oracle_lib):
+    """The point of a higher-order predictor: on a smooth beam-like map
+    the cubic details are smaller, so the same relative eps keeps fewer nodes."""
+    n = 81
+    y, x = np.meshgrid(np.linspace(-1, 1, n), np.linspace(-1, 1, n), indexing="ij")
+    b = np.exp(-((x - 0.2) ** 2 + y ** 2) / 0.08) + 0.5 * np.exp(-((x + 0.3) ** 2 + (y - 0.1) ** 2) / 0.05)
+    k1, *_ = oracle_lib.compress(n, b.ravel(), 0.005, order=1)
+    k3, *_ = oracle_lib.compress(n, b.ravel(), 0.005, order=3)
+    assert len(k3) < len(k1)
+    g0 = np.flatnonzero(oracle_lib.wavelet_details(n, b.ravel(), order=3)[1] == 0)
+    assert set(g0) <= set(k3)
