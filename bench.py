@@ -173,7 +173,13 @@ def run_ours(args, cfg):
         band = synth.make_band(cfg, bins=shard_bins(cfg.n_bins, rank, world))
     K = len(band.freqs)
     geom = Geometry(band.mic_xyz, cfg.n, cfg.side_len, cfg.z0, cfg.c0, cfg.cx, cfg.cy)
-    csm_dev = torch.from_numpy(band.csm).to(dev)
+    snapshots = args.input == "snapshots"
+    if snapshots:   # NEXT-3: the CSMs are formed on the device from the snapshot spectra (Eq. 1)
+        snap_np = synth.make_snapshots(cfg, seed=rank if (args.scaling == "weak" or world == 1) else 0,
+                                       bins=band.bins)
+        snap_dev = torch.from_numpy(snap_np).to(dev)
+    else:
+        csm_dev = torch.from_numpy(band.csm).to(dev)
     ctx = Context(dev.index)
     ctx.set_timing(True)
     stream = torch.cuda.current_stream(dev)
@@ -182,8 +188,12 @@ def run_ours(args, cfg):
     strong = args.scaling == "strong" and world > 1
 
     def step():
-        out = ctx.solve_band(geom, band.freqs, csm_dev, cfg.epsilon, cfg.sweeps, cfg.eps_mode,
-                             full_grid=cfg.full_grid, order=args.order, stream=stream)
+        if snapshots:
+            out = ctx.solve_band_snapshots(geom, band.freqs, snap_dev, cfg.epsilon, cfg.sweeps, cfg.eps_mode,
+                                           full_grid=cfg.full_grid, order=args.order, stream=stream)
+        else:
+            out = ctx.solve_band(geom, band.freqs, csm_dev, cfg.epsilon, cfg.sweeps, cfg.eps_mode,
+                                 full_grid=cfg.full_grid, order=args.order, stream=stream)
         if strong:
             # the one collective: maps + keep bitmasks + counts, all ranks
             mask = ctx.keep_mask(out["n_keep"], out["keep_idx"], stream=stream)
@@ -239,12 +249,25 @@ def run_ours(args, cfg):
     launches = int(sum(s["launches"] for s in st_list))
 
     # e2e through the C ABI with host buffers (pinned), copies inside the timed region
-    csm_host = torch.from_numpy(band.csm).pin_memory()
     h_out = {"n_keep": torch.empty(K, dtype=torch.int32).pin_memory(),
              "keep_idx": torch.empty((K, S), dtype=torch.int32).pin_memory(),
              "x_map": torch.empty((K, S), dtype=torch.float32).pin_memory(), "b_map": None}
-    ctx.solve_band_host(geom, band.freqs, csm_host, cfg.epsilon, cfg.sweeps, cfg.eps_mode, cfg.full_grid,
-                        out=h_out, stream=stream, order=args.order)
+    if snapshots:
+        snap_host = torch.from_numpy(snap_np).pin_memory()
+
+        def e2e_call():
+            snap_dev.copy_(snap_host, non_blocking=True)
+            out = ctx.solve_band_snapshots(geom, band.freqs, snap_dev, cfg.epsilon, cfg.sweeps, cfg.eps_mode,
+                                           full_grid=cfg.full_grid, order=args.order, stream=stream)
+            for key in ("n_keep", "keep_idx", "x_map"):
+                h_out[key].copy_(out[key], non_blocking=True)
+    else:
+        csm_host = torch.from_numpy(band.csm).pin_memory()
+
+        def e2e_call():
+            ctx.solve_band_host(geom, band.freqs, csm_host, cfg.epsilon, cfg.sweeps, cfg.eps_mode, cfg.full_grid,
+                                out=h_out, stream=stream, order=args.order)
+    e2e_call()
     e2e_ms = []
     for it in range(args.steps):
         flush.zero_()
@@ -254,8 +277,7 @@ def run_ours(args, cfg):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        ctx.solve_band_host(geom, band.freqs, csm_host, cfg.epsilon, cfg.sweeps, cfg.eps_mode, cfg.full_grid,
-                            out=h_out, stream=stream, order=args.order)
+        e2e_call()
         e1.record(stream)
         torch.cuda.synchronize(dev)
         e2e_ms.append(e0.elapsed_time(e1))
@@ -265,7 +287,7 @@ def run_ours(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ems = float(t.item())
     e2e_value = ((K * world) if args.scaling == "weak" else cfg.n_bins) / (ems / 1000.0)
-    h2d = band.csm.nbytes
+    h2d = snap_np.nbytes if snapshots else band.csm.nbytes
     d2h = K * 4 + K * S * 4 + K * S * 4
 
     if rank == 0:
@@ -279,7 +301,9 @@ def run_ours(args, cfg):
             "dtype": "f32 (PSF + Gauss-Seidel); f64 (DAS map + wavelet threshold)", "data": "synthetic",
             "config": {"workload": workload_desc(cfg), "bins_per_gpu": K,
                        "predictor": "cubic (R19)" if args.order == 3 else "linear (R7)", "parallelism": f"bins-dp{world}",
-                       "l2_flush": "256 MiB write between timed steps", "inputs": "CSMs resident in HBM"},
+                       "l2_flush": "256 MiB write between timed steps",
+                       "inputs": ("snapshot spectra resident in HBM, CSM formed on device (Eq. 1)" if snapshots
+                                  else "CSMs resident in HBM")},
             "psf_stream_gbs": achieved,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel": "gs_kernel",
@@ -312,6 +336,8 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--ref-bins", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--input", default="csm", choices=["csm", "snapshots"],
+                    help="csm: CSMs resident in HBM (default); snapshots: snapshot spectra, Eq. 1 on device")
     ap.add_argument("--order", type=int, default=1, choices=[1, 3],
                     help="S3 predictor: 1 linear (reading R7, default), 3 cubic (R19)")
     args = ap.parse_args()

@@ -122,7 +122,22 @@ DWC_API dwc_status dwc_solve_band_host(dwc_ctx *ctx, const dwc_array *arr, const
                                const double *csm, int32_t *n_keep, int32_t *keep_idx,
                                float *x_map, double *b_map, uint32_t *warn, void *cuda_stream);
 
+/* The same path from the microphones' snapshot spectra: the CSM of each
+ * bin is formed on the device by Eq. 1, C = (1/I) sum_i p_i p_i^H, in fp64,
+ * and consumed by the DAS without leaving the GPU.  snap dev complex128
+ * [n_bins][m][n_snap] (interleaved re,im; row = microphone, snapshots contiguous); the other
+ * arguments as dwc_solve_band.  Errors as dwc_solve_band, DWC_EINVAL for n_snap < 1. */
+DWC_API dwc_status dwc_solve_band_snapshots(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid,
+                                    const dwc_params *p, int32_t n_bins, const double *freq_hz,
+                                    int32_t n_snap, const double *snap, int32_t *n_keep, int32_t *keep_idx,
+                                    float *x_map, double *b_map, uint32_t *warn, void *cuda_stream);
+
 /* ---- stage entry points (parity tests feed identical inputs to GPU and oracle) ---- */
+
+/* Eq. 1: CSMs from snapshot spectra.  snap as dwc_solve_band_snapshots; csm dev complex128
+ * [n_bins][m][m] row-major (out), fp64.  Errors: DWC_EINVAL, DWC_ECUDA. */
+DWC_API dwc_status dwc_csm(dwc_ctx *ctx, int32_t m, int32_t n_bins, int32_t n_snap, const double *snap,
+                           double *csm, void *cuda_stream);
 
 /* S1: normalised steering vectors e_s = sqrt(M) g_s/||g_s|| of n_pts nodes (reading R1).
  * idx dev int32[n_pts]; E dev complex128 [n_pts][m] interleaved (out). */

@@ -53,6 +53,7 @@ def lib():
         _lib.or_compress.argtypes = [i, _P, d, i, i, _P, _P, _P, _P, i]
         _lib.or_psf.argtypes = geo + [d, i, _P, _P]
         _lib.or_gs.argtypes = [i, _P, _P, i, _P]
+        _lib.or_csm.argtypes = [i, i, _P, _P]
         _lib.or_solve_bin.argtypes = geo + [d, _P, d, i, i, i, _P, _P, _P, _P]
         _lib.or_solve_band.argtypes = geo + [i, _P, _P, d, i, i, i, _P, _P, _P, _P, i]
     return _lib
@@ -147,6 +148,17 @@ def psf(mic, c0, n, L, z0, cx, cy, freq, keep) -> np.ndarray:
     A = np.zeros((len(keep), len(keep)))
     _chk(lib().or_psf(*g, float(freq), len(keep), _p(keep), _p(A)), "psf")
     return A
+
+
+def csm(snap) -> np.ndarray:
+    """Eq. 1: snap complex128 [M, I] (or [K, M, I]) -> C complex128 [M, M] ([K, M, M])."""
+    snap = np.ascontiguousarray(snap, dtype=np.complex128)
+    if snap.ndim == 3:
+        return np.stack([csm(s) for s in snap])
+    M, I = snap.shape
+    C = np.zeros((M, M), dtype=np.complex128)
+    _chk(lib().or_csm(int(M), int(I), _p(snap), _p(C)), "csm")
+    return C
 
 
 def gs(A, b, sweeps: int) -> np.ndarray:

@@ -306,6 +306,28 @@ int or_psf(int m, const double *mic, double c0, int n, double L, double z0,
 }
 
 /* ------------------------------------------------------------------------ */
+/* Eq. 1, the step before the path:
+ *   C = (1/I) sum_i p_i p_i^H,   p_i = snap[:, i],
+ * snap complex128 [m][I] interleaved (row = microphone), C complex128 [m][m];
+ * sums over i ascending in fp64, then divided by I.                            */
+int or_csm(int m, int I, const double *snap, double *C) {
+    if (m < 1 || I < 1) return OR_EINVAL;
+    for (int a = 0; a < m; a++)
+        for (int b = 0; b < m; b++) {
+            double re = 0.0, im = 0.0;
+            for (int i = 0; i < I; i++) {
+                double pr = snap[2 * ((size_t)a * I + i)], pi = snap[2 * ((size_t)a * I + i) + 1];
+                double qr = snap[2 * ((size_t)b * I + i)], qi = snap[2 * ((size_t)b * I + i) + 1];
+                re += pr * qr + pi * qi;            /* p_a conj(p_b) */
+                im += pi * qr - pr * qi;
+            }
+            C[2 * ((size_t)a * m + b)] = re / (double)I;
+            C[2 * ((size_t)a * m + b) + 1] = im / (double)I;
+        }
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------ */
 /* S7 DAMAS Gauss-Seidel with positivity, Eq. 13-14:
  *   r_i = sum_{j<i} A_ij x_j^(n+1) + sum_{j>=i} A_ij x_j^(n) - b_i
  *   x_i^(n+1) = max(x_i^(n) - r_i / A_ii, 0),   x^0 = 0.

@@ -24,6 +24,7 @@ SOURCES = {
     "k_psf.cu": [],
     "k_gs.cu": [],
     "k_keep.cu": [],
+    "k_csm.cu": [],
 }
 
 

@@ -262,11 +262,12 @@ void ev(dwc_ctx *ctx, int i, cudaStream_t st) {
     if (ctx->timing) cudaEventRecord(ctx->ev[i], st);
 }
 
-// The batched path on device buffers.
+// The batched path on device buffers.  Input: the CSMs (csm) or, when snap != NULL, the
+// snapshot spectra [n_bins][M][n_snap] from which Eq. 1 forms them on the device.
 dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, const dwc_params *p,
                           int n_bins, const double *freq, const double *csm, int32_t *n_keep,
                           int32_t *keep_idx, float *x_map, double *b_map, uint32_t *warn,
-                          cudaStream_t st) {
+                          cudaStream_t st, const double *snap = nullptr, int n_snap = 0) {
     dwc_status s;
     int launches = 0;
     const int M = arr->m, n = grid->n;
@@ -281,7 +282,10 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
         if ((s = ensure(ctx, ctx->bint, sizeof(double) * (size_t)n_bins * S))) return s;
         b = (double *)ctx->bint.p;
     }
-    LAUNCH(launch_hermitize(M, n_bins, csm, (double *)ctx->herm.p, st));
+    if (snap)
+        LAUNCH(launch_csm(M, n_bins, n_snap, snap, (double *)ctx->herm.p, 1, st));   // Eq. 1 -> Ch
+    else
+        LAUNCH(launch_hermitize(M, n_bins, csm, (double *)ctx->herm.p, st));
     LAUNCH(launch_das(G, (double *)ctx->dist.p, (double *)ctx->amp.p, n_bins, (double *)ctx->freq.p,
                       (double *)ctx->herm.p, b, st));
     ev(ctx, 1, st);
@@ -474,6 +478,32 @@ dwc_status dwc_solve_band(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
     if (!csm || !n_keep || !keep_idx || !x_map) return fail(DWC_EINVAL, "NULL device buffer");
     return solve_band_dev(ctx, arr, grid, p, n_bins, freq_hz, csm, n_keep, keep_idx, x_map, b_map, warn,
                           (cudaStream_t)cuda_stream);
+}
+
+dwc_status dwc_solve_band_snapshots(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid,
+                                    const dwc_params *p, int32_t n_bins, const double *freq_hz, int32_t n_snap,
+                                    const double *snap, int32_t *n_keep, int32_t *keep_idx, float *x_map,
+                                    double *b_map, uint32_t *warn, void *cuda_stream) {
+    dwc_status s;
+    if ((s = check_ctx(ctx)) || (s = check_array(arr)) || (s = check_grid(grid)) || (s = check_params(p)) ||
+        (s = check_freqs(n_bins, freq_hz)))
+        return s;
+    if (n_snap < 1) return fail(DWC_EINVAL, "n_snap must be >= 1");
+    if (!snap || !n_keep || !keep_idx || !x_map) return fail(DWC_EINVAL, "NULL device buffer");
+    return solve_band_dev(ctx, arr, grid, p, n_bins, freq_hz, nullptr, n_keep, keep_idx, x_map, b_map, warn,
+                          (cudaStream_t)cuda_stream, snap, n_snap);
+}
+
+dwc_status dwc_csm(dwc_ctx *ctx, int32_t m, int32_t n_bins, int32_t n_snap, const double *snap, double *csm,
+                   void *cuda_stream) {
+    dwc_status s;
+    if ((s = check_ctx(ctx))) return s;
+    if (m < 1 || m > DWC_MAX_MICS || n_bins < 1 || n_snap < 1)
+        return fail(DWC_EINVAL, "m = %d, n_bins = %d, n_snap = %d", m, n_bins, n_snap);
+    if (!snap || !csm) return fail(DWC_EINVAL, "NULL device buffer");
+    int launches = 0;
+    LAUNCH(launch_csm(m, n_bins, n_snap, snap, csm, 0, (cudaStream_t)cuda_stream));
+    return DWC_OK;
 }
 
 dwc_status dwc_solve_band_host(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid,

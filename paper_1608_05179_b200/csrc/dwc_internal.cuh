@@ -38,6 +38,10 @@ int launch_steer(const Geo &g, const double *dist, const double *amp, const doub
 int das_mpad(int M);
 int launch_hermitize(int M, int n_bins, const double *csm, double *H, cudaStream_t st);
 
+// Eq. 1 (k_csm.cu): C_k = P_k P_k^H / I from snapshot spectra snap [n_bins][M][I] complex128.
+// half = 0: full C [n_bins][M][M]; half = 1: the half-Hermitian padded Ch of launch_hermitize.
+int launch_csm(int M, int n_bins, int I, const double *snap, double *out, int half, cudaStream_t st);
+
 // S2: b[k][s] for n_bins bins; freq dev[n_bins]; csm_half = launch_hermitize's output.
 int launch_das(const Geo &g, const double *dist, const double *amp, int n_bins,
                const double *freq, const double *csm_half, double *b, cudaStream_t st);

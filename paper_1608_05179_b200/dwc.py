@@ -72,6 +72,8 @@ def lib() -> C.CDLL:
         L.dwc_psf.argtypes = [P, ap, gp, d, i32, P, P, P]
         L.dwc_gs.argtypes = [P, i32, P, P, i32, P, P]
         L.dwc_keep_mask.argtypes = [P, i32, i32, P, P, P, P]
+        L.dwc_solve_band_snapshots.argtypes = [P, ap, gp, pp, i32, P, i32, P, P, P, P, P, P, P]
+        L.dwc_csm.argtypes = [P, i32, i32, i32, P, P, P]
         L.dwc_keep_unmask.argtypes = [P, i32, i32, P, P, P, P]
         L.dwc_set_timing.argtypes = [P, C.c_int]
         L.dwc_get_stats.argtypes = [P, C.POINTER(Stats)]
@@ -81,6 +83,7 @@ def lib() -> C.CDLL:
         L.dwc_workspace_bytes.restype = C.c_size_t
         for name in ("dwc_create", "dwc_destroy", "dwc_solve_band", "dwc_solve_band_host", "dwc_steer",
                      "dwc_das", "dwc_compress", "dwc_psf", "dwc_gs", "dwc_keep_mask", "dwc_keep_unmask",
+                     "dwc_solve_band_snapshots", "dwc_csm",
                      "dwc_set_timing", "dwc_get_stats"):
             getattr(L, name).restype = C.c_int
         _lib = L
@@ -220,6 +223,41 @@ class Context:
         return out
 
     # ---- stage entry points ---------------------------------------------------------
+    def solve_band_snapshots(self, geom: Geometry, freqs: Sequence[float], snap, epsilon: float, sweeps: int,
+                             eps_mode: int = 0, full_grid: bool = False, want_b: bool = False, order: int = 1,
+                             stream=None):
+        """The path from snapshot spectra (Eq. 1 on the device).  snap: cuda complex128 [K,M,I]."""
+        import torch
+        freqs = np.ascontiguousarray(freqs, dtype=np.float64)
+        K, S = len(freqs), geom.S
+        if snap.dim() != 3 or tuple(snap.shape[:2]) != (K, geom.m):
+            raise ValueError(f"snap shape {tuple(snap.shape)} != {(K, geom.m, 'I')}")
+        dev = snap.device
+        out = {"n_keep": torch.empty(K, dtype=torch.int32, device=dev),
+               "keep_idx": torch.empty((K, S), dtype=torch.int32, device=dev),
+               "x_map": torch.empty((K, S), dtype=torch.float32, device=dev),
+               "b_map": torch.empty((K, S), dtype=torch.float64, device=dev) if want_b else None}
+        warn = np.zeros(K, dtype=np.uint32)
+        arr, grid = geom.c_array(), geom.c_grid()
+        prm = Params(float(epsilon), int(eps_mode), int(sweeps), _flags(full_grid, order))
+        _check(lib().dwc_solve_band_snapshots(
+            self._h, C.byref(arr), C.byref(grid), C.byref(prm), K, freqs.ctypes.data, int(snap.shape[2]),
+            _dev(snap, torch.complex128, "snap"), _dev(out["n_keep"], torch.int32, "n_keep"),
+            _dev(out["keep_idx"], torch.int32, "keep_idx"), _dev(out["x_map"], torch.float32, "x_map"),
+            _dev(out["b_map"], torch.float64, "b_map") if out["b_map"] is not None else None,
+            warn.ctypes.data, _stream(stream)))
+        out["warn"] = warn
+        return out
+
+    def csm(self, snap, stream=None):
+        """Eq. 1 on the device: snap cuda complex128 [K,M,I] -> C complex128 [K,M,M]."""
+        import torch
+        K, M, I = snap.shape
+        out = torch.empty((K, M, M), dtype=torch.complex128, device=snap.device)
+        _check(lib().dwc_csm(self._h, M, K, I, _dev(snap, torch.complex128, "snap"),
+                             _dev(out, torch.complex128, "csm"), _stream(stream)))
+        return out
+
     def steer(self, geom: Geometry, freq: float, idx, stream=None):
         import torch
         idx = idx.to(torch.int32).contiguous()

@@ -208,11 +208,12 @@ def csm_exact(mic_xyz: np.ndarray, src_xyz: np.ndarray, powers: np.ndarray,
     return (g * powers[None, :]) @ g.conj().T
 
 
-def csm_sampled(mic_xyz: np.ndarray, src_xyz: np.ndarray, powers: np.ndarray,
-                freq: float, c0: float, snapshots: int, snr_db: float,
-                rng: np.random.Generator) -> np.ndarray:
-    """Eq. 1 averaged over I snapshots with incoherent CN(0,1) source phasors
-    and white microphone noise at the given SNR."""
+def snapshots_sampled(mic_xyz: np.ndarray, src_xyz: np.ndarray, powers: np.ndarray,
+                      freq: float, c0: float, snapshots: int, snr_db: float,
+                      rng: np.random.Generator) -> np.ndarray:
+    """The I snapshot spectra p_i (M x I complex128) of incoherent CN(0,1) source phasors
+    propagated by Eq. 5-7 plus white microphone noise at the given SNR.
+    Input of the on-device Eq. 1 path (NEXT-3); csm_sampled averages the same draws."""
     g = propagation_vectors(mic_xyz, src_xyz, freq, c0)
     m = g.shape[0]
     ns = g.shape[1]
@@ -223,7 +224,33 @@ def csm_sampled(mic_xyz: np.ndarray, src_xyz: np.ndarray, powers: np.ndarray,
         sigma2 = sig_pow / (10.0 ** (snr_db / 10.0))
         noise = (rng.standard_normal((m, snapshots)) + 1j * rng.standard_normal((m, snapshots))) * math.sqrt(sigma2 / 2.0)
         p = p + noise
+    return p
+
+
+def csm_sampled(mic_xyz: np.ndarray, src_xyz: np.ndarray, powers: np.ndarray,
+                freq: float, c0: float, snapshots: int, snr_db: float,
+                rng: np.random.Generator) -> np.ndarray:
+    """Eq. 1 averaged over I snapshots (the CSM input of the CSM-in path)."""
+    p = snapshots_sampled(mic_xyz, src_xyz, powers, freq, c0, snapshots, snr_db, rng)
     return (p @ p.conj().T) / snapshots
+
+
+def make_snapshots(cfg: "Config | str", seed: int = 0, bins: Optional[Sequence[int]] = None) -> np.ndarray:
+    """Snapshot spectra [K, M, I] of a sampled-CSM config, the same draws make_band averages."""
+    if isinstance(cfg, str):
+        cfg = CONFIGS[cfg]
+    if cfg.csm == "exact":
+        raise ValueError(f"{cfg.name} has an exact CSM (no snapshots)")
+    mics = cfg.mics()
+    allf = cfg.freqs()
+    bins = np.arange(cfg.n_bins) if bins is None else np.asarray(bins, dtype=np.int64)
+    src_idx, src_pow = scene_sources(cfg, seed)
+    src_xyz = grid_node_xyz(cfg.n, cfg.side_len, cfg.z0, cfg.cx, cfg.cy, src_idx)
+    out = np.empty((len(bins), cfg.m, cfg.snapshots), dtype=np.complex128)
+    for j, k in enumerate(bins):
+        rng = np.random.default_rng(np.random.SeedSequence([cfg.cfg_id, seed, int(k)]))
+        out[j] = snapshots_sampled(mics, src_xyz, src_pow, float(allf[k]), cfg.c0, cfg.snapshots, cfg.snr_db, rng)
+    return out
 
 
 @dataclasses.dataclass

@@ -350,3 +350,36 @@ def test_errors(ctx, torch_cuda):
     assert e.value.code == -2
     # the context still works after errors
     ctx.solve_band(g, band.freqs, csm, 0.1, 5)
+
+
+# ---------------------------------------------------------------------------- NEXT-3: Eq. 1 on device
+@pytest.mark.parametrize("m,I", [(16, 1), (13, 37), (64, 1000), (128, 100)])
+def test_csm_parity(ctx, torch_cuda, oracle_lib, m, I):
+    """C = (1/I) sum_i p_i p_i^H in fp64 on the GPU vs the oracle's loops (odd M, ragged I)."""
+    torch = torch_cuda
+    rng = np.random.default_rng(m * 1000 + I)
+    snap = rng.standard_normal((3, m, I)) + 1j * rng.standard_normal((3, m, I))
+    C = ctx.csm(torch.from_numpy(snap).cuda()).cpu().numpy()
+    ref = oracle_lib.csm(snap)
+    assert np.abs(C - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+def test_e2e_from_snapshots_cfg2(ctx, torch_cuda, oracle_lib):
+    """The whole path from snapshot spectra (Eq. 1 on device) vs the oracle's Eq. 1 + path."""
+    torch = torch_cuda
+    bins = [0, 3, 7]
+    band = synth.make_band("cfg2", bins=bins)
+    snap = synth.make_snapshots("cfg2", bins=bins)
+    cfg = band.cfg
+    g = geom_of(band)
+    out = ctx.solve_band_snapshots(g, band.freqs, torch.from_numpy(snap).cuda(), cfg.epsilon, cfg.sweeps,
+                                   want_b=True)
+    import dataclasses
+    ob = dataclasses.replace(band, csm=oracle_lib.csm(snap))
+    rnk, rkeep, rx, rb = oracle_lib.solve_band_cfg(ob)
+    for k in range(len(bins)):
+        assert rel_l2(out["b_map"][k].cpu().numpy(), rb[k]) < TOL_B
+        assert np.array_equal(out["keep_idx"][k].cpu().numpy(), rkeep[k])
+        x = out["x_map"][k].cpu().numpy()
+        assert rel_l2(x, rx[k]) < TOL_X
+        assert abs(x.sum() - rx[k].sum()) <= TOL_P * rx[k].sum()
