@@ -290,6 +290,13 @@ def run_ours(args, cfg):
     h2d = snap_np.nbytes if snapshots else band.csm.nbytes
     d2h = K * 4 + K * S * 4 + K * S * 4
 
+    cvf = None
+    if world == 1 and not args.no_cvf:
+        # compressed-grid vs full-grid DAMAS on the same bins (north_star), scripts/compressed_vs_full.py
+        sys.path.insert(0, os.path.join(ROOT, "scripts"))
+        import compressed_vs_full
+        cvf = compressed_vs_full.measure(ctx)
+        ctx.set_timing(True)
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
@@ -317,6 +324,7 @@ def run_ours(args, cfg):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": ems},
             "gpu_launches": launches,
+            "compressed_vs_full": cvf,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
@@ -336,6 +344,7 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--ref-bins", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cvf", action="store_true", help="skip the compressed-vs-full-grid measurement")
     ap.add_argument("--input", default="csm", choices=["csm", "snapshots"],
                     help="csm: CSMs resident in HBM (default); snapshots: snapshot spectra, Eq. 1 on device")
     ap.add_argument("--order", type=int, default=1, choices=[1, 3],
