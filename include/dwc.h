@@ -80,7 +80,8 @@ typedef struct {
     double epsilon;   /* > 0; relative (eps * max|b|) or absolute */
     int32_t eps_mode; /* 0 = relative, 1 = absolute (reading R6) */
     int32_t sweeps;   /* Gauss-Seidel sweeps >= 1 from x0 = 0 */
-    int32_t flags;    /* DWC_FULL_GRID: keep every node (the paper's "original grid"); DWC_CUBIC */
+    int32_t flags;    /* DWC_FULL_GRID: keep every node (the paper's "original grid"); DWC_CUBIC;
+                         DWC_DIAG_REMOVAL */
 } dwc_params;
 
 #define DWC_FULL_GRID 1
@@ -89,6 +90,11 @@ typedef struct {
  * the 4 nearest coarse nodes, linear rule where fewer than 4 are in reach.  Changes only the
  * compressed index set (and so everything downstream). */
 #define DWC_CUBIC 2
+/* DWC_DIAG_REMOVAL: CSM diagonal removal (reading R20): the DAS map
+ * leaves out the C_mm terms, is normalised by M^2 - M and clamped at 0; the PSF is the
+ * matching A_ij = (|e_i^H e_j|^2 - sum_m |e_mi|^2 |e_mj|^2) / (M^2 - M), clamped at 0.
+ * Uncorrelated microphone noise (a diagonal CSM term) then drops out of the map. */
+#define DWC_DIAG_REMOVAL 4
 #define DWC_MAX_MICS 512
 
 /* Create / destroy a context on CUDA device `device`.  The device must be sm_100
@@ -145,9 +151,9 @@ DWC_API dwc_status dwc_steer(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid 
                      int32_t n_pts, const int32_t *idx, double *E, void *cuda_stream);
 
 /* S2: DAS maps b_k(s) = Re(e_s^H C_k e_s)/M^2 in fp64.  csm dev as in dwc_solve_band;
- * b_map dev double[n_bins*S] (out). */
+ * flags: 0 or DWC_DIAG_REMOVAL; b_map dev double[n_bins*S] (out). */
 DWC_API dwc_status dwc_das(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, int32_t n_bins,
-                   const double *freq_hz, const double *csm, double *b_map, void *cuda_stream);
+                   const double *freq_hz, const double *csm, int32_t flags, double *b_map, void *cuda_stream);
 
 /* S3+S4: wavelet details in fp64 (no FMA contraction, reading R7 stencil) and threshold;
  * b_map dev double[n_bins*S]; n_keep/keep_idx as in dwc_solve_band (out);
@@ -157,9 +163,10 @@ DWC_API dwc_status dwc_compress(dwc_ctx *ctx, const dwc_grid *grid, const dwc_pa
                         int32_t *keep_idx, uint8_t *level, void *cuda_stream);
 
 /* S5: PSF matrix on n_keep nodes, A[i][j] = |e_i^H e_j|^2/M^2, fp32 accurate.
- * keep_idx dev int32[n_keep]; A dev float[n_keep*n_keep] row-major (out). */
+ * keep_idx dev int32[n_keep]; flags: 0 or DWC_DIAG_REMOVAL; A dev float[n_keep*n_keep]
+ * row-major (out). */
 DWC_API dwc_status dwc_psf(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, double freq_hz,
-                   int32_t n_keep, const int32_t *keep_idx, float *A, void *cuda_stream);
+                   int32_t n_keep, const int32_t *keep_idx, int32_t flags, float *A, void *cuda_stream);
 
 /* S7: `sweeps` forward projected Gauss-Seidel sweeps from x0 = 0 on one system.
  * A dev float[n*n] row-major, symmetric (as A~ is, reading R1) with A_ii > 0: only the upper

@@ -47,11 +47,11 @@ def lib():
         _lib.or_rayleigh_beamwidth.restype = d
         _lib.or_spacing_warning.argtypes = [i, _P, d, i, d, d, d]
         _lib.or_steering.argtypes = geo + [d, i, _P, _P]
-        _lib.or_das.argtypes = geo + [d, _P, _P]
+        _lib.or_das.argtypes = geo + [d, _P, _P, i]
         _lib.or_max_level.argtypes = [i]
         _lib.or_wavelet_details.argtypes = [i, _P, _P, _P, i]
         _lib.or_compress.argtypes = [i, _P, d, i, i, _P, _P, _P, _P, i]
-        _lib.or_psf.argtypes = geo + [d, i, _P, _P]
+        _lib.or_psf.argtypes = geo + [d, i, _P, _P, i]
         _lib.or_gs.argtypes = [i, _P, _P, i, _P]
         _lib.or_csm.argtypes = [i, i, _P, _P]
         _lib.or_solve_bin.argtypes = geo + [d, _P, d, i, i, i, _P, _P, _P, _P]
@@ -109,11 +109,12 @@ def steering(mic, c0, n, L, z0, cx, cy, freq, idx) -> np.ndarray:
     return E[..., 0] + 1j * E[..., 1]
 
 
-def das(mic, c0, n, L, z0, cx, cy, freq, csm) -> np.ndarray:
+def das(mic, c0, n, L, z0, cx, cy, freq, csm, dr: bool = False) -> np.ndarray:
+    """Eq. 2; dr: diagonal removal (R20)."""
     mic, g = _geo(mic, c0, n, L, z0, cx, cy)
     csm = np.ascontiguousarray(csm, dtype=np.complex128)
     b = np.zeros(n * n)
-    _chk(lib().or_das(*g, float(freq), _p(csm), _p(b)), "das")
+    _chk(lib().or_das(*g, float(freq), _p(csm), _p(b), int(bool(dr))), "das")
     return b
 
 
@@ -142,11 +143,12 @@ def compress(n: int, b, eps: float, eps_mode: int = 0, full_grid: bool = False, 
     return keep[:nk].copy(), lv, d, float(ee[0])
 
 
-def psf(mic, c0, n, L, z0, cx, cy, freq, keep) -> np.ndarray:
+def psf(mic, c0, n, L, z0, cx, cy, freq, keep, dr: bool = False) -> np.ndarray:
+    """Eq. 10 restricted to keep; dr: the diagonal-removal PSF (R20)."""
     mic, g = _geo(mic, c0, n, L, z0, cx, cy)
     keep = np.ascontiguousarray(keep, dtype=np.int32)
     A = np.zeros((len(keep), len(keep)))
-    _chk(lib().or_psf(*g, float(freq), len(keep), _p(keep), _p(A)), "psf")
+    _chk(lib().or_psf(*g, float(freq), len(keep), _p(keep), _p(A), int(bool(dr))), "psf")
     return A
 
 
@@ -169,11 +171,11 @@ def gs(A, b, sweeps: int) -> np.ndarray:
     return x
 
 
-def _flags(full_grid, order):
-    return (1 if full_grid else 0) | (2 if order == 3 else 0)
+def _flags(full_grid, order, dr=False):
+    return (1 if full_grid else 0) | (2 if order == 3 else 0) | (4 if dr else 0)
 
 
-def solve_bin(mic, c0, n, L, z0, cx, cy, freq, csm, eps, eps_mode, sweeps, full_grid=False, order=1):
+def solve_bin(mic, c0, n, L, z0, cx, cy, freq, csm, eps, eps_mode, sweeps, full_grid=False, order=1, dr=False):
     """-> (keep, x_map fp64[S], b fp64[S])."""
     mic, g = _geo(mic, c0, n, L, z0, cx, cy)
     csm = np.ascontiguousarray(csm, dtype=np.complex128)
@@ -183,12 +185,12 @@ def solve_bin(mic, c0, n, L, z0, cx, cy, freq, csm, eps, eps_mode, sweeps, full_
     x = np.zeros(S)
     b = np.zeros(S)
     _chk(lib().or_solve_bin(*g, float(freq), _p(csm), float(eps), int(eps_mode), int(sweeps),
-                            _flags(full_grid, order), _p(nk), _p(keep), _p(x), _p(b)), "solve_bin")
+                            _flags(full_grid, order, dr), _p(nk), _p(keep), _p(x), _p(b)), "solve_bin")
     return keep[: nk[0]].copy(), x, b
 
 
 def solve_band(mic, c0, n, L, z0, cx, cy, freqs, csm, eps, eps_mode, sweeps,
-               full_grid=False, n_threads: Optional[int] = None, order: int = 1):
+               full_grid=False, n_threads: Optional[int] = None, order: int = 1, dr: bool = False):
     """Batched S0..S8 over K bins on a pthread pool.
     -> (n_keep int32[K], keep int32[K,S] (-1 padded), x_map fp64[K,S], b fp64[K,S])."""
     mic, g = _geo(mic, c0, n, L, z0, cx, cy)
@@ -203,16 +205,17 @@ def solve_band(mic, c0, n, L, z0, cx, cy, freqs, csm, eps, eps_mode, sweeps,
     if n_threads is None:
         n_threads = os.cpu_count() or 1
     _chk(lib().or_solve_band(*g, K, _p(freqs), _p(csm), float(eps), int(eps_mode), int(sweeps),
-                             _flags(full_grid, order), _p(nk), _p(keep), _p(x), _p(b), int(n_threads)),
+                             _flags(full_grid, order, dr), _p(nk), _p(keep), _p(x), _p(b), int(n_threads)),
          "solve_band")
     return nk, keep, x, b
 
 
 def solve_band_cfg(band, n_threads: Optional[int] = None, sweeps: Optional[int] = None,
-                   full_grid: Optional[bool] = None, eps: Optional[float] = None, order: int = 1):
+                   full_grid: Optional[bool] = None, eps: Optional[float] = None, order: int = 1,
+                   dr: bool = False):
     """Convenience: run the oracle on a synth.Band."""
     cfg = band.cfg
     return solve_band(band.mic_xyz, cfg.c0, cfg.n, cfg.side_len, cfg.z0, cfg.cx, cfg.cy,
                       band.freqs, band.csm, cfg.epsilon if eps is None else eps, cfg.eps_mode,
                       cfg.sweeps if sweeps is None else sweeps,
-                      cfg.full_grid if full_grid is None else full_grid, n_threads, order)
+                      cfg.full_grid if full_grid is None else full_grid, n_threads, order, dr)

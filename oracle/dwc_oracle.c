@@ -114,8 +114,12 @@ int or_steering(int m, const double *mic, double c0, int n, double L, double z0,
 /* S2 DAS map, Eq. 2: b(r) = v^H C v / M^2 with v = e (R1).
  * Real part of the Hermitian form (reading R3); m outer, n inner, complex
  * fp64 accumulation.  csm is M x M complex128 row-major (C[m][n]).           */
+/* dr != 0: diagonal removal ("Diagonal removal is usually applied to CSM";
+ * reading R20): the m == j terms are left out, the quadratic form is
+ * normalised by M^2 - M instead of M^2 and negative map values are clamped to 0.           */
 int or_das(int m, const double *mic, double c0, int n, double L, double z0,
-           double cx, double cy, double freq, const double *csm, double *b) {
+           double cx, double cy, double freq, const double *csm, double *b, int dr) {
+    if (dr && m < 2) return OR_EINVAL;
     int S = n * n;
     double *e = (double *)malloc(sizeof(double) * 2 * (size_t)m);
     if (!e) return OR_ENOMEM;
@@ -126,6 +130,7 @@ int or_das(int m, const double *mic, double c0, int n, double L, double z0,
         for (int i = 0; i < m; i++) {
             double ar = e[2 * i], ai = -e[2 * i + 1];          /* conj(e_i) */
             for (int j = 0; j < m; j++) {
+                if (dr && j == i) continue;                     /* C with its diagonal removed */
                 double cr = csm[2 * ((size_t)i * m + j)];
                 double ci = csm[2 * ((size_t)i * m + j) + 1];
                 double er = e[2 * j], ei = e[2 * j + 1];
@@ -136,7 +141,12 @@ int or_das(int m, const double *mic, double c0, int n, double L, double z0,
             }
         }
         (void)acc_im;                                           /* rounding residue (R3) */
-        b[s] = acc_re / ((double)m * (double)m);
+        if (dr) {
+            b[s] = acc_re / ((double)m * (double)m - (double)m);
+            if (b[s] < 0.0) b[s] = 0.0;
+        } else {
+            b[s] = acc_re / ((double)m * (double)m);
+        }
         if (!isfinite(b[s])) { free(e); return OR_ENUMERIC; }
     }
     free(e);
@@ -281,9 +291,13 @@ int or_compress(int n, const double *b, double eps, int eps_mode, int full_grid,
 /* ------------------------------------------------------------------------ */
 /* S5 PSF on the kept points, Eq. 9-12 with v = g = e (R1):
  *   A_ij = |e_i^H e_j|^2 / M^2     (Eq. 23 restriction).  */
+/* dr != 0 (reading R20): the PSF consistent with the diagonal-removed DAS, i.e. b = A x for
+ * C = sum_s x_s e_s e_s^H with its diagonal removed:
+ *   A_ij = (|e_i^H e_j|^2 - sum_q |e_qi|^2 |e_qj|^2) / (M^2 - M),  negative entries clamped to 0. */
 int or_psf(int m, const double *mic, double c0, int n, double L, double z0,
            double cx, double cy, double freq, int nk, const int *keep,
-           double *A /* nk x nk row-major */) {
+           double *A /* nk x nk row-major */, int dr) {
+    if (dr && m < 2) return OR_EINVAL;
     double *E = (double *)malloc(sizeof(double) * 2 * (size_t)m * (size_t)nk);
     if (!E) return OR_ENOMEM;
     int rc = or_steering(m, mic, c0, n, L, z0, cx, cy, freq, nk, keep, E);
@@ -299,7 +313,18 @@ int or_psf(int m, const double *mic, double c0, int n, double L, double z0,
                 gr += ar * br - ai * bi;
                 gi += ar * bi + ai * br;
             }
-            A[(size_t)i * nk + j] = (gr * gr + gi * gi) / m2;
+            if (dr) {
+                double q4 = 0.0;
+                for (int q = 0; q < m; q++) {
+                    double pi2 = ei[2 * q] * ei[2 * q] + ei[2 * q + 1] * ei[2 * q + 1];
+                    double pj2 = ej[2 * q] * ej[2 * q] + ej[2 * q + 1] * ej[2 * q + 1];
+                    q4 += pi2 * pj2;
+                }
+                double v = (gr * gr + gi * gi - q4) / (m2 - (double)m);
+                A[(size_t)i * nk + j] = v > 0.0 ? v : 0.0;
+            } else {
+                A[(size_t)i * nk + j] = (gr * gr + gi * gi) / m2;
+            }
         }
     free(E);
     return OR_OK;
@@ -357,7 +382,8 @@ int or_gs(int nk, const double *A, const double *b, int sweeps, double *x) {
 /* ------------------------------------------------------------------------ */
 /* One bin, S1..S8.  keep (S ints) ascending, first n_keep valid.  x_map (S)
  * is the source power on the full grid, zero off the kept set (S8).
- * flags: bit 0 full grid (keep every node), bit 1 cubic predictor (R19).      */
+ * flags: bit 0 full grid (keep every node), bit 1 cubic predictor (R19),
+ * bit 2 diagonal removal (R20).                                                */
 int or_solve_bin(int m, const double *mic, double c0, int n, double L, double z0,
                  double cx, double cy, double freq, const double *csm,
                  double eps, int eps_mode, int sweeps, int flags,
@@ -365,7 +391,7 @@ int or_solve_bin(int m, const double *mic, double c0, int n, double L, double z0
     int S = n * n;
     double *b = b_map ? b_map : (double *)malloc(sizeof(double) * (size_t)S);
     if (!b) return OR_ENOMEM;
-    int rc = or_das(m, mic, c0, n, L, z0, cx, cy, freq, csm, b);
+    int rc = or_das(m, mic, c0, n, L, z0, cx, cy, freq, csm, b, flags & 4);
     int nk = 0;
     double *A = NULL, *bt = NULL, *xt = NULL;
     if (rc == OR_OK) {
@@ -378,7 +404,7 @@ int or_solve_bin(int m, const double *mic, double c0, int n, double L, double z0
         xt = (double *)malloc(sizeof(double) * (size_t)nk);
         if (!A || !bt || !xt) rc = OR_ENOMEM;
     }
-    if (rc == OR_OK) rc = or_psf(m, mic, c0, n, L, z0, cx, cy, freq, nk, keep, A);
+    if (rc == OR_OK) rc = or_psf(m, mic, c0, n, L, z0, cx, cy, freq, nk, keep, A, flags & 4);
     if (rc == OR_OK) {
         for (int i = 0; i < nk; i++) bt[i] = b[keep[i]];   /* S6: b~ = b[keep] */
         rc = or_gs(nk, A, bt, sweeps, xt);

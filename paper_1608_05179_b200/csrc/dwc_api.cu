@@ -56,7 +56,7 @@ struct dwc_ctx {
     int device = 0;
     int num_sms = 148;
     size_t total_bytes = 0;
-    DevBuf mic, freq, dist, amp, herm, bint, opa, opb, rsc, bt, A, lay, order, counter, tiles, flag, items, packets,
+    DevBuf mic, freq, dist, amp, herm, bint, opa, opb, rsc, wt, bt, A, lay, order, counter, tiles, flag, items, packets,
         csm_h, nk_h, keep_h, xmap_h, bmap_h, gs_x, gs_b;
     PinBuf stage, readback;
     size_t stage_off = 0;
@@ -183,7 +183,7 @@ dwc_status check_params(const dwc_params *p) {
     if (!(p->epsilon > 0.0) || !finite(p->epsilon)) return fail(DWC_EINVAL, "epsilon must be > 0");
     if (p->eps_mode != 0 && p->eps_mode != 1) return fail(DWC_EINVAL, "eps_mode must be 0 or 1");
     if (p->sweeps < 1) return fail(DWC_EINVAL, "sweeps must be >= 1");
-    if (p->flags & ~(DWC_FULL_GRID | DWC_CUBIC)) return fail(DWC_EINVAL, "unknown flags 0x%x", p->flags);
+    if (p->flags & ~(DWC_FULL_GRID | DWC_CUBIC | DWC_DIAG_REMOVAL)) return fail(DWC_EINVAL, "unknown flags 0x%x", p->flags);
     return DWC_OK;
 }
 
@@ -282,12 +282,13 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
         if ((s = ensure(ctx, ctx->bint, sizeof(double) * (size_t)n_bins * S))) return s;
         b = (double *)ctx->bint.p;
     }
+    const int dr = (p->flags & DWC_DIAG_REMOVAL) ? 1 : 0;
     if (snap)
-        LAUNCH(launch_csm(M, n_bins, n_snap, snap, (double *)ctx->herm.p, 1, st));   // Eq. 1 -> Ch
+        LAUNCH(launch_csm(M, n_bins, n_snap, snap, (double *)ctx->herm.p, 1, dr, st));   // Eq. 1 -> Ch
     else
-        LAUNCH(launch_hermitize(M, n_bins, csm, (double *)ctx->herm.p, st));
+        LAUNCH(launch_hermitize(M, n_bins, csm, (double *)ctx->herm.p, dr, st));
     LAUNCH(launch_das(G, (double *)ctx->dist.p, (double *)ctx->amp.p, n_bins, (double *)ctx->freq.p,
-                      (double *)ctx->herm.p, b, st));
+                      (double *)ctx->herm.p, b, dr, st));
     ev(ctx, 1, st);
     // S3+S4
     LAUNCH(launch_compress(n, n_bins, b, p->epsilon, p->eps_mode, (p->flags & DWC_FULL_GRID) ? 1 : 0, (p->flags & DWC_CUBIC) ? 3 : 1,
@@ -340,6 +341,7 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
     if ((s = ensure(ctx, ctx->opa, psf_opa_bytes(M, r_off))) || (s = ensure(ctx, ctx->opb, psf_opb_bytes(M, r_off))) ||
         (s = ensure(ctx, ctx->rsc, sizeof(double) * (size_t)r_off)))
         return s;
+    if (dr && (s = ensure(ctx, ctx->wt, sizeof(double) * (size_t)r_off * M))) return s;
     if ((s = ensure(ctx, ctx->bt, sizeof(double) * (size_t)v_off))) return s;
     if ((s = ensure(ctx, ctx->A, sizeof(float) * (size_t)a_off))) return s;
     if ((s = ensure(ctx, ctx->packets, (size_t)gs_packet_bytes() * (size_t)(v_off / 32)))) return s;
@@ -354,7 +356,7 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
     LAUNCH(launch_psf(G, (double *)ctx->dist.p, (double *)ctx->amp.p, n_bins, (double *)ctx->freq.p,
                       (BinLayout *)ctx->lay.p, keep_idx, b, max_rp, (int)tiles.size(), (int4 *)ctx->tiles.p,
                       (int8_t *)ctx->opa.p, (int8_t *)ctx->opb.p, (double *)ctx->rsc.p, (double *)ctx->bt.p,
-                      (float *)ctx->A.p, st));
+                      dr ? (double *)ctx->wt.p : nullptr, (float *)ctx->A.p, st));
     ev(ctx, 4, st);
     // S7 + S8
     CU(cudaMemsetAsync(x_map, 0, sizeof(float) * (size_t)n_bins * S, st));
@@ -432,7 +434,7 @@ dwc_status dwc_destroy(dwc_ctx *ctx) {
     if (!ctx) return DWC_OK;
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();
-    DevBuf *bufs[] = {&ctx->mic, &ctx->freq, &ctx->dist, &ctx->amp, &ctx->herm, &ctx->bint, &ctx->opa, &ctx->opb, &ctx->rsc,
+    DevBuf *bufs[] = {&ctx->mic, &ctx->freq, &ctx->dist, &ctx->amp, &ctx->herm, &ctx->bint, &ctx->opa, &ctx->opb, &ctx->rsc, &ctx->wt,
                       &ctx->bt, &ctx->A, &ctx->lay, &ctx->order, &ctx->counter, &ctx->tiles, &ctx->flag,
                       &ctx->items, &ctx->packets, &ctx->csm_h, &ctx->nk_h, &ctx->keep_h, &ctx->xmap_h, &ctx->bmap_h, &ctx->gs_x, &ctx->gs_b};
     for (DevBuf *b : bufs)
@@ -502,7 +504,7 @@ dwc_status dwc_csm(dwc_ctx *ctx, int32_t m, int32_t n_bins, int32_t n_snap, cons
         return fail(DWC_EINVAL, "m = %d, n_bins = %d, n_snap = %d", m, n_bins, n_snap);
     if (!snap || !csm) return fail(DWC_EINVAL, "NULL device buffer");
     int launches = 0;
-    LAUNCH(launch_csm(m, n_bins, n_snap, snap, csm, 0, (cudaStream_t)cuda_stream));
+    LAUNCH(launch_csm(m, n_bins, n_snap, snap, csm, 0, 0, (cudaStream_t)cuda_stream));
     return DWC_OK;
 }
 
@@ -551,7 +553,7 @@ dwc_status dwc_steer(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, d
 }
 
 dwc_status dwc_das(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, int32_t n_bins,
-                   const double *freq_hz, const double *csm, double *b_map, void *cuda_stream) {
+                   const double *freq_hz, const double *csm, int32_t flags, double *b_map, void *cuda_stream) {
     dwc_status s;
     if ((s = check_ctx(ctx)) || (s = check_array(arr)) || (s = check_grid(grid)) || (s = check_freqs(n_bins, freq_hz)))
         return s;
@@ -562,9 +564,11 @@ dwc_status dwc_das(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, int
     if ((s = prepare_geometry(ctx, arr, grid, n_bins, freq_hz, G, launches, st))) return s;
     if ((s = ensure(ctx, ctx->herm, sizeof(double) * 2 * (size_t)n_bins * das_mpad(arr->m) * das_mpad(arr->m))))
         return s;
-    LAUNCH(launch_hermitize(arr->m, n_bins, csm, (double *)ctx->herm.p, st));
+    if (flags & ~DWC_DIAG_REMOVAL) return fail(DWC_EINVAL, "unknown flags 0x%x", flags);
+    const int dr = (flags & DWC_DIAG_REMOVAL) ? 1 : 0;
+    LAUNCH(launch_hermitize(arr->m, n_bins, csm, (double *)ctx->herm.p, dr, st));
     LAUNCH(launch_das(G, (double *)ctx->dist.p, (double *)ctx->amp.p, n_bins, (double *)ctx->freq.p,
-                      (double *)ctx->herm.p, b_map, st));
+                      (double *)ctx->herm.p, b_map, dr, st));
     return DWC_OK;
 }
 
@@ -584,13 +588,15 @@ dwc_status dwc_compress(dwc_ctx *ctx, const dwc_grid *grid, const dwc_params *p,
 }
 
 dwc_status dwc_psf(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, double freq_hz,
-                   int32_t n_keep, const int32_t *keep_idx, float *A, void *cuda_stream) {
+                   int32_t n_keep, const int32_t *keep_idx, int32_t flags, float *A, void *cuda_stream) {
     dwc_status s;
     if ((s = check_ctx(ctx)) || (s = check_array(arr)) || (s = check_grid(grid)) || (s = check_freqs(1, &freq_hz)))
         return s;
     const int S = grid->n * grid->n;
     if (n_keep < 1 || n_keep > S) return fail(DWC_EINVAL, "n_keep = %d outside [1, S]", n_keep);
     if (!keep_idx || !A) return fail(DWC_EINVAL, "NULL device buffer");
+    if (flags & ~DWC_DIAG_REMOVAL) return fail(DWC_EINVAL, "unknown flags 0x%x", flags);
+    const int dr = (flags & DWC_DIAG_REMOVAL) ? 1 : 0;
     cudaStream_t st = (cudaStream_t)cuda_stream;
     int launches = 0;
     Geo G;
@@ -605,6 +611,7 @@ dwc_status dwc_psf(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, dou
         (s = ensure(ctx, ctx->rsc, sizeof(double) * rp)) || (s = ensure(ctx, ctx->bt, sizeof(double) * sp)) ||
         (s = ensure(ctx, ctx->A, sizeof(float) * 1024 * (size_t)sym_tiles(sp / 32))))
         return s;
+    if (dr && (s = ensure(ctx, ctx->wt, sizeof(double) * (size_t)rp * arr->m))) return s;
     if ((s = stage_begin(ctx, sizeof(BinLayout) + sizeof(int4) * tiles.size() + 1024))) return s;
     if ((s = stage_upload(ctx, ctx->lay.p, &lay, sizeof(BinLayout), st))) return s;
     if ((s = stage_upload(ctx, ctx->tiles.p, tiles.data(), sizeof(int4) * tiles.size(), st))) return s;
@@ -612,7 +619,7 @@ dwc_status dwc_psf(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, dou
     LAUNCH(launch_psf(G, (double *)ctx->dist.p, (double *)ctx->amp.p, 1, (double *)ctx->freq.p,
                       (BinLayout *)ctx->lay.p, keep_idx, nullptr, rp, (int)tiles.size(), (int4 *)ctx->tiles.p,
                       (int8_t *)ctx->opa.p, (int8_t *)ctx->opb.p, (double *)ctx->rsc.p, (double *)ctx->bt.p,
-                      (float *)ctx->A.p, st));
+                      dr ? (double *)ctx->wt.p : nullptr, (float *)ctx->A.p, st));
     LAUNCH(launch_tile_convert(0, n_keep, sp, lay.g, (float *)ctx->A.p, A, st));
     return DWC_OK;
 }

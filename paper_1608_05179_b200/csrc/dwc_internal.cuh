@@ -36,15 +36,16 @@ int launch_steer(const Geo &g, const double *dist, const double *amp, const doub
 // Half-Hermitian part of the CSMs (reading R3), zero padded to das_mpad(M): H (dev) holds
 // n_bins * Mp * Mp complex128 (upper triangle of (C + C^H)/2, diagonal halved).
 int das_mpad(int M);
-int launch_hermitize(int M, int n_bins, const double *csm, double *H, cudaStream_t st);
+// dr: diagonal removal (reading R20) -- the diagonal of Ch is zero.
+int launch_hermitize(int M, int n_bins, const double *csm, double *H, int dr, cudaStream_t st);
 
 // Eq. 1 (k_csm.cu): C_k = P_k P_k^H / I from snapshot spectra snap [n_bins][M][I] complex128.
 // half = 0: full C [n_bins][M][M]; half = 1: the half-Hermitian padded Ch of launch_hermitize.
-int launch_csm(int M, int n_bins, int I, const double *snap, double *out, int half, cudaStream_t st);
+int launch_csm(int M, int n_bins, int I, const double *snap, double *out, int half, int dr, cudaStream_t st);
 
 // S2: b[k][s] for n_bins bins; freq dev[n_bins]; csm_half = launch_hermitize's output.
 int launch_das(const Geo &g, const double *dist, const double *amp, int n_bins,
-               const double *freq, const double *csm_half, double *b, cudaStream_t st);
+               const double *freq, const double *csm_half, double *b, int dr, cudaStream_t st);
 
 // S3+S4: compaction of kept nodes.  order 1: linear predictor (R7), 3: cubic (R19).
 // flag (dev int): bit 1 set when b has a non-finite value.
@@ -67,6 +68,8 @@ struct BinLayout {
 // (opA: psf_opa_bytes, opB: psf_opb_bytes for sum rp rows; rsc: sum rp doubles), b~ = b[keep]
 // into bt (fp64, zero padded to sp; skipped when b is NULL), then A~_k over the (bin, I, J)
 // list of 128x64 output tiles touching the upper triangle, both triangles written.
+// wt != NULL: diagonal removal (R20) -- the slice kernel writes |e_mr|^2 there (M doubles per
+// padded row, layout wt[r_off*M + m*rp + r]) and the epilogue forms the DR PSF.
 int psf_kp(int m);
 size_t psf_opa_bytes(int m, int64_t rows);
 size_t psf_opb_bytes(int m, int64_t rows);
@@ -74,7 +77,8 @@ int psf_tile_rows();
 int psf_tile_cols();
 int launch_psf(const Geo &g, const double *dist, const double *amp, int n_bins, const double *freq,
                const BinLayout *lay, const int32_t *keep_idx, const double *b, int max_rp, int n_tiles,
-               const int4 *tiles, int8_t *opA, int8_t *opB, double *rsc, double *bt, float *A, cudaStream_t st);
+               const int4 *tiles, int8_t *opA, int8_t *opB, double *rsc, double *bt, double *wt, float *A,
+               cudaStream_t st);
 
 // S5 storage layout of A~_k (written by the PSF epilogue, streamed by the GS kernel).
 // A~ is symmetric (reading R1), so only one triangle is stored.  32x32 fp32 tiles, column-major

@@ -17,7 +17,7 @@ constexpr int kCsmK = 16;    // snapshots per stage
 constexpr int kCsmLd = kCsmK + 1;
 
 __global__ void __launch_bounds__(256)
-csm_kernel(int M, int Mp, int I, const double2 *__restrict__ snap, double2 *__restrict__ out, int half) {
+csm_kernel(int M, int Mp, int I, const double2 *__restrict__ snap, double2 *__restrict__ out, int half, int dr) {
     __shared__ double2 As[kCsmT * kCsmLd], Bs[kCsmT * kCsmLd];
     const int bin = blockIdx.z, mt = blockIdx.y, nt = blockIdx.x;
     const int Mo = half ? Mp : M;   // output leading dimension
@@ -69,17 +69,17 @@ csm_kernel(int M, int Mp, int I, const double2 *__restrict__ snap, double2 *__re
             double2 v = make_double2(acc[a][b].x * inv, acc[a][b].y * inv);
             if (half) {
                 if (m >= M || n >= M || n < m) v = make_double2(0.0, 0.0);
-                else if (n == m) v = make_double2(v.x * 0.5, 0.0);
+                else if (n == m) v = dr ? make_double2(0.0, 0.0) : make_double2(v.x * 0.5, 0.0);
             }
             O[(size_t)m * Mo + n] = v;
         }
 }
 
-int launch_csm(int M, int n_bins, int I, const double *snap, double *out, int half, cudaStream_t st) {
+int launch_csm(int M, int n_bins, int I, const double *snap, double *out, int half, int dr, cudaStream_t st) {
     const int Mo = half ? das_mpad(M) : M;
     const int t = (Mo + kCsmT - 1) / kCsmT;
     dim3 grid(t, t, n_bins);
-    csm_kernel<<<grid, 256, 0, st>>>(M, das_mpad(M), I, (const double2 *)snap, (double2 *)out, half);
+    csm_kernel<<<grid, 256, 0, st>>>(M, das_mpad(M), I, (const double2 *)snap, (double2 *)out, half, dr);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

@@ -129,7 +129,7 @@ __device__ __forceinline__ void das_rows(const double2 *__restrict__ Cw, const d
 template <int PPL>
 __global__ void __launch_bounds__(kDasThreads, 1)
 das_kernel(Geo g, const double *__restrict__ dist, const double *__restrict__ amp,
-           const double *__restrict__ freq, const double2 *__restrict__ Ch, int Mp, double *__restrict__ b) {
+           const double *__restrict__ freq, const double2 *__restrict__ Ch, int Mp, double *__restrict__ b, int dr) {
     constexpr int P = 32 * PPL;
     extern __shared__ double2 smem_d2[];
     double2 *Es = smem_d2;                       // [Mp][P]
@@ -184,14 +184,19 @@ das_kernel(Geo g, const double *__restrict__ dist, const double *__restrict__ am
         double v = 0.0;
 #pragma unroll
         for (int q = 0; q < kDasWarps; q++) v += part[q][threadIdx.x];
-        b[(size_t)bin * g.S + s0 + threadIdx.x] = 2.0 * v / ((double)M * (double)M);
+        if (dr) {   // R20: normalised by M^2 - M, negative values clamped (the diagonal is already gone)
+            const double bv = 2.0 * v / ((double)M * (double)M - (double)M);
+            b[(size_t)bin * g.S + s0 + threadIdx.x] = bv > 0.0 ? bv : 0.0;
+        } else {
+            b[(size_t)bin * g.S + s0 + threadIdx.x] = 2.0 * v / ((double)M * (double)M);
+        }
     }
 }
 
 // Half-Hermitian, zero-padded CSM Ch (Mp x Mp per bin) from the input C (reading R3: only the
 // Hermitian part H = (C + C^H)/2 enters Re(e^H C e)).
 __global__ void hermitize_kernel(int M, int Mp, long total, const double2 *__restrict__ C,
-                                 double2 *__restrict__ Ch) {
+                                 double2 *__restrict__ Ch, int dr) {
     for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total; t += (long)gridDim.x * blockDim.x) {
         const long bin = t / ((long)Mp * Mp);
         const int r = (int)(t - bin * Mp * Mp);
@@ -201,23 +206,23 @@ __global__ void hermitize_kernel(int M, int Mp, long total, const double2 *__res
             const double2 a = C[bin * M * M + (long)i * M + j];
             const double2 c = C[bin * M * M + (long)j * M + i];
             v = make_double2((a.x + c.x) * 0.5, (a.y - c.y) * 0.5);
-            if (j == i) v = make_double2(v.x * 0.5, 0.0);
+            if (j == i) v = dr ? make_double2(0.0, 0.0) : make_double2(v.x * 0.5, 0.0);   // R20: no diagonal
         }
         Ch[t] = v;
     }
 }
 
-int launch_hermitize(int M, int n_bins, const double *csm, double *H, cudaStream_t st) {
+int launch_hermitize(int M, int n_bins, const double *csm, double *H, int dr, cudaStream_t st) {
     const int Mp = das_mpad(M);
     long total = (long)n_bins * Mp * Mp;
     int blocks = (int)((total + 255) / 256);
     if (blocks > 148 * 16) blocks = 148 * 16;
-    hermitize_kernel<<<blocks, 256, 0, st>>>(M, Mp, total, (const double2 *)csm, (double2 *)H);
+    hermitize_kernel<<<blocks, 256, 0, st>>>(M, Mp, total, (const double2 *)csm, (double2 *)H, dr);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
 int launch_das(const Geo &g, const double *dist, const double *amp, int n_bins,
-               const double *freq, const double *csm_half, double *b, cudaStream_t st) {
+               const double *freq, const double *csm_half, double *b, int dr, cudaStream_t st) {
     const int Mp = das_mpad(g.m);
     const int P = (Mp <= 64) ? 64 : 32;
     const size_t smem = (size_t)16 * Mp * (P + 8 * kDasWarps);
@@ -232,9 +237,9 @@ int launch_das(const Geo &g, const double *dist, const double *amp, int n_bins,
     }
     dim3 grid((g.S + P - 1) / P, n_bins);
     if (P == 64)
-        das_kernel<2><<<grid, kDasThreads, smem, st>>>(g, dist, amp, freq, (const double2 *)csm_half, Mp, b);
+        das_kernel<2><<<grid, kDasThreads, smem, st>>>(g, dist, amp, freq, (const double2 *)csm_half, Mp, b, dr);
     else
-        das_kernel<1><<<grid, kDasThreads, smem, st>>>(g, dist, amp, freq, (const double2 *)csm_half, Mp, b);
+        das_kernel<1><<<grid, kDasThreads, smem, st>>>(g, dist, amp, freq, (const double2 *)csm_half, Mp, b, dr);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

@@ -84,7 +84,7 @@ psf_slice_kernel(Geo g, const double *__restrict__ dist, const double *__restric
                  const double *__restrict__ freq, const BinLayout *__restrict__ lay,
                  const int32_t *__restrict__ keep_idx, const double *__restrict__ b, int kp,
                  int8_t *__restrict__ opA, int8_t *__restrict__ opB, double *__restrict__ rsc,
-                 double *__restrict__ bt) {
+                 double *__restrict__ bt, double *__restrict__ wt) {
     const int bin = blockIdx.y;
     const BinLayout L = lay[bin];
     const int lane = threadIdx.x & 31;
@@ -109,8 +109,10 @@ psf_slice_kernel(Geo g, const double *__restrict__ dist, const double *__restric
             double sn, cs;
             sincospi(kpi * d, &sn, &cs);
             int dr[kSl], di[kSl];
-            digits(ldexp(a * cs, q), dr);
-            digits(ldexp(-(a * sn), q), di);
+            const double er = a * cs, ei = -(a * sn);
+            digits(ldexp(er, q), dr);
+            digits(ldexp(ei, q), di);
+            if (wt) wt[(size_t)L.r_off * M + (size_t)m * L.rp + r] = er * er + ei * ei;   // |e_mr|^2 (R20)
 #pragma unroll
             for (int t = 0; t < kSl; t++) {
                 A[opa_index(L.rp, t, r, m)] = (int8_t)dr[t];            // X_t = [Re; Im]
@@ -134,6 +136,8 @@ psf_slice_kernel(Geo g, const double *__restrict__ dist, const double *__restric
             if (b) bt[L.v_off + r] = b[(size_t)bin * g.S + s];
         }
     } else {
+        if (wt)
+            for (int m = lane; m < M; m += 32) wt[(size_t)L.r_off * M + (size_t)m * L.rp + r] = 0.0;
         for (int kk = lane; kk < kp; kk += 32) {
 #pragma unroll
             for (int t = 0; t < kSl; t++) {
@@ -159,7 +163,7 @@ struct __align__(1024) PsfSmem {
 __global__ void __launch_bounds__(kPsfThreads, 1)
 psf_tc_kernel(int M, int kp, const int4 *__restrict__ tiles, const BinLayout *__restrict__ lay,
               const int8_t *__restrict__ opA, const int8_t *__restrict__ opB, const double *__restrict__ rsc,
-              float *__restrict__ Aout) {
+              const double *__restrict__ wt, float *__restrict__ Aout) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     PsfSmem &sm = *reinterpret_cast<PsfSmem *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -225,9 +229,22 @@ psf_tc_kernel(int M, int kp, const int4 *__restrict__ tiles, const BinLayout *__
         const bool row_ok = i < L.sp;
         const double ri = row_ok ? rsc[L.r_off + i] : 0.0;
         const double inv_m2 = 1.0 / ((double)M * (double)M);
+        const double inv_dr = 1.0 / ((double)M * (double)M - (double)M);
         float *Ab = Aout + L.a_off;
         mbar_wait(&sm.tmem_full, 0);
         tc_fence_after();
+        // diagonal removal (R20): Q_ij = sum_m |e_mi|^2 |e_mj|^2 in fp64; the tile's 64 column
+        // vectors are staged in the (now idle) operand ring
+        double *ws = reinterpret_cast<double *>(sm.a[0]);
+        const double *wti = wt ? wt + (size_t)L.r_off * M + min(i, L.rp - 1) : nullptr;
+        if (wt) {
+            const double *wb = wt + (size_t)L.r_off * M;
+            for (int e = threadIdx.x - 64; e < kTN * M; e += 128) {
+                const int jj = e / M, m = e - (e / M) * M;
+                ws[e] = wb[(size_t)m * L.rp + tl.z * kTN + jj];
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+        }
         for (int jc = 0; jc < kTN; jc += 8) {
             __syncwarp();
             int32_t acc[2 * kSl][8];
@@ -238,6 +255,16 @@ psf_tc_kernel(int M, int kp, const int4 *__restrict__ tiles, const BinLayout *__
             const int j0 = tl.z * kTN + jc;
             if (!row_ok || j0 >= L.sp) continue;  // sp is a multiple of 32: all 8 columns valid
             float v[8];
+            double q4[8];
+#pragma unroll
+            for (int c = 0; c < 8; c++) q4[c] = 0.0;
+            if (wt) {
+                for (int m = 0; m < M; m++) {
+                    const double wi = wti[(size_t)m * L.rp];
+#pragma unroll
+                    for (int c = 0; c < 8; c++) q4[c] = fma(wi, ws[(jc + c) * M + m], q4[c]);
+                }
+            }
 #pragma unroll
             for (int c = 0; c < 8; c++) {
                 const long long gre = ((long long)acc[0][c] << 21) + ((long long)acc[1][c] << 14) +
@@ -246,7 +273,12 @@ psf_tc_kernel(int M, int kp, const int4 *__restrict__ tiles, const BinLayout *__
                                       ((long long)acc[6][c] << 7) + (long long)acc[7][c];
                 const double dre = (double)gre, dim = (double)gim;
                 const double sq = dre * dre + dim * dim;
-                v[c] = (float)(sq * ri * rsc[L.r_off + j0 + c] * inv_m2);
+                if (wt) {
+                    const double a = (sq * ri * rsc[L.r_off + j0 + c] - q4[c]) * inv_dr;
+                    v[c] = (float)(a > 0.0 ? a : 0.0);
+                } else {
+                    v[c] = (float)(sq * ri * rsc[L.r_off + j0 + c] * inv_m2);
+                }
             }
             // direct (i, j0..j0+7): coalesced over lanes; mirror (j0..j0+7, i): two float4 per lane
             int td[3], tm[3];
@@ -277,10 +309,11 @@ int psf_tile_cols() { return kTN; }
 
 int launch_psf(const Geo &g, const double *dist, const double *amp, int n_bins, const double *freq,
                const BinLayout *lay, const int32_t *keep_idx, const double *b, int max_rp, int n_tiles,
-               const int4 *tiles, int8_t *opA, int8_t *opB, double *rsc, double *bt, float *A, cudaStream_t st) {
+               const int4 *tiles, int8_t *opA, int8_t *opB, double *rsc, double *bt, double *wt, float *A,
+               cudaStream_t st) {
     const int kp = psf_kp(g.m);
     dim3 grid((max_rp + 7) / 8, n_bins);
-    psf_slice_kernel<<<grid, 256, 0, st>>>(g, dist, amp, freq, lay, keep_idx, b, kp, opA, opB, rsc, bt);
+    psf_slice_kernel<<<grid, 256, 0, st>>>(g, dist, amp, freq, lay, keep_idx, b, kp, opA, opB, rsc, bt, wt);
     if (cudaPeekAtLastError() != cudaSuccess) return -1;
     if (n_tiles <= 0) return 1;
     const size_t smem = sizeof(PsfSmem) + 1024;
@@ -290,7 +323,7 @@ int launch_psf(const Geo &g, const double *dist, const double *amp, int n_bins, 
             return -1;
         attr = true;
     }
-    psf_tc_kernel<<<n_tiles, kPsfThreads, smem, st>>>(g.m, kp, tiles, lay, opA, opB, rsc, A);
+    psf_tc_kernel<<<n_tiles, kPsfThreads, smem, st>>>(g.m, kp, tiles, lay, opA, opB, rsc, wt, A);
     return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
 }
 

@@ -215,17 +215,17 @@ def test_gs_parity_on_oracle_system(ctx, torch_cuda, oracle_lib, nk, sweeps):
 
 
 # ---------------------------------------------------------------------------- end to end
-def _e2e(ctx, torch, oracle_lib, band, sweeps=None, full=False, check_b=True, order=1):
+def _e2e(ctx, torch, oracle_lib, band, sweeps=None, full=False, check_b=True, order=1, dr=False):
     cfg = band.cfg
     g = geom_of(band)
     sw = sweeps or cfg.sweeps
     out = ctx.solve_band(g, band.freqs, torch.from_numpy(band.csm).cuda(), cfg.epsilon, sw, cfg.eps_mode,
-                         full_grid=full, want_b=True, order=order)
+                         full_grid=full, want_b=True, order=order, dr=dr)
     nk = out["n_keep"].cpu().numpy()
     keep = out["keep_idx"].cpu().numpy()
     x = out["x_map"].cpu().numpy()
     bm = out["b_map"].cpu().numpy()
-    rnk, rkeep, rx, rb = oracle_lib.solve_band_cfg(band, sweeps=sw, full_grid=full, order=order)
+    rnk, rkeep, rx, rb = oracle_lib.solve_band_cfg(band, sweeps=sw, full_grid=full, order=order, dr=dr)
     for k in range(len(band.freqs)):
         assert rel_l2(bm[k], rb[k]) < TOL_B
         assert nk[k] == rnk[k], (k, nk[k], rnk[k])
@@ -383,3 +383,33 @@ def test_e2e_from_snapshots_cfg2(ctx, torch_cuda, oracle_lib):
         x = out["x_map"][k].cpu().numpy()
         assert rel_l2(x, rx[k]) < TOL_X
         assert abs(x.sum() - rx[k].sum()) <= TOL_P * rx[k].sum()
+
+
+# ---------------------------------------------------------------------------- NEXT-2: diagonal removal
+@pytest.mark.parametrize("cfgname", ["cfg1", "cfg2"])
+def test_das_dr_parity(ctx, torch_cuda, oracle_lib, cfgname):
+    torch = torch_cuda
+    band = synth.make_band(cfgname)
+    g = geom_of(band)
+    b = ctx.das(g, band.freqs, torch.from_numpy(band.csm).cuda(), dr=True).cpu().numpy()
+    for k, (f, c) in enumerate(zip(band.freqs, band.csm)):
+        ref = oracle_lib.das(*oracle_args(g), f, c, dr=True)
+        assert rel_l2(b[k], ref) < TOL_B
+        assert b[k].min() >= 0.0
+
+
+@pytest.mark.parametrize("m,n,nk", [(24, 15, 65), (24, 15, 200), (128, 21, 300), (13, 15, 100)])
+def test_psf_dr_parity(ctx, torch_cuda, oracle_lib, m, n, nk):
+    torch = torch_cuda
+    g = small_geom(m, n, 3 if m % 3 == 0 else 1)
+    keep = np.sort(np.random.default_rng(nk).choice(g.S, size=nk, replace=False)).astype(np.int32)
+    A = ctx.psf(g, 5100.0, torch.from_numpy(keep).cuda(), dr=True).cpu().numpy()
+    ref = oracle_lib.psf(*oracle_args(g), 5100.0, keep, dr=True)
+    assert rel_l2(A, ref) < TOL_A
+    assert np.max(np.abs(A - ref)) <= 2.0 ** -22
+    assert np.array_equal(A, A.T) and A.min() >= 0.0
+
+
+def test_e2e_cfg2_diag_removal(ctx, torch_cuda, oracle_lib):
+    """NEXT-2 end to end: cfg2's 20 dB noisy CSMs with the diagonal removed."""
+    _e2e(ctx, torch_cuda, oracle_lib, synth.make_band("cfg2"), dr=True)

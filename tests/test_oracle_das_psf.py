@@ -115,3 +115,56 @@ def test_psf_restriction_is_submatrix(oracle_lib, geom):
     keep = np.array([3, 17, 18, 60, 119, 120])
     sub = oracle_lib.psf(*_args(g), f, keep)
     assert np.array_equal(sub, full[np.ix_(keep, keep)])
+
+
+# ---------------------------------------------------------------------------- NEXT-2: diagonal removal
+def test_dr_removes_uncorrelated_noise_exactly(oracle_lib, geom):
+    """Diagonal removal (reading R20) drops the uncorrelated microphone noise of
+    the CSM: the map of C + sigma^2 I equals the map of C; a pure noise CSM maps to 0."""
+    g = geom
+    f = 3100.0
+    M = g["mic"].shape[0]
+    C = synth.csm_exact(g["mic"], _nodes(g, [20, 77]), np.array([1.0, 0.3]), f, g["c0"])
+    noisy = C + 0.8 * np.eye(M)
+    b0 = oracle_lib.das(*_args(g), f, C, dr=True)
+    b1 = oracle_lib.das(*_args(g), f, noisy, dr=True)
+    assert np.max(np.abs(b1 - b0)) <= 1e-13 * np.max(b0)
+    assert np.all(oracle_lib.das(*_args(g), f, 2.5 * np.eye(M), dr=True) == 0.0)
+    assert np.any(oracle_lib.das(*_args(g), f, 2.5 * np.eye(M)) > 0.0)   # not without DR
+
+
+def test_dr_single_source_is_dr_psf_column(oracle_lib, geom):
+    """b = A_DR x for the exact single-source CSM (Eq. 9-12 with the diagonal removed):
+    b_r = x (|e_r^H e_s|^2 - sum_q |e_qr|^2 |e_qs|^2) / (M^2 - M), clamped at 0 on both
+    sides (clamp(x a) = x clamp(a) for x > 0).  The exact CSM is built from the normalised
+    steering vector of s0 (oracle.steering), x = 1.7."""
+    g = geom
+    f = 2800.0
+    s0 = 64
+    x = 1.7
+    e = oracle_lib.steering(*_args(g), f, np.array([s0], dtype=np.int32))[0]
+    C = x * np.outer(e, e.conj())
+    b = oracle_lib.das(*_args(g), f, C, dr=True)
+    A = oracle_lib.psf(*_args(g), f, np.arange(g["n"] ** 2), dr=True)
+    assert np.max(np.abs(b - x * A[:, s0])) <= 1e-12 * x
+    assert np.argmax(b) == s0
+
+
+def test_dr_psf_closed_forms(oracle_lib, geom):
+    """A_DR diagonal = (M^2 - sum_q |e_q|^4) / (M^2 - M) (closed form from the steering
+    vectors); symmetric; entries in [0, 1.0x] (clamped); equals the plain PSF minus the
+    fourth-moment term where the plain entry is large."""
+    g = geom
+    f = 4200.0
+    keep = np.arange(0, g["n"] ** 2, 3, dtype=np.int32)
+    M = g["mic"].shape[0]
+    A = oracle_lib.psf(*_args(g), f, keep, dr=True)
+    A0 = oracle_lib.psf(*_args(g), f, keep)
+    E = oracle_lib.steering(*_args(g), f, keep)
+    w = np.abs(E) ** 2                                     # [nk, M]
+    diag = (M * M - np.sum(w ** 2, axis=1)) / (M * M - M)
+    assert np.max(np.abs(np.diag(A) - diag)) < 1e-12
+    assert np.array_equal(A, A.T)
+    assert A.min() >= 0.0
+    ref = np.maximum((A0 * M * M - w @ w.T) / (M * M - M), 0.0)
+    assert np.max(np.abs(A - ref)) < 1e-12
