@@ -101,13 +101,24 @@ __host__ __device__ inline int own_of(int g, int J) {
     if (g == 2) return (0xB6u >> (J % 8)) & 1u;                                // 0,1,1,0,1,1,0,1
     return 0;
 }
-// number of J in [0, x] owned by o
+// positions of owner o inside one period (bit r set: J = r mod period is owned by o)
+__host__ __device__ inline uint32_t own_mask(int g, int o) {
+    if (g == 4) return o == 0 ? 0x4081u : (o == 1 ? 0x8912u : (o == 2 ? 0x11224u : 0x22448u));
+    if (g == 2) return o == 0 ? 0x49u : 0xB6u;
+    return 1u;
+}
+__host__ __device__ inline int popc32(uint32_t v) {
+#ifdef __CUDA_ARCH__
+    return __popc(v);
+#else
+    return __builtin_popcount(v);
+#endif
+}
+// number of J in [0, x] owned by o (O(1): whole periods + popcount of the partial one)
 __host__ __device__ inline int sym_cnt(int x, int o, int g) {
     if (x < 0) return 0;
     const int P = own_period(g), full = (x + 1) / P, rem = (x + 1) - full * P;
-    int c = full * own_weight(g, o);
-    for (int r = 0; r < rem; r++) c += (own_of(g, r) == o);
-    return c;
+    return full * own_weight(g, o) + popc32(own_mask(g, o) & ((1u << rem) - 1u));
 }
 // the idx-th (0-based) J owned by o
 __host__ __device__ inline int own_nth(int g, int o, int idx) {

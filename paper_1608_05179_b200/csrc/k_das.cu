@@ -127,7 +127,7 @@ __device__ __forceinline__ void das_rows(const double2 *__restrict__ Cw, const d
 }
 
 template <int PPL>
-__global__ void __launch_bounds__(kDasThreads, 1)
+__global__ void __launch_bounds__(kDasThreads, 2)
 das_kernel(Geo g, const double *__restrict__ dist, const double *__restrict__ amp,
            const double *__restrict__ freq, const double2 *__restrict__ Ch, int Mp, double *__restrict__ b, int dr) {
     constexpr int P = 32 * PPL;
@@ -224,7 +224,10 @@ int launch_hermitize(int M, int n_bins, const double *csm, double *H, int dr, cu
 int launch_das(const Geo &g, const double *dist, const double *amp, int n_bins,
                const double *freq, const double *csm_half, double *b, int dr, cudaStream_t st) {
     const int Mp = das_mpad(g.m);
-    const int P = (Mp <= 64) ? 64 : 32;
+#ifndef DAS_P64
+#define DAS_P64 0
+#endif
+    const int P = (Mp <= 64 && DAS_P64) ? 64 : 32;   // 32 points: Es + Cw <= 96 KB -> two CTAs per SM (M <= 64)
     const size_t smem = (size_t)16 * Mp * (P + 8 * kDasWarps);
     if (smem > 220 * 1024) return -1;
     static size_t attr2 = 0, attr1 = 0;

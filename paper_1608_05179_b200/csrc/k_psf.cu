@@ -160,6 +160,7 @@ struct __align__(1024) PsfSmem {
     uint32_t tmem_base;
 };
 
+template <bool kDR>
 __global__ void __launch_bounds__(kPsfThreads, 1)
 psf_tc_kernel(int M, int kp, const int4 *__restrict__ tiles, const BinLayout *__restrict__ lay,
               const int8_t *__restrict__ opA, const int8_t *__restrict__ opB, const double *__restrict__ rsc,
@@ -236,8 +237,8 @@ psf_tc_kernel(int M, int kp, const int4 *__restrict__ tiles, const BinLayout *__
         // diagonal removal (R20): Q_ij = sum_m |e_mi|^2 |e_mj|^2 in fp64; the tile's 64 column
         // vectors are staged in the (now idle) operand ring
         double *ws = reinterpret_cast<double *>(sm.a[0]);
-        const double *wti = wt ? wt + (size_t)L.r_off * M + min(i, L.rp - 1) : nullptr;
-        if (wt) {
+        const double *wti = kDR ? wt + (size_t)L.r_off * M + min(i, L.rp - 1) : nullptr;
+        if (kDR) {
             const double *wb = wt + (size_t)L.r_off * M;
             for (int e = threadIdx.x - 64; e < kTN * M; e += 128) {
                 const int jj = e / M, m = e - (e / M) * M;
@@ -258,7 +259,7 @@ psf_tc_kernel(int M, int kp, const int4 *__restrict__ tiles, const BinLayout *__
             double q4[8];
 #pragma unroll
             for (int c = 0; c < 8; c++) q4[c] = 0.0;
-            if (wt) {
+            if (kDR) {
                 for (int m = 0; m < M; m++) {
                     const double wi = wti[(size_t)m * L.rp];
 #pragma unroll
@@ -273,7 +274,7 @@ psf_tc_kernel(int M, int kp, const int4 *__restrict__ tiles, const BinLayout *__
                                       ((long long)acc[6][c] << 7) + (long long)acc[7][c];
                 const double dre = (double)gre, dim = (double)gim;
                 const double sq = dre * dre + dim * dim;
-                if (wt) {
+                if (kDR) {
                     const double a = (sq * ri * rsc[L.r_off + j0 + c] - q4[c]) * inv_dr;
                     v[c] = (float)(a > 0.0 ? a : 0.0);
                 } else {
@@ -319,11 +320,17 @@ int launch_psf(const Geo &g, const double *dist, const double *amp, int n_bins, 
     const size_t smem = sizeof(PsfSmem) + 1024;
     static bool attr = false;
     if (!attr) {
-        if (cudaFuncSetAttribute(psf_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        if (cudaFuncSetAttribute(psf_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+                cudaSuccess ||
+            cudaFuncSetAttribute(psf_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+                cudaSuccess)
             return -1;
         attr = true;
     }
-    psf_tc_kernel<<<n_tiles, kPsfThreads, smem, st>>>(g.m, kp, tiles, lay, opA, opB, rsc, wt, A);
+    if (wt)
+        psf_tc_kernel<true><<<n_tiles, kPsfThreads, smem, st>>>(g.m, kp, tiles, lay, opA, opB, rsc, wt, A);
+    else
+        psf_tc_kernel<false><<<n_tiles, kPsfThreads, smem, st>>>(g.m, kp, tiles, lay, opA, opB, rsc, nullptr, A);
     return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
 }
 
