@@ -89,6 +89,7 @@ struct __align__(128) GsSmem {
     unsigned long long pready[2];      // leader: 1 arrival + g*kCons*128 tx bytes per step
     unsigned long long xr[2];          // leader: solver arrival; others: 1 arrival + 128 tx
     int item;
+    unsigned long long issue_t[kRing + kStg];   // profiling: clock64 at which each slot's copy was issued
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -316,7 +317,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 // ring: the ring then only has to cover L2 latency, not HBM latency
                 for (int s = 0, kn = 0, kp = kPf % T; s < total;
                      s++, kn = (kn + 1 == T) ? 0 : kn + 1, kp = (kp + 1 == T) ? 0 : kp + 1) {
-                    if (s + kPf < total) {
+                    if (kPf > 0 && s + kPf < total) {
                         const Seg *sp = segt + 2 * kp;
                         for (int sg = 0; sg < 2; sg++)
                             if (sp[sg].len > 0)
@@ -330,6 +331,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                         mbar_wait(&sh.empty[slot], ph ^ 1);
                         if (ppf) { const unsigned long long t = clock64(); p_wait += t - t0; t0 = t; }
                         mbar_expect_tx(&sh.full[slot], (uint32_t)nt * kTile * 4);
+                        if (prof) sh.issue_t[slot] = clock64();
                         bulk_g2s(sh.ring[slot][0], Ab + (size_t)tt * kTile, (uint32_t)nt * kTile * 4, &sh.full[slot]);
                         if (ppf) { const unsigned long long t = clock64(); p_issue += t - t0; }
                         seq++;
@@ -380,7 +382,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
             // profile item 0 (the largest bin): consumer 0 of the leader and of cluster rank 1
             const bool pf = prof && item == 0 && c == 0 && lane == 0 && crank <= 1;
             unsigned long long *pc = prof + (crank == 0 ? 5 : 16);
-            unsigned long long tA = 0, cw_x = 0, cw_full = 0, c_comp = 0, c_red = 0;
+            unsigned long long tA = 0, cw_x = 0, cw_full = 0, c_comp = 0, c_red = 0, lat_sum = 0, lat_n = 0;
             for (int s = 0, kn = 0, kx = T - 1; s < total; s++, kx = kn, kn = (kn + 1 == T) ? 0 : kn + 1) {
                 if (pf) tA = clock64();
                 // x of solver step s-3 (the newest any stream tile needs).  The solver publishes it
@@ -434,8 +436,13 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                             const int nt = min(kChunk, sr.len - off);
                             // every warp observes and releases every chunk (parity-tracked barriers: no
                             // warp may fall a ring lap behind or run one ahead)
+                            const unsigned long long tw0 = pf ? clock64() : 0ull;
                             mbar_wait(&sh.full[slot], ph);
-                            if (pf) { const unsigned long long t = clock64(); cw_full += t - tA; tA = t; }
+                            if (pf) {
+                                const unsigned long long t = clock64();
+                                cw_full += t - tA; tA = t;
+                                if (t - tw0 > 40) { lat_sum += t - sh.issue_t[slot]; lat_n++; }   // waited: ~ latency
+                            }
                             int t = first;
                             for (; t < nt; t += n_sw) {
                                 const int ord = sr.ord0 + off + t, J = ownJ[ord];
@@ -497,6 +504,8 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
             }
             if (pf) {
                 pc[0] = cw_x; pc[1] = cw_full; pc[2] = c_comp; pc[3] = c_red;
+                prof[crank == 0 ? 24 : 20] = lat_sum;
+                prof[crank == 0 ? 25 : 21] = lat_n;
                 if (crank == 0) prof[9] = total;
             }
         } else if (is_leader && total > 0) {
@@ -832,6 +841,8 @@ int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_s
                 h[14] / n, h[14] ? (double)h[12] / h[14] : 0.0, h[14] ? (double)h[13] / h[14] : 0.0);
         fprintf(stderr, "[gs-prof] rank-1 consumer0: wait_x %.0f wait_tile %.0f compute %.0f reduce+send %.0f\n",
                 h[16] / n, h[17] / n, h[18] / n, h[19] / n);
+        fprintf(stderr, "[gs-prof] copy issue->arrival when a consumer had to wait: leader %.0f cyc (%llu waits), rank-1 %.0f cyc (%llu waits)\n",
+                h[25] ? (double)h[24] / h[25] : 0.0, h[25], h[21] ? (double)h[20] / h[21] : 0.0, h[21]);
         cudaFree(prof);
     }
     return e == cudaSuccess ? 1 : -1;
