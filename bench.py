@@ -190,10 +190,10 @@ def run_ours(args, cfg):
     def step():
         if snapshots:
             out = ctx.solve_band_snapshots(geom, band.freqs, snap_dev, cfg.epsilon, cfg.sweeps, cfg.eps_mode,
-                                           full_grid=cfg.full_grid, order=args.order, dr=args.dr, stream=stream)
+                                           full_grid=cfg.full_grid, order=args.order, dr=args.dr, alt=args.alt, stream=stream)
         else:
             out = ctx.solve_band(geom, band.freqs, csm_dev, cfg.epsilon, cfg.sweeps, cfg.eps_mode,
-                                 full_grid=cfg.full_grid, order=args.order, dr=args.dr, stream=stream)
+                                 full_grid=cfg.full_grid, order=args.order, dr=args.dr, alt=args.alt, stream=stream)
         if strong:
             # the one collective: maps + keep bitmasks + counts, all ranks
             mask = ctx.keep_mask(out["n_keep"], out["keep_idx"], stream=stream)
@@ -258,7 +258,7 @@ def run_ours(args, cfg):
         def e2e_call():
             snap_dev.copy_(snap_host, non_blocking=True)
             out = ctx.solve_band_snapshots(geom, band.freqs, snap_dev, cfg.epsilon, cfg.sweeps, cfg.eps_mode,
-                                           full_grid=cfg.full_grid, order=args.order, dr=args.dr, stream=stream)
+                                           full_grid=cfg.full_grid, order=args.order, dr=args.dr, alt=args.alt, stream=stream)
             for key in ("n_keep", "keep_idx", "x_map"):
                 h_out[key].copy_(out[key], non_blocking=True)
     else:
@@ -266,7 +266,7 @@ def run_ours(args, cfg):
 
         def e2e_call():
             ctx.solve_band_host(geom, band.freqs, csm_host, cfg.epsilon, cfg.sweeps, cfg.eps_mode, cfg.full_grid,
-                                out=h_out, stream=stream, order=args.order, dr=args.dr)
+                                out=h_out, stream=stream, order=args.order, dr=args.dr, alt=args.alt)
     e2e_call()
     e2e_ms = []
     for it in range(args.steps):
@@ -308,7 +308,7 @@ def run_ours(args, cfg):
             "dtype": "f32 (PSF + Gauss-Seidel); f64 (DAS map + wavelet threshold)", "data": "synthetic",
             "config": {"workload": workload_desc(cfg), "bins_per_gpu": K,
                        "predictor": "cubic (R19)" if args.order == 3 else "linear (R7)",
-                       "diagonal_removal": bool(args.dr), "parallelism": f"bins-dp{world}",
+                       "diagonal_removal": bool(args.dr), "alternating_sweeps": bool(args.alt), "parallelism": f"bins-dp{world}",
                        "l2_flush": "256 MiB write between timed steps",
                        "inputs": ("snapshot spectra resident in HBM, CSM formed on device (Eq. 1)" if snapshots
                                   else "CSMs resident in HBM")},
@@ -349,6 +349,7 @@ def main():
     ap.add_argument("--input", default="csm", choices=["csm", "snapshots"],
                     help="csm: CSMs resident in HBM (default); snapshots: snapshot spectra, Eq. 1 on device")
     ap.add_argument("--dr", action="store_true", help="CSM diagonal removal (reading R20)")
+    ap.add_argument("--alt", action="store_true", help="alternating sweep directions (reading R21, variant kernel)")
     ap.add_argument("--order", type=int, default=1, choices=[1, 3],
                     help="S3 predictor: 1 linear (reading R7, default), 3 cubic (R19)")
     args = ap.parse_args()

@@ -81,7 +81,7 @@ typedef struct {
     int32_t eps_mode; /* 0 = relative, 1 = absolute (reading R6) */
     int32_t sweeps;   /* Gauss-Seidel sweeps >= 1 from x0 = 0 */
     int32_t flags;    /* DWC_FULL_GRID: keep every node (the paper's "original grid"); DWC_CUBIC;
-                         DWC_DIAG_REMOVAL */
+                         DWC_DIAG_REMOVAL; DWC_ALT_SWEEPS */
 } dwc_params;
 
 #define DWC_FULL_GRID 1
@@ -95,6 +95,10 @@ typedef struct {
  * matching A_ij = (|e_i^H e_j|^2 - sum_m |e_mi|^2 |e_mj|^2) / (M^2 - M), clamped at 0.
  * Uncorrelated microphone noise (a diagonal CSM term) then drops out of the map. */
 #define DWC_DIAG_REMOVAL 4
+/* DWC_ALT_SWEEPS: alternating sweep directions (original DAMAS practice; reading
+ * R21): sweep 2p in ascending row order (Eq. 13-14), sweep 2p+1 descending.  Runs a simpler
+ * one-CTA-per-bin kernel (a fidelity-study variant, not the tuned path). */
+#define DWC_ALT_SWEEPS 8
 #define DWC_MAX_MICS 512
 
 /* Create / destroy a context on CUDA device `device`.  The device must be sm_100
@@ -171,9 +175,9 @@ DWC_API dwc_status dwc_psf(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *g
 /* S7: `sweeps` forward projected Gauss-Seidel sweeps from x0 = 0 on one system.
  * A dev float[n*n] row-major, symmetric (as A~ is, reading R1) with A_ii > 0: only the upper
  * triangle (j >= i) is read, the lower one is taken as its transpose.
- * b dev double[n], x dev float[n] (out). */
+ * flags: 0 or DWC_ALT_SWEEPS; b dev double[n], x dev float[n] (out). */
 DWC_API dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int32_t sweeps,
-                  float *x, void *cuda_stream);
+                  int32_t flags, float *x, void *cuda_stream);
 
 /* ---- multi-GPU gather helpers --------------------------------------- */
 

@@ -52,7 +52,9 @@ def lib():
         _lib.or_wavelet_details.argtypes = [i, _P, _P, _P, i]
         _lib.or_compress.argtypes = [i, _P, d, i, i, _P, _P, _P, _P, i]
         _lib.or_psf.argtypes = geo + [d, i, _P, _P, i]
-        _lib.or_gs.argtypes = [i, _P, _P, i, _P]
+        _lib.or_gs.argtypes = [i, _P, _P, i, _P, i]
+        _lib.or_das_paper.argtypes = geo + [d, _P, _P]
+        _lib.or_psf_paper.argtypes = geo + [d, i, _P, _P]
         _lib.or_csm.argtypes = [i, i, _P, _P]
         _lib.or_solve_bin.argtypes = geo + [d, _P, d, i, i, i, _P, _P, _P, _P]
         _lib.or_solve_band.argtypes = geo + [i, _P, _P, d, i, i, i, _P, _P, _P, _P, i]
@@ -152,6 +154,24 @@ def psf(mic, c0, n, L, z0, cx, cy, freq, keep, dr: bool = False) -> np.ndarray:
     return A
 
 
+def das_paper(mic, c0, n, L, z0, cx, cy, freq, csm) -> np.ndarray:
+    """Eq. 2 with the paper's Eq. 4 focus vector (fidelity variant, not the GPU path)."""
+    mic, g = _geo(mic, c0, n, L, z0, cx, cy)
+    csm = np.ascontiguousarray(csm, dtype=np.complex128)
+    b = np.zeros(n * n)
+    _chk(lib().or_das_paper(*g, float(freq), _p(csm), _p(b)), "das_paper")
+    return b
+
+
+def psf_paper(mic, c0, n, L, z0, cx, cy, freq, keep) -> np.ndarray:
+    """Eq. 10 with the paper's v (Eq. 4) and g (Eq. 7): asymmetric (fidelity variant)."""
+    mic, g = _geo(mic, c0, n, L, z0, cx, cy)
+    keep = np.ascontiguousarray(keep, dtype=np.int32)
+    A = np.zeros((len(keep), len(keep)))
+    _chk(lib().or_psf_paper(*g, float(freq), len(keep), _p(keep), _p(A)), "psf_paper")
+    return A
+
+
 def csm(snap) -> np.ndarray:
     """Eq. 1: snap complex128 [M, I] (or [K, M, I]) -> C complex128 [M, M] ([K, M, M])."""
     snap = np.ascontiguousarray(snap, dtype=np.complex128)
@@ -163,19 +183,21 @@ def csm(snap) -> np.ndarray:
     return C
 
 
-def gs(A, b, sweeps: int) -> np.ndarray:
+def gs(A, b, sweeps: int, alt: bool = False) -> np.ndarray:
+    """Eq. 13-14 forward sweeps; alt: alternating directions (R21)."""
     A = _f64(A)
     b = _f64(b)
     x = np.zeros(len(b))
-    _chk(lib().or_gs(len(b), _p(A), _p(b), int(sweeps), _p(x)), "gs")
+    _chk(lib().or_gs(len(b), _p(A), _p(b), int(sweeps), _p(x), int(bool(alt))), "gs")
     return x
 
 
-def _flags(full_grid, order, dr=False):
-    return (1 if full_grid else 0) | (2 if order == 3 else 0) | (4 if dr else 0)
+def _flags(full_grid, order, dr=False, alt=False):
+    return (1 if full_grid else 0) | (2 if order == 3 else 0) | (4 if dr else 0) | (8 if alt else 0)
 
 
-def solve_bin(mic, c0, n, L, z0, cx, cy, freq, csm, eps, eps_mode, sweeps, full_grid=False, order=1, dr=False):
+def solve_bin(mic, c0, n, L, z0, cx, cy, freq, csm, eps, eps_mode, sweeps, full_grid=False, order=1, dr=False,
+              alt=False):
     """-> (keep, x_map fp64[S], b fp64[S])."""
     mic, g = _geo(mic, c0, n, L, z0, cx, cy)
     csm = np.ascontiguousarray(csm, dtype=np.complex128)
@@ -185,12 +207,13 @@ def solve_bin(mic, c0, n, L, z0, cx, cy, freq, csm, eps, eps_mode, sweeps, full_
     x = np.zeros(S)
     b = np.zeros(S)
     _chk(lib().or_solve_bin(*g, float(freq), _p(csm), float(eps), int(eps_mode), int(sweeps),
-                            _flags(full_grid, order, dr), _p(nk), _p(keep), _p(x), _p(b)), "solve_bin")
+                            _flags(full_grid, order, dr, alt), _p(nk), _p(keep), _p(x), _p(b)), "solve_bin")
     return keep[: nk[0]].copy(), x, b
 
 
 def solve_band(mic, c0, n, L, z0, cx, cy, freqs, csm, eps, eps_mode, sweeps,
-               full_grid=False, n_threads: Optional[int] = None, order: int = 1, dr: bool = False):
+               full_grid=False, n_threads: Optional[int] = None, order: int = 1, dr: bool = False,
+               alt: bool = False):
     """Batched S0..S8 over K bins on a pthread pool.
     -> (n_keep int32[K], keep int32[K,S] (-1 padded), x_map fp64[K,S], b fp64[K,S])."""
     mic, g = _geo(mic, c0, n, L, z0, cx, cy)
@@ -205,17 +228,17 @@ def solve_band(mic, c0, n, L, z0, cx, cy, freqs, csm, eps, eps_mode, sweeps,
     if n_threads is None:
         n_threads = os.cpu_count() or 1
     _chk(lib().or_solve_band(*g, K, _p(freqs), _p(csm), float(eps), int(eps_mode), int(sweeps),
-                             _flags(full_grid, order, dr), _p(nk), _p(keep), _p(x), _p(b), int(n_threads)),
+                             _flags(full_grid, order, dr, alt), _p(nk), _p(keep), _p(x), _p(b), int(n_threads)),
          "solve_band")
     return nk, keep, x, b
 
 
 def solve_band_cfg(band, n_threads: Optional[int] = None, sweeps: Optional[int] = None,
                    full_grid: Optional[bool] = None, eps: Optional[float] = None, order: int = 1,
-                   dr: bool = False):
+                   dr: bool = False, alt: bool = False):
     """Convenience: run the oracle on a synth.Band."""
     cfg = band.cfg
     return solve_band(band.mic_xyz, cfg.c0, cfg.n, cfg.side_len, cfg.z0, cfg.cx, cfg.cy,
                       band.freqs, band.csm, cfg.epsilon if eps is None else eps, cfg.eps_mode,
                       cfg.sweeps if sweeps is None else sweeps,
-                      cfg.full_grid if full_grid is None else full_grid, n_threads, order, dr)
+                      cfg.full_grid if full_grid is None else full_grid, n_threads, order, dr, alt)

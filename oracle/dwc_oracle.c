@@ -331,6 +331,79 @@ int or_psf(int m, const double *mic, double c0, int n, double L, double z0,
 }
 
 /* ------------------------------------------------------------------------ */
+/* The paper-literal beamformer and PSF (SURVEY §8(c) "paper-literal variant", NEXT-4; for the
+ * fidelity discussion of reading R1 only): Eq. 4 v_m(r) = (d_m/|r|) e^{-jk d_m}
+ * for the focus, Eq. 7 g_m(r_s) = (|r_s|/d_m) e^{-jk d_m} (exponent per R2) for
+ * the source, |r| = distance to the array centre (the coordinate origin of the array plane):
+ *   b_P(r) = Re(v(r)^H C v(r)) / M^2 (Eq. 2),   A_P[r][s] = |v(r)^H g(r_s)|^2 / M^2 (Eq. 10).
+ * A_P[r][r] = 1 exactly in exact arithmetic (conj(v_m) g_m = 1), A_P is not symmetric.       */
+static int paper_vectors(int m, const double *mic, double c0, int n, double L, double z0, double cx,
+                         double cy, double freq, int s, double *v, double *g) {
+    double p[3];
+    double k = 2.0 * M_PI * freq / c0;
+    or_grid_point(n, L, z0, cx, cy, s, p);
+    double rn = sqrt(p[0] * p[0] + p[1] * p[1] + p[2] * p[2]);
+    for (int i = 0; i < m; i++) {
+        double dx = p[0] - mic[3 * i + 0], dy = p[1] - mic[3 * i + 1], dz = p[2] - mic[3 * i + 2];
+        double d = sqrt(dx * dx + dy * dy + dz * dz);
+        if (!(d > 0.0)) return OR_ESINGULAR;
+        double c = cos(k * d), sn = sin(k * d);
+        v[2 * i] = (d / rn) * c;  v[2 * i + 1] = -(d / rn) * sn;
+        g[2 * i] = (rn / d) * c;  g[2 * i + 1] = -(rn / d) * sn;
+    }
+    return OR_OK;
+}
+
+int or_das_paper(int m, const double *mic, double c0, int n, double L, double z0,
+                 double cx, double cy, double freq, const double *csm, double *b) {
+    int S = n * n;
+    double *v = (double *)malloc(sizeof(double) * 4 * (size_t)m);
+    if (!v) return OR_ENOMEM;
+    for (int s = 0; s < S; s++) {
+        int rc = paper_vectors(m, mic, c0, n, L, z0, cx, cy, freq, s, v, v + 2 * m);
+        if (rc) { free(v); return rc; }
+        double acc = 0.0;
+        for (int i = 0; i < m; i++) {
+            double ar = v[2 * i], ai = -v[2 * i + 1];
+            for (int j = 0; j < m; j++) {
+                double cr = csm[2 * ((size_t)i * m + j)], ci = csm[2 * ((size_t)i * m + j) + 1];
+                double tr = cr * v[2 * j] - ci * v[2 * j + 1], ti = cr * v[2 * j + 1] + ci * v[2 * j];
+                acc += ar * tr - ai * ti;
+            }
+        }
+        b[s] = acc / ((double)m * (double)m);
+    }
+    free(v);
+    return OR_OK;
+}
+
+int or_psf_paper(int m, const double *mic, double c0, int n, double L, double z0,
+                 double cx, double cy, double freq, int nk, const int *keep, double *A) {
+    double *V = (double *)malloc(sizeof(double) * 4 * (size_t)m * (size_t)nk);
+    if (!V) return OR_ENOMEM;
+    double *G = V + (size_t)2 * m * nk;
+    for (int i = 0; i < nk; i++) {
+        int rc = paper_vectors(m, mic, c0, n, L, z0, cx, cy, freq, keep[i], V + (size_t)2 * m * i,
+                               G + (size_t)2 * m * i);
+        if (rc) { free(V); return rc; }
+    }
+    double m2 = (double)m * (double)m;
+    for (int i = 0; i < nk; i++)
+        for (int j = 0; j < nk; j++) {
+            const double *vi = V + (size_t)2 * m * i, *gj = G + (size_t)2 * m * j;
+            double gr = 0.0, gi = 0.0;
+            for (int q = 0; q < m; q++) {
+                double ar = vi[2 * q], ai = -vi[2 * q + 1];
+                gr += ar * gj[2 * q] - ai * gj[2 * q + 1];
+                gi += ar * gj[2 * q + 1] + ai * gj[2 * q];
+            }
+            A[(size_t)i * nk + j] = (gr * gr + gi * gi) / m2;
+        }
+    free(V);
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------ */
 /* Eq. 1, the step before the path:
  *   C = (1/I) sum_i p_i p_i^H,   p_i = snap[:, i],
  * snap complex128 [m][I] interleaved (row = microphone), C complex128 [m][m];
@@ -358,7 +431,9 @@ int or_csm(int m, int I, const double *snap, double *C) {
  *   x_i^(n+1) = max(x_i^(n) - r_i / A_ii, 0),   x^0 = 0.
  * In-place forward sweep, i ascending; "l" of Eq. 13 = n (R4); fixed sweep
  * count (R18).  The sum runs left to right in fp64.                          */
-int or_gs(int nk, const double *A, const double *b, int sweeps, double *x) {
+/* alt != 0 (reading R21): the original DAMAS practice of alternating
+ * sweep directions: odd-numbered sweeps run i descending, same update.         */
+int or_gs(int nk, const double *A, const double *b, int sweeps, double *x, int alt) {
     if (nk < 1 || sweeps < 1) return OR_EINVAL;
     for (int i = 0; i < nk; i++) {
         double aii = A[(size_t)i * nk + i];
@@ -366,7 +441,9 @@ int or_gs(int nk, const double *A, const double *b, int sweeps, double *x) {
         x[i] = 0.0;
     }
     for (int it = 0; it < sweeps; it++) {
-        for (int i = 0; i < nk; i++) {
+        const int back = alt && (it & 1);
+        for (int ii = 0; ii < nk; ii++) {
+            const int i = back ? nk - 1 - ii : ii;
             const double *row = A + (size_t)i * nk;
             double r = 0.0;
             for (int j = 0; j < nk; j++) r += row[j] * x[j];
@@ -383,7 +460,7 @@ int or_gs(int nk, const double *A, const double *b, int sweeps, double *x) {
 /* One bin, S1..S8.  keep (S ints) ascending, first n_keep valid.  x_map (S)
  * is the source power on the full grid, zero off the kept set (S8).
  * flags: bit 0 full grid (keep every node), bit 1 cubic predictor (R19),
- * bit 2 diagonal removal (R20).                                                */
+ * bit 2 diagonal removal (R20), bit 3 alternating sweep directions (R21).         */
 int or_solve_bin(int m, const double *mic, double c0, int n, double L, double z0,
                  double cx, double cy, double freq, const double *csm,
                  double eps, int eps_mode, int sweeps, int flags,
@@ -407,7 +484,7 @@ int or_solve_bin(int m, const double *mic, double c0, int n, double L, double z0
     if (rc == OR_OK) rc = or_psf(m, mic, c0, n, L, z0, cx, cy, freq, nk, keep, A, flags & 4);
     if (rc == OR_OK) {
         for (int i = 0; i < nk; i++) bt[i] = b[keep[i]];   /* S6: b~ = b[keep] */
-        rc = or_gs(nk, A, bt, sweeps, xt);
+        rc = or_gs(nk, A, bt, sweeps, xt, flags & 8);
     }
     if (rc == OR_OK) {
         for (int s = 0; s < S; s++) x_map[s] = 0.0;         /* S8 embed */

@@ -25,6 +25,7 @@ SOURCES = {
     "k_gs.cu": [],
     "k_keep.cu": [],
     "k_csm.cu": [],
+    "k_gs_alt.cu": [],
 }
 
 

@@ -183,7 +183,8 @@ dwc_status check_params(const dwc_params *p) {
     if (!(p->epsilon > 0.0) || !finite(p->epsilon)) return fail(DWC_EINVAL, "epsilon must be > 0");
     if (p->eps_mode != 0 && p->eps_mode != 1) return fail(DWC_EINVAL, "eps_mode must be 0 or 1");
     if (p->sweeps < 1) return fail(DWC_EINVAL, "sweeps must be >= 1");
-    if (p->flags & ~(DWC_FULL_GRID | DWC_CUBIC | DWC_DIAG_REMOVAL)) return fail(DWC_EINVAL, "unknown flags 0x%x", p->flags);
+    if (p->flags & ~(DWC_FULL_GRID | DWC_CUBIC | DWC_DIAG_REMOVAL | DWC_ALT_SWEEPS))
+        return fail(DWC_EINVAL, "unknown flags 0x%x", p->flags);
     return DWC_OK;
 }
 
@@ -362,11 +363,16 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
     CU(cudaMemsetAsync(x_map, 0, sizeof(float) * (size_t)n_bins * S, st));
     CU(cudaMemsetAsync(ctx->counter.p, 0, 64, st));
     ev(ctx, 5, st);
+    if (p->flags & DWC_ALT_SWEEPS) {
+        LAUNCH(launch_gs_alt(n_bins, (BinLayout *)ctx->lay.p, max_sp, (float *)ctx->A.p, (double *)ctx->bt.p,
+                             p->sweeps, nullptr, x_map, keep_idx, S, st));
+    } else {
     LAUNCH(launch_gs_prep(n_bins, max_sp, (BinLayout *)ctx->lay.p, (float *)ctx->A.p, (double *)ctx->bt.p,
                           ctx->packets.p, st));
     LAUNCH(launch_gs(n_items, (int *)ctx->items.p, (BinLayout *)ctx->lay.p, max_sp, ystride, (int *)ctx->counter.p,
                      (float *)ctx->A.p, ctx->packets.p, p->sweeps, nullptr, x_map, keep_idx, S,
                      ctx->num_sms, st));
+    }
     ev(ctx, 6, st);
     // warnings (host, Eq. 24)
     if (warn) {
@@ -624,13 +630,14 @@ dwc_status dwc_psf(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, dou
     return DWC_OK;
 }
 
-dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int32_t sweeps, float *x,
-                  void *cuda_stream) {
+dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int32_t sweeps, int32_t flags,
+                  float *x, void *cuda_stream) {
     dwc_status s;
     if ((s = check_ctx(ctx))) return s;
     if (n < 1) return fail(DWC_EINVAL, "n must be >= 1");
     if (sweeps < 1) return fail(DWC_EINVAL, "sweeps must be >= 1");
     if (!A || !b || !x) return fail(DWC_EINVAL, "NULL device buffer");
+    if (flags & ~DWC_ALT_SWEEPS) return fail(DWC_EINVAL, "unknown flags 0x%x", flags);
     const int sp = (n + 31) & ~31;
     if (gs_smem_bytes(sp, gs_ystride(n)) > 227 * 1024)
         return fail(DWC_EINVAL, "n = %d exceeds the on-chip x capacity", n);
@@ -654,6 +661,11 @@ dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int3
     CU(cudaMemsetAsync(ctx->gs_b.p, 0, sizeof(double) * sp, st));
     CU(cudaMemcpyAsync(ctx->gs_b.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     CU(cudaMemsetAsync(ctx->counter.p, 0, 64, st));
+    if (flags & DWC_ALT_SWEEPS) {
+        LAUNCH(launch_gs_alt(1, (BinLayout *)ctx->lay.p, sp, Ap, (double *)ctx->gs_b.p, sweeps, x, nullptr, nullptr,
+                             0, st));
+        return DWC_OK;
+    }
     LAUNCH(launch_gs_prep(1, sp, (BinLayout *)ctx->lay.p, Ap, (double *)ctx->gs_b.p, ctx->packets.p, st));
     LAUNCH(launch_gs((int)items.size() / gs_item_ints(), (int *)ctx->items.p, (BinLayout *)ctx->lay.p, sp,
                      gs_ystride(n),

@@ -174,6 +174,11 @@ int gs_packet_bytes();
 int launch_gs_prep(int n_bins, int max_sp, const BinLayout *lay_dev, const float *A, const double *bt,
                    void *packets, cudaStream_t st);
 
+// S7 with alternating sweep directions (k_gs_alt.cu, reading R21): one CTA per bin on the same
+// symmetric-packed A~ and b~ (bt, fp64, zero padded to sp).
+int launch_gs_alt(int n_bins, const BinLayout *lay_dev, int max_sp, const float *A, const double *bt, int sweeps,
+                  float *x_out, float *x_map, const int32_t *keep_idx, int S, cudaStream_t st);
+
 // Keep-set bitmasks (k_keep.cu): ceil(S/32) uint32 words per bin.
 int launch_keep_mask(int n_bins, int S, const int32_t *n_keep, const int32_t *keep_idx, uint32_t *mask,
                      cudaStream_t st);

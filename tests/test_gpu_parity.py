@@ -215,17 +215,17 @@ def test_gs_parity_on_oracle_system(ctx, torch_cuda, oracle_lib, nk, sweeps):
 
 
 # ---------------------------------------------------------------------------- end to end
-def _e2e(ctx, torch, oracle_lib, band, sweeps=None, full=False, check_b=True, order=1, dr=False):
+def _e2e(ctx, torch, oracle_lib, band, sweeps=None, full=False, check_b=True, order=1, dr=False, alt=False):
     cfg = band.cfg
     g = geom_of(band)
     sw = sweeps or cfg.sweeps
     out = ctx.solve_band(g, band.freqs, torch.from_numpy(band.csm).cuda(), cfg.epsilon, sw, cfg.eps_mode,
-                         full_grid=full, want_b=True, order=order, dr=dr)
+                         full_grid=full, want_b=True, order=order, dr=dr, alt=alt)
     nk = out["n_keep"].cpu().numpy()
     keep = out["keep_idx"].cpu().numpy()
     x = out["x_map"].cpu().numpy()
     bm = out["b_map"].cpu().numpy()
-    rnk, rkeep, rx, rb = oracle_lib.solve_band_cfg(band, sweeps=sw, full_grid=full, order=order, dr=dr)
+    rnk, rkeep, rx, rb = oracle_lib.solve_band_cfg(band, sweeps=sw, full_grid=full, order=order, dr=dr, alt=alt)
     for k in range(len(band.freqs)):
         assert rel_l2(bm[k], rb[k]) < TOL_B
         assert nk[k] == rnk[k], (k, nk[k], rnk[k])
@@ -413,3 +413,26 @@ def test_psf_dr_parity(ctx, torch_cuda, oracle_lib, m, n, nk):
 def test_e2e_cfg2_diag_removal(ctx, torch_cuda, oracle_lib):
     """NEXT-2 end to end: cfg2's 20 dB noisy CSMs with the diagonal removed."""
     _e2e(ctx, torch_cuda, oracle_lib, synth.make_band("cfg2"), dr=True)
+
+
+# ---------------------------------------------------------------------------- NEXT-4: alternating sweeps
+@pytest.mark.parametrize("nk,sweeps", [(1, 3), (31, 40), (33, 41), (130, 100), (300, 200)])
+def test_gs_alternating_parity(ctx, torch_cuda, oracle_lib, nk, sweeps):
+    """Alternating forward/backward sweeps (R21) on oracle PSF systems (odd sweep counts end on
+    a forward sweep, even ones on a backward sweep)."""
+    torch = torch_cuda
+    g = small_geom(24, 19, 3)
+    rng = np.random.default_rng(nk)
+    keep = np.sort(rng.choice(g.S, size=nk, replace=False)).astype(np.int32)
+    A = oracle_lib.psf(*oracle_args(g), 3000.0, keep)
+    b = A @ np.abs(rng.standard_normal(nk)) + 0.01 * rng.standard_normal(nk)
+    ref = oracle_lib.gs(A, b, sweeps, alt=True)
+    x = ctx.gs(torch.from_numpy(A.astype(np.float32)).cuda(), torch.from_numpy(b).cuda(), sweeps,
+               alt=True).cpu().numpy()
+    assert x.min() >= 0
+    assert rel_l2(x, ref) < TOL_X
+    assert abs(x.sum() - ref.sum()) < TOL_P * ref.sum()
+
+
+def test_e2e_cfg2_alternating_sweeps(ctx, torch_cuda, oracle_lib):
+    _e2e(ctx, torch_cuda, oracle_lib, synth.make_band("cfg2", bins=[0, 4, 7]), alt=True)
