@@ -6,33 +6,35 @@
 // Row order and sweep order are kept exactly; only the summation order of each row dot
 // differs from the oracle (fp32 A~ and fp32 partial dots; residual against fp64 b~).
 //
-// Block formulation (B = 32 rows, T = sp/32 blocks): solver step j solves block k = j mod T.
-//   r_{I_k} = P_k + A[I_k, I_{k-1}] x_{k-1}^new - b_{I_k},
-//   P_k    = sum over column blocks J != k-1 of A[I_k, I_J] x_J   (in-block: old values)
-// P_k is produced by "stream" warps WHILE block k-1 is being solved (stream step s = k runs
-// concurrently with solver step s-1); only the 32x32 sub-diagonal product and the in-block
-// recurrence are on the critical path.  In-block recurrence, one warp, "step form":
+// Block formulation (B = 32 rows, T = sp/32 blocks): solver step j solves block k = j mod T
+// with the residual r_{I_k} = P_k + (increments of the blocks solved in the last two steps)
+// - b_{I_k}.  P_k is produced by "stream" warps ahead of the solver.  A~ is symmetric and only
+// its upper tiles are stored (dwc_internal.cuh layout), so the contributions to row block kn are
+//   row use   U(kn, J) x_J^old, J > kn (minus the two blocks below)      stream, step kn
+//   scatter   U(kn-3, J)^T x_{kn-3}^new, J >= kn  -> P_kn (J = kn) or y_J stream, step kn
+//   L, LL     A[kn, kn-1], A[kn, kn-2]: old-x products by the leader's L warp, increments by
+//             the solver's role-1 / role-2 lanes while it solves those blocks
+//   D         old-x product by the leader's D warp; the in-block recurrence by the solver
+// so the stream depends only on x of solver step s-3 and runs up to two steps ahead.
+// In-block recurrence, one warp, "step form":
 //   w_l = -r_l / A_ll;  delta_t = max(w_t, -x_t)  (x_t + delta_t = max(x_t + w_t, 0))
 //   w_l -= (A_lt / A_ll) delta_t for all lanes;   x_t += delta_t.
 //
 // B200 mapping
-//  * A~_k stored as 32x32 fp32 tiles, column-major inside a tile, row-block-major:
-//    tile (I,J) at ((I*T + J) * 1024) floats, element (32I+r, 32J+c) at [c*32 + r].
-//  * A CTA = warp 0 solver, warp 1 TMA producer, warps 2..7 consumers.  The producer
-//    streams this CTA's tiles of each row block with cp.async.bulk (4 KB, mbarrier
-//    complete_tx) into a kStages-deep shared-memory ring, running ahead of the consumers
-//    across steps (tiles do not depend on x); consumers compute 32-row partial dots with
-//    LDS.128 (conflict-free on the column-major tile) and release the slots.
-//  * Clusters of kCl = 4 CTAs.  A work item gives the cluster either one large bin
-//    (sub-group of g = 4 CTAs), two medium bins (g = 2) or four small bins (g = 1).
-//    Inside a sub-group every CTA keeps a full copy of x in shared memory; stream tiles of
-//    a row block are dealt round-robin over the g CTAs; each CTA reduces its consumer
-//    warps' partials and pushes 32 floats into the leader CTA's shared memory over DSMEM
-//    (st.shared::cluster + remote mbarrier arrive, release.cluster); the leader's solver
-//    broadcasts each new x block the same way.  No grid-wide or cluster barrier inside the
-//    sweep loop; cluster barriers only between work items.
-//  * g depends on S~ only (host), so a bin's result is bit-identical whatever else is in
-//    the batch (and on however many GPUs the band is sharded); items run largest first.
+//  * A CTA = warp 0 solver, warp 1 bulk-copy producer, warp 4 staging producer (leader), warps
+//    2,3,5,6,7 consumers (in the leader 6 = D product, 7 = L/LL products).  The producer streams
+//    this CTA's runs of each step with cp.async.bulk (<= 3 tiles per copy, mbarrier complete_tx)
+//    into a shared-memory ring (3-4 slots; non-leader CTAs also use the staging area: 7), running
+//    ahead across steps (tiles do not depend on x) and prefetching runs 4 steps ahead into L2.
+//  * Clusters of kCl = 4 CTAs.  A work item gives the cluster either one large bin (sub-group of
+//    g = 4 CTAs), two medium bins (g = 2) or four small bins (g = 1).  Inside a sub-group every
+//    CTA keeps a full copy of x in shared memory; column blocks are owned by CTAs in a periodic
+//    pattern weighted by stream warps (dwc_internal.cuh own_of); every consumer warp sends its 32
+//    partial row sums to the leader with st.async (DSMEM, complete_tx on the leader's
+//    P-ready barrier); the leader's D warp forwards each new x block the same way.  No grid or
+//    cluster barrier inside the sweep loop; cluster barriers only between work items.
+//  * g depends on S~ only (host), so a bin's result is bit-identical whatever else is in the
+//    batch (and on however many GPUs the band is sharded); items run largest first (LPT).
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
