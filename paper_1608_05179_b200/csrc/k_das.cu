@@ -89,6 +89,10 @@ int launch_steer(const Geo &g, const double *dist, const double *amp, const doub
 // Re(conj(e_m) W_m) over the rows and the warps in fixed order (deterministic).  fp64 CUDA
 // cores (B200 DFMA and DMMA peak are the same, ~36 TFLOP/s measured).
 constexpr int kDasThreads = 256;
+#ifndef DAS_UNROLL
+#define DAS_UNROLL 4
+#endif
+constexpr int kDasUnroll = DAS_UNROLL;
 constexpr int kDasWarps = kDasThreads / 32;
 
 __device__ __forceinline__ void cmac(double2 &acc, double2 a, double2 b) {  // acc += a*b
@@ -104,7 +108,7 @@ template <int PPL, bool kBoth>
 __device__ __forceinline__ void das_rows(const double2 *__restrict__ Cw, const double2 *__restrict__ Es, int Mp,
                                          int n0, int n1, int lane, double2 Wa[4][PPL], double2 Wb[4][PPL]) {
     constexpr int P = 32 * PPL;
-#pragma unroll 2
+#pragma unroll kDasUnroll
     for (int n = n0; n < n1; n++) {
         double2 e[PPL];
 #pragma unroll
