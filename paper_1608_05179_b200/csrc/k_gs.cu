@@ -23,8 +23,8 @@
 // B200 mapping
 //  * A CTA = warp 0 solver, warp 1 bulk-copy producer, warp 4 staging producer (leader), warps
 //    2,3,5,6,7 consumers (in the leader 6 = D product, 7 = L/LL products).  The producer streams
-//    this CTA's runs of each step with cp.async.bulk (<= 3 tiles per copy, mbarrier complete_tx)
-//    into a shared-memory ring (3-4 slots; non-leader CTAs also use the staging area: 7), running
+//    this CTA's runs of each step with cp.async.bulk (<= 6 tiles per copy, mbarrier complete_tx)
+//    into a shared-memory ring (2 slots of 24 KB; non-leader CTAs also use the staging area: 3), running
 //    ahead across steps (tiles do not depend on x) and prefetching runs 4 steps ahead into L2.
 //  * Clusters of kCl = 4 CTAs.  A work item gives the cluster either one large bin (sub-group of
 //    g = 4 CTAs), two medium bins (g = 2) or four small bins (g = 1).  Inside a sub-group every
@@ -49,8 +49,14 @@ constexpr int kCl = 4;             // cluster size
 constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
 constexpr int kCons = kWarps - 3;  // consumer warps (3..7)
-constexpr int kChunk = 3;          // tiles per ring slot (one contiguous bulk copy)
-constexpr int kRing = 4;           // ring slots
+#ifndef GS_CHUNK
+#define GS_CHUNK 6
+#endif
+#ifndef GS_RING
+#define GS_RING 2
+#endif
+constexpr int kChunk = GS_CHUNK;   // tiles per ring slot (one contiguous bulk copy)
+constexpr int kRing = GS_RING;     // stream ring slots of the leader
 #ifndef GS_PF
 #define GS_PF 4
 #endif
@@ -79,19 +85,20 @@ struct GsItem {
     int bin[kCl];   // bins of the sub-groups (-1 = idle)
 };
 
-static_assert(kChunk == 3, "a staging slot (L, D, LL) doubles as one stream ring slot");
+constexpr int kRsTiles = kRing * kChunk + kStg * 3;   // stream ring + staging area (tiles)
+constexpr int kNringMax = kRsTiles / kChunk;          // stream slots of a non-leader CTA
 struct __align__(128) GsSmem {
-    // stream ring slots 0..kRing-1; slots kRing..kRing+kStg-1 are the leader's staging slots
-    // ([step j % kStg]: L_j, D_j, LL_{j+2}) and extra stream slots in the other CTAs
-    float ring[kRing + kStg][kChunk][kTile];
+    // stream slot p = tiles [p*kChunk, (p+1)*kChunk); in the leader the tiles from kRing*kChunk on
+    // are the staging slots (slot q = 3 tiles: L_j, D_j, LL_{j+2}), in the other CTAs more stream slots
+    float rs[kRsTiles][kTile];
     GsPacket pk[kStg];                 // solver packet of the staged block
     float pr[2][kCl][kCons][32];       // leader: partial row sums of every consumer warp of the sub-group
-    unsigned long long full[kRing + kStg], empty[kRing + kStg];
+    unsigned long long full[kNringMax], empty[kNringMax];
     unsigned long long stg_full[kStg], stg_empty[kStg];
     unsigned long long pready[2];      // leader: 1 arrival + g*kCons*128 tx bytes per step
     unsigned long long xr[2];          // leader: solver arrival; others: 1 arrival + 128 tx
     int item;
-    unsigned long long issue_t[kRing + kStg];   // profiling: clock64 at which each slot's copy was issued
+    unsigned long long issue_t[kNringMax];   // profiling: clock64 at which each slot's copy was issued
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -273,7 +280,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
         const int sg = (int)crank / g, rg = (int)crank % g;
         const uint32_t leader = (uint32_t)(sg * g);
         const bool is_leader = (rg == 0);
-        const int nring = is_leader ? kRing : kRing + kStg;   // non-leaders stream into the staging slots too
+        const int nring = is_leader ? kRing : kNringMax;   // non-leaders stream into the staging area too
         const int bin = IT.bin[sg];
         BinLayout L = {0, 0, 0, 0, 0, 0, 0};
         if (bin >= 0) L = lay[bin];
@@ -293,7 +300,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
         }
         if (tid == 0) {
             const int n_sw = is_leader ? kCons - 2 : kCons;
-            for (int i = 0; i < kRing + kStg; i++) {
+            for (int i = 0; i < kNringMax; i++) {
                 mbar_init(&sh.full[i], 1);
                 mbar_init(&sh.empty[i], (uint32_t)n_sw);   // every stream warp releases every chunk
             }
@@ -334,7 +341,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                         if (ppf) { const unsigned long long t = clock64(); p_wait += t - t0; t0 = t; }
                         mbar_expect_tx(&sh.full[slot], (uint32_t)nt * kTile * 4);
                         if (prof) sh.issue_t[slot] = clock64();
-                        bulk_g2s(sh.ring[slot][0], Ab + (size_t)tt * kTile, (uint32_t)nt * kTile * 4, &sh.full[slot]);
+                        bulk_g2s(&sh.rs[slot * kChunk][0], Ab + (size_t)tt * kTile, (uint32_t)nt * kTile * 4, &sh.full[slot]);
                         if (ppf) { const unsigned long long t = clock64(); p_issue += t - t0; }
                         seq++;
                         if (++slot == (uint32_t)nring) { slot = 0; ph ^= 1; }
@@ -351,9 +358,9 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                     const int kn2 = (kn + 2 >= T) ? kn + 2 - T : kn + 2;   // (mod T again for T < 2)
                     mbar_wait(&sh.stg_empty[sl], ((s / kStg) & 1) ^ 1);
                     mbar_expect_tx(&sh.stg_full[sl], 3 * kTile * 4 + kPacketBytes);
-                    bulk_g2s(sh.ring[kRing + sl][0], Ab + (size_t)(T + kn) * kTile, kTile * 4, &sh.stg_full[sl]);   // L_kn
-                    bulk_g2s(sh.ring[kRing + sl][1], Ab + (size_t)kn * kTile, kTile * 4, &sh.stg_full[sl]);         // D_kn
-                    bulk_g2s(sh.ring[kRing + sl][2], Ab + (size_t)(2 * T + kn2 % T) * kTile, kTile * 4,
+                    bulk_g2s(sh.rs[kRing * kChunk + 3 * (sl) + 0], Ab + (size_t)(T + kn) * kTile, kTile * 4, &sh.stg_full[sl]);   // L_kn
+                    bulk_g2s(sh.rs[kRing * kChunk + 3 * (sl) + 1], Ab + (size_t)kn * kTile, kTile * 4, &sh.stg_full[sl]);         // D_kn
+                    bulk_g2s(sh.rs[kRing * kChunk + 3 * (sl) + 2], Ab + (size_t)(2 * T + kn2 % T) * kTile, kTile * 4,
                              &sh.stg_full[sl]);                                                      // LL_{kn+2}
                     bulk_g2s(&sh.pk[sl], pkb + kn, kPacketBytes, &sh.stg_full[sl]);
                 }
@@ -411,12 +418,12 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                         // (tile staged at step s-1) for the next step, while x_kx is still old
 #pragma unroll
                         for (int q = 0; q < 4; q++) { acc[q] = lcarry[q]; lcarry[q] = 0.f; }
-                        tile_dot(sh.ring[kRing + b][0], xs + 32 * kx, rq, cq, acc);
-                        if (T >= 3 && s >= 1) tile_dot(sh.ring[kRing + (s - 1) % kStg][2], xs + 32 * kx, rq, cq, lcarry);
+                        tile_dot(sh.rs[kRing * kChunk + 3 * (b) + 0], xs + 32 * kx, rq, cq, acc);
+                        if (T >= 3 && s >= 1) tile_dot(sh.rs[kRing * kChunk + 3 * ((s - 1) % kStg) + 2], xs + 32 * kx, rq, cq, lcarry);
                         __syncwarp();
                         if (lane == 0 && s >= 1) mbar_arrive_local(&sh.stg_empty[(s - 1) % kStg]);
                     } else {
-                        if (T >= 2) tile_dot(sh.ring[kRing + b][1], xs + 32 * kn, rq, cq, acc);
+                        if (T >= 2) tile_dot(sh.rs[kRing * kChunk + 3 * (b) + 1], xs + 32 * kn, rq, cq, acc);
                         __syncwarp();
                         if (lane == 0) mbar_arrive_local(&sh.stg_empty[b]);
                     }
@@ -448,7 +455,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                             int t = first;
                             for (; t < nt; t += n_sw) {
                                 const int ord = sr.ord0 + off + t, J = ownJ[ord];
-                                const float *tile = sh.ring[slot][t];
+                                const float *tile = &sh.rs[slot * kChunk + t][0];
                                 if (sg == 0) {
                                     tile_dot(tile, xs + 32 * J, rq, cq, acc);
                                 } else {
@@ -580,10 +587,10 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 const int kn1 = (k + 1 == T) ? 0 : k + 1;   // next block
                 const bool has_next = (j + 1 < total);
                 if (pf) tA = clock64();
-                const float *Dt = sh.ring[kRing + sl][1];
+                const float *Dt = sh.rs[kRing * kChunk + 3 * (sl) + 1];
                 // role 1 streams the next block's L tile (with no next step it re-reads Dt, unused),
                 // role 2 the LL tile staged with this step
-                const float *tp = (role1 && has_next) ? sh.ring[kRing + sl1][0] : (role2 ? sh.ring[kRing + sl][2] : Dt);
+                const float *tp = (role1 && has_next) ? sh.rs[kRing * kChunk + 3 * (sl1) + 0] : (role2 ? sh.rs[kRing * kChunk + 3 * (sl) + 2] : Dt);
                 // ---- critical path: P_k -> residual -> publish x_{k-1} -> recurrence
                 mbar_wait(&sh.pready[b], (j >> 1) & 1);
                 if (pf) { const unsigned long long t = clock64(); w_p += t - tA; tA = t; }
