@@ -846,6 +846,8 @@ int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_s
                 " | consumer0: wait_x %.0f wait_tile %.0f compute %.0f reduce+send %.0f\n",
                 h[9], n_clusters * kCl, h[0] / n, h[1] / n, h[10] / n, h[2] / n, h[3] / n, h[11] / n,
                 (h[4] - h[11]) / n, h[5] / n, h[6] / n, h[7] / n, h[8] / n);
+        fprintf(stderr, "[gs-prof] dynamic smem %zu B per CTA (GsSmem %zu), %d clusters of %d\n", smem, sizeof(GsSmem),
+                n_clusters, kCl);
         fprintf(stderr, "[gs-prof] producer: chunks=%llu (%.1f/step) wait_empty %.0f issue %.0f cyc/chunk\n", h[14],
                 h[14] / n, h[14] ? (double)h[12] / h[14] : 0.0, h[14] ? (double)h[13] / h[14] : 0.0);
         fprintf(stderr, "[gs-prof] rank-1 consumer0: wait_x %.0f wait_tile %.0f compute %.0f reduce+send %.0f\n",
