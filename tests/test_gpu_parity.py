@@ -436,3 +436,35 @@ def test_gs_alternating_parity(ctx, torch_cuda, oracle_lib, nk, sweeps):
 
 def test_e2e_cfg2_alternating_sweeps(ctx, torch_cuda, oracle_lib):
     _e2e(ctx, torch_cuda, oracle_lib, synth.make_band("cfg2", bins=[0, 4, 7]), alt=True)
+
+
+def test_errors_flags_and_new_entry_points(ctx, torch_cuda):
+    """Unknown flag bits, bad snapshot counts, sizes over the on-chip capacity, bad stage flags."""
+    torch = torch_cuda
+    import ctypes as C
+
+    from paper_1608_05179_b200 import DwcError
+    from paper_1608_05179_b200.dwc import Array, Grid, Params, lib
+    band = synth.make_band("cfg1")
+    g = geom_of(band)
+    csm = torch.from_numpy(band.csm).cuda()
+    arr, grid = g.c_array(), g.c_grid()
+    nk = torch.empty(1, dtype=torch.int32, device="cuda")
+    keep = torch.empty((1, g.S), dtype=torch.int32, device="cuda")
+    x = torch.empty((1, g.S), dtype=torch.float32, device="cuda")
+    f = np.array(band.freqs, dtype=np.float64)
+    prm = Params(0.1, 0, 5, 16)   # unknown flag bit
+    rc = lib().dwc_solve_band(ctx._h, C.byref(arr), C.byref(grid), C.byref(prm), 1, f.ctypes.data,
+                              csm.data_ptr(), nk.data_ptr(), keep.data_ptr(), x.data_ptr(), None, None,
+                              torch.cuda.current_stream().cuda_stream)
+    assert rc == -1 and b"flags" in lib().dwc_last_error()
+    with pytest.raises(DwcError):
+        ctx.solve_band_snapshots(g, band.freqs, torch.zeros((1, 16, 0), dtype=torch.complex128).cuda(), 0.1, 5)
+    with pytest.raises(DwcError):   # S~ beyond the GS kernel's on-chip x capacity (rejected before any launch)
+        n = 20000
+        ctx.gs(torch.zeros((n, n), dtype=torch.float32).cuda(), torch.zeros(n, dtype=torch.float64).cuda(), 1)
+    # keep masks: n_bins 0 is a no-op, S < 1 rejected
+    assert lib().dwc_keep_mask(ctx._h, 0, 10, None, None, None, None) == 0
+    assert lib().dwc_keep_mask(ctx._h, 1, 0, nk.data_ptr(), keep.data_ptr(), x.data_ptr(), None) == -1
+    # the context still works
+    ctx.solve_band(g, band.freqs, csm, 0.1, 5, dr=True, order=3)
