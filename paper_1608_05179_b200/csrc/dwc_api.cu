@@ -371,7 +371,7 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
                           ctx->packets.p, st));
     LAUNCH(launch_gs(n_items, (int *)ctx->items.p, (BinLayout *)ctx->lay.p, max_sp, ystride, (int *)ctx->counter.p,
                      (float *)ctx->A.p, ctx->packets.p, p->sweeps, nullptr, x_map, keep_idx, S,
-                     ctx->num_sms, st));
+                     ctx->num_sms, items.data(), lay.data(), st));
     }
     ev(ctx, 6, st);
     // warnings (host, Eq. 24)
@@ -670,7 +670,7 @@ dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int3
     LAUNCH(launch_gs((int)items.size() / gs_item_ints(), (int *)ctx->items.p, (BinLayout *)ctx->lay.p, sp,
                      gs_ystride(n),
                      (int *)ctx->counter.p, Ap, ctx->packets.p, sweeps, x, nullptr, nullptr, 0, ctx->num_sms,
-                     st));
+                     items.data(), &lay, st));
     return DWC_OK;
 }
 

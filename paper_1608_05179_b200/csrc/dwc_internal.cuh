@@ -164,9 +164,10 @@ int gs_ystride(int nk);
 int gs_cluster_size();
 int gs_item_ints();
 int gs_group_size(int nk);
+// items_host / lay_host (nullable): host copies used to size the L2 prefetch window.
 int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_sp, int ystride, int *counter,
               const float *A, const void *packets, int sweeps, float *x_out, float *x_map, const int32_t *keep_idx,
-              int S, int num_sms, cudaStream_t st);
+              int S, int num_sms, const int *items_host, const BinLayout *lay_host, cudaStream_t st);
 
 // Per-block solver packets (1/A_ii, within-group scaled coefficients, b~ block) for the GS
 // kernel: gs_packet_bytes() bytes per 32-row block, bin k's packets at v_off/32.

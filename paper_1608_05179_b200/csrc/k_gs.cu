@@ -61,6 +61,7 @@ constexpr int kRing = GS_RING;     // stream ring slots of the leader
 #define GS_PF 4
 #endif
 constexpr int kPf = GS_PF;         // L2 prefetch distance of the stream runs, in steps
+constexpr double kL2WindowBytes = 48.0 * 1024 * 1024;   // L2 share the prefetch window may use
 constexpr int kTile = 1024;        // floats per tile
 #ifndef GS_KSTG
 #define GS_KSTG 3
@@ -254,7 +255,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout *__restrict__ lay,
                   int *__restrict__ counter, const float *__restrict__ A, const GsPacket *__restrict__ packets,
                   int sweeps, float *__restrict__ x_out, float *__restrict__ x_map,
-                  const int32_t *__restrict__ keep_idx, int S, int xcap, int ystride,
+                  const int32_t *__restrict__ keep_idx, int S, int xcap, int ystride, int pf,
                   unsigned long long *__restrict__ prof) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     GsSmem &sh = *reinterpret_cast<GsSmem *>(smem_raw);
@@ -322,11 +323,11 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 uint32_t seq = 0, slot = 0, ph = 0;
                 const bool ppf = prof && item == 0 && crank == 0;   // item 0 = the largest bin (LPT)
                 unsigned long long t0 = 0, p_wait = 0, p_issue = 0;
-                // the row runs of step s + kPf are prefetched into L2 while step s is copied into the
+                // the row runs of step s + pf are prefetched into L2 while step s is copied into the
                 // ring: the ring then only has to cover L2 latency, not HBM latency
-                for (int s = 0, kn = 0, kp = kPf % T; s < total;
+                for (int s = 0, kn = 0, kp = (T > 0 ? pf % T : 0); s < total;
                      s++, kn = (kn + 1 == T) ? 0 : kn + 1, kp = (kp + 1 == T) ? 0 : kp + 1) {
-                    if (kPf > 0 && s + kPf < total) {
+                    if (pf > 0 && s + pf < total) {
                         const Seg *sp = segt + 2 * kp;
                         for (int sg = 0; sg < 2; sg++)
                             if (sp[sg].len > 0)
@@ -803,7 +804,7 @@ int gs_group_size(int nk) { return nk >= 768 ? 4 : (nk >= 384 ? 2 : 1); }
 int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_sp, int ystride, int *counter,
               const float *A,
               const void *packets, int sweeps, float *x_out, float *x_map, const int32_t *keep_idx, int S,
-              int num_sms, cudaStream_t st) {
+              int num_sms, const int *items_host, const BinLayout *lay_host, cudaStream_t st) {
     // DWC_GS_PROFILE=1: clock64 breakdown of the first CTA's solver / consumer warp (stderr).
     static const bool profile = getenv("DWC_GS_PROFILE") != nullptr;
     unsigned long long *prof = nullptr;
@@ -833,9 +834,26 @@ int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_s
     if (n_clusters > n_items) n_clusters = n_items;
     if (n_clusters < 1) n_clusters = 1;
     cfg.gridDim = dim3(n_clusters * kCl);
+    // L2 prefetch distance: the runs are prefetched kPf steps ahead only while the prefetch and
+    // scatter windows ((kPf + 3) steps of row runs) of the bins running at once fit in a share of
+    // L2.  Full-grid systems (cfg4: 64 bins of T = 319) do not fit: the prefetched tiles were
+    // evicted before use and DRAM read 3.3x the algorithmic bytes (profiles/r01/next).
+    int pf = kPf;
+    if (kPf > 0 && items_host && lay_host) {
+        const int ni = gs_item_ints();
+        double win = 0.0;
+        for (int it = 0; it < std::min(n_items, n_clusters); it++)
+            for (int q = 0; q < kCl; q++) {
+                const int b = items_host[it * ni + 1 + q];
+                if (b < 0) continue;
+                const int T = lay_host[b].sp >> 5;
+                win += (kPf + 3) * (double)kTile * 4.0 * 0.5 * (T - 1);
+            }
+        if (win > kL2WindowBytes) pf = 0;
+    }
     cudaError_t e = cudaLaunchKernelEx(&cfg, gs_cluster_kernel, n_items, (const GsItem *)items, lay_dev, counter, A,
                                        (const GsPacket *)packets, sweeps, x_out, x_map, keep_idx, S, max_sp, ystride,
-                                       prof);
+                                       pf, prof);
     if (profile) {
         unsigned long long h[32];
         cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, st);

@@ -24,12 +24,14 @@
 //  psf_slice_kernel  one warp per kept node: fp64 steering (sincospi of k d / pi, amplitude table),
 //                    power-of-two row scale, int8 digits of X and Z written directly in the
 //                    tensor-core operand layout; b~ = b[keep] (S6, fp64).
-//  psf_tc_kernel     one CTA per 128 x 64 output tile (bin, I, J): warp 0 streams the K steps
-//                    (32 bytes of K per step: 32 KB of A digits, 8 KB of B digits, two bulk
-//                    copies) into a 4-deep shared-memory ring; one thread of warp 1 issues the
-//                    20 MMAs (128x64x32, int8 -> s32) per step into 8 TMEM accumulators
-//                    (512 columns); warps 2-5 read TMEM and write A~ in the GS tile layout
-//                    (symmetric tile layout, dwc_internal.cuh), from (i, j) and the mirror (j, i).
+//  psf_tc_kernel     one CTA per 128 x 32 output tile (bin, I, J), two CTAs per SM (256 TMEM
+//                    columns and 110 KB of shared memory each) so one CTA's epilogue overlaps the
+//                    other's loads and MMAs: warp 0 streams the K steps (32 bytes of K per step:
+//                    32 KB of A digits, 4 KB of B digits, two bulk copies) into a 3-deep ring;
+//                    one thread of warp 1 issues the 20 MMAs (128x32x32, int8 -> s32) per step
+//                    into 8 TMEM accumulators; warps 2-5 read TMEM and write A~ in the GS tile
+//                    layout (symmetric tile layout, dwc_internal.cuh), from (i, j) and the
+//                    mirror (j, i); the target tiles of the warp's 32x32 block are resolved once.
 //
 // Operand layout (per bin; rp = nk rounded up to 128 rows, kp = 2M rounded up to 32 bytes):
 //   A side (8 matrices mt = X_0..X_3, Z_0..Z_3), byte of (mt, row r, k):
@@ -50,13 +52,13 @@ using namespace sm100;
 
 constexpr int kSl = 4;                     // int8 digits per value
 constexpr int kTM = 128;                   // output tile rows (MMA M)
-constexpr int kTN = 64;                    // output tile cols (MMA N)
+constexpr int kTN = 32;                    // output tile cols (MMA N) = one 32-column block
 constexpr int kAMat = 2 * kSl;             // X_s, Z_s
 constexpr int kBMat = kSl;                 // X_t
 constexpr int kABytes = kTM * 32 * kAMat;  // 32 KB per K step
-constexpr int kBBytes = kTN * 32 * kBMat;  //  8 KB per K step
-constexpr int kNS = 4;                     // ring depth
-constexpr int kTmemCols = 2 * kSl * kTN;   // 8 accumulators x 64 columns = 512
+constexpr int kBBytes = kTN * 32 * kBMat;  //  4 KB per K step
+constexpr int kNS = 3;                     // ring depth
+constexpr int kTmemCols = 2 * kSl * kTN;   // 8 accumulators x 32 columns = 256
 constexpr int kPsfThreads = 192;
 
 __host__ __device__ inline size_t opa_index(int rp, int mt, int r, int k) {
@@ -156,12 +158,13 @@ psf_slice_kernel(Geo g, const double *__restrict__ dist, const double *__restric
 struct __align__(1024) PsfSmem {
     int8_t a[kNS][kABytes];
     int8_t b[kNS][kBBytes];
+    double rcol[kTN];                      // row scales of the tile's columns
     unsigned long long full[kNS], empty[kNS], tmem_full;
     uint32_t tmem_base;
 };
 
 template <bool kDR>
-__global__ void __launch_bounds__(kPsfThreads, 1)
+__global__ void __launch_bounds__(kPsfThreads, 2)
 psf_tc_kernel(int M, int kp, const int4 *__restrict__ tiles, const BinLayout *__restrict__ lay,
               const int8_t *__restrict__ opA, const int8_t *__restrict__ opB, const double *__restrict__ rsc,
               const double *__restrict__ wt, float *__restrict__ Aout) {
@@ -222,78 +225,84 @@ psf_tc_kernel(int M, int kp, const int4 *__restrict__ tiles, const BinLayout *__
             mma_commit(&sm.tmem_full);
         }
     } else {
-        // epilogue: warp w reads TMEM lanes 32*(w%4) .. +31 (= tile rows)
+        // epilogue: warp w reads TMEM lanes 32*(w%4) .. +31 (= tile rows); its 32 rows are one
+        // row block of A~ (sp is a multiple of 32), the tile's 32 columns one column block
         const int q = warp & 3;
         const int il = q * 32 + lane;
         const int i = tl.y * kTM + il;
+        const int j0 = tl.z * kTN;
         const int T = L.sp >> 5;
-        const bool row_ok = i < L.sp;
-        const double ri = row_ok ? rsc[L.r_off + i] : 0.0;
+        const bool blk_ok = (tl.y * kTM + q * 32) < L.sp && j0 < L.sp;   // warp-uniform
         const double inv_m2 = 1.0 / ((double)M * (double)M);
         const double inv_dr = 1.0 / ((double)M * (double)M - (double)M);
         float *Ab = Aout + L.a_off;
+        const int et = threadIdx.x - 64;   // 0..127
+        if (et < kTN) sm.rcol[et] = rsc[L.r_off + min(j0 + et, L.rp - 1)];
         mbar_wait(&sm.tmem_full, 0);
         tc_fence_after();
-        // diagonal removal (R20): Q_ij = sum_m |e_mi|^2 |e_mj|^2 in fp64; the tile's 64 column
-        // vectors are staged in the (now idle) operand ring
-        double *ws = reinterpret_cast<double *>(sm.a[0]);
-        const double *wti = kDR ? wt + (size_t)L.r_off * M + min(i, L.rp - 1) : nullptr;
-        if (kDR) {
-            const double *wb = wt + (size_t)L.r_off * M;
-            for (int e = threadIdx.x - 64; e < kTN * M; e += 128) {
-                const int jj = e / M, m = e - (e / M) * M;
-                ws[e] = wb[(size_t)m * L.rp + tl.z * kTN + jj];
-            }
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-        }
-        for (int jc = 0; jc < kTN; jc += 8) {
-            __syncwarp();
-            int32_t acc[2 * kSl][8];
-#pragma unroll
-            for (int a = 0; a < 2 * kSl; a++)
-                tmem_ld8(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * kTN + jc), acc[a]);
-            tmem_ld_wait();
-            const int j0 = tl.z * kTN + jc;
-            if (!row_ok || j0 >= L.sp) continue;  // sp is a multiple of 32: all 8 columns valid
-            float v[8];
-            double q4[8];
-#pragma unroll
-            for (int c = 0; c < 8; c++) q4[c] = 0.0;
-            if (kDR) {
-                for (int m = 0; m < M; m++) {
-                    const double wi = wti[(size_t)m * L.rp];
-#pragma unroll
-                    for (int c = 0; c < 8; c++) q4[c] = fma(wi, ws[(jc + c) * M + m], q4[c]);
-                }
-            }
-#pragma unroll
-            for (int c = 0; c < 8; c++) {
-                const long long gre = ((long long)acc[0][c] << 21) + ((long long)acc[1][c] << 14) +
-                                      ((long long)acc[2][c] << 7) + (long long)acc[3][c];
-                const long long gim = ((long long)acc[4][c] << 21) + ((long long)acc[5][c] << 14) +
-                                      ((long long)acc[6][c] << 7) + (long long)acc[7][c];
-                const double dre = (double)gre, dim = (double)gim;
-                const double sq = dre * dre + dim * dim;
-                if (kDR) {
-                    const double a = (sq * ri * rsc[L.r_off + j0 + c] - q4[c]) * inv_dr;
-                    v[c] = (float)(a > 0.0 ? a : 0.0);
-                } else {
-                    v[c] = (float)(sq * ri * rsc[L.r_off + j0 + c] * inv_m2);
-                }
-            }
-            // direct (i, j0..j0+7): coalesced over lanes; mirror (j0..j0+7, i): two float4 per lane
+        // diagonal removal (R20): Q_ij = sum_m |e_mi|^2 |e_mj|^2 in fp64 (row i per lane, the
+        // 8 columns of a chunk are warp-uniform loads)
+        const double *wb = kDR ? wt + (size_t)L.r_off * M : nullptr;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (blk_ok) {
+            const double ri = rsc[L.r_off + i];
+            // stored tiles of block (i/32, j0/32) and of its mirror: resolved once per warp
             int td[3], tm[3];
             const int nd = sym_targets(T, L.g, i >> 5, j0 >> 5, td);
             const int nm = sym_targets(T, L.g, j0 >> 5, i >> 5, tm);
-            for (int u = 0; u < nd; u++) {
-                float *dst = Ab + (size_t)td[u] * 1024 + (i & 31);
+#pragma unroll 1
+            for (int jc = 0; jc < kTN; jc += 8) {
+                int32_t acc[2 * kSl][8];
 #pragma unroll
-                for (int c = 0; c < 8; c++) dst[((j0 + c) & 31) * 32] = v[c];
-            }
-            for (int u = 0; u < nm; u++) {
-                float4 *mir = reinterpret_cast<float4 *>(Ab + (size_t)tm[u] * 1024 + (i & 31) * 32 + (j0 & 31));
-                mir[0] = make_float4(v[0], v[1], v[2], v[3]);
-                mir[1] = make_float4(v[4], v[5], v[6], v[7]);
+                for (int a = 0; a < 2 * kSl; a++)
+                    tmem_ld8(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * kTN + jc), acc[a]);
+                tmem_ld_wait();
+                float v[8];
+                double q4[8];
+#pragma unroll
+                for (int c = 0; c < 8; c++) q4[c] = 0.0;
+                if (kDR) {
+                    for (int m = 0; m < M; m++) {
+                        const double wi = wb[(size_t)m * L.rp + i];
+                        const double2 *wc = reinterpret_cast<const double2 *>(wb + (size_t)m * L.rp + j0 + jc);
+#pragma unroll
+                        for (int c = 0; c < 4; c++) {
+                            const double2 w2 = __ldg(wc + c);
+                            q4[2 * c] = fma(wi, w2.x, q4[2 * c]);
+                            q4[2 * c + 1] = fma(wi, w2.y, q4[2 * c + 1]);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < 8; c++) {
+                    const long long gre = ((long long)acc[0][c] << 21) + ((long long)acc[1][c] << 14) +
+                                          ((long long)acc[2][c] << 7) + (long long)acc[3][c];
+                    const long long gim = ((long long)acc[4][c] << 21) + ((long long)acc[5][c] << 14) +
+                                          ((long long)acc[6][c] << 7) + (long long)acc[7][c];
+                    const double dre = (double)gre, dim = (double)gim;
+                    const double sq = dre * dre + dim * dim;
+                    if (kDR) {
+                        const double a = (sq * ri * sm.rcol[jc + c] - q4[c]) * inv_dr;
+                        v[c] = (float)(a > 0.0 ? a : 0.0);
+                    } else {
+                        v[c] = (float)(sq * ri * sm.rcol[jc + c] * inv_m2);
+                    }
+                }
+                // direct (i, j0+jc..+7): coalesced over lanes; mirror (j0+jc..+7, i): two float4 per lane
+#pragma unroll
+                for (int u = 0; u < 3; u++) {
+                    if (u >= nd) break;
+                    float *dst = Ab + (size_t)td[u] * 1024 + (i & 31) + jc * 32;
+#pragma unroll
+                    for (int c = 0; c < 8; c++) dst[c * 32] = v[c];
+                }
+#pragma unroll
+                for (int u = 0; u < 3; u++) {
+                    if (u >= nm) break;
+                    float4 *mir = reinterpret_cast<float4 *>(Ab + (size_t)tm[u] * 1024 + (i & 31) * 32 + jc);
+                    mir[0] = make_float4(v[0], v[1], v[2], v[3]);
+                    mir[1] = make_float4(v[4], v[5], v[6], v[7]);
+                }
             }
         }
         tc_fence_before();

@@ -1,0 +1,220 @@
+// recur.cu -- cycles of the GS solver's 32-row in-block recurrence (step form) in isolation.
+// V4: 4 rows per lane, 8 groups (the kernel's form); V8: 8 rows per lane, 4 groups.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o recur recur.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ float4 lds4(const float *p) { return *reinterpret_cast<const float4 *>(p); }
+
+__global__ void v4_kernel(const float *g_tile, float *out, int iters, long long *cyc) {
+    __shared__ __align__(16) float tile[1024];
+    const int lane = threadIdx.x & 31;
+    for (int i = lane; i < 1024; i += 32) tile[i] = g_tile[i];
+    __syncwarp();
+    const int L4 = 4 * (lane & 7);
+    float ac[4], invd[4], xo[4];
+    for (int i = 0; i < 4; i++) { ac[i] = 0.1f * (L4 + i) - 1.f; invd[i] = 1.f; xo[i] = 0.5f; }
+    const float wg10 = tile[L4 * 32 + L4 + 1] , wg20 = 0.01f, wg30 = 0.02f, wg21 = 0.03f, wg31 = 0.01f, wg32 = 0.02f;
+    long long t0 = clock64();
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int G = 0; G < 8; G++) {
+            const float m = (lane == G) ? 1.f : 0.f;
+            float4 v[4];
+#pragma unroll
+            for (int i = 0; i < 4; i++) v[i] = lds4(tile + (4 * G + i) * 32 + L4);
+            const float w0 = -ac[0] * invd[0], w1 = -ac[1] * invd[1], w2 = -ac[2] * invd[2], w3 = -ac[3] * invd[3];
+            auto apply = [&](const float4 &t, float d) {
+                ac[0] = fmaf(t.x, d, ac[0]); ac[1] = fmaf(t.y, d, ac[1]);
+                ac[2] = fmaf(t.z, d, ac[2]); ac[3] = fmaf(t.w, d, ac[3]);
+            };
+            const float c0 = fmaxf(w0, -xo[0]);
+            apply(v[0], __shfl_sync(0xffffffffu, c0, G));
+            float u1 = fmaf(-wg10, c0, w1), u2 = fmaf(-wg20, c0, w2), u3 = fmaf(-wg30, c0, w3);
+            const float c1 = fmaxf(u1, -xo[1]);
+            apply(v[1], __shfl_sync(0xffffffffu, c1, G));
+            u2 = fmaf(-wg21, c1, u2); u3 = fmaf(-wg31, c1, u3);
+            const float c2 = fmaxf(u2, -xo[2]);
+            apply(v[2], __shfl_sync(0xffffffffu, c2, G));
+            u3 = fmaf(-wg32, c2, u3);
+            const float c3 = fmaxf(u3, -xo[3]);
+            apply(v[3], __shfl_sync(0xffffffffu, c3, G));
+            xo[0] = fmaf(m, c0, xo[0]); xo[1] = fmaf(m, c1, xo[1]);
+            xo[2] = fmaf(m, c2, xo[2]); xo[3] = fmaf(m, c3, xo[3]);
+        }
+        for (int i = 0; i < 4; i++) ac[i] = ac[i] * 0.5f - 0.3f;   // next block's residual (stand-in)
+    }
+    long long t1 = clock64();
+    if (lane == 0 && threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+    out[blockIdx.x * 32 + lane] = xo[0] + xo[1] + xo[2] + xo[3] + ac[0];
+}
+
+__global__ void v4f2_kernel(const float *g_tile, float *out, int iters, long long *cyc) {
+    __shared__ __align__(16) float tile[1024];
+    const int lane = threadIdx.x & 31;
+    for (int i = lane; i < 1024; i += 32) tile[i] = g_tile[i];
+    __syncwarp();
+    const int L4 = 4 * (lane & 7);
+    float ac[4], invd[4], xo[4];
+    for (int i = 0; i < 4; i++) { ac[i] = 0.1f * (L4 + i) - 1.f; invd[i] = 1.f; xo[i] = 0.5f; }
+    const float wg10 = tile[L4 * 32 + L4 + 1] , wg20 = 0.01f, wg30 = 0.02f, wg21 = 0.03f, wg31 = 0.01f, wg32 = 0.02f;
+    long long t0 = clock64();
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int G = 0; G < 8; G++) {
+            const float m = (lane == G) ? 1.f : 0.f;
+            float4 v[4];
+#pragma unroll
+            for (int i = 0; i < 4; i++) v[i] = lds4(tile + (4 * G + i) * 32 + L4);
+            const float w0 = -ac[0] * invd[0], w1 = -ac[1] * invd[1], w2 = -ac[2] * invd[2], w3 = -ac[3] * invd[3];
+            auto apply = [&](const float4 &t, float d) {
+                const float2 dd = make_float2(d, d);
+                float2 a01 = __ffma2_rn(make_float2(t.x, t.y), dd, make_float2(ac[0], ac[1]));
+                float2 a23 = __ffma2_rn(make_float2(t.z, t.w), dd, make_float2(ac[2], ac[3]));
+                ac[0] = a01.x; ac[1] = a01.y; ac[2] = a23.x; ac[3] = a23.y;
+            };
+            const float c0 = fmaxf(w0, -xo[0]);
+            apply(v[0], __shfl_sync(0xffffffffu, c0, G));
+            float u1 = fmaf(-wg10, c0, w1), u2 = fmaf(-wg20, c0, w2), u3 = fmaf(-wg30, c0, w3);
+            const float c1 = fmaxf(u1, -xo[1]);
+            apply(v[1], __shfl_sync(0xffffffffu, c1, G));
+            u2 = fmaf(-wg21, c1, u2); u3 = fmaf(-wg31, c1, u3);
+            const float c2 = fmaxf(u2, -xo[2]);
+            apply(v[2], __shfl_sync(0xffffffffu, c2, G));
+            u3 = fmaf(-wg32, c2, u3);
+            const float c3 = fmaxf(u3, -xo[3]);
+            apply(v[3], __shfl_sync(0xffffffffu, c3, G));
+            xo[0] = fmaf(m, c0, xo[0]); xo[1] = fmaf(m, c1, xo[1]);
+            xo[2] = fmaf(m, c2, xo[2]); xo[3] = fmaf(m, c3, xo[3]);
+        }
+        for (int i = 0; i < 4; i++) ac[i] = ac[i] * 0.5f - 0.3f;   // next block's residual (stand-in)
+    }
+    long long t1 = clock64();
+    if (lane == 0 && threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+    out[blockIdx.x * 32 + lane] = xo[0] + xo[1] + xo[2] + xo[3] + ac[0];
+}
+
+__global__ void v4ps_kernel(const float *g_tile, float *out, int iters, long long *cyc) {
+    __shared__ __align__(16) float tile[1024];
+    const int lane = threadIdx.x & 31;
+    for (int i = lane; i < 1024; i += 32) tile[i] = g_tile[i];
+    __syncwarp();
+    const int L4 = 4 * (lane & 7);
+    float ac[4], invd[4], xo[4];
+    for (int i = 0; i < 4; i++) { ac[i] = 0.1f * (L4 + i) - 1.f; invd[i] = 1.f; xo[i] = 0.5f; }
+    const float wg10 = tile[L4 * 32 + L4 + 1] , wg20 = 0.01f, wg30 = 0.02f, wg21 = 0.03f, wg31 = 0.01f, wg32 = 0.02f;
+    long long t0 = clock64();
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int G = 0; G < 8; G++) {
+            const float m = (lane == G) ? 1.f : 0.f;
+            float4 v[4];
+#pragma unroll
+            for (int i = 0; i < 4; i++) v[i] = lds4(tile + (4 * G + i) * 32 + L4);
+            const float w0 = ac[0], w1 = ac[1], w2 = ac[2], w3 = ac[3];
+            auto apply = [&](const float4 &t, float d) {
+                const float2 dd = make_float2(d, d);
+                float2 a01 = __ffma2_rn(make_float2(t.x, t.y), dd, make_float2(ac[0], ac[1]));
+                float2 a23 = __ffma2_rn(make_float2(t.z, t.w), dd, make_float2(ac[2], ac[3]));
+                ac[0] = a01.x; ac[1] = a01.y; ac[2] = a23.x; ac[3] = a23.y;
+            };
+            const float c0 = fmaxf(w0, -xo[0]);
+            apply(v[0], __shfl_sync(0xffffffffu, c0, G));
+            float u1 = fmaf(-wg10, c0, w1), u2 = fmaf(-wg20, c0, w2), u3 = fmaf(-wg30, c0, w3);
+            const float c1 = fmaxf(u1, -xo[1]);
+            apply(v[1], __shfl_sync(0xffffffffu, c1, G));
+            u2 = fmaf(-wg21, c1, u2); u3 = fmaf(-wg31, c1, u3);
+            const float c2 = fmaxf(u2, -xo[2]);
+            apply(v[2], __shfl_sync(0xffffffffu, c2, G));
+            u3 = fmaf(-wg32, c2, u3);
+            const float c3 = fmaxf(u3, -xo[3]);
+            apply(v[3], __shfl_sync(0xffffffffu, c3, G));
+            xo[0] = fmaf(m, c0, xo[0]); xo[1] = fmaf(m, c1, xo[1]);
+            xo[2] = fmaf(m, c2, xo[2]); xo[3] = fmaf(m, c3, xo[3]);
+        }
+        for (int i = 0; i < 4; i++) ac[i] = ac[i] * 0.5f - 0.3f;   // next block's residual (stand-in)
+    }
+    long long t1 = clock64();
+    if (lane == 0 && threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+    out[blockIdx.x * 32 + lane] = xo[0] + xo[1] + xo[2] + xo[3] + ac[0];
+}
+
+// 8 rows per lane (lanes 0-3 solve, rows 8L..8L+7), 4 groups; within-group weights wg[28]
+__global__ void v8_kernel(const float *g_tile, float *out, int iters, long long *cyc) {
+    __shared__ __align__(16) float tile[1024];
+    const int lane = threadIdx.x & 31;
+    for (int i = lane; i < 1024; i += 32) tile[i] = g_tile[i];
+    __syncwarp();
+    const int L8 = 8 * (lane & 3);
+    float ac[8], invd[8], xo[8], wg[28];
+    for (int i = 0; i < 8; i++) { ac[i] = 0.1f * (L8 + i) - 1.f; invd[i] = 1.f; xo[i] = 0.5f; }
+    for (int i = 0; i < 28; i++) wg[i] = tile[L8 * 32 + i] * 0.1f;
+    long long t0 = clock64();
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int G = 0; G < 4; G++) {
+            const float m = (lane == G) ? 1.f : 0.f;
+            float w[8];
+#pragma unroll
+            for (int i = 0; i < 8; i++) w[i] = -ac[i] * invd[i];
+            float c[8];
+            int q = 0;
+#pragma unroll
+            for (int t = 0; t < 8; t++) {
+                c[t] = fmaxf(w[t], -xo[t]);
+#pragma unroll
+                for (int i = t + 1; i < 8; i++) w[i] = fmaf(-wg[q++], c[t], w[i]);
+            }
+#pragma unroll
+            for (int t = 0; t < 8; t++) {
+                const float d = __shfl_sync(0xffffffffu, c[t], G);
+                const float4 a = lds4(tile + (8 * G + t) * 32 + L8);
+                const float4 b = lds4(tile + (8 * G + t) * 32 + L8 + 4);
+                ac[0] = fmaf(a.x, d, ac[0]); ac[1] = fmaf(a.y, d, ac[1]);
+                ac[2] = fmaf(a.z, d, ac[2]); ac[3] = fmaf(a.w, d, ac[3]);
+                ac[4] = fmaf(b.x, d, ac[4]); ac[5] = fmaf(b.y, d, ac[5]);
+                ac[6] = fmaf(b.z, d, ac[6]); ac[7] = fmaf(b.w, d, ac[7]);
+            }
+#pragma unroll
+            for (int t = 0; t < 8; t++) xo[t] = fmaf(m, c[t], xo[t]);
+        }
+        for (int i = 0; i < 8; i++) ac[i] = ac[i] * 0.5f - 0.3f;
+    }
+    long long t1 = clock64();
+    if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+    float s = 0.f;
+    for (int i = 0; i < 8; i++) s += xo[i] + ac[i];
+    out[blockIdx.x * 32 + lane] = s;
+}
+
+// busy warps that keep the solver's SM sub-partition issuing (like the co-resident warps)
+__global__ void dummy() {}
+
+int main() {
+    float *tile, *out;
+    long long *cyc;
+    cudaMalloc(&tile, 4096);
+    cudaMalloc(&out, 1 << 20);
+    cudaMalloc(&cyc, 1024 * 8);
+    float h[1024];
+    for (int i = 0; i < 1024; i++) h[i] = ((i * 37) % 101) * 1e-3f;
+    cudaMemcpy(tile, h, 4096, cudaMemcpyHostToDevice);
+    const int iters = 10000;
+    long long c;
+    for (int rep = 0; rep < 2; rep++) {
+        v4_kernel<<<1, 32>>>(tile, out, iters, cyc);
+        cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+        printf("V4 (4 rows/lane, 8 groups): %.1f cycles per 32-row block\n", (double)c / iters);
+        v4f2_kernel<<<1, 32>>>(tile, out, iters, cyc);
+        cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+        printf("V4 FFMA2 applies: %.1f cycles per 32-row block\n", (double)c / iters);
+        v4ps_kernel<<<1, 32>>>(tile, out, iters, cyc);
+        cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+        printf("V4 FFMA2 + prescaled (no FMUL): %.1f cycles per 32-row block\n", (double)c / iters);
+        v8_kernel<<<1, 32>>>(tile, out, iters, cyc);
+        cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+        printf("V8 (8 rows/lane, 4 groups): %.1f cycles per 32-row block\n", (double)c / iters);
+    }
+    printf("%s\n", cudaGetErrorString(cudaGetLastError()));
+    return 0;
+}
