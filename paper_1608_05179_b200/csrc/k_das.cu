@@ -143,11 +143,24 @@ das_kernel(Geo g, const double *__restrict__ dist, const double *__restrict__ am
     const int bin = blockIdx.y;
     const int s0 = blockIdx.x * P;
     const double k = 2.0 * freq[bin] / g.c0;   // half-turns per metre
-    for (int t = threadIdx.x; t < Mp * P; t += kDasThreads) {
-        const int m = t / P, p = t % P;
-        const int s = s0 + p;
-        Es[t] = (m < M && s < g.S) ? steer_elem(dist[(size_t)m * g.S + s], amp[(size_t)m * g.S + s], k)
-                                   : make_double2(0.0, 0.0);
+    // steering vectors of the CTA's points: the (dist, amp) table entries of 8 elements per
+    // thread are loaded before any is used, so their latency is paid once per 8 (not per element)
+    constexpr int kEU = 8;
+    for (int base = 0; base < Mp * P; base += kDasThreads * kEU) {
+        double dd[kEU], aa[kEU];
+#pragma unroll
+        for (int u = 0; u < kEU; u++) {
+            const int t = base + u * kDasThreads + threadIdx.x;
+            const int m = t / P, s = s0 + t % P;
+            const bool ok = t < Mp * P && m < M && s < g.S;
+            dd[u] = ok ? __ldg(dist + (size_t)m * g.S + s) : 0.0;
+            aa[u] = ok ? __ldg(amp + (size_t)m * g.S + s) : -1.0;   // -1: padding element
+        }
+#pragma unroll
+        for (int u = 0; u < kEU; u++) {
+            const int t = base + u * kDasThreads + threadIdx.x;
+            if (t < Mp * P) Es[t] = (aa[u] >= 0.0) ? steer_elem(dd[u], aa[u], k) : make_double2(0.0, 0.0);
+        }
     }
     __syncthreads();
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -160,11 +173,14 @@ das_kernel(Geo g, const double *__restrict__ dist, const double *__restrict__ am
     for (int qa = w; qa < G / 2; qa += kDasWarps) {
         const int qb = G - 1 - qa;
         __syncwarp();
-        for (int t = lane; t < 8 * Mp; t += 32) {   // rows 4qa..4qa+3, 4qb..4qb+3 of Ch
-            const int r = t / Mp, n = t - (t / Mp) * Mp;
+        for (int t = lane; t < 8 * Mp; t += 32) {   // rows 4qa..4qa+3, 4qb..4qb+3 of Ch (cp.async:
+            const int r = t / Mp, n = t - (t / Mp) * Mp;   // all 16-byte copies in flight at once)
             const int m = (r < 4) ? 4 * qa + r : 4 * qb + r - 4;
-            cw[t] = __ldg(C + (size_t)m * Mp + n);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(cw + t)),
+                         "l"(C + (size_t)m * Mp + n)
+                         : "memory");
         }
+        asm volatile("cp.async.wait_all;" ::: "memory");
         __syncwarp();
         double2 Wa[4][PPL], Wb[4][PPL];
 #pragma unroll
