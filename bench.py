@@ -150,6 +150,19 @@ def cpu_baseline(cfg, budget_bins=None):
 
 
 # ------------------------------------------------------------------------------ our arm
+FP64_PEAK_TFLOPS = 36.0   # DFMA and DMMA, measured on B200 by scripts/ubench/fp64.cu
+
+
+def step_roofline(st, sweeps, hbm_gbs, ms_step):
+    """Lower bound of one step from the method's algorithmic work (per step, whole band)."""
+    stream_ms = st["gs_bytes"] / (hbm_gbs * 1e9) * 1e3
+    write_ms = st["gs_bytes"] / sweeps / (hbm_gbs * 1e9) * 1e3
+    das_ms = 0.5 * st["das_flops"] / (FP64_PEAK_TFLOPS * 1e12) * 1e3
+    total = stream_ms + write_ms + das_ms
+    return {"gs_stream_ms": stream_ms, "psf_write_ms": write_ms, "das_fp64_ms": das_ms, "roofline_ms": total,
+            "measured_ms": ms_step, "frac": total / ms_step}
+
+
 def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
@@ -320,6 +333,10 @@ def run_ours(args, cfg):
                          "compress": float(np.mean([s["ms_compress"] for s in st_list])),
                          "psf": float(np.mean([s["ms_psf"] for s in st_list])), "gs": gs_ms,
                          "total_events": float(np.mean([s["ms_total"] for s in st_list]))},
+            # whole-step roofline: the method's own minimal work at the measured
+            # peaks -- the packed A~ stream and the A~ write over HBM, the Hermitian-half DAS on the
+            # fp64 pipes (36 TF/s, scripts/ubench/fp64.cu) -- against the measured step time
+            "step_roofline": step_roofline(st, cfg.sweeps, peak, ms),
             "sum_keep": int(st["sum_keep"]), "mean_keep_frac": st["sum_keep"] / (K * S),
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

@@ -150,6 +150,37 @@ __host__ __device__ inline int sym_targets(int T, int g, int a, int b, int t[3])
     if (b == (a + 2 * T - 2) % T) t[n++] = 2 * T + a;
     return n;
 }
+// The same with the sub-group size G a compile-time constant (the period divisions become
+// multiplies); sym_targets_g dispatches on g.  For per-element hot paths (the PSF epilogue).
+template <int G>
+__host__ __device__ inline int sym_cnt_t(int x, int o) {
+    constexpr int P = G == 4 ? 18 : (G == 2 ? 8 : 1);
+    if (x < 0) return 0;
+    const int full = (x + 1) / P, rem = (x + 1) - full * P;
+    return full * own_weight(G, o) + popc32(own_mask(G, o) & ((1u << rem) - 1u));
+}
+template <int G>
+__host__ __device__ inline int sym_u_tile_t(int T, int I, int J) {
+    const int o = own_of(G, J);
+    int s = 3 * T + sym_row_base(T, I);
+    for (int q = 0; q < o; q++) s += sym_cnt_t<G>(T - 1, q) - sym_cnt_t<G>(I, q);
+    return s + (sym_cnt_t<G>(J - 1, o) - sym_cnt_t<G>(I, o));
+}
+template <int G>
+__host__ __device__ inline int sym_targets_t(int T, int a, int b, int t[3]) {
+    int n = 0;
+    if (a == b) t[n++] = a;
+    else if (b > a) t[n++] = sym_u_tile_t<G>(T, a, b);
+    int k1 = a + T - 1, k2 = a + 2 * T - 2;   // (a - 1) mod T, (a - 2) mod T
+    while (k1 >= T) k1 -= T;
+    while (k2 >= T) k2 -= T;
+    if (b == k1) t[n++] = T + a;
+    if (b == k2) t[n++] = 2 * T + a;
+    return n;
+}
+__host__ __device__ inline int sym_targets_g(int T, int g, int a, int b, int t[3]) {
+    return g == 4 ? sym_targets_t<4>(T, a, b, t) : (g == 2 ? sym_targets_t<2>(T, a, b, t) : sym_targets_t<1>(T, a, b, t));
+}
 __host__ __device__ inline int64_t sym_tiles(int T) { return (int64_t)T * (T - 1) / 2 + 3 * (int64_t)T; }
 
 // dense row-major n x n <-> symmetric tile layout (zero padded to sp; g as above) for the

@@ -24,23 +24,29 @@
 //  psf_slice_kernel  one warp per kept node: fp64 steering (sincospi of k d / pi, amplitude table),
 //                    power-of-two row scale, int8 digits of X and Z written directly in the
 //                    tensor-core operand layout; b~ = b[keep] (S6, fp64).
-//  psf_tc_kernel     one CTA per 128 x 32 output tile (bin, I, J), two CTAs per SM (256 TMEM
-//                    columns and 110 KB of shared memory each) so one CTA's epilogue overlaps the
-//                    other's loads and MMAs: warp 0 streams the K steps (32 bytes of K per step:
-//                    32 KB of A digits, 4 KB of B digits, two bulk copies) into a 3-deep ring;
-//                    one thread of warp 1 issues the 20 MMAs (128x32x32, int8 -> s32) per step
-//                    into 8 TMEM accumulators; warps 2-5 read TMEM and write A~ in the GS tile
-//                    layout (symmetric tile layout, dwc_internal.cuh), from (i, j) and the
-//                    mirror (j, i); the target tiles of the warp's 32x32 block are resolved once.
+//  psf_tc_kernel     persistent, one CTA per SM over the list of 128 x 32 output tiles (bin, I, J):
+//                    warp 0 streams the K steps (32 bytes of K per step: 16 KB of A digits, 8 KB
+//                    of B digits, two bulk copies) into an 8-deep ring, running ahead across
+//                    tiles; one thread of warp 1 issues the 10 MMAs (128x64x32, int8 -> s32) per
+//                    step into 4 TMEM level accumulators (Re | Im) of one of two buffers (2 x 256);
+//                    8 epilogue warps drain the other buffer (TMEM reads, 64 B/cycle per SM, are
+//                    the epilogue's bound) and write A~ in the GS tile layout (symmetric tile
+//                    layout, dwc_internal.cuh) from (i, j) and the mirror (j, i); the target tiles
+//                    of a warp's 32x32 block are resolved once per tile.
 //
-// Operand layout (per bin; rp = nk rounded up to 128 rows, kp = 2M rounded up to 32 bytes):
-//   A side (8 matrices mt = X_0..X_3, Z_0..Z_3), byte of (mt, row r, k):
-//     (k/32)*(rp*256) + (r/8)*2048 + mt*256 + ((k/16)%2)*128 + (r%8)*16 + k%16
-//   B side (4 matrices t = X_0..X_3):
-//     (k/32)*(rp*128) + (r/8)*1024 + t*256 + ((k/16)%2)*128 + (r%8)*16 + k%16
-// so a 128-row A tile (64-row B tile) of one K step is a single contiguous 32 KB (8 KB) block,
-// and in shared memory each matrix is the canonical K-major no-swizzle UMMA layout with
-// LBO = 128 B and SBO = 2048 B (A) / 1024 B (B).
+// Operand layout (per bin; rp = nk rounded up to 128 rows, kp = 2M rounded up to 32 bytes).
+// Z sits on the B side (Im G_ij = -X_i . Z_j; only its square is used), and one MMA per digit
+// pair (s, t) multiplies A = X_s (128 rows) with B = [X_t ; Z_t] (2 x 32 rows, N = 64), so its
+// 64 accumulator columns hold Re (0..31) and Im (32..63) of digit level w = s + t:
+//   A side (4 matrices s = X_0..X_3), byte of (s, row r, k):
+//     (k/32)*(rp*128) + (r/8)*1024 + s*256 + ((k/16)%2)*128 + (r%8)*16 + k%16
+//   B side (per 32-row block: digit t, part p = X / Z), byte of (t, p, row r, k):
+//     (k/32)*(rp*256) + (r/32)*8192 + t*2048 + p*1024 + ((r/8)%4)*256 + ((k/16)%2)*128 + (r%8)*16 + k%16
+// so a 128-row A tile (32-row B block) of one K step is a single contiguous 16 KB (8 KB) block,
+// and in shared memory every operand is the canonical K-major no-swizzle UMMA layout with
+// LBO = 128 B and SBO = 1024 B (A) / 256 B (B: the 64 rows of [X_t ; Z_t] are 8 groups of 8).
+// Per K step 10 MMAs of 128x64x32 read 60 KB of shared memory (20 MMAs of 128x32x32 with Z on
+// the A side read 100 KB: the tensor pipe was bound by the shared-memory operand reads).
 #include <math.h>
 
 #include "dwc_internal.cuh"
@@ -53,21 +59,32 @@ using namespace sm100;
 constexpr int kSl = 4;                     // int8 digits per value
 constexpr int kTM = 128;                   // output tile rows (MMA M)
 constexpr int kTN = 32;                    // output tile cols (MMA N) = one 32-column block
-constexpr int kAMat = 2 * kSl;             // X_s, Z_s
-constexpr int kBMat = kSl;                 // X_t
-constexpr int kABytes = kTM * 32 * kAMat;  // 32 KB per K step
-constexpr int kBBytes = kTN * 32 * kBMat;  //  4 KB per K step
-constexpr int kNS = 3;                     // ring depth
-constexpr int kTmemCols = 2 * kSl * kTN;   // 8 accumulators x 32 columns = 256
-constexpr int kPsfThreads = 192;
+constexpr int kAMat = kSl;                 // X_s
+constexpr int kBMat = 2 * kSl;             // X_t, Z_t
+constexpr int kABytes = kTM * 32 * kAMat;  // 16 KB per K step
+constexpr int kBBytes = kTN * 32 * kBMat;  //  8 KB per K step
+constexpr int kNS = 8;                     // ring depth (K steps in flight, across tiles)
+constexpr int kTmemCols = kSl * 2 * kTN;   // 4 levels x (Re | Im) 64 columns = 256 (x 2 buffers)
+constexpr int kPsfThreads = 320;   // producer, MMA, 8 epilogue warps
+// TMEM column of accumulator a = p * kSl + w (p: Re / Im, w: digit level)
+__device__ __forceinline__ constexpr int acc_col(int a) { return (a % kSl) * 2 * kTN + (a / kSl) * kTN; }
 
-__host__ __device__ inline size_t opa_index(int rp, int mt, int r, int k) {
-    return (size_t)(k >> 5) * ((size_t)rp * 256) + (size_t)(r >> 3) * 2048 + mt * 256 + ((k >> 4) & 1) * 128 +
+__host__ __device__ inline size_t opa_index(int rp, int s, int r, int k) {
+    return (size_t)(k >> 5) * ((size_t)rp * 128) + (size_t)(r >> 3) * 1024 + s * 256 + ((k >> 4) & 1) * 128 +
            (r & 7) * 16 + (k & 15);
 }
-__host__ __device__ inline size_t opb_index(int rp, int t, int r, int k) {
-    return (size_t)(k >> 5) * ((size_t)rp * 128) + (size_t)(r >> 3) * 1024 + t * 256 + ((k >> 4) & 1) * 128 +
-           (r & 7) * 16 + (k & 15);
+__host__ __device__ inline size_t opb_index(int rp, int t, int p, int r, int k) {
+    return (size_t)(k >> 5) * ((size_t)rp * 256) + (size_t)(r >> 5) * 8192 + t * 2048 + p * 1024 +
+           ((r >> 3) & 3) * 256 + ((k >> 4) & 1) * 128 + (r & 7) * 16 + (k & 15);
+}
+
+// int64 -> fp64 for |x| < 2^51 without the conversion unit (I2F.F64.S64 runs on the XU pipe,
+// which ncu showed saturated in the epilogue): x + (2^52 + 2^51) as the bit pattern of a double
+// in [2^52, 2^53) holds x exactly in its mantissa; subtracting 2^52 + 2^51 is exact.  The Gram
+// accumulators combine to |G| < 2^46 (K <= 1024 products of |digit| <= 127, scaled by <= 2^21).
+__device__ __forceinline__ double exact_i64_to_f64(long long x) {
+    constexpr long long kMagic = 0x4338000000000000LL;   // bits of 2^52 + 2^51
+    return __longlong_as_double(x + kMagic) - 6755399441055744.0;
 }
 
 // exact int8 digits of v in [-127/128, 127/128]: v = sum_s a[s] 128^-(s+1) + rho
@@ -119,18 +136,18 @@ psf_slice_kernel(Geo g, const double *__restrict__ dist, const double *__restric
             for (int t = 0; t < kSl; t++) {
                 A[opa_index(L.rp, t, r, m)] = (int8_t)dr[t];            // X_t = [Re; Im]
                 A[opa_index(L.rp, t, r, M + m)] = (int8_t)di[t];
-                A[opa_index(L.rp, kSl + t, r, m)] = (int8_t)(-di[t]);   // Z_t = [-Im; Re]
-                A[opa_index(L.rp, kSl + t, r, M + m)] = (int8_t)dr[t];
-                B[opb_index(L.rp, t, r, m)] = (int8_t)dr[t];
-                B[opb_index(L.rp, t, r, M + m)] = (int8_t)di[t];
+                B[opb_index(L.rp, t, 0, r, m)] = (int8_t)dr[t];
+                B[opb_index(L.rp, t, 0, r, M + m)] = (int8_t)di[t];
+                B[opb_index(L.rp, t, 1, r, m)] = (int8_t)(-di[t]);      // Z_t = [-Im; Re]
+                B[opb_index(L.rp, t, 1, r, M + m)] = (int8_t)dr[t];
             }
         }
         for (int kk = 2 * M + lane; kk < kp; kk += 32) {
 #pragma unroll
             for (int t = 0; t < kSl; t++) {
                 A[opa_index(L.rp, t, r, kk)] = 0;
-                A[opa_index(L.rp, kSl + t, r, kk)] = 0;
-                B[opb_index(L.rp, t, r, kk)] = 0;
+                B[opb_index(L.rp, t, 0, r, kk)] = 0;
+                B[opb_index(L.rp, t, 1, r, kk)] = 0;
             }
         }
         if (lane == 0) {
@@ -144,8 +161,8 @@ psf_slice_kernel(Geo g, const double *__restrict__ dist, const double *__restric
 #pragma unroll
             for (int t = 0; t < kSl; t++) {
                 A[opa_index(L.rp, t, r, kk)] = 0;
-                A[opa_index(L.rp, kSl + t, r, kk)] = 0;
-                B[opb_index(L.rp, t, r, kk)] = 0;
+                B[opb_index(L.rp, t, 0, r, kk)] = 0;
+                B[opb_index(L.rp, t, 1, r, kk)] = 0;
             }
         }
         if (lane == 0) {
@@ -158,21 +175,23 @@ psf_slice_kernel(Geo g, const double *__restrict__ dist, const double *__restric
 struct __align__(1024) PsfSmem {
     int8_t a[kNS][kABytes];
     int8_t b[kNS][kBBytes];
-    double rcol[kTN];                      // row scales of the tile's columns
-    unsigned long long full[kNS], empty[kNS], tmem_full;
+    double rcol[2][kTN];                   // row scales of the tile's columns, per TMEM buffer
+    unsigned long long full[kNS], empty[kNS], tmem_full[2], tmem_empty[2];
     uint32_t tmem_base;
 };
 
+// Persistent: CTA c takes tiles c, c + gridDim.x, ... (neighbouring CTAs work on neighbouring
+// tiles at the same time, so a 128-row A block is read from HBM once and shared through L2).
+// Two TMEM accumulator sets (2 x 256 columns): the MMAs of tile n+1 run while the epilogue
+// warps drain tile n; the producer runs up to kNS K steps ahead across tile boundaries.
 template <bool kDR>
-__global__ void __launch_bounds__(kPsfThreads, 2)
-psf_tc_kernel(int M, int kp, const int4 *__restrict__ tiles, const BinLayout *__restrict__ lay,
+__global__ void __launch_bounds__(kPsfThreads, 1)
+psf_tc_kernel(int M, int kp, int n_tiles, const int4 *__restrict__ tiles, const BinLayout *__restrict__ lay,
               const int8_t *__restrict__ opA, const int8_t *__restrict__ opB, const double *__restrict__ rsc,
               const double *__restrict__ wt, float *__restrict__ Aout) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     PsfSmem &sm = *reinterpret_cast<PsfSmem *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int4 tl = tiles[blockIdx.x];  // (bin, I: 128-row block, J: 64-col block)
-    const BinLayout L = lay[tl.x];
     const int nkc = kp >> 5;
 
     if (threadIdx.x == 0) {
@@ -180,135 +199,183 @@ psf_tc_kernel(int M, int kp, const int4 *__restrict__ tiles, const BinLayout *__
             mbar_init(&sm.full[i], 1);
             mbar_init(&sm.empty[i], 1);
         }
-        mbar_init(&sm.tmem_full, 1);
+        for (int b = 0; b < 2; b++) {
+            mbar_init(&sm.tmem_full[b], 1);
+            mbar_init(&sm.tmem_empty[b], 8);   // one arrival per epilogue warp
+        }
         fence_mbar_init();
     }
-    if (warp == 1) tmem_alloc(&sm.tmem_base, kTmemCols);
+    if (warp == 1) tmem_alloc(&sm.tmem_base, 2 * kTmemCols);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
 
     if (warp == 0) {
-        if (lane == 0) {  // producer: one K step = one 32 KB A block + one 8 KB B block
-            const int8_t *ga = opA + (size_t)L.r_off * kp * kAMat + (size_t)tl.y * (kTM / 8) * 2048;
-            const int8_t *gb = opB + (size_t)L.r_off * kp * kBMat + (size_t)tl.z * (kTN / 8) * 1024;
-            for (int kc = 0; kc < nkc; kc++) {
-                const int st = kc % kNS;
-                if (kc >= kNS) mbar_wait(&sm.empty[st], ((kc / kNS) - 1) & 1);
-                mbar_expect_tx(&sm.full[st], kABytes + kBBytes);
-                bulk_g2s(sm.a[st], ga + (size_t)kc * L.rp * 256, kABytes, &sm.full[st]);
-                bulk_g2s(sm.b[st], gb + (size_t)kc * L.rp * 128, kBBytes, &sm.full[st]);
+        if (lane == 0) {  // producer: one K step = one 16 KB A block + one 8 KB B block
+            int it = 0;
+            for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+                const int4 tl = tiles[tile];   // (bin, I: 128-row block, J: 32-column block)
+                const BinLayout L = lay[tl.x];
+                const int8_t *ga = opA + (size_t)L.r_off * kp * kAMat + (size_t)tl.y * kABytes;
+                const int8_t *gb = opB + (size_t)L.r_off * kp * kBMat + (size_t)tl.z * kBBytes;
+                for (int kc = 0; kc < nkc; kc++, it++) {
+                    const int st = it % kNS;
+                    if (it >= kNS) mbar_wait(&sm.empty[st], ((it / kNS) - 1) & 1);
+                    mbar_expect_tx(&sm.full[st], kABytes + kBBytes);
+                    bulk_g2s(sm.a[st], ga + (size_t)kc * L.rp * 32 * kAMat, kABytes, &sm.full[st]);
+                    bulk_g2s(sm.b[st], gb + (size_t)kc * L.rp * 32 * kBMat, kBBytes, &sm.full[st]);
+                }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {  // MMA issuer
-            constexpr uint32_t idesc = idesc_i8(kTM, kTN);
-            for (int kc = 0; kc < nkc; kc++) {
-                const int st = kc % kNS;
-                mbar_wait(&sm.full[st], (kc / kNS) & 1);
+            constexpr uint32_t idesc = idesc_i8(kTM, 2 * kTN);
+            int it = 0, n = 0;
+            for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, n++) {
+                const int bf = n & 1;
+                if (n >= 2) mbar_wait(&sm.tmem_empty[bf], ((n >> 1) - 1) & 1);   // tile n-2 drained
                 tc_fence_after();
-                const uint32_t sa = smem_u32(sm.a[st]), sb = smem_u32(sm.b[st]);
-#pragma unroll
-                for (int p = 0; p < 2; p++)
+                const uint32_t td = tmem + (uint32_t)(bf * kTmemCols);
+                for (int kc = 0; kc < nkc; kc++, it++) {
+                    const int st = it % kNS;
+                    mbar_wait(&sm.full[st], (it / kNS) & 1);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(sm.a[st]), sb = smem_u32(sm.b[st]);
 #pragma unroll
                     for (int s = 0; s < kSl; s++)
 #pragma unroll
-                        for (int t = 0; t + s < kSl; t++) {
-                            const uint64_t ad = smem_desc(sa + (p * kSl + s) * 256, 128, 2048);
-                            const uint64_t bd = smem_desc(sb + t * 256, 128, 1024);
-                            mma_i8(tmem + (uint32_t)((p * kSl + s + t) * kTN), ad, bd, idesc,
-                                   (kc > 0 || s > 0) ? 1u : 0u);
+                        for (int t = 0; t + s < kSl; t++) {   // level s + t; (0, w) first initialises it
+                            const uint64_t ad = smem_desc(sa + s * 256, 128, 1024);
+                            const uint64_t bd = smem_desc(sb + t * 2048, 128, 256);
+                            mma_i8(td + (uint32_t)((s + t) * 2 * kTN), ad, bd, idesc, (kc > 0 || s > 0) ? 1u : 0u);
                         }
-                mma_commit(&sm.empty[st]);  // frees the ring slot when these MMAs complete
+                    mma_commit(&sm.empty[st]);  // frees the ring slot when these MMAs complete
+                }
+                mma_commit(&sm.tmem_full[bf]);
             }
-            mma_commit(&sm.tmem_full);
         }
     } else {
-        // epilogue: warp w reads TMEM lanes 32*(w%4) .. +31 (= tile rows); its 32 rows are one
-        // row block of A~ (sp is a multiple of 32), the tile's 32 columns one column block
-        const int q = warp & 3;
-        const int il = q * 32 + lane;
-        const int i = tl.y * kTM + il;
-        const int j0 = tl.z * kTN;
-        const int T = L.sp >> 5;
-        const bool blk_ok = (tl.y * kTM + q * 32) < L.sp && j0 < L.sp;   // warp-uniform
+        // epilogue, 8 warps: warp w reads TMEM lanes 32*(w%4) .. +31 (= tile rows; one row block of
+        // A~, sp is a multiple of 32) and columns 16h .. 16h+15 of the tile's 32-column block,
+        // h = (w-2)/4, as two 8-column chunks; the second chunk's TMEM loads are in flight while
+        // the first is converted and stored (TMEM reads are the epilogue's bound)
+        const int q = warp & 3, h = (warp - 2) >> 2;
+        const int et = threadIdx.x - 64;   // 0..255
         const double inv_m2 = 1.0 / ((double)M * (double)M);
         const double inv_dr = 1.0 / ((double)M * (double)M - (double)M);
-        float *Ab = Aout + L.a_off;
-        const int et = threadIdx.x - 64;   // 0..127
-        if (et < kTN) sm.rcol[et] = rsc[L.r_off + min(j0 + et, L.rp - 1)];
-        mbar_wait(&sm.tmem_full, 0);
-        tc_fence_after();
-        // diagonal removal (R20): Q_ij = sum_m |e_mi|^2 |e_mj|^2 in fp64 (row i per lane, the
-        // 8 columns of a chunk are warp-uniform loads)
-        const double *wb = kDR ? wt + (size_t)L.r_off * M : nullptr;
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (blk_ok) {
-            const double ri = rsc[L.r_off + i];
-            // stored tiles of block (i/32, j0/32) and of its mirror: resolved once per warp
-            int td[3], tm[3];
-            const int nd = sym_targets(T, L.g, i >> 5, j0 >> 5, td);
-            const int nm = sym_targets(T, L.g, j0 >> 5, i >> 5, tm);
-#pragma unroll 1
-            for (int jc = 0; jc < kTN; jc += 8) {
-                int32_t acc[2 * kSl][8];
+        int n = 0;
+        // tile metadata one tile ahead (two dependent global loads per tile, off the critical path)
+        int4 tl_nx = make_int4(0, 0, 0, 0);
+        BinLayout L_nx = {0, 0, 0, 0, 0, 0, 0};
+        if (blockIdx.x < n_tiles) {
+            tl_nx = tiles[blockIdx.x];
+            L_nx = lay[tl_nx.x];
+        }
+        for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, n++) {
+            const int bf = n & 1;
+            const int4 tl = tl_nx;
+            const BinLayout L = L_nx;
+            if (tile + (int)gridDim.x < n_tiles) {
+                tl_nx = tiles[tile + gridDim.x];
+                L_nx = lay[tl_nx.x];
+            }
+            const int i = tl.y * kTM + q * 32 + lane;
+            const int j0 = tl.z * kTN;
+            const int T = L.sp >> 5;
+            const bool blk_ok = (tl.y * kTM + q * 32) < L.sp && j0 < L.sp;   // warp-uniform
+            float *Ab = Aout + L.a_off;
+            // rcol[bf] was last read for tile n-2, before every epilogue warp passed tile n-1's barrier
+            if (et < kTN) sm.rcol[bf][et] = rsc[L.r_off + min(j0 + et, L.rp - 1)];
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            // diagonal removal (R20): Q_ij = sum_m |e_mi|^2 |e_mj|^2 in fp64 (row i per lane, the
+            // 8 columns of a chunk are warp-uniform loads)
+            const double *wb = kDR ? wt + (size_t)L.r_off * M : nullptr;
+            mbar_wait(&sm.tmem_full[bf], (n >> 1) & 1);
+            tc_fence_after();
+            if (blk_ok) {
+                const double ri = rsc[L.r_off + i];
+                // stored tiles of block (i/32, j0/32) and of its mirror: resolved once per tile
+                int td[3], tm[3];
+                const int nd = sym_targets_g(T, L.g, i >> 5, j0 >> 5, td);
+                const int nm = sym_targets_g(T, L.g, j0 >> 5, i >> 5, tm);
+                const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(bf * kTmemCols);
+                auto emit = [&](int32_t (&acc)[2 * kSl][8], int jc) {
+                    float v[8];
+                    double q4[8];
 #pragma unroll
-                for (int a = 0; a < 2 * kSl; a++)
-                    tmem_ld8(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * kTN + jc), acc[a]);
-                tmem_ld_wait();
-                float v[8];
-                double q4[8];
+                    for (int c = 0; c < 8; c++) q4[c] = 0.0;
+                    if (kDR) {
+                        for (int m = 0; m < M; m++) {
+                            const double wi = wb[(size_t)m * L.rp + i];
+                            const double2 *wc = reinterpret_cast<const double2 *>(wb + (size_t)m * L.rp + j0 + jc);
 #pragma unroll
-                for (int c = 0; c < 8; c++) q4[c] = 0.0;
-                if (kDR) {
-                    for (int m = 0; m < M; m++) {
-                        const double wi = wb[(size_t)m * L.rp + i];
-                        const double2 *wc = reinterpret_cast<const double2 *>(wb + (size_t)m * L.rp + j0 + jc);
-#pragma unroll
-                        for (int c = 0; c < 4; c++) {
-                            const double2 w2 = __ldg(wc + c);
-                            q4[2 * c] = fma(wi, w2.x, q4[2 * c]);
-                            q4[2 * c + 1] = fma(wi, w2.y, q4[2 * c + 1]);
+                            for (int c = 0; c < 4; c++) {
+                                const double2 w2 = __ldg(wc + c);
+                                q4[2 * c] = fma(wi, w2.x, q4[2 * c]);
+                                q4[2 * c + 1] = fma(wi, w2.y, q4[2 * c + 1]);
+                            }
                         }
                     }
-                }
 #pragma unroll
-                for (int c = 0; c < 8; c++) {
-                    const long long gre = ((long long)acc[0][c] << 21) + ((long long)acc[1][c] << 14) +
-                                          ((long long)acc[2][c] << 7) + (long long)acc[3][c];
-                    const long long gim = ((long long)acc[4][c] << 21) + ((long long)acc[5][c] << 14) +
-                                          ((long long)acc[6][c] << 7) + (long long)acc[7][c];
-                    const double dre = (double)gre, dim = (double)gim;
-                    const double sq = dre * dre + dim * dim;
-                    if (kDR) {
-                        const double a = (sq * ri * sm.rcol[jc + c] - q4[c]) * inv_dr;
-                        v[c] = (float)(a > 0.0 ? a : 0.0);
-                    } else {
-                        v[c] = (float)(sq * ri * sm.rcol[jc + c] * inv_m2);
+                    for (int c = 0; c < 8; c++) {
+                        const long long gre = ((long long)acc[0][c] << 21) + ((long long)acc[1][c] << 14) +
+                                              ((long long)acc[2][c] << 7) + (long long)acc[3][c];
+                        const long long gim = ((long long)acc[4][c] << 21) + ((long long)acc[5][c] << 14) +
+                                              ((long long)acc[6][c] << 7) + (long long)acc[7][c];
+                        const double dre = exact_i64_to_f64(gre), dim = exact_i64_to_f64(gim);
+                        const double sq = dre * dre + dim * dim;
+                        if (kDR) {
+                            const double a = (sq * ri * sm.rcol[bf][jc + c] - q4[c]) * inv_dr;
+                            v[c] = (float)(a > 0.0 ? a : 0.0);
+                        } else {
+                            v[c] = (float)(sq * ri * sm.rcol[bf][jc + c] * inv_m2);
+                        }
                     }
-                }
-                // direct (i, j0+jc..+7): coalesced over lanes; mirror (j0+jc..+7, i): two float4 per lane
+                    // direct (i, j0+jc..+7): coalesced over lanes; mirror (j0+jc..+7, i): two float4 per lane
 #pragma unroll
-                for (int u = 0; u < 3; u++) {
-                    if (u >= nd) break;
-                    float *dst = Ab + (size_t)td[u] * 1024 + (i & 31) + jc * 32;
+                    for (int u = 0; u < 3; u++) {
+                        if (u >= nd) break;
+                        float *dst = Ab + (size_t)td[u] * 1024 + (i & 31) + jc * 32;
 #pragma unroll
-                    for (int c = 0; c < 8; c++) dst[c * 32] = v[c];
-                }
+                        for (int c = 0; c < 8; c++) dst[c * 32] = v[c];
+                    }
 #pragma unroll
-                for (int u = 0; u < 3; u++) {
-                    if (u >= nm) break;
-                    float4 *mir = reinterpret_cast<float4 *>(Ab + (size_t)tm[u] * 1024 + (i & 31) * 32 + jc);
-                    mir[0] = make_float4(v[0], v[1], v[2], v[3]);
-                    mir[1] = make_float4(v[4], v[5], v[6], v[7]);
-                }
+                    for (int u = 0; u < 3; u++) {
+                        if (u >= nm) break;
+                        float4 *mir = reinterpret_cast<float4 *>(Ab + (size_t)tm[u] * 1024 + (i & 31) * 32 + jc);
+                        mir[0] = make_float4(v[0], v[1], v[2], v[3]);
+                        mir[1] = make_float4(v[4], v[5], v[6], v[7]);
+                    }
+                };
+                // the registers of a tcgen05.ld are valid only after tcgen05.wait::ld: tie them to it
+                auto settle = [](int32_t (&acc)[2 * kSl][8]) {
+#pragma unroll
+                    for (int a = 0; a < 2 * kSl; a++)
+#pragma unroll
+                        for (int c = 0; c < 8; c++) asm volatile("" : "+r"(acc[a][c]));
+                };
+                const int jA = 16 * h, jB = 16 * h + 8;
+                int32_t acc0[2 * kSl][8], acc1[2 * kSl][8];
+#pragma unroll
+                for (int a = 0; a < 2 * kSl; a++) tmem_ld8(tb + (uint32_t)(acc_col(a) + jA), acc0[a]);
+                tmem_ld_wait();
+                settle(acc0);
+#pragma unroll
+                for (int a = 0; a < 2 * kSl; a++) tmem_ld8(tb + (uint32_t)(acc_col(a) + jB), acc1[a]);
+                emit(acc0, jA);
+                tmem_ld_wait();
+                settle(acc1);
+                emit(acc1, jB);
             }
+            // TMEM buffer bf is free for tile n+2
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_local(&sm.tmem_empty[bf]);
         }
-        tc_fence_before();
     }
     __syncthreads();
-    if (warp == 1) tmem_dealloc(tmem, kTmemCols);
+    if (warp == 1) tmem_dealloc(tmem, 2 * kTmemCols);
 }
 
 int psf_kp(int m) { return ((2 * m + 31) / 32) * 32; }
@@ -327,6 +394,14 @@ int launch_psf(const Geo &g, const double *dist, const double *amp, int n_bins, 
     if (cudaPeekAtLastError() != cudaSuccess) return -1;
     if (n_tiles <= 0) return 1;
     const size_t smem = sizeof(PsfSmem) + 1024;
+    static int num_sms = 0;
+    if (!num_sms) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+            return -1;
+    }
+    const int n_cta = n_tiles < num_sms ? n_tiles : num_sms;
     static bool attr = false;
     if (!attr) {
         if (cudaFuncSetAttribute(psf_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
@@ -337,9 +412,9 @@ int launch_psf(const Geo &g, const double *dist, const double *amp, int n_bins, 
         attr = true;
     }
     if (wt)
-        psf_tc_kernel<true><<<n_tiles, kPsfThreads, smem, st>>>(g.m, kp, tiles, lay, opA, opB, rsc, wt, A);
+        psf_tc_kernel<true><<<n_cta, kPsfThreads, smem, st>>>(g.m, kp, n_tiles, tiles, lay, opA, opB, rsc, wt, A);
     else
-        psf_tc_kernel<false><<<n_tiles, kPsfThreads, smem, st>>>(g.m, kp, tiles, lay, opA, opB, rsc, nullptr, A);
+        psf_tc_kernel<false><<<n_cta, kPsfThreads, smem, st>>>(g.m, kp, n_tiles, tiles, lay, opA, opB, rsc, nullptr, A);
     return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
 }
 

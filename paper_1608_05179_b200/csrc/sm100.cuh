@@ -22,6 +22,9 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *b, uint32_t parity
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ void mbar_arrive_local(unsigned long long *b) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
 __device__ __forceinline__ void mbar_expect_tx(unsigned long long *b, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
 }
