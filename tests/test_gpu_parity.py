@@ -168,9 +168,13 @@ def test_psf_parity_on_oracle_keep(ctx, torch_cuda, oracle_lib, cfgname, bin_):
 
 @pytest.mark.parametrize("m,n,nk", [(24, 15, 1), (24, 15, 2), (24, 15, 31), (24, 15, 32), (24, 15, 33),
                                     (24, 15, 64), (24, 15, 65), (24, 15, 127), (24, 15, 128), (24, 15, 129),
-                                    (24, 15, 200), (13, 15, 100), (5, 15, 40), (128, 21, 300), (128, 21, 441)])
+                                    (24, 15, 200), (13, 15, 100), (5, 15, 40), (128, 21, 300), (128, 21, 441),
+                                    (200, 15, 150), (512, 21, 300), (64, 47, 2000)])
 def test_psf_ragged_sizes(ctx, torch_cuda, oracle_lib, m, n, nk):
-    """Ragged S~ (one tile, tile edges, several 128x64 tiles + tail) and odd M (K padding)."""
+    """Ragged S~ (one tile, tile edges, several 128x32 tiles + tail), odd M (K padding), K
+    steps wrapping the operand ring inside a tile (M = 200: 13 steps; M = 512 = DWC_MAX_MICS:
+    32 steps, the largest int32 level sums), and more tiles than CTAs (nk = 2000: every CTA
+    of the persistent kernel runs several tiles through both TMEM buffers)."""
     torch = torch_cuda
     g = small_geom(m, n, 3 if m % 3 == 0 else 1)
     keep = np.sort(np.random.default_rng(nk).choice(g.S, size=nk, replace=False)).astype(np.int32)
