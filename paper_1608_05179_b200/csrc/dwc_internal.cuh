@@ -178,6 +178,9 @@ __host__ __device__ inline int sym_targets_t(int T, int a, int b, int t[3]) {
     if (b == k2) t[n++] = 2 * T + a;
     return n;
 }
+__host__ __device__ inline int sym_u_tile_g(int T, int g, int I, int J) {
+    return g == 4 ? sym_u_tile_t<4>(T, I, J) : (g == 2 ? sym_u_tile_t<2>(T, I, J) : sym_u_tile_t<1>(T, I, J));
+}
 __host__ __device__ inline int sym_targets_g(int T, int g, int a, int b, int t[3]) {
     return g == 4 ? sym_targets_t<4>(T, a, b, t) : (g == 2 ? sym_targets_t<2>(T, a, b, t) : sym_targets_t<1>(T, a, b, t));
 }

@@ -7,7 +7,8 @@
 // k (in sweep order) the warps form P_k = sum_{J != k} A[I_k, I_J] x_J with the latest x --
 // U(k, J) as a row tile for J > k, U(J, k)^T for J < k, read straight from global/L2 -- then one
 // warp runs the in-block recurrence in the sweep's row order: lane l holds column l of the
-// diagonal tile in registers, each row's residual is a warp reduction, b~ enters in fp64.
+// diagonal tile in registers and row l's scaled residual (step form, one shuffle per row; the
+// block's starting residual is formed with b~ in fp64).
 #include "dwc_internal.cuh"
 
 namespace dwc {
@@ -44,20 +45,30 @@ __device__ __forceinline__ float alt_col_dot(const float *__restrict__ tile, con
     return t;
 }
 
+__device__ __forceinline__ void alt_prefetch_l2(const float *tiles, int n) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(tiles), "r"(n * 4096) : "memory");
+}
+
+// In-block recurrence in "step form" (as the main kernel): lane l owns row l; with
+// w_l = -r_l / A_ll the rows t in sweep order take delta_t = max(w_t, -x_t) (x_t + delta_t =
+// max(x_t - r_t / A_tt, 0), Eq. 14), broadcast it, and every lane applies w_l -= (A_lt / A_ll)
+// delta_t -- one shuffle per row instead of a warp reduction per row.  col[t] = D[t][l] = A_lt.
 template <bool kBack>
 __device__ __forceinline__ void alt_block_recurrence(const float col[32], double base, float &xl, float dll, int lane) {
-    // rows t in sweep order; lane l owns row l (x_l, base_l) and column l of D (col[t] = D[t][l])
+    const float inv = dll > 0.f ? 1.f / dll : 0.f;   // padding rows never move (w = 0, x = 0)
+    float part = 0.f;                                 // D x^old for row l: the in-block part of r_l
+#pragma unroll
+    for (int t = 0; t < 32; t++) part = fmaf(col[t], __shfl_sync(0xffffffffu, xl, t), part);
+    float w = (float)(-(base + (double)part) * (double)inv);
+    float sc[32];
+#pragma unroll
+    for (int t = 0; t < 32; t++) sc[t] = col[t] * inv;   // A_lt / A_ll
 #pragma unroll
     for (int tt = 0; tt < 32; tt++) {
         const int t = kBack ? 31 - tt : tt;
-        float part = col[t] * xl;                                 // D[t][l] x_l
-#pragma unroll
-        for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-        if (lane == t && dll > 0.f) {
-            const double r = base + (double)part;                 // residual of row t (Eq. 13)
-            const float v = (float)((double)xl - r / (double)dll);
-            xl = v > 0.f ? v : 0.f;                                // Eq. 14 projection
-        }
+        const float d = __shfl_sync(0xffffffffu, fmaxf(w, -xl), t);
+        if (lane == t) xl += d;
+        w = fmaf(-sc[t], d, w);
     }
 }
 
@@ -79,14 +90,28 @@ gs_alt_kernel(const BinLayout *__restrict__ lay, const float *__restrict__ A, co
         const bool back = it & 1;
         for (int kk = 0; kk < T; kk++) {
             const int k = back ? T - 1 - kk : kk;
+            // the next step's tiles into L2 while this step runs (they do not depend on x): its row
+            // runs (one contiguous run per owner group of the layout) and its column tiles
+            if (lane == 0) {
+                const bool last = kk + 1 == T;
+                const int kn = last ? (back ? 0 : T - 1) : (back ? k - 1 : k + 1);
+                if (w == 0)
+                    for (int o = 0; o < g; o++) {
+                        const int len = sym_run_len(T, g, kn, o);
+                        if (len > 0) alt_prefetch_l2(Ab + (size_t)sym_run_start(T, g, kn, o) * 1024, len);
+                    }
+                for (int J = w; J < kn; J += kAltWarps) alt_prefetch_l2(Ab + (size_t)sym_u_tile_g(T, g, J, kn) * 1024, 1);
+            }
             // P_k over the other column blocks, with the latest x
             float acc[4] = {0.f, 0.f, 0.f, 0.f};
             float acc_t = 0.f;
-            for (int J = w; J < T; J += kAltWarps) {
-                if (J == k) continue;
-                if (J > k) alt_row_dot(Ab + (size_t)sym_u_tile(T, g, k, J) * 1024, xs + 32 * J, rq, cq, acc);
-                else acc_t += alt_col_dot(Ab + (size_t)sym_u_tile(T, g, J, k) * 1024, xs + 32 * J, lane);
-            }
+#pragma unroll 2
+            for (int J = w; J < k; J += kAltWarps)
+                acc_t += alt_col_dot(Ab + (size_t)sym_u_tile_g(T, g, J, k) * 1024, xs + 32 * J, lane);
+            const int J1 = k + 1 + ((w - (k + 1)) % kAltWarps + kAltWarps) % kAltWarps;   // first J > k with J = w mod 8
+#pragma unroll 2
+            for (int J = J1; J < T; J += kAltWarps)
+                alt_row_dot(Ab + (size_t)sym_u_tile_g(T, g, k, J) * 1024, xs + 32 * J, rq, cq, acc);
 #pragma unroll
             for (int q = 0; q < 4; q++) {
                 acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], 8);
