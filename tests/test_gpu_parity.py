@@ -472,3 +472,49 @@ def test_errors_flags_and_new_entry_points(ctx, torch_cuda):
     assert lib().dwc_keep_mask(ctx._h, 1, 0, nk.data_ptr(), keep.data_ptr(), x.data_ptr(), None) == -1
     # the context still works
     ctx.solve_band(g, band.freqs, csm, 0.1, 5, dr=True, order=3)
+
+
+# ---------------------------------------------------------------------------- degenerate inputs
+@pytest.mark.gpu
+def test_zero_csm_bin_in_a_batch(ctx, torch_cuda, oracle_lib):
+    """A bin with C = 0 (max|b| = 0, reading R6): b = 0, only the coarsest level G^0 is kept and
+    x = 0; the other bins of the same batch are bit-identical to solving them alone."""
+    torch = torch_cuda
+    band = synth.make_band("cfg2", bins=[0, 3, 6])
+    cfg = band.cfg
+    g = geom_of(band)
+    csm = band.csm.copy()
+    csm[1] = 0.0
+    out = ctx.solve_band(g, band.freqs, torch.from_numpy(csm).cuda(), cfg.epsilon, 200, cfg.eps_mode, want_b=True)
+    nk = out["n_keep"].cpu().numpy()
+    keep = out["keep_idx"].cpu().numpy()
+    n = cfg.n
+    J = int(np.floor(np.log2(n)))
+    h = 2 ** J
+    g0 = sorted(r * n + c for r in range(0, n, h) for c in range(0, n, h))
+    assert nk[1] == len(g0) == 4
+    assert list(keep[1][:4]) == g0 and np.all(keep[1][4:] == -1)
+    assert np.all(out["x_map"].cpu().numpy()[1] == 0.0)
+    assert np.all(out["b_map"].cpu().numpy()[1] == 0.0)
+    for k in (0, 2):
+        solo = ctx.solve_band(g, band.freqs[k:k + 1], torch.from_numpy(band.csm[k:k + 1]).cuda(), cfg.epsilon, 200,
+                              cfg.eps_mode)
+        assert nk[k] == solo["n_keep"].cpu().numpy()[0]
+        assert np.array_equal(out["x_map"].cpu().numpy()[k], solo["x_map"].cpu().numpy()[0])
+
+
+@pytest.mark.gpu
+def test_absolute_threshold_mode_matches_relative(ctx, torch_cuda):
+    """eps_mode = 1 (absolute) with eps_abs = eps * max|b| selects the same kept set and map as
+    the relative mode (reading R6: eps_eff = eps * max_s |b_s|)."""
+    torch = torch_cuda
+    band = synth.make_band("cfg2", bins=[2])
+    cfg = band.cfg
+    g = geom_of(band)
+    csm = torch.from_numpy(band.csm).cuda()
+    rel = ctx.solve_band(g, band.freqs, csm, cfg.epsilon, 100, 0, want_b=True)
+    bmax = float(np.max(np.abs(rel["b_map"].cpu().numpy()[0])))
+    ab = ctx.solve_band(g, band.freqs, csm, cfg.epsilon * bmax, 100, 1)
+    assert np.array_equal(rel["n_keep"].cpu().numpy(), ab["n_keep"].cpu().numpy())
+    assert np.array_equal(rel["keep_idx"].cpu().numpy(), ab["keep_idx"].cpu().numpy())
+    assert np.array_equal(rel["x_map"].cpu().numpy(), ab["x_map"].cpu().numpy())
