@@ -41,3 +41,14 @@ for n in sorted(set([int(srt[0]), int(srt[len(srt) // 8]), 768, 512])):
     ms = e0.elapsed_time(e1)
     T = (n + 31) // 32
     print("alone n=%d T=%d: %.2f ms = %.3f us/step" % (n, T, ms, ms * 1e3 / (T * cfg.sweeps)))
+
+# the band restricted to its largest bins: how the chain of the largest bin stretches with the
+# number of large bins running beside it
+order = np.argsort(-nk, kind="stable")
+for top in (1, 8, 16, 37, 74, 128):
+    sel = np.sort(order[:top])
+    sub = torch.from_numpy(band.csm[sel]).cuda()
+    for _ in range(2):
+        ctx.solve_band(geom, band.freqs[sel], sub, cfg.epsilon, cfg.sweeps, cfg.eps_mode, full_grid=cfg.full_grid)
+    torch.cuda.synchronize()
+    print("top %3d bins (S~ %d..%d): GS %.2f ms" % (top, nk[order[0]], nk[order[top - 1]], ctx.stats()["ms_gs"]))
