@@ -80,9 +80,10 @@ int launch_steer(const Geo &g, const double *dist, const double *amp, const doub
 // S2 as a register-blocked triangular complex GEMM.  With the half-Hermitian matrix
 //   Ch[m][n] = H[m][n] (n > m),  H[m][m] / 2 (n = m),  0 (n < m),   H = (C + C^H)/2,
 // b_s = 2 Re(e_s^H Ch e_s) / M^2 -- the Hermitian form at half the flops.  A CTA = P scan points
-// of one bin (P = 64, or 32 when Mp > 64); their steering vectors Es[n][p] (Mp x P complex,
+// of one bin (P = 64 with 4 warps, 2 points per lane, when Mp <= 64; else P = 32 with 8 warps,
+// 1 point per lane); their steering vectors Es[n][p] (Mp x P complex,
 // Mp = M rounded up to 8, zero rows beyond M) in shared memory.  Warp w owns the row-group
-// pairs (q, G-1-q), q = w, w+8, ... (G = Mp/4 groups of 4 rows), paired so every warp has the
+// pairs (q, G-1-q), q = w, w+NW, ... (G = Mp/4 groups of 4 rows), paired so every warp has the
 // same triangular work, and stages those 8 rows of Ch in its own shared-memory slice.  Lane l
 // owns points l (+32).  Per n a thread reads 8 row entries (broadcast LDS.128) and e_n of its
 // points and does 8 or 16 complex MACs; W = Ch e stays in registers; the epilogue reduces
@@ -130,15 +131,15 @@ __device__ __forceinline__ void das_rows(const double2 *__restrict__ Cw, const d
     }
 }
 
-template <int PPL>
-__global__ void __launch_bounds__(kDasThreads, 2)
+template <int PPL, int NW>
+__global__ void __launch_bounds__(32 * NW, 2)
 das_kernel(Geo g, const double *__restrict__ dist, const double *__restrict__ amp,
            const double *__restrict__ freq, const double2 *__restrict__ Ch, int Mp, double *__restrict__ b, int dr) {
     constexpr int P = 32 * PPL;
     extern __shared__ double2 smem_d2[];
     double2 *Es = smem_d2;                       // [Mp][P]
     double2 *Cw = smem_d2 + (size_t)Mp * P;      // [warp][8 rows][Mp]
-    __shared__ double part[kDasWarps][P];
+    __shared__ double part[NW][P];
     const int M = g.m;
     const int bin = blockIdx.y;
     const int s0 = blockIdx.x * P;
@@ -146,11 +147,11 @@ das_kernel(Geo g, const double *__restrict__ dist, const double *__restrict__ am
     // steering vectors of the CTA's points: the (dist, amp) table entries of 8 elements per
     // thread are loaded before any is used, so their latency is paid once per 8 (not per element)
     constexpr int kEU = 8;
-    for (int base = 0; base < Mp * P; base += kDasThreads * kEU) {
+    for (int base = 0; base < Mp * P; base += (32 * NW) * kEU) {
         double dd[kEU], aa[kEU];
 #pragma unroll
         for (int u = 0; u < kEU; u++) {
-            const int t = base + u * kDasThreads + threadIdx.x;
+            const int t = base + u * (32 * NW) + threadIdx.x;
             const int m = t / P, s = s0 + t % P;
             const bool ok = t < Mp * P && m < M && s < g.S;
             dd[u] = ok ? __ldg(dist + (size_t)m * g.S + s) : 0.0;
@@ -158,7 +159,7 @@ das_kernel(Geo g, const double *__restrict__ dist, const double *__restrict__ am
         }
 #pragma unroll
         for (int u = 0; u < kEU; u++) {
-            const int t = base + u * kDasThreads + threadIdx.x;
+            const int t = base + u * (32 * NW) + threadIdx.x;
             if (t < Mp * P) Es[t] = (aa[u] >= 0.0) ? steer_elem(dd[u], aa[u], k) : make_double2(0.0, 0.0);
         }
     }
@@ -170,7 +171,7 @@ das_kernel(Geo g, const double *__restrict__ dist, const double *__restrict__ am
     double acc[PPL];
 #pragma unroll
     for (int j = 0; j < PPL; j++) acc[j] = 0.0;
-    for (int qa = w; qa < G / 2; qa += kDasWarps) {
+    for (int qa = w; qa < G / 2; qa += NW) {
         const int qb = G - 1 - qa;
         __syncwarp();
         for (int t = lane; t < 8 * Mp; t += 32) {   // rows 4qa..4qa+3, 4qb..4qb+3 of Ch (cp.async:
@@ -203,7 +204,7 @@ das_kernel(Geo g, const double *__restrict__ dist, const double *__restrict__ am
     if (threadIdx.x < P && s0 + (int)threadIdx.x < g.S) {
         double v = 0.0;
 #pragma unroll
-        for (int q = 0; q < kDasWarps; q++) v += part[q][threadIdx.x];
+        for (int q = 0; q < NW; q++) v += part[q][threadIdx.x];
         if (dr) {   // R20: normalised by M^2 - M, negative values clamped (the diagonal is already gone)
             const double bv = 2.0 * v / ((double)M * (double)M - (double)M);
             b[(size_t)bin * g.S + s0 + threadIdx.x] = bv > 0.0 ? bv : 0.0;
@@ -245,24 +246,27 @@ int launch_das(const Geo &g, const double *dist, const double *amp, int n_bins,
                const double *freq, const double *csm_half, double *b, int dr, cudaStream_t st) {
     const int Mp = das_mpad(g.m);
 #ifndef DAS_P64
-#define DAS_P64 0
+#define DAS_P64 1
 #endif
-    const int P = (Mp <= 64 && DAS_P64) ? 64 : 32;   // 32 points: Es + Cw <= 96 KB -> two CTAs per SM (M <= 64)
-    const size_t smem = (size_t)16 * Mp * (P + 8 * kDasWarps);
+    // 32 points x 8 warps (Es + Cw <= 96 KB -> two CTAs per SM for M <= 64); DAS_P64: 64 points
+    // (2 per lane) x 4 warps, same shared memory, twice the DFMA per shared-memory load
+    const int P = (Mp <= 64 && DAS_P64) ? 64 : 32;
+    const int NWv = (P == 64) ? 4 : kDasWarps;
+    const size_t smem = (size_t)16 * Mp * (P + 8 * NWv);
     if (smem > 220 * 1024) return -1;
     static size_t attr2 = 0, attr1 = 0;
     size_t &attr = (P == 64) ? attr2 : attr1;
     if (smem > attr) {
-        const cudaError_t e = (P == 64) ? cudaFuncSetAttribute(das_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
-                                        : cudaFuncSetAttribute(das_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const cudaError_t e = (P == 64) ? cudaFuncSetAttribute(das_kernel<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                                        : cudaFuncSetAttribute(das_kernel<1, kDasWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return -1;
         attr = smem;
     }
     dim3 grid((g.S + P - 1) / P, n_bins);
     if (P == 64)
-        das_kernel<2><<<grid, kDasThreads, smem, st>>>(g, dist, amp, freq, (const double2 *)csm_half, Mp, b, dr);
+        das_kernel<2, 4><<<grid, 128, smem, st>>>(g, dist, amp, freq, (const double2 *)csm_half, Mp, b, dr);
     else
-        das_kernel<1><<<grid, kDasThreads, smem, st>>>(g, dist, amp, freq, (const double2 *)csm_half, Mp, b, dr);
+        das_kernel<1, kDasWarps><<<grid, kDasThreads, smem, st>>>(g, dist, amp, freq, (const double2 *)csm_half, Mp, b, dr);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
