@@ -254,14 +254,10 @@ int launch_das(const Geo &g, const double *dist, const double *amp, int n_bins,
     const int NWv = (P == 64) ? 4 : kDasWarps;
     const size_t smem = (size_t)16 * Mp * (P + 8 * NWv);
     if (smem > 220 * 1024) return -1;
-    static size_t attr2 = 0, attr1 = 0;
-    size_t &attr = (P == 64) ? attr2 : attr1;
-    if (smem > attr) {
-        const cudaError_t e = (P == 64) ? cudaFuncSetAttribute(das_kernel<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
-                                        : cudaFuncSetAttribute(das_kernel<1, kDasWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return -1;
-        attr = smem;
-    }
+    // set on every call: the attribute is per device, and a process may drive several devices
+    const cudaError_t e = (P == 64) ? cudaFuncSetAttribute(das_kernel<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                                    : cudaFuncSetAttribute(das_kernel<1, kDasWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return -1;
     dim3 grid((g.S + P - 1) / P, n_bins);
     if (P == 64)
         das_kernel<2, 4><<<grid, 128, smem, st>>>(g, dist, amp, freq, (const double2 *)csm_half, Mp, b, dr);

@@ -394,23 +394,15 @@ int launch_psf(const Geo &g, const double *dist, const double *amp, int n_bins, 
     if (cudaPeekAtLastError() != cudaSuccess) return -1;
     if (n_tiles <= 0) return 1;
     const size_t smem = sizeof(PsfSmem) + 1024;
-    static int num_sms = 0;
-    if (!num_sms) {
-        int dev = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess ||
-            cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-            return -1;
-    }
+    // queried and set on every call: both are per device, and a process may drive several
+    int dev = 0, num_sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || num_sms < 1)
+        return -1;
     const int n_cta = n_tiles < num_sms ? n_tiles : num_sms;
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(psf_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-                cudaSuccess ||
-            cudaFuncSetAttribute(psf_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-                cudaSuccess)
-            return -1;
-        attr = true;
-    }
+    if (cudaFuncSetAttribute(wt ? psf_tc_kernel<true> : psf_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+        return -1;
     if (wt)
         psf_tc_kernel<true><<<n_cta, kPsfThreads, smem, st>>>(g.m, kp, n_tiles, tiles, lay, opA, opB, rsc, wt, A);
     else
