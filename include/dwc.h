@@ -175,7 +175,10 @@ DWC_API dwc_status dwc_psf(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *g
 /* S7: `sweeps` forward projected Gauss-Seidel sweeps from x0 = 0 on one system.
  * A dev float[n*n] row-major, symmetric (as A~ is, reading R1) with A_ii > 0: only the upper
  * triangle (j >= i) is read, the lower one is taken as its transpose.
- * flags: 0 or DWC_ALT_SWEEPS; b dev double[n], x dev float[n] (out). */
+ * flags: 0 or DWC_ALT_SWEEPS; b dev double[n], x dev float[n] (out).
+ * Errors: DWC_EINVAL (n < 1, sweeps < 1, NULL, unknown flags, n beyond the on-chip x capacity),
+ * DWC_ENUMERIC (some A_ii <= 0 or non-finite: checked on the device and read back, so this
+ * call synchronises `cuda_stream` once before the sweeps), DWC_ECUDA. */
 DWC_API dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int32_t sweeps,
                   int32_t flags, float *x, void *cuda_stream);
 

@@ -643,6 +643,13 @@ dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int3
         return fail(DWC_EINVAL, "n = %d exceeds the on-chip x capacity", n);
     cudaStream_t st = (cudaStream_t)cuda_stream;
     int launches = 0;
+    // precondition A_ii > 0: checked on the device, read back before the sweeps
+    if ((s = ensure(ctx, ctx->flag, 64)) || (s = ensure_pin(ctx->readback, 64))) return s;
+    CU(cudaMemsetAsync(ctx->flag.p, 0, sizeof(int), st));
+    LAUNCH(launch_diag_check(n, A, (int *)ctx->flag.p, st));
+    CU(cudaMemcpyAsync(ctx->readback.p, ctx->flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    if (*(int *)ctx->readback.p & 2) return fail(DWC_ENUMERIC, "A has a diagonal entry <= 0 or non-finite");
     BinLayout lay{n, sp, 0, 0, 0, gs_group_size(n), 0};
     std::vector<int32_t> order{0};
     int32_t nk0 = n;

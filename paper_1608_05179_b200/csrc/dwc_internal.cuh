@@ -214,6 +214,9 @@ int launch_gs_prep(int n_bins, int max_sp, const BinLayout *lay_dev, const float
 int launch_gs_alt(int n_bins, const BinLayout *lay_dev, int max_sp, const float *A, const double *bt, int sweeps,
                   float *x_out, float *x_map, const int32_t *keep_idx, int S, cudaStream_t st);
 
+// dwc_gs precondition: bit 2 of *flag set when some A_ii <= 0 or non-finite (k_keep.cu).
+int launch_diag_check(int n, const float *A, int *flag, cudaStream_t st);
+
 // Keep-set bitmasks (k_keep.cu): ceil(S/32) uint32 words per bin.
 int launch_keep_mask(int n_bins, int S, const int32_t *n_keep, const int32_t *keep_idx, uint32_t *mask,
                      cudaStream_t st);

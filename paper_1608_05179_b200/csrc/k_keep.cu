@@ -77,4 +77,17 @@ int launch_keep_unmask(int n_bins, int S, const uint32_t *mask, int32_t *n_keep,
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
+// dwc_gs precondition: every A_ii > 0 and finite; sets bit 2 of *flag otherwise.
+__global__ void diag_check_kernel(int n, const float *__restrict__ A, int *__restrict__ flag) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const float v = A[(size_t)i * n + i];
+        if (!(v > 0.f) || !isfinite(v)) atomicOr(flag, 2);
+    }
+}
+
+int launch_diag_check(int n, const float *A, int *flag, cudaStream_t st) {
+    diag_check_kernel<<<(n + 255) / 256 < 148 ? (n + 255) / 256 : 148, 256, 0, st>>>(n, A, flag);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
 }  // namespace dwc

@@ -467,6 +467,15 @@ def test_errors_flags_and_new_entry_points(ctx, torch_cuda):
     with pytest.raises(DwcError):   # S~ beyond the GS kernel's on-chip x capacity (rejected before any launch)
         n = 20000
         ctx.gs(torch.zeros((n, n), dtype=torch.float32).cuda(), torch.zeros(n, dtype=torch.float64).cuda(), 1)
+    # A_ii <= 0 -> DWC_ENUMERIC, detected on the device before any sweep
+    Abad = torch.eye(40, dtype=torch.float32).cuda()
+    Abad[17, 17] = 0.0
+    with pytest.raises(DwcError) as ei:
+        ctx.gs(Abad, torch.ones(40, dtype=torch.float64).cuda(), 3)
+    assert ei.value.code == -3
+    Abad[17, 17] = float("nan")
+    with pytest.raises(DwcError):
+        ctx.gs(Abad, torch.ones(40, dtype=torch.float64).cuda(), 3)
     # keep masks: n_bins 0 is a no-op, S < 1 rejected
     assert lib().dwc_keep_mask(ctx._h, 0, 10, None, None, None, None) == 0
     assert lib().dwc_keep_mask(ctx._h, 1, 0, nk.data_ptr(), keep.data_ptr(), x.data_ptr(), None) == -1
