@@ -130,6 +130,19 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *b, uint32_t parity
         "r"(parity)
         : "memory");
 }
+// CTA-scope acquire, for barriers completed only by this CTA's own threads or by its own bulk
+// copies (ring, staging, the leader's x-ready): no L1 invalidation (ptxas emits CCTL.IVALL for
+// the cluster-scope acquire above, which the barriers completed by other CTAs -- partial sums,
+// the non-leaders' x-ready -- need).
+__device__ __forceinline__ void mbar_wait_cta(unsigned long long *b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "C_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra C_%=;\n\t}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_local(unsigned long long *b) {
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
@@ -338,7 +351,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                     for (int off = 0; off < sd[sg].len; off += kChunk) {
                         const int tt = sd[sg].t0 + off, nt = min(kChunk, sd[sg].len - off);
                         if (ppf) t0 = clock64();
-                        mbar_wait(&sh.empty[slot], ph ^ 1);
+                        mbar_wait_cta(&sh.empty[slot], ph ^ 1);
                         if (ppf) { const unsigned long long t = clock64(); p_wait += t - t0; t0 = t; }
                         mbar_expect_tx(&sh.full[slot], (uint32_t)nt * kTile * 4);
                         if (prof) sh.issue_t[slot] = clock64();
@@ -357,7 +370,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 for (int s = 0, kn = 0, sl = 0; s < total;
                      s++, kn = (kn + 1 == T) ? 0 : kn + 1, sl = (sl + 1 == kStg) ? 0 : sl + 1) {
                     const int kn2 = (kn + 2 >= T) ? kn + 2 - T : kn + 2;   // (mod T again for T < 2)
-                    mbar_wait(&sh.stg_empty[sl], ((s / kStg) & 1) ^ 1);
+                    mbar_wait_cta(&sh.stg_empty[sl], ((s / kStg) & 1) ^ 1);
                     mbar_expect_tx(&sh.stg_full[sl], 3 * kTile * 4 + kPacketBytes);
                     bulk_g2s(sh.rs[kRing * kChunk + 3 * (sl) + 0], Ab + (size_t)(T + kn) * kTile, kTile * 4, &sh.stg_full[sl]);   // L_kn
                     bulk_g2s(sh.rs[kRing * kChunk + 3 * (sl) + 1], Ab + (size_t)kn * kTile, kTile * 4, &sh.stg_full[sl]);         // D_kn
@@ -401,8 +414,13 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 // Non-leader: arm x-ready for solver step s-2 first (its previous phase, step s-4,
                 // was observed by this warp at step s-1), since the waits below may target it.
                 if (!is_leader && c == 0 && lane == 0 && s >= 2) mbar_expect_tx(&sh.xr[s & 1], 128);
-                if (s >= 3) mbar_wait(&sh.xr[(s - 3) & 1], ((s - 3) >> 1) & 1);
-                else if (s == 2) mbar_wait(&sh.xr[0], 0);
+                if (s >= 3) {
+                    if (is_leader) mbar_wait_cta(&sh.xr[(s - 3) & 1], ((s - 3) >> 1) & 1);
+                    else mbar_wait(&sh.xr[(s - 3) & 1], ((s - 3) >> 1) & 1);
+                } else if (s == 2) {
+                    if (is_leader) mbar_wait_cta(&sh.xr[0], 0);
+                    else mbar_wait(&sh.xr[0], 0);
+                }
                 // leader: arm this step's P-ready (its previous phase, step s-2, is complete)
                 if (is_leader && c == 0 && lane == 0) mbar_expect_tx(&sh.pready[s & 1], (uint32_t)(g * kCons * 128));
                 if (pf) { const unsigned long long t = clock64(); cw_x += t - tA; tA = t; }
@@ -410,10 +428,10 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 float acc_t = 0.f;   // row `lane` of P_kn from transposed tiles and y
                 if (do_L || do_D) {
                     const int b = s % kStg;
-                    mbar_wait(&sh.stg_full[b], (s / kStg) & 1);
+                    mbar_wait_cta(&sh.stg_full[b], (s / kStg) & 1);
                     // L: x_kx^old (last updated at step s-1-T); D: x_kn^old (step s-T).  With T <= 2
                     // those may be step s-2.
-                    if (T <= 2 && s >= 2) mbar_wait(&sh.xr[s & 1], ((s - 2) >> 1) & 1);
+                    if (T <= 2 && s >= 2) mbar_wait_cta(&sh.xr[s & 1], ((s - 2) >> 1) & 1);
                     if (do_L) {
                         // L_kn x_kx^old + the carried LL_kn x_{kn-2}^old; then LL_{kn+1} x_kx^old
                         // (tile staged at step s-1) for the next step, while x_kx is still old
@@ -447,7 +465,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                             // every warp observes and releases every chunk (parity-tracked barriers: no
                             // warp may fall a ring lap behind or run one ahead)
                             const unsigned long long tw0 = pf ? clock64() : 0ull;
-                            mbar_wait(&sh.full[slot], ph);
+                            mbar_wait_cta(&sh.full[slot], ph);
                             if (pf) {
                                 const unsigned long long t = clock64();
                                 cw_full += t - tA; tA = t;
@@ -490,7 +508,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 if (do_D && s >= 2) {
                     // forward x of solver step s-2 to the sub-group's other CTAs (they need it from
                     // their step s+1 on); after this step's partial so P_s never waits for it
-                    if (T > 2) mbar_wait(&sh.xr[s & 1], ((s - 2) >> 1) & 1);
+                    if (T > 2) mbar_wait_cta(&sh.xr[s & 1], ((s - 2) >> 1) & 1);
                     push_x(s - 2);
                 }
                 if (pf) { const unsigned long long t = clock64(); c_red += t - tA; tA = t; }
@@ -564,7 +582,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                     xo[0] = v.x; xo[1] = v.y; xo[2] = v.z; xo[3] = v.w;
                 }
             };
-            mbar_wait(&sh.stg_full[0], 0);
+            mbar_wait_cta(&sh.stg_full[0], 0);
             prepare(0);
             // operands of the next block, loaded ahead of the recurrence (latency hidden)
             float n_invd[4], n_xo[4], n_wg[6], n_bhi[4], n_blo[4];
@@ -626,7 +644,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 if (prev_row0 >= 0) publish(j - 1, prev_row0);
                 if (pf) { const unsigned long long t = clock64(); c_pub += t - tA; tA = t; }
                 if (has_next) {
-                    mbar_wait(&sh.stg_full[sl1], ((j + 1) / kStg) & 1);
+                    mbar_wait_cta(&sh.stg_full[sl1], ((j + 1) / kStg) & 1);
                     fetch_next(j + 1, kn1);
                 }
                 if (pf) { const unsigned long long t = clock64(); c_set += t - tA; tA = t; }
