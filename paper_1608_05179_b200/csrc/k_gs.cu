@@ -817,7 +817,16 @@ int gs_cluster_size() { return kCl; }
 int gs_item_ints() { return (int)(sizeof(GsItem) / sizeof(int)); }
 
 // CTAs per bin from S~ alone (batch-independent => bit-identical per-bin results).
-int gs_group_size(int nk) { return nk >= 768 ? 4 : (nk >= 384 ? 2 : 1); }
+// Thresholds 896 / 448 (28 / 14 row blocks): measured best on cfg3 (GS 48.8-49.1 ms; 768 / 384:
+// 50.1, 1024 / 512: 60.0, 640 / 320: 55.0; scripts/gs_group_sweep.sh), neutral on cfg2 and cfg5.
+// The band is bound both by the largest bin's chain and by the CTA-steps all bins occupy; more
+// CTAs per medium bin shorten chains that are not the longest but cost slots.
+// DWC_GS_G4 / DWC_GS_G2 override them (experiments).
+int gs_group_size(int nk) {
+    static const int t4 = getenv("DWC_GS_G4") ? atoi(getenv("DWC_GS_G4")) : 896;
+    static const int t2 = getenv("DWC_GS_G2") ? atoi(getenv("DWC_GS_G2")) : 448;
+    return nk >= t4 ? 4 : (nk >= t2 ? 2 : 1);
+}
 
 int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_sp, int ystride, int *counter,
               const float *A,

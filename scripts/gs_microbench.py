@@ -30,7 +30,7 @@ def main():
         ms = e0.elapsed_time(e1)
         T = (n + 31) // 32
         steps = sweeps * T
-        g = 4 if n >= 768 else (2 if n >= 384 else 1)
+        g = 4 if n >= 896 else (2 if n >= 448 else 1)
         gbs = 4.0 * (32 * T) ** 2 * sweeps / (ms / 1e3) / 1e9
         print(f"n={n:5d} T={T:4d} g={g} ms={ms:9.3f} ns/step={1e6 * ms / steps:8.1f} GB/s={gbs:8.1f}", flush=True)
 
