@@ -25,7 +25,8 @@
 //    2,3,5,6,7 consumers (in the leader 6 = D product, 7 = L/LL products).  The producer streams
 //    this CTA's runs of each step with cp.async.bulk (<= 6 tiles per copy, mbarrier complete_tx)
 //    into a shared-memory ring (2 slots of 24 KB; non-leader CTAs also use the staging area: 3), running
-//    ahead across steps (tiles do not depend on x) and prefetching runs 4 steps ahead into L2.
+//    ahead across steps (tiles do not depend on x); an L2 prefetch of the runs n steps ahead is
+//    available with -DGS_PF=n (off by default: measured not to pay).
 //  * Clusters of kCl = 4 CTAs.  A work item gives the cluster either one large bin (sub-group of
 //    g = 4 CTAs), two medium bins (g = 2) or four small bins (g = 1).  Inside a sub-group every
 //    CTA keeps a full copy of x in shared memory; column blocks are owned by CTAs in a periodic
@@ -58,9 +59,12 @@ constexpr int kCons = kWarps - 3;  // consumer warps (3..7)
 constexpr int kChunk = GS_CHUNK;   // tiles per ring slot (one contiguous bulk copy)
 constexpr int kRing = GS_RING;     // stream ring slots of the leader
 #ifndef GS_PF
-#define GS_PF 4
+#define GS_PF 0
 #endif
-constexpr int kPf = GS_PF;         // L2 prefetch distance of the stream runs, in steps
+// L2 prefetch distance of the stream runs, in steps.  Off: with the current CTA-per-bin
+// thresholds it no longer pays (cfg3 GS 48.3 ms without, 49.3 with 4 steps, 51.0 with 6; cfg2,
+// cfg5 neutral; scripts/ab_multi.sh); -DGS_PF=n re-enables it.
+constexpr int kPf = GS_PF;
 constexpr double kL2WindowBytes = 48.0 * 1024 * 1024;   // L2 share the prefetch window may use
 constexpr int kTile = 1024;        // floats per tile
 #ifndef GS_KSTG
