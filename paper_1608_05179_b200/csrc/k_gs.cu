@@ -268,7 +268,10 @@ __device__ __forceinline__ float tile_tdot(const float *__restrict__ tile, const
 // Stream step s computes P for block kn = s mod T excluding kx = (s-1) mod T.  Stream tiles
 // of sub-group rank rg: J in [0,T), J mod g == rg, J != kx, J != kn.  The leader also stages
 // tile (kn,kx) (L, for the solver) and (kn,kn) (D, solver + its old-x product).
-__global__ void __launch_bounds__(kThreads, 2)
+#ifndef GS_MINB
+#define GS_MINB 2
+#endif
+__global__ void __launch_bounds__(kThreads, GS_MINB)
 gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout *__restrict__ lay,
                   int *__restrict__ counter, const float *__restrict__ A, const GsPacket *__restrict__ packets,
                   int sweeps, float *__restrict__ x_out, float *__restrict__ x_map,
@@ -862,6 +865,8 @@ int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_s
         cudaGetLastError();
         n_clusters = num_sms / kCl;
     }
+    static const int cl_env = getenv("DWC_GS_CLUSTERS") ? atoi(getenv("DWC_GS_CLUSTERS")) : 0;   // experiment
+    if (cl_env > 0 && cl_env < n_clusters) n_clusters = cl_env;
     if (n_clusters > n_items) n_clusters = n_items;
     if (n_clusters < 1) n_clusters = 1;
     cfg.gridDim = dim3(n_clusters * kCl);
