@@ -41,6 +41,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "dwc_internal.cuh"
 
@@ -286,6 +287,8 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
     int *ordOf = ownJ + (xcap / 32);                             // J -> ordinal (-1: not owned)
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint32_t crank = cluster_rank();
+    auto gtime = []() { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; };
+    if (prof && tid == 0 && blockIdx.x < 1024) prof[32 + 2 * blockIdx.x] = gtime();   // CTA start (ns)
 
     for (;;) {
         // ---- the cluster's next item: rank 0 pops and writes it into every CTA
@@ -295,7 +298,10 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
         }
         cluster_sync();
         const int item = sh.item;
-        if (item >= n_items) break;
+        if (item >= n_items) {
+            if (prof && tid == 0 && blockIdx.x < 1024) prof[33 + 2 * blockIdx.x] = gtime();   // CTA idle from here
+            break;
+        }
         const GsItem IT = items[item];
         const int g = IT.g;   // 1, 2 or 4
         const int sg = (int)crank / g, rg = (int)crank % g;
@@ -843,8 +849,8 @@ int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_s
     static const bool profile = getenv("DWC_GS_PROFILE") != nullptr;
     unsigned long long *prof = nullptr;
     if (profile) {
-        cudaMalloc(&prof, 32 * sizeof(unsigned long long));
-        cudaMemsetAsync(prof, 0, 32 * sizeof(unsigned long long), st);
+        cudaMalloc(&prof, (32 + 2048) * sizeof(unsigned long long));
+        cudaMemsetAsync(prof, 0, (32 + 2048) * sizeof(unsigned long long), st);
     }
     const size_t smem = gs_smem_bytes(max_sp, ystride);
     cudaFuncSetAttribute(gs_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -891,9 +897,20 @@ int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_s
                                        (const GsPacket *)packets, sweeps, x_out, x_map, keep_idx, S, max_sp, ystride,
                                        pf, prof);
     if (profile) {
-        unsigned long long h[32];
+        static unsigned long long h[32 + 2048];
         cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, st);
         cudaStreamSynchronize(st);
+        {   // when each CTA ran out of items, relative to the first CTA start: the band's tail
+            const int nc = std::min(n_clusters * kCl, 1024);
+            unsigned long long t0 = ~0ull;
+            std::vector<double> idle;
+            for (int c = 0; c < nc; c++) t0 = std::min(t0, h[32 + 2 * c]);
+            for (int c = 0; c < nc; c++) idle.push_back((h[33 + 2 * c] - t0) * 1e-6);
+            std::sort(idle.begin(), idle.end());
+            if (!idle.empty())
+                fprintf(stderr, "[gs-prof] CTAs out of items at (ms): min %.2f p10 %.2f median %.2f p90 %.2f max %.2f\n",
+                        idle.front(), idle[idle.size() / 10], idle[idle.size() / 2], idle[idle.size() * 9 / 10], idle.back());
+        }
         const double n = h[9] ? (double)h[9] : 1.0;
         fprintf(stderr,
                 "[gs-prof] steps=%llu grid=%d | solver cyc/step: wait_P %.0f wait_stg %.0f sum+publish %.0f fetch %.0f recur %.0f post %.0f prep %.0f"
