@@ -94,17 +94,51 @@ int launch_psf(const Geo &g, const double *dist, const double *amp, int n_bins, 
 // solver, L and D warps and streams with 3 warps, the others with 5, so for g = 4 the leader
 // owns 3 of every 18 column blocks (period 0123123 0123123 0123, 5 each for 1..3), for g = 2 3
 // of every 8 (01101101).
-__host__ __device__ inline int own_period(int g) { return g == 4 ? 18 : (g == 2 ? 8 : 1); }
-__host__ __device__ inline int own_weight(int g, int o) { return g == 4 ? (o == 0 ? 3 : 5) : (g == 2 ? (o == 0 ? 3 : 5) : 1); }
+// GS_PAT4 / GS_PAT2 (experiment): period of the g = 4 / g = 2 pattern, the leader owning
+// period - 15 / period - 5 blocks of it (17, 18, 19 / 7, 8, 9); defaults 18 and 8.
+#ifndef GS_PAT4
+#define GS_PAT4 18
+#endif
+#ifndef GS_PAT2
+#define GS_PAT2 8
+#endif
+__host__ __device__ inline int own_period(int g) { return g == 4 ? GS_PAT4 : (g == 2 ? GS_PAT2 : 1); }
+__host__ __device__ inline int own_weight(int g, int o) {
+    return g == 4 ? (o == 0 ? GS_PAT4 - 15 : 5) : (g == 2 ? (o == 0 ? GS_PAT2 - 5 : 5) : 1);
+}
 __host__ __device__ inline int own_of(int g, int J) {
+#if GS_PAT4 == 17
+    if (g == 4) return (int)((0x39e7939e4ull >> (2 * (J % 17))) & 3ull);   // 0123 1230 1231 2312 3
+#elif GS_PAT4 == 19
+    if (g == 4) return (int)((0x39e4e4e4e4ull >> (2 * (J % 19))) & 3ull);  // 0123 0123 0123 0123 123
+#else
     if (g == 4) return (int)((0xE4E7939E4ull >> (2 * (J % 18))) & 3ull);   // 0,1,2,3,1,2,3,0,1,2,3,1,2,3,0,1,2,3
+#endif
+#if GS_PAT2 == 7
+    if (g == 2) return (0x6Eu >> (J % 7)) & 1u;                                // 0,1,1,1,0,1,1
+#elif GS_PAT2 == 9
+    if (g == 2) return (0x1AAu >> (J % 9)) & 1u;                               // 0,1,0,1,0,1,0,1,1
+#else
     if (g == 2) return (0xB6u >> (J % 8)) & 1u;                                // 0,1,1,0,1,1,0,1
+#endif
     return 0;
 }
 // positions of owner o inside one period (bit r set: J = r mod period is owned by o)
 __host__ __device__ inline uint32_t own_mask(int g, int o) {
+#if GS_PAT4 == 17
+    if (g == 4) return o == 0 ? 0x81u : (o == 1 ? 0x4912u : (o == 2 ? 0x9224u : 0x12448u));
+#elif GS_PAT4 == 19
+    if (g == 4) return o == 0 ? 0x1111u : (o == 1 ? 0x12222u : (o == 2 ? 0x24444u : 0x48888u));
+#else
     if (g == 4) return o == 0 ? 0x4081u : (o == 1 ? 0x8912u : (o == 2 ? 0x11224u : 0x22448u));
+#endif
+#if GS_PAT2 == 7
+    if (g == 2) return o == 0 ? 0x11u : 0x6Eu;
+#elif GS_PAT2 == 9
+    if (g == 2) return o == 0 ? 0x55u : 0x1AAu;
+#else
     if (g == 2) return o == 0 ? 0x49u : 0xB6u;
+#endif
     return 1u;
 }
 __host__ __device__ inline int popc32(uint32_t v) {
@@ -154,7 +188,7 @@ __host__ __device__ inline int sym_targets(int T, int g, int a, int b, int t[3])
 // multiplies); sym_targets_g dispatches on g.  For per-element hot paths (the PSF epilogue).
 template <int G>
 __host__ __device__ inline int sym_cnt_t(int x, int o) {
-    constexpr int P = G == 4 ? 18 : (G == 2 ? 8 : 1);
+    constexpr int P = G == 4 ? GS_PAT4 : (G == 2 ? GS_PAT2 : 1);
     if (x < 0) return 0;
     const int full = (x + 1) / P, rem = (x + 1) - full * P;
     return full * own_weight(G, o) + popc32(own_mask(G, o) & ((1u << rem) - 1u));
