@@ -21,8 +21,10 @@
 //   w_l -= (A_lt / A_ll) delta_t for all lanes;   x_t += delta_t.
 //
 // B200 mapping
-//  * A CTA = warp 0 solver, warp 1 bulk-copy producer, warp 4 staging producer (leader), warps
-//    2,3,5,6,7 consumers (in the leader 6 = D product, 7 = L/LL products).  The producer streams
+//  * A CTA = warp 0 solver, warp 1 bulk-copy producer (in the leader also of the solver's staged
+//    blocks), warp 4 partial-sum helper (leader: sums the g*kCons partial vectors of each step
+//    so the solver reads P as one float4 per lane), warps 2,3,5,6,7 consumers (in the leader
+//    6 = D product, 7 = L/LL products).  The producer streams
 //    this CTA's runs of each step with cp.async.bulk (<= 6 tiles per copy, mbarrier complete_tx)
 //    into a shared-memory ring (2 slots of 24 KB; non-leader CTAs also use the staging area: 3), running
 //    ahead across steps (tiles do not depend on x); an L2 prefetch of the runs n steps ahead is
@@ -103,6 +105,8 @@ struct __align__(128) GsSmem {
     unsigned long long stg_full[kStg], stg_empty[kStg];
     unsigned long long pready[2];      // leader: 1 arrival + g*kCons*128 tx bytes per step
     unsigned long long xr[2];          // leader: solver arrival; others: 1 arrival + 128 tx
+    float psum[2][32];                 // leader: P of the step, summed by the helper warp
+    unsigned long long psum_full[2];   // leader: helper arrival
     int item;
     unsigned long long issue_t[kNringMax];   // profiling: clock64 at which each slot's copy was issued
 };
@@ -338,6 +342,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
             for (int b = 0; b < 2; b++) {
                 mbar_init(&sh.pready[b], 1);
                 mbar_init(&sh.xr[b], 1);
+                mbar_init(&sh.psum_full[b], 1);
             }
             fence_mbar_init();
         }
@@ -359,6 +364,18 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                             if (sp[sg].len > 0)
                                 bulk_prefetch_l2(Ab + (size_t)sp[sg].t0 * kTile, (uint32_t)sp[sg].len * kTile * 4);
                     }
+                    if (is_leader) {
+                        // the solver's staged block of step s: L = (kn,kx), D = (kn,kn), LL_{kn+2}, packet
+                        const int sl = s % kStg;
+                        const int kn2 = (kn + 2 >= T) ? kn + 2 - T : kn + 2;   // (mod T again for T < 2)
+                        mbar_wait_cta(&sh.stg_empty[sl], ((s / kStg) & 1) ^ 1);
+                        mbar_expect_tx(&sh.stg_full[sl], 3 * kTile * 4 + kPacketBytes);
+                        bulk_g2s(sh.rs[kRing * kChunk + 3 * (sl) + 0], Ab + (size_t)(T + kn) * kTile, kTile * 4, &sh.stg_full[sl]);   // L_kn
+                        bulk_g2s(sh.rs[kRing * kChunk + 3 * (sl) + 1], Ab + (size_t)kn * kTile, kTile * 4, &sh.stg_full[sl]);         // D_kn
+                        bulk_g2s(sh.rs[kRing * kChunk + 3 * (sl) + 2], Ab + (size_t)(2 * T + kn2 % T) * kTile, kTile * 4,
+                                 &sh.stg_full[sl]);                                                      // LL_{kn+2}
+                        bulk_g2s(&sh.pk[sl], pkb + kn, kPacketBytes, &sh.stg_full[sl]);
+                    }
                     const Seg *sd = segt + 2 * kn;
                     for (int sg = 0; sg < 2; sg++)
                     for (int off = 0; off < sd[sg].len; off += kChunk) {
@@ -377,19 +394,20 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 if (ppf) { prof[12] = p_wait; prof[13] = p_issue; prof[14] = seq; }
             }
         } else if (wid == 4) {
-            // ================= staging producer (leader, one lane): L = (kn,kx), D = (kn,kn)
-            // (warp 4 shares the solver's SM sub-partition; it is mostly asleep in try_wait)
-            if (is_leader && lane == 0) {
-                for (int s = 0, kn = 0, sl = 0; s < total;
-                     s++, kn = (kn + 1 == T) ? 0 : kn + 1, sl = (sl + 1 == kStg) ? 0 : sl + 1) {
-                    const int kn2 = (kn + 2 >= T) ? kn + 2 - T : kn + 2;   // (mod T again for T < 2)
-                    mbar_wait_cta(&sh.stg_empty[sl], ((s / kStg) & 1) ^ 1);
-                    mbar_expect_tx(&sh.stg_full[sl], 3 * kTile * 4 + kPacketBytes);
-                    bulk_g2s(sh.rs[kRing * kChunk + 3 * (sl) + 0], Ab + (size_t)(T + kn) * kTile, kTile * 4, &sh.stg_full[sl]);   // L_kn
-                    bulk_g2s(sh.rs[kRing * kChunk + 3 * (sl) + 1], Ab + (size_t)kn * kTile, kTile * 4, &sh.stg_full[sl]);         // D_kn
-                    bulk_g2s(sh.rs[kRing * kChunk + 3 * (sl) + 2], Ab + (size_t)(2 * T + kn2 % T) * kTile, kTile * 4,
-                             &sh.stg_full[sl]);                                                      // LL_{kn+2}
-                    bulk_g2s(&sh.pk[sl], pkb + kn, kPacketBytes, &sh.stg_full[sl]);
+            // ================= partial-sum helper (leader): P of step j = the g*kCons partial
+            // vectors, lane r summing row r, so the solver finds it summed (one float4 per lane)
+            // -- off the solver's path whenever the stream is ahead of it
+            if (is_leader) {
+                const int np = g * kCons;
+                for (int j = 0; j < total; j++) {
+                    const int b = j & 1;
+                    mbar_wait(&sh.pready[b], (j >> 1) & 1);
+                    const float *prb = &sh.pr[b][0][0][lane];
+                    float v = 0.f;
+                    for (int idx = 0; idx < np; idx++) v += prb[idx * 32];
+                    sh.psum[b][lane] = v;
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_local(&sh.psum_full[b]);
                 }
             }
         } else if (wid >= 2) {
@@ -624,29 +642,15 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 // role 2 the LL tile staged with this step
                 const float *tp = (role1 && has_next) ? sh.rs[kRing * kChunk + 3 * (sl1) + 0] : (role2 ? sh.rs[kRing * kChunk + 3 * (sl) + 2] : Dt);
                 // ---- critical path: P_k -> residual -> publish x_{k-1} -> recurrence
-                mbar_wait(&sh.pready[b], (j >> 1) & 1);
+                mbar_wait_cta(&sh.psum_full[b], (j >> 1) & 1);
                 if (pf) { const unsigned long long t = clock64(); w_p += t - tA; tA = t; }
                 float ac[4];
                 {
-                    // the g*kCons partials, a quarter per lane group, then summed across groups
-                    float a[4] = {0.f, 0.f, 0.f, 0.f};
-                    const float *prb = &sh.pr[b][0][0][0];
-                    const int np = g * kCons;
-                    float4 v[(kCl * kCons + 3) / 4];
-#pragma unroll
-                    for (int it = 0; it < (kCl * kCons + 3) / 4; it++) {   // all loads in flight at once
-                        const int idx = (lane >> 3) + 4 * it;
-                        v[it] = (idx < np) ? *reinterpret_cast<const float4 *>(prb + idx * 32 + L4)
-                                           : make_float4(0.f, 0.f, 0.f, 0.f);
-                    }
-#pragma unroll
-                    for (int it = 0; it < (kCl * kCons + 3) / 4; it++) {
-                        a[0] += v[it].x; a[1] += v[it].y; a[2] += v[it].z; a[3] += v[it].w;
-                    }
+                    // P_j, summed by the helper warp
+                    const float4 pv = *reinterpret_cast<const float4 *>(&sh.psum[b][L4]);
+                    float a[4] = {pv.x, pv.y, pv.z, pv.w};
 #pragma unroll
                     for (int i = 0; i < 4; i++) {
-                        a[i] += __shfl_xor_sync(0xffffffffu, a[i], 8);
-                        a[i] += __shfl_xor_sync(0xffffffffu, a[i], 16);
                         a[i] += lres[i];
                         if (use_ll) a[i] += (j & 1) ? ll1[i] : ll0[i];
                         const float r = (a[i] - bhi[i]) - blo[i];   // residual against b~ = bhi + blo
