@@ -615,26 +615,10 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
             };
             mbar_wait_cta(&sh.stg_full[0], 0);
             prepare(0);
-            // operands of the next block, loaded ahead of the recurrence (latency hidden)
-            float n_invd[4], n_xo[4], n_wg[6], n_bhi[4], n_blo[4];
-            auto fetch_next = [&](int jj, int kk) {
-                const GsPacket &P = sh.pk[jj % kStg];
-                const float4 iv = *reinterpret_cast<const float4 *>(&P.invd[L4]);
-                n_invd[0] = iv.x; n_invd[1] = iv.y; n_invd[2] = iv.z; n_invd[3] = iv.w;
-                const float4 w0 = *reinterpret_cast<const float4 *>(&P.wg[L4 >> 2][0]);
-                const float4 w1 = *reinterpret_cast<const float4 *>(&P.wg[L4 >> 2][4]);
-                n_wg[0] = w0.x; n_wg[1] = w0.y; n_wg[2] = w0.z; n_wg[3] = w0.w; n_wg[4] = w1.x; n_wg[5] = w1.y;
-                const float4 bh = *reinterpret_cast<const float4 *>(&P.bhi[L4]);
-                const float4 bl = *reinterpret_cast<const float4 *>(&P.blo[L4]);
-                n_bhi[0] = bh.x; n_bhi[1] = bh.y; n_bhi[2] = bh.z; n_bhi[3] = bh.w;
-                n_blo[0] = bl.x; n_blo[1] = bl.y; n_blo[2] = bl.z; n_blo[3] = bl.w;
-                const float4 v = *reinterpret_cast<const float4 *>(xs + 32 * kk + L4);
-                n_xo[0] = v.x; n_xo[1] = v.y; n_xo[2] = v.z; n_xo[3] = v.w;
-            };
             for (int j = 0, k = 0, sl = 0; j < total;
                  j++, k = (k + 1 == T) ? 0 : k + 1, sl = (sl + 1 == kStg) ? 0 : sl + 1) {
                 const int b = j & 1, row0 = 32 * k, sl1 = (sl + 1 == kStg) ? 0 : sl + 1;
-                const int kn1 = (k + 1 == T) ? 0 : k + 1;   // next block
+
                 const bool has_next = (j + 1 < total);
                 if (pf) tA = clock64();
                 const float *Dt = sh.rs[kRing * kChunk + 3 * (sl) + 1];
@@ -660,10 +644,6 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 // partials of P_j are consumed: x of step j-1 may now release the stream warps
                 if (prev_row0 >= 0) publish(j - 1, prev_row0);
                 if (pf) { const unsigned long long t = clock64(); c_pub += t - tA; tA = t; }
-                if (has_next) {
-                    mbar_wait_cta(&sh.stg_full[sl1], ((j + 1) / kStg) & 1);
-                    fetch_next(j + 1, kn1);
-                }
                 if (pf) { const unsigned long long t = clock64(); c_set += t - tA; tA = t; }
 #pragma unroll
                 for (int G = 0; G < 8; G++) {
@@ -717,15 +697,11 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 __syncwarp();
                 if (lane == 0) mbar_arrive_local(&sh.stg_empty[sl]);
                 if (pf) { const unsigned long long t = clock64(); c_post += t - tA; tA = t; }
+                // the next block's operands, after the recurrence: their load latency overlaps the
+                // wait for the next P (the solver's registers stay free during the recurrence)
                 if (has_next) {
-#pragma unroll
-                    for (int i = 0; i < 4; i++) {
-                        invd[i] = n_invd[i];
-                        bhi[i] = n_bhi[i];
-                        blo[i] = n_blo[i];
-                        xo[i] = (T == 1) ? xprev[i] : n_xo[i];
-                    }
-                    wg10 = n_wg[0]; wg20 = n_wg[1]; wg30 = n_wg[2]; wg21 = n_wg[3]; wg31 = n_wg[4]; wg32 = n_wg[5];
+                    mbar_wait_cta(&sh.stg_full[sl1], ((j + 1) / kStg) & 1);
+                    prepare(j + 1);
                 }
                 if (pf) { const unsigned long long t = clock64(); c_bc += t - tA; tA = t; }
             }
