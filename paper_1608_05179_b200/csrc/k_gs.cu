@@ -22,9 +22,10 @@
 //
 // B200 mapping
 //  * A CTA = warp 0 solver, warp 1 bulk-copy producer (in the leader also of the solver's staged
-//    blocks), warp 4 partial-sum helper (leader: sums the g*kCons partial vectors of each step
-//    so the solver reads P as one float4 per lane), warps 2,3,5,6,7 consumers (in the leader
-//    6 = D product, 7 = L/LL products).  The producer streams
+//    blocks), warp 4 helper (leader: sums the g*kCons partial vectors of each step so the
+//    solver reads P as one float4 per lane, and forwards each new x block to the other CTAs
+//    as soon as the solver publishes it), warps 2,3,5,6,7 consumers (in the leader 6 = D
+//    product, 7 = L/LL products).  The producer streams
 //    this CTA's runs of each step with cp.async.bulk (<= 6 tiles per copy, mbarrier complete_tx)
 //    into a shared-memory ring (2 slots of 24 KB; non-leader CTAs also use the staging area: 3), running
 //    ahead across steps (tiles do not depend on x); an L2 prefetch of the runs n steps ahead is
@@ -397,8 +398,21 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
             // ================= partial-sum helper (leader): P of step j = the g*kCons partial
             // vectors, lane r summing row r, so the solver finds it summed (one float4 per lane)
             // -- off the solver's path whenever the stream is ahead of it
+            // It also forwards each new x block to the sub-group's other CTAs (st.async completes
+            // 128 bytes on their x-ready barrier) as soon as the solver publishes it: the solver
+            // publishes x of step j-1 once it has consumed P_j, so the others have finished step j
+            // and observed x of step j-3, the previous phase of the slot this store completes.
             if (is_leader) {
                 const int np = g * kCons;
+                auto push_x = [&](int jj) {
+                    mbar_wait_cta(&sh.xr[jj & 1], (jj >> 1) & 1);
+                    if (lane < 8) {
+                        const int r0 = 32 * (jj % T) + 4 * lane;
+                        const float4 xv = *reinterpret_cast<const float4 *>(xs + r0);
+                        const uint32_t xa = smem_u32(xs + r0), xra = smem_u32(&sh.xr[jj & 1]);
+                        for (int q = 1; q < g; q++) st_async_v4(mapa(xa, leader + q), xv, mapa(xra, leader + q));
+                    }
+                };
                 for (int j = 0; j < total; j++) {
                     const int b = j & 1;
                     mbar_wait(&sh.pready[b], (j >> 1) & 1);
@@ -408,7 +422,9 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                     sh.psum[b][lane] = v;
                     __syncwarp();
                     if (lane == 0) mbar_arrive_local(&sh.psum_full[b]);
+                    if (g > 1 && j >= 1) push_x(j - 1);
                 }
+                if (g > 1 && total > 0) push_x(total - 1);
             }
         } else if (wid >= 2) {
             // ================= consumers: P_s = sum over J != kn of A[I_kn, I_J] x_J (old x for the
@@ -423,16 +439,6 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
             const bool do_L = is_leader && c == kCons - 1, do_D = is_leader && c == kCons - 2;
             uint32_t slot = 0, ph = 0;
             float lcarry[4] = {0.f, 0.f, 0.f, 0.f};   // L warp: LL_{kn+1} x_kx^old for the next step
-            // leader, D warp: forward x of solver step jj to the sub-group's other CTAs (st.async
-            // completes 128 bytes on their x-ready barrier)
-            auto push_x = [&](int jj) {
-                if (g > 1 && lane < 8) {
-                    const int r0 = 32 * (jj % T) + 4 * lane;
-                    const float4 xv = *reinterpret_cast<const float4 *>(xs + r0);
-                    const uint32_t xa = smem_u32(xs + r0), xra = smem_u32(&sh.xr[jj & 1]);
-                    for (int q = 1; q < g; q++) st_async_v4(mapa(xa, leader + q), xv, mapa(xra, leader + q));
-                }
-            };
             // profile item 0 (the largest bin): consumer 0 of the leader and of cluster rank 1
             const bool pf = prof && item == 0 && c == 0 && lane == 0 && crank <= 1;
             unsigned long long *pc = prof + (crank == 0 ? 5 : 16);
@@ -536,21 +542,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 if (cq == 0)
                     st_async_v4(mapa(smem_u32(&sh.pr[s & 1][rg][c][4 * rq]), leader),
                                 make_float4(acc[0], acc[1], acc[2], acc[3]), mapa(smem_u32(&sh.pready[s & 1]), leader));
-                if (do_D && s >= 2) {
-                    // forward x of solver step s-2 to the sub-group's other CTAs (they need it from
-                    // their step s+1 on); after this step's partial so P_s never waits for it
-                    if (T > 2) mbar_wait_cta(&sh.xr[s & 1], ((s - 2) >> 1) & 1);
-                    push_x(s - 2);
-                }
                 if (pf) { const unsigned long long t = clock64(); c_red += t - tA; tA = t; }
-            }
-            if (do_D) {
-                // the solver's last two blocks (steps total-2, total-1)
-                for (int s = total; s < total + 2; s++) {
-                    if (s < 2) continue;
-                    mbar_wait(&sh.xr[s & 1], ((s - 2) >> 1) & 1);
-                    push_x(s - 2);
-                }
             }
             if (!is_leader && c == 0 && total > 0) {
                 // observe every remaining x-ready phase (steps total-3 .. total-1; the last two are
