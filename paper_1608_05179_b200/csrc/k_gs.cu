@@ -636,6 +636,9 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 // partials of P_j are consumed: x of step j-1 may now release the stream warps
                 if (prev_row0 >= 0) publish(j - 1, prev_row0);
                 if (pf) { const unsigned long long t = clock64(); c_pub += t - tA; tA = t; }
+                // the next block's staged slot must have landed before the recurrence: role-1 lanes
+                // read its L tile during it (its operands are loaded after the recurrence)
+                if (has_next) mbar_wait_cta(&sh.stg_full[sl1], ((j + 1) / kStg) & 1);
                 if (pf) { const unsigned long long t = clock64(); c_set += t - tA; tA = t; }
 #pragma unroll
                 for (int G = 0; G < 8; G++) {
@@ -691,10 +694,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                 if (pf) { const unsigned long long t = clock64(); c_post += t - tA; tA = t; }
                 // the next block's operands, after the recurrence: their load latency overlaps the
                 // wait for the next P (the solver's registers stay free during the recurrence)
-                if (has_next) {
-                    mbar_wait_cta(&sh.stg_full[sl1], ((j + 1) / kStg) & 1);
-                    prepare(j + 1);
-                }
+                if (has_next) prepare(j + 1);
                 if (pf) { const unsigned long long t = clock64(); c_bc += t - tA; tA = t; }
             }
             publish(total - 1, prev_row0);

@@ -527,3 +527,24 @@ def test_absolute_threshold_mode_matches_relative(ctx, torch_cuda):
     assert np.array_equal(rel["n_keep"].cpu().numpy(), ab["n_keep"].cpu().numpy())
     assert np.array_equal(rel["keep_idx"].cpu().numpy(), ab["keep_idx"].cpu().numpy())
     assert np.array_equal(rel["x_map"].cpu().numpy(), ab["x_map"].cpu().numpy())
+
+
+@pytest.mark.gpu
+def test_batched_path_bitwise_deterministic_cfg3():
+    """The whole 256-bin cfg3 band, three calls: every map bit-identical (all summation orders are
+    fixed, so any difference is a race -- this test caught one in the GS solver's staging)."""
+    import torch
+    from paper_1608_05179_b200 import Context
+    cfg = synth.CONFIGS["cfg3"]
+    band = synth.make_band(cfg)
+    g = geom_of(band)
+    ctx = Context(0)
+    csm = torch.from_numpy(band.csm).cuda()
+    ref = None
+    for _ in range(3):
+        x = ctx.solve_band(g, band.freqs, csm, cfg.epsilon, 300, cfg.eps_mode)["x_map"].cpu().numpy()
+        if ref is None:
+            ref = x
+        else:
+            assert np.array_equal(x, ref)
+    ctx.close()
