@@ -246,10 +246,11 @@ __device__ __forceinline__ void tile_dot(const float *__restrict__ tile, const f
         const int c = cq + 4 * i;
         const float4 v = *reinterpret_cast<const float4 *>(tile + c * 32 + 4 * rq);
         const float xv = xcol[c];
-        acc[0] = fmaf(v.x, xv, acc[0]);
-        acc[1] = fmaf(v.y, xv, acc[1]);
-        acc[2] = fmaf(v.z, xv, acc[2]);
-        acc[3] = fmaf(v.w, xv, acc[3]);
+        // packed fp32x2 FMA (FFMA2): the same two correctly rounded FMAs in one instruction
+        const float2 xx = make_float2(xv, xv);
+        const float2 a01 = __ffma2_rn(make_float2(v.x, v.y), xx, make_float2(acc[0], acc[1]));
+        const float2 a23 = __ffma2_rn(make_float2(v.z, v.w), xx, make_float2(acc[2], acc[3]));
+        acc[0] = a01.x; acc[1] = a01.y; acc[2] = a23.x; acc[3] = a23.y;
     }
 }
 
