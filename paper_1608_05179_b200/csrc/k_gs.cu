@@ -258,18 +258,16 @@ __device__ __forceinline__ void tile_dot(const float *__restrict__ tile, const f
 // column o of the column-major tile, read as 8 float4 in the lane-rotated order (k + o) mod 8 so
 // every quarter-warp touches 8 distinct 16-byte bank groups (x likewise).  No cross-lane reduction.
 __device__ __forceinline__ float tile_tdot(const float *__restrict__ tile, const float *__restrict__ x, int lane) {
-    float t = 0.f;
+    float2 t2 = make_float2(0.f, 0.f);   // two interleaved partial sums, packed FMAs
 #pragma unroll
     for (int k = 0; k < 8; k++) {
         const int r0 = 4 * ((k + lane) & 7);
         const float4 v = *reinterpret_cast<const float4 *>(tile + lane * 32 + r0);
         const float4 xv = *reinterpret_cast<const float4 *>(x + r0);
-        t = fmaf(v.x, xv.x, t);
-        t = fmaf(v.y, xv.y, t);
-        t = fmaf(v.z, xv.z, t);
-        t = fmaf(v.w, xv.w, t);
+        t2 = __ffma2_rn(make_float2(v.x, v.y), make_float2(xv.x, xv.y), t2);
+        t2 = __ffma2_rn(make_float2(v.z, v.w), make_float2(xv.z, xv.w), t2);
     }
-    return t;
+    return t2.x + t2.y;
 }
 
 // Stream step s computes P for block kn = s mod T excluding kx = (s-1) mod T.  Stream tiles
