@@ -126,7 +126,9 @@ DWC_API dwc_status dwc_solve_band(dwc_ctx *ctx, const dwc_array *arr, const dwc_
 /* Same computation with HOST buffers (csm, n_keep, keep_idx, x_map, b_map all host; b_map
  * nullable).  The host<->device copies are part of the call, which returns when the
  * outputs are in host memory.  Page-locked (pinned) host buffers make the copies
- * asynchronous DMA; pageable buffers work but are staged by the CUDA runtime. */
+ * asynchronous DMA; pageable buffers work but are staged by the CUDA runtime.  With a pinned
+ * keep_idx the keep set is read back on an internal copy stream as soon as it is final (after
+ * S4), overlapping the PSF and the sweeps. */
 DWC_API dwc_status dwc_solve_band_host(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid,
                                const dwc_params *p, int32_t n_bins, const double *freq_hz,
                                const double *csm, int32_t *n_keep, int32_t *keep_idx,

@@ -61,6 +61,8 @@ struct dwc_ctx {
     PinBuf stage, readback;
     size_t stage_off = 0;
     cudaEvent_t stage_done = nullptr;
+    cudaStream_t copy_st = nullptr;         // host API: early keep-set readback (overlaps S5-S7)
+    cudaEvent_t keep_ready = nullptr, copy_done = nullptr;
     int geo_m = -1, geo_n = -1;
     bool timing = false;
     cudaEvent_t ev[8] = {};
@@ -268,7 +270,8 @@ void ev(dwc_ctx *ctx, int i, cudaStream_t st) {
 dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, const dwc_params *p,
                           int n_bins, const double *freq, const double *csm, int32_t *n_keep,
                           int32_t *keep_idx, float *x_map, double *b_map, uint32_t *warn,
-                          cudaStream_t st, const double *snap = nullptr, int n_snap = 0) {
+                          cudaStream_t st, const double *snap = nullptr, int n_snap = 0,
+                          int32_t *early_nk_host = nullptr, int32_t *early_keep_host = nullptr) {
     dwc_status s;
     int launches = 0;
     const int M = arr->m, n = grid->n;
@@ -304,6 +307,21 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
     const int flags = hk[n_bins];
     if (flags & kFlagSingular) return fail(DWC_ESINGULAR, "a scan-grid node coincides with a microphone");
     if (flags & kFlagNonFinite) return fail(DWC_ENUMERIC, "non-finite value in the CSM / DAS map");
+    if (early_keep_host) {
+        // the keep set is final: read it back on the copy stream while S5-S7 run
+        if (!ctx->copy_st) {
+            CU(cudaStreamCreateWithFlags(&ctx->copy_st, cudaStreamNonBlocking));
+            CU(cudaEventCreateWithFlags(&ctx->keep_ready, cudaEventDisableTiming));
+            CU(cudaEventCreateWithFlags(&ctx->copy_done, cudaEventDisableTiming));
+        }
+        CU(cudaEventRecord(ctx->keep_ready, st));
+        CU(cudaStreamWaitEvent(ctx->copy_st, ctx->keep_ready, 0));
+        memcpy(early_nk_host, hk, sizeof(int32_t) * n_bins);
+        CU(cudaMemcpyAsync(early_keep_host, keep_idx, sizeof(int32_t) * (size_t)n_bins * S, cudaMemcpyDeviceToHost,
+                           ctx->copy_st));
+        CU(cudaEventRecord(ctx->copy_done, ctx->copy_st));
+        CU(cudaStreamWaitEvent(st, ctx->copy_done, 0));   // the call's stream covers the copy too
+    }
     // host layout of the compressed systems
     std::vector<BinLayout> lay(n_bins);
     int64_t a_off = 0, v_off = 0, r_off = 0;
@@ -448,6 +466,9 @@ dwc_status dwc_destroy(dwc_ctx *ctx) {
     if (ctx->stage.p) cudaFreeHost(ctx->stage.p);
     if (ctx->readback.p) cudaFreeHost(ctx->readback.p);
     if (ctx->stage_done) cudaEventDestroy(ctx->stage_done);
+    if (ctx->copy_st) cudaStreamDestroy(ctx->copy_st);
+    if (ctx->keep_ready) cudaEventDestroy(ctx->keep_ready);
+    if (ctx->copy_done) cudaEventDestroy(ctx->copy_done);
     for (auto &e : ctx->ev)
         if (e) cudaEventDestroy(e);
     delete ctx;
@@ -532,12 +553,20 @@ dwc_status dwc_solve_band_host(dwc_ctx *ctx, const dwc_array *arr, const dwc_gri
         return s;
     if (b_map && (s = ensure(ctx, ctx->bmap_h, sizeof(double) * S * n_bins))) return s;
     CU(cudaMemcpyAsync(ctx->csm_h.p, csm, csm_b, cudaMemcpyHostToDevice, st));
+    // a pinned keep_idx buffer is filled while the PSF and Gauss-Seidel run (the keep set is final
+    // after S4); pageable buffers are copied at the end (an early async copy would block the host)
+    cudaPointerAttributes pa{};
+    const bool pinned = cudaPointerGetAttributes(&pa, keep_idx) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();
     s = solve_band_dev(ctx, arr, grid, p, n_bins, freq_hz, (double *)ctx->csm_h.p, (int32_t *)ctx->nk_h.p,
                        (int32_t *)ctx->keep_h.p, (float *)ctx->xmap_h.p,
-                       b_map ? (double *)ctx->bmap_h.p : nullptr, warn, st);
+                       b_map ? (double *)ctx->bmap_h.p : nullptr, warn, st, nullptr, 0,
+                       pinned ? n_keep : nullptr, pinned ? keep_idx : nullptr);
     if (s) return s;
-    CU(cudaMemcpyAsync(n_keep, ctx->nk_h.p, sizeof(int32_t) * n_bins, cudaMemcpyDeviceToHost, st));
-    CU(cudaMemcpyAsync(keep_idx, ctx->keep_h.p, sizeof(int32_t) * S * n_bins, cudaMemcpyDeviceToHost, st));
+    if (!pinned) {
+        CU(cudaMemcpyAsync(n_keep, ctx->nk_h.p, sizeof(int32_t) * n_bins, cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(keep_idx, ctx->keep_h.p, sizeof(int32_t) * S * n_bins, cudaMemcpyDeviceToHost, st));
+    }
     CU(cudaMemcpyAsync(x_map, ctx->xmap_h.p, sizeof(float) * S * n_bins, cudaMemcpyDeviceToHost, st));
     if (b_map) CU(cudaMemcpyAsync(b_map, ctx->bmap_h.p, sizeof(double) * S * n_bins, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));

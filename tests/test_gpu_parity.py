@@ -303,10 +303,19 @@ def test_host_api_equals_device_api_and_deterministic(ctx, torch_cuda):
     d1 = ctx.solve_band(g, band.freqs, torch.from_numpy(band.csm).cuda(), cfg.epsilon, 200, want_b=True)
     d2 = ctx.solve_band(g, band.freqs, torch.from_numpy(band.csm).cuda(), cfg.epsilon, 200, want_b=True)
     h = ctx.solve_band_host(g, band.freqs, torch.from_numpy(band.csm).pin_memory(), cfg.epsilon, 200, want_b=True)
+    # pinned outputs take the early keep-set readback (on a copy stream, overlapping S5-S7)
+    K, S = len(band.freqs), g.S
+    pin = {"n_keep": torch.full((K,), -7, dtype=torch.int32).pin_memory(),
+           "keep_idx": torch.full((K, S), -7, dtype=torch.int32).pin_memory(),
+           "x_map": torch.empty((K, S), dtype=torch.float32).pin_memory(),
+           "b_map": torch.empty((K, S), dtype=torch.float64).pin_memory()}
+    hp = ctx.solve_band_host(g, band.freqs, torch.from_numpy(band.csm).pin_memory(), cfg.epsilon, 200,
+                             want_b=True, out=pin)
     for key in ["n_keep", "keep_idx", "x_map", "b_map"]:
         a = d1[key].cpu()
         assert torch.equal(a, d2[key].cpu())
         assert torch.equal(a, h[key])
+        assert torch.equal(a, hp[key])
 
 
 def test_shard_invariance(ctx, torch_cuda):
