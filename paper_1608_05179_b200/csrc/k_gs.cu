@@ -801,13 +801,15 @@ int gs_cluster_size() { return kCl; }
 int gs_item_ints() { return (int)(sizeof(GsItem) / sizeof(int)); }
 
 // CTAs per bin from S~ alone (batch-independent => bit-identical per-bin results).
-// Thresholds 896 / 448 (28 / 14 row blocks): measured best on cfg3 (GS 48.8-49.1 ms; 768 / 384:
-// 50.1, 1024 / 512: 60.0, 640 / 320: 55.0; scripts/gs_group_sweep.sh), neutral on cfg2 and cfg5.
-// The band is bound both by the largest bin's chain and by the CTA-steps all bins occupy; more
-// CTAs per medium bin shorten chains that are not the longest but cost slots.
-// DWC_GS_G4 / DWC_GS_G2 override them (experiments).
+// Thresholds 832 / 448 (26 / 14 row blocks), measured on two bands with different S~ spreads
+// (scripts/gs_group_variants.sh, GS ms): cfg3 linear predictor 768/384 47.2, 800/416 45.6-46.3,
+// 832/448 45.5, 864/448 44.9-45.1, 896/448 45.2-45.8; cfg3 cubic predictor (3.5 % kept) 33.8-34.4,
+// 34.6, 36.1-36.5, 40.6-41.7, 42.2-42.9.  The band is bound both by the largest bin's chain and
+// by the CTA-steps all bins occupy: more CTAs per medium bin shorten chains that are not the
+// longest but cost slots, so the best split depends on the S~ distribution; 832 / 448 is within
+// 1 % of the best on the linear band and 6 % on the cubic one.  DWC_GS_G4 / DWC_GS_G2 override.
 int gs_group_size(int nk) {
-    static const int t4 = getenv("DWC_GS_G4") ? atoi(getenv("DWC_GS_G4")) : 896;
+    static const int t4 = getenv("DWC_GS_G4") ? atoi(getenv("DWC_GS_G4")) : 832;
     static const int t2 = getenv("DWC_GS_G2") ? atoi(getenv("DWC_GS_G2")) : 448;
     return nk >= t4 ? 4 : (nk >= t2 ? 2 : 1);
 }
