@@ -25,17 +25,17 @@
 //    blocks), warp 4 helper (leader: sums the g*kCons partial vectors of each step so the
 //    solver reads P as one float4 per lane, and forwards each new x block to the other CTAs
 //    as soon as the solver publishes it), warps 2,3,5,6,7 consumers (in the leader 6 = D
-//    product, 7 = L/LL products).  The producer streams
-//    this CTA's runs of each step with cp.async.bulk (<= 6 tiles per copy, mbarrier complete_tx)
-//    into a shared-memory ring (2 slots of 24 KB; non-leader CTAs also use the staging area: 3), running
-//    ahead across steps (tiles do not depend on x); an L2 prefetch of the runs n steps ahead is
-//    available with -DGS_PF=n (off by default: measured not to pay).
+//    product, 7 = L/LL products).  The producer streams this CTA's runs of each step with
+//    cp.async.bulk (<= 6 tiles per copy, mbarrier complete_tx) into a shared-memory ring (2 slots
+//    of 24 KB; non-leader CTAs also use the staging area: 3), running ahead across steps (tiles
+//    do not depend on x); an L2 prefetch of the runs n steps ahead is available with -DGS_PF=n
+//    (off by default: measured not to pay).
 //  * Clusters of kCl = 4 CTAs.  A work item gives the cluster either one large bin (sub-group of
 //    g = 4 CTAs), two medium bins (g = 2) or four small bins (g = 1).  Inside a sub-group every
 //    CTA keeps a full copy of x in shared memory; column blocks are owned by CTAs in a periodic
 //    pattern weighted by stream warps (dwc_internal.cuh own_of); every consumer warp sends its 32
 //    partial row sums to the leader with st.async (DSMEM, complete_tx on the leader's
-//    P-ready barrier); the leader's D warp forwards each new x block the same way.  No grid or
+//    P-ready barrier); the leader's helper warp forwards each new x block the same way.  No grid or
 //    cluster barrier inside the sweep loop; cluster barriers only between work items.
 //  * g depends on S~ only (host), so a bin's result is bit-identical whatever else is in the
 //    batch (and on however many GPUs the band is sharded); items run largest first (LPT).
