@@ -198,10 +198,13 @@ def test_gs_identity_and_scalar(ctx, torch_cuda):
 
 
 @pytest.mark.parametrize("nk,sweeps", [(2, 7), (31, 50), (32, 50), (33, 50), (97, 200), (300, 1000),
-                                       (1000, 100)])
+                                       (447, 80), (448, 80), (640, 80), (831, 60), (832, 60), (1000, 100),
+                                       (1190, 60)])
 def test_gs_parity_on_oracle_system(ctx, torch_cuda, oracle_lib, nk, sweeps):
     """GS on the oracle's own A~ (rounded to fp32) and b~: ragged sizes around the 32-row
-    block and multi-block systems."""
+    block and multi-block systems, both sides of the CTAs-per-bin thresholds (g = 1 below 448
+    kept points, 2 from 448, 4 from 832) and a g = 4 system whose T = 38 blocks end inside the
+    18-block column-ownership period."""
     torch = torch_cuda
     band = synth.make_band("cfg3", bins=[150])
     g = geom_of(band)
