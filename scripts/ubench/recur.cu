@@ -187,6 +187,90 @@ __global__ void v8_kernel(const float *g_tile, float *out, int iters, long long 
     out[blockIdx.x * 32 + lane] = s;
 }
 
+
+// VR: the chain over the 32 rows is computed redundantly by every lane (no shuffle on it): the
+// group's packet (1/A_ii, within-group weights, old x) is read as smem broadcasts, the next
+// group's residual = partial (lane G+1's own rows, contributions of groups <= G-1, shuffled out
+// off the critical path) + the current group's contribution computed redundantly (16 FMAs).
+// Every lane applies each group's c's one group late (its rows / role rows).
+__global__ void vr_kernel(const float *g_tile, float *out, int iters, long long *cyc) {
+    __shared__ __align__(16) float tile[1024];
+    __shared__ __align__(16) float pinv[32], pwg[64], xs[32];
+    const int lane = threadIdx.x & 31;
+    for (int i = lane; i < 1024; i += 32) tile[i] = g_tile[i];
+    pinv[lane] = 1.f;
+    xs[lane] = 0.5f;
+    pwg[lane] = 0.01f * (lane % 7);
+    pwg[lane + 32] = 0.01f * (lane % 5);
+    __syncwarp();
+    const int L4 = 4 * (lane & 7);
+    float ac[4], xo[4];
+    for (int i = 0; i < 4; i++) { ac[i] = 0.1f * (L4 + i) - 1.f; xo[i] = 0.5f; }
+    long long t0 = clock64();
+    for (int it = 0; it < iters; it++) {
+        float r[4], cp[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int i = 0; i < 4; i++) r[i] = __shfl_sync(0xffffffffu, ac[i], 0);
+#pragma unroll
+        for (int G = 0; G < 8; G++) {
+            const float m = (lane == G) ? 1.f : 0.f;
+            const float4 iv = lds4(pinv + 4 * G), xg = lds4(xs + 4 * G);
+            const float4 wa = lds4(pwg + 8 * G), wb = lds4(pwg + 8 * G + 4);
+            auto apply = [&](const float4 &t, float d) {
+                const float2 dd = make_float2(d, d);
+                float2 a01 = __ffma2_rn(make_float2(t.x, t.y), dd, make_float2(ac[0], ac[1]));
+                float2 a23 = __ffma2_rn(make_float2(t.z, t.w), dd, make_float2(ac[2], ac[3]));
+                ac[0] = a01.x; ac[1] = a01.y; ac[2] = a23.x; ac[3] = a23.y;
+            };
+            if (G > 0) {
+#pragma unroll
+                for (int j = 0; j < 4; j++) apply(lds4(tile + (4 * (G - 1) + j) * 32 + L4), cp[j]);
+            }
+            float pn[4] = {0.f, 0.f, 0.f, 0.f};
+            if (G < 7) {
+#pragma unroll
+                for (int i = 0; i < 4; i++) pn[i] = __shfl_sync(0xffffffffu, ac[i], G + 1);
+            }
+            const float w0 = -r[0] * iv.x, w1 = -r[1] * iv.y, w2 = -r[2] * iv.z, w3 = -r[3] * iv.w;
+            const float c0 = fmaxf(w0, -xg.x);
+            float u1 = fmaf(-wa.x, c0, w1), u2 = fmaf(-wa.y, c0, w2), u3 = fmaf(-wa.z, c0, w3);
+            const float c1 = fmaxf(u1, -xg.y);
+            u2 = fmaf(-wa.w, c1, u2); u3 = fmaf(-wb.x, c1, u3);
+            const float c2 = fmaxf(u2, -xg.z);
+            u3 = fmaf(-wb.y, c2, u3);
+            const float c3 = fmaxf(u3, -xg.w);
+            xo[0] = fmaf(m, c0, xo[0]); xo[1] = fmaf(m, c1, xo[1]);
+            xo[2] = fmaf(m, c2, xo[2]); xo[3] = fmaf(m, c3, xo[3]);
+            if (G < 7) {
+                const float4 d0 = lds4(tile + (4 * G + 0) * 32 + 4 * (G + 1));
+                const float4 d1 = lds4(tile + (4 * G + 1) * 32 + 4 * (G + 1));
+                const float4 d2 = lds4(tile + (4 * G + 2) * 32 + 4 * (G + 1));
+                const float4 d3 = lds4(tile + (4 * G + 3) * 32 + 4 * (G + 1));
+                float2 e01 = __fmul2_rn(make_float2(d0.x, d0.y), make_float2(c0, c0));
+                float2 e23 = __fmul2_rn(make_float2(d0.z, d0.w), make_float2(c0, c0));
+                e01 = __ffma2_rn(make_float2(d1.x, d1.y), make_float2(c1, c1), e01);
+                e23 = __ffma2_rn(make_float2(d1.z, d1.w), make_float2(c1, c1), e23);
+                e01 = __ffma2_rn(make_float2(d2.x, d2.y), make_float2(c2, c2), e01);
+                e23 = __ffma2_rn(make_float2(d2.z, d2.w), make_float2(c2, c2), e23);
+                e01 = __ffma2_rn(make_float2(d3.x, d3.y), make_float2(c3, c3), e01);
+                e23 = __ffma2_rn(make_float2(d3.z, d3.w), make_float2(c3, c3), e23);
+                r[0] = pn[0] + e01.x; r[1] = pn[1] + e01.y; r[2] = pn[2] + e23.x; r[3] = pn[3] + e23.y;
+            }
+            cp[0] = c0; cp[1] = c1; cp[2] = c2; cp[3] = c3;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const float4 t = lds4(tile + (28 + j) * 32 + L4);
+            ac[0] = fmaf(t.x, cp[j], ac[0]); ac[1] = fmaf(t.y, cp[j], ac[1]);
+            ac[2] = fmaf(t.z, cp[j], ac[2]); ac[3] = fmaf(t.w, cp[j], ac[3]);
+        }
+        for (int i = 0; i < 4; i++) ac[i] = ac[i] * 0.5f - 0.3f;   // next block's residual (stand-in)
+    }
+    long long t1 = clock64();
+    if (lane == 0 && threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+    out[blockIdx.x * 32 + lane] = xo[0] + xo[1] + xo[2] + xo[3] + ac[0];
+}
+
 // busy warps that keep the solver's SM sub-partition issuing (like the co-resident warps)
 __global__ void dummy() {}
 
@@ -211,6 +295,9 @@ int main() {
         v4ps_kernel<<<1, 32>>>(tile, out, iters, cyc);
         cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
         printf("V4 FFMA2 + prescaled (no FMUL): %.1f cycles per 32-row block\n", (double)c / iters);
+        vr_kernel<<<1, 32>>>(tile, out, iters, cyc);
+        cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+        printf("VR (redundant chain, partials shuffled one group ahead): %.1f cycles per 32-row block\n", (double)c / iters);
         v8_kernel<<<1, 32>>>(tile, out, iters, cyc);
         cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
         printf("V8 (8 rows/lane, 4 groups): %.1f cycles per 32-row block\n", (double)c / iters);
