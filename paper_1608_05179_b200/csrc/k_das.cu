@@ -84,14 +84,14 @@ int launch_steer(const Geo &g, const double *dist, const double *amp, const doub
 // 1 point per lane); their steering vectors Es[n][p] (Mp x P complex,
 // Mp = M rounded up to 8, zero rows beyond M) in shared memory.  Warp w owns the row-group
 // pairs (q, G-1-q), q = w, w+NW, ... (G = Mp/4 groups of 4 rows), paired so every warp has the
-// same triangular work, and stages those 8 rows of Ch in its own shared-memory slice.  Lane l
-// owns points l (+32).  Per n a thread reads 8 row entries (broadcast LDS.128) and e_n of its
+// same triangular work, and reads those 8 rows of Ch through L1 (DAS_DIRECT_C).  Lane l
+// owns points l (+32).  Per n a thread reads 8 row entries (broadcast loads) and e_n of its
 // points and does 8 or 16 complex MACs; W = Ch e stays in registers; the epilogue reduces
 // Re(conj(e_m) W_m) over the rows and the warps in fixed order (deterministic).  fp64 CUDA
 // cores (B200 DFMA and DMMA peak are the same, ~36 TFLOP/s measured).
 constexpr int kDasThreads = 256;
 #ifndef DAS_UNROLL
-#define DAS_UNROLL 4
+#define DAS_UNROLL 8
 #endif
 constexpr int kDasUnroll = DAS_UNROLL;
 constexpr int kDasWarps = kDasThreads / 32;
@@ -106,7 +106,8 @@ __device__ __forceinline__ void cmac(double2 &acc, double2 a, double2 b) {  // a
 int das_mpad(int M) { return (M + 7) / 8 * 8; }
 
 template <int PPL, bool kBoth>
-__device__ __forceinline__ void das_rows(const double2 *__restrict__ Cw, const double2 *__restrict__ Es, int Mp,
+__device__ __forceinline__ void das_rows(const double2 *__restrict__ ca, const double2 *__restrict__ cb,
+                                         const double2 *__restrict__ Es, int Mp,
                                          int n0, int n1, int lane, double2 Wa[4][PPL], double2 Wb[4][PPL]) {
     constexpr int P = 32 * PPL;
 #pragma unroll kDasUnroll
@@ -116,14 +117,14 @@ __device__ __forceinline__ void das_rows(const double2 *__restrict__ Cw, const d
         for (int j = 0; j < PPL; j++) e[j] = Es[n * P + lane + 32 * j];
 #pragma unroll
         for (int r = 0; r < 4; r++) {
-            const double2 c = Cw[r * Mp + n];
+            const double2 c = ca[r * Mp + n];
 #pragma unroll
             for (int j = 0; j < PPL; j++) cmac(Wa[r][j], c, e[j]);
         }
         if (kBoth) {
 #pragma unroll
             for (int r = 0; r < 4; r++) {
-                const double2 c = Cw[(4 + r) * Mp + n];
+                const double2 c = cb[r * Mp + n];
 #pragma unroll
                 for (int j = 0; j < PPL; j++) cmac(Wb[r][j], c, e[j]);
             }
@@ -131,11 +132,21 @@ __device__ __forceinline__ void das_rows(const double2 *__restrict__ Cw, const d
     }
 }
 
+// DAS_DIRECT_C (default): the 8 Ch rows a warp works on are read as warp-broadcast read-only
+// global loads (L1-resident) instead of being staged in a per-warp shared-memory slice: 64 KB
+// of shared memory per CTA instead of 96 -> three CTAs per SM (register-limited at 168), cfg3
+// DAS stage 3.18 -> 2.94 ms with DAS_UNROLL 8 (4: 2.98, 2: 3.10).  Only for the 2-points-per-
+// lane form (M <= 64): with one point per lane (M = 128) the broadcast loads per DFMA double and
+// the direct form was slower (cfg5 DAS 196 -> 215 ms), so that form keeps the staging.
+#ifndef DAS_DIRECT_C
+#define DAS_DIRECT_C 1
+#endif
 template <int PPL, int NW>
-__global__ void __launch_bounds__(32 * NW, 2)
+__global__ void __launch_bounds__(32 * NW, (DAS_DIRECT_C && PPL == 2) ? 3 : 2)
 das_kernel(Geo g, const double *__restrict__ dist, const double *__restrict__ amp,
            const double *__restrict__ freq, const double2 *__restrict__ Ch, int Mp, double *__restrict__ b, int dr) {
     constexpr int P = 32 * PPL;
+    constexpr bool kDirect = DAS_DIRECT_C && PPL == 2;
     extern __shared__ double2 smem_d2[];
     double2 *Es = smem_d2;                       // [Mp][P]
     double2 *Cw = smem_d2 + (size_t)Mp * P;      // [warp][8 rows][Mp]
@@ -173,23 +184,27 @@ das_kernel(Geo g, const double *__restrict__ dist, const double *__restrict__ am
     for (int j = 0; j < PPL; j++) acc[j] = 0.0;
     for (int qa = w; qa < G / 2; qa += NW) {
         const int qb = G - 1 - qa;
-        __syncwarp();
-        for (int t = lane; t < 8 * Mp; t += 32) {   // rows 4qa..4qa+3, 4qb..4qb+3 of Ch (cp.async:
-            const int r = t / Mp, n = t - (t / Mp) * Mp;   // all 16-byte copies in flight at once)
-            const int m = (r < 4) ? 4 * qa + r : 4 * qb + r - 4;
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(cw + t)),
-                         "l"(C + (size_t)m * Mp + n)
-                         : "memory");
+        const double2 *ca = kDirect ? C + (size_t)(4 * qa) * Mp : cw;
+        const double2 *cb = kDirect ? C + (size_t)(4 * qb) * Mp : cw + 4 * Mp;
+        if constexpr (!kDirect) {
+            __syncwarp();
+            for (int t = lane; t < 8 * Mp; t += 32) {   // rows 4qa..4qa+3, 4qb..4qb+3 of Ch (cp.async:
+                const int r = t / Mp, n = t - (t / Mp) * Mp;   // all 16-byte copies in flight at once)
+                const int m = (r < 4) ? 4 * qa + r : 4 * qb + r - 4;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(cw + t)),
+                             "l"(C + (size_t)m * Mp + n)
+                             : "memory");
+            }
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncwarp();
         }
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        __syncwarp();
         double2 Wa[4][PPL], Wb[4][PPL];
 #pragma unroll
         for (int r = 0; r < 4; r++)
 #pragma unroll
             for (int j = 0; j < PPL; j++) Wa[r][j] = Wb[r][j] = make_double2(0.0, 0.0);
-        das_rows<PPL, false>(cw, Es, Mp, 4 * qa, 4 * qb, lane, Wa, Wb);   // only rows of qa reach n < 4 qb
-        das_rows<PPL, true>(cw, Es, Mp, 4 * qb, Mp, lane, Wa, Wb);
+        das_rows<PPL, false>(ca, cb, Es, Mp, 4 * qa, 4 * qb, lane, Wa, Wb);   // only rows of qa reach n < 4 qb
+        das_rows<PPL, true>(ca, cb, Es, Mp, 4 * qb, Mp, lane, Wa, Wb);
 #pragma unroll
         for (int r = 0; r < 4; r++)
 #pragma unroll
@@ -248,11 +263,11 @@ int launch_das(const Geo &g, const double *dist, const double *amp, int n_bins,
 #ifndef DAS_P64
 #define DAS_P64 1
 #endif
-    // 32 points x 8 warps (Es + Cw <= 96 KB -> two CTAs per SM for M <= 64); DAS_P64: 64 points
-    // (2 per lane) x 4 warps, same shared memory, twice the DFMA per shared-memory load
+    // 32 points x 8 warps; DAS_P64: 64 points
+    // (2 per lane) x 4 warps, twice the DFMAs per loaded Ch entry
     const int P = (Mp <= 64 && DAS_P64) ? 64 : 32;
     const int NWv = (P == 64) ? 4 : kDasWarps;
-    const size_t smem = (size_t)16 * Mp * (P + 8 * NWv);
+    const size_t smem = (size_t)16 * Mp * (P + ((DAS_DIRECT_C && P == 64) ? 0 : 8 * NWv));
     if (smem > 220 * 1024) return -1;
     // set on every call: the attribute is per device, and a process may drive several devices
     const cudaError_t e = (P == 64) ? cudaFuncSetAttribute(das_kernel<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
