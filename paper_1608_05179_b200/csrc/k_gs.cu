@@ -822,11 +822,14 @@ int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_s
     static const bool profile = getenv("DWC_GS_PROFILE") != nullptr;
     unsigned long long *prof = nullptr;
     if (profile) {
-        cudaMalloc(&prof, (32 + 2048) * sizeof(unsigned long long));
+        if (cudaMalloc(&prof, (32 + 2048) * sizeof(unsigned long long)) != cudaSuccess) return -1;
         cudaMemsetAsync(prof, 0, (32 + 2048) * sizeof(unsigned long long), st);
     }
     const size_t smem = gs_smem_bytes(max_sp, ystride);
-    cudaFuncSetAttribute(gs_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cudaFuncSetAttribute(gs_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        if (prof) cudaFree(prof);
+        return -1;
+    }
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
