@@ -80,8 +80,8 @@ int launch_steer(const Geo &g, const double *dist, const double *amp, const doub
 // S2 as a register-blocked triangular complex GEMM.  With the half-Hermitian matrix
 //   Ch[m][n] = H[m][n] (n > m),  H[m][m] / 2 (n = m),  0 (n < m),   H = (C + C^H)/2,
 // b_s = 2 Re(e_s^H Ch e_s) / M^2 -- the Hermitian form at half the flops.  A CTA = P scan points
-// of one bin (P = 64 with 4 warps, 2 points per lane, when Mp <= 64; else P = 32 with 8 warps,
-// 1 point per lane); their steering vectors Es[n][p] (Mp x P complex,
+// of one bin, 2 points per lane (P = 64; 4 warps when Mp <= 64, else 8 warps; the 1-point-per-
+// lane form, P = 32 with 8 warps, remains behind DAS_BIG=0); their steering vectors Es[n][p] (Mp x P complex,
 // Mp = M rounded up to 8, zero rows beyond M) in shared memory.  Warp w owns the row-group
 // pairs (q, G-1-q), q = w, w+NW, ... (G = Mp/4 groups of 4 rows), paired so every warp has the
 // same triangular work, and reads those 8 rows of Ch through L1 (DAS_DIRECT_C).  Lane l
@@ -136,13 +136,13 @@ __device__ __forceinline__ void das_rows(const double2 *__restrict__ ca, const d
 // global loads (L1-resident) instead of being staged in a per-warp shared-memory slice: 64 KB
 // of shared memory per CTA instead of 96 -> three CTAs per SM (register-limited at 168), cfg3
 // DAS stage 3.18 -> 2.94 ms with DAS_UNROLL 8 (4: 2.98, 2: 3.10).  Only for the 2-points-per-
-// lane form (M <= 64): with one point per lane (M = 128) the broadcast loads per DFMA double and
-// the direct form was slower (cfg5 DAS 196 -> 215 ms), so that form keeps the staging.
+// lane forms: with one point per lane the broadcast loads per DFMA double and the direct form
+// was slower (cfg5 DAS 196 -> 215 ms), so that form keeps the staging.
 #ifndef DAS_DIRECT_C
 #define DAS_DIRECT_C 1
 #endif
 template <int PPL, int NW>
-__global__ void __launch_bounds__(32 * NW, (DAS_DIRECT_C && PPL == 2) ? 3 : 2)
+__global__ void __launch_bounds__(32 * NW, (DAS_DIRECT_C && PPL == 2) ? (NW == 4 ? 3 : 1) : 2)
 das_kernel(Geo g, const double *__restrict__ dist, const double *__restrict__ amp,
            const double *__restrict__ freq, const double2 *__restrict__ Ch, int Mp, double *__restrict__ b, int dr) {
     constexpr int P = 32 * PPL;
@@ -265,16 +265,26 @@ int launch_das(const Geo &g, const double *dist, const double *amp, int n_bins,
 #endif
     // 32 points x 8 warps; DAS_P64: 64 points
     // (2 per lane) x 4 warps, twice the DFMAs per loaded Ch entry
-    const int P = (Mp <= 64 && DAS_P64) ? 64 : 32;
-    const int NWv = (P == 64) ? 4 : kDasWarps;
+#ifndef DAS_BIG
+#define DAS_BIG 1
+#endif
+    // DAS_BIG (M > 64): 64 points (2 per lane) x 8 warps, Ch through L1, one CTA per SM (128 KB
+    // of steering vectors, 252 registers): cfg5 DAS 192 -> 170 ms, cfg4 3.15 -> 2.80 ms against
+    // 32 points x 8 warps with the Ch rows staged
+    const bool big = DAS_BIG && DAS_DIRECT_C && Mp > 64 && DAS_P64;
+    const int P = ((Mp <= 64 && DAS_P64) || big) ? 64 : 32;
+    const int NWv = (P == 64 && !big) ? 4 : kDasWarps;
     const size_t smem = (size_t)16 * Mp * (P + ((DAS_DIRECT_C && P == 64) ? 0 : 8 * NWv));
     if (smem > 220 * 1024) return -1;
     // set on every call: the attribute is per device, and a process may drive several devices
-    const cudaError_t e = (P == 64) ? cudaFuncSetAttribute(das_kernel<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+    const cudaError_t e = big ? cudaFuncSetAttribute(das_kernel<2, kDasWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                        : (P == 64) ? cudaFuncSetAttribute(das_kernel<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
                                     : cudaFuncSetAttribute(das_kernel<1, kDasWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return -1;
     dim3 grid((g.S + P - 1) / P, n_bins);
-    if (P == 64)
+    if (big)
+        das_kernel<2, kDasWarps><<<grid, kDasThreads, smem, st>>>(g, dist, amp, freq, (const double2 *)csm_half, Mp, b, dr);
+    else if (P == 64)
         das_kernel<2, 4><<<grid, 128, smem, st>>>(g, dist, amp, freq, (const double2 *)csm_half, Mp, b, dr);
     else
         das_kernel<1, kDasWarps><<<grid, kDasThreads, smem, st>>>(g, dist, amp, freq, (const double2 *)csm_half, Mp, b, dr);
