@@ -95,7 +95,15 @@ struct GsItem {
 };
 
 constexpr int kRsTiles = kRing * kChunk + kStg * 3;   // stream ring + staging area (tiles)
-constexpr int kNringMax = kRsTiles / kChunk;          // stream slots of a non-leader CTA
+// Non-leader CTAs have no staging slots and use the whole area as 3 slots of 7 tiles (6-tile
+// slots left 3 tiles idle): cfg3 GS 45.9-46.0 -> 45.5-45.9 ms, cubic band 35.7 -> 34.5 ms
+// (5 tiles: 45.5-45.9 / 35.9-36.5, 4: 46.0 / 36.4-37.2, 3: 47.0 / 39.1-39.5; scripts/ab_modes.sh).
+#ifndef GS_NLCHUNK
+#define GS_NLCHUNK 7
+#endif
+constexpr int kChunkNL = GS_NLCHUNK;                  // tiles per slot of a non-leader CTA
+constexpr int kNringNL = kRsTiles / kChunkNL;         // stream slots of a non-leader CTA
+constexpr int kNringMax = kNringNL > kRing ? kNringNL : kRing;
 struct __align__(128) GsSmem {
     // stream slot p = tiles [p*kChunk, (p+1)*kChunk); in the leader the tiles from kRing*kChunk on
     // are the staging slots (slot q = 3 tiles: L_j, D_j, LL_{j+2}), in the other CTAs more stream slots
@@ -311,7 +319,8 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
         const int sg = (int)crank / g, rg = (int)crank % g;
         const uint32_t leader = (uint32_t)(sg * g);
         const bool is_leader = (rg == 0);
-        const int nring = is_leader ? kRing : kNringMax;   // non-leaders stream into the staging area too
+        const int nring = is_leader ? kRing : kNringNL;    // non-leaders stream into the staging area too
+        const int chunk = is_leader ? kChunk : kChunkNL;
         const int bin = IT.bin[sg];
         BinLayout L = {0, 0, 0, 0, 0, 0, 0};
         if (bin >= 0) L = lay[bin];
@@ -378,14 +387,14 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                     }
                     const Seg *sd = segt + 2 * kn;
                     for (int sg = 0; sg < 2; sg++)
-                    for (int off = 0; off < sd[sg].len; off += kChunk) {
-                        const int tt = sd[sg].t0 + off, nt = min(kChunk, sd[sg].len - off);
+                    for (int off = 0; off < sd[sg].len; off += chunk) {
+                        const int tt = sd[sg].t0 + off, nt = min(chunk, sd[sg].len - off);
                         if (ppf) t0 = clock64();
                         mbar_wait_cta(&sh.empty[slot], ph ^ 1);
                         if (ppf) { const unsigned long long t = clock64(); p_wait += t - t0; t0 = t; }
                         mbar_expect_tx(&sh.full[slot], (uint32_t)nt * kTile * 4);
                         if (prof) sh.issue_t[slot] = clock64();
-                        bulk_g2s(&sh.rs[slot * kChunk][0], Ab + (size_t)tt * kTile, (uint32_t)nt * kTile * 4, &sh.full[slot]);
+                        bulk_g2s(&sh.rs[slot * chunk][0], Ab + (size_t)tt * kTile, (uint32_t)nt * kTile * 4, &sh.full[slot]);
                         if (ppf) { const unsigned long long t = clock64(); p_issue += t - t0; }
                         seq++;
                         if (++slot == (uint32_t)nring) { slot = 0; ph ^= 1; }
@@ -496,8 +505,8 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                     int first = c;   // index (within the next chunk) of this warp's first tile
                     for (int sg = 0; sg < 2; sg++) {
                         const Seg sr = sd[sg];
-                        for (int off = 0; off < sr.len; off += kChunk) {
-                            const int nt = min(kChunk, sr.len - off);
+                        for (int off = 0; off < sr.len; off += chunk) {
+                            const int nt = min(chunk, sr.len - off);
                             // every warp observes and releases every chunk (parity-tracked barriers: no
                             // warp may fall a ring lap behind or run one ahead)
                             const unsigned long long tw0 = pf ? clock64() : 0ull;
@@ -510,7 +519,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                             int t = first;
                             for (; t < nt; t += n_sw) {
                                 const int ord = sr.ord0 + off + t, J = ownJ[ord];
-                                const float *tile = &sh.rs[slot * kChunk + t][0];
+                                const float *tile = &sh.rs[slot * chunk + t][0];
                                 if (sg == 0) {
                                     tile_dot(tile, xs + 32 * J, rq, cq, acc);
                                 } else {
