@@ -103,7 +103,10 @@ constexpr int kRsTiles = kRing * kChunk + kStg * 3;   // stream ring + staging a
 #endif
 constexpr int kChunkNL = GS_NLCHUNK;                  // tiles per slot of a non-leader CTA
 constexpr int kNringNL = kRsTiles / kChunkNL;         // stream slots of a non-leader CTA
-constexpr int kNringMax = kNringNL > kRing ? kNringNL : kRing;
+// Systems whose x, y and tables already keep the kernel at one CTA per SM (cfg4, cfg5) get the
+// shared memory left over as extra ring slots after the dynamic tables (launch_gs: xtra tiles).
+constexpr int kNringMax = 8;
+static_assert(kNringNL <= kNringMax && kRing <= kNringMax, "ring barrier arrays");
 struct __align__(128) GsSmem {
     // stream slot p = tiles [p*kChunk, (p+1)*kChunk); in the leader the tiles from kRing*kChunk on
     // are the staging slots (slot q = 3 tiles: L_j, D_j, LL_{j+2}), in the other CTAs more stream slots
@@ -284,13 +287,15 @@ __device__ __forceinline__ float tile_tdot(const float *__restrict__ tile, const
 #ifndef GS_MINB
 #define GS_MINB 2
 #endif
+template <bool kXtra>   // extra ring slots in use (an instantiation of its own: no cost otherwise)
 __global__ void __launch_bounds__(kThreads, GS_MINB)
 gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout *__restrict__ lay,
                   int *__restrict__ counter, const float *__restrict__ A, const GsPacket *__restrict__ packets,
                   int sweeps, float *__restrict__ x_out, float *__restrict__ x_map,
                   const int32_t *__restrict__ keep_idx, int S, int xcap, int ystride, int pf,
-                  unsigned long long *__restrict__ prof) {
+                  int xtra_off, int xtra_tiles, unsigned long long *__restrict__ prof) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
+    float *xtra = reinterpret_cast<float *>(smem_raw + xtra_off);   // extra ring tiles (may be none)
     GsSmem &sh = *reinterpret_cast<GsSmem *>(smem_raw);
     float *xs = reinterpret_cast<float *>(smem_raw + sizeof(GsSmem));
     float *ys = xs + xcap;   // per stream warp: y_J (lower part of row J) for the owned J, J/g-indexed
@@ -319,8 +324,14 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
         const int sg = (int)crank / g, rg = (int)crank % g;
         const uint32_t leader = (uint32_t)(sg * g);
         const bool is_leader = (rg == 0);
-        const int nring = is_leader ? kRing : kNringNL;    // non-leaders stream into the staging area too
         const int chunk = is_leader ? kChunk : kChunkNL;
+        const int nbase = is_leader ? kRing : kNringNL;    // non-leaders stream into the staging area too
+        const int nring = kXtra ? min(kNringMax, nbase + xtra_tiles / chunk) : nbase;
+        // first tile of ring slot sl: the fixed area, then the extra tiles
+        auto slot_ptr = [&](uint32_t sl) -> float * {
+            if constexpr (!kXtra) return &sh.rs[sl * chunk][0];
+            return (int)sl < nbase ? &sh.rs[sl * chunk][0] : xtra + (size_t)((int)sl - nbase) * chunk * kTile;
+        };
         const int bin = IT.bin[sg];
         BinLayout L = {0, 0, 0, 0, 0, 0, 0};
         if (bin >= 0) L = lay[bin];
@@ -394,7 +405,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                         if (ppf) { const unsigned long long t = clock64(); p_wait += t - t0; t0 = t; }
                         mbar_expect_tx(&sh.full[slot], (uint32_t)nt * kTile * 4);
                         if (prof) sh.issue_t[slot] = clock64();
-                        bulk_g2s(&sh.rs[slot * chunk][0], Ab + (size_t)tt * kTile, (uint32_t)nt * kTile * 4, &sh.full[slot]);
+                        bulk_g2s(slot_ptr(slot), Ab + (size_t)tt * kTile, (uint32_t)nt * kTile * 4, &sh.full[slot]);
                         if (ppf) { const unsigned long long t = clock64(); p_issue += t - t0; }
                         seq++;
                         if (++slot == (uint32_t)nring) { slot = 0; ph ^= 1; }
@@ -519,7 +530,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                             int t = first;
                             for (; t < nt; t += n_sw) {
                                 const int ord = sr.ord0 + off + t, J = ownJ[ord];
-                                const float *tile = &sh.rs[slot * chunk + t][0];
+                                const float *tile = slot_ptr(slot) + t * kTile;
                                 if (sg == 0) {
                                     tile_dot(tile, xs + 32 * J, rq, cq, acc);
                                 } else {
@@ -834,8 +845,16 @@ int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_s
         if (cudaMalloc(&prof, (32 + 2048) * sizeof(unsigned long long)) != cudaSuccess) return -1;
         cudaMemsetAsync(prof, 0, (32 + 2048) * sizeof(unsigned long long), st);
     }
-    const size_t smem = gs_smem_bytes(max_sp, ystride);
-    if (cudaFuncSetAttribute(gs_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    // one CTA per SM anyway (two would need 2 x (smem + 1 KB) <= 228 KB): the rest of the 227 KB
+    // becomes extra ring tiles
+    const size_t base = (gs_smem_bytes(max_sp, ystride) + 127) / 128 * 128;
+    int xtra_tiles = 0;
+    if (2 * (base + 1024) > 228 * 1024) xtra_tiles = (int)std::min<size_t>((227 * 1024 - base) / (kTile * 4), 4 * kChunkNL);
+    static const int xt_env = getenv("DWC_GS_XTRA") ? atoi(getenv("DWC_GS_XTRA")) : -1;   // experiment
+    if (xt_env >= 0 && xt_env < xtra_tiles) xtra_tiles = xt_env;
+    const size_t smem = base + (size_t)xtra_tiles * kTile * 4;
+    auto kern = xtra_tiles > 0 ? gs_cluster_kernel<true> : gs_cluster_kernel<false>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
         if (prof) cudaFree(prof);
         return -1;
     }
@@ -852,7 +871,7 @@ int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_s
     cfg.numAttrs = 1;
     int n_clusters = 0;
     cfg.gridDim = dim3(num_sms * 2);
-    if (cudaOccupancyMaxActiveClusters(&n_clusters, gs_cluster_kernel, &cfg) != cudaSuccess || n_clusters < 1) {
+    if (cudaOccupancyMaxActiveClusters(&n_clusters, kern, &cfg) != cudaSuccess || n_clusters < 1) {
         cudaGetLastError();
         n_clusters = num_sms / kCl;
     }
@@ -878,9 +897,9 @@ int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_s
             }
         if (win > kL2WindowBytes) pf = 0;
     }
-    cudaError_t e = cudaLaunchKernelEx(&cfg, gs_cluster_kernel, n_items, (const GsItem *)items, lay_dev, counter, A,
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, n_items, (const GsItem *)items, lay_dev, counter, A,
                                        (const GsPacket *)packets, sweeps, x_out, x_map, keep_idx, S, max_sp, ystride,
-                                       pf, prof);
+                                       pf, (int)base, xtra_tiles, prof);
     if (profile) {
         static unsigned long long h[32 + 2048];
         cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, st);
@@ -902,7 +921,7 @@ int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_s
                 " | consumer0: wait_x %.0f wait_tile %.0f compute %.0f reduce+send %.0f\n",
                 h[9], n_clusters * kCl, h[0] / n, h[1] / n, h[10] / n, h[2] / n, h[3] / n, h[11] / n,
                 (h[4] - h[11]) / n, h[5] / n, h[6] / n, h[7] / n, h[8] / n);
-        fprintf(stderr, "[gs-prof] dynamic smem %zu B per CTA (GsSmem %zu), %d clusters of %d\n", smem, sizeof(GsSmem),
+        fprintf(stderr, "[gs-prof] dynamic smem %zu B per CTA (GsSmem %zu, %d extra ring tiles), %d clusters of %d\n", smem, sizeof(GsSmem), xtra_tiles,
                 n_clusters, kCl);
         fprintf(stderr, "[gs-prof] producer: chunks=%llu (%.1f/step) wait_empty %.0f issue %.0f cyc/chunk\n", h[14],
                 h[14] / n, h[14] ? (double)h[12] / h[14] : 0.0, h[14] ? (double)h[13] / h[14] : 0.0);
