@@ -11,10 +11,14 @@ over one band of synthetic input (BASELINE.json configs[2] = cfg3: 64 mics, 101x
 bracketed by barrier + cuda.synchronize, each step timed with CUDA events on the stream the
 library launches on, and the L2 is flushed (256 MiB write) between timed steps.
 
-Multi-GPU (torchrun, one rank per GPU, NCCL): bins are independent.  --scaling weak
-(default): every rank solves its own 256-bin band (per-rank seed), no data-path collective.
---scaling strong: the 256 bins are strided over ranks and the maps are gathered once with
-all_gather_into_tensor at the end (inside the timed region).  Time = max over ranks.
+Multi-GPU (torchrun, one rank per GPU, NCCL): bins are independent.  --scaling strong
+(default for N > 1, the north_star's "256-bin workload ... bins sharded over 1/2/4/8 GPUs"):
+the band's bins are strided over ranks (bin k -> rank k mod N) and the maps are gathered once
+with a single all_gather_into_tensor at the end, inside the timed region; value = the band's
+bins / max-over-ranks step time.  --scaling weak (explicit option): every rank solves its own
+full band (per-rank seed), no data-path collective; value = N * bins / max-rank time.
+`chain_floor_ms`: the band's largest bin solved alone in the same run -- the sequential
+Gauss-Seidel chain that bounds any sharding of the band.
 
 --impl reference: the fp64 CPU oracle (oracle/) as it stands, on this host's cores, timed
 on a bounded strided sample of the same workload (rank 0 only).
@@ -163,6 +167,21 @@ def step_roofline(st, sweeps, hbm_gbs, ms_step):
             "measured_ms": ms_step, "frac": total / ms_step}
 
 
+def bench_value(n_bins_band: int, k_local: int, world: int, scaling: str, ms_max: float) -> float:
+    """freq-bins/s of the whole job: strong = the band's bins / the max-over-ranks step time;
+    weak = every rank's own band (world * k_local bins) / the same time."""
+    total = n_bins_band if (scaling == "strong" and world > 1) else k_local * world
+    return total / (ms_max / 1000.0)
+
+
+def variant_key(cfg, args) -> str:
+    """Key of profiles/gs_traffic.json: the ncu DRAM bytes of a GS launch are only reported for
+    the exact config and variant they were captured on."""
+    return (f"{cfg.name}|order{args.order}|dr{int(bool(args.dr))}|alt{int(bool(args.alt))}|{args.input}"
+            f"|{args.scaling if int(os.environ.get('WORLD_SIZE', '1')) > 1 else 'n1'}"
+            f"|g{int(os.environ.get('WORLD_SIZE', '1'))}")
+
+
 def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
@@ -180,6 +199,8 @@ def run_ours(args, cfg):
     torch.cuda.set_device(dev)
 
     # inputs: weak = own full band per rank (seed = rank); strong = strided shard of one band
+    if args.scaling is None:
+        args.scaling = "strong" if world > 1 else "weak"
     if args.scaling == "weak" or world == 1:
         band = synth.make_band(cfg, seed=rank)
     else:
@@ -243,8 +264,7 @@ def run_ours(args, cfg):
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    total_bins = (K * world) if args.scaling == "weak" else cfg.n_bins
-    value = total_bins / (ms / 1000.0)
+    value = bench_value(cfg.n_bins, K, world, args.scaling, ms)
 
     # roofline of the dominant kernel (GS sweep stream), per launch, CUDA-event timed
     st = st_list[-1]
@@ -252,11 +272,13 @@ def run_ours(args, cfg):
     algo_bytes = st["gs_bytes"]
     achieved = algo_bytes / (gs_ms / 1000.0) / 1e9
     peak, peak_src = load_peaks()
-    traffic = None
+    traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "gs_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(cfg.name)
+            rec = json.load(open(tp)).get(variant_key(cfg, args))
+            if rec is not None and rec.get("gs_kernel") == st.get("gs_kernel"):
+                traffic, traffic_src = rec["dram_bytes"], rec["source"]
         except Exception:
             traffic = None
     launches = int(sum(s["launches"] for s in st_list))
@@ -299,7 +321,32 @@ def run_ours(args, cfg):
         t = torch.tensor([ems], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ems = float(t.item())
-    e2e_value = ((K * world) if args.scaling == "weak" else cfg.n_bins) / (ems / 1000.0)
+    e2e_value = bench_value(cfg.n_bins, K, world, args.scaling, ems)
+
+    # chain floor: this rank's largest bin solved alone (same kernels, same stream, timing on)
+    last = step()
+    nk_last = last["n_keep"].cpu().numpy()
+    kbig = int(np.argmax(nk_last))
+    one_csm = csm_dev[kbig:kbig + 1] if not snapshots else None
+    chain = []
+    for it in range(3):
+        torch.cuda.synchronize(dev)
+        if snapshots:
+            ctx.solve_band_snapshots(geom, band.freqs[kbig:kbig + 1], snap_dev[kbig:kbig + 1], cfg.epsilon, cfg.sweeps,
+                                     cfg.eps_mode, full_grid=cfg.full_grid, order=args.order, dr=args.dr, alt=args.alt,
+                                     stream=stream)
+        else:
+            ctx.solve_band(geom, band.freqs[kbig:kbig + 1], one_csm, cfg.epsilon, cfg.sweeps, cfg.eps_mode,
+                           full_grid=cfg.full_grid, order=args.order, dr=args.dr, alt=args.alt, stream=stream)
+        torch.cuda.synchronize(dev)
+        chain.append(ctx.stats())
+    chain_floor = {"bin": int(band.bins[kbig]), "n_keep": int(nk_last[kbig]),
+                   "gs_ms": float(np.min([c["ms_gs"] for c in chain])),
+                   "total_ms": float(np.min([c["ms_total"] for c in chain]))}
+    if world > 1:
+        t = torch.tensor([chain_floor["gs_ms"], chain_floor["total_ms"]], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        chain_floor["gs_ms"], chain_floor["total_ms"] = float(t[0]), float(t[1])
     h2d = snap_np.nbytes if snapshots else band.csm.nbytes
     d2h = K * 4 + K * S * 4 + K * S * 4
 
@@ -317,7 +364,7 @@ def run_ours(args, cfg):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": args.scaling if world > 1 else "weak", "vs_baseline": None,
+            "scaling": args.scaling if world > 1 else "strong", "vs_baseline": None,
             "dtype": "f32 (PSF + Gauss-Seidel); f64 (DAS map + wavelet threshold)", "data": "synthetic",
             "config": {"workload": workload_desc(cfg), "bins_per_gpu": K,
                        "predictor": "cubic (R19)" if args.order == 3 else "linear (R7)",
@@ -327,8 +374,11 @@ def run_ours(args, cfg):
                                   else "CSMs resident in HBM")},
             "psf_stream_gbs": achieved,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": "gs_kernel",
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "kernel": {1: "gs_cluster_kernel<false>", 2: "gs_cluster_kernel<true>",
+                                    3: "gs_alt_kernel"}.get(int(st["gs_kernel"]), str(st["gs_kernel"])),
                          "algorithmic_bytes_per_launch": algo_bytes, "kernel_ms": gs_ms, "peak_source": peak_src},
+            "chain_floor_ms": chain_floor["total_ms"], "chain_floor": chain_floor,
             "stage_ms": {"das": float(np.mean([s["ms_das"] for s in st_list])),
                          "compress": float(np.mean([s["ms_compress"] for s in st_list])),
                          "psf": float(np.mean([s["ms_psf"] for s in st_list])), "gs": gs_ms,
@@ -359,7 +409,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="cfg3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
+                    help="N > 1: strong (default) shards one band over the ranks; weak gives every rank its own band")
     ap.add_argument("--ref-bins", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cvf", action="store_true", help="skip the compressed-vs-full-grid measurement")

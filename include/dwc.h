@@ -214,7 +214,19 @@ typedef struct {
     int32_t launches;         /* kernels launched by the call */
     float ms_total;           /* event time of the whole call (timing on) */
     float ms_das, ms_compress, ms_psf, ms_gs; /* per-stage event times (timing on) */
+    /* Which Gauss-Seidel kernel the last dwc_solve_band / dwc_gs launched (also set by dwc_gs):
+     * DWC_GS_KERNEL_* below, the extra shared-memory ring tiles it was given, the CTAs of its
+     * grid and the largest number of CTAs it gave one bin. */
+    int32_t gs_kernel;
+    int32_t gs_xtra_tiles;
+    int32_t gs_ctas;
+    int32_t gs_max_group;
 } dwc_stats;
+
+#define DWC_GS_KERNEL_NONE 0
+#define DWC_GS_KERNEL_CLUSTER 1       /* dense-stream cluster kernel, fixed shared-memory ring   */
+#define DWC_GS_KERNEL_CLUSTER_XTRA 2  /* the same with extra ring tiles behind its tables        */
+#define DWC_GS_KERNEL_ALT 3           /* alternating-direction sweeps (DWC_ALT_SWEEPS)           */
 
 DWC_API dwc_status dwc_set_timing(dwc_ctx *ctx, int enable);
 DWC_API dwc_status dwc_get_stats(dwc_ctx *ctx, dwc_stats *out);

@@ -3,10 +3,11 @@
 Bins are independent problems (the paper processes a band of frequencies one by one,
 PAPER.md:22, :545-547), so the hot path has no inter-GPU traffic: bin k is solved on rank
 k mod G (strided, so every rank gets the same spread of frequencies and about the same
-sum of S~_k^2).  The only collective is one gather of the results at the end:
-x_map [K_r, S] fp32, the keep sets as bitmask words [K_r, ceil(S/32)] (dwc_keep_mask) and
-n_keep [K_r], each padded to ceil(K/G) rows per rank, moved with all_gather_into_tensor
-(NCCL over NVLink on the GPU box; the same code runs on gloo in the CPU tests).
+sum of S~_k^2).  The only collective is ONE all_gather_into_tensor of the results at the end:
+each rank packs, per bin row, x_map [S] fp32 (as its 32-bit words), the keep set as bitmask
+words [ceil(S/32)] (dwc_keep_mask) and n_keep into one int32 row of S + ceil(S/32) + 1 words,
+padded to ceil(K/G) rows (NCCL over NVLink on the GPU box; the same code runs on gloo in the
+CPU tests).
 
 This module is plumbing: it moves and reorders bytes; every computation on the path runs
 in the library's kernels.
@@ -51,19 +52,18 @@ def gather_band(x_local, n_keep_local, mask_local, n_bins: int, group=None):
         raise ValueError(f"rank {rank} holds {x_local.shape[0]} bins, expected {k_r}")
     S, W = x_local.shape[1], mask_local.shape[1]
     dev = x_local.device
-
-    def padded(t, shape_tail, dtype):
-        out = torch.zeros((kmax,) + shape_tail, dtype=dtype, device=dev)
-        out[:k_r].copy_(t)
-        return out
-
-    xs = torch.empty((world * kmax, S), dtype=x_local.dtype, device=dev)
-    ms = torch.empty((world * kmax, W), dtype=mask_local.dtype, device=dev)
-    ns = torch.empty((world * kmax,), dtype=n_keep_local.dtype, device=dev)
-    dist.all_gather_into_tensor(xs, padded(x_local, (S,), x_local.dtype), group=group)
-    dist.all_gather_into_tensor(ms, padded(mask_local, (W,), mask_local.dtype), group=group)
-    dist.all_gather_into_tensor(ns, padded(n_keep_local, (), n_keep_local.dtype), group=group)
+    if x_local.dtype != torch.float32 or mask_local.dtype != torch.int32 or n_keep_local.dtype != torch.int32:
+        raise TypeError("x_map float32, mask int32 and n_keep int32 expected")
+    row = S + W + 1
+    # one packed send buffer: [x_map bits | mask words | n_keep] per bin row (zero padded rows)
+    send = torch.zeros((kmax, row), dtype=torch.int32, device=dev)
+    send[:k_r, :S].copy_(x_local.contiguous().view(torch.int32))
+    send[:k_r, S:S + W].copy_(mask_local)
+    send[:k_r, S + W].copy_(n_keep_local)
+    recv = torch.empty((world * kmax, row), dtype=torch.int32, device=dev)
+    dist.all_gather_into_tensor(recv, send, group=group)
     # global bin k lives at [k % world, k // world]: a transpose of the (world, kmax) grid
     order = torch.arange(n_bins, device=dev)
     src = (order % world) * kmax + order // world
-    return xs.index_select(0, src), ns.index_select(0, src), ms.index_select(0, src)
+    g = recv.index_select(0, src)
+    return g[:, :S].contiguous().view(torch.float32), g[:, S + W].contiguous(), g[:, S:S + W].contiguous()

@@ -381,7 +381,11 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
     CU(cudaMemsetAsync(x_map, 0, sizeof(float) * (size_t)n_bins * S, st));
     CU(cudaMemsetAsync(ctx->counter.p, 0, 64, st));
     ev(ctx, 5, st);
+    GsLaunchInfo gsi;
     if (p->flags & DWC_ALT_SWEEPS) {
+        gsi.kernel = DWC_GS_KERNEL_ALT;
+        gsi.ctas = n_bins;
+        gsi.max_group = 1;
         LAUNCH(launch_gs_alt(n_bins, (BinLayout *)ctx->lay.p, max_sp, (float *)ctx->A.p, (double *)ctx->bt.p,
                              p->sweeps, nullptr, x_map, keep_idx, S, st));
     } else {
@@ -389,7 +393,7 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
                           ctx->packets.p, st));
     LAUNCH(launch_gs(n_items, (int *)ctx->items.p, (BinLayout *)ctx->lay.p, max_sp, ystride, (int *)ctx->counter.p,
                      (float *)ctx->A.p, ctx->packets.p, p->sweeps, nullptr, x_map, keep_idx, S,
-                     ctx->num_sms, items.data(), lay.data(), st));
+                     ctx->num_sms, items.data(), lay.data(), st, &gsi));
     }
     ev(ctx, 6, st);
     // warnings (host, Eq. 24)
@@ -415,6 +419,10 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
     stt.psf_flops = 8.0 * M * sum_sq;
     stt.das_flops = 8.0 * (double)M * M * S * n_bins;
     stt.launches = launches;
+    stt.gs_kernel = gsi.kernel;
+    stt.gs_xtra_tiles = gsi.xtra_tiles;
+    stt.gs_ctas = gsi.ctas;
+    stt.gs_max_group = gsi.max_group;
     ctx->stats_events_valid = ctx->timing;
     return DWC_OK;
 }
@@ -697,16 +705,31 @@ dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int3
     CU(cudaMemsetAsync(ctx->gs_b.p, 0, sizeof(double) * sp, st));
     CU(cudaMemcpyAsync(ctx->gs_b.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     CU(cudaMemsetAsync(ctx->counter.p, 0, 64, st));
+    dwc_stats &stt = ctx->stats;
+    stt = dwc_stats{};
+    ctx->stats_events_valid = false;
     if (flags & DWC_ALT_SWEEPS) {
         LAUNCH(launch_gs_alt(1, (BinLayout *)ctx->lay.p, sp, Ap, (double *)ctx->gs_b.p, sweeps, x, nullptr, nullptr,
                              0, st));
+        stt.gs_kernel = DWC_GS_KERNEL_ALT;
+        stt.gs_ctas = stt.gs_max_group = 1;
         return DWC_OK;
     }
+    GsLaunchInfo gsi;
     LAUNCH(launch_gs_prep(1, sp, (BinLayout *)ctx->lay.p, Ap, (double *)ctx->gs_b.p, ctx->packets.p, st));
     LAUNCH(launch_gs((int)items.size() / gs_item_ints(), (int *)ctx->items.p, (BinLayout *)ctx->lay.p, sp,
                      gs_ystride(n),
                      (int *)ctx->counter.p, Ap, ctx->packets.p, sweeps, x, nullptr, nullptr, 0, ctx->num_sms,
-                     items.data(), &lay, st));
+                     items.data(), &lay, st, &gsi));
+    stt.n_bins = 1;
+    stt.sum_keep = n;
+    stt.sum_keep_sq = (double)n * n;
+    stt.gs_bytes = 2.0 * (double)n * (n + 1) * sweeps;
+    stt.launches = launches;
+    stt.gs_kernel = gsi.kernel;
+    stt.gs_xtra_tiles = gsi.xtra_tiles;
+    stt.gs_ctas = gsi.ctas;
+    stt.gs_max_group = gsi.max_group;
     return DWC_OK;
 }
 

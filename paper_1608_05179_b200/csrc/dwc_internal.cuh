@@ -232,10 +232,18 @@ int gs_ystride(int nk);
 int gs_cluster_size();
 int gs_item_ints();
 int gs_group_size(int nk);
+// What a GS launch ran (dwc_stats gs_* fields).
+struct GsLaunchInfo {
+    int kernel = 0;      // DWC_GS_KERNEL_*
+    int xtra_tiles = 0;  // extra ring tiles (the <true> instantiation) or 0
+    int ctas = 0;        // CTAs of the grid
+    int max_group = 0;   // largest CTAs-per-bin of the launch
+};
 // items_host / lay_host (nullable): host copies used to size the L2 prefetch window.
 int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_sp, int ystride, int *counter,
               const float *A, const void *packets, int sweeps, float *x_out, float *x_map, const int32_t *keep_idx,
-              int S, int num_sms, const int *items_host, const BinLayout *lay_host, cudaStream_t st);
+              int S, int num_sms, const int *items_host, const BinLayout *lay_host, cudaStream_t st,
+              GsLaunchInfo *info);
 
 // Per-block solver packets (1/A_ii, within-group scaled coefficients, b~ block) for the GS
 // kernel: gs_packet_bytes() bytes per 32-row block, bin k's packets at v_off/32.

@@ -837,7 +837,8 @@ int gs_group_size(int nk) {
 int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_sp, int ystride, int *counter,
               const float *A,
               const void *packets, int sweeps, float *x_out, float *x_map, const int32_t *keep_idx, int S,
-              int num_sms, const int *items_host, const BinLayout *lay_host, cudaStream_t st) {
+              int num_sms, const int *items_host, const BinLayout *lay_host, cudaStream_t st,
+              GsLaunchInfo *info) {
     // DWC_GS_PROFILE=1: clock64 breakdown of the first CTA's solver / consumer warp (stderr).
     static const bool profile = getenv("DWC_GS_PROFILE") != nullptr;
     unsigned long long *prof = nullptr;
@@ -896,6 +897,14 @@ int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_s
                 win += (kPf + 3) * (double)kTile * 4.0 * 0.5 * (T - 1);
             }
         if (win > kL2WindowBytes) pf = 0;
+    }
+    if (info) {
+        info->kernel = xtra_tiles > 0 ? DWC_GS_KERNEL_CLUSTER_XTRA : DWC_GS_KERNEL_CLUSTER;
+        info->xtra_tiles = xtra_tiles;
+        info->ctas = n_clusters * kCl;
+        info->max_group = 0;
+        if (items_host)
+            for (int it = 0; it < n_items; it++) info->max_group = std::max(info->max_group, items_host[it * gs_item_ints()]);
     }
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, n_items, (const GsItem *)items, lay_dev, counter, A,
                                        (const GsPacket *)packets, sweeps, x_out, x_map, keep_idx, S, max_sp, ystride,

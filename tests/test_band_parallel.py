@@ -68,7 +68,18 @@ def _gather_worker(rank, world, port, n_bins, S):
         x = torch.tensor(np.array([k * 1000.0 + np.arange(S) for k in mine]).reshape(len(mine), S), dtype=torch.float32)
         nk = torch.tensor([len(keeps[k]) for k in mine], dtype=torch.int32)
         m = torch.tensor(np.array([pack_words(keeps[k], S) for k in mine]).reshape(len(mine), -1))
-        gx, gn, gm = gather_band(x, nk, m, n_bins)
+        calls = []
+        real = dist.all_gather_into_tensor
+
+        def counting(*a, **kw):
+            calls.append(1)
+            return real(*a, **kw)
+        dist.all_gather_into_tensor = counting
+        try:
+            gx, gn, gm = gather_band(x, nk, m, n_bins)
+        finally:
+            dist.all_gather_into_tensor = real
+        assert len(calls) == 1   # exactly one all_gather_into_tensor
         ref_x = np.array([k * 1000.0 + np.arange(S) for k in range(n_bins)], dtype=np.float32)
         assert np.array_equal(gx.numpy(), ref_x)
         assert np.array_equal(gn.numpy(), [len(kk) for kk in keeps])

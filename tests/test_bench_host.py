@@ -53,3 +53,27 @@ def test_clock_sampler_reduction():
     out = c.stop()
     assert out["sm_mhz"] == 1920.0 and out["sm_max_mhz"] == 1965.0
     assert out["reasons"] == ["sw_power_cap"] and out["samples"] == 3
+
+
+def test_multi_gpu_value_is_band_over_max_rank_time():
+    """N > 1 defaults to strong scaling: value = the band's bins / the max-over-ranks ms (the
+    north_star's 256-bin workload sharded); weak (explicit) counts every rank's own band."""
+    import bench
+    assert abs(bench.bench_value(256, 32, 8, "strong", 20.0) - 256 / 0.020) < 1e-6
+    assert abs(bench.bench_value(256, 256, 1, "strong", 50.0) - 256 / 0.050) < 1e-6
+    assert abs(bench.bench_value(256, 256, 1, "weak", 50.0) - 256 / 0.050) < 1e-6
+    assert abs(bench.bench_value(256, 256, 4, "weak", 50.0) - 4 * 256 / 0.050) < 1e-6
+    src = open(os.path.join(ROOT, "bench.py")).read()
+    assert 'args.scaling = "strong" if world > 1' in src
+
+
+def test_traffic_only_from_a_matching_capture():
+    """roofline.traffic is read only under the exact config/variant key it was captured on."""
+    import argparse
+
+    import bench
+    import synth
+    a = argparse.Namespace(order=1, dr=False, alt=False, input="csm", scaling=None)
+    b = argparse.Namespace(order=3, dr=False, alt=False, input="csm", scaling=None)
+    assert bench.variant_key(synth.CONFIGS["cfg3"], a) != bench.variant_key(synth.CONFIGS["cfg3"], b)
+    assert bench.variant_key(synth.CONFIGS["cfg3"], a) != bench.variant_key(synth.CONFIGS["cfg5"], a)
