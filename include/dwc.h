@@ -99,6 +99,12 @@ typedef struct {
  * R21): sweep 2p in ascending row order (Eq. 13-14), sweep 2p+1 descending.  Runs a simpler
  * one-CTA-per-bin kernel (a fidelity-study variant, not the tuned path). */
 #define DWC_ALT_SWEEPS 8
+/* DWC_GS_DENSE_STREAM: run the forward sweeps on the dense-stream cluster kernel (every row dot
+ * recomputed from the symmetric-packed A~ streamed through shared memory, up to 4 CTAs per bin)
+ * instead of the default residual-update kernel (the residual r = A x - b kept on chip in fp64,
+ * updated by the rows of A~ whose x changed).  Both keep Eq. 13-14's row and sweep order; they
+ * differ in summation order only. */
+#define DWC_GS_DENSE_STREAM 16
 #define DWC_MAX_MICS 512
 
 /* Create / destroy a context on CUDA device `device`.  The device must be sm_100
@@ -221,12 +227,15 @@ typedef struct {
     int32_t gs_xtra_tiles;
     int32_t gs_ctas;
     int32_t gs_max_group;
+    int64_t gs_updates;       /* residual kernel: row updates (x changes) over all bins and sweeps;
+                                 each one reads one row of A~ (4 sp bytes) */
 } dwc_stats;
 
 #define DWC_GS_KERNEL_NONE 0
 #define DWC_GS_KERNEL_CLUSTER 1       /* dense-stream cluster kernel, fixed shared-memory ring   */
 #define DWC_GS_KERNEL_CLUSTER_XTRA 2  /* the same with extra ring tiles behind its tables        */
 #define DWC_GS_KERNEL_ALT 3           /* alternating-direction sweeps (DWC_ALT_SWEEPS)           */
+#define DWC_GS_KERNEL_RESIDUAL 4      /* residual-update kernel (the default forward sweeps)     */
 
 DWC_API dwc_status dwc_set_timing(dwc_ctx *ctx, int enable);
 DWC_API dwc_status dwc_get_stats(dwc_ctx *ctx, dwc_stats *out);

@@ -26,6 +26,7 @@ SOURCES = {
     "k_keep.cu": [],
     "k_csm.cu": [],
     "k_gs_alt.cu": [],
+    "k_rgs.cu": [],
 }
 
 

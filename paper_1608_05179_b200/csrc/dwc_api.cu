@@ -57,7 +57,7 @@ struct dwc_ctx {
     int num_sms = 148;
     size_t total_bytes = 0;
     DevBuf mic, freq, dist, amp, herm, bint, opa, opb, rsc, wt, bt, A, lay, order, counter, tiles, flag, items, packets,
-        csm_h, nk_h, keep_h, xmap_h, bmap_h, gs_x, gs_b;
+        csm_h, nk_h, keep_h, xmap_h, bmap_h, gs_x, gs_b, Ad, upd;
     PinBuf stage, readback;
     size_t stage_off = 0;
     cudaEvent_t stage_done = nullptr;
@@ -68,6 +68,7 @@ struct dwc_ctx {
     cudaEvent_t ev[8] = {};
     dwc_stats stats{};
     bool stats_events_valid = false;
+    bool stats_upd_valid = false;   // the residual kernel's update counter belongs to the last call
 };
 
 namespace {
@@ -185,7 +186,7 @@ dwc_status check_params(const dwc_params *p) {
     if (!(p->epsilon > 0.0) || !finite(p->epsilon)) return fail(DWC_EINVAL, "epsilon must be > 0");
     if (p->eps_mode != 0 && p->eps_mode != 1) return fail(DWC_EINVAL, "eps_mode must be 0 or 1");
     if (p->sweeps < 1) return fail(DWC_EINVAL, "sweeps must be >= 1");
-    if (p->flags & ~(DWC_FULL_GRID | DWC_CUBIC | DWC_DIAG_REMOVAL | DWC_ALT_SWEEPS))
+    if (p->flags & ~(DWC_FULL_GRID | DWC_CUBIC | DWC_DIAG_REMOVAL | DWC_ALT_SWEEPS | DWC_GS_DENSE_STREAM))
         return fail(DWC_EINVAL, "unknown flags 0x%x", p->flags);
     return DWC_OK;
 }
@@ -324,7 +325,9 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
     }
     // host layout of the compressed systems
     std::vector<BinLayout> lay(n_bins);
-    int64_t a_off = 0, v_off = 0, r_off = 0;
+    // the residual kernel runs every forward-sweep band unless the dense-stream kernel is asked for
+    const bool resid = !(p->flags & (DWC_ALT_SWEEPS | DWC_GS_DENSE_STREAM));
+    int64_t a_off = 0, v_off = 0, r_off = 0, d_off = 0;
     int max_sp = 0, max_rp = 0, ystride = 0;
     double sum_sq = 0.0, sum_sym = 0.0;
     int64_t sum_k = 0;
@@ -333,8 +336,9 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
         const int nk = hk[k];
         const int sp = (nk + 31) & ~31;
         const int rp = (nk + TR - 1) / TR * TR;
-        lay[k] = {nk, sp, a_off, v_off, rp, gs_group_size(nk), r_off};
-        a_off += sym_tiles(sp / 32) * 1024;
+        lay[k] = {nk, sp, a_off, v_off, rp, gs_group_size(nk), r_off, d_off};
+        a_off += (resid ? rgs_band_tiles(sp / 32) : sym_tiles(sp / 32)) * 1024;
+        if (resid) d_off += (int64_t)sp * sp;
         ystride = std::max(ystride, gs_ystride(nk));
         sum_sym += (double)nk * (nk + 1) / 2.0;
         v_off += sp;
@@ -344,7 +348,7 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
         sum_sq += (double)nk * nk;
         sum_k += nk;
     }
-    if (gs_smem_bytes(max_sp, ystride) > 227 * 1024)
+    if (resid ? rgs_smem_bytes(max_sp) > 227 * 1024 : gs_smem_bytes(max_sp, ystride) > 227 * 1024)
         return fail(DWC_EINVAL, "compressed grid of %d points exceeds the on-chip x capacity", max_sp);
     std::vector<int32_t> order(n_bins);
     std::iota(order.begin(), order.end(), 0);
@@ -363,26 +367,35 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
     if (dr && (s = ensure(ctx, ctx->wt, sizeof(double) * (size_t)r_off * M))) return s;
     if ((s = ensure(ctx, ctx->bt, sizeof(double) * (size_t)v_off))) return s;
     if ((s = ensure(ctx, ctx->A, sizeof(float) * (size_t)a_off))) return s;
+    if (resid && ((s = ensure(ctx, ctx->Ad, sizeof(float) * (size_t)d_off)) || (s = ensure(ctx, ctx->upd, 64)) ||
+                  (s = ensure(ctx, ctx->order, sizeof(int32_t) * n_bins))))
+        return s;
     if ((s = ensure(ctx, ctx->packets, (size_t)gs_packet_bytes() * (size_t)(v_off / 32)))) return s;
     if ((s = stage_begin(ctx, sizeof(BinLayout) * n_bins + sizeof(int) * items.size() +
                                   sizeof(int4) * tiles.size() + 4096))) return s;
     if ((s = stage_upload(ctx, ctx->lay.p, lay.data(), sizeof(BinLayout) * n_bins, st))) return s;
     if ((s = stage_upload(ctx, ctx->items.p, items.data(), sizeof(int) * items.size(), st))) return s;
     if ((s = stage_upload(ctx, ctx->tiles.p, tiles.data(), sizeof(int4) * tiles.size(), st))) return s;
+    if (resid && (s = stage_upload(ctx, ctx->order.p, order.data(), sizeof(int32_t) * n_bins, st))) return s;
     if ((s = stage_end(ctx, st))) return s;
     ev(ctx, 3, st);
     // S5 (+S6)
     LAUNCH(launch_psf(G, (double *)ctx->dist.p, (double *)ctx->amp.p, n_bins, (double *)ctx->freq.p,
                       (BinLayout *)ctx->lay.p, keep_idx, b, max_rp, (int)tiles.size(), (int4 *)ctx->tiles.p,
                       (int8_t *)ctx->opa.p, (int8_t *)ctx->opb.p, (double *)ctx->rsc.p, (double *)ctx->bt.p,
-                      dr ? (double *)ctx->wt.p : nullptr, (float *)ctx->A.p, st));
+                      dr ? (double *)ctx->wt.p : nullptr, (float *)ctx->A.p, resid ? (float *)ctx->Ad.p : nullptr, st));
     ev(ctx, 4, st);
     // S7 + S8
     CU(cudaMemsetAsync(x_map, 0, sizeof(float) * (size_t)n_bins * S, st));
     CU(cudaMemsetAsync(ctx->counter.p, 0, 64, st));
     ev(ctx, 5, st);
     GsLaunchInfo gsi;
-    if (p->flags & DWC_ALT_SWEEPS) {
+    if (resid) {
+        CU(cudaMemsetAsync(ctx->upd.p, 0, 64, st));
+        LAUNCH(launch_rgs(n_bins, (int *)ctx->order.p, (BinLayout *)ctx->lay.p, max_sp, (int *)ctx->counter.p,
+                          (float *)ctx->A.p, (float *)ctx->Ad.p, (double *)ctx->bt.p, p->sweeps, nullptr, x_map, keep_idx,
+                          S, ctx->num_sms, (unsigned long long *)ctx->upd.p, st, &gsi));
+    } else if (p->flags & DWC_ALT_SWEEPS) {
         gsi.kernel = DWC_GS_KERNEL_ALT;
         gsi.ctas = n_bins;
         gsi.max_group = 1;
@@ -423,6 +436,7 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
     stt.gs_xtra_tiles = gsi.xtra_tiles;
     stt.gs_ctas = gsi.ctas;
     stt.gs_max_group = gsi.max_group;
+    ctx->stats_upd_valid = resid;
     ctx->stats_events_valid = ctx->timing;
     return DWC_OK;
 }
@@ -468,7 +482,8 @@ dwc_status dwc_destroy(dwc_ctx *ctx) {
     cudaDeviceSynchronize();
     DevBuf *bufs[] = {&ctx->mic, &ctx->freq, &ctx->dist, &ctx->amp, &ctx->herm, &ctx->bint, &ctx->opa, &ctx->opb, &ctx->rsc, &ctx->wt,
                       &ctx->bt, &ctx->A, &ctx->lay, &ctx->order, &ctx->counter, &ctx->tiles, &ctx->flag,
-                      &ctx->items, &ctx->packets, &ctx->csm_h, &ctx->nk_h, &ctx->keep_h, &ctx->xmap_h, &ctx->bmap_h, &ctx->gs_x, &ctx->gs_b};
+                      &ctx->items, &ctx->packets, &ctx->csm_h, &ctx->nk_h, &ctx->keep_h, &ctx->xmap_h, &ctx->bmap_h, &ctx->gs_x, &ctx->gs_b,
+                      &ctx->Ad, &ctx->upd};
     for (DevBuf *b : bufs)
         if (b->p) cudaFree(b->p);
     if (ctx->stage.p) cudaFreeHost(ctx->stage.p);
@@ -492,6 +507,14 @@ dwc_status dwc_set_timing(dwc_ctx *ctx, int enable) {
 dwc_status dwc_get_stats(dwc_ctx *ctx, dwc_stats *out) {
     if (!ctx || !out) return fail(DWC_EINVAL, "NULL argument");
     dwc_stats s = ctx->stats;
+    if (ctx->stats_upd_valid) {
+        // residual kernel: rows of A~ the sweeps had to read (x changes), read back once
+        unsigned long long u = 0;
+        CU(cudaMemcpy(&u, ctx->upd.p, sizeof u, cudaMemcpyDeviceToHost));
+        s.gs_updates = (int64_t)u;
+        ctx->stats.gs_updates = s.gs_updates;
+        ctx->stats_upd_valid = false;
+    }
     if (ctx->stats_events_valid) {
         CU(cudaEventSynchronize(ctx->ev[6]));
         cudaEventElapsedTime(&s.ms_total, ctx->ev[0], ctx->ev[6]);
@@ -646,7 +669,7 @@ dwc_status dwc_psf(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, dou
     if ((s = prepare_geometry(ctx, arr, grid, 1, &freq_hz, G, launches, st))) return s;
     const int sp = (n_keep + 31) & ~31;
     const int rp = (n_keep + psf_tile_rows() - 1) / psf_tile_rows() * psf_tile_rows();
-    BinLayout lay{n_keep, sp, 0, 0, rp, gs_group_size(n_keep), 0};
+    BinLayout lay{n_keep, sp, 0, 0, rp, gs_group_size(n_keep), 0, 0};
     std::vector<int4> tiles;
     append_psf_tiles(tiles, 0, sp);
     if ((s = ensure(ctx, ctx->lay, sizeof(BinLayout))) || (s = ensure(ctx, ctx->tiles, sizeof(int4) * tiles.size())) ||
@@ -662,7 +685,7 @@ dwc_status dwc_psf(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, dou
     LAUNCH(launch_psf(G, (double *)ctx->dist.p, (double *)ctx->amp.p, 1, (double *)ctx->freq.p,
                       (BinLayout *)ctx->lay.p, keep_idx, nullptr, rp, (int)tiles.size(), (int4 *)ctx->tiles.p,
                       (int8_t *)ctx->opa.p, (int8_t *)ctx->opb.p, (double *)ctx->rsc.p, (double *)ctx->bt.p,
-                      dr ? (double *)ctx->wt.p : nullptr, (float *)ctx->A.p, st));
+                      dr ? (double *)ctx->wt.p : nullptr, (float *)ctx->A.p, nullptr, st));
     LAUNCH(launch_tile_convert(0, n_keep, sp, lay.g, (float *)ctx->A.p, A, st));
     return DWC_OK;
 }
@@ -674,9 +697,10 @@ dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int3
     if (n < 1) return fail(DWC_EINVAL, "n must be >= 1");
     if (sweeps < 1) return fail(DWC_EINVAL, "sweeps must be >= 1");
     if (!A || !b || !x) return fail(DWC_EINVAL, "NULL device buffer");
-    if (flags & ~DWC_ALT_SWEEPS) return fail(DWC_EINVAL, "unknown flags 0x%x", flags);
+    if (flags & ~(DWC_ALT_SWEEPS | DWC_GS_DENSE_STREAM)) return fail(DWC_EINVAL, "unknown flags 0x%x", flags);
+    const bool resid = !(flags & (DWC_ALT_SWEEPS | DWC_GS_DENSE_STREAM));
     const int sp = (n + 31) & ~31;
-    if (gs_smem_bytes(sp, gs_ystride(n)) > 227 * 1024)
+    if (resid ? rgs_smem_bytes(sp) > 227 * 1024 : gs_smem_bytes(sp, gs_ystride(n)) > 227 * 1024)
         return fail(DWC_EINVAL, "n = %d exceeds the on-chip x capacity", n);
     cudaStream_t st = (cudaStream_t)cuda_stream;
     int launches = 0;
@@ -687,44 +711,61 @@ dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int3
     CU(cudaMemcpyAsync(ctx->readback.p, ctx->flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     if (*(int *)ctx->readback.p & 2) return fail(DWC_ENUMERIC, "A has a diagonal entry <= 0 or non-finite");
-    BinLayout lay{n, sp, 0, 0, 0, gs_group_size(n), 0};
+    BinLayout lay{n, sp, 0, 0, 0, gs_group_size(n), 0, 0};
     std::vector<int32_t> order{0};
     int32_t nk0 = n;
     std::vector<int> items = build_gs_items(order, &nk0);
+    const size_t a_floats = 1024 * (size_t)(resid ? rgs_band_tiles(sp / 32) : sym_tiles(sp / 32));
     if ((s = ensure(ctx, ctx->lay, sizeof(BinLayout))) || (s = ensure(ctx, ctx->items, sizeof(int) * items.size())) ||
         (s = ensure(ctx, ctx->counter, 64)) || (s = ensure(ctx, ctx->gs_b, sizeof(double) * sp)) ||
-        (s = ensure(ctx, ctx->gs_x, sizeof(float) * 1024 * (size_t)sym_tiles(sp / 32))) ||
-        (s = ensure(ctx, ctx->packets, (size_t)gs_packet_bytes() * (size_t)(sp / 32))))
+        (s = ensure(ctx, ctx->gs_x, sizeof(float) * a_floats)) ||
+        (s = ensure(ctx, ctx->packets, (size_t)gs_packet_bytes() * (size_t)(sp / 32))) ||
+        (s = ensure(ctx, ctx->order, sizeof(int32_t))))
+        return s;
+    if (resid && ((s = ensure(ctx, ctx->Ad, sizeof(float) * (size_t)sp * sp)) || (s = ensure(ctx, ctx->upd, 64))))
         return s;
     if ((s = stage_begin(ctx, 1024 + sizeof(int) * items.size()))) return s;
     if ((s = stage_upload(ctx, ctx->lay.p, &lay, sizeof(BinLayout), st))) return s;
     if ((s = stage_upload(ctx, ctx->items.p, items.data(), sizeof(int) * items.size(), st))) return s;
+    if ((s = stage_upload(ctx, ctx->order.p, order.data(), sizeof(int32_t), st))) return s;
     if ((s = stage_end(ctx, st))) return s;
     float *Ap = (float *)ctx->gs_x.p;
-    LAUNCH(launch_tile_convert(1, n, sp, lay.g, A, Ap, st));
+    if (resid)
+        LAUNCH(launch_rgs_convert(n, sp, A, (float *)ctx->Ad.p, Ap, st));
+    else
+        LAUNCH(launch_tile_convert(1, n, sp, lay.g, A, Ap, st));
     CU(cudaMemsetAsync(ctx->gs_b.p, 0, sizeof(double) * sp, st));
     CU(cudaMemcpyAsync(ctx->gs_b.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     CU(cudaMemsetAsync(ctx->counter.p, 0, 64, st));
     dwc_stats &stt = ctx->stats;
     stt = dwc_stats{};
     ctx->stats_events_valid = false;
+    ctx->stats_upd_valid = false;
+    stt.n_bins = 1;
+    stt.sum_keep = n;
+    stt.sum_keep_sq = (double)n * n;
+    stt.gs_bytes = 2.0 * (double)n * (n + 1) * sweeps;
     if (flags & DWC_ALT_SWEEPS) {
         LAUNCH(launch_gs_alt(1, (BinLayout *)ctx->lay.p, sp, Ap, (double *)ctx->gs_b.p, sweeps, x, nullptr, nullptr,
                              0, st));
         stt.gs_kernel = DWC_GS_KERNEL_ALT;
         stt.gs_ctas = stt.gs_max_group = 1;
+        stt.launches = launches;
         return DWC_OK;
     }
     GsLaunchInfo gsi;
-    LAUNCH(launch_gs_prep(1, sp, (BinLayout *)ctx->lay.p, Ap, (double *)ctx->gs_b.p, ctx->packets.p, st));
-    LAUNCH(launch_gs((int)items.size() / gs_item_ints(), (int *)ctx->items.p, (BinLayout *)ctx->lay.p, sp,
-                     gs_ystride(n),
-                     (int *)ctx->counter.p, Ap, ctx->packets.p, sweeps, x, nullptr, nullptr, 0, ctx->num_sms,
-                     items.data(), &lay, st, &gsi));
-    stt.n_bins = 1;
-    stt.sum_keep = n;
-    stt.sum_keep_sq = (double)n * n;
-    stt.gs_bytes = 2.0 * (double)n * (n + 1) * sweeps;
+    if (resid) {
+        CU(cudaMemsetAsync(ctx->upd.p, 0, 64, st));
+        LAUNCH(launch_rgs(1, (int *)ctx->order.p, (BinLayout *)ctx->lay.p, sp, (int *)ctx->counter.p, Ap,
+                          (float *)ctx->Ad.p, (double *)ctx->gs_b.p, sweeps, x, nullptr, nullptr, 0, ctx->num_sms,
+                          (unsigned long long *)ctx->upd.p, st, &gsi));
+        ctx->stats_upd_valid = true;
+    } else {
+        LAUNCH(launch_gs_prep(1, sp, (BinLayout *)ctx->lay.p, Ap, (double *)ctx->gs_b.p, ctx->packets.p, st));
+        LAUNCH(launch_gs((int)items.size() / gs_item_ints(), (int *)ctx->items.p, (BinLayout *)ctx->lay.p, sp,
+                         gs_ystride(n), (int *)ctx->counter.p, Ap, ctx->packets.p, sweeps, x, nullptr, nullptr, 0,
+                         ctx->num_sms, items.data(), &lay, st, &gsi));
+    }
     stt.launches = launches;
     stt.gs_kernel = gsi.kernel;
     stt.gs_xtra_tiles = gsi.xtra_tiles;

@@ -188,7 +188,7 @@ template <bool kDR>
 __global__ void __launch_bounds__(kPsfThreads, 1)
 psf_tc_kernel(int M, int kp, int n_tiles, const int4 *__restrict__ tiles, const BinLayout *__restrict__ lay,
               const int8_t *__restrict__ opA, const int8_t *__restrict__ opB, const double *__restrict__ rsc,
-              const double *__restrict__ wt, float *__restrict__ Aout) {
+              const double *__restrict__ wt, float *__restrict__ Aout, float *__restrict__ Adense) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     PsfSmem &sm = *reinterpret_cast<PsfSmem *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -267,7 +267,7 @@ psf_tc_kernel(int M, int kp, int n_tiles, const int4 *__restrict__ tiles, const 
         int n = 0;
         // tile metadata one tile ahead (two dependent global loads per tile, off the critical path)
         int4 tl_nx = make_int4(0, 0, 0, 0);
-        BinLayout L_nx = {0, 0, 0, 0, 0, 0, 0};
+        BinLayout L_nx = {0, 0, 0, 0, 0, 0, 0, 0};
         if (blockIdx.x < n_tiles) {
             tl_nx = tiles[blockIdx.x];
             L_nx = lay[tl_nx.x];
@@ -296,9 +296,18 @@ psf_tc_kernel(int M, int kp, int n_tiles, const int4 *__restrict__ tiles, const 
             if (blk_ok) {
                 const double ri = rsc[L.r_off + i];
                 // stored tiles of block (i/32, j0/32) and of its mirror: resolved once per tile
-                int td[3], tm[3];
-                const int nd = sym_targets_g(T, L.g, i >> 5, j0 >> 5, td);
-                const int nm = sym_targets_g(T, L.g, j0 >> 5, i >> 5, tm);
+                int td[3], tm[3], nd, nm;
+                float *Dn = Adense ? Adense + L.d_off : nullptr;
+                if (Adense) {
+                    // residual-GS layout: the band tiles only (the dense matrix holds everything)
+                    td[0] = rgs_band_target(T, i >> 5, j0 >> 5);
+                    tm[0] = rgs_band_target(T, j0 >> 5, i >> 5);
+                    nd = td[0] >= 0 ? 1 : 0;
+                    nm = tm[0] >= 0 ? 1 : 0;
+                } else {
+                    nd = sym_targets_g(T, L.g, i >> 5, j0 >> 5, td);
+                    nm = sym_targets_g(T, L.g, j0 >> 5, i >> 5, tm);
+                }
                 const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(bf * kTmemCols);
                 auto emit = [&](int32_t (&acc)[2 * kSl][8], int jc) {
                     float v[8];
@@ -347,6 +356,15 @@ psf_tc_kernel(int M, int kp, int n_tiles, const int4 *__restrict__ tiles, const 
                         mir[0] = make_float4(v[0], v[1], v[2], v[3]);
                         mir[1] = make_float4(v[4], v[5], v[6], v[7]);
                     }
+                    if (Dn) {
+                        // dense row-major: row i (two float4 per lane), and the mirror column i
+                        // (rows j0+jc..+7, coalesced over the lanes)
+                        float4 *drow = reinterpret_cast<float4 *>(Dn + (size_t)i * L.sp + j0 + jc);
+                        drow[0] = make_float4(v[0], v[1], v[2], v[3]);
+                        drow[1] = make_float4(v[4], v[5], v[6], v[7]);
+#pragma unroll
+                        for (int c = 0; c < 8; c++) Dn[(size_t)(j0 + jc + c) * L.sp + i] = v[c];
+                    }
                 };
                 // the registers of a tcgen05.ld are valid only after tcgen05.wait::ld: tie them to it
                 auto settle = [](int32_t (&acc)[2 * kSl][8]) {
@@ -387,7 +405,7 @@ int psf_tile_cols() { return kTN; }
 int launch_psf(const Geo &g, const double *dist, const double *amp, int n_bins, const double *freq,
                const BinLayout *lay, const int32_t *keep_idx, const double *b, int max_rp, int n_tiles,
                const int4 *tiles, int8_t *opA, int8_t *opB, double *rsc, double *bt, double *wt, float *A,
-               cudaStream_t st) {
+               float *Adense, cudaStream_t st) {
     const int kp = psf_kp(g.m);
     dim3 grid((max_rp + 7) / 8, n_bins);
     psf_slice_kernel<<<grid, 256, 0, st>>>(g, dist, amp, freq, lay, keep_idx, b, kp, opA, opB, rsc, bt, wt);
@@ -404,9 +422,10 @@ int launch_psf(const Geo &g, const double *dist, const double *amp, int n_bins, 
                              (int)smem) != cudaSuccess)
         return -1;
     if (wt)
-        psf_tc_kernel<true><<<n_cta, kPsfThreads, smem, st>>>(g.m, kp, n_tiles, tiles, lay, opA, opB, rsc, wt, A);
+        psf_tc_kernel<true><<<n_cta, kPsfThreads, smem, st>>>(g.m, kp, n_tiles, tiles, lay, opA, opB, rsc, wt, A, Adense);
     else
-        psf_tc_kernel<false><<<n_cta, kPsfThreads, smem, st>>>(g.m, kp, n_tiles, tiles, lay, opA, opB, rsc, nullptr, A);
+        psf_tc_kernel<false><<<n_cta, kPsfThreads, smem, st>>>(g.m, kp, n_tiles, tiles, lay, opA, opB, rsc, nullptr, A,
+                                                               Adense);
     return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
 }
 

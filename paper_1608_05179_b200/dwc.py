@@ -18,7 +18,8 @@ DWC_FULL_GRID = 1
 DWC_CUBIC = 2
 DWC_DIAG_REMOVAL = 4
 DWC_ALT_SWEEPS = 8
-GS_KERNELS = {0: "none", 1: "cluster", 2: "cluster_xtra", 3: "alternating"}
+DWC_GS_DENSE_STREAM = 16
+GS_KERNELS = {0: "none", 1: "cluster", 2: "cluster_xtra", 3: "alternating", 4: "residual"}
 STATUS = {0: "DWC_OK", -1: "DWC_EINVAL", -2: "DWC_ESINGULAR", -3: "DWC_ENUMERIC",
           -4: "DWC_ENOMEM", -5: "DWC_ECUDA", -6: "DWC_ESTATE"}
 
@@ -49,7 +50,7 @@ class Stats(C.Structure):
                 ("launches", C.c_int32), ("ms_total", C.c_float), ("ms_das", C.c_float),
                 ("ms_compress", C.c_float), ("ms_psf", C.c_float), ("ms_gs", C.c_float),
                 ("gs_kernel", C.c_int32), ("gs_xtra_tiles", C.c_int32), ("gs_ctas", C.c_int32),
-                ("gs_max_group", C.c_int32)]
+                ("gs_max_group", C.c_int32), ("gs_updates", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
