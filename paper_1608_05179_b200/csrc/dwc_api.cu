@@ -337,7 +337,7 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
         const int sp = (nk + 31) & ~31;
         const int rp = (nk + TR - 1) / TR * TR;
         lay[k] = {nk, sp, a_off, v_off, rp, gs_group_size(nk), r_off, d_off};
-        a_off += (resid ? rgs_band_tiles(sp / 32) : sym_tiles(sp / 32)) * 1024;
+        if (!resid) a_off += sym_tiles(sp / 32) * 1024;
         if (resid) d_off += (int64_t)sp * sp;
         ystride = std::max(ystride, gs_ystride(nk));
         sum_sym += (double)nk * (nk + 1) / 2.0;
@@ -366,7 +366,7 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
         return s;
     if (dr && (s = ensure(ctx, ctx->wt, sizeof(double) * (size_t)r_off * M))) return s;
     if ((s = ensure(ctx, ctx->bt, sizeof(double) * (size_t)v_off))) return s;
-    if ((s = ensure(ctx, ctx->A, sizeof(float) * (size_t)a_off))) return s;
+    if ((s = ensure(ctx, ctx->A, sizeof(float) * (size_t)std::max<int64_t>(a_off, 1024)))) return s;
     if (resid && ((s = ensure(ctx, ctx->Ad, sizeof(float) * (size_t)d_off)) || (s = ensure(ctx, ctx->upd, 64)) ||
                   (s = ensure(ctx, ctx->order, sizeof(int32_t) * n_bins))))
         return s;
@@ -393,7 +393,7 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
     if (resid) {
         CU(cudaMemsetAsync(ctx->upd.p, 0, 64, st));
         LAUNCH(launch_rgs(n_bins, (int *)ctx->order.p, (BinLayout *)ctx->lay.p, max_sp, (int *)ctx->counter.p,
-                          (float *)ctx->A.p, (float *)ctx->Ad.p, (double *)ctx->bt.p, p->sweeps, nullptr, x_map, keep_idx,
+                          (float *)ctx->Ad.p, (double *)ctx->bt.p, p->sweeps, nullptr, x_map, keep_idx,
                           S, ctx->num_sms, (unsigned long long *)ctx->upd.p, st, &gsi));
     } else if (p->flags & DWC_ALT_SWEEPS) {
         gsi.kernel = DWC_GS_KERNEL_ALT;
@@ -715,7 +715,7 @@ dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int3
     std::vector<int32_t> order{0};
     int32_t nk0 = n;
     std::vector<int> items = build_gs_items(order, &nk0);
-    const size_t a_floats = 1024 * (size_t)(resid ? rgs_band_tiles(sp / 32) : sym_tiles(sp / 32));
+    const size_t a_floats = 1024 * (size_t)(resid ? 1 : sym_tiles(sp / 32));
     if ((s = ensure(ctx, ctx->lay, sizeof(BinLayout))) || (s = ensure(ctx, ctx->items, sizeof(int) * items.size())) ||
         (s = ensure(ctx, ctx->counter, 64)) || (s = ensure(ctx, ctx->gs_b, sizeof(double) * sp)) ||
         (s = ensure(ctx, ctx->gs_x, sizeof(float) * a_floats)) ||
@@ -731,7 +731,7 @@ dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int3
     if ((s = stage_end(ctx, st))) return s;
     float *Ap = (float *)ctx->gs_x.p;
     if (resid)
-        LAUNCH(launch_rgs_convert(n, sp, A, (float *)ctx->Ad.p, Ap, st));
+        LAUNCH(launch_rgs_convert(n, sp, A, (float *)ctx->Ad.p, st));
     else
         LAUNCH(launch_tile_convert(1, n, sp, lay.g, A, Ap, st));
     CU(cudaMemsetAsync(ctx->gs_b.p, 0, sizeof(double) * sp, st));
@@ -756,7 +756,7 @@ dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int3
     GsLaunchInfo gsi;
     if (resid) {
         CU(cudaMemsetAsync(ctx->upd.p, 0, 64, st));
-        LAUNCH(launch_rgs(1, (int *)ctx->order.p, (BinLayout *)ctx->lay.p, sp, (int *)ctx->counter.p, Ap,
+        LAUNCH(launch_rgs(1, (int *)ctx->order.p, (BinLayout *)ctx->lay.p, sp, (int *)ctx->counter.p,
                           (float *)ctx->Ad.p, (double *)ctx->gs_b.p, sweeps, x, nullptr, nullptr, 0, ctx->num_sms,
                           (unsigned long long *)ctx->upd.p, st, &gsi));
         ctx->stats_upd_valid = true;

@@ -65,16 +65,9 @@ struct BinLayout {
     int64_t d_off;    // residual GS kernel: float offset of the dense row-major sp x sp A~_k
 };
 
-// Sub-diagonal tiles the residual GS kernel's solver carries (k_rgs.cu): its band storage holds,
-// per bin, the tiles d*T + k = A[k][(k - d) mod T] for d = 0..min(kRgsSub, T-1) (d = 0: D_k),
-// 32x32 fp32, column-major inside a tile.
-constexpr int kRgsSub = 3;
-__host__ __device__ inline int rgs_band_target(int T, int a, int b) {
-    int d = a - b;
-    if (d < 0) d += T;
-    const int nsub = (T - 1 < kRgsSub) ? T - 1 : kRgsSub;
-    return d <= nsub ? d * T + a : -1;
-}
+// The residual GS kernel's solver carries the contributions of each step's changes to the next
+// kRgsWin row blocks itself (k_rgs.cu); it reads them from the dense row-major A~ only.
+constexpr int kRgsWin = 7;
 
 // S5 + S6 on the tensor cores (k_psf.cu): int8 digit operands of the kept steering vectors
 // (opA: psf_opa_bytes, opB: psf_opb_bytes for sum rp rows; rsc: sum rp doubles), b~ = b[keep]
@@ -88,8 +81,8 @@ size_t psf_opb_bytes(int m, int64_t rows);
 int psf_tile_rows();
 int psf_tile_cols();
 // Adense != NULL: the residual GS layout -- A~_k dense row-major at Adense + d_off (row stride
-// sp, zero padded) plus the band tiles (rgs_band_target) at A + a_off; else the symmetric tile
-// layout of the dense-stream kernel at A + a_off.
+// sp, zero padded), nothing at A; else the symmetric tile layout of the dense-stream kernel at
+// A + a_off.
 int launch_psf(const Geo &g, const double *dist, const double *amp, int n_bins, const double *freq,
                const BinLayout *lay, const int32_t *keep_idx, const double *b, int max_rp, int n_tiles,
                const int4 *tiles, int8_t *opA, int8_t *opB, double *rsc, double *bt, double *wt, float *A,
@@ -264,13 +257,12 @@ int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_s
 // (LPT); A~ as written by launch_psf with Adense; bt = b~ (fp64, zero padded to sp);
 // n_updates (dev, nullable) += the number of row updates (x changes) over all sweeps.
 size_t rgs_smem_bytes(int max_sp);
-int rgs_band_tiles(int T);
 int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int max_sp, int *counter,
-               const float *Aband, const float *Adense, const double *bt, int sweeps, float *x_out, float *x_map,
+               const float *Adense, const double *bt, int sweeps, float *x_out, float *x_map,
                const int32_t *keep_idx, int S, int num_sms, unsigned long long *n_updates, cudaStream_t st,
                GsLaunchInfo *info);
-// dwc_gs: dense row-major n x n (upper triangle) -> padded dense sp x sp + band tiles.
-int launch_rgs_convert(int n, int sp, const float *src, float *dense, float *band, cudaStream_t st);
+// dwc_gs: dense row-major n x n (upper triangle) -> padded dense sp x sp.
+int launch_rgs_convert(int n, int sp, const float *src, float *dense, cudaStream_t st);
 
 // Per-block solver packets (1/A_ii, within-group scaled coefficients, b~ block) for the GS
 // kernel: gs_packet_bytes() bytes per 32-row block, bin k's packets at v_off/32.

@@ -299,11 +299,7 @@ psf_tc_kernel(int M, int kp, int n_tiles, const int4 *__restrict__ tiles, const 
                 int td[3], tm[3], nd, nm;
                 float *Dn = Adense ? Adense + L.d_off : nullptr;
                 if (Adense) {
-                    // residual-GS layout: the band tiles only (the dense matrix holds everything)
-                    td[0] = rgs_band_target(T, i >> 5, j0 >> 5);
-                    tm[0] = rgs_band_target(T, j0 >> 5, i >> 5);
-                    nd = td[0] >= 0 ? 1 : 0;
-                    nm = tm[0] >= 0 ? 1 : 0;
+                    nd = nm = 0;   // residual-GS layout: the dense matrix holds everything
                 } else {
                     nd = sym_targets_g(T, L.g, i >> 5, j0 >> 5, td);
                     nm = sym_targets_g(T, L.g, j0 >> 5, i >> 5, tm);

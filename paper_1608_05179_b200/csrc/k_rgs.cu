@@ -7,35 +7,43 @@
 // from A (S~^2 multiply-adds per sweep), the kernel keeps the residual vector r = A x - b of
 // the current iterate on chip, in fp64, and whenever x_c changes by dx_c adds dx_c * A[c, :]
 // (row c = column c, A is symmetric, reading R1) to it.  In exact arithmetic this is the same
-// sequence of iterates; r only ever receives products of A (fp32) and exact x differences, so
+// sequence of iterates; r only receives products of A (fp32) with exact x differences (fp64), so
 // it equals A x - b of the fp32 iterate to fp64 rounding -- more accurate than an fp32 row dot.
-// The work per sweep is (number of rows whose x changes) x S~ instead of S~^2: DAMAS solutions
-// are sparse (measured on cfg2-cfg5: 5-25 % of the kept nodes change per sweep, fewer as the
-// sweeps converge), and a row whose x does not change costs no memory traffic at all.
+// The memory traffic per sweep is (rows whose x changes) x S~ instead of S~^2: DAMAS solutions
+// are sparse (cfg2-cfg5: 5-25 % of the kept nodes change per sweep, fewer as the sweeps
+// converge), and a row whose x does not change is not read at all.
 //
 // Block formulation (B = 32 rows, T = sp/32 blocks, global step s solves block k = s mod T):
-//  * solver (warp 0, lane = row of the block): the residuals of the block are
-//      ac_i = r_i (stored, fp64 -> fp32) + carry_i
-//    where carry holds the contributions of the changes of the last nsub = min(kSub, T-1)
-//    steps, accumulated by the solver itself from the staged sub-diagonal tiles
-//    A[k+d, k] (d = 1..nsub).  Then, in row order, the next row whose x changes is found with
-//    one ballot over the block (the rows in between keep their x exactly), its change is
-//    broadcast, and every row's ac (D tile) and carry (sub-diagonal tiles) are updated; a
-//    block with q changing rows takes q + 1 ballot rounds instead of a 32-row chain.
-//  * stream (warps 2..7): after the solver publishes the changes of step s (a list of
-//    (c, dx_c), dx in fp64), add dx_c * A[c, :] to the stored r of every block except the
-//    nsub blocks the solver carries (those are added after the solver has read them, at the
-//    stream step of that block), reading the rows of the dense row-major A~ from L2/HBM.
-//    The solver of step s needs stream step s - nsub - 1 complete: nsub steps of slack.
-//  * producer (warp 1): bulk copies of the tiles D_k, A[k+1, k] .. A[k+nsub, k] of each step
-//    into a 3-deep staging ring.
-// One CTA per bin (every bin of a band runs concurrently when the band fits the SMs); bins
-// are taken in descending S~ order from a global counter.
+//  * solver (warp 4, lane = row 32k + lane): the block's residuals are the stored r plus the
+//    carried contributions of the changes of the last W = min(kRgsWin, T-1) steps, which the
+//    solver accumulates itself (fp32, for its own residuals only).  In row
+//    order, the next row whose x changes is found with one ballot over the block (the rows in
+//    between keep x exactly); its change is broadcast and applied to every row's fp32 residual
+//    and to the carries of blocks k+1..k+W.  Both use row t of A~ (= column t, symmetric) over
+//    the columns of blocks k..k+W: the "panel" of row t.  A block with q changing rows takes
+//    q + 1 ballot rounds instead of a 32-row chain.  The changes (row, dx in fp64) are published
+//    as the step's change list.
+//  * panel producer (warp 5): per step, cp.async copies of the panels of the rows PREDICTED to change:
+//    those that changed at the block's previous visit (before the first visit: the rows with
+//    b > 0, exactly the rows sweep 1 changes).  A change outside the prediction (rare: the
+//    active set of a DAMAS iteration is stable) makes the solver load that panel itself.
+//  * row producer (warp 6): bulk-copies the rows of A~ (dense row-major) of every listed change
+//    into a double-buffered shared-memory ring, whole rows or segments of them, as batches.
+//  * stream (warps 0..3, 7): apply dx_c * A[c, :] (fp64) to the stored r of every block, except that
+//    the W blocks the solver carries accumulate into a pending buffer that is added to r when the
+//    solver has read the block (its own step); 128-column chunks are owned by warps (chunk mod 5), so every
+//    element of r has one writer and a fixed update order.  The solver of step s needs stream
+//    step s - W - 1 complete: W steps of slack for the row fetch.
+// One CTA per bin; bins are taken in descending S~ order from a global counter.
+// Numerics: the carries and the stream accumulate A~ (fp32) x dx (fp64) in fp64; A~ entries are
+// widened to fp64 exactly, except values below 2^-126 (never produced by the PSF: they would need
+// |e_i^H e_j|^2 / M^2 < 1.2e-38), which the solver's integer widening flushes to zero.
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "dwc_internal.cuh"
 
@@ -44,23 +52,32 @@ namespace dwc {
 namespace {
 
 constexpr int kRThreads = 256;
-constexpr int kNStream = 6;          // stream warps 2..7
-constexpr int kRStg = 3;             // band-tile staging depth (steps)
-constexpr int kNList = 8;            // change-list ring (steps)
-constexpr int kTileF = 1024;         // floats per 32x32 tile
+constexpr int kNStream = 5;          // stream warps 0..3 and 7
+// warp roles: the latency-critical warps take the higher warp of each SMSP pair (w, w+4): the
+// issue arbiter prefers the higher warp id
+constexpr int kWSolver = 4, kWPanel = 5, kWRows = 6;
+constexpr int kRStg = 5;             // panel staging depth (steps)
+constexpr int kNP = 8;               // panels staged per step (predicted rows beyond: loaded on demand)
+constexpr int kPW = (kRgsWin + 1) * 32;   // panel floats: blocks k..k+W of one row
+constexpr int kNList = 16;           // change-list ring (steps; > kRgsWin + 1)
+constexpr int kCP = 3;               // stream: chunks held in registers per pass
 
 struct __align__(16) RgsEntry {
-    double dx;   // x_new - x_old, exact in fp64
-    int c;       // row (bin-relative)
+    float xn, xo;   // x of the row after / before the change (dx = xn - xo, exact in fp64)
+    int c;          // row (bin-relative)
     int pad;
 };
+__device__ __forceinline__ double entry_dx(const RgsEntry &e) { return (double)e.xn - (double)e.xo; }
 
 struct __align__(128) RgsSmem {
-    float tiles[kRStg][kRgsSub + 1][kTileF];   // D_k, A[k+1,k], ..., A[k+kSub,k] (column-major tiles)
+    float panel[kRStg][kNP][kPW];     // staged panels (ascending row), element m = column 32k + m (mod sp)
+    unsigned smask[kRStg];            // rows (bits) whose panels a stage holds
     RgsEntry list[kNList][32];
+    double dxs[kNList][32];           // dx of each listed change (written by the row producer)
     int cnt[kNList];
     unsigned long long stg_full[kRStg], stg_empty[kRStg];
-    unsigned long long dready[kNList], sdone[kNList];
+    unsigned long long dready[kNList], sdone[kNList], dxready[kNList];
+    unsigned long long rfull[2], rempty[2];   // row ring halves
     int item;
 };
 
@@ -69,6 +86,27 @@ __device__ __forceinline__ void mbar_init(unsigned long long *b, uint32_t count)
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
 }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+#ifdef RGS_WATCHDOG
+// debug build: a wait that has not completed after ~2^24 polls reports itself and traps
+__device__ __forceinline__ void mbar_wait(unsigned long long *b, uint32_t parity) {
+    for (unsigned it = 0;; it++) {
+        uint32_t ok;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(b)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (it == (1u << 24)) {
+            printf("[rgs watchdog] block %d warp %d lane %d stuck on barrier smem+%u parity %u\n", blockIdx.x,
+                   threadIdx.x / 32, threadIdx.x % 32, smem_u32(b), parity);
+            __trap();
+        }
+    }
+}
+#else
 __device__ __forceinline__ void mbar_wait(unsigned long long *b, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
@@ -78,6 +116,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *b, uint32_t parity
         "r"(parity)
         : "memory");
 }
+#endif
 __device__ __forceinline__ void mbar_arrive(unsigned long long *b) {
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
@@ -91,25 +130,62 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
-__device__ __forceinline__ float4 ldg_stream(const float *p) {
-    float4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                 : "l"(p));
-    return v;
+// fp32 -> fp64 on the integer pipes (the F2F conversion unit runs ~15 lanes/clk/SM and is busy
+// with the stream's conversions): exponent rebias and mantissa shift of a normal float; zero and
+// values below 2^-126 give 0.
+__device__ __forceinline__ double widen(float f) {
+    const unsigned b = __float_as_uint(f), a = b & 0x7fffffffu;
+    const unsigned hi = (a >= 0x00800000u) ? ((a >> 3) + 0x38000000u) | (b & 0x80000000u) : 0u;
+    const unsigned lo = (a >= 0x00800000u) ? (a << 29) : 0u;
+    return __hiloint2double((int)hi, (int)lo);
+}
+__device__ __forceinline__ unsigned long long clk() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+    return t;
+}
+
+// Row-ring batching, identical in the row producer and the stream warps: the changes of a step
+// are cut into units (row e, segment g) of seg floats (the last segment of a row shorter); one
+// batch = up to upb units = one ring half.
+struct RingGeom {
+    int seg;    // floats per unit slot (sp, or a multiple of 128 when rows are cut)
+    int nseg;   // segments per row
+    int upb;    // units per batch
+};
+__device__ __forceinline__ RingGeom ring_geom(int sp, int half_floats) {
+    RingGeom g;
+    // whole rows when a row fits a half (slots of sp floats, 128-byte aligned), else segments
+    // that start on 128-column chunk boundaries
+    g.seg = (sp <= half_floats) ? sp : (half_floats / 128) * 128;
+    g.nseg = (sp + g.seg - 1) / g.seg;
+    g.upb = half_floats / g.seg;
+    return g;
 }
 
 }  // namespace
 
-// r (fp64, sp) and x (fp32, sp) follow RgsSmem in dynamic shared memory.
+// Profile slots (DWC_RGS_PROF=1), item 0 = the largest bin: solver [0] tile wait, [1] stream
+// wait, [2] ballot loop, [3] rest, [4] steps, [5] changes; stream warp 0 [8] list wait, [9]
+// batch wait, [10] apply, [11] batches; row producer [12] ring wait, [13] issue; [14] total.
+constexpr int kProfSlots = 16;
+constexpr int kProfItems = 1024;   // then per item: start, end (globaltimer ns), bin, changes
+
+// r (fp64, sp), x (fp32, sp), 1/A_ii (fp32, sp), the prediction masks (T words) and the row
+// ring (2 halves of half_floats) follow RgsSmem.
 __global__ void __launch_bounds__(kRThreads, 2)
 rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restrict__ lay, int *__restrict__ counter,
-           const float *__restrict__ Aband, const float *__restrict__ Adense, const double *__restrict__ bt, int sweeps,
-           float *__restrict__ x_out, float *__restrict__ x_map, const int32_t *__restrict__ keep_idx, int S,
-           unsigned long long *__restrict__ n_updates) {
+           const float *__restrict__ Adense, const double *__restrict__ bt, int sweeps, float *__restrict__ x_out,
+           float *__restrict__ x_map, const int32_t *__restrict__ keep_idx, int S, int max_sp, int half_floats,
+           unsigned long long *__restrict__ n_updates, unsigned long long *__restrict__ prof) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     RgsSmem &sh = *reinterpret_cast<RgsSmem *>(smem_raw);
     double *rs = reinterpret_cast<double *>(smem_raw + sizeof(RgsSmem));
+    double *pend = rs + max_sp;                                 // carried contributions not yet in r
+    float *xs = reinterpret_cast<float *>(pend + max_sp);
+    float *ivs = xs + max_sp;                                   // 1/A_ii
+    unsigned *pmask = reinterpret_cast<unsigned *>(ivs + max_sp);   // per block: rows predicted to change
+    float *ring = reinterpret_cast<float *>(pmask + ((max_sp / 32 + 31) & ~31));   // 128-byte aligned
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     unsigned long long my_updates = 0;
 
@@ -121,175 +197,332 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
         const int bin = order[item];
         const BinLayout L = lay[bin];
         const int sp = L.sp, nk = L.nk, T = sp >> 5;
-        const int nsub = min(kRgsSub, T - 1);
+        const int nsub = min(kRgsWin, T - 1);      // blocks the solver carries
+        const int pw = (nsub + 1) * 32;            // panel floats
         const int total = sweeps * T;
-        float *xs = reinterpret_cast<float *>(rs + sp);
+        const bool pf = prof != nullptr && item == 0;
+        const unsigned long long t_item = pf ? clk() : 0ull;
+        if (prof && tid == 0 && item < kProfItems) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            prof[kProfSlots + 4 * item] = t;
+        }
+        const float *Ad = Adense + L.d_off;    // dense row-major sp x sp
         for (int i = tid; i < sp; i += kRThreads) {
-            rs[i] = -bt[L.v_off + i];   // r = A x0 - b with x0 = 0 (b~ zero padded)
+            const double b = bt[L.v_off + i];
+            rs[i] = -b;   // r = A x0 - b with x0 = 0 (b~ zero padded)
+            pend[i] = 0.0;
             xs[i] = 0.f;
+            // 1/A_ii as the dense-stream kernel forms it; padding rows never change
+            ivs[i] = (i < nk) ? __frcp_rn(Ad[(size_t)i * sp + i]) : 0.f;
+            // sweep 1 from x0 = 0 changes exactly the rows with b~ > 0
+            const unsigned m = __ballot_sync(0xffffffffu, i < nk && b > 0.0);
+            if ((i & 31) == 0) pmask[i >> 5] = m;
         }
         if (tid == 0) {
             for (int i = 0; i < kRStg; i++) {
-                mbar_init(&sh.stg_full[i], 1);
+                mbar_init(&sh.stg_full[i], 33);   // 32 cp.async arrivals + the mask publisher
                 mbar_init(&sh.stg_empty[i], 1);
             }
             for (int i = 0; i < kNList; i++) {
                 mbar_init(&sh.dready[i], 1);
                 mbar_init(&sh.sdone[i], kNStream);
+                mbar_init(&sh.dxready[i], 1);
+            }
+            for (int h = 0; h < 2; h++) {
+                mbar_init(&sh.rfull[h], 1);
+                mbar_init(&sh.rempty[h], kNStream);
             }
             fence_mbar_init();
         }
         __syncthreads();
-        const float *Ab = Aband + L.a_off;     // band tiles: tile d*T + k = A[k][(k - d) mod T]
-        const float *Ad = Adense + L.d_off;    // dense row-major sp x sp
+        const RingGeom rg = ring_geom(sp, half_floats);
 
-        if (wid == 1) {
-            // ================= producer: the band tiles of every step
-            if (lane == 0) {
-                for (int s = 0, k = 0; s < total; s++, k = (k + 1 == T) ? 0 : k + 1) {
-                    const int sl = s % kRStg;
-                    mbar_wait(&sh.stg_empty[sl], ((s / kRStg) & 1) ^ 1);
-                    mbar_expect_tx(&sh.stg_full[sl], (uint32_t)(nsub + 1) * kTileF * 4);
-                    bulk_g2s(sh.tiles[sl][0], Ab + (size_t)k * kTileF, kTileF * 4, &sh.stg_full[sl]);
-                    for (int d = 1; d <= nsub; d++) {
-                        int kd = k + d;
-                        if (kd >= T) kd -= T;   // A[k+d, k] = tile d*T + (k+d)
-                        bulk_g2s(sh.tiles[sl][d], Ab + ((size_t)d * T + kd) * kTileF, kTileF * 4, &sh.stg_full[sl]);
+        if (wid == kWPanel) {
+            // ================= panel producer: the panels of the rows predicted to change, as
+            // 16-byte cp.async copies spread over the warp's lanes (a 1 KB panel is 2 instructions;
+            // one bulk copy per panel cost ~80 cycles of issue on a single lane)
+            unsigned long long pw_wait = 0, pw_issue = 0;
+            for (int s = 0, k = 0; s < total; s++, k = (k + 1 == T) ? 0 : k + 1) {
+                const int sl = s % kRStg;
+                const unsigned long long t0 = pf ? clk() : 0ull;
+                mbar_wait(&sh.stg_empty[sl], ((s / kRStg) & 1) ^ 1);
+                const unsigned long long t1 = pf ? clk() : 0ull;
+                // the mask of block k as the solver left it at the previous visit (a hint: for
+                // T <= kRStg the solver may be updating it right now, either value is valid)
+                unsigned m = *(volatile unsigned *)&pmask[k];
+                unsigned st = 0;
+                for (int n = 0; m && n < kNP; n++) {
+                    st |= m & (0u - m);   // lowest set bit
+                    m &= m - 1;
+                }
+                const int c0 = 32 * k, q4 = pw >> 2;   // 16-byte pieces per panel
+                unsigned mm = st;
+                for (int j = 0; mm; j++) {
+                    const int t = __ffs(mm) - 1;
+                    mm &= mm - 1;
+                    const float *rowp = Ad + (size_t)(c0 + t) * sp;
+                    for (int pc = lane; pc < q4; pc += 32) {
+                        int col = c0 + 4 * pc;
+                        if (col >= sp) col -= sp;   // the window wraps (a piece never straddles sp)
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&sh.panel[sl][j][4 * pc])),
+                                     "l"(rowp + col)
+                                     : "memory");
                     }
                 }
+                // each lane's copies complete on stg_full (32 async arrivals + lane 0's below)
+                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&sh.stg_full[sl]))
+                             : "memory");
+                if (lane == 0) {
+                    sh.smask[sl] = st;
+                    mbar_arrive(&sh.stg_full[sl]);
+                }
+                if (pf) { pw_wait += t1 - t0; pw_issue += clk() - t1; }
             }
-        } else if (wid == 0) {
-            // ================= solver: lane = row 32k + lane of the current block
-            float carry[kRgsSub];
+            if (pf && lane == 0) { prof[7] = pw_wait; prof[15] = pw_issue; }
+        } else if (wid == kWRows) {
+            // ================= row producer: the exact dx of every change (all lanes), then the rows
+            // of every step's changes into the ring (lane 0)
+            unsigned long long tw = 0, ti = 0;
+            int b = 0;   // global batch counter (ring half = b & 1)
+            for (int s = 0; s < total; s++) {
+                const int li = s % kNList;
+                mbar_wait(&sh.dready[li], (s / kNList) & 1);
+                const int n = sh.cnt[li];
+                if (lane < n) sh.dxs[li][lane] = entry_dx(sh.list[li][lane]);
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&sh.dxready[li]);
+                    const int nu = n * rg.nseg;
+                    for (int u0 = 0; u0 < nu; u0 += rg.upb, b++) {
+                        const int h = b & 1;
+                        const unsigned long long t0 = pf ? clk() : 0ull;
+                        mbar_wait(&sh.rempty[h], ((b >> 1) & 1) ^ 1);
+                        const unsigned long long t1 = pf ? clk() : 0ull;
+                        const int nb = min(rg.upb, nu - u0);
+                        float *dst = ring + (size_t)h * half_floats;
+                        if (rg.nseg == 1) {
+                            mbar_expect_tx(&sh.rfull[h], (uint32_t)nb * sp * 4);
+                            for (int j = 0; j < nb; j++)
+                                bulk_g2s(dst + (size_t)j * sp, Ad + (size_t)sh.list[li][u0 + j].c * sp, (uint32_t)sp * 4,
+                                         &sh.rfull[h]);
+                        } else {
+                            uint32_t bytes = 0;
+                            for (int j = 0; j < nb; j++) {
+                                const int u = u0 + j, e = u / rg.nseg, g = u - e * rg.nseg;
+                                bytes += (uint32_t)min(rg.seg, sp - g * rg.seg) * 4;
+                            }
+                            mbar_expect_tx(&sh.rfull[h], bytes);
+                            for (int j = 0; j < nb; j++) {
+                                const int u = u0 + j, e = u / rg.nseg, g = u - e * rg.nseg;
+                                const int c = sh.list[li][e].c;
+                                bulk_g2s(dst + (size_t)j * rg.seg, Ad + (size_t)c * sp + (size_t)g * rg.seg,
+                                         (uint32_t)min(rg.seg, sp - g * rg.seg) * 4, &sh.rfull[h]);
+                            }
+                        }
+                        if (pf) { tw += t1 - t0; ti += clk() - t1; }
+                    }
+                }
+                __syncwarp();
+            }
+            if (pf && lane == 0) { prof[12] = tw; prof[13] = ti; }
+        } else if (wid == kWSolver) {
+            // ================= solver: lane = row 32k + lane of the current block.  Its carries are
+            // fp32 (the residual only needs fp32 for the chain); the exact fp64 contributions are
+            // committed to r by the stream warps (pending buffer, see below).
+            float carry[kRgsWin];
 #pragma unroll
-            for (int d = 0; d < kRgsSub; d++) carry[d] = 0.f;
+            for (int d = 0; d < kRgsWin; d++) carry[d] = 0.f;
+            unsigned long long tt = 0, tsd = 0, tl = 0, tr = 0, nch = 0, nmiss = 0;
             for (int s = 0, k = 0; s < total; s++, k = (k + 1 == T) ? 0 : k + 1) {
+                const unsigned long long t0 = pf ? clk() : 0ull;
                 const int sl = s % kRStg, li = s % kNList;
-                mbar_wait(&sh.stg_full[sl], (s / kRStg) & 1);
-                const float *Dt = sh.tiles[sl][0];
                 const int row = 32 * k + lane;
-                // 1/A_ii as the dense-stream kernel forms it; padding rows never change
-                const float invd = (row < nk) ? __frcp_rn(Dt[lane * 33]) : 0.f;
+                const float invd = ivs[row];
                 float xo = xs[row];
+                mbar_wait(&sh.stg_full[sl], (s / kRStg) & 1);
+                const unsigned smk = sh.smask[sl];
+                // this lane's panel slot (its rank among the staged rows), -1 if not staged
+                const int myp = ((smk >> lane) & 1u) ? __popc(smk & ((1u << lane) - 1u)) : -1;
+                const unsigned long long t1 = pf ? clk() : 0ull;
                 const int sw = s - nsub - 1;   // the stream step the stored r of this block needs
                 if (sw >= 0) mbar_wait(&sh.sdone[sw % kNList], (sw / kNList) & 1);
+                const unsigned long long t2 = pf ? clk() : 0ull;
                 float ac = (float)rs[row] + carry[0];
-                float acc[kRgsSub];
+                float acc[kRgsWin];
 #pragma unroll
-                for (int d = 0; d < kRgsSub; d++) acc[d] = 0.f;
+                for (int d = 0; d < kRgsWin; d++) acc[d] = 0.f;
                 RgsEntry *lst = sh.list[li];
                 int pos = 0, q = 0;
+                unsigned chg = 0;
                 for (;;) {
                     const float w = -ac * invd;
                     const float xn = xo + fmaxf(w, -xo);   // = max(xo - ac/A_ii, 0)
                     const unsigned m = __ballot_sync(0xffffffffu, lane >= pos && xn != xo);
                     if (m == 0u) break;
                     const int t = __ffs(m) - 1;
-                    const float dv = __shfl_sync(0xffffffffu, xn - xo, t);
+                    const float xn_t = __shfl_sync(0xffffffffu, xn, t);
+                    const float xo_t = __shfl_sync(0xffffffffu, xo, t);
+                    const int pt = __shfl_sync(0xffffffffu, myp, t);
+                    const float dv = xn_t - xo_t;
                     if (lane == t) {
-                        lst[q].dx = (double)xn - (double)xo;
+                        lst[q].xn = xn;
+                        lst[q].xo = xo;
                         lst[q].c = row;
                         xo = xn;
                     }
-                    ac = fmaf(Dt[t * 32 + lane], dv, ac);
+                    // panel of row t: element 32d + lane = A[32k+t][32(k+d)+lane] = A[32(k+d)+lane][32k+t]
+                    float pv[kRgsWin + 1];
+                    if (pt >= 0) {
+                        const float *pr = sh.panel[sl][pt];
 #pragma unroll
-                    for (int d = 0; d < kRgsSub; d++)
-                        if (d < nsub) acc[d] = fmaf(sh.tiles[sl][d + 1][t * 32 + lane], dv, acc[d]);
+                        for (int d = 0; d <= kRgsWin; d++) pv[d] = (d <= nsub) ? pr[32 * d + lane] : 0.f;
+                    } else {
+                        // not predicted: the panel from global memory (L2/HBM latency, rare)
+                        const float *rw = Ad + (size_t)(32 * k + t) * sp;
+#pragma unroll
+                        for (int d = 0; d <= kRgsWin; d++) {
+                            int b = k + d;
+                            if (b >= T) b -= T;
+                            pv[d] = (d <= nsub) ? __ldg(rw + 32 * b + lane) : 0.f;
+                        }
+                        nmiss++;
+                    }
+                    ac = fmaf(pv[0], dv, ac);
+#pragma unroll
+                    for (int d = 0; d < kRgsWin; d++) acc[d] = fmaf(pv[d + 1], dv, acc[d]);
+                    chg |= 1u << t;
                     pos = t + 1;
                     q++;
                 }
+                const unsigned long long t3 = pf ? clk() : 0ull;
                 xs[row] = xo;
-                if (lane == 0) sh.cnt[li] = q;
+                if (lane == 0) {
+                    sh.cnt[li] = q;
+                    pmask[k] = chg;   // the prediction for the next visit
+                }
                 my_updates += (unsigned long long)q;
                 __syncwarp();
                 if (lane == 0) {
                     mbar_arrive(&sh.dready[li]);
                     mbar_arrive(&sh.stg_empty[sl]);
                 }
-                // contributions destined for the next nsub steps (fixed summation order)
 #pragma unroll
-                for (int d = 0; d + 1 < kRgsSub; d++) carry[d] = carry[d + 1] + acc[d];
-                carry[kRgsSub - 1] = acc[kRgsSub - 1];
+                for (int d = 0; d + 1 < kRgsWin; d++) carry[d] = carry[d + 1] + acc[d];
+                carry[kRgsWin - 1] = acc[kRgsWin - 1];
+                if (pf) { tt += t1 - t0; tsd += t2 - t1; tl += t3 - t2; tr += clk() - t3; }
+                nch += q;
             }
+            if (prof && lane == 0 && item < kProfItems) prof[kProfSlots + 4 * item + 3] = nch;
+            if (pf && lane == 0) { prof[0] = tt; prof[1] = tsd; prof[2] = tl; prof[3] = tr; prof[4] = total; prof[5] = nch; prof[6] = nmiss; }
         } else {
-            // ================= stream warps: r += dx_c A[c, :] for every change of every step
-            // warp w owns the 128-column chunks q = w, w + 6, ...; lane l the 4 columns 128q + 4l..+3
-            const int w = wid - 2;
-            const int nq = (sp + 127) >> 7;
-            const int sub = lane >> 3;   // 32-column block inside the chunk
+            // ================= stream warps: r += dx_c A[c, :] for every change of every step;
+            // warp w owns the 128-column chunks q = w, w + 5, ...; lane l columns 128q + 4l..+3
+            const int w = (wid < 4) ? wid : 4;
+            unsigned long long tlw = 0, tbw = 0, tap = 0, nb_all = 0;
+            int b = 0;
             for (int s = 0, k = 0; s < total; s++, k = (k + 1 == T) ? 0 : k + 1) {
                 const int li = s % kNList;
+                const unsigned long long t0 = pf ? clk() : 0ull;
                 mbar_wait(&sh.dready[li], (s / kNList) & 1);
+                if (pf) tlw += clk() - t0;
                 const int n = sh.cnt[li];
-                const RgsEntry *lst = sh.list[li];
-                // blocks the solver carries for this step's changes (applied at their own steps)
-                int kd[kRgsSub];
-#pragma unroll
-                for (int d = 0; d < kRgsSub; d++) {
-                    int b = k + 1 + d;
-                    while (b >= T) b -= T;
-                    kd[d] = (d < nsub) ? b : -1;
-                }
-                for (int q = w; q < nq; q += kNStream) {
-                    const int col = 128 * q + 4 * lane;
-                    const int blk = 4 * q + sub;
-                    bool on = col < sp;
-#pragma unroll
-                    for (int d = 0; d < kRgsSub; d++) on = on && blk != kd[d];
-                    if (!on || n == 0) continue;
-                    double2 *rp = reinterpret_cast<double2 *>(rs + col);
-                    double2 r01 = rp[0], r23 = rp[1];
-                    for (int e0 = 0; e0 < n; e0 += 8) {
-                        float4 v[8];
-                        double dx[8];
-#pragma unroll
-                        for (int u = 0; u < 8; u++) {
-                            if (e0 + u < n) {
-                                const RgsEntry E = lst[e0 + u];
-                                v[u] = ldg_stream(Ad + (size_t)E.c * sp + col);
-                                dx[u] = E.dx;
-                            }
-                        }
-#pragma unroll
-                        for (int u = 0; u < 8; u++) {
-                            if (e0 + u < n) {
-                                r01.x = fma((double)v[u].x, dx[u], r01.x);
-                                r01.y = fma((double)v[u].y, dx[u], r01.y);
-                                r23.x = fma((double)v[u].z, dx[u], r23.x);
-                                r23.y = fma((double)v[u].w, dx[u], r23.y);
-                            }
-                        }
-                    }
-                    rp[0] = r01;
-                    rp[1] = r23;
-                }
-                // the carried contributions of steps s-1 .. s-nsub to block k, now that the
-                // solver has read it (its owner warp, in step order: no other warp writes block k)
-                if (((k >> 2) % kNStream) == w && sub == (k & 3)) {
+                const int nu = n * rg.nseg;
+                // the solver has read block k: commit the contributions the solver carried for it
+                // (steps s-nsub .. s-1, held in pend) -- by the owner warp of block k's chunk
+                if ((((k >> 2) % kNStream) == w) && (lane >> 3) == (k & 3)) {
                     const int col = 32 * k + 4 * (lane & 7);
                     double2 *rp = reinterpret_cast<double2 *>(rs + col);
-                    double2 r01 = rp[0], r23 = rp[1];
-                    for (int d = 1; d <= nsub; d++) {
-                        if (s - d < 0) break;
-                        const int lj = (s - d) % kNList;
-                        const int nd = sh.cnt[lj];
-                        for (int e = 0; e < nd; e++) {
-                            const RgsEntry E = sh.list[lj][e];
-                            const float4 v = ldg_stream(Ad + (size_t)E.c * sp + col);
-                            r01.x = fma((double)v.x, E.dx, r01.x);
-                            r01.y = fma((double)v.y, E.dx, r01.y);
-                            r23.x = fma((double)v.z, E.dx, r23.x);
-                            r23.y = fma((double)v.w, E.dx, r23.y);
+                    double2 *pp = reinterpret_cast<double2 *>(pend + col);
+                    double2 r0 = rp[0], r1 = rp[1];
+                    const double2 p0 = pp[0], p1 = pp[1];
+                    r0.x += p0.x; r0.y += p0.y; r1.x += p1.x; r1.y += p1.y;
+                    rp[0] = r0; rp[1] = r1;
+                    pp[0] = make_double2(0.0, 0.0);
+                    pp[1] = make_double2(0.0, 0.0);
+                }
+                // every step, also without changes: it keeps the row producer within kNList steps
+                // of the solver (the solver runs at most nsub + 1 steps ahead of the stream)
+                mbar_wait(&sh.dxready[li], (s / kNList) & 1);
+                for (int u0 = 0; u0 < nu; u0 += rg.upb, b++) {
+                    const int h = b & 1;
+                    const unsigned long long t1 = pf ? clk() : 0ull;
+                    mbar_wait(&sh.rfull[h], (b >> 1) & 1);
+                    const unsigned long long t2 = pf ? clk() : 0ull;
+                    const int nb = min(rg.upb, nu - u0);
+                    const float *src = ring + (size_t)h * half_floats;
+                    // the warp's chunks of each segment, kCP at a time: their r in registers while
+                    // every unit of that segment is applied (independent DFMA chains per chunk)
+                    for (int g = 0; g < rg.nseg; g++) {
+                        const int q0 = (g * rg.seg) >> 7, q1 = (min(sp, (g + 1) * rg.seg) + 127) >> 7;
+                        const int qs = q0 + ((w - q0) % kNStream + kNStream) % kNStream;
+                        for (int qp = qs; qp < q1; qp += kCP * kNStream) {
+                            // loads and fp64 updates run unconditionally on clamped addresses
+                            // (no divergence, all kCP chunks in flight); only the stores are masked
+                            // blocks k+1..k+nsub (carried by the solver) accumulate into pend until
+                            // the solver has read them; the others into r
+                            double2 ra[kCP], rb[kCP];
+                            bool on[kCP];
+                            int cc[kCP];
+                            double *tg[kCP];
+#pragma unroll
+                            for (int i = 0; i < kCP; i++) {
+                                const int qq = qp + i * kNStream, col = 128 * qq + 4 * lane;
+                                int o = (col >> 5) - k;   // block offset from k: 1..nsub are carried
+                                if (o < 0) o += T;
+                                on[i] = qq < q1 && col < sp;
+                                cc[i] = (qq < q1) ? 128 * qq : 128 * qp;   // a chunk of this segment
+                                tg[i] = ((o >= 1 && o <= nsub) ? pend : rs) + cc[i] + 4 * lane;
+                                const double2 *rp = reinterpret_cast<const double2 *>(tg[i]);
+                                ra[i] = rp[0];
+                                rb[i] = rp[1];
+                            }
+                            for (int j = 0; j < nb; j++) {
+                                int e = u0 + j;
+                                if (rg.nseg > 1) {
+                                    const int u = e;
+                                    e = u / rg.nseg;
+                                    if (u - e * rg.nseg != g) continue;
+                                }
+                                const double dx = sh.dxs[li][e];
+                                const float *rowp = src + ((long)j - g) * rg.seg + 4 * lane;   // + chunk column
+                                float4 v[kCP];
+#pragma unroll
+                                for (int i = 0; i < kCP; i++) v[i] = *reinterpret_cast<const float4 *>(rowp + cc[i]);
+#pragma unroll
+                                for (int i = 0; i < kCP; i++) {
+                                    ra[i].x = fma((double)v[i].x, dx, ra[i].x);
+                                    ra[i].y = fma((double)v[i].y, dx, ra[i].y);
+                                    rb[i].x = fma((double)v[i].z, dx, rb[i].x);
+                                    rb[i].y = fma((double)v[i].w, dx, rb[i].y);
+                                }
+                            }
+#pragma unroll
+                            for (int i = 0; i < kCP; i++) {
+                                if (!on[i]) continue;
+                                double2 *rp = reinterpret_cast<double2 *>(tg[i]);
+                                rp[0] = ra[i];
+                                rp[1] = rb[i];
+                            }
                         }
                     }
-                    rp[0] = r01;
-                    rp[1] = r23;
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&sh.rempty[h]);
+                    if (pf) { tbw += t2 - t1; tap += clk() - t2; nb_all++; }
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&sh.sdone[li]);
             }
+            if (pf && w == 0 && lane == 0) { prof[8] = tlw; prof[9] = tbw; prof[10] = tap; prof[11] = nb_all; }
         }
         __syncthreads();
+        if (pf && tid == 0) prof[14] = clk() - t_item;
+        if (prof && tid == 0 && item < kProfItems) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            prof[kProfSlots + 4 * item + 1] = t;
+            prof[kProfSlots + 4 * item + 2] = (unsigned long long)bin;
+        }
         // ---- output: x~ and the embedded full-grid map (S8)
         for (int i = tid; i < nk; i += kRThreads) {
             const float v = xs[i];
@@ -298,19 +531,40 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
         }
         __syncthreads();
     }
-    if (n_updates && wid == 0 && lane == 0 && my_updates) atomicAdd(n_updates, my_updates);
+    if (n_updates && wid == kWSolver && lane == 0 && my_updates) atomicAdd(n_updates, my_updates);
 }
 
-size_t rgs_smem_bytes(int max_sp) { return sizeof(RgsSmem) + (size_t)max_sp * (8 + 4); }
+namespace {
+size_t rgs_base_bytes(int max_sp) { return sizeof(RgsSmem) + (size_t)max_sp * (8 + 8 + 4 + 4) + (((size_t)max_sp / 32 + 31) & ~(size_t)31) * 4; }
+}  // namespace
 
-int rgs_band_tiles(int T) { return (std::min(kRgsSub, T - 1) + 1) * T; }
+// The minimum ring (two halves of 128 floats); launch_rgs gives it what shared memory allows.
+size_t rgs_smem_bytes(int max_sp) { return rgs_base_bytes(max_sp) + 2 * 128 * 4 + 512; }
+
 
 int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int max_sp, int *counter,
-               const float *Aband, const float *Adense, const double *bt, int sweeps, float *x_out, float *x_map,
+               const float *Adense, const double *bt, int sweeps, float *x_out, float *x_map,
                const int32_t *keep_idx, int S, int num_sms, unsigned long long *n_updates, cudaStream_t st,
                GsLaunchInfo *info) {
-    const size_t smem = (rgs_smem_bytes(max_sp) + 127) / 128 * 128;
-    if (smem > 227 * 1024) return -1;
+    const size_t base = (rgs_base_bytes(max_sp) + 127) / 128 * 128;
+    if (base + 1536 > 227 * 1024) return -1;
+    // two CTAs per SM (2 x (smem + 1 KB reserved) <= 228 KB) when the band has the bins for it
+    // and the ring still holds a row; else one CTA per SM with the rest of the 227 KB as ring
+    static const int ring_env = getenv("DWC_RGS_RING_KB") ? atoi(getenv("DWC_RGS_RING_KB")) : 0;   // experiment
+    static const int per_sm_env = getenv("DWC_RGS_PER_SM") ? atoi(getenv("DWC_RGS_PER_SM")) : 0;   // experiment
+    const size_t per2 = 114 * 1024 - 1024;
+    size_t ring;
+    // two per SM when the band has more bins than SMs and a ring half still holds 4 rows
+    const bool two = per_sm_env ? per_sm_env == 2 && per2 > base + 2048
+                                : n_bins > num_sms && per2 > base && (per2 - base) / 8 >= 4 * (size_t)max_sp;
+    if (two)
+        ring = (per2 - base - 512) / 1024 * 1024;
+    else
+        ring = (227 * 1024 - base - 512) / 1024 * 1024;
+    if (ring_env > 0 && (size_t)ring_env * 1024 < ring) ring = (size_t)ring_env * 1024;
+    const int half_floats = (int)(ring / 8) / 128 * 128;   // floats per half (ring bytes / 2 / 4)
+    if (half_floats < 128) return -1;
+    const size_t smem = base + (size_t)half_floats * 8 + 512;   // + slack: a row's last chunk reads past it
     if (cudaFuncSetAttribute(rgs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return -1;
     int per_sm = 0;
@@ -329,32 +583,62 @@ int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int m
         info->ctas = grid;
         info->max_group = 1;
     }
-    rgs_kernel<<<grid, kRThreads, smem, st>>>(n_bins, order_dev, lay_dev, counter, Aband, Adense, bt, sweeps, x_out,
-                                              x_map, keep_idx, S, n_updates);
-    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+    // DWC_RGS_PROF=1: clock64 breakdown of the largest bin (stderr)
+    static const bool profile = getenv("DWC_RGS_PROF") != nullptr;
+    unsigned long long *prof = nullptr;
+    if (profile) {
+        const size_t pb = (kProfSlots + 4 * kProfItems + 2) * sizeof(unsigned long long);
+        if (cudaMalloc(&prof, pb) != cudaSuccess) return -1;
+        cudaMemsetAsync(prof, 0, pb, st);
+    }
+    rgs_kernel<<<grid, kRThreads, smem, st>>>(n_bins, order_dev, lay_dev, counter, Adense, bt, sweeps, x_out, x_map,
+                                              keep_idx, S, max_sp, half_floats, n_updates, prof);
+    const cudaError_t e = cudaPeekAtLastError();
+    if (profile) {
+        static unsigned long long h[kProfSlots + 4 * kProfItems + 2];
+        cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        {   // the items that ended last (the band's tail) and when
+            const int ni = std::min(n_bins, kProfItems);
+            unsigned long long t0 = ~0ull;
+            for (int i = 0; i < ni; i++) t0 = std::min(t0, h[kProfSlots + 4 * i]);
+            std::vector<int> idx(ni);
+            for (int i = 0; i < ni; i++) idx[i] = i;
+            std::sort(idx.begin(), idx.end(), [&](int a, int b) { return h[kProfSlots + 4 * a + 1] > h[kProfSlots + 4 * b + 1]; });
+            fprintf(stderr, "[rgs-prof] last items to end (item bin: start..end ms, changes):");
+            for (int j = 0; j < std::min(ni, 8); j++) {
+                const unsigned long long *r = h + kProfSlots + 4 * idx[j];
+                fprintf(stderr, " %d b%llu: %.2f..%.2f (%llu)", idx[j], r[2], (r[0] - t0) * 1e-6, (r[1] - t0) * 1e-6, r[3]);
+            }
+            fprintf(stderr, "\n");
+        }
+        const double n = h[4] ? (double)h[4] : 1.0;
+        fprintf(stderr,
+                "[rgs-prof] grid %d x %zu B smem (ring 2 x %d floats), steps %llu, changes %llu (%.2f/step), item %.0f cyc"
+                " | solver cyc/step: tiles %.0f stream %.0f loop %.0f rest %.0f | stream0: list %.0f batch %.0f apply %.0f"
+                " (%llu batches) | rowprod: ring wait %.0f issue %.0f | panel misses %llu | panelprod wait %.0f issue %.0f\n",
+                grid, smem, half_floats, h[4], h[5], h[5] / n, (double)h[14], h[0] / n, h[1] / n, h[2] / n, h[3] / n,
+                h[8] / n, h[9] / n, h[10] / n, h[11], h[12] / n, h[13] / n, h[6], h[7] / n, h[15] / n);
+        cudaFree(prof);
+    }
+    return e == cudaSuccess ? 1 : -1;
 }
 
 // dwc_gs input conversion: dense row-major n x n (upper triangle read, reading R1) -> the
-// padded dense sp x sp matrix and the band tiles of the residual kernel.
-__global__ void rgs_convert_kernel(int n, int sp, const float *__restrict__ src, float *__restrict__ dense,
-                                   float *__restrict__ band) {
-    const int T = sp >> 5, nsub = min(kRgsSub, T - 1);
+// padded dense sp x sp matrix of the residual kernel.
+__global__ void rgs_convert_kernel(int n, int sp, const float *__restrict__ src, float *__restrict__ dense) {
     const long total = (long)sp * sp;
     for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
         const int i = (int)(e / sp), j = (int)(e - (long)(e / sp) * sp);
         const int lo = min(i, j), hi = max(i, j);
-        const float v = (hi < n) ? src[(size_t)lo * n + hi] : 0.f;
-        dense[e] = v;
-        int d = (i >> 5) - (j >> 5);
-        if (d < 0) d += T;
-        if (d <= nsub) band[((size_t)d * T + (i >> 5)) * kTileF + (j & 31) * 32 + (i & 31)] = v;
+        dense[e] = (hi < n) ? src[(size_t)lo * n + hi] : 0.f;
     }
 }
 
-int launch_rgs_convert(int n, int sp, const float *src, float *dense, float *band, cudaStream_t st) {
+int launch_rgs_convert(int n, int sp, const float *src, float *dense, cudaStream_t st) {
     const long total = (long)sp * sp;
     const int blocks = (int)std::min<long>((total + 255) / 256, 148L * 32);
-    rgs_convert_kernel<<<blocks, 256, 0, st>>>(n, sp, src, dense, band);
+    rgs_convert_kernel<<<blocks, 256, 0, st>>>(n, sp, src, dense);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

@@ -130,11 +130,12 @@ class Geometry:
         return Grid(int(self.n), float(self.side_len), float(self.z0), float(self.cx), float(self.cy))
 
 
-def _flags(full_grid: bool, order: int, dr: bool = False, alt: bool = False) -> int:
+def _flags(full_grid: bool, order: int, dr: bool = False, alt: bool = False, dense_stream: bool = False) -> int:
     if order not in (1, 3):
         raise ValueError("order must be 1 (linear predictor) or 3 (cubic)")
     return ((DWC_FULL_GRID if full_grid else 0) | (DWC_CUBIC if order == 3 else 0) |
-            (DWC_DIAG_REMOVAL if dr else 0) | (DWC_ALT_SWEEPS if alt else 0))
+            (DWC_DIAG_REMOVAL if dr else 0) | (DWC_ALT_SWEEPS if alt else 0) |
+            (DWC_GS_DENSE_STREAM if dense_stream else 0))
 
 
 def _stream(stream) -> int:
@@ -176,7 +177,7 @@ class Context:
     # ---- hot path ---------------------------------------------------------------
     def solve_band(self, geom: Geometry, freqs: Sequence[float], csm, epsilon: float, sweeps: int,
                    eps_mode: int = 0, full_grid: bool = False, want_b: bool = False, out=None, order: int = 1,
-                   stream=None, dr: bool = False, alt: bool = False):
+                   stream=None, dr: bool = False, alt: bool = False, dense_stream: bool = False):
         """Batched S0..S8 on device tensors.  csm: cuda complex128 [K,M,M].
         Returns dict(n_keep int32[K], keep_idx int32[K,S], x_map float32[K,S], b_map, warn)."""
         import torch
@@ -192,7 +193,7 @@ class Context:
                    "b_map": torch.empty((K, S), dtype=torch.float64, device=dev) if want_b else None}
         warn = np.zeros(K, dtype=np.uint32)
         arr, grid = geom.c_array(), geom.c_grid()
-        prm = Params(float(epsilon), int(eps_mode), int(sweeps), _flags(full_grid, order, dr, alt))
+        prm = Params(float(epsilon), int(eps_mode), int(sweeps), _flags(full_grid, order, dr, alt, dense_stream))
         _check(lib().dwc_solve_band(
             self._h, C.byref(arr), C.byref(grid), C.byref(prm), K, freqs.ctypes.data,
             _dev(csm, torch.complex128, "csm"), _dev(out["n_keep"], torch.int32, "n_keep"),
@@ -204,7 +205,7 @@ class Context:
 
     def solve_band_host(self, geom: Geometry, freqs, csm, epsilon: float, sweeps: int, eps_mode: int = 0,
                         full_grid: bool = False, want_b: bool = False, out=None, stream=None, order: int = 1,
-                        dr: bool = False, alt: bool = False):
+                        dr: bool = False, alt: bool = False, dense_stream: bool = False):
         """Same as solve_band with host buffers (numpy or CPU tensors, pinned or not); the
         host<->device copies happen inside the C call, which returns when results are on the host."""
         import torch
@@ -220,7 +221,7 @@ class Context:
                    "b_map": torch.empty((K, S), dtype=torch.float64) if want_b else None}
         warn = np.zeros(K, dtype=np.uint32)
         arr, grid = geom.c_array(), geom.c_grid()
-        prm = Params(float(epsilon), int(eps_mode), int(sweeps), _flags(full_grid, order, dr, alt))
+        prm = Params(float(epsilon), int(eps_mode), int(sweeps), _flags(full_grid, order, dr, alt, dense_stream))
         csm = csm.contiguous()
         _check(lib().dwc_solve_band_host(
             self._h, C.byref(arr), C.byref(grid), C.byref(prm), K, freqs.ctypes.data, csm.data_ptr(),
@@ -233,7 +234,7 @@ class Context:
     # ---- stage entry points ---------------------------------------------------------
     def solve_band_snapshots(self, geom: Geometry, freqs: Sequence[float], snap, epsilon: float, sweeps: int,
                              eps_mode: int = 0, full_grid: bool = False, want_b: bool = False, order: int = 1,
-                             stream=None, dr: bool = False, alt: bool = False):
+                             stream=None, dr: bool = False, alt: bool = False, dense_stream: bool = False):
         """The path from snapshot spectra (Eq. 1 on the device).  snap: cuda complex128 [K,M,I]."""
         import torch
         freqs = np.ascontiguousarray(freqs, dtype=np.float64)
@@ -247,7 +248,7 @@ class Context:
                "b_map": torch.empty((K, S), dtype=torch.float64, device=dev) if want_b else None}
         warn = np.zeros(K, dtype=np.uint32)
         arr, grid = geom.c_array(), geom.c_grid()
-        prm = Params(float(epsilon), int(eps_mode), int(sweeps), _flags(full_grid, order, dr, alt))
+        prm = Params(float(epsilon), int(eps_mode), int(sweeps), _flags(full_grid, order, dr, alt, dense_stream))
         _check(lib().dwc_solve_band_snapshots(
             self._h, C.byref(arr), C.byref(grid), C.byref(prm), K, freqs.ctypes.data, int(snap.shape[2]),
             _dev(snap, torch.complex128, "snap"), _dev(out["n_keep"], torch.int32, "n_keep"),
@@ -310,12 +311,13 @@ class Context:
                              _dev(A, torch.float32, "A"), _stream(stream)))
         return A
 
-    def gs(self, A, b, sweeps: int, stream=None, alt: bool = False):
+    def gs(self, A, b, sweeps: int, stream=None, alt: bool = False, dense_stream: bool = False):
         import torch
         n = A.shape[0]
         x = torch.empty(n, dtype=torch.float32, device=A.device)
+        fl = (DWC_ALT_SWEEPS if alt else 0) | (DWC_GS_DENSE_STREAM if dense_stream else 0)
         _check(lib().dwc_gs(self._h, n, _dev(A, torch.float32, "A"), _dev(b, torch.float64, "b"), int(sweeps),
-                            DWC_ALT_SWEEPS if alt else 0, _dev(x, torch.float32, "x"), _stream(stream)))
+                            fl, _dev(x, torch.float32, "x"), _stream(stream)))
         return x
 
     # ---- multi-GPU gather helpers ----------------------------------------------------------

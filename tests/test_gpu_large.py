@@ -57,6 +57,7 @@ def oracle_args(g):
 
 
 _SYS = {}
+_ORACLE = {}
 
 
 def cfg5_system(oracle_lib, nk):
@@ -73,33 +74,38 @@ def cfg5_system(oracle_lib, nk):
     return _SYS[nk]
 
 
+@pytest.mark.parametrize("dense", [False, True], ids=["residual", "dense_stream"])
 @pytest.mark.parametrize("nk,sweeps", [(2100, 20), (4500, 20), (9150, 20)])
-def test_gs_large_systems(ctx, torch_cuda, oracle_lib, nk, sweeps):
+def test_gs_large_systems(ctx, torch_cuda, oracle_lib, nk, sweeps, dense):
     """dwc_gs on S~ = 2100 / 4500 / 9150 (T = 66 / 141 / 286 row blocks: ownership tables,
-    y strides and segment runs far beyond the cfg3 sizes)."""
+    y strides and segment runs far beyond the cfg3 sizes; on the dense-stream kernel the
+    extra-ring instantiation)."""
     torch = torch_cuda
     A, bt = cfg5_system(oracle_lib, nk)
     ref = oracle_lib.gs(A, bt, sweeps)
-    x = ctx.gs(torch.from_numpy(A.astype(np.float32)).cuda(), torch.from_numpy(bt).cuda(), sweeps).cpu().numpy()
+    x = ctx.gs(torch.from_numpy(A.astype(np.float32)).cuda(), torch.from_numpy(bt).cuda(), sweeps,
+               dense_stream=dense).cpu().numpy()
     st = ctx.stats()
-    assert st["gs_kernel"] in (1, 2) and st["gs_max_group"] >= 1
-    if st["gs_kernel"] == 2:
-        assert st["gs_xtra_tiles"] > 0
+    if dense:
+        assert st["gs_kernel"] == 2 and st["gs_xtra_tiles"] > 0 and st["gs_max_group"] == 4
+    else:
+        assert st["gs_kernel"] == 4 and st["gs_updates"] > 0
     assert x.min() >= 0
     assert rel_l2(x, ref) < TOL_X, rel_l2(x, ref)
     assert abs(x.sum() - ref.sum()) < TOL_P * ref.sum()
 
 
-def test_gs_large_system_bitwise_deterministic(ctx, torch_cuda, oracle_lib):
+@pytest.mark.parametrize("dense", [False, True], ids=["residual", "dense_stream"])
+def test_gs_large_system_bitwise_deterministic(ctx, torch_cuda, oracle_lib, dense):
     """Repeated runs of an S~ = 4500 system are bit-identical (every summation order is fixed, so
     a difference would be an ordering race in the ring / partial-sum / x-forwarding protocol)."""
     torch = torch_cuda
     A, bt = cfg5_system(oracle_lib, 4500)
     Ad = torch.from_numpy(A.astype(np.float32)).cuda()
     bd = torch.from_numpy(bt).cuda()
-    ref = ctx.gs(Ad, bd, 30).cpu().numpy()
+    ref = ctx.gs(Ad, bd, 30, dense_stream=dense).cpu().numpy()
     for _ in range(3):
-        assert np.array_equal(ctx.gs(Ad, bd, 30).cpu().numpy(), ref)
+        assert np.array_equal(ctx.gs(Ad, bd, 30, dense_stream=dense).cpu().numpy(), ref)
 
 
 _XTRA_SCRIPT = r"""
@@ -108,7 +114,7 @@ sys.path.insert(0, {root!r})
 from paper_1608_05179_b200 import Context
 A = np.load({a!r}); b = np.load({b!r})
 c = Context(0)
-x = c.gs(torch.from_numpy(A).cuda(), torch.from_numpy(b).cuda(), 25).cpu().numpy()
+x = c.gs(torch.from_numpy(A).cuda(), torch.from_numpy(b).cuda(), 25, dense_stream=True).cpu().numpy()
 st = c.stats()
 np.save({out!r}, x)
 print(st["gs_kernel"], st["gs_xtra_tiles"])
@@ -121,7 +127,7 @@ def test_gs_extra_ring_tiles_do_not_change_results(ctx, torch_cuda, oracle_lib, 
     torch = torch_cuda
     A, bt = cfg5_system(oracle_lib, 2100)
     A32 = A.astype(np.float32)
-    x_default = ctx.gs(torch.from_numpy(A32).cuda(), torch.from_numpy(bt).cuda(), 25).cpu().numpy()
+    x_default = ctx.gs(torch.from_numpy(A32).cuda(), torch.from_numpy(bt).cuda(), 25, dense_stream=True).cpu().numpy()
     kern_default = ctx.stats()["gs_kernel"]
     pa, pb, po = tmp_path / "A.npy", tmp_path / "b.npy", tmp_path / "x.npy"
     np.save(pa, A32)
@@ -136,16 +142,19 @@ def test_gs_extra_ring_tiles_do_not_change_results(ctx, torch_cuda, oracle_lib, 
     assert np.array_equal(np.load(po), x_default)
 
 
-def _e2e(ctx, torch, oracle_lib, band, sweeps, full=False):
+def _e2e(ctx, torch, oracle_lib, band, sweeps, full=False, dense=False):
     cfg = band.cfg
     g = geom_of(band)
     out = ctx.solve_band(g, band.freqs, torch.from_numpy(band.csm).cuda(), cfg.epsilon, sweeps, cfg.eps_mode,
-                         full_grid=full, want_b=True)
+                         full_grid=full, want_b=True, dense_stream=dense)
     st = ctx.stats()
     nk = out["n_keep"].cpu().numpy()
     keep = out["keep_idx"].cpu().numpy()
     x = out["x_map"].cpu().numpy()
-    rnk, rkeep, rx, rb = oracle_lib.solve_band_cfg(band, sweeps=sweeps, full_grid=full)
+    key = (cfg.name, cfg.n, tuple(int(b) for b in band.bins), sweeps, full)
+    if key not in _ORACLE:   # one oracle run serves both kernels
+        _ORACLE[key] = oracle_lib.solve_band_cfg(band, sweeps=sweeps, full_grid=full)
+    rnk, rkeep, rx, rb = _ORACLE[key]
     for k in range(len(band.freqs)):
         assert rel_l2(out["b_map"][k].cpu().numpy(), rb[k]) < 1e-5
         assert nk[k] == rnk[k], (k, nk[k], rnk[k])
@@ -156,25 +165,29 @@ def _e2e(ctx, torch, oracle_lib, band, sweeps, full=False):
     return st, nk
 
 
-def test_e2e_cfg5_largest_bins(ctx, torch_cuda, oracle_lib):
+@pytest.mark.parametrize("dense", [False, True], ids=["residual", "dense_stream"])
+def test_e2e_cfg5_largest_bins(ctx, torch_cuda, oracle_lib, dense):
     """cfg5's three largest bins (11.2-12 kHz, S~ ~ 8-9k of 40401) at 20 sweeps, in one call."""
     band = synth.make_band("cfg5", bins=[1000, 1012, 1023])
-    st, nk = _e2e(ctx, torch_cuda, oracle_lib, band, 20)
+    st, nk = _e2e(ctx, torch_cuda, oracle_lib, band, 20, dense=dense)
     assert nk.min() > 6000
-    assert st["gs_kernel"] != 0
+    assert st["gs_kernel"] == (2 if dense else 4)
 
 
-def test_e2e_cfg4_full_grid_n47(ctx, torch_cuda, oracle_lib):
+@pytest.mark.parametrize("dense", [False, True], ids=["residual", "dense_stream"])
+def test_e2e_cfg4_full_grid_n47(ctx, torch_cuda, oracle_lib, dense):
     """Full-grid mode on cfg4's array at n = 47 (S = 2209, T = 70 row blocks): three bins."""
     cfg = dataclasses.replace(synth.CONFIGS["cfg4"], n=47, n_bins=3)
     band = synth.make_band(cfg)
-    st, nk = _e2e(ctx, torch_cuda, oracle_lib, band, 30, full=True)
+    st, nk = _e2e(ctx, torch_cuda, oracle_lib, band, 30, full=True, dense=dense)
     assert np.all(nk == 47 * 47)
 
 
-def test_e2e_cfg4_full_grid_defining_size(ctx, torch_cuda, oracle_lib):
+@pytest.mark.parametrize("dense", [False, True], ids=["residual", "dense_stream"])
+def test_e2e_cfg4_full_grid_defining_size(ctx, torch_cuda, oracle_lib, dense):
     """Full-grid mode at cfg4's own size (n = 101, S = 10201, A~ 416 MB per bin): one bin of the
     band (8 kHz), 10 sweeps; the oracle builds the dense 10201 x 10201 PSF."""
     band = synth.make_band("cfg4", bins=[63])
-    st, nk = _e2e(ctx, torch_cuda, oracle_lib, band, 10, full=True)
+    st, nk = _e2e(ctx, torch_cuda, oracle_lib, band, 10, full=True, dense=dense)
     assert nk[0] == 10201
+    assert st["gs_kernel"] == (2 if dense else 4)

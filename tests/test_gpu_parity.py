@@ -197,10 +197,11 @@ def test_gs_identity_and_scalar(ctx, torch_cuda):
     assert x[0] == 0.75
 
 
-@pytest.mark.parametrize("nk,sweeps", [(2, 7), (31, 50), (32, 50), (33, 50), (97, 200), (300, 1000),
-                                       (447, 80), (448, 80), (640, 80), (831, 60), (832, 60), (1000, 100),
-                                       (1190, 60)])
-def test_gs_parity_on_oracle_system(ctx, torch_cuda, oracle_lib, nk, sweeps):
+@pytest.mark.parametrize("dense", [False, True], ids=["residual", "dense_stream"])
+@pytest.mark.parametrize("nk,sweeps", [(1, 5), (2, 7), (31, 50), (32, 50), (33, 50), (64, 40), (65, 40), (97, 200),
+                                       (300, 1000), (447, 80), (448, 80), (640, 80), (831, 60), (832, 60),
+                                       (1000, 100), (1190, 60)])
+def test_gs_parity_on_oracle_system(ctx, torch_cuda, oracle_lib, nk, sweeps, dense):
     """GS on the oracle's own A~ (rounded to fp32) and b~: ragged sizes around the 32-row
     block and multi-block systems, both sides of the CTAs-per-bin thresholds (g = 1 below 448
     kept points, 2 from 448, 4 from 832) and a g = 4 system whose T = 38 blocks end inside the
@@ -215,19 +216,24 @@ def test_gs_parity_on_oracle_system(ctx, torch_cuda, oracle_lib, nk, sweeps):
     A = oracle_lib.psf(*oracle_args(g), f, keep)
     bt = b[keep]
     ref = oracle_lib.gs(A, bt, sweeps)
-    x = ctx.gs(torch.from_numpy(A.astype(np.float32)).cuda(), torch.from_numpy(bt).cuda(), sweeps).cpu().numpy()
+    x = ctx.gs(torch.from_numpy(A.astype(np.float32)).cuda(), torch.from_numpy(bt).cuda(), sweeps,
+               dense_stream=dense).cpu().numpy()
+    assert ctx.stats()["gs_kernel"] == (1 if dense else 4) or (dense and ctx.stats()["gs_kernel"] == 2)
     assert x.min() >= 0
     assert rel_l2(x, ref) < TOL_X
     assert abs(x.sum() - ref.sum()) < TOL_P * ref.sum()
 
 
 # ---------------------------------------------------------------------------- end to end
-def _e2e(ctx, torch, oracle_lib, band, sweeps=None, full=False, check_b=True, order=1, dr=False, alt=False):
+def _e2e(ctx, torch, oracle_lib, band, sweeps=None, full=False, check_b=True, order=1, dr=False, alt=False,
+         dense=False):
     cfg = band.cfg
     g = geom_of(band)
     sw = sweeps or cfg.sweeps
     out = ctx.solve_band(g, band.freqs, torch.from_numpy(band.csm).cuda(), cfg.epsilon, sw, cfg.eps_mode,
-                         full_grid=full, want_b=True, order=order, dr=dr, alt=alt)
+                         full_grid=full, want_b=True, order=order, dr=dr, alt=alt, dense_stream=dense)
+    kern = ctx.stats()["gs_kernel"]
+    assert kern == (3 if alt else (4 if not dense else kern)) and kern != 0
     nk = out["n_keep"].cpu().numpy()
     keep = out["keep_idx"].cpu().numpy()
     x = out["x_map"].cpu().numpy()
@@ -243,14 +249,16 @@ def _e2e(ctx, torch, oracle_lib, band, sweeps=None, full=False, check_b=True, or
     return out
 
 
-def test_e2e_cfg1_compressed_and_full(ctx, torch_cuda, oracle_lib):
+@pytest.mark.parametrize("dense", [False, True], ids=["residual", "dense_stream"])
+def test_e2e_cfg1_compressed_and_full(ctx, torch_cuda, oracle_lib, dense):
     band = synth.make_band("cfg1")
-    _e2e(ctx, torch_cuda, oracle_lib, band)
-    _e2e(ctx, torch_cuda, oracle_lib, band, full=True)
+    _e2e(ctx, torch_cuda, oracle_lib, band, dense=dense)
+    _e2e(ctx, torch_cuda, oracle_lib, band, full=True, dense=dense)
 
 
-def test_e2e_cfg2_all_bins(ctx, torch_cuda, oracle_lib):
-    _e2e(ctx, torch_cuda, oracle_lib, synth.make_band("cfg2"))
+@pytest.mark.parametrize("dense", [False, True], ids=["residual", "dense_stream"])
+def test_e2e_cfg2_all_bins(ctx, torch_cuda, oracle_lib, dense):
+    _e2e(ctx, torch_cuda, oracle_lib, synth.make_band("cfg2"), dense=dense)
 
 
 def test_e2e_cfg2_cubic_predictor(ctx, torch_cuda, oracle_lib):
@@ -258,18 +266,20 @@ def test_e2e_cfg2_cubic_predictor(ctx, torch_cuda, oracle_lib):
     _e2e(ctx, torch_cuda, oracle_lib, synth.make_band("cfg2"), order=3)
 
 
-def test_e2e_cfg3_strided_bins(ctx, torch_cuda, oracle_lib):
+@pytest.mark.parametrize("dense", [False, True], ids=["residual", "dense_stream"])
+def test_e2e_cfg3_strided_bins(ctx, torch_cuda, oracle_lib, dense):
     band = synth.make_band("cfg3", bins=synth.strided_bins(256, 6))
-    _e2e(ctx, torch_cuda, oracle_lib, band)
+    _e2e(ctx, torch_cuda, oracle_lib, band, dense=dense)
 
 
-def test_e2e_full_grid_m128(ctx, torch_cuda, oracle_lib):
+@pytest.mark.parametrize("dense", [False, True], ids=["residual", "dense_stream"])
+def test_e2e_full_grid_m128(ctx, torch_cuda, oracle_lib, dense):
     """Full-grid mode (cfg4's 128-mic array, exact CSM) on a 31x31 grid the oracle can
     build the dense S x S PSF for; several 32-row blocks and a ragged tail (961 = 30*32+1)."""
     import dataclasses
     cfg = dataclasses.replace(synth.CONFIGS["cfg4"], n=31, n_bins=3)
     band = synth.make_band(cfg)
-    _e2e(ctx, torch_cuda, oracle_lib, band, sweeps=60, full=True)
+    _e2e(ctx, torch_cuda, oracle_lib, band, sweeps=60, full=True, dense=dense)
 
 
 def test_e2e_cfg5_strided_bins_few_sweeps(ctx, torch_cuda, oracle_lib):
@@ -278,14 +288,16 @@ def test_e2e_cfg5_strided_bins_few_sweeps(ctx, torch_cuda, oracle_lib):
     _e2e(ctx, torch_cuda, oracle_lib, band, sweeps=20)
 
 
-def test_full_size_cfg3_sampled(ctx, torch_cuda, oracle_lib):
+@pytest.mark.parametrize("dense", [False, True], ids=["residual", "dense_stream"])
+def test_full_size_cfg3_sampled(ctx, torch_cuda, oracle_lib, dense):
     """BASELINE configs[2] at full size in the bench's launch configuration (all 256 bins in
     one call); the oracle recomputes a strided sample of 8 bins one by one."""
     torch = torch_cuda
     cfg = synth.CONFIGS["cfg3"]
     band = synth.make_band(cfg)
     g = geom_of(band)
-    out = ctx.solve_band(g, band.freqs, torch.from_numpy(band.csm).cuda(), cfg.epsilon, cfg.sweeps)
+    out = ctx.solve_band(g, band.freqs, torch.from_numpy(band.csm).cuda(), cfg.epsilon, cfg.sweeps,
+                         dense_stream=dense)
     nk = out["n_keep"].cpu().numpy()
     keep = out["keep_idx"].cpu().numpy()
     x = out["x_map"].cpu().numpy()
@@ -469,7 +481,7 @@ def test_errors_flags_and_new_entry_points(ctx, torch_cuda):
     keep = torch.empty((1, g.S), dtype=torch.int32, device="cuda")
     x = torch.empty((1, g.S), dtype=torch.float32, device="cuda")
     f = np.array(band.freqs, dtype=np.float64)
-    prm = Params(0.1, 0, 5, 16)   # unknown flag bit
+    prm = Params(0.1, 0, 5, 64)   # unknown flag bit
     rc = lib().dwc_solve_band(ctx._h, C.byref(arr), C.byref(grid), C.byref(prm), 1, f.ctypes.data,
                               csm.data_ptr(), nk.data_ptr(), keep.data_ptr(), x.data_ptr(), None, None,
                               torch.cuda.current_stream().cuda_stream)
@@ -542,7 +554,8 @@ def test_absolute_threshold_mode_matches_relative(ctx, torch_cuda):
 
 
 @pytest.mark.gpu
-def test_batched_path_bitwise_deterministic_cfg3():
+@pytest.mark.parametrize("dense", [False, True], ids=["residual", "dense_stream"])
+def test_batched_path_bitwise_deterministic_cfg3(dense):
     """The whole 256-bin cfg3 band, three calls: every map bit-identical (all summation orders are
     fixed, so any difference is a race -- this test caught one in the GS solver's staging)."""
     import torch
@@ -554,7 +567,7 @@ def test_batched_path_bitwise_deterministic_cfg3():
     csm = torch.from_numpy(band.csm).cuda()
     ref = None
     for _ in range(3):
-        x = ctx.solve_band(g, band.freqs, csm, cfg.epsilon, 300, cfg.eps_mode)["x_map"].cpu().numpy()
+        x = ctx.solve_band(g, band.freqs, csm, cfg.epsilon, 300, cfg.eps_mode, dense_stream=dense)["x_map"].cpu().numpy()
         if ref is None:
             ref = x
         else:
