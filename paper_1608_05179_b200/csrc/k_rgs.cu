@@ -60,7 +60,7 @@ constexpr int kRStg = 5;             // panel staging depth (steps)
 constexpr int kNP = 8;               // panels staged per step (predicted rows beyond: loaded on demand)
 constexpr int kPW = (kRgsWin + 1) * 32;   // panel floats: blocks k..k+W of one row
 constexpr int kNList = 16;           // change-list ring (steps; > kRgsWin + 1)
-constexpr int kCP = 3;               // stream: chunks held in registers per pass
+constexpr int kCP = 2;               // stream: chunks held in registers per pass
 
 struct __align__(16) RgsEntry {
     float xn, xo;   // x of the row after / before the change (dx = xn - xo, exact in fp64)
@@ -424,7 +424,11 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
             for (int s = 0, k = 0; s < total; s++, k = (k + 1 == T) ? 0 : k + 1) {
                 const int li = s % kNList;
                 const unsigned long long t0 = pf ? clk() : 0ull;
-                mbar_wait(&sh.dready[li], (s / kNList) & 1);
+                // the row producer arrives dxready after it observed the solver's dready (the list
+                // and its dx are then visible); waiting on it every step, also without changes, keeps
+                // the row producer within kNList steps of the solver (which runs at most nsub + 1
+                // steps ahead of the stream)
+                mbar_wait(&sh.dxready[li], (s / kNList) & 1);
                 if (pf) tlw += clk() - t0;
                 const int n = sh.cnt[li];
                 const int nu = n * rg.nseg;
@@ -441,9 +445,6 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                     pp[0] = make_double2(0.0, 0.0);
                     pp[1] = make_double2(0.0, 0.0);
                 }
-                // every step, also without changes: it keeps the row producer within kNList steps
-                // of the solver (the solver runs at most nsub + 1 steps ahead of the stream)
-                mbar_wait(&sh.dxready[li], (s / kNList) & 1);
                 for (int u0 = 0; u0 < nu; u0 += rg.upb, b++) {
                     const int h = b & 1;
                     const unsigned long long t1 = pf ? clk() : 0ull;
