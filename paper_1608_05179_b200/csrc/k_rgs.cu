@@ -61,6 +61,7 @@ constexpr int kNP = 8;               // panels staged per step (predicted rows b
 constexpr int kPW = (kRgsWin + 1) * 32;   // panel floats: blocks k..k+W of one row
 constexpr int kNList = 16;           // change-list ring (steps; > kRgsWin + 1)
 constexpr int kCP = 2;               // stream: chunks held in registers per pass
+constexpr int kNSlot = 6;            // row ring: batches in flight
 
 struct __align__(16) RgsEntry {
     float xn, xo;   // x of the row after / before the change (dx = xn - xo, exact in fp64)
@@ -77,7 +78,7 @@ struct __align__(128) RgsSmem {
     int cnt[kNList];
     unsigned long long stg_full[kRStg], stg_empty[kRStg];
     unsigned long long dready[kNList], sdone[kNList], dxready[kNList];
-    unsigned long long rfull[2], rempty[2];   // row ring halves
+    unsigned long long rfull[kNSlot], rempty[kNSlot];   // row ring slots
     int item;
 };
 
@@ -147,19 +148,19 @@ __device__ __forceinline__ unsigned long long clk() {
 
 // Row-ring batching, identical in the row producer and the stream warps: the changes of a step
 // are cut into units (row e, segment g) of seg floats (the last segment of a row shorter); one
-// batch = up to upb units = one ring half.
+// batch = up to upb units = one ring slot.
 struct RingGeom {
     int seg;    // floats per unit slot (sp, or a multiple of 128 when rows are cut)
     int nseg;   // segments per row
     int upb;    // units per batch
 };
-__device__ __forceinline__ RingGeom ring_geom(int sp, int half_floats) {
+__device__ __forceinline__ RingGeom ring_geom(int sp, int slot_floats) {
     RingGeom g;
-    // whole rows when a row fits a half (slots of sp floats, 128-byte aligned), else segments
+    // whole rows when a row fits a slot (units of sp floats, 128-byte aligned), else segments
     // that start on 128-column chunk boundaries
-    g.seg = (sp <= half_floats) ? sp : (half_floats / 128) * 128;
+    g.seg = (sp <= slot_floats) ? sp : (slot_floats / 128) * 128;
     g.nseg = (sp + g.seg - 1) / g.seg;
-    g.upb = half_floats / g.seg;
+    g.upb = slot_floats / g.seg;
     return g;
 }
 
@@ -172,11 +173,11 @@ constexpr int kProfSlots = 16;
 constexpr int kProfItems = 1024;   // then per item: start, end (globaltimer ns), bin, changes
 
 // r (fp64, sp), x (fp32, sp), 1/A_ii (fp32, sp), the prediction masks (T words) and the row
-// ring (2 halves of half_floats) follow RgsSmem.
+// ring (kNSlot slots of slot_floats) follow RgsSmem.
 __global__ void __launch_bounds__(kRThreads, 2)
 rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restrict__ lay, int *__restrict__ counter,
            const float *__restrict__ Adense, const double *__restrict__ bt, int sweeps, float *__restrict__ x_out,
-           float *__restrict__ x_map, const int32_t *__restrict__ keep_idx, int S, int max_sp, int half_floats,
+           float *__restrict__ x_map, const int32_t *__restrict__ keep_idx, int S, int max_sp, int slot_floats,
            unsigned long long *__restrict__ n_updates, unsigned long long *__restrict__ prof) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     RgsSmem &sh = *reinterpret_cast<RgsSmem *>(smem_raw);
@@ -229,14 +230,14 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 mbar_init(&sh.sdone[i], kNStream);
                 mbar_init(&sh.dxready[i], 1);
             }
-            for (int h = 0; h < 2; h++) {
+            for (int h = 0; h < kNSlot; h++) {
                 mbar_init(&sh.rfull[h], 1);
                 mbar_init(&sh.rempty[h], kNStream);
             }
             fence_mbar_init();
         }
         __syncthreads();
-        const RingGeom rg = ring_geom(sp, half_floats);
+        const RingGeom rg = ring_geom(sp, slot_floats);
 
         if (wid == kWPanel) {
             // ================= panel producer: the panels of the rows predicted to change, as
@@ -284,7 +285,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
             // ================= row producer: the exact dx of every change (all lanes), then the rows
             // of every step's changes into the ring (lane 0)
             unsigned long long tw = 0, ti = 0;
-            int b = 0;   // global batch counter (ring half = b & 1)
+            int b = 0;   // global batch counter (ring slot = b % kNSlot)
             for (int s = 0; s < total; s++) {
                 const int li = s % kNList;
                 mbar_wait(&sh.dready[li], (s / kNList) & 1);
@@ -295,12 +296,12 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                     mbar_arrive(&sh.dxready[li]);
                     const int nu = n * rg.nseg;
                     for (int u0 = 0; u0 < nu; u0 += rg.upb, b++) {
-                        const int h = b & 1;
+                        const int h = b % kNSlot;
                         const unsigned long long t0 = pf ? clk() : 0ull;
-                        mbar_wait(&sh.rempty[h], ((b >> 1) & 1) ^ 1);
+                        mbar_wait(&sh.rempty[h], ((b / kNSlot) & 1) ^ 1);
                         const unsigned long long t1 = pf ? clk() : 0ull;
                         const int nb = min(rg.upb, nu - u0);
-                        float *dst = ring + (size_t)h * half_floats;
+                        float *dst = ring + (size_t)h * slot_floats;
                         if (rg.nseg == 1) {
                             mbar_expect_tx(&sh.rfull[h], (uint32_t)nb * sp * 4);
                             for (int j = 0; j < nb; j++)
@@ -446,12 +447,12 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                     pp[1] = make_double2(0.0, 0.0);
                 }
                 for (int u0 = 0; u0 < nu; u0 += rg.upb, b++) {
-                    const int h = b & 1;
+                    const int h = b % kNSlot;
                     const unsigned long long t1 = pf ? clk() : 0ull;
-                    mbar_wait(&sh.rfull[h], (b >> 1) & 1);
+                    mbar_wait(&sh.rfull[h], (b / kNSlot) & 1);
                     const unsigned long long t2 = pf ? clk() : 0ull;
                     const int nb = min(rg.upb, nu - u0);
-                    const float *src = ring + (size_t)h * half_floats;
+                    const float *src = ring + (size_t)h * slot_floats;
                     // the warp's chunks of each segment, kCP at a time: their r in registers while
                     // every unit of that segment is applied (independent DFMA chains per chunk)
                     for (int g = 0; g < rg.nseg; g++) {
@@ -540,7 +541,7 @@ size_t rgs_base_bytes(int max_sp) { return sizeof(RgsSmem) + (size_t)max_sp * (8
 }  // namespace
 
 // The minimum ring (two halves of 128 floats); launch_rgs gives it what shared memory allows.
-size_t rgs_smem_bytes(int max_sp) { return rgs_base_bytes(max_sp) + 2 * 128 * 4 + 512; }
+size_t rgs_smem_bytes(int max_sp) { return rgs_base_bytes(max_sp) + kNSlot * 128 * 4 + 512; }
 
 
 int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int max_sp, int *counter,
@@ -555,17 +556,17 @@ int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int m
     static const int per_sm_env = getenv("DWC_RGS_PER_SM") ? atoi(getenv("DWC_RGS_PER_SM")) : 0;   // experiment
     const size_t per2 = 114 * 1024 - 1024;
     size_t ring;
-    // two per SM when the band has more bins than SMs and a ring half still holds 4 rows
+    // two per SM when the band has more bins than SMs and every ring slot still holds 2 rows
     const bool two = per_sm_env ? per_sm_env == 2 && per2 > base + 2048
-                                : n_bins > num_sms && per2 > base && (per2 - base) / 8 >= 4 * (size_t)max_sp;
+                                : n_bins > num_sms && per2 > base && (per2 - base) / (4 * kNSlot) >= 2 * (size_t)max_sp;
     if (two)
         ring = (per2 - base - 512) / 1024 * 1024;
     else
         ring = (227 * 1024 - base - 512) / 1024 * 1024;
     if (ring_env > 0 && (size_t)ring_env * 1024 < ring) ring = (size_t)ring_env * 1024;
-    const int half_floats = (int)(ring / 8) / 128 * 128;   // floats per half (ring bytes / 2 / 4)
-    if (half_floats < 128) return -1;
-    const size_t smem = base + (size_t)half_floats * 8 + 512;   // + slack: a row's last chunk reads past it
+    const int slot_floats = (int)(ring / (4 * kNSlot)) / 128 * 128;   // floats per ring slot
+    if (slot_floats < 128) return -1;
+    const size_t smem = base + (size_t)slot_floats * 4 * kNSlot + 512;   // + slack: a row's last chunk reads past it
     if (cudaFuncSetAttribute(rgs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return -1;
     int per_sm = 0;
@@ -593,7 +594,7 @@ int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int m
         cudaMemsetAsync(prof, 0, pb, st);
     }
     rgs_kernel<<<grid, kRThreads, smem, st>>>(n_bins, order_dev, lay_dev, counter, Adense, bt, sweeps, x_out, x_map,
-                                              keep_idx, S, max_sp, half_floats, n_updates, prof);
+                                              keep_idx, S, max_sp, slot_floats, n_updates, prof);
     const cudaError_t e = cudaPeekAtLastError();
     if (profile) {
         static unsigned long long h[kProfSlots + 4 * kProfItems + 2];
@@ -615,10 +616,10 @@ int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int m
         }
         const double n = h[4] ? (double)h[4] : 1.0;
         fprintf(stderr,
-                "[rgs-prof] grid %d x %zu B smem (ring 2 x %d floats), steps %llu, changes %llu (%.2f/step), item %.0f cyc"
+                "[rgs-prof] grid %d x %zu B smem (ring 6 x %d floats), steps %llu, changes %llu (%.2f/step), item %.0f cyc"
                 " | solver cyc/step: tiles %.0f stream %.0f loop %.0f rest %.0f | stream0: list %.0f batch %.0f apply %.0f"
                 " (%llu batches) | rowprod: ring wait %.0f issue %.0f | panel misses %llu | panelprod wait %.0f issue %.0f\n",
-                grid, smem, half_floats, h[4], h[5], h[5] / n, (double)h[14], h[0] / n, h[1] / n, h[2] / n, h[3] / n,
+                grid, smem, slot_floats, h[4], h[5], h[5] / n, (double)h[14], h[0] / n, h[1] / n, h[2] / n, h[3] / n,
                 h[8] / n, h[9] / n, h[10] / n, h[11], h[12] / n, h[13] / n, h[6], h[7] / n, h[15] / n);
         cudaFree(prof);
     }
