@@ -56,12 +56,24 @@ constexpr int kNStream = 5;          // stream warps 0..3 and 7
 // warp roles: the latency-critical warps take the higher warp of each SMSP pair (w, w+4): the
 // issue arbiter prefers the higher warp id
 constexpr int kWSolver = 4, kWPanel = 5, kWRows = 6;
-constexpr int kRStg = 5;             // panel staging depth (steps)
-constexpr int kNP = 8;               // panels staged per step (predicted rows beyond: loaded on demand)
+#ifndef RGS_STG
+#define RGS_STG 5
+#endif
+#ifndef RGS_NP
+#define RGS_NP 8
+#endif
+#ifndef RGS_NLIST
+#define RGS_NLIST 16
+#endif
+#ifndef RGS_NSLOT
+#define RGS_NSLOT 6
+#endif
+constexpr int kRStg = RGS_STG;       // panel staging depth (steps)
+constexpr int kNP = RGS_NP;          // panels staged per step (predicted rows beyond: loaded on demand)
 constexpr int kPW = (kRgsWin + 1) * 32;   // panel floats: blocks k..k+W of one row
-constexpr int kNList = 16;           // change-list ring (steps; > kRgsWin + 1)
+constexpr int kNList = RGS_NLIST;    // change-list ring (steps; > kRgsWin + 2)
 constexpr int kCP = 2;               // stream: chunks held in registers per pass
-constexpr int kNSlot = 6;            // row ring: batches in flight
+constexpr int kNSlot = RGS_NSLOT;    // row ring: batches in flight
 
 struct __align__(16) RgsEntry {
     float xn, xo;   // x of the row after / before the change (dx = xn - xo, exact in fp64)
