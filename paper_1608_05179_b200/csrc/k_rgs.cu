@@ -71,6 +71,15 @@ constexpr int kWSolver = 4, kWPanel = 5, kWRows = 6;
 constexpr int kRStg = RGS_STG;       // panel staging depth (steps)
 constexpr int kNP = RGS_NP;          // panels staged per step (predicted rows beyond: loaded on demand)
 constexpr int kPW = (kRgsWin + 1) * 32;   // panel floats: blocks k..k+W of one row
+// pending-buffer slots: the contributions to a block wait in the slot of the step that will read
+// it, (step mod 16).  At stream step s the pending visits are those of steps s .. s + nsub; a slot is
+// written for the visit at step S + 16 from stream step S + 16 - nsub >= S + 9 on, and the stream
+// warps are at most nsub steps apart (the solver of step s waited for all of them to finish step
+// s - nsub - 1), so a slot is never written for its next visit before the owner warp of the
+// previous visit's block has committed it.
+constexpr int kPendBlk = 16;
+constexpr int kPendF = kPendBlk * 32;
+static_assert(kRgsWin == 7, "pending-slot reuse distance assumes a 7-block carry window");
 constexpr int kNList = RGS_NLIST;    // change-list ring (steps; > kRgsWin + 2)
 constexpr int kCP = 2;               // stream: chunks held in registers per pass
 constexpr int kNSlot = RGS_NSLOT;    // row ring: batches in flight
@@ -85,6 +94,7 @@ __device__ __forceinline__ double entry_dx(const RgsEntry &e) { return (double)e
 struct __align__(128) RgsSmem {
     float panel[kRStg][kNP][kPW];     // staged panels (ascending row), element m = column 32k + m (mod sp)
     unsigned smask[kRStg];            // rows (bits) whose panels a stage holds
+    float sinv[kRStg][32];            // 1/A_ii of the stage's block (0 for padding rows)
     RgsEntry list[kNList][32];
     double dxs[kNList][32];           // dx of each listed change (written by the row producer)
     int cnt[kNList];
@@ -184,20 +194,23 @@ __device__ __forceinline__ RingGeom ring_geom(int sp, int slot_floats) {
 constexpr int kProfSlots = 16;
 constexpr int kProfItems = 1024;   // then per item: start, end (globaltimer ns), bin, changes
 
-// r (fp64, sp), x (fp32, sp), 1/A_ii (fp32, sp), the prediction masks (T words) and the row
-// ring (kNSlot slots of slot_floats) follow RgsSmem.
+// r (fp64, sp), the pending carried contributions (fp64, 16 blocks), x (fp32, sp), the prediction
+// masks (T words) and the row ring (kNSlot slots of slot_floats) follow RgsSmem.
 __global__ void __launch_bounds__(kRThreads, 2)
 rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restrict__ lay, int *__restrict__ counter,
            const float *__restrict__ Adense, const double *__restrict__ bt, int sweeps, float *__restrict__ x_out,
            float *__restrict__ x_map, const int32_t *__restrict__ keep_idx, int S, int max_sp, int slot_floats,
+           int use_ivs,
            unsigned long long *__restrict__ n_updates, unsigned long long *__restrict__ prof) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     RgsSmem &sh = *reinterpret_cast<RgsSmem *>(smem_raw);
     double *rs = reinterpret_cast<double *>(smem_raw + sizeof(RgsSmem));
-    double *pend = rs + max_sp;                                 // carried contributions not yet in r
-    float *xs = reinterpret_cast<float *>(pend + max_sp);
-    float *ivs = xs + max_sp;                                   // 1/A_ii
-    unsigned *pmask = reinterpret_cast<unsigned *>(ivs + max_sp);   // per block: rows predicted to change
+    // carried contributions not yet in r (the visit at step S in slot S mod kPendBlk)
+    double *pend = rs + max_sp;
+    float *xs = reinterpret_cast<float *>(pend + kPendF);
+    // 1/A_ii of every row when shared memory allows (use_ivs), else per stage from the panel producer
+    float *ivs = xs + max_sp;
+    unsigned *pmask = reinterpret_cast<unsigned *>(ivs + (use_ivs ? max_sp : 0));   // per block: rows predicted to change
     float *ring = reinterpret_cast<float *>(pmask + ((max_sp / 32 + 31) & ~31));   // 128-byte aligned
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     unsigned long long my_updates = 0;
@@ -224,14 +237,13 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
         for (int i = tid; i < sp; i += kRThreads) {
             const double b = bt[L.v_off + i];
             rs[i] = -b;   // r = A x0 - b with x0 = 0 (b~ zero padded)
-            pend[i] = 0.0;
             xs[i] = 0.f;
-            // 1/A_ii as the dense-stream kernel forms it; padding rows never change
-            ivs[i] = (i < nk) ? __frcp_rn(Ad[(size_t)i * sp + i]) : 0.f;
+            if (use_ivs) ivs[i] = (i < nk) ? __frcp_rn(Ad[(size_t)i * sp + i]) : 0.f;
             // sweep 1 from x0 = 0 changes exactly the rows with b~ > 0
             const unsigned m = __ballot_sync(0xffffffffu, i < nk && b > 0.0);
             if ((i & 31) == 0) pmask[i >> 5] = m;
         }
+        for (int i = tid; i < kPendF; i += kRThreads) pend[i] = 0.0;
         if (tid == 0) {
             for (int i = 0; i < kRStg; i++) {
                 mbar_init(&sh.stg_full[i], 33);   // 32 cp.async arrivals + the mask publisher
@@ -256,6 +268,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
             // 16-byte cp.async copies spread over the warp's lanes (a 1 KB panel is 2 instructions;
             // one bulk copy per panel cost ~80 cycles of issue on a single lane)
             unsigned long long pw_wait = 0, pw_issue = 0;
+            float dnext = (!use_ivs && lane < nk) ? __ldg(Ad + (size_t)lane * sp + lane) : 1.f;
             for (int s = 0, k = 0; s < total; s++, k = (k + 1 == T) ? 0 : k + 1) {
                 const int sl = s % kRStg;
                 const unsigned long long t0 = pf ? clk() : 0ull;
@@ -283,9 +296,18 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                                      : "memory");
                     }
                 }
+                // 1/A_ii of the block's rows, as the dense-stream kernel forms it (padding rows: 0);
+                // the diagonal of the next block is loaded one step ahead
+                if (!use_ivs) {
+                    const int rw = c0 + lane;
+                    sh.sinv[sl][lane] = (rw < nk) ? __frcp_rn(dnext) : 0.f;
+                    const int rn = (k + 1 == T) ? lane : rw + 32;
+                    dnext = (rn < nk) ? __ldg(Ad + (size_t)rn * sp + rn) : 1.f;
+                }
                 // each lane's copies complete on stg_full (32 async arrivals + lane 0's below)
                 asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&sh.stg_full[sl]))
                              : "memory");
+                __syncwarp();
                 if (lane == 0) {
                     sh.smask[sl] = st;
                     mbar_arrive(&sh.stg_full[sl]);
@@ -351,10 +373,10 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 const unsigned long long t0 = pf ? clk() : 0ull;
                 const int sl = s % kRStg, li = s % kNList;
                 const int row = 32 * k + lane;
-                const float invd = ivs[row];
                 float xo = xs[row];
                 mbar_wait(&sh.stg_full[sl], (s / kRStg) & 1);
                 const unsigned smk = sh.smask[sl];
+                const float invd = use_ivs ? ivs[row] : sh.sinv[sl][lane];
                 // this lane's panel slot (its rank among the staged rows), -1 if not staged
                 const int myp = ((smk >> lane) & 1u) ? __popc(smk & ((1u << lane) - 1u)) : -1;
                 const unsigned long long t1 = pf ? clk() : 0ull;
@@ -450,7 +472,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 if ((((k >> 2) % kNStream) == w) && (lane >> 3) == (k & 3)) {
                     const int col = 32 * k + 4 * (lane & 7);
                     double2 *rp = reinterpret_cast<double2 *>(rs + col);
-                    double2 *pp = reinterpret_cast<double2 *>(pend + col);
+                    double2 *pp = reinterpret_cast<double2 *>(pend + 32 * (s & (kPendBlk - 1)) + 4 * (lane & 7));
                     double2 r0 = rp[0], r1 = rp[1];
                     const double2 p0 = pp[0], p1 = pp[1];
                     r0.x += p0.x; r0.y += p0.y; r1.x += p1.x; r1.y += p1.y;
@@ -482,11 +504,12 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
 #pragma unroll
                             for (int i = 0; i < kCP; i++) {
                                 const int qq = qp + i * kNStream, col = 128 * qq + 4 * lane;
-                                int o = (col >> 5) - k;   // block offset from k: 1..nsub are carried
-                                if (o < 0) o += T;
                                 on[i] = qq < q1 && col < sp;
                                 cc[i] = (qq < q1) ? 128 * qq : 128 * qp;   // a chunk of this segment
-                                tg[i] = ((o >= 1 && o <= nsub) ? pend : rs) + cc[i] + 4 * lane;
+                                const int ce = cc[i] + 4 * lane, blk = ce >> 5;
+                                int o = blk - k;   // block offset from k: 1..nsub are carried
+                                if (o < 0) o += T;
+                                tg[i] = (o >= 1 && o <= nsub) ? pend + 32 * ((s + o) & (kPendBlk - 1)) + (ce & 31) : rs + ce;
                                 const double2 *rp = reinterpret_cast<const double2 *>(tg[i]);
                                 ra[i] = rp[0];
                                 rb[i] = rp[1];
@@ -549,7 +572,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
 }
 
 namespace {
-size_t rgs_base_bytes(int max_sp) { return sizeof(RgsSmem) + (size_t)max_sp * (8 + 8 + 4 + 4) + (((size_t)max_sp / 32 + 31) & ~(size_t)31) * 4; }
+size_t rgs_base_bytes(int max_sp) { return sizeof(RgsSmem) + kPendF * 8 + (size_t)max_sp * (8 + 4) + (((size_t)max_sp / 32 + 31) & ~(size_t)31) * 4; }
 }  // namespace
 
 // The minimum ring (two halves of 128 floats); launch_rgs gives it what shared memory allows.
@@ -560,7 +583,9 @@ int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int m
                const float *Adense, const double *bt, int sweeps, float *x_out, float *x_map,
                const int32_t *keep_idx, int S, int num_sms, unsigned long long *n_updates, cudaStream_t st,
                GsLaunchInfo *info) {
-    const size_t base = (rgs_base_bytes(max_sp) + 127) / 128 * 128;
+    // 1/A_ii in shared memory for the whole system when a ring of >= 24 KB still fits beside it
+    const int use_ivs = (rgs_base_bytes(max_sp) + (size_t)max_sp * 4 + 24 * 1024 + 1536 <= 227 * 1024) ? 1 : 0;
+    const size_t base = (rgs_base_bytes(max_sp) + (use_ivs ? (size_t)max_sp * 4 : 0) + 127) / 128 * 128;
     if (base + 1536 > 227 * 1024) return -1;
     // two CTAs per SM (2 x (smem + 1 KB reserved) <= 228 KB) when the band has the bins for it
     // and the ring still holds a row; else one CTA per SM with the rest of the 227 KB as ring
@@ -606,7 +631,7 @@ int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int m
         cudaMemsetAsync(prof, 0, pb, st);
     }
     rgs_kernel<<<grid, kRThreads, smem, st>>>(n_bins, order_dev, lay_dev, counter, Adense, bt, sweeps, x_out, x_map,
-                                              keep_idx, S, max_sp, slot_floats, n_updates, prof);
+                                              keep_idx, S, max_sp, slot_floats, use_ivs, n_updates, prof);
     const cudaError_t e = cudaPeekAtLastError();
     if (profile) {
         static unsigned long long h[kProfSlots + 4 * kProfItems + 2];
