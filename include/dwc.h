@@ -99,12 +99,17 @@ typedef struct {
  * R21): sweep 2p in ascending row order (Eq. 13-14), sweep 2p+1 descending.  Runs a simpler
  * one-CTA-per-bin kernel (a fidelity-study variant, not the tuned path). */
 #define DWC_ALT_SWEEPS 8
-/* DWC_GS_DENSE_STREAM: run the forward sweeps on the dense-stream cluster kernel (every row dot
- * recomputed from the symmetric-packed A~ streamed through shared memory, up to 4 CTAs per bin)
- * instead of the default residual-update kernel (the residual r = A x - b kept on chip in fp64,
- * updated by the rows of A~ whose x changed).  Both keep Eq. 13-14's row and sweep order; they
- * differ in summation order only. */
+/* Gauss-Seidel kernel of the forward sweeps (both keep Eq. 13-14's row and sweep order exactly and
+ * differ in summation order only):
+ *  - residual-update kernel: the residual r = A x - b of the current iterate kept on chip in fp64,
+ *    updated with the row of A~ of every x that changes (one CTA per bin);
+ *  - dense-stream cluster kernel: every row dot recomputed from the symmetric-packed A~ streamed
+ *    through shared memory (up to 4 CTAs per bin).
+ * Default: the residual kernel when the band's largest compressed system has at most 2048 points
+ * (padded to 32), else the dense-stream kernel.  DWC_GS_DENSE_STREAM / DWC_GS_RESIDUAL force one
+ * (setting both is DWC_EINVAL).  dwc_stats.gs_kernel reports which ran. */
 #define DWC_GS_DENSE_STREAM 16
+#define DWC_GS_RESIDUAL 32
 #define DWC_MAX_MICS 512
 
 /* Create / destroy a context on CUDA device `device`.  The device must be sm_100

@@ -186,8 +186,10 @@ dwc_status check_params(const dwc_params *p) {
     if (!(p->epsilon > 0.0) || !finite(p->epsilon)) return fail(DWC_EINVAL, "epsilon must be > 0");
     if (p->eps_mode != 0 && p->eps_mode != 1) return fail(DWC_EINVAL, "eps_mode must be 0 or 1");
     if (p->sweeps < 1) return fail(DWC_EINVAL, "sweeps must be >= 1");
-    if (p->flags & ~(DWC_FULL_GRID | DWC_CUBIC | DWC_DIAG_REMOVAL | DWC_ALT_SWEEPS | DWC_GS_DENSE_STREAM))
+    if (p->flags & ~(DWC_FULL_GRID | DWC_CUBIC | DWC_DIAG_REMOVAL | DWC_ALT_SWEEPS | DWC_GS_DENSE_STREAM | DWC_GS_RESIDUAL))
         return fail(DWC_EINVAL, "unknown flags 0x%x", p->flags);
+    if ((p->flags & DWC_GS_DENSE_STREAM) && (p->flags & DWC_GS_RESIDUAL))
+        return fail(DWC_EINVAL, "DWC_GS_DENSE_STREAM and DWC_GS_RESIDUAL exclude each other");
     return DWC_OK;
 }
 
@@ -325,8 +327,14 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
     }
     // host layout of the compressed systems
     std::vector<BinLayout> lay(n_bins);
-    // the residual kernel runs every forward-sweep band unless the dense-stream kernel is asked for
-    const bool resid = !(p->flags & (DWC_ALT_SWEEPS | DWC_GS_DENSE_STREAM));
+    // GS kernel of the band (forward sweeps): DWC_GS_RESIDUAL / DWC_GS_DENSE_STREAM force one, else
+    // the residual kernel when the band's largest system is at most rgs_auto_max_sp() points (one
+    // SM streams a residual bin's changed rows; the dense-stream kernel spreads a large bin's
+    // stream over 4 SMs)
+    int band_sp = 0;
+    for (int k = 0; k < n_bins; k++) band_sp = std::max(band_sp, (hk[k] + 31) & ~31);
+    const bool resid = !(p->flags & DWC_ALT_SWEEPS) &&
+                       ((p->flags & DWC_GS_RESIDUAL) || (!(p->flags & DWC_GS_DENSE_STREAM) && band_sp <= rgs_auto_max_sp()));
     int64_t a_off = 0, v_off = 0, r_off = 0, d_off = 0;
     int max_sp = 0, max_rp = 0, ystride = 0;
     double sum_sq = 0.0, sum_sym = 0.0;
@@ -697,9 +705,13 @@ dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int3
     if (n < 1) return fail(DWC_EINVAL, "n must be >= 1");
     if (sweeps < 1) return fail(DWC_EINVAL, "sweeps must be >= 1");
     if (!A || !b || !x) return fail(DWC_EINVAL, "NULL device buffer");
-    if (flags & ~(DWC_ALT_SWEEPS | DWC_GS_DENSE_STREAM)) return fail(DWC_EINVAL, "unknown flags 0x%x", flags);
-    const bool resid = !(flags & (DWC_ALT_SWEEPS | DWC_GS_DENSE_STREAM));
+    if (flags & ~(DWC_ALT_SWEEPS | DWC_GS_DENSE_STREAM | DWC_GS_RESIDUAL))
+        return fail(DWC_EINVAL, "unknown flags 0x%x", flags);
+    if ((flags & DWC_GS_DENSE_STREAM) && (flags & DWC_GS_RESIDUAL))
+        return fail(DWC_EINVAL, "DWC_GS_DENSE_STREAM and DWC_GS_RESIDUAL exclude each other");
     const int sp = (n + 31) & ~31;
+    const bool resid = !(flags & DWC_ALT_SWEEPS) &&
+                       ((flags & DWC_GS_RESIDUAL) || (!(flags & DWC_GS_DENSE_STREAM) && sp <= rgs_auto_max_sp()));
     if (resid ? rgs_smem_bytes(sp) > 227 * 1024 : gs_smem_bytes(sp, gs_ystride(n)) > 227 * 1024)
         return fail(DWC_EINVAL, "n = %d exceeds the on-chip x capacity", n);
     cudaStream_t st = (cudaStream_t)cuda_stream;

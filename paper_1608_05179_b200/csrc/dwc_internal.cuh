@@ -257,6 +257,8 @@ int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_s
 // (LPT); A~ as written by launch_psf with Adense; bt = b~ (fp64, zero padded to sp);
 // n_updates (dev, nullable) += the number of row updates (x changes) over all sweeps.
 size_t rgs_smem_bytes(int max_sp);
+// largest padded system the automatic kernel choice gives the residual kernel (DWC_RGS_AUTO_MAX_SP overrides)
+int rgs_auto_max_sp();
 int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int max_sp, int *counter,
                const float *Adense, const double *bt, int sweeps, float *x_out, float *x_map,
                const int32_t *keep_idx, int S, int num_sms, unsigned long long *n_updates, cudaStream_t st,

@@ -576,6 +576,14 @@ size_t rgs_base_bytes(int max_sp) { return sizeof(RgsSmem) + kPendF * 8 + (size_
 }  // namespace
 
 // The minimum ring (two halves of 128 floats); launch_rgs gives it what shared memory allows.
+// Measured (cfg3 S~ <= 1184: residual band GS 30 ms vs 45 dense-stream; cfg2 full grid S = 6561:
+// 805 vs 590 ms; cfg4/cfg5 (S~ up to 10201): 1.6-2.8x slower on the residual kernel): one SM per
+// residual bin streams its changed rows, the dense-stream kernel spreads a large bin over 4 SMs.
+int rgs_auto_max_sp() {
+    static const int v = getenv("DWC_RGS_AUTO_MAX_SP") ? atoi(getenv("DWC_RGS_AUTO_MAX_SP")) : 2048;
+    return v;
+}
+
 size_t rgs_smem_bytes(int max_sp) { return rgs_base_bytes(max_sp) + kNSlot * 128 * 4 + 512; }
 
 

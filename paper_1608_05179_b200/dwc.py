@@ -19,6 +19,7 @@ DWC_CUBIC = 2
 DWC_DIAG_REMOVAL = 4
 DWC_ALT_SWEEPS = 8
 DWC_GS_DENSE_STREAM = 16
+DWC_GS_RESIDUAL = 32
 GS_KERNELS = {0: "none", 1: "cluster", 2: "cluster_xtra", 3: "alternating", 4: "residual"}
 STATUS = {0: "DWC_OK", -1: "DWC_EINVAL", -2: "DWC_ESINGULAR", -3: "DWC_ENUMERIC",
           -4: "DWC_ENOMEM", -5: "DWC_ECUDA", -6: "DWC_ESTATE"}
@@ -130,12 +131,19 @@ class Geometry:
         return Grid(int(self.n), float(self.side_len), float(self.z0), float(self.cx), float(self.cy))
 
 
-def _flags(full_grid: bool, order: int, dr: bool = False, alt: bool = False, dense_stream: bool = False) -> int:
+def _gs_kernel_flag(dense_stream) -> int:
+    """dense_stream: None = automatic (by system size), True = dense-stream kernel, False = residual."""
+    if dense_stream is None:
+        return 0
+    return DWC_GS_DENSE_STREAM if dense_stream else DWC_GS_RESIDUAL
+
+
+def _flags(full_grid: bool, order: int, dr: bool = False, alt: bool = False, dense_stream=None) -> int:
     if order not in (1, 3):
         raise ValueError("order must be 1 (linear predictor) or 3 (cubic)")
     return ((DWC_FULL_GRID if full_grid else 0) | (DWC_CUBIC if order == 3 else 0) |
             (DWC_DIAG_REMOVAL if dr else 0) | (DWC_ALT_SWEEPS if alt else 0) |
-            (DWC_GS_DENSE_STREAM if dense_stream else 0))
+            (0 if alt else _gs_kernel_flag(dense_stream)))
 
 
 def _stream(stream) -> int:
@@ -177,7 +185,7 @@ class Context:
     # ---- hot path ---------------------------------------------------------------
     def solve_band(self, geom: Geometry, freqs: Sequence[float], csm, epsilon: float, sweeps: int,
                    eps_mode: int = 0, full_grid: bool = False, want_b: bool = False, out=None, order: int = 1,
-                   stream=None, dr: bool = False, alt: bool = False, dense_stream: bool = False):
+                   stream=None, dr: bool = False, alt: bool = False, dense_stream=None):
         """Batched S0..S8 on device tensors.  csm: cuda complex128 [K,M,M].
         Returns dict(n_keep int32[K], keep_idx int32[K,S], x_map float32[K,S], b_map, warn)."""
         import torch
@@ -205,7 +213,7 @@ class Context:
 
     def solve_band_host(self, geom: Geometry, freqs, csm, epsilon: float, sweeps: int, eps_mode: int = 0,
                         full_grid: bool = False, want_b: bool = False, out=None, stream=None, order: int = 1,
-                        dr: bool = False, alt: bool = False, dense_stream: bool = False):
+                        dr: bool = False, alt: bool = False, dense_stream=None):
         """Same as solve_band with host buffers (numpy or CPU tensors, pinned or not); the
         host<->device copies happen inside the C call, which returns when results are on the host."""
         import torch
@@ -234,7 +242,7 @@ class Context:
     # ---- stage entry points ---------------------------------------------------------
     def solve_band_snapshots(self, geom: Geometry, freqs: Sequence[float], snap, epsilon: float, sweeps: int,
                              eps_mode: int = 0, full_grid: bool = False, want_b: bool = False, order: int = 1,
-                             stream=None, dr: bool = False, alt: bool = False, dense_stream: bool = False):
+                             stream=None, dr: bool = False, alt: bool = False, dense_stream=None):
         """The path from snapshot spectra (Eq. 1 on the device).  snap: cuda complex128 [K,M,I]."""
         import torch
         freqs = np.ascontiguousarray(freqs, dtype=np.float64)
@@ -311,11 +319,11 @@ class Context:
                              _dev(A, torch.float32, "A"), _stream(stream)))
         return A
 
-    def gs(self, A, b, sweeps: int, stream=None, alt: bool = False, dense_stream: bool = False):
+    def gs(self, A, b, sweeps: int, stream=None, alt: bool = False, dense_stream=None):
         import torch
         n = A.shape[0]
         x = torch.empty(n, dtype=torch.float32, device=A.device)
-        fl = (DWC_ALT_SWEEPS if alt else 0) | (DWC_GS_DENSE_STREAM if dense_stream else 0)
+        fl = DWC_ALT_SWEEPS if alt else _gs_kernel_flag(dense_stream)
         _check(lib().dwc_gs(self._h, n, _dev(A, torch.float32, "A"), _dev(b, torch.float64, "b"), int(sweeps),
                             fl, _dev(x, torch.float32, "x"), _stream(stream)))
         return x

@@ -191,3 +191,37 @@ def test_e2e_cfg4_full_grid_defining_size(ctx, torch_cuda, oracle_lib, dense):
     st, nk = _e2e(ctx, torch_cuda, oracle_lib, band, 10, full=True, dense=dense)
     assert nk[0] == 10201
     assert st["gs_kernel"] == (2 if dense else 4)
+
+
+def test_automatic_kernel_choice(ctx, torch_cuda):
+    """Without a kernel flag the band's largest compressed system picks the GS kernel: cfg3's
+    compressed bins (S~ <= 1184) run the residual kernel, a full-grid band of S = 2209 (padded
+    2240 > 2048) the dense-stream cluster kernel; both flags at once are rejected."""
+    torch = torch_cuda
+    from paper_1608_05179_b200 import DwcError
+    band = synth.make_band("cfg3", bins=[0, 255])
+    cfg = band.cfg
+    ctx.solve_band(geom_of(band), band.freqs, torch.from_numpy(band.csm).cuda(), cfg.epsilon, 5)
+    assert ctx.stats()["gs_kernel"] == 4
+    cfg4 = dataclasses.replace(synth.CONFIGS["cfg4"], n=47, n_bins=1)
+    b4 = synth.make_band(cfg4)
+    ctx.solve_band(geom_of(b4), b4.freqs, torch.from_numpy(b4.csm).cuda(), cfg4.epsilon, 3, full_grid=True)
+    assert ctx.stats()["gs_kernel"] in (1, 2)
+    import ctypes as C
+
+    from paper_1608_05179_b200.dwc import Params, lib
+    g = geom_of(band)
+    arr, grid = g.c_array(), g.c_grid()
+    nk = torch.empty(2, dtype=torch.int32, device="cuda")
+    keep = torch.empty((2, g.S), dtype=torch.int32, device="cuda")
+    x = torch.empty((2, g.S), dtype=torch.float32, device="cuda")
+    f = np.array(band.freqs, dtype=np.float64)
+    csm = torch.from_numpy(band.csm).cuda()
+    rc = lib().dwc_solve_band(ctx._h, C.byref(arr), C.byref(grid), C.byref(Params(cfg.epsilon, 0, 5, 16 | 32)), 2,
+                              f.ctypes.data, csm.data_ptr(), nk.data_ptr(), keep.data_ptr(), x.data_ptr(), None, None,
+                              torch.cuda.current_stream().cuda_stream)
+    assert rc == -1
+    A8 = torch.eye(8, dtype=torch.float32).cuda()
+    b8 = torch.ones(8, dtype=torch.float64).cuda()
+    x8 = torch.empty(8, dtype=torch.float32).cuda()
+    assert lib().dwc_gs(ctx._h, 8, A8.data_ptr(), b8.data_ptr(), 1, 16 | 32, x8.data_ptr(), None) == -1
