@@ -232,8 +232,9 @@ typedef struct {
     int32_t gs_xtra_tiles;
     int32_t gs_ctas;
     int32_t gs_max_group;
-    int64_t gs_updates;       /* residual kernel: row updates (x changes) over all bins and sweeps;
-                                 each one reads one row of A~ (4 sp bytes) */
+    int64_t gs_updates;       /* residual kernel: row updates (x changes) over all bins and sweeps */
+    double gs_row_bytes;      /* residual kernel: bytes of the rows of A~ those updates streamed
+                                 (4 sp per update; the panels of predicted rows come on top) */
 } dwc_stats;
 
 #define DWC_GS_KERNEL_NONE 0

@@ -517,10 +517,12 @@ dwc_status dwc_get_stats(dwc_ctx *ctx, dwc_stats *out) {
     dwc_stats s = ctx->stats;
     if (ctx->stats_upd_valid) {
         // residual kernel: rows of A~ the sweeps had to read (x changes), read back once
-        unsigned long long u = 0;
-        CU(cudaMemcpy(&u, ctx->upd.p, sizeof u, cudaMemcpyDeviceToHost));
-        s.gs_updates = (int64_t)u;
+        unsigned long long u[2] = {0, 0};
+        CU(cudaMemcpy(u, ctx->upd.p, sizeof u, cudaMemcpyDeviceToHost));
+        s.gs_updates = (int64_t)u[0];
+        s.gs_row_bytes = (double)u[1];
         ctx->stats.gs_updates = s.gs_updates;
+        ctx->stats.gs_row_bytes = s.gs_row_bytes;
         ctx->stats_upd_valid = false;
     }
     if (ctx->stats_events_valid) {

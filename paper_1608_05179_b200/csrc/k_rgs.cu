@@ -213,7 +213,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
     unsigned *pmask = reinterpret_cast<unsigned *>(ivs + (use_ivs ? max_sp : 0));   // per block: rows predicted to change
     float *ring = reinterpret_cast<float *>(pmask + ((max_sp / 32 + 31) & ~31));   // 128-byte aligned
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    unsigned long long my_updates = 0;
+    unsigned long long my_updates = 0, my_bytes = 0;
 
     for (;;) {
         if (tid == 0) sh.item = atomicAdd(counter, 1);
@@ -437,6 +437,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                     pmask[k] = chg;   // the prediction for the next visit
                 }
                 my_updates += (unsigned long long)q;
+                my_bytes += (unsigned long long)q * sp * 4;
                 __syncwarp();
                 if (lane == 0) {
                     mbar_arrive(&sh.dready[li]);
@@ -568,7 +569,10 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
         }
         __syncthreads();
     }
-    if (n_updates && wid == kWSolver && lane == 0 && my_updates) atomicAdd(n_updates, my_updates);
+    if (n_updates && wid == kWSolver && lane == 0 && my_updates) {
+        atomicAdd(n_updates, my_updates);        // row updates
+        atomicAdd(n_updates + 1, my_bytes);      // bytes of the rows they streamed
+    }
 }
 
 namespace {

@@ -51,7 +51,7 @@ class Stats(C.Structure):
                 ("launches", C.c_int32), ("ms_total", C.c_float), ("ms_das", C.c_float),
                 ("ms_compress", C.c_float), ("ms_psf", C.c_float), ("ms_gs", C.c_float),
                 ("gs_kernel", C.c_int32), ("gs_xtra_tiles", C.c_int32), ("gs_ctas", C.c_int32),
-                ("gs_max_group", C.c_int32), ("gs_updates", C.c_int64)]
+                ("gs_max_group", C.c_int32), ("gs_updates", C.c_int64), ("gs_row_bytes", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
