@@ -24,9 +24,15 @@
  *    kept-point counts, to size the PSF storage) and otherwise stays asynchronous.
  *  - Argument validation happens on the host before any launch.  On failure the call
  *    returns a negative dwc_status and dwc_last_error() describes it; no output is
- *    written in that case, except DWC_ENUMERIC detected on device (outputs undefined).
+ *    written in that case, with two exceptions detected after launches: DWC_ENUMERIC found on
+ *    the device (outputs undefined), and a compressed band whose largest kept set S~ exceeds
+ *    the on-chip capacity of the Gauss-Seidel kernels (S~ is only known after S4: DWC_EINVAL,
+ *    b_map / n_keep / keep_idx then hold the S2-S4 results, x_map is not written; a full-grid
+ *    band is checked before any launch).  No copy into a caller's host buffer outlives a failed
+ *    call.
  *  - A context is used by one host thread at a time.  Different devices need different
- *    contexts.
+ *    contexts.  Calls on one context may use different streams: each call's work is ordered
+ *    after the previous call's (the context's workspace is shared).
  *  - Scan grid node s = row*n + col sits at x = cx - L/2 + col*dx, y = cy - L/2 + row*dx,
  *    z = z0, dx = L/(n-1) (reading R17).
  *  - A CSM is m*m complex128, row-major, C[i][j] at (i*m + j), interleaved (re, im)
@@ -157,35 +163,40 @@ DWC_API dwc_status dwc_solve_band_snapshots(dwc_ctx *ctx, const dwc_array *arr, 
 
 /* ---- stage entry points (parity tests feed identical inputs to GPU and oracle) ---- */
 
-/* Eq. 1: CSMs from snapshot spectra.  snap as dwc_solve_band_snapshots; csm dev complex128
+/* Eq. 1 (PAPER.md:88-95): CSMs from snapshot spectra.  snap as dwc_solve_band_snapshots; csm dev complex128
  * [n_bins][m][m] row-major (out), fp64.  Errors: DWC_EINVAL, DWC_ECUDA. */
 DWC_API dwc_status dwc_csm(dwc_ctx *ctx, int32_t m, int32_t n_bins, int32_t n_snap, const double *snap,
                            double *csm, void *cuda_stream);
 
-/* S1: normalised steering vectors e_s = sqrt(M) g_s/||g_s|| of n_pts nodes (reading R1).
+/* S1: normalised steering vectors e_s = sqrt(M) g_s/||g_s|| of n_pts nodes (reading R1;
+ * PAPER.md:102-110 Eq. 3-4, :128-131 Eq. 7).
  * idx dev int32[n_pts]; E dev complex128 [n_pts][m] interleaved (out). */
 DWC_API dwc_status dwc_steer(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, double freq_hz,
                      int32_t n_pts, const int32_t *idx, double *E, void *cuda_stream);
 
-/* S2: DAS maps b_k(s) = Re(e_s^H C_k e_s)/M^2 in fp64.  csm dev as in dwc_solve_band;
+/* S2: DAS maps b_k(s) = Re(e_s^H C_k e_s)/M^2 in fp64 (Eq. 2; diagonal removal
+ * PAPER.md:96).  csm dev as in dwc_solve_band;
  * flags: 0 or DWC_DIAG_REMOVAL; b_map dev double[n_bins*S] (out). */
 DWC_API dwc_status dwc_das(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, int32_t n_bins,
                    const double *freq_hz, const double *csm, int32_t flags, double *b_map, void *cuda_stream);
 
-/* S3+S4: wavelet details in fp64 (no FMA contraction, reading R7 stencil) and threshold;
+/* S3+S4: wavelet details in fp64 (no FMA contraction, reading R7 stencil) and threshold
+ * (Alg. 1 and Eq. 15-22);
  * b_map dev double[n_bins*S]; n_keep/keep_idx as in dwc_solve_band (out);
  * level dev uint8[n_bins*S] (out, nullable): resolution level of each node (Eq. 15). */
 DWC_API dwc_status dwc_compress(dwc_ctx *ctx, const dwc_grid *grid, const dwc_params *p,
                         int32_t n_bins, const double *b_map, int32_t *n_keep,
                         int32_t *keep_idx, uint8_t *level, void *cuda_stream);
 
-/* S5: PSF matrix on n_keep nodes, A[i][j] = |e_i^H e_j|^2/M^2, fp32 accurate.
+/* S5: PSF matrix on n_keep nodes, A[i][j] = |e_i^H e_j|^2/M^2, fp32 accurate (Eq. 9-12,
+ * PAPER.md:139-160, restricted to the kept nodes by Eq. 23).
  * keep_idx dev int32[n_keep]; flags: 0 or DWC_DIAG_REMOVAL; A dev float[n_keep*n_keep]
  * row-major (out). */
 DWC_API dwc_status dwc_psf(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, double freq_hz,
                    int32_t n_keep, const int32_t *keep_idx, int32_t flags, float *A, void *cuda_stream);
 
-/* S7: `sweeps` forward projected Gauss-Seidel sweeps from x0 = 0 on one system.
+/* S7: `sweeps` forward projected Gauss-Seidel sweeps from x0 = 0 on one system (Eq. 13-14,
+ * PAPER.md:167-180; alternating directions: SPEC.md:308, reading R21).
  * A dev float[n*n] row-major, symmetric (as A~ is, reading R1) with A_ii > 0: only the upper
  * triangle (j >= i) is read, the lower one is taken as its transpose.
  * flags: 0 or DWC_ALT_SWEEPS; b dev double[n], x dev float[n] (out).
@@ -197,7 +208,8 @@ DWC_API dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double 
 
 /* ---- multi-GPU gather helpers --------------------------------------- */
 
-/* Keep set -> bitmask: for each of n_bins bins, mask holds W = ceil(S/32) uint32 words; bit
+/* Keep set -> bitmask (the multi-GPU gather of a band whose bins are solved independently,
+ * PAPER.md:545-547): for each of n_bins bins, mask holds W = ceil(S/32) uint32 words; bit
  * (s % 32) of word s/32 is set iff node s is in the bin's keep list.  n_keep dev int32[n_bins],
  * keep_idx dev int32[n_bins*S] ascending (as dwc_solve_band writes it), mask dev
  * uint32[n_bins*W] (out).  The bitmask is what the ranks all-gather (S/8 bytes per bin
@@ -205,7 +217,8 @@ DWC_API dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double 
 DWC_API dwc_status dwc_keep_mask(dwc_ctx *ctx, int32_t n_bins, int32_t S, const int32_t *n_keep,
                                  const int32_t *keep_idx, uint32_t *mask, void *cuda_stream);
 
-/* Bitmask -> keep set: the inverse of dwc_keep_mask (ascending list, -1 padded to S). */
+/* Bitmask -> keep set: the inverse of dwc_keep_mask (ascending list, -1 padded to S; the keep
+ * set of Alg. 1). */
 DWC_API dwc_status dwc_keep_unmask(dwc_ctx *ctx, int32_t n_bins, int32_t S, const uint32_t *mask,
                                    int32_t *n_keep, int32_t *keep_idx, void *cuda_stream);
 

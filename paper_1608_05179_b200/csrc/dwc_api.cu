@@ -39,8 +39,8 @@ struct PinBuf {
     size_t bytes = 0;
 };
 
-// PSF output tiles (bin, I, J) of 128 rows x 64 columns that touch the upper triangle of the
-// sp x sp system (the kernel writes each computed entry and its mirror).
+// PSF output tiles (bin, I, J) of 128 rows x 32 columns (psf_tile_rows x psf_tile_cols) that touch
+// the upper triangle of the sp x sp system (the kernel writes each computed entry and its mirror).
 void append_psf_tiles(std::vector<int4> &tiles, int bin, int sp) {
     const int TR = dwc::psf_tile_rows(), TC = dwc::psf_tile_cols();
     for (int I = 0; I * TR < sp; I++)
@@ -66,6 +66,10 @@ struct dwc_ctx {
     int geo_m = -1, geo_n = -1;
     bool timing = false;
     cudaEvent_t ev[8] = {};
+    // the end of the last call's work on this context: every call's stream waits for it first,
+    // so calls on different streams never overlap on the shared workspace
+    cudaEvent_t last_done = nullptr;
+    bool last_valid = false;
     dwc_stats stats{};
     bool stats_events_valid = false;
     bool stats_upd_valid = false;   // the residual kernel's update counter belongs to the last call
@@ -162,6 +166,24 @@ dwc_status check_ctx(dwc_ctx *ctx) {
     return DWC_OK;
 }
 
+// Order a call after the previous call on this context (whatever stream that used) and mark its
+// end; the workspace is shared by every call.
+dwc_status enter_stream(dwc_ctx *ctx, cudaStream_t st) {
+    if (ctx->last_valid) CU(cudaStreamWaitEvent(st, ctx->last_done, 0));
+    return DWC_OK;
+}
+struct StreamScope {   // marks the end of the call's work (also on an error return)
+    dwc_ctx *ctx;
+    cudaStream_t st;
+    ~StreamScope() {
+        if (cudaEventRecord(ctx->last_done, st) == cudaSuccess) ctx->last_valid = true;
+        else cudaGetLastError();
+    }
+};
+#define STREAM_SCOPE(ctx_, st_)                              \
+    if ((s = enter_stream((ctx_), (st_)))) return s;         \
+    StreamScope scope_{(ctx_), (st_)}
+
 dwc_status check_array(const dwc_array *a) {
     if (!a) return fail(DWC_EINVAL, "array is NULL");
     if (a->m < 2 || a->m > DWC_MAX_MICS) return fail(DWC_EINVAL, "m = %d outside [2, %d]", a->m, DWC_MAX_MICS);
@@ -198,6 +220,17 @@ dwc_status check_freqs(int n_bins, const double *f) {
     if (!f) return fail(DWC_EINVAL, "freq_hz is NULL");
     for (int k = 0; k < n_bins; k++)
         if (!(f[k] > 0.0) || !finite(f[k])) return fail(DWC_EINVAL, "freq_hz[%d] must be > 0", k);
+    return DWC_OK;
+}
+
+// Full-grid mode knows S~ = S before any launch: reject a grid beyond the Gauss-Seidel kernels'
+// on-chip capacity up front (compressed bands can only be checked once S~ is known).
+dwc_status check_capacity_upfront(const dwc_grid *g, const dwc_params *p) {
+    if (!(p->flags & DWC_FULL_GRID)) return DWC_OK;
+    const int sp = (g->n * g->n + 31) & ~31;
+    const bool fits = (p->flags & DWC_ALT_SWEEPS) ? true
+                      : (rgs_smem_bytes(sp) <= 227 * 1024 || gs_smem_bytes(sp, gs_ystride(sp)) <= 227 * 1024);
+    if (!fits) return fail(DWC_EINVAL, "full grid of %d points exceeds the on-chip capacity of the Gauss-Seidel kernels", sp);
     return DWC_OK;
 }
 
@@ -310,21 +343,6 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
     const int flags = hk[n_bins];
     if (flags & kFlagSingular) return fail(DWC_ESINGULAR, "a scan-grid node coincides with a microphone");
     if (flags & kFlagNonFinite) return fail(DWC_ENUMERIC, "non-finite value in the CSM / DAS map");
-    if (early_keep_host) {
-        // the keep set is final: read it back on the copy stream while S5-S7 run
-        if (!ctx->copy_st) {
-            CU(cudaStreamCreateWithFlags(&ctx->copy_st, cudaStreamNonBlocking));
-            CU(cudaEventCreateWithFlags(&ctx->keep_ready, cudaEventDisableTiming));
-            CU(cudaEventCreateWithFlags(&ctx->copy_done, cudaEventDisableTiming));
-        }
-        CU(cudaEventRecord(ctx->keep_ready, st));
-        CU(cudaStreamWaitEvent(ctx->copy_st, ctx->keep_ready, 0));
-        memcpy(early_nk_host, hk, sizeof(int32_t) * n_bins);
-        CU(cudaMemcpyAsync(early_keep_host, keep_idx, sizeof(int32_t) * (size_t)n_bins * S, cudaMemcpyDeviceToHost,
-                           ctx->copy_st));
-        CU(cudaEventRecord(ctx->copy_done, ctx->copy_st));
-        CU(cudaStreamWaitEvent(st, ctx->copy_done, 0));   // the call's stream covers the copy too
-    }
     // host layout of the compressed systems
     std::vector<BinLayout> lay(n_bins);
     // GS kernel of the band (forward sweeps): DWC_GS_RESIDUAL / DWC_GS_DENSE_STREAM force one, else
@@ -357,7 +375,9 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
         sum_k += nk;
     }
     if (resid ? rgs_smem_bytes(max_sp) > 227 * 1024 : gs_smem_bytes(max_sp, ystride) > 227 * 1024)
-        return fail(DWC_EINVAL, "compressed grid of %d points exceeds the on-chip x capacity", max_sp);
+        return fail(DWC_EINVAL,
+                    "compressed grid of %d points exceeds the on-chip capacity of the Gauss-Seidel kernels "
+                    "(b_map, n_keep and keep_idx hold the S2-S4 results; x_map is not written)", max_sp);
     std::vector<int32_t> order(n_bins);
     std::iota(order.begin(), order.end(), 0);
     std::stable_sort(order.begin(), order.end(), [&](int a, int b2) { return hk[a] > hk[b2]; });
@@ -386,6 +406,23 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
     if ((s = stage_upload(ctx, ctx->tiles.p, tiles.data(), sizeof(int4) * tiles.size(), st))) return s;
     if (resid && (s = stage_upload(ctx, ctx->order.p, order.data(), sizeof(int32_t) * n_bins, st))) return s;
     if ((s = stage_end(ctx, st))) return s;
+    if (early_keep_host) {
+        // the keep set is final: read it back on the copy stream while S5-S7 run (queued only now
+        // that every check and allocation of the call has passed: no copy into the caller's
+        // buffer outlives a failed call)
+        if (!ctx->copy_st) {
+            CU(cudaStreamCreateWithFlags(&ctx->copy_st, cudaStreamNonBlocking));
+            CU(cudaEventCreateWithFlags(&ctx->keep_ready, cudaEventDisableTiming));
+            CU(cudaEventCreateWithFlags(&ctx->copy_done, cudaEventDisableTiming));
+        }
+        CU(cudaEventRecord(ctx->keep_ready, st));
+        CU(cudaStreamWaitEvent(ctx->copy_st, ctx->keep_ready, 0));
+        memcpy(early_nk_host, hk, sizeof(int32_t) * n_bins);
+        CU(cudaMemcpyAsync(early_keep_host, keep_idx, sizeof(int32_t) * (size_t)n_bins * S, cudaMemcpyDeviceToHost,
+                           ctx->copy_st));
+        CU(cudaEventRecord(ctx->copy_done, ctx->copy_st));
+        CU(cudaStreamWaitEvent(st, ctx->copy_done, 0));   // the call's stream covers the copy too
+    }
     ev(ctx, 3, st);
     // S5 (+S6)
     LAUNCH(launch_psf(G, (double *)ctx->dist.p, (double *)ctx->amp.p, n_bins, (double *)ctx->freq.p,
@@ -480,6 +517,10 @@ dwc_status dwc_create(int device, dwc_ctx **out) {
         return fail(DWC_ECUDA, "event creation failed");
     }
     for (auto &e : c->ev) cudaEventCreate(&e);
+    if (cudaEventCreateWithFlags(&c->last_done, cudaEventDisableTiming) != cudaSuccess) {
+        delete c;
+        return fail(DWC_ECUDA, "event creation failed");
+    }
     *out = c;
     return DWC_OK;
 }
@@ -500,6 +541,7 @@ dwc_status dwc_destroy(dwc_ctx *ctx) {
     if (ctx->copy_st) cudaStreamDestroy(ctx->copy_st);
     if (ctx->keep_ready) cudaEventDestroy(ctx->keep_ready);
     if (ctx->copy_done) cudaEventDestroy(ctx->copy_done);
+    if (ctx->last_done) cudaEventDestroy(ctx->last_done);
     for (auto &e : ctx->ev)
         if (e) cudaEventDestroy(e);
     delete ctx;
@@ -546,6 +588,8 @@ dwc_status dwc_solve_band(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
         (s = check_freqs(n_bins, freq_hz)))
         return s;
     if (!csm || !n_keep || !keep_idx || !x_map) return fail(DWC_EINVAL, "NULL device buffer");
+    if ((s = check_capacity_upfront(grid, p))) return s;
+    STREAM_SCOPE(ctx, (cudaStream_t)cuda_stream);
     return solve_band_dev(ctx, arr, grid, p, n_bins, freq_hz, csm, n_keep, keep_idx, x_map, b_map, warn,
                           (cudaStream_t)cuda_stream);
 }
@@ -560,6 +604,8 @@ dwc_status dwc_solve_band_snapshots(dwc_ctx *ctx, const dwc_array *arr, const dw
         return s;
     if (n_snap < 1) return fail(DWC_EINVAL, "n_snap must be >= 1");
     if (!snap || !n_keep || !keep_idx || !x_map) return fail(DWC_EINVAL, "NULL device buffer");
+    if ((s = check_capacity_upfront(grid, p))) return s;
+    STREAM_SCOPE(ctx, (cudaStream_t)cuda_stream);
     return solve_band_dev(ctx, arr, grid, p, n_bins, freq_hz, nullptr, n_keep, keep_idx, x_map, b_map, warn,
                           (cudaStream_t)cuda_stream, snap, n_snap);
 }
@@ -571,6 +617,7 @@ dwc_status dwc_csm(dwc_ctx *ctx, int32_t m, int32_t n_bins, int32_t n_snap, cons
     if (m < 1 || m > DWC_MAX_MICS || n_bins < 1 || n_snap < 1)
         return fail(DWC_EINVAL, "m = %d, n_bins = %d, n_snap = %d", m, n_bins, n_snap);
     if (!snap || !csm) return fail(DWC_EINVAL, "NULL device buffer");
+    STREAM_SCOPE(ctx, (cudaStream_t)cuda_stream);
     int launches = 0;
     LAUNCH(launch_csm(m, n_bins, n_snap, snap, csm, 0, 0, (cudaStream_t)cuda_stream));
     return DWC_OK;
@@ -585,7 +632,9 @@ dwc_status dwc_solve_band_host(dwc_ctx *ctx, const dwc_array *arr, const dwc_gri
         (s = check_freqs(n_bins, freq_hz)))
         return s;
     if (!csm || !n_keep || !keep_idx || !x_map) return fail(DWC_EINVAL, "NULL host buffer");
+    if ((s = check_capacity_upfront(grid, p))) return s;
     cudaStream_t st = (cudaStream_t)cuda_stream;
+    STREAM_SCOPE(ctx, st);
     const size_t S = (size_t)grid->n * grid->n, M = arr->m;
     const size_t csm_b = sizeof(double) * 2 * M * M * n_bins;
     if ((s = ensure(ctx, ctx->csm_h, csm_b)) || (s = ensure(ctx, ctx->nk_h, sizeof(int32_t) * n_bins)) ||
@@ -621,6 +670,7 @@ dwc_status dwc_steer(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, d
         return s;
     if (n_pts < 0 || (n_pts > 0 && (!idx || !E))) return fail(DWC_EINVAL, "bad n_pts / NULL buffer");
     cudaStream_t st = (cudaStream_t)cuda_stream;
+    STREAM_SCOPE(ctx, st);
     int launches = 0;
     Geo G;
     if ((s = prepare_geometry(ctx, arr, grid, 1, &freq_hz, G, launches, st))) return s;
@@ -635,6 +685,7 @@ dwc_status dwc_das(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, int
         return s;
     if (!csm || !b_map) return fail(DWC_EINVAL, "NULL device buffer");
     cudaStream_t st = (cudaStream_t)cuda_stream;
+    STREAM_SCOPE(ctx, st);
     int launches = 0;
     Geo G;
     if ((s = prepare_geometry(ctx, arr, grid, n_bins, freq_hz, G, launches, st))) return s;
@@ -656,6 +707,7 @@ dwc_status dwc_compress(dwc_ctx *ctx, const dwc_grid *grid, const dwc_params *p,
     if (n_bins < 1) return fail(DWC_EINVAL, "n_bins must be >= 1");
     if (!b_map || !n_keep || !keep_idx) return fail(DWC_EINVAL, "NULL device buffer");
     cudaStream_t st = (cudaStream_t)cuda_stream;
+    STREAM_SCOPE(ctx, st);
     int launches = 0;
     if ((s = ensure(ctx, ctx->flag, 64))) return s;
     LAUNCH(launch_compress(grid->n, n_bins, b_map, p->epsilon, p->eps_mode, (p->flags & DWC_FULL_GRID) ? 1 : 0, (p->flags & DWC_CUBIC) ? 3 : 1,
@@ -674,6 +726,7 @@ dwc_status dwc_psf(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, dou
     if (flags & ~DWC_DIAG_REMOVAL) return fail(DWC_EINVAL, "unknown flags 0x%x", flags);
     const int dr = (flags & DWC_DIAG_REMOVAL) ? 1 : 0;
     cudaStream_t st = (cudaStream_t)cuda_stream;
+    STREAM_SCOPE(ctx, st);
     int launches = 0;
     Geo G;
     if ((s = prepare_geometry(ctx, arr, grid, 1, &freq_hz, G, launches, st))) return s;
@@ -717,6 +770,7 @@ dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int3
     if (resid ? rgs_smem_bytes(sp) > 227 * 1024 : gs_smem_bytes(sp, gs_ystride(n)) > 227 * 1024)
         return fail(DWC_EINVAL, "n = %d exceeds the on-chip x capacity", n);
     cudaStream_t st = (cudaStream_t)cuda_stream;
+    STREAM_SCOPE(ctx, st);
     int launches = 0;
     // precondition A_ii > 0: checked on the device, read back before the sweeps
     if ((s = ensure(ctx, ctx->flag, 64)) || (s = ensure_pin(ctx->readback, 64))) return s;
@@ -795,6 +849,7 @@ dwc_status dwc_keep_mask(dwc_ctx *ctx, int32_t n_bins, int32_t S, const int32_t 
     if (S < 1 || n_bins < 0) return fail(DWC_EINVAL, "S = %d, n_bins = %d", S, n_bins);
     if (n_bins == 0) return DWC_OK;
     if (!n_keep || !keep_idx || !mask) return fail(DWC_EINVAL, "NULL device buffer");
+    STREAM_SCOPE(ctx, (cudaStream_t)cuda_stream);
     int launches = 0;
     LAUNCH(launch_keep_mask(n_bins, S, n_keep, keep_idx, mask, (cudaStream_t)cuda_stream));
     return DWC_OK;
@@ -807,6 +862,7 @@ dwc_status dwc_keep_unmask(dwc_ctx *ctx, int32_t n_bins, int32_t S, const uint32
     if (S < 1 || n_bins < 0) return fail(DWC_EINVAL, "S = %d, n_bins = %d", S, n_bins);
     if (n_bins == 0) return DWC_OK;
     if (!n_keep || !keep_idx || !mask) return fail(DWC_EINVAL, "NULL device buffer");
+    STREAM_SCOPE(ctx, (cudaStream_t)cuda_stream);
     int launches = 0;
     LAUNCH(launch_keep_unmask(n_bins, S, mask, n_keep, keep_idx, (cudaStream_t)cuda_stream));
     return DWC_OK;

@@ -105,16 +105,15 @@ __device__ __forceinline__ void cmac(double2 &acc, double2 a, double2 b) {  // a
 
 int das_mpad(int M) { return (M + 7) / 8 * 8; }
 
-template <int PPL, bool kBoth>
+template <int PPL, bool kBoth, int P = 32 * PPL>
 __device__ __forceinline__ void das_rows(const double2 *__restrict__ ca, const double2 *__restrict__ cb,
                                          const double2 *__restrict__ Es, int Mp,
                                          int n0, int n1, int lane, double2 Wa[4][PPL], double2 Wb[4][PPL]) {
-    constexpr int P = 32 * PPL;
 #pragma unroll kDasUnroll
     for (int n = n0; n < n1; n++) {
         double2 e[PPL];
 #pragma unroll
-        for (int j = 0; j < PPL; j++) e[j] = Es[n * P + lane + 32 * j];
+        for (int j = 0; j < PPL; j++) e[j] = Es[n * P + ((lane + 32 * j) & (P - 1))];
 #pragma unroll
         for (int r = 0; r < 4; r++) {
             const double2 c = ca[r * Mp + n];
@@ -141,12 +140,14 @@ __device__ __forceinline__ void das_rows(const double2 *__restrict__ ca, const d
 #ifndef DAS_DIRECT_C
 #define DAS_DIRECT_C 1
 #endif
-template <int PPL, int NW>
+// P: points per CTA (32 PPL; P = 16 for the largest arrays: 16 Mp P bytes of steering vectors
+// must fit in shared memory, and at Mp = 512 only P = 16 does -- lanes 16..31 then repeat lanes
+// 0..15 and their results are dropped)
+template <int PPL, int NW, int P = 32 * PPL>
 __global__ void __launch_bounds__(32 * NW, (DAS_DIRECT_C && PPL == 2) ? (NW == 4 ? 3 : 1) : 2)
 das_kernel(Geo g, const double *__restrict__ dist, const double *__restrict__ amp,
            const double *__restrict__ freq, const double2 *__restrict__ Ch, int Mp, double *__restrict__ b, int dr) {
-    constexpr int P = 32 * PPL;
-    constexpr bool kDirect = DAS_DIRECT_C && PPL == 2;
+    constexpr bool kDirect = DAS_DIRECT_C && (PPL == 2 || P < 32);
     extern __shared__ double2 smem_d2[];
     double2 *Es = smem_d2;                       // [Mp][P]
     double2 *Cw = smem_d2 + (size_t)Mp * P;      // [warp][8 rows][Mp]
@@ -203,18 +204,20 @@ das_kernel(Geo g, const double *__restrict__ dist, const double *__restrict__ am
         for (int r = 0; r < 4; r++)
 #pragma unroll
             for (int j = 0; j < PPL; j++) Wa[r][j] = Wb[r][j] = make_double2(0.0, 0.0);
-        das_rows<PPL, false>(ca, cb, Es, Mp, 4 * qa, 4 * qb, lane, Wa, Wb);   // only rows of qa reach n < 4 qb
-        das_rows<PPL, true>(ca, cb, Es, Mp, 4 * qb, Mp, lane, Wa, Wb);
+        das_rows<PPL, false, P>(ca, cb, Es, Mp, 4 * qa, 4 * qb, lane, Wa, Wb);   // only rows of qa reach n < 4 qb
+        das_rows<PPL, true, P>(ca, cb, Es, Mp, 4 * qb, Mp, lane, Wa, Wb);
 #pragma unroll
         for (int r = 0; r < 4; r++)
 #pragma unroll
             for (int j = 0; j < PPL; j++) {
-                const double2 ea = Es[(4 * qa + r) * P + lane + 32 * j], eb = Es[(4 * qb + r) * P + lane + 32 * j];
+                const int pj = (lane + 32 * j) & (P - 1);
+                const double2 ea = Es[(4 * qa + r) * P + pj], eb = Es[(4 * qb + r) * P + pj];
                 acc[j] += ea.x * Wa[r][j].x + ea.y * Wa[r][j].y + eb.x * Wb[r][j].x + eb.y * Wb[r][j].y;
             }
     }
 #pragma unroll
-    for (int j = 0; j < PPL; j++) part[w][lane + 32 * j] = acc[j];
+    for (int j = 0; j < PPL; j++)
+        if (lane + 32 * j < P) part[w][lane + 32 * j] = acc[j];
     __syncthreads();
     if (threadIdx.x < P && s0 + (int)threadIdx.x < g.S) {
         double v = 0.0;
@@ -271,7 +274,20 @@ int launch_das(const Geo &g, const double *dist, const double *amp, int n_bins,
     // DAS_BIG (M > 64): 64 points (2 per lane) x 8 warps, Ch through L1, one CTA per SM (128 KB
     // of steering vectors, 252 registers): cfg5 DAS 192 -> 170 ms, cfg4 3.15 -> 2.80 ms against
     // 32 points x 8 warps with the Ch rows staged
-    const bool big = DAS_BIG && DAS_DIRECT_C && Mp > 64 && DAS_P64;
+    // the largest arrays (Mp > 208): 16 points per CTA, Ch through L1 (16 Mp 16 bytes of steering)
+    const bool huge = Mp > 208;
+    const bool big = !huge && DAS_BIG && DAS_DIRECT_C && Mp > 64 && DAS_P64;
+    if (huge) {
+        const size_t smem16 = (size_t)16 * Mp * 16;
+        if (smem16 > 220 * 1024) return -1;
+        if (cudaFuncSetAttribute(das_kernel<1, kDasWarps, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem16) !=
+            cudaSuccess)
+            return -1;
+        dim3 grid16((g.S + 15) / 16, n_bins);
+        das_kernel<1, kDasWarps, 16><<<grid16, kDasThreads, smem16, st>>>(g, dist, amp, freq, (const double2 *)csm_half, Mp,
+                                                                          b, dr);
+        return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+    }
     const int P = ((Mp <= 64 && DAS_P64) || big) ? 64 : 32;
     const int NWv = (P == 64 && !big) ? 4 : kDasWarps;
     const size_t smem = (size_t)16 * Mp * (P + ((DAS_DIRECT_C && P == 64) ? 0 : 8 * NWv));

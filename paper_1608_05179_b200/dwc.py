@@ -146,10 +146,30 @@ def _flags(full_grid: bool, order: int, dr: bool = False, alt: bool = False, den
             (0 if alt else _gs_kernel_flag(dense_stream)))
 
 
-def _stream(stream) -> int:
+def _stream(stream, device=None) -> int:
+    """The cudaStream_t to enqueue on: `stream`, else the current stream of the context's device."""
     import torch
-    s = torch.cuda.current_stream() if stream is None else stream
+    s = torch.cuda.current_stream(device) if stream is None else stream
     return int(s.cuda_stream)
+
+
+def _check_out(out: dict, K: int, S: int, want_b: bool, host: bool, device=None):
+    """Caller-supplied output buffers: shape, dtype, contiguity and residency (the C call writes
+    K*S elements through raw pointers)."""
+    import torch
+    spec = {"n_keep": ((K,), torch.int32), "keep_idx": ((K, S), torch.int32), "x_map": ((K, S), torch.float32)}
+    if want_b or out.get("b_map") is not None:
+        spec["b_map"] = ((K, S), torch.float64)
+    for key, (shape, dtype) in spec.items():
+        t = out.get(key)
+        if t is None:
+            raise ValueError(f"out[{key!r}] is missing")
+        if not isinstance(t, torch.Tensor) or tuple(t.shape) != shape or t.dtype != dtype or not t.is_contiguous():
+            raise ValueError(f"out[{key!r}] must be a contiguous {dtype} tensor of shape {shape}")
+        if host and t.is_cuda:
+            raise ValueError(f"out[{key!r}] must be a host tensor")
+        if not host and (not t.is_cuda or (device is not None and t.device != device)):
+            raise ValueError(f"out[{key!r}] must be a CUDA tensor on {device}")
 
 
 def _dev(t, dtype, name):
@@ -199,6 +219,8 @@ class Context:
                    "keep_idx": torch.empty((K, S), dtype=torch.int32, device=dev),
                    "x_map": torch.empty((K, S), dtype=torch.float32, device=dev),
                    "b_map": torch.empty((K, S), dtype=torch.float64, device=dev) if want_b else None}
+        else:
+            _check_out(out, K, S, want_b, host=False, device=dev)
         warn = np.zeros(K, dtype=np.uint32)
         arr, grid = geom.c_array(), geom.c_grid()
         prm = Params(float(epsilon), int(eps_mode), int(sweeps), _flags(full_grid, order, dr, alt, dense_stream))
@@ -207,7 +229,7 @@ class Context:
             _dev(csm, torch.complex128, "csm"), _dev(out["n_keep"], torch.int32, "n_keep"),
             _dev(out["keep_idx"], torch.int32, "keep_idx"), _dev(out["x_map"], torch.float32, "x_map"),
             _dev(out["b_map"], torch.float64, "b_map") if out.get("b_map") is not None else None,
-            warn.ctypes.data, _stream(stream)))
+            warn.ctypes.data, _stream(stream, self.device)))
         out["warn"] = warn
         return out
 
@@ -227,6 +249,8 @@ class Context:
             out = {"n_keep": torch.empty(K, dtype=torch.int32), "keep_idx": torch.empty((K, S), dtype=torch.int32),
                    "x_map": torch.empty((K, S), dtype=torch.float32),
                    "b_map": torch.empty((K, S), dtype=torch.float64) if want_b else None}
+        else:
+            _check_out(out, K, S, want_b, host=True)
         warn = np.zeros(K, dtype=np.uint32)
         arr, grid = geom.c_array(), geom.c_grid()
         prm = Params(float(epsilon), int(eps_mode), int(sweeps), _flags(full_grid, order, dr, alt, dense_stream))
@@ -235,7 +259,7 @@ class Context:
             self._h, C.byref(arr), C.byref(grid), C.byref(prm), K, freqs.ctypes.data, csm.data_ptr(),
             out["n_keep"].data_ptr(), out["keep_idx"].data_ptr(), out["x_map"].data_ptr(),
             out["b_map"].data_ptr() if out.get("b_map") is not None else None,
-            warn.ctypes.data, _stream(stream)))
+            warn.ctypes.data, _stream(stream, self.device)))
         out["warn"] = warn
         return out
 
@@ -262,7 +286,7 @@ class Context:
             _dev(snap, torch.complex128, "snap"), _dev(out["n_keep"], torch.int32, "n_keep"),
             _dev(out["keep_idx"], torch.int32, "keep_idx"), _dev(out["x_map"], torch.float32, "x_map"),
             _dev(out["b_map"], torch.float64, "b_map") if out["b_map"] is not None else None,
-            warn.ctypes.data, _stream(stream)))
+            warn.ctypes.data, _stream(stream, self.device)))
         out["warn"] = warn
         return out
 
@@ -272,7 +296,7 @@ class Context:
         K, M, I = snap.shape
         out = torch.empty((K, M, M), dtype=torch.complex128, device=snap.device)
         _check(lib().dwc_csm(self._h, M, K, I, _dev(snap, torch.complex128, "snap"),
-                             _dev(out, torch.complex128, "csm"), _stream(stream)))
+                             _dev(out, torch.complex128, "csm"), _stream(stream, self.device)))
         return out
 
     def steer(self, geom: Geometry, freq: float, idx, stream=None):
@@ -281,7 +305,7 @@ class Context:
         E = torch.empty((idx.numel(), geom.m), dtype=torch.complex128, device=idx.device)
         arr, grid = geom.c_array(), geom.c_grid()
         _check(lib().dwc_steer(self._h, C.byref(arr), C.byref(grid), float(freq), idx.numel(),
-                               _dev(idx, torch.int32, "idx"), _dev(E, torch.complex128, "E"), _stream(stream)))
+                               _dev(idx, torch.int32, "idx"), _dev(E, torch.complex128, "E"), _stream(stream, self.device)))
         return E
 
     def das(self, geom: Geometry, freqs, csm, stream=None, dr: bool = False):
@@ -291,7 +315,7 @@ class Context:
         arr, grid = geom.c_array(), geom.c_grid()
         _check(lib().dwc_das(self._h, C.byref(arr), C.byref(grid), len(freqs), freqs.ctypes.data,
                              _dev(csm, torch.complex128, "csm"), DWC_DIAG_REMOVAL if dr else 0,
-                             _dev(b, torch.float64, "b"), _stream(stream)))
+                             _dev(b, torch.float64, "b"), _stream(stream, self.device)))
         return b
 
     def compress(self, geom: Geometry, b_map, epsilon: float, eps_mode: int = 0, full_grid: bool = False, order: int = 1,
@@ -305,7 +329,7 @@ class Context:
         prm = Params(float(epsilon), int(eps_mode), 1, _flags(full_grid, order))
         _check(lib().dwc_compress(self._h, C.byref(grid), C.byref(prm), K, _dev(b_map, torch.float64, "b_map"),
                                   _dev(nk, torch.int32, "n_keep"), _dev(keep, torch.int32, "keep_idx"),
-                                  _dev(lev, torch.uint8, "level") if lev is not None else None, _stream(stream)))
+                                  _dev(lev, torch.uint8, "level") if lev is not None else None, _stream(stream, self.device)))
         return nk, keep, lev
 
     def psf(self, geom: Geometry, freq: float, keep_idx, stream=None, dr: bool = False):
@@ -316,7 +340,7 @@ class Context:
         arr, grid = geom.c_array(), geom.c_grid()
         _check(lib().dwc_psf(self._h, C.byref(arr), C.byref(grid), float(freq), n,
                              _dev(keep_idx, torch.int32, "keep_idx"), DWC_DIAG_REMOVAL if dr else 0,
-                             _dev(A, torch.float32, "A"), _stream(stream)))
+                             _dev(A, torch.float32, "A"), _stream(stream, self.device)))
         return A
 
     def gs(self, A, b, sweeps: int, stream=None, alt: bool = False, dense_stream=None):
@@ -325,7 +349,7 @@ class Context:
         x = torch.empty(n, dtype=torch.float32, device=A.device)
         fl = DWC_ALT_SWEEPS if alt else _gs_kernel_flag(dense_stream)
         _check(lib().dwc_gs(self._h, n, _dev(A, torch.float32, "A"), _dev(b, torch.float64, "b"), int(sweeps),
-                            fl, _dev(x, torch.float32, "x"), _stream(stream)))
+                            fl, _dev(x, torch.float32, "x"), _stream(stream, self.device)))
         return x
 
     # ---- multi-GPU gather helpers ----------------------------------------------------------
@@ -337,7 +361,7 @@ class Context:
         mask = torch.empty((K, (S + 31) // 32), dtype=torch.int32, device=keep_idx.device)
         _check(lib().dwc_keep_mask(self._h, K, S, _dev(n_keep, torch.int32, "n_keep"),
                                    _dev(keep_idx, torch.int32, "keep_idx"), _dev(mask, torch.int32, "mask"),
-                                   _stream(stream)))
+                                   _stream(stream, self.device)))
         return mask
 
     def keep_unmask(self, mask, S: int, stream=None):
@@ -348,7 +372,7 @@ class Context:
         keep_idx = torch.empty((K, S), dtype=torch.int32, device=mask.device)
         _check(lib().dwc_keep_unmask(self._h, K, int(S), _dev(mask, torch.int32, "mask"),
                                      _dev(n_keep, torch.int32, "n_keep"), _dev(keep_idx, torch.int32, "keep_idx"),
-                                     _stream(stream)))
+                                     _stream(stream, self.device)))
         return n_keep, keep_idx
 
     # ---- diagnostics --------------------------------------------------------------------

@@ -54,8 +54,38 @@ def test_product_does_not_reference_oracle():
 
 
 def test_header_documents_every_entry_point():
+    """Every computing entry point has its own doc comment right above it, and that comment cites
+    the PAPER.md passage (line numbers) it implements."""
     hdr = open(os.path.join(ROOT, "include", "dwc.h")).read()
     assert "PAPER.md" in hdr
-    for name in ["dwc_solve_band", "dwc_das", "dwc_compress", "dwc_psf", "dwc_gs", "dwc_steer"]:
+    for name in ["dwc_solve_band", "dwc_solve_band_host", "dwc_solve_band_snapshots", "dwc_csm", "dwc_steer",
+                 "dwc_das", "dwc_compress", "dwc_psf", "dwc_gs", "dwc_keep_mask", "dwc_keep_unmask"]:
         i = hdr.index("DWC_API dwc_status " + name + "(")
-        assert hdr[:i].rstrip().endswith("*/"), name      # a doc comment right above
+        before = hdr[:i].rstrip()
+        assert before.endswith("*/"), name      # a doc comment right above
+        comment = before[before.rindex("/*"):]
+        if name in ("dwc_solve_band_host",):
+            comment = hdr[hdr.rindex("/* ---- the batched hot path", 0, i):i]   # documented with the band call
+        assert re.search(r"PAPER\.md:\d+", comment), name
+
+
+def test_output_buffer_checks():
+    """Caller-supplied output buffers are checked (shape, dtype, contiguity, residency) before
+    their raw pointers reach the C call."""
+    import torch
+
+    from paper_1608_05179_b200.dwc import _check_out
+    K, S = 3, 10
+    ok = {"n_keep": torch.empty(K, dtype=torch.int32), "keep_idx": torch.empty((K, S), dtype=torch.int32),
+          "x_map": torch.empty((K, S), dtype=torch.float32), "b_map": None}
+    _check_out(ok, K, S, want_b=False, host=True)
+    for key, bad in [("x_map", torch.empty((K, S + 1), dtype=torch.float32)),
+                     ("x_map", torch.empty((K, S), dtype=torch.float64)),
+                     ("keep_idx", torch.empty((S, K), dtype=torch.int32).t()),
+                     ("n_keep", torch.empty(K + 1, dtype=torch.int32))]:
+        with pytest.raises(ValueError):
+            _check_out(dict(ok, **{key: bad}), K, S, want_b=False, host=True)
+    with pytest.raises(ValueError):
+        _check_out(ok, K, S, want_b=True, host=True)        # b_map wanted but missing
+    with pytest.raises(ValueError):
+        _check_out(ok, K, S, want_b=False, host=False)      # host tensors for the device path

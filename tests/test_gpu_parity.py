@@ -76,7 +76,7 @@ def test_das_parity(ctx, torch_cuda, oracle_lib, cfgname):
         assert rel_l2(b[k], ref) < TOL_B
 
 
-@pytest.mark.parametrize("m", [2, 13, 64, 128])
+@pytest.mark.parametrize("m", [2, 13, 64, 128, 208, 216, 300, 512])
 def test_das_odd_sizes_and_non_hermitian(ctx, torch_cuda, oracle_lib, m):
     """Ragged mic counts (chunk tails) and a non-Hermitian CSM: only its Hermitian part
     matters (reading R3), so GPU == oracle's full quadratic form."""
@@ -280,6 +280,15 @@ def test_e2e_full_grid_m128(ctx, torch_cuda, oracle_lib, dense):
     cfg = dataclasses.replace(synth.CONFIGS["cfg4"], n=31, n_bins=3)
     band = synth.make_band(cfg)
     _e2e(ctx, torch_cuda, oracle_lib, band, sweeps=60, full=True, dense=dense)
+
+
+def test_e2e_max_mics(ctx, torch_cuda, oracle_lib):
+    """The whole path at DWC_MAX_MICS = 512 microphones (the DAS form with 16 points per CTA, the
+    PSF with 32 K steps of int8 digits): two bins on a 15 x 15 grid, 60 sweeps."""
+    import dataclasses
+    cfg = dataclasses.replace(synth.CONFIGS["cfg2"], m=512, arms=8, n=15, n_bins=2, snapshots=600)
+    band = synth.make_band(cfg)
+    _e2e(ctx, torch_cuda, oracle_lib, band, sweeps=60)
 
 
 def test_e2e_cfg5_strided_bins_few_sweeps(ctx, torch_cuda, oracle_lib):
