@@ -192,12 +192,13 @@ def gs(A, b, sweeps: int, alt: bool = False) -> np.ndarray:
     return x
 
 
-def _flags(full_grid, order, dr=False, alt=False):
-    return (1 if full_grid else 0) | (2 if order == 3 else 0) | (4 if dr else 0) | (8 if alt else 0)
+def _flags(full_grid, order, dr=False, alt=False, paper=False):
+    return (1 if full_grid else 0) | (2 if order == 3 else 0) | (4 if dr else 0) | (8 if alt else 0) | \
+        (16 if paper else 0)
 
 
 def solve_bin(mic, c0, n, L, z0, cx, cy, freq, csm, eps, eps_mode, sweeps, full_grid=False, order=1, dr=False,
-              alt=False):
+              alt=False, paper=False):
     """-> (keep, x_map fp64[S], b fp64[S])."""
     mic, g = _geo(mic, c0, n, L, z0, cx, cy)
     csm = np.ascontiguousarray(csm, dtype=np.complex128)
@@ -207,13 +208,13 @@ def solve_bin(mic, c0, n, L, z0, cx, cy, freq, csm, eps, eps_mode, sweeps, full_
     x = np.zeros(S)
     b = np.zeros(S)
     _chk(lib().or_solve_bin(*g, float(freq), _p(csm), float(eps), int(eps_mode), int(sweeps),
-                            _flags(full_grid, order, dr, alt), _p(nk), _p(keep), _p(x), _p(b)), "solve_bin")
+                            _flags(full_grid, order, dr, alt, paper), _p(nk), _p(keep), _p(x), _p(b)), "solve_bin")
     return keep[: nk[0]].copy(), x, b
 
 
 def solve_band(mic, c0, n, L, z0, cx, cy, freqs, csm, eps, eps_mode, sweeps,
                full_grid=False, n_threads: Optional[int] = None, order: int = 1, dr: bool = False,
-               alt: bool = False):
+               alt: bool = False, paper: bool = False):
     """Batched S0..S8 over K bins on a pthread pool.
     -> (n_keep int32[K], keep int32[K,S] (-1 padded), x_map fp64[K,S], b fp64[K,S])."""
     mic, g = _geo(mic, c0, n, L, z0, cx, cy)
@@ -228,17 +229,17 @@ def solve_band(mic, c0, n, L, z0, cx, cy, freqs, csm, eps, eps_mode, sweeps,
     if n_threads is None:
         n_threads = os.cpu_count() or 1
     _chk(lib().or_solve_band(*g, K, _p(freqs), _p(csm), float(eps), int(eps_mode), int(sweeps),
-                             _flags(full_grid, order, dr, alt), _p(nk), _p(keep), _p(x), _p(b), int(n_threads)),
+                             _flags(full_grid, order, dr, alt, paper), _p(nk), _p(keep), _p(x), _p(b), int(n_threads)),
          "solve_band")
     return nk, keep, x, b
 
 
 def solve_band_cfg(band, n_threads: Optional[int] = None, sweeps: Optional[int] = None,
                    full_grid: Optional[bool] = None, eps: Optional[float] = None, order: int = 1,
-                   dr: bool = False, alt: bool = False):
+                   dr: bool = False, alt: bool = False, paper: bool = False):
     """Convenience: run the oracle on a synth.Band."""
     cfg = band.cfg
     return solve_band(band.mic_xyz, cfg.c0, cfg.n, cfg.side_len, cfg.z0, cfg.cx, cfg.cy,
                       band.freqs, band.csm, cfg.epsilon if eps is None else eps, cfg.eps_mode,
                       cfg.sweeps if sweeps is None else sweeps,
-                      cfg.full_grid if full_grid is None else full_grid, n_threads, order, dr, alt)
+                      cfg.full_grid if full_grid is None else full_grid, n_threads, order, dr, alt, paper)

@@ -460,7 +460,9 @@ int or_gs(int nk, const double *A, const double *b, int sweeps, double *x, int a
 /* One bin, S1..S8.  keep (S ints) ascending, first n_keep valid.  x_map (S)
  * is the source power on the full grid, zero off the kept set (S8).
  * flags: bit 0 full grid (keep every node), bit 1 cubic predictor (R19),
- * bit 2 diagonal removal (R20), bit 3 alternating sweep directions (R21).         */
+ * bit 2 diagonal removal (R20), bit 3 alternating sweep directions (R21),
+ * bit 4 paper-literal beamformer and PSF (Eq. 4 v for the focus, Eq. 7 g for the source,
+ * PAPER.md:108, :130; asymmetric A, fidelity variant of R1; not with bit 2).        */
 int or_solve_bin(int m, const double *mic, double c0, int n, double L, double z0,
                  double cx, double cy, double freq, const double *csm,
                  double eps, int eps_mode, int sweeps, int flags,
@@ -468,7 +470,12 @@ int or_solve_bin(int m, const double *mic, double c0, int n, double L, double z0
     int S = n * n;
     double *b = b_map ? b_map : (double *)malloc(sizeof(double) * (size_t)S);
     if (!b) return OR_ENOMEM;
-    int rc = or_das(m, mic, c0, n, L, z0, cx, cy, freq, csm, b, flags & 4);
+    if ((flags & 16) && (flags & 4)) {
+        if (!b_map) free(b);
+        return OR_EINVAL;
+    }
+    int rc = (flags & 16) ? or_das_paper(m, mic, c0, n, L, z0, cx, cy, freq, csm, b)
+                          : or_das(m, mic, c0, n, L, z0, cx, cy, freq, csm, b, flags & 4);
     int nk = 0;
     double *A = NULL, *bt = NULL, *xt = NULL;
     if (rc == OR_OK) {
@@ -481,7 +488,9 @@ int or_solve_bin(int m, const double *mic, double c0, int n, double L, double z0
         xt = (double *)malloc(sizeof(double) * (size_t)nk);
         if (!A || !bt || !xt) rc = OR_ENOMEM;
     }
-    if (rc == OR_OK) rc = or_psf(m, mic, c0, n, L, z0, cx, cy, freq, nk, keep, A, flags & 4);
+    if (rc == OR_OK)
+        rc = (flags & 16) ? or_psf_paper(m, mic, c0, n, L, z0, cx, cy, freq, nk, keep, A)
+                          : or_psf(m, mic, c0, n, L, z0, cx, cy, freq, nk, keep, A, flags & 4);
     if (rc == OR_OK) {
         for (int i = 0; i < nk; i++) bt[i] = b[keep[i]];   /* S6: b~ = b[keep] */
         rc = or_gs(nk, A, bt, sweeps, xt, flags & 8);

@@ -82,3 +82,27 @@ def test_paper_das_of_model_csm_is_paper_psf_column(oracle_lib, geom1):
     b = oracle_lib.das_paper(*_g(cfg, mic), 4000.0, C)
     AP = oracle_lib.psf_paper(*_g(cfg, mic), 4000.0, np.arange(cfg.S, dtype=np.int32))
     assert np.max(np.abs(b - q2 * AP[:, s0])) < 1e-12 * q2
+
+
+def test_paper_mode_end_to_end_recovers_a_single_source(oracle_lib):
+    """The paper-literal path end to end (Eq. 4 beamformer, Eq. 7 PSF, Eq. 13-14 sweeps): for the
+    paper's own model CSM of one source at node s0, C = q^2 g g^H (Eq. 8), b_P = q^2 A_P[:, s0]
+    (Eq. 9-12), so x = q^2 e_s0 is the fixed point of the sweeps.  On a coarse 7x7 grid (dx/B ~
+    0.8) the sweeps reach it from x0 = 0; the R1 path on the same CSM returns a different power
+    (its x is the array-averaged descriptor, reading R1/R14)."""
+    m = 16
+    mic = synth.spiral_array(m, 0.5, 1)
+    n, L, z0, f = 7, 1.0, 1.0, 4000.0
+    s0, q2 = 24, 0.7
+    src = synth.grid_node_xyz(n, L, z0, 0.0, 0.0, np.array([s0]))
+    C = synth.csm_exact(mic, src, np.array([q2]), f, 343.0)
+    keep, x, b = oracle_lib.solve_bin(mic, 343.0, n, L, z0, 0.0, 0.0, f, C, 0.1, 0, 2000, full_grid=True,
+                                      paper=True)
+    assert len(keep) == n * n
+    e = np.zeros(n * n)
+    e[s0] = q2
+    assert np.max(np.abs(x - e)) < 1e-6 * q2
+    _, x1, _ = oracle_lib.solve_bin(mic, 343.0, n, L, z0, 0.0, 0.0, f, C, 0.1, 0, 2000, full_grid=True)
+    assert abs(x1.sum() - q2) > 1e-3 * q2
+    with pytest.raises(oracle_lib.OracleError):
+        oracle_lib.solve_bin(mic, 343.0, n, L, z0, 0.0, 0.0, f, C, 0.1, 0, 5, dr=True, paper=True)
