@@ -155,6 +155,7 @@ def cpu_baseline(cfg, budget_bins=None):
 
 # ------------------------------------------------------------------------------ our arm
 FP64_PEAK_TFLOPS = 36.0   # DFMA and DMMA, measured on B200 by scripts/ubench/fp64.cu
+KERNEL_FLAG = {"auto": None, "residual": False, "dense": True}   # dwc.py dense_stream argument
 
 
 def step_roofline(st, sweeps, hbm_gbs, ms_step):
@@ -178,6 +179,8 @@ def variant_key(cfg, args) -> str:
     """Key of profiles/gs_traffic.json: the ncu DRAM bytes of a GS launch are only reported for
     the exact config and variant they were captured on."""
     return (f"{cfg.name}|order{args.order}|dr{int(bool(args.dr))}|alt{int(bool(args.alt))}|{args.input}"
+            f"{'|paper' if getattr(args, 'paper', False) else ''}"
+            f"{'' if getattr(args, 'kernel', 'auto') == 'auto' else '|' + args.kernel}"
             f"|{args.scaling if int(os.environ.get('WORLD_SIZE', '1')) > 1 else 'n1'}"
             f"|g{int(os.environ.get('WORLD_SIZE', '1'))}")
 
@@ -224,10 +227,12 @@ def run_ours(args, cfg):
     def step():
         if snapshots:
             out = ctx.solve_band_snapshots(geom, band.freqs, snap_dev, cfg.epsilon, cfg.sweeps, cfg.eps_mode,
-                                           full_grid=cfg.full_grid, order=args.order, dr=args.dr, alt=args.alt, stream=stream)
+                                           full_grid=cfg.full_grid, order=args.order, dr=args.dr, alt=args.alt, stream=stream,
+                                           paper=args.paper, dense_stream=KERNEL_FLAG[args.kernel])
         else:
             out = ctx.solve_band(geom, band.freqs, csm_dev, cfg.epsilon, cfg.sweeps, cfg.eps_mode,
-                                 full_grid=cfg.full_grid, order=args.order, dr=args.dr, alt=args.alt, stream=stream)
+                                 full_grid=cfg.full_grid, order=args.order, dr=args.dr, alt=args.alt, stream=stream,
+                                           paper=args.paper, dense_stream=KERNEL_FLAG[args.kernel])
         if strong:
             # the one collective: maps + keep bitmasks + counts, all ranks
             mask = ctx.keep_mask(out["n_keep"], out["keep_idx"], stream=stream)
@@ -293,7 +298,8 @@ def run_ours(args, cfg):
         def e2e_call():
             snap_dev.copy_(snap_host, non_blocking=True)
             out = ctx.solve_band_snapshots(geom, band.freqs, snap_dev, cfg.epsilon, cfg.sweeps, cfg.eps_mode,
-                                           full_grid=cfg.full_grid, order=args.order, dr=args.dr, alt=args.alt, stream=stream)
+                                           full_grid=cfg.full_grid, order=args.order, dr=args.dr, alt=args.alt, stream=stream,
+                                           paper=args.paper, dense_stream=KERNEL_FLAG[args.kernel])
             for key in ("n_keep", "keep_idx", "x_map"):
                 h_out[key].copy_(out[key], non_blocking=True)
     else:
@@ -301,7 +307,8 @@ def run_ours(args, cfg):
 
         def e2e_call():
             ctx.solve_band_host(geom, band.freqs, csm_host, cfg.epsilon, cfg.sweeps, cfg.eps_mode, cfg.full_grid,
-                                out=h_out, stream=stream, order=args.order, dr=args.dr, alt=args.alt)
+                                out=h_out, stream=stream, order=args.order, dr=args.dr, alt=args.alt,
+                                paper=args.paper, dense_stream=KERNEL_FLAG[args.kernel])
     e2e_call()
     e2e_ms = []
     for it in range(args.steps):
@@ -337,7 +344,8 @@ def run_ours(args, cfg):
                                      stream=stream)
         else:
             ctx.solve_band(geom, band.freqs[kbig:kbig + 1], one_csm, cfg.epsilon, cfg.sweeps, cfg.eps_mode,
-                           full_grid=cfg.full_grid, order=args.order, dr=args.dr, alt=args.alt, stream=stream)
+                           full_grid=cfg.full_grid, order=args.order, dr=args.dr, alt=args.alt, stream=stream,
+                                           paper=args.paper, dense_stream=KERNEL_FLAG[args.kernel])
         torch.cuda.synchronize(dev)
         chain.append(ctx.stats())
     chain_floor = {"bin": int(band.bins[kbig]), "n_keep": int(nk_last[kbig]),
@@ -368,7 +376,9 @@ def run_ours(args, cfg):
             "dtype": "f32 (PSF + Gauss-Seidel); f64 (DAS map + wavelet threshold)", "data": "synthetic",
             "config": {"workload": workload_desc(cfg), "bins_per_gpu": K,
                        "predictor": "cubic (R19)" if args.order == 3 else "linear (R7)",
-                       "diagonal_removal": bool(args.dr), "alternating_sweeps": bool(args.alt), "parallelism": f"bins-dp{world}",
+                       "diagonal_removal": bool(args.dr), "alternating_sweeps": bool(args.alt),
+                       "paper_literal_psf": bool(args.paper), "gs_kernel_choice": args.kernel,
+                       "parallelism": f"bins-dp{world}",
                        "l2_flush": "256 MiB write between timed steps",
                        "inputs": ("snapshot spectra resident in HBM, CSM formed on device (Eq. 1)" if snapshots
                                   else "CSMs resident in HBM")},
@@ -424,6 +434,10 @@ def main():
                     help="csm: CSMs resident in HBM (default); snapshots: snapshot spectra, Eq. 1 on device")
     ap.add_argument("--dr", action="store_true", help="CSM diagonal removal (reading R20)")
     ap.add_argument("--alt", action="store_true", help="alternating sweep directions (reading R21, variant kernel)")
+    ap.add_argument("--paper", action="store_true",
+                    help="paper-literal beamformer and PSF (Eq. 4 v, Eq. 7 g; asymmetric, NEXT-4)")
+    ap.add_argument("--kernel", default="auto", choices=["auto", "residual", "dense"],
+                    help="Gauss-Seidel kernel: automatic by system size (default), residual, dense-stream")
     ap.add_argument("--order", type=int, default=1, choices=[1, 3],
                     help="S3 predictor: 1 linear (reading R7, default), 3 cubic (R19)")
     args = ap.parse_args()

@@ -116,6 +116,14 @@ typedef struct {
  * (setting both is DWC_EINVAL).  dwc_stats.gs_kernel reports which ran. */
 #define DWC_GS_DENSE_STREAM 16
 #define DWC_GS_RESIDUAL 32
+/* DWC_PAPER_PSF: the paper-literal beamformer and PSF (NEXT-4, fidelity study of reading R1): the
+ * DAS map with Eq. 4's focus vector v_m = (d_m/|r|) e^{-jkd_m} and the PSF
+ * A_P[i][j] = |v_i^H g_j|^2 / M^2 with Eq. 7's g_m = (|r|/d_m) e^{-jkd_m}, |r| the
+ * distance to the array centre (the origin).  A_P is not symmetric: the PSF covers
+ * every tile, the sweeps (Eq. 13-14, forward) run on the residual kernel with A_P stored
+ * transposed.  Not with DWC_DIAG_REMOVAL, DWC_ALT_SWEEPS or DWC_GS_DENSE_STREAM (DWC_EINVAL).
+ * The sweeps' convergence is not guaranteed (A_P has an indefinite symmetric part). */
+#define DWC_PAPER_PSF 64
 #define DWC_MAX_MICS 512
 
 /* Create / destroy a context on CUDA device `device`.  The device must be sm_100
@@ -176,7 +184,8 @@ DWC_API dwc_status dwc_steer(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid 
 
 /* S2: DAS maps b_k(s) = Re(e_s^H C_k e_s)/M^2 in fp64 (Eq. 2; diagonal removal
  * PAPER.md:96).  csm dev as in dwc_solve_band;
- * flags: 0 or DWC_DIAG_REMOVAL; b_map dev double[n_bins*S] (out). */
+ * flags: 0, DWC_DIAG_REMOVAL, or DWC_PAPER_PSF (Eq. 4's v instead of e);
+ * b_map dev double[n_bins*S] (out). */
 DWC_API dwc_status dwc_das(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, int32_t n_bins,
                    const double *freq_hz, const double *csm, int32_t flags, double *b_map, void *cuda_stream);
 
@@ -190,7 +199,8 @@ DWC_API dwc_status dwc_compress(dwc_ctx *ctx, const dwc_grid *grid, const dwc_pa
 
 /* S5: PSF matrix on n_keep nodes, A[i][j] = |e_i^H e_j|^2/M^2, fp32 accurate (Eq. 9-12,
  * PAPER.md:139-160, restricted to the kept nodes by Eq. 23).
- * keep_idx dev int32[n_keep]; flags: 0 or DWC_DIAG_REMOVAL; A dev float[n_keep*n_keep]
+ * keep_idx dev int32[n_keep]; flags: 0, DWC_DIAG_REMOVAL, or DWC_PAPER_PSF (the asymmetric
+ * A_P[i][j] = |v_i^H g_j|^2/M^2, Eq. 4 x Eq. 7); A dev float[n_keep*n_keep]
  * row-major (out). */
 DWC_API dwc_status dwc_psf(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, double freq_hz,
                    int32_t n_keep, const int32_t *keep_idx, int32_t flags, float *A, void *cuda_stream);
@@ -198,8 +208,11 @@ DWC_API dwc_status dwc_psf(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *g
 /* S7: `sweeps` forward projected Gauss-Seidel sweeps from x0 = 0 on one system (Eq. 13-14,
  * PAPER.md:167-180; alternating directions: SPEC.md:308, reading R21).
  * A dev float[n*n] row-major, symmetric (as A~ is, reading R1) with A_ii > 0: only the upper
- * triangle (j >= i) is read, the lower one is taken as its transpose.
- * flags: 0 or DWC_ALT_SWEEPS; b dev double[n], x dev float[n] (out).
+ * triangle (j >= i) is read, the lower one is taken as its transpose -- unless flags has
+ * DWC_PAPER_PSF: then A is a general matrix (the paper-literal PSF), read in full, forward sweeps
+ * on the residual kernel.
+ * flags: 0, DWC_ALT_SWEEPS, DWC_GS_DENSE_STREAM / DWC_GS_RESIDUAL (kernel choice), DWC_PAPER_PSF;
+ * b dev double[n], x dev float[n] (out).
  * Errors: DWC_EINVAL (n < 1, sweeps < 1, NULL, unknown flags, n beyond the on-chip x capacity),
  * DWC_ENUMERIC (some A_ii <= 0 or non-finite: checked on the device and read back, so this
  * call synchronises `cuda_stream` once before the sweeps), DWC_ECUDA. */

@@ -41,11 +41,11 @@ struct PinBuf {
 
 // PSF output tiles (bin, I, J) of 128 rows x 32 columns (psf_tile_rows x psf_tile_cols) that touch
 // the upper triangle of the sp x sp system (the kernel writes each computed entry and its mirror).
-void append_psf_tiles(std::vector<int4> &tiles, int bin, int sp) {
+void append_psf_tiles(std::vector<int4> &tiles, int bin, int sp, bool all = false) {
     const int TR = dwc::psf_tile_rows(), TC = dwc::psf_tile_cols();
     for (int I = 0; I * TR < sp; I++)
         for (int J = 0; J * TC < sp; J++)
-            if (J * TC + TC - 1 >= I * TR) tiles.push_back(make_int4(bin, I, J, 0));
+            if (all || J * TC + TC - 1 >= I * TR) tiles.push_back(make_int4(bin, I, J, 0));
 }
 
 enum FlagBits { kFlagNonFinite = 1, kFlagSingular = 4 };
@@ -57,7 +57,7 @@ struct dwc_ctx {
     int num_sms = 148;
     size_t total_bytes = 0;
     DevBuf mic, freq, dist, amp, herm, bint, opa, opb, rsc, wt, bt, A, lay, order, counter, tiles, flag, items, packets,
-        csm_h, nk_h, keep_h, xmap_h, bmap_h, gs_x, gs_b, Ad, upd;
+        csm_h, nk_h, keep_h, xmap_h, bmap_h, gs_x, gs_b, Ad, upd, ampv, ampg, rscb;
     PinBuf stage, readback;
     size_t stage_off = 0;
     cudaEvent_t stage_done = nullptr;
@@ -208,10 +208,13 @@ dwc_status check_params(const dwc_params *p) {
     if (!(p->epsilon > 0.0) || !finite(p->epsilon)) return fail(DWC_EINVAL, "epsilon must be > 0");
     if (p->eps_mode != 0 && p->eps_mode != 1) return fail(DWC_EINVAL, "eps_mode must be 0 or 1");
     if (p->sweeps < 1) return fail(DWC_EINVAL, "sweeps must be >= 1");
-    if (p->flags & ~(DWC_FULL_GRID | DWC_CUBIC | DWC_DIAG_REMOVAL | DWC_ALT_SWEEPS | DWC_GS_DENSE_STREAM | DWC_GS_RESIDUAL))
+    if (p->flags & ~(DWC_FULL_GRID | DWC_CUBIC | DWC_DIAG_REMOVAL | DWC_ALT_SWEEPS | DWC_GS_DENSE_STREAM | DWC_GS_RESIDUAL |
+                     DWC_PAPER_PSF))
         return fail(DWC_EINVAL, "unknown flags 0x%x", p->flags);
     if ((p->flags & DWC_GS_DENSE_STREAM) && (p->flags & DWC_GS_RESIDUAL))
         return fail(DWC_EINVAL, "DWC_GS_DENSE_STREAM and DWC_GS_RESIDUAL exclude each other");
+    if ((p->flags & DWC_PAPER_PSF) && (p->flags & (DWC_DIAG_REMOVAL | DWC_GS_DENSE_STREAM | DWC_ALT_SWEEPS)))
+        return fail(DWC_EINVAL, "DWC_PAPER_PSF runs forward sweeps on the residual kernel, without diagonal removal");
     return DWC_OK;
 }
 
@@ -251,9 +254,11 @@ Geo make_geo(dwc_ctx *ctx, const dwc_array *a, const dwc_grid *g) {
 
 // Upload mic + frequencies, build the steering tables.  Returns the launch count via *launches.
 dwc_status prepare_geometry(dwc_ctx *ctx, const dwc_array *a, const dwc_grid *g, int n_freq,
-                            const double *freq, Geo &G, int &launches, cudaStream_t st) {
+                            const double *freq, Geo &G, int &launches, cudaStream_t st, bool paper = false) {
     dwc_status s;
     const size_t S = (size_t)g->n * g->n;
+    if (paper && ((s = ensure(ctx, ctx->ampv, sizeof(double) * a->m * S)) || (s = ensure(ctx, ctx->ampg, sizeof(double) * a->m * S))))
+        return s;
     if ((s = ensure(ctx, ctx->mic, sizeof(double) * 3 * a->m))) return s;
     if ((s = ensure(ctx, ctx->freq, sizeof(double) * std::max(n_freq, 1)))) return s;
     if ((s = ensure(ctx, ctx->dist, sizeof(double) * a->m * S))) return s;
@@ -265,7 +270,8 @@ dwc_status prepare_geometry(dwc_ctx *ctx, const dwc_array *a, const dwc_grid *g,
     if ((s = stage_end(ctx, st))) return s;
     CU(cudaMemsetAsync(ctx->flag.p, 0, 64, st));
     G = make_geo(ctx, a, g);
-    LAUNCH(launch_geom_tables(G, (double *)ctx->dist.p, (double *)ctx->amp.p, (int *)ctx->flag.p, st));
+    LAUNCH(launch_geom_tables(G, (double *)ctx->dist.p, (double *)ctx->amp.p, (int *)ctx->flag.p, st,
+                              paper ? (double *)ctx->ampv.p : nullptr, paper ? (double *)ctx->ampg.p : nullptr));
     return DWC_OK;
 }
 
@@ -312,9 +318,10 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
     int launches = 0;
     const int M = arr->m, n = grid->n;
     const int S = n * n;
+    const bool paper = (p->flags & DWC_PAPER_PSF) != 0;   // NEXT-4: Eq. 4 / Eq. 7 as printed
     ev(ctx, 0, st);
     Geo G;
-    if ((s = prepare_geometry(ctx, arr, grid, n_bins, freq, G, launches, st))) return s;
+    if ((s = prepare_geometry(ctx, arr, grid, n_bins, freq, G, launches, st, paper))) return s;
     // S2 DAS on the Hermitian part of each CSM
     if ((s = ensure(ctx, ctx->herm, sizeof(double) * 2 * (size_t)n_bins * das_mpad(M) * das_mpad(M)))) return s;
     double *b = b_map;
@@ -327,8 +334,8 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
         LAUNCH(launch_csm(M, n_bins, n_snap, snap, (double *)ctx->herm.p, 1, dr, st));   // Eq. 1 -> Ch
     else
         LAUNCH(launch_hermitize(M, n_bins, csm, (double *)ctx->herm.p, dr, st));
-    LAUNCH(launch_das(G, (double *)ctx->dist.p, (double *)ctx->amp.p, n_bins, (double *)ctx->freq.p,
-                      (double *)ctx->herm.p, b, dr, st));
+    LAUNCH(launch_das(G, (double *)ctx->dist.p, (double *)(paper ? ctx->ampv.p : ctx->amp.p), n_bins,
+                      (double *)ctx->freq.p, (double *)ctx->herm.p, b, dr, st));
     ev(ctx, 1, st);
     // S3+S4
     LAUNCH(launch_compress(n, n_bins, b, p->epsilon, p->eps_mode, (p->flags & DWC_FULL_GRID) ? 1 : 0, (p->flags & DWC_CUBIC) ? 3 : 1,
@@ -351,8 +358,8 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
     // stream over 4 SMs)
     int band_sp = 0;
     for (int k = 0; k < n_bins; k++) band_sp = std::max(band_sp, (hk[k] + 31) & ~31);
-    const bool resid = !(p->flags & DWC_ALT_SWEEPS) &&
-                       ((p->flags & DWC_GS_RESIDUAL) || (!(p->flags & DWC_GS_DENSE_STREAM) && band_sp <= rgs_auto_max_sp()));
+    const bool resid = paper || (!(p->flags & DWC_ALT_SWEEPS) &&
+                       ((p->flags & DWC_GS_RESIDUAL) || (!(p->flags & DWC_GS_DENSE_STREAM) && band_sp <= rgs_auto_max_sp())));
     int64_t a_off = 0, v_off = 0, r_off = 0, d_off = 0;
     int max_sp = 0, max_rp = 0, ystride = 0;
     double sum_sq = 0.0, sum_sym = 0.0;
@@ -384,7 +391,7 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
     std::vector<int> items = build_gs_items(order, hk);
     const int n_items = (int)items.size() / gs_item_ints();
     std::vector<int4> tiles;
-    for (int k = 0; k < n_bins; k++) append_psf_tiles(tiles, k, lay[k].sp);
+    for (int k = 0; k < n_bins; k++) append_psf_tiles(tiles, k, lay[k].sp, paper);
     if ((s = ensure(ctx, ctx->lay, sizeof(BinLayout) * n_bins))) return s;
     if ((s = ensure(ctx, ctx->items, sizeof(int) * items.size()))) return s;
     if ((s = ensure(ctx, ctx->tiles, sizeof(int4) * std::max<size_t>(tiles.size(), 1)))) return s;
@@ -393,6 +400,7 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
         (s = ensure(ctx, ctx->rsc, sizeof(double) * (size_t)r_off)))
         return s;
     if (dr && (s = ensure(ctx, ctx->wt, sizeof(double) * (size_t)r_off * M))) return s;
+    if (paper && (s = ensure(ctx, ctx->rscb, sizeof(double) * (size_t)r_off))) return s;
     if ((s = ensure(ctx, ctx->bt, sizeof(double) * (size_t)v_off))) return s;
     if ((s = ensure(ctx, ctx->A, sizeof(float) * (size_t)std::max<int64_t>(a_off, 1024)))) return s;
     if (resid && ((s = ensure(ctx, ctx->Ad, sizeof(float) * (size_t)d_off)) || (s = ensure(ctx, ctx->upd, 64)) ||
@@ -425,10 +433,12 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
     }
     ev(ctx, 3, st);
     // S5 (+S6)
-    LAUNCH(launch_psf(G, (double *)ctx->dist.p, (double *)ctx->amp.p, n_bins, (double *)ctx->freq.p,
-                      (BinLayout *)ctx->lay.p, keep_idx, b, max_rp, (int)tiles.size(), (int4 *)ctx->tiles.p,
-                      (int8_t *)ctx->opa.p, (int8_t *)ctx->opb.p, (double *)ctx->rsc.p, (double *)ctx->bt.p,
-                      dr ? (double *)ctx->wt.p : nullptr, (float *)ctx->A.p, resid ? (float *)ctx->Ad.p : nullptr, st));
+    LAUNCH(launch_psf(G, (double *)ctx->dist.p, (double *)(paper ? ctx->ampv.p : ctx->amp.p), n_bins,
+                      (double *)ctx->freq.p, (BinLayout *)ctx->lay.p, keep_idx, b, max_rp, (int)tiles.size(),
+                      (int4 *)ctx->tiles.p, (int8_t *)ctx->opa.p, (int8_t *)ctx->opb.p, (double *)ctx->rsc.p,
+                      (double *)ctx->bt.p, dr ? (double *)ctx->wt.p : nullptr, (float *)ctx->A.p,
+                      resid ? (float *)ctx->Ad.p : nullptr, st, paper ? (double *)ctx->ampg.p : nullptr,
+                      paper ? (double *)ctx->rscb.p : nullptr));
     ev(ctx, 4, st);
     // S7 + S8
     CU(cudaMemsetAsync(x_map, 0, sizeof(float) * (size_t)n_bins * S, st));
@@ -532,7 +542,7 @@ dwc_status dwc_destroy(dwc_ctx *ctx) {
     DevBuf *bufs[] = {&ctx->mic, &ctx->freq, &ctx->dist, &ctx->amp, &ctx->herm, &ctx->bint, &ctx->opa, &ctx->opb, &ctx->rsc, &ctx->wt,
                       &ctx->bt, &ctx->A, &ctx->lay, &ctx->order, &ctx->counter, &ctx->tiles, &ctx->flag,
                       &ctx->items, &ctx->packets, &ctx->csm_h, &ctx->nk_h, &ctx->keep_h, &ctx->xmap_h, &ctx->bmap_h, &ctx->gs_x, &ctx->gs_b,
-                      &ctx->Ad, &ctx->upd};
+                      &ctx->Ad, &ctx->upd, &ctx->ampv, &ctx->ampg, &ctx->rscb};
     for (DevBuf *b : bufs)
         if (b->p) cudaFree(b->p);
     if (ctx->stage.p) cudaFreeHost(ctx->stage.p);
@@ -687,15 +697,18 @@ dwc_status dwc_das(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, int
     cudaStream_t st = (cudaStream_t)cuda_stream;
     STREAM_SCOPE(ctx, st);
     int launches = 0;
+    if (flags & ~(DWC_DIAG_REMOVAL | DWC_PAPER_PSF)) return fail(DWC_EINVAL, "unknown flags 0x%x", flags);
+    if ((flags & DWC_DIAG_REMOVAL) && (flags & DWC_PAPER_PSF))
+        return fail(DWC_EINVAL, "DWC_PAPER_PSF excludes DWC_DIAG_REMOVAL");
+    const bool paper = (flags & DWC_PAPER_PSF) != 0;
     Geo G;
-    if ((s = prepare_geometry(ctx, arr, grid, n_bins, freq_hz, G, launches, st))) return s;
+    if ((s = prepare_geometry(ctx, arr, grid, n_bins, freq_hz, G, launches, st, paper))) return s;
     if ((s = ensure(ctx, ctx->herm, sizeof(double) * 2 * (size_t)n_bins * das_mpad(arr->m) * das_mpad(arr->m))))
         return s;
-    if (flags & ~DWC_DIAG_REMOVAL) return fail(DWC_EINVAL, "unknown flags 0x%x", flags);
     const int dr = (flags & DWC_DIAG_REMOVAL) ? 1 : 0;
     LAUNCH(launch_hermitize(arr->m, n_bins, csm, (double *)ctx->herm.p, dr, st));
-    LAUNCH(launch_das(G, (double *)ctx->dist.p, (double *)ctx->amp.p, n_bins, (double *)ctx->freq.p,
-                      (double *)ctx->herm.p, b_map, dr, st));
+    LAUNCH(launch_das(G, (double *)ctx->dist.p, (double *)(paper ? ctx->ampv.p : ctx->amp.p), n_bins,
+                      (double *)ctx->freq.p, (double *)ctx->herm.p, b_map, dr, st));
     return DWC_OK;
 }
 
@@ -723,18 +736,23 @@ dwc_status dwc_psf(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, dou
     const int S = grid->n * grid->n;
     if (n_keep < 1 || n_keep > S) return fail(DWC_EINVAL, "n_keep = %d outside [1, S]", n_keep);
     if (!keep_idx || !A) return fail(DWC_EINVAL, "NULL device buffer");
-    if (flags & ~DWC_DIAG_REMOVAL) return fail(DWC_EINVAL, "unknown flags 0x%x", flags);
+    if (flags & ~(DWC_DIAG_REMOVAL | DWC_PAPER_PSF)) return fail(DWC_EINVAL, "unknown flags 0x%x", flags);
+    if ((flags & DWC_DIAG_REMOVAL) && (flags & DWC_PAPER_PSF))
+        return fail(DWC_EINVAL, "DWC_PAPER_PSF excludes DWC_DIAG_REMOVAL");
     const int dr = (flags & DWC_DIAG_REMOVAL) ? 1 : 0;
+    const bool paper = (flags & DWC_PAPER_PSF) != 0;
     cudaStream_t st = (cudaStream_t)cuda_stream;
     STREAM_SCOPE(ctx, st);
     int launches = 0;
     Geo G;
-    if ((s = prepare_geometry(ctx, arr, grid, 1, &freq_hz, G, launches, st))) return s;
+    if ((s = prepare_geometry(ctx, arr, grid, 1, &freq_hz, G, launches, st, paper))) return s;
     const int sp = (n_keep + 31) & ~31;
     const int rp = (n_keep + psf_tile_rows() - 1) / psf_tile_rows() * psf_tile_rows();
     BinLayout lay{n_keep, sp, 0, 0, rp, gs_group_size(n_keep), 0, 0};
     std::vector<int4> tiles;
-    append_psf_tiles(tiles, 0, sp);
+    append_psf_tiles(tiles, 0, sp, paper);
+    if (paper && ((s = ensure(ctx, ctx->rscb, sizeof(double) * rp)) || (s = ensure(ctx, ctx->Ad, sizeof(float) * (size_t)sp * sp))))
+        return s;
     if ((s = ensure(ctx, ctx->lay, sizeof(BinLayout))) || (s = ensure(ctx, ctx->tiles, sizeof(int4) * tiles.size())) ||
         (s = ensure(ctx, ctx->opa, psf_opa_bytes(arr->m, rp))) || (s = ensure(ctx, ctx->opb, psf_opb_bytes(arr->m, rp))) ||
         (s = ensure(ctx, ctx->rsc, sizeof(double) * rp)) || (s = ensure(ctx, ctx->bt, sizeof(double) * sp)) ||
@@ -745,6 +763,16 @@ dwc_status dwc_psf(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *grid, dou
     if ((s = stage_upload(ctx, ctx->lay.p, &lay, sizeof(BinLayout), st))) return s;
     if ((s = stage_upload(ctx, ctx->tiles.p, tiles.data(), sizeof(int4) * tiles.size(), st))) return s;
     if ((s = stage_end(ctx, st))) return s;
+    if (paper) {
+        // asymmetric: every tile, written transposed into the dense scratch, then A = its transpose
+        LAUNCH(launch_psf(G, (double *)ctx->dist.p, (double *)ctx->ampv.p, 1, (double *)ctx->freq.p,
+                          (BinLayout *)ctx->lay.p, keep_idx, nullptr, rp, (int)tiles.size(), (int4 *)ctx->tiles.p,
+                          (int8_t *)ctx->opa.p, (int8_t *)ctx->opb.p, (double *)ctx->rsc.p, (double *)ctx->bt.p,
+                          nullptr, (float *)ctx->A.p, (float *)ctx->Ad.p, st, (double *)ctx->ampg.p,
+                          (double *)ctx->rscb.p));
+        LAUNCH(launch_dense_extract(n_keep, sp, (float *)ctx->Ad.p, A, 1, st));
+        return DWC_OK;
+    }
     LAUNCH(launch_psf(G, (double *)ctx->dist.p, (double *)ctx->amp.p, 1, (double *)ctx->freq.p,
                       (BinLayout *)ctx->lay.p, keep_idx, nullptr, rp, (int)tiles.size(), (int4 *)ctx->tiles.p,
                       (int8_t *)ctx->opa.p, (int8_t *)ctx->opb.p, (double *)ctx->rsc.p, (double *)ctx->bt.p,
@@ -760,13 +788,17 @@ dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int3
     if (n < 1) return fail(DWC_EINVAL, "n must be >= 1");
     if (sweeps < 1) return fail(DWC_EINVAL, "sweeps must be >= 1");
     if (!A || !b || !x) return fail(DWC_EINVAL, "NULL device buffer");
-    if (flags & ~(DWC_ALT_SWEEPS | DWC_GS_DENSE_STREAM | DWC_GS_RESIDUAL))
+    if (flags & ~(DWC_ALT_SWEEPS | DWC_GS_DENSE_STREAM | DWC_GS_RESIDUAL | DWC_PAPER_PSF))
         return fail(DWC_EINVAL, "unknown flags 0x%x", flags);
     if ((flags & DWC_GS_DENSE_STREAM) && (flags & DWC_GS_RESIDUAL))
         return fail(DWC_EINVAL, "DWC_GS_DENSE_STREAM and DWC_GS_RESIDUAL exclude each other");
+    // DWC_PAPER_PSF: A is a general (asymmetric) matrix, read in full; residual kernel
+    const bool general = (flags & DWC_PAPER_PSF) != 0;
+    if (general && (flags & (DWC_ALT_SWEEPS | DWC_GS_DENSE_STREAM)))
+        return fail(DWC_EINVAL, "a general (DWC_PAPER_PSF) matrix runs forward sweeps on the residual kernel");
     const int sp = (n + 31) & ~31;
-    const bool resid = !(flags & DWC_ALT_SWEEPS) &&
-                       ((flags & DWC_GS_RESIDUAL) || (!(flags & DWC_GS_DENSE_STREAM) && sp <= rgs_auto_max_sp()));
+    const bool resid = general || (!(flags & DWC_ALT_SWEEPS) &&
+                       ((flags & DWC_GS_RESIDUAL) || (!(flags & DWC_GS_DENSE_STREAM) && sp <= rgs_auto_max_sp())));
     if (resid ? rgs_smem_bytes(sp) > 227 * 1024 : gs_smem_bytes(sp, gs_ystride(n)) > 227 * 1024)
         return fail(DWC_EINVAL, "n = %d exceeds the on-chip x capacity", n);
     cudaStream_t st = (cudaStream_t)cuda_stream;
@@ -799,7 +831,7 @@ dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int3
     if ((s = stage_end(ctx, st))) return s;
     float *Ap = (float *)ctx->gs_x.p;
     if (resid)
-        LAUNCH(launch_rgs_convert(n, sp, A, (float *)ctx->Ad.p, st));
+        LAUNCH(launch_rgs_convert(n, sp, A, (float *)ctx->Ad.p, st, general));
     else
         LAUNCH(launch_tile_convert(1, n, sp, lay.g, A, Ap, st));
     CU(cudaMemsetAsync(ctx->gs_b.p, 0, sizeof(double) * sp, st));

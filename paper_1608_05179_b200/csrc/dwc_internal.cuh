@@ -27,7 +27,9 @@ constexpr double kTwoPi = 6.283185307179586476925286766559;
 // Frequency-independent steering tables: dist[m][s] = |r_s - r_m| and
 // amp[m][s] = sqrt(M) / (dist * ||g_s||) with ||g_s||^2 = sum_m 1/dist^2 (reading R1).
 // Sets *singular (dev int) to 1 when some distance is 0.
-int launch_geom_tables(const Geo &g, double *dist, double *amp, int *flag, cudaStream_t st);
+// ampv / ampg (nullable, M x S each): the paper-literal amplitudes d/|r| (Eq. 4) and |r|/d (Eq. 7).
+int launch_geom_tables(const Geo &g, double *dist, double *amp, int *flag, cudaStream_t st, double *ampv = nullptr,
+                       double *ampg = nullptr);
 
 // S1 for a list of nodes: E[pt][m] complex128 interleaved.
 int launch_steer(const Geo &g, const double *dist, const double *amp, const double *freq,
@@ -83,10 +85,14 @@ int psf_tile_cols();
 // Adense != NULL: the residual GS layout -- A~_k dense row-major at Adense + d_off (row stride
 // sp, zero padded), nothing at A; else the symmetric tile layout of the dense-stream kernel at
 // A + a_off.
+// ampb != NULL: the paper-literal PSF (NEXT-4): the A side (rows) from amp = d/|r| (Eq. 4 v), the
+// B side (columns) from ampb = |r|/d (Eq. 7 g), rscb their column scales (sum rp doubles); the
+// tile list then covers every tile and Adense receives the TRANSPOSE of the asymmetric A_P
+// (Adense[j][i] = A_P[i][j], so the residual kernel reads column c of A_P as row c).
 int launch_psf(const Geo &g, const double *dist, const double *amp, int n_bins, const double *freq,
                const BinLayout *lay, const int32_t *keep_idx, const double *b, int max_rp, int n_tiles,
                const int4 *tiles, int8_t *opA, int8_t *opB, double *rsc, double *bt, double *wt, float *A,
-               float *Adense, cudaStream_t st);
+               float *Adense, cudaStream_t st, const double *ampb = nullptr, double *rscb = nullptr);
 
 // S5 storage layout of A~_k (written by the PSF epilogue, streamed by the GS kernel).
 // A~ is symmetric (reading R1), so only one triangle is stored.  32x32 fp32 tiles, column-major
@@ -263,8 +269,11 @@ int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int m
                const float *Adense, const double *bt, int sweeps, float *x_out, float *x_map,
                const int32_t *keep_idx, int S, int num_sms, unsigned long long *n_updates, cudaStream_t st,
                GsLaunchInfo *info);
-// dwc_gs: dense row-major n x n (upper triangle) -> padded dense sp x sp.
-int launch_rgs_convert(int n, int sp, const float *src, float *dense, cudaStream_t st);
+// dwc_gs: dense row-major n x n -> padded dense sp x sp (symmetric: from the upper triangle;
+// general: transposed).
+int launch_rgs_convert(int n, int sp, const float *src, float *dense, cudaStream_t st, int general = 0);
+// n x n row-major out of a padded sp x sp dense matrix (transposed if transpose).
+int launch_dense_extract(int n, int sp, const float *src, float *out, int transpose, cudaStream_t st);
 
 // Per-block solver packets (1/A_ii, within-group scaled coefficients, b~ block) for the GS
 // kernel: gs_packet_bytes() bytes per 32-row block, bin k's packets at v_off/32.

@@ -14,8 +14,11 @@
 
 namespace dwc {
 
+// Paper-literal amplitudes (NEXT-4, Eq. 4 and :130 Eq. 7, distances to the array
+// centre = the origin): ampv[m][s] = d_ms / |r_s| (the focus vector v) and ampg[m][s] = |r_s| / d_ms
+// (the propagation vector g); written when the pointers are not NULL.
 __global__ void geom_tables_kernel(Geo g, double *__restrict__ dist, double *__restrict__ amp,
-                                   int *__restrict__ flag) {
+                                   int *__restrict__ flag, double *__restrict__ ampv, double *__restrict__ ampg) {
     const double sqm = sqrt((double)g.m);
     for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < g.S; s += gridDim.x * blockDim.x) {
         const int r = s / g.n, c = s - (s / g.n) * g.n;
@@ -30,18 +33,24 @@ __global__ void geom_tables_kernel(Geo g, double *__restrict__ dist, double *__r
             inv2 += 1.0 / (d * d);
         }
         const double nrm = sqrt(inv2);
+        const double rn = sqrt(px * px + py * py + pz * pz);
         for (int m = 0; m < g.m; m++) {
             const double d = dist[(size_t)m * g.S + s];
             amp[(size_t)m * g.S + s] = sqm / (d * nrm);
+            if (ampv) {
+                ampv[(size_t)m * g.S + s] = d / rn;
+                ampg[(size_t)m * g.S + s] = rn / d;
+            }
         }
         if (sing) atomicOr(flag, 4);
     }
 }
 
-int launch_geom_tables(const Geo &g, double *dist, double *amp, int *flag, cudaStream_t st) {
+int launch_geom_tables(const Geo &g, double *dist, double *amp, int *flag, cudaStream_t st, double *ampv,
+                       double *ampg) {
     const int threads = 256;
     int blocks = (g.S + threads - 1) / threads;
-    geom_tables_kernel<<<blocks, threads, 0, st>>>(g, dist, amp, flag);
+    geom_tables_kernel<<<blocks, threads, 0, st>>>(g, dist, amp, flag, ampv, ampg);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

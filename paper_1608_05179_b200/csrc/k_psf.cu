@@ -103,7 +103,8 @@ psf_slice_kernel(Geo g, const double *__restrict__ dist, const double *__restric
                  const double *__restrict__ freq, const BinLayout *__restrict__ lay,
                  const int32_t *__restrict__ keep_idx, const double *__restrict__ b, int kp,
                  int8_t *__restrict__ opA, int8_t *__restrict__ opB, double *__restrict__ rsc,
-                 double *__restrict__ bt, double *__restrict__ wt) {
+                 double *__restrict__ bt, double *__restrict__ wt, const double *__restrict__ ampb,
+                 double *__restrict__ rscb) {
     const int bin = blockIdx.y;
     const BinLayout L = lay[bin];
     const int lane = threadIdx.x & 31;
@@ -114,32 +115,45 @@ psf_slice_kernel(Geo g, const double *__restrict__ dist, const double *__restric
     int8_t *B = opB + (size_t)L.r_off * kp * kBMat;
     if (r < L.nk) {
         const int s = keep_idx[(size_t)bin * g.S + r];
-        // power-of-two row scale from the amplitude bound |Re e|, |Im e| <= amp
-        double amax = 0.0;
-        for (int m = lane; m < M; m += 32) amax = fmax(amax, amp[(size_t)m * g.S + s]);
+        // power-of-two row scale from the amplitude bound |Re e|, |Im e| <= amp (per side: the
+        // paper-literal PSF has v on the A side and g on the B side)
+        auto scale_of = [&](const double *ap) {
+            double amax = 0.0;
+            for (int m = lane; m < M; m += 32) amax = fmax(amax, ap[(size_t)m * g.S + s]);
 #pragma unroll
-        for (int o = 16; o; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-        int e;
-        const double f = frexp(amax, &e);         // amax = f 2^e, f in [0.5, 1)
-        const int q = (f > 127.0 / 128.0) ? -e - 1 : -e;  // |v| 2^q <= 127/128
+            for (int o = 16; o; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+            int e;
+            const double f = frexp(amax, &e);         // amax = f 2^e, f in [0.5, 1)
+            return (f > 127.0 / 128.0) ? -e - 1 : -e;  // |v| 2^q <= 127/128
+        };
+        const double *apb = ampb ? ampb : amp;
+        const int q = scale_of(amp), qb = ampb ? scale_of(ampb) : q;
         const double kpi = 2.0 * freq[bin] / g.c0;   // k / pi: phase in half-turns
         for (int m = lane; m < M; m += 32) {
             const double d = dist[(size_t)m * g.S + s], a = amp[(size_t)m * g.S + s];
             double sn, cs;
             sincospi(kpi * d, &sn, &cs);
-            int dr[kSl], di[kSl];
+            int dr[kSl], di[kSl], gr[kSl], gi[kSl];
             const double er = a * cs, ei = -(a * sn);
             digits(ldexp(er, q), dr);
             digits(ldexp(ei, q), di);
+            if (ampb) {
+                const double ab = apb[(size_t)m * g.S + s];
+                digits(ldexp(ab * cs, qb), gr);
+                digits(ldexp(-(ab * sn), qb), gi);
+            } else {
+#pragma unroll
+                for (int t = 0; t < kSl; t++) { gr[t] = dr[t]; gi[t] = di[t]; }
+            }
             if (wt) wt[(size_t)L.r_off * M + (size_t)m * L.rp + r] = er * er + ei * ei;   // |e_mr|^2 (R20)
 #pragma unroll
             for (int t = 0; t < kSl; t++) {
                 A[opa_index(L.rp, t, r, m)] = (int8_t)dr[t];            // X_t = [Re; Im]
                 A[opa_index(L.rp, t, r, M + m)] = (int8_t)di[t];
-                B[opb_index(L.rp, t, 0, r, m)] = (int8_t)dr[t];
-                B[opb_index(L.rp, t, 0, r, M + m)] = (int8_t)di[t];
-                B[opb_index(L.rp, t, 1, r, m)] = (int8_t)(-di[t]);      // Z_t = [-Im; Re]
-                B[opb_index(L.rp, t, 1, r, M + m)] = (int8_t)dr[t];
+                B[opb_index(L.rp, t, 0, r, m)] = (int8_t)gr[t];
+                B[opb_index(L.rp, t, 0, r, M + m)] = (int8_t)gi[t];
+                B[opb_index(L.rp, t, 1, r, m)] = (int8_t)(-gi[t]);      // Z_t = [-Im; Re]
+                B[opb_index(L.rp, t, 1, r, M + m)] = (int8_t)gr[t];
             }
         }
         for (int kk = 2 * M + lane; kk < kp; kk += 32) {
@@ -152,6 +166,7 @@ psf_slice_kernel(Geo g, const double *__restrict__ dist, const double *__restric
         }
         if (lane == 0) {
             rsc[L.r_off + r] = ldexp(1.0, -2 * q - 35);
+            if (rscb) rscb[L.r_off + r] = ldexp(1.0, -2 * qb - 35);
             if (b) bt[L.v_off + r] = b[(size_t)bin * g.S + s];
         }
     } else {
@@ -167,6 +182,7 @@ psf_slice_kernel(Geo g, const double *__restrict__ dist, const double *__restric
         }
         if (lane == 0) {
             rsc[L.r_off + r] = 0.0;
+            if (rscb) rscb[L.r_off + r] = 0.0;
             if (b && r < L.sp) bt[L.v_off + r] = 0.0;
         }
     }
@@ -188,7 +204,10 @@ template <bool kDR>
 __global__ void __launch_bounds__(kPsfThreads, 1)
 psf_tc_kernel(int M, int kp, int n_tiles, const int4 *__restrict__ tiles, const BinLayout *__restrict__ lay,
               const int8_t *__restrict__ opA, const int8_t *__restrict__ opB, const double *__restrict__ rsc,
-              const double *__restrict__ wt, float *__restrict__ Aout, float *__restrict__ Adense) {
+              const double *__restrict__ wt, float *__restrict__ Aout, float *__restrict__ Adense,
+              const double *__restrict__ rscb) {
+    const bool paper = rscb != nullptr;   // asymmetric paper-literal PSF: every tile, transposed out
+    const double *rscc = paper ? rscb : rsc;   // column scales
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     PsfSmem &sm = *reinterpret_cast<PsfSmem *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -286,7 +305,7 @@ psf_tc_kernel(int M, int kp, int n_tiles, const int4 *__restrict__ tiles, const 
             const bool blk_ok = (tl.y * kTM + q * 32) < L.sp && j0 < L.sp;   // warp-uniform
             float *Ab = Aout + L.a_off;
             // rcol[bf] was last read for tile n-2, before every epilogue warp passed tile n-1's barrier
-            if (et < kTN) sm.rcol[bf][et] = rsc[L.r_off + min(j0 + et, L.rp - 1)];
+            if (et < kTN) sm.rcol[bf][et] = rscc[L.r_off + min(j0 + et, L.rp - 1)];
             asm volatile("bar.sync 1, 256;" ::: "memory");
             // diagonal removal (R20): Q_ij = sum_m |e_mi|^2 |e_mj|^2 in fp64 (row i per lane, the
             // 8 columns of a chunk are warp-uniform loads)
@@ -353,11 +372,14 @@ psf_tc_kernel(int M, int kp, int n_tiles, const int4 *__restrict__ tiles, const 
                         mir[1] = make_float4(v[4], v[5], v[6], v[7]);
                     }
                     if (Dn) {
-                        // dense row-major: row i (two float4 per lane), and the mirror column i
-                        // (rows j0+jc..+7, coalesced over the lanes)
-                        float4 *drow = reinterpret_cast<float4 *>(Dn + (size_t)i * L.sp + j0 + jc);
-                        drow[0] = make_float4(v[0], v[1], v[2], v[3]);
-                        drow[1] = make_float4(v[4], v[5], v[6], v[7]);
+                        // dense row-major: row i (two float4 per lane; not for the asymmetric
+                        // paper-literal PSF, which is stored transposed), and column i (rows
+                        // j0+jc..+7, coalesced over the lanes: the mirror, or the transpose)
+                        if (!paper) {
+                            float4 *drow = reinterpret_cast<float4 *>(Dn + (size_t)i * L.sp + j0 + jc);
+                            drow[0] = make_float4(v[0], v[1], v[2], v[3]);
+                            drow[1] = make_float4(v[4], v[5], v[6], v[7]);
+                        }
 #pragma unroll
                         for (int c = 0; c < 8; c++) Dn[(size_t)(j0 + jc + c) * L.sp + i] = v[c];
                     }
@@ -401,10 +423,11 @@ int psf_tile_cols() { return kTN; }
 int launch_psf(const Geo &g, const double *dist, const double *amp, int n_bins, const double *freq,
                const BinLayout *lay, const int32_t *keep_idx, const double *b, int max_rp, int n_tiles,
                const int4 *tiles, int8_t *opA, int8_t *opB, double *rsc, double *bt, double *wt, float *A,
-               float *Adense, cudaStream_t st) {
+               float *Adense, cudaStream_t st, const double *ampb, double *rscb) {
     const int kp = psf_kp(g.m);
     dim3 grid((max_rp + 7) / 8, n_bins);
-    psf_slice_kernel<<<grid, 256, 0, st>>>(g, dist, amp, freq, lay, keep_idx, b, kp, opA, opB, rsc, bt, wt);
+    psf_slice_kernel<<<grid, 256, 0, st>>>(g, dist, amp, freq, lay, keep_idx, b, kp, opA, opB, rsc, bt, wt, ampb,
+                                           rscb);
     if (cudaPeekAtLastError() != cudaSuccess) return -1;
     if (n_tiles <= 0) return 1;
     const size_t smem = sizeof(PsfSmem) + 1024;
@@ -418,10 +441,11 @@ int launch_psf(const Geo &g, const double *dist, const double *amp, int n_bins, 
                              (int)smem) != cudaSuccess)
         return -1;
     if (wt)
-        psf_tc_kernel<true><<<n_cta, kPsfThreads, smem, st>>>(g.m, kp, n_tiles, tiles, lay, opA, opB, rsc, wt, A, Adense);
+        psf_tc_kernel<true><<<n_cta, kPsfThreads, smem, st>>>(g.m, kp, n_tiles, tiles, lay, opA, opB, rsc, wt, A, Adense,
+                                                              nullptr);
     else
         psf_tc_kernel<false><<<n_cta, kPsfThreads, smem, st>>>(g.m, kp, n_tiles, tiles, lay, opA, opB, rsc, nullptr, A,
-                                                               Adense);
+                                                               Adense, rscb);
     return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
 }
 

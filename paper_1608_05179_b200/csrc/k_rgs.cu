@@ -675,21 +675,43 @@ int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int m
     return e == cudaSuccess ? 1 : -1;
 }
 
-// dwc_gs input conversion: dense row-major n x n (upper triangle read, reading R1) -> the
-// padded dense sp x sp matrix of the residual kernel.
-__global__ void rgs_convert_kernel(int n, int sp, const float *__restrict__ src, float *__restrict__ dense) {
+// dwc_gs input conversion: dense row-major n x n -> the padded dense sp x sp matrix of the
+// residual kernel: symmetric (reading R1): the upper triangle is read; general (the paper-literal
+// PSF): the transpose (the kernel reads column c of A as row c).
+__global__ void rgs_convert_kernel(int n, int sp, const float *__restrict__ src, float *__restrict__ dense, int general) {
     const long total = (long)sp * sp;
     for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
         const int i = (int)(e / sp), j = (int)(e - (long)(e / sp) * sp);
-        const int lo = min(i, j), hi = max(i, j);
-        dense[e] = (hi < n) ? src[(size_t)lo * n + hi] : 0.f;
+        if (general) {
+            dense[e] = (i < n && j < n) ? src[(size_t)j * n + i] : 0.f;
+        } else {
+            const int lo = min(i, j), hi = max(i, j);
+            dense[e] = (hi < n) ? src[(size_t)lo * n + hi] : 0.f;
+        }
     }
 }
 
-int launch_rgs_convert(int n, int sp, const float *src, float *dense, cudaStream_t st) {
+int launch_rgs_convert(int n, int sp, const float *src, float *dense, cudaStream_t st, int general) {
     const long total = (long)sp * sp;
     const int blocks = (int)std::min<long>((total + 255) / 256, 148L * 32);
-    rgs_convert_kernel<<<blocks, 256, 0, st>>>(n, sp, src, dense);
+    rgs_convert_kernel<<<blocks, 256, 0, st>>>(n, sp, src, dense, general);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+// dwc_psf (paper-literal): out[i][j] = src[j][i] (transpose = 1) or src[i][j], n x n out of the
+// padded sp x sp dense layout.
+__global__ void dense_extract_kernel(int n, int sp, const float *__restrict__ src, float *__restrict__ out, int transpose) {
+    const long total = (long)n * n;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
+        const int i = (int)(e / n), j = (int)(e - (long)(e / n) * n);
+        out[e] = transpose ? src[(size_t)j * sp + i] : src[(size_t)i * sp + j];
+    }
+}
+
+int launch_dense_extract(int n, int sp, const float *src, float *out, int transpose, cudaStream_t st) {
+    const long total = (long)n * n;
+    const int blocks = (int)std::min<long>((total + 255) / 256, 148L * 32);
+    dense_extract_kernel<<<blocks, 256, 0, st>>>(n, sp, src, out, transpose);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

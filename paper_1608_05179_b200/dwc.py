@@ -20,6 +20,7 @@ DWC_DIAG_REMOVAL = 4
 DWC_ALT_SWEEPS = 8
 DWC_GS_DENSE_STREAM = 16
 DWC_GS_RESIDUAL = 32
+DWC_PAPER_PSF = 64
 GS_KERNELS = {0: "none", 1: "cluster", 2: "cluster_xtra", 3: "alternating", 4: "residual"}
 STATUS = {0: "DWC_OK", -1: "DWC_EINVAL", -2: "DWC_ESINGULAR", -3: "DWC_ENUMERIC",
           -4: "DWC_ENOMEM", -5: "DWC_ECUDA", -6: "DWC_ESTATE"}
@@ -138,12 +139,13 @@ def _gs_kernel_flag(dense_stream) -> int:
     return DWC_GS_DENSE_STREAM if dense_stream else DWC_GS_RESIDUAL
 
 
-def _flags(full_grid: bool, order: int, dr: bool = False, alt: bool = False, dense_stream=None) -> int:
+def _flags(full_grid: bool, order: int, dr: bool = False, alt: bool = False, dense_stream=None,
+           paper: bool = False) -> int:
     if order not in (1, 3):
         raise ValueError("order must be 1 (linear predictor) or 3 (cubic)")
     return ((DWC_FULL_GRID if full_grid else 0) | (DWC_CUBIC if order == 3 else 0) |
             (DWC_DIAG_REMOVAL if dr else 0) | (DWC_ALT_SWEEPS if alt else 0) |
-            (0 if alt else _gs_kernel_flag(dense_stream)))
+            (0 if (alt or paper) else _gs_kernel_flag(dense_stream)) | (DWC_PAPER_PSF if paper else 0))
 
 
 def _stream(stream, device=None) -> int:
@@ -205,7 +207,7 @@ class Context:
     # ---- hot path ---------------------------------------------------------------
     def solve_band(self, geom: Geometry, freqs: Sequence[float], csm, epsilon: float, sweeps: int,
                    eps_mode: int = 0, full_grid: bool = False, want_b: bool = False, out=None, order: int = 1,
-                   stream=None, dr: bool = False, alt: bool = False, dense_stream=None):
+                   stream=None, dr: bool = False, alt: bool = False, dense_stream=None, paper: bool = False):
         """Batched S0..S8 on device tensors.  csm: cuda complex128 [K,M,M].
         Returns dict(n_keep int32[K], keep_idx int32[K,S], x_map float32[K,S], b_map, warn)."""
         import torch
@@ -223,7 +225,7 @@ class Context:
             _check_out(out, K, S, want_b, host=False, device=dev)
         warn = np.zeros(K, dtype=np.uint32)
         arr, grid = geom.c_array(), geom.c_grid()
-        prm = Params(float(epsilon), int(eps_mode), int(sweeps), _flags(full_grid, order, dr, alt, dense_stream))
+        prm = Params(float(epsilon), int(eps_mode), int(sweeps), _flags(full_grid, order, dr, alt, dense_stream, paper))
         _check(lib().dwc_solve_band(
             self._h, C.byref(arr), C.byref(grid), C.byref(prm), K, freqs.ctypes.data,
             _dev(csm, torch.complex128, "csm"), _dev(out["n_keep"], torch.int32, "n_keep"),
@@ -235,7 +237,7 @@ class Context:
 
     def solve_band_host(self, geom: Geometry, freqs, csm, epsilon: float, sweeps: int, eps_mode: int = 0,
                         full_grid: bool = False, want_b: bool = False, out=None, stream=None, order: int = 1,
-                        dr: bool = False, alt: bool = False, dense_stream=None):
+                        dr: bool = False, alt: bool = False, dense_stream=None, paper: bool = False):
         """Same as solve_band with host buffers (numpy or CPU tensors, pinned or not); the
         host<->device copies happen inside the C call, which returns when results are on the host."""
         import torch
@@ -253,7 +255,7 @@ class Context:
             _check_out(out, K, S, want_b, host=True)
         warn = np.zeros(K, dtype=np.uint32)
         arr, grid = geom.c_array(), geom.c_grid()
-        prm = Params(float(epsilon), int(eps_mode), int(sweeps), _flags(full_grid, order, dr, alt, dense_stream))
+        prm = Params(float(epsilon), int(eps_mode), int(sweeps), _flags(full_grid, order, dr, alt, dense_stream, paper))
         csm = csm.contiguous()
         _check(lib().dwc_solve_band_host(
             self._h, C.byref(arr), C.byref(grid), C.byref(prm), K, freqs.ctypes.data, csm.data_ptr(),
@@ -266,7 +268,7 @@ class Context:
     # ---- stage entry points ---------------------------------------------------------
     def solve_band_snapshots(self, geom: Geometry, freqs: Sequence[float], snap, epsilon: float, sweeps: int,
                              eps_mode: int = 0, full_grid: bool = False, want_b: bool = False, order: int = 1,
-                             stream=None, dr: bool = False, alt: bool = False, dense_stream=None):
+                             stream=None, dr: bool = False, alt: bool = False, dense_stream=None, paper: bool = False):
         """The path from snapshot spectra (Eq. 1 on the device).  snap: cuda complex128 [K,M,I]."""
         import torch
         freqs = np.ascontiguousarray(freqs, dtype=np.float64)
@@ -280,7 +282,7 @@ class Context:
                "b_map": torch.empty((K, S), dtype=torch.float64, device=dev) if want_b else None}
         warn = np.zeros(K, dtype=np.uint32)
         arr, grid = geom.c_array(), geom.c_grid()
-        prm = Params(float(epsilon), int(eps_mode), int(sweeps), _flags(full_grid, order, dr, alt, dense_stream))
+        prm = Params(float(epsilon), int(eps_mode), int(sweeps), _flags(full_grid, order, dr, alt, dense_stream, paper))
         _check(lib().dwc_solve_band_snapshots(
             self._h, C.byref(arr), C.byref(grid), C.byref(prm), K, freqs.ctypes.data, int(snap.shape[2]),
             _dev(snap, torch.complex128, "snap"), _dev(out["n_keep"], torch.int32, "n_keep"),
@@ -308,13 +310,14 @@ class Context:
                                _dev(idx, torch.int32, "idx"), _dev(E, torch.complex128, "E"), _stream(stream, self.device)))
         return E
 
-    def das(self, geom: Geometry, freqs, csm, stream=None, dr: bool = False):
+    def das(self, geom: Geometry, freqs, csm, stream=None, dr: bool = False, paper: bool = False):
         import torch
         freqs = np.ascontiguousarray(freqs, dtype=np.float64)
         b = torch.empty((len(freqs), geom.S), dtype=torch.float64, device=csm.device)
         arr, grid = geom.c_array(), geom.c_grid()
         _check(lib().dwc_das(self._h, C.byref(arr), C.byref(grid), len(freqs), freqs.ctypes.data,
-                             _dev(csm, torch.complex128, "csm"), DWC_DIAG_REMOVAL if dr else 0,
+                             _dev(csm, torch.complex128, "csm"),
+                             (DWC_DIAG_REMOVAL if dr else 0) | (DWC_PAPER_PSF if paper else 0),
                              _dev(b, torch.float64, "b"), _stream(stream, self.device)))
         return b
 
@@ -332,22 +335,23 @@ class Context:
                                   _dev(lev, torch.uint8, "level") if lev is not None else None, _stream(stream, self.device)))
         return nk, keep, lev
 
-    def psf(self, geom: Geometry, freq: float, keep_idx, stream=None, dr: bool = False):
+    def psf(self, geom: Geometry, freq: float, keep_idx, stream=None, dr: bool = False, paper: bool = False):
         import torch
         keep_idx = keep_idx.to(torch.int32).contiguous()
         n = keep_idx.numel()
         A = torch.empty((n, n), dtype=torch.float32, device=keep_idx.device)
         arr, grid = geom.c_array(), geom.c_grid()
         _check(lib().dwc_psf(self._h, C.byref(arr), C.byref(grid), float(freq), n,
-                             _dev(keep_idx, torch.int32, "keep_idx"), DWC_DIAG_REMOVAL if dr else 0,
+                             _dev(keep_idx, torch.int32, "keep_idx"),
+                             (DWC_DIAG_REMOVAL if dr else 0) | (DWC_PAPER_PSF if paper else 0),
                              _dev(A, torch.float32, "A"), _stream(stream, self.device)))
         return A
 
-    def gs(self, A, b, sweeps: int, stream=None, alt: bool = False, dense_stream=None):
+    def gs(self, A, b, sweeps: int, stream=None, alt: bool = False, dense_stream=None, general: bool = False):
         import torch
         n = A.shape[0]
         x = torch.empty(n, dtype=torch.float32, device=A.device)
-        fl = DWC_ALT_SWEEPS if alt else _gs_kernel_flag(dense_stream)
+        fl = DWC_PAPER_PSF if general else (DWC_ALT_SWEEPS if alt else _gs_kernel_flag(dense_stream))
         _check(lib().dwc_gs(self._h, n, _dev(A, torch.float32, "A"), _dev(b, torch.float64, "b"), int(sweeps),
                             fl, _dev(x, torch.float32, "x"), _stream(stream, self.device)))
         return x

@@ -490,7 +490,7 @@ def test_errors_flags_and_new_entry_points(ctx, torch_cuda):
     keep = torch.empty((1, g.S), dtype=torch.int32, device="cuda")
     x = torch.empty((1, g.S), dtype=torch.float32, device="cuda")
     f = np.array(band.freqs, dtype=np.float64)
-    prm = Params(0.1, 0, 5, 64)   # unknown flag bit
+    prm = Params(0.1, 0, 5, 128)   # unknown flag bit
     rc = lib().dwc_solve_band(ctx._h, C.byref(arr), C.byref(grid), C.byref(prm), 1, f.ctypes.data,
                               csm.data_ptr(), nk.data_ptr(), keep.data_ptr(), x.data_ptr(), None, None,
                               torch.cuda.current_stream().cuda_stream)
@@ -582,3 +582,73 @@ def test_batched_path_bitwise_deterministic_cfg3(dense):
         else:
             assert np.array_equal(x, ref)
     ctx.close()
+
+
+# ---------------------------------------------------------------------------- NEXT-4: paper-literal PSF
+@pytest.mark.parametrize("cfgname", ["cfg1", "cfg2"])
+def test_das_paper_parity(ctx, torch_cuda, oracle_lib, cfgname):
+    """The DAS map with Eq. 4's focus vector v against the oracle's or_das_paper."""
+    torch = torch_cuda
+    band = synth.make_band(cfgname)
+    g = geom_of(band)
+    b = ctx.das(g, band.freqs, torch.from_numpy(band.csm).cuda(), paper=True).cpu().numpy()
+    for k in range(len(band.freqs)):
+        ref = oracle_lib.das_paper(*oracle_args(g), band.freqs[k], band.csm[k])
+        assert rel_l2(b[k], ref) < 1e-12
+
+
+@pytest.mark.parametrize("m,n,nk", [(16, 21, 441), (24, 15, 33), (24, 15, 129), (13, 15, 100), (128, 21, 300)])
+def test_psf_paper_parity(ctx, torch_cuda, oracle_lib, m, n, nk):
+    """The asymmetric paper-literal PSF A_P = |V^H G|^2 / M^2 (Eq. 4 x Eq. 7) on every tile: the
+    exact int8-digit Gram with v on the A side and g on the B side, each with its own scales."""
+    torch = torch_cuda
+    g = small_geom(m, n, 3 if m % 3 == 0 else 1)
+    keep = np.sort(np.random.default_rng(nk).choice(g.S, size=nk, replace=False)).astype(np.int32)
+    A = ctx.psf(g, 5100.0, torch.from_numpy(keep).cuda(), paper=True).cpu().numpy()
+    ref = oracle_lib.psf_paper(*oracle_args(g), 5100.0, keep)
+    assert rel_l2(A, ref) < 1e-7
+    assert np.max(np.abs(A - ref)) <= 2.0 ** -23 * max(1.0, np.abs(ref).max())
+    if nk > 1:
+        assert np.max(np.abs(A - A.T)) > 1e-4          # really asymmetric
+    assert np.max(np.abs(np.diag(A) - 1.0)) < 1e-6
+
+
+@pytest.mark.parametrize("nk,sweeps", [(1, 3), (33, 40), (130, 60), (441, 40)])
+def test_gs_general_matrix_parity(ctx, torch_cuda, oracle_lib, nk, sweeps):
+    """Forward sweeps on a general (paper-literal, asymmetric) matrix: the residual kernel on the
+    transpose, against the oracle's Eq. 13-14 loop."""
+    torch = torch_cuda
+    band = synth.make_band("cfg1")
+    g = geom_of(band)
+    f = band.freqs[0]
+    b_full = oracle_lib.das_paper(*oracle_args(g), f, band.csm[0])
+    keep = np.sort(np.argsort(-b_full)[:nk]).astype(np.int32)
+    A = oracle_lib.psf_paper(*oracle_args(g), f, keep)
+    bt = b_full[keep]
+    ref = oracle_lib.gs(A, bt, sweeps)
+    x = ctx.gs(torch.from_numpy(A.astype(np.float32)).cuda(), torch.from_numpy(bt).cuda(), sweeps,
+               general=True).cpu().numpy()
+    assert ctx.stats()["gs_kernel"] == 4
+    assert x.min() >= 0
+    assert rel_l2(x, ref) < TOL_X, rel_l2(x, ref)
+    assert abs(x.sum() - ref.sum()) < TOL_P * ref.sum()
+
+
+@pytest.mark.parametrize("cfgname,bins,sweeps", [("cfg1", None, 100), ("cfg2", [0, 3, 7], 300)])
+def test_e2e_paper_mode(ctx, torch_cuda, oracle_lib, cfgname, bins, sweeps):
+    """NEXT-4 end to end: Eq. 4 beamformer, Alg. 1 on its map, the asymmetric Eq. 4 x Eq. 7 PSF,
+    forward sweeps -- keep sets bit-exact, maps within the north_star tolerances."""
+    torch = torch_cuda
+    band = synth.make_band(cfgname, bins=bins)
+    cfg = band.cfg
+    g = geom_of(band)
+    out = ctx.solve_band(g, band.freqs, torch.from_numpy(band.csm).cuda(), cfg.epsilon, sweeps, cfg.eps_mode,
+                         want_b=True, paper=True)
+    assert ctx.stats()["gs_kernel"] == 4
+    rnk, rkeep, rx, rb = oracle_lib.solve_band_cfg(band, sweeps=sweeps, paper=True)
+    for k in range(len(band.freqs)):
+        assert rel_l2(out["b_map"][k].cpu().numpy(), rb[k]) < 1e-12
+        assert np.array_equal(out["keep_idx"][k].cpu().numpy(), rkeep[k])
+        x = out["x_map"][k].cpu().numpy()
+        assert rel_l2(x, rx[k]) < TOL_X, (k, rel_l2(x, rx[k]))
+        assert abs(x.sum() - rx[k].sum()) <= TOL_P * rx[k].sum()
