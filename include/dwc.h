@@ -102,8 +102,9 @@ typedef struct {
  * Uncorrelated microphone noise (a diagonal CSM term) then drops out of the map. */
 #define DWC_DIAG_REMOVAL 4
 /* DWC_ALT_SWEEPS: alternating sweep directions (original DAMAS practice; reading
- * R21): sweep 2p in ascending row order (Eq. 13-14), sweep 2p+1 descending.  Runs a simpler
- * one-CTA-per-bin kernel (a fidelity-study variant, not the tuned path). */
+ * R21): sweep 2p in ascending row order (Eq. 13-14), sweep 2p+1 descending.  Runs on the kernel
+ * the choice below picks: the residual kernel walks the alternating visit sequence; in place of
+ * the dense-stream kernel a simpler one-CTA-per-bin kernel runs (DWC_GS_KERNEL_ALT). */
 #define DWC_ALT_SWEEPS 8
 /* Gauss-Seidel kernel of the forward sweeps (both keep Eq. 13-14's row and sweep order exactly and
  * differ in summation order only):
@@ -121,7 +122,7 @@ typedef struct {
  * A_P[i][j] = |v_i^H g_j|^2 / M^2 with Eq. 7's g_m = (|r|/d_m) e^{-jkd_m}, |r| the
  * distance to the array centre (the origin).  A_P is not symmetric: the PSF covers
  * every tile, the sweeps (Eq. 13-14, forward) run on the residual kernel with A_P stored
- * transposed.  Not with DWC_DIAG_REMOVAL, DWC_ALT_SWEEPS or DWC_GS_DENSE_STREAM (DWC_EINVAL).
+ * transposed.  Not with DWC_DIAG_REMOVAL or DWC_GS_DENSE_STREAM (DWC_EINVAL); with DWC_ALT_SWEEPS.
  * The sweeps' convergence is not guaranteed (A_P has an indefinite symmetric part). */
 #define DWC_PAPER_PSF 64
 #define DWC_MAX_MICS 512
@@ -209,8 +210,8 @@ DWC_API dwc_status dwc_psf(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *g
  * PAPER.md:167-180; alternating directions: SPEC.md:308, reading R21).
  * A dev float[n*n] row-major, symmetric (as A~ is, reading R1) with A_ii > 0: only the upper
  * triangle (j >= i) is read, the lower one is taken as its transpose -- unless flags has
- * DWC_PAPER_PSF: then A is a general matrix (the paper-literal PSF), read in full, forward sweeps
- * on the residual kernel.
+ * DWC_PAPER_PSF: then A is a general matrix (the paper-literal PSF), read in full, sweeps on the
+ * residual kernel.
  * flags: 0, DWC_ALT_SWEEPS, DWC_GS_DENSE_STREAM / DWC_GS_RESIDUAL (kernel choice), DWC_PAPER_PSF;
  * b dev double[n], x dev float[n] (out).
  * Errors: DWC_EINVAL (n < 1, sweeps < 1, NULL, unknown flags, n beyond the on-chip x capacity),
@@ -266,8 +267,8 @@ typedef struct {
 #define DWC_GS_KERNEL_NONE 0
 #define DWC_GS_KERNEL_CLUSTER 1       /* dense-stream cluster kernel, fixed shared-memory ring   */
 #define DWC_GS_KERNEL_CLUSTER_XTRA 2  /* the same with extra ring tiles behind its tables        */
-#define DWC_GS_KERNEL_ALT 3           /* alternating-direction sweeps (DWC_ALT_SWEEPS)           */
-#define DWC_GS_KERNEL_RESIDUAL 4      /* residual-update kernel (the default forward sweeps)     */
+#define DWC_GS_KERNEL_ALT 3           /* one-CTA-per-bin alternating sweeps (ALT + DENSE_STREAM) */
+#define DWC_GS_KERNEL_RESIDUAL 4      /* residual-update kernel (either sweep order)             */
 
 DWC_API dwc_status dwc_set_timing(dwc_ctx *ctx, int enable);
 DWC_API dwc_status dwc_get_stats(dwc_ctx *ctx, dwc_stats *out);

@@ -213,8 +213,8 @@ dwc_status check_params(const dwc_params *p) {
         return fail(DWC_EINVAL, "unknown flags 0x%x", p->flags);
     if ((p->flags & DWC_GS_DENSE_STREAM) && (p->flags & DWC_GS_RESIDUAL))
         return fail(DWC_EINVAL, "DWC_GS_DENSE_STREAM and DWC_GS_RESIDUAL exclude each other");
-    if ((p->flags & DWC_PAPER_PSF) && (p->flags & (DWC_DIAG_REMOVAL | DWC_GS_DENSE_STREAM | DWC_ALT_SWEEPS)))
-        return fail(DWC_EINVAL, "DWC_PAPER_PSF runs forward sweeps on the residual kernel, without diagonal removal");
+    if ((p->flags & DWC_PAPER_PSF) && (p->flags & (DWC_DIAG_REMOVAL | DWC_GS_DENSE_STREAM)))
+        return fail(DWC_EINVAL, "DWC_PAPER_PSF runs on the residual kernel, without diagonal removal");
     return DWC_OK;
 }
 
@@ -358,8 +358,11 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
     // stream over 4 SMs)
     int band_sp = 0;
     for (int k = 0; k < n_bins; k++) band_sp = std::max(band_sp, (hk[k] + 31) & ~31);
-    const bool resid = paper || (!(p->flags & DWC_ALT_SWEEPS) &&
-                       ((p->flags & DWC_GS_RESIDUAL) || (!(p->flags & DWC_GS_DENSE_STREAM) && band_sp <= rgs_auto_max_sp())));
+    // (alternating sweeps: the residual kernel's visit sequence; the one-CTA-per-bin alternating
+    // kernel only when the dense-stream kernel is asked for or the systems are too large)
+    const bool resid = paper ||
+                       ((p->flags & DWC_GS_RESIDUAL) || (!(p->flags & DWC_GS_DENSE_STREAM) && band_sp <= rgs_auto_max_sp()));
+    const int alt = (p->flags & DWC_ALT_SWEEPS) ? 1 : 0;
     int64_t a_off = 0, v_off = 0, r_off = 0, d_off = 0;
     int max_sp = 0, max_rp = 0, ystride = 0;
     double sum_sq = 0.0, sum_sym = 0.0;
@@ -449,7 +452,7 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
         CU(cudaMemsetAsync(ctx->upd.p, 0, 64, st));
         LAUNCH(launch_rgs(n_bins, (int *)ctx->order.p, (BinLayout *)ctx->lay.p, max_sp, (int *)ctx->counter.p,
                           (float *)ctx->Ad.p, (double *)ctx->bt.p, p->sweeps, nullptr, x_map, keep_idx,
-                          S, ctx->num_sms, (unsigned long long *)ctx->upd.p, st, &gsi));
+                          S, ctx->num_sms, (unsigned long long *)ctx->upd.p, st, &gsi, alt));
     } else if (p->flags & DWC_ALT_SWEEPS) {
         gsi.kernel = DWC_GS_KERNEL_ALT;
         gsi.ctas = n_bins;
@@ -794,11 +797,10 @@ dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int3
         return fail(DWC_EINVAL, "DWC_GS_DENSE_STREAM and DWC_GS_RESIDUAL exclude each other");
     // DWC_PAPER_PSF: A is a general (asymmetric) matrix, read in full; residual kernel
     const bool general = (flags & DWC_PAPER_PSF) != 0;
-    if (general && (flags & (DWC_ALT_SWEEPS | DWC_GS_DENSE_STREAM)))
-        return fail(DWC_EINVAL, "a general (DWC_PAPER_PSF) matrix runs forward sweeps on the residual kernel");
+    if (general && (flags & DWC_GS_DENSE_STREAM))
+        return fail(DWC_EINVAL, "a general (DWC_PAPER_PSF) matrix runs on the residual kernel");
     const int sp = (n + 31) & ~31;
-    const bool resid = general || (!(flags & DWC_ALT_SWEEPS) &&
-                       ((flags & DWC_GS_RESIDUAL) || (!(flags & DWC_GS_DENSE_STREAM) && sp <= rgs_auto_max_sp())));
+    const bool resid = general || (flags & DWC_GS_RESIDUAL) || (!(flags & DWC_GS_DENSE_STREAM) && sp <= rgs_auto_max_sp());
     if (resid ? rgs_smem_bytes(sp) > 227 * 1024 : gs_smem_bytes(sp, gs_ystride(n)) > 227 * 1024)
         return fail(DWC_EINVAL, "n = %d exceeds the on-chip x capacity", n);
     cudaStream_t st = (cudaStream_t)cuda_stream;
@@ -845,7 +847,7 @@ dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int3
     stt.sum_keep = n;
     stt.sum_keep_sq = (double)n * n;
     stt.gs_bytes = 2.0 * (double)n * (n + 1) * sweeps;
-    if (flags & DWC_ALT_SWEEPS) {
+    if ((flags & DWC_ALT_SWEEPS) && !resid) {
         LAUNCH(launch_gs_alt(1, (BinLayout *)ctx->lay.p, sp, Ap, (double *)ctx->gs_b.p, sweeps, x, nullptr, nullptr,
                              0, st));
         stt.gs_kernel = DWC_GS_KERNEL_ALT;
@@ -858,7 +860,7 @@ dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int3
         CU(cudaMemsetAsync(ctx->upd.p, 0, 64, st));
         LAUNCH(launch_rgs(1, (int *)ctx->order.p, (BinLayout *)ctx->lay.p, sp, (int *)ctx->counter.p,
                           (float *)ctx->Ad.p, (double *)ctx->gs_b.p, sweeps, x, nullptr, nullptr, 0, ctx->num_sms,
-                          (unsigned long long *)ctx->upd.p, st, &gsi));
+                          (unsigned long long *)ctx->upd.p, st, &gsi, (flags & DWC_ALT_SWEEPS) ? 1 : 0));
         ctx->stats_upd_valid = true;
     } else {
         LAUNCH(launch_gs_prep(1, sp, (BinLayout *)ctx->lay.p, Ap, (double *)ctx->gs_b.p, ctx->packets.p, st));

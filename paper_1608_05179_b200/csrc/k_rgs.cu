@@ -168,6 +168,16 @@ __device__ __forceinline__ unsigned long long clk() {
     return t;
 }
 
+// The visit sequence (reading R21 for alternating sweeps): global step s visits block
+// blk(s) = pos or T-1-pos (pos = s mod T; descending on odd sweeps when alt).  win_blk gives the
+// block of step s+d (0 <= d < T) from s's (sweep p, position pos) without a division.
+__device__ __forceinline__ bool sweep_fwd(int p, int alt) { return !(alt && (p & 1)); }
+__device__ __forceinline__ int win_blk(int p, int pos, int d, int T, int alt) {
+    int q = pos + d, pp = p;
+    if (q >= T) { q -= T; pp++; }
+    return sweep_fwd(pp, alt) ? q : T - 1 - q;
+}
+
 // Row-ring batching, identical in the row producer and the stream warps: the changes of a step
 // are cut into units (row e, segment g) of seg floats (the last segment of a row shorter); one
 // batch = up to upb units = one ring slot.
@@ -196,6 +206,7 @@ constexpr int kProfItems = 1024;   // then per item: start, end (globaltimer ns)
 
 // r (fp64, sp), the pending carried contributions (fp64, 16 blocks), x (fp32, sp), the prediction
 // masks (T words) and the row ring (kNSlot slots of slot_floats) follow RgsSmem.
+template <bool ALT>
 __global__ void __launch_bounds__(kRThreads, 2)
 rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restrict__ lay, int *__restrict__ counter,
            const float *__restrict__ Adense, const double *__restrict__ bt, int sweeps, float *__restrict__ x_out,
@@ -214,6 +225,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
     float *ring = reinterpret_cast<float *>(pmask + ((max_sp / 32 + 31) & ~31));   // 128-byte aligned
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     unsigned long long my_updates = 0, my_bytes = 0;
+    constexpr int alt = ALT ? 1 : 0;   // forward sweeps: the visit sequence folds to pos, pos+1, ...
 
     for (;;) {
         if (tid == 0) sh.item = atomicAdd(counter, 1);
@@ -269,39 +281,46 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
             // one bulk copy per panel cost ~80 cycles of issue on a single lane)
             unsigned long long pw_wait = 0, pw_issue = 0;
             float dnext = (!use_ivs && lane < nk) ? __ldg(Ad + (size_t)lane * sp + lane) : 1.f;
-            for (int s = 0, k = 0; s < total; s++, k = (k + 1 == T) ? 0 : k + 1) {
+            for (int s = 0, p = 0, pos = 0; s < total; s++, pos = (pos + 1 == T) ? 0 : pos + 1, p += (pos == 0)) {
+                const int k = sweep_fwd(p, alt) ? pos : T - 1 - pos;
                 const int sl = s % kRStg;
                 const unsigned long long t0 = pf ? clk() : 0ull;
                 mbar_wait(&sh.stg_empty[sl], ((s / kRStg) & 1) ^ 1);
                 const unsigned long long t1 = pf ? clk() : 0ull;
-                // the mask of block k as the solver left it at the previous visit (a hint: for
-                // T <= kRStg the solver may be updating it right now, either value is valid)
+                // the mask of block k as the solver left it at the previous visit (a hint: the
+                // solver may be updating it right now when the block was visited < kRStg steps
+                // ago, either value is valid)
                 unsigned m = *(volatile unsigned *)&pmask[k];
                 unsigned st = 0;
                 for (int n = 0; m && n < kNP; n++) {
                     st |= m & (0u - m);   // lowest set bit
                     m &= m - 1;
                 }
-                const int c0 = 32 * k, q4 = pw >> 2;   // 16-byte pieces per panel
+                // panel segment d (pieces 8d .. 8d+7) holds the columns of the block of step s+d
+                const int q4 = pw >> 2;   // 16-byte pieces per panel
+                const int d0 = lane >> 3, d1 = d0 + 4;
+                const int cb0 = 32 * win_blk(p, pos, d0, T, alt) + 4 * (lane & 7);
+                const int cb1 = 32 * win_blk(p, pos, d1 < T ? d1 : 0, T, alt) + 4 * (lane & 7);
                 unsigned mm = st;
                 for (int j = 0; mm; j++) {
                     const int t = __ffs(mm) - 1;
                     mm &= mm - 1;
-                    const float *rowp = Ad + (size_t)(c0 + t) * sp;
-                    for (int pc = lane; pc < q4; pc += 32) {
-                        int col = c0 + 4 * pc;
-                        if (col >= sp) col -= sp;   // the window wraps (a piece never straddles sp)
-                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&sh.panel[sl][j][4 * pc])),
-                                     "l"(rowp + col)
+                    const float *rowp = Ad + (size_t)(32 * k + t) * sp;
+                    if (lane < q4)
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&sh.panel[sl][j][4 * lane])),
+                                     "l"(rowp + cb0)
                                      : "memory");
-                    }
+                    if (lane + 32 < q4)
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&sh.panel[sl][j][4 * lane + 128])),
+                                     "l"(rowp + cb1)
+                                     : "memory");
                 }
                 // 1/A_ii of the block's rows, as the dense-stream kernel forms it (padding rows: 0);
-                // the diagonal of the next block is loaded one step ahead
+                // the diagonal of the next step's block is loaded one step ahead
                 if (!use_ivs) {
-                    const int rw = c0 + lane;
+                    const int rw = 32 * k + lane;
                     sh.sinv[sl][lane] = (rw < nk) ? __frcp_rn(dnext) : 0.f;
-                    const int rn = (k + 1 == T) ? lane : rw + 32;
+                    const int rn = 32 * win_blk(p, pos, 1 < T ? 1 : 0, T, alt) + lane;
                     dnext = (rn < nk) ? __ldg(Ad + (size_t)rn * sp + rn) : 1.f;
                 }
                 // each lane's copies complete on stg_full (32 async arrivals + lane 0's below)
@@ -369,18 +388,37 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
 #pragma unroll
             for (int d = 0; d < kRgsWin; d++) carry[d] = 0.f;
             unsigned long long tt = 0, tsd = 0, tl = 0, tr = 0, nch = 0, nmiss = 0;
-            for (int s = 0, k = 0; s < total; s++, k = (k + 1 == T) ? 0 : k + 1) {
+            for (int s = 0, p = 0, pos = 0; s < total; s++, pos = (pos + 1 == T) ? 0 : pos + 1, p += (pos == 0)) {
                 const unsigned long long t0 = pf ? clk() : 0ull;
+                const bool fwd = sweep_fwd(p, alt);
+                const int k = fwd ? pos : T - 1 - pos;
                 const int sl = s % kRStg, li = s % kNList;
                 const int row = 32 * k + lane;
                 float xo = xs[row];
+                // the blocks of the next nsub steps: the carry of step s + d goes to wb[d] only at its
+                // first occurrence in the window (a block visited twice in the window -- the turn of
+                // alternating sweeps -- gets the contribution committed at its first visit)
+                int wb[kRgsWin + 1];
+                unsigned vmask = (1u << nsub) - 1u;   // bit d-1: step s+d is the first visit of its block in the window
+#pragma unroll
+                for (int d = 0; d <= kRgsWin; d++) wb[d] = (d <= nsub) ? win_blk(p, pos, d, T, alt) : -1;
+                // alternating sweeps (the window holds at most one turn, nsub < T): step s+dt is the
+                // first of the next sweep, which walks the blocks back, so step s+d (d >= dt) revisits
+                // the block of step s+2dt-1-d: not a first occurrence for dt <= d <= 2dt-2.  Block k
+                // itself was last visited at step s-2pos-1 (the previous sweep's mirror position).
+                int vprev = -1;   // the last visit of block k within the window behind, else -1
+                if (ALT) {
+                    const int dt = T - pos;
+                    if (dt <= nsub && dt >= 2) vmask &= ~(((1u << (dt - 1)) - 1u) << (dt - 1));
+                    if (p >= 1 && 2 * pos + 1 <= nsub) vprev = s - 2 * pos - 1;
+                }
                 mbar_wait(&sh.stg_full[sl], (s / kRStg) & 1);
                 const unsigned smk = sh.smask[sl];
                 const float invd = use_ivs ? ivs[row] : sh.sinv[sl][lane];
                 // this lane's panel slot (its rank among the staged rows), -1 if not staged
                 const int myp = ((smk >> lane) & 1u) ? __popc(smk & ((1u << lane) - 1u)) : -1;
                 const unsigned long long t1 = pf ? clk() : 0ull;
-                const int sw = s - nsub - 1;   // the stream step the stored r of this block needs
+                const int sw = max(s - nsub - 1, vprev);   // the stream step the stored r of this block needs
                 if (sw >= 0) mbar_wait(&sh.sdone[sw % kNList], (sw / kNList) & 1);
                 const unsigned long long t2 = pf ? clk() : 0ull;
                 float ac = (float)rs[row] + carry[0];
@@ -388,14 +426,14 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
 #pragma unroll
                 for (int d = 0; d < kRgsWin; d++) acc[d] = 0.f;
                 RgsEntry *lst = sh.list[li];
-                int pos = 0, q = 0;
+                int pos_r = fwd ? 0 : 31, q = 0;   // next row of the block in sweep order
                 unsigned chg = 0;
                 for (;;) {
                     const float w = -ac * invd;
                     const float xn = xo + fmaxf(w, -xo);   // = max(xo - ac/A_ii, 0)
-                    const unsigned m = __ballot_sync(0xffffffffu, lane >= pos && xn != xo);
+                    const unsigned m = __ballot_sync(0xffffffffu, (fwd ? lane >= pos_r : lane <= pos_r) && xn != xo);
                     if (m == 0u) break;
-                    const int t = __ffs(m) - 1;
+                    const int t = fwd ? __ffs(m) - 1 : 31 - __clz(m);
                     const float xn_t = __shfl_sync(0xffffffffu, xn, t);
                     const float xo_t = __shfl_sync(0xffffffffu, xo, t);
                     const int pt = __shfl_sync(0xffffffffu, myp, t);
@@ -406,7 +444,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                         lst[q].c = row;
                         xo = xn;
                     }
-                    // panel of row t: element 32d + lane = A[32k+t][32(k+d)+lane] = A[32(k+d)+lane][32k+t]
+                    // panel of row t: element 32d + lane = A[32k+t][32 wb[d] + lane] = A[32 wb[d] + lane][32k+t]
                     float pv[kRgsWin + 1];
                     if (pt >= 0) {
                         const float *pr = sh.panel[sl][pt];
@@ -416,18 +454,15 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                         // not predicted: the panel from global memory (L2/HBM latency, rare)
                         const float *rw = Ad + (size_t)(32 * k + t) * sp;
 #pragma unroll
-                        for (int d = 0; d <= kRgsWin; d++) {
-                            int b = k + d;
-                            if (b >= T) b -= T;
-                            pv[d] = (d <= nsub) ? __ldg(rw + 32 * b + lane) : 0.f;
-                        }
+                        for (int d = 0; d <= kRgsWin; d++) pv[d] = (d <= nsub) ? __ldg(rw + 32 * wb[d] + lane) : 0.f;
                         nmiss++;
                     }
                     ac = fmaf(pv[0], dv, ac);
 #pragma unroll
-                    for (int d = 0; d < kRgsWin; d++) acc[d] = fmaf(pv[d + 1], dv, acc[d]);
+                    for (int d = 0; d < kRgsWin; d++)   // (forward: pv = 0 beyond nsub)
+                        if (!ALT || ((vmask >> d) & 1u)) acc[d] = fmaf(pv[d + 1], dv, acc[d]);
                     chg |= 1u << t;
-                    pos = t + 1;
+                    pos_r = fwd ? t + 1 : t - 1;
                     q++;
                 }
                 const unsigned long long t3 = pf ? clk() : 0ull;
@@ -457,7 +492,15 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
             const int w = (wid < 4) ? wid : 4;
             unsigned long long tlw = 0, tbw = 0, tap = 0, nb_all = 0;
             int b = 0;
-            for (int s = 0, k = 0; s < total; s++, k = (k + 1 == T) ? 0 : k + 1) {
+            for (int s = 0, p = 0, pos = 0; s < total; s++, pos = (pos + 1 == T) ? 0 : pos + 1, p += (pos == 0)) {
+                const int k = sweep_fwd(p, alt) ? pos : T - 1 - pos;
+                // the blocks of the next nsub steps (their contributions wait in pend for that
+                // step's visit; first occurrence only, see the solver)
+                int wb[kRgsWin + 1];
+                if (ALT) {
+#pragma unroll
+                    for (int d = 1; d <= kRgsWin; d++) wb[d] = (d <= nsub) ? win_blk(p, pos, d, T, alt) : -1;
+                }
                 const int li = s % kNList;
                 const unsigned long long t0 = pf ? clk() : 0ull;
                 // the row producer arrives dxready after it observed the solver's dready (the list
@@ -508,9 +551,17 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                                 on[i] = qq < q1 && col < sp;
                                 cc[i] = (qq < q1) ? 128 * qq : 128 * qp;   // a chunk of this segment
                                 const int ce = cc[i] + 4 * lane, blk = ce >> 5;
-                                int o = blk - k;   // block offset from k: 1..nsub are carried
-                                if (o < 0) o += T;
-                                tg[i] = (o >= 1 && o <= nsub) ? pend + 32 * ((s + o) & (kPendBlk - 1)) + (ce & 31) : rs + ce;
+                                int o = 0;   // the first step s+o (1 <= o <= nsub) that visits blk, else 0
+                                if (ALT) {
+#pragma unroll
+                                    for (int d = kRgsWin; d >= 1; d--)
+                                        if (wb[d] == blk) o = d;
+                                } else {   // forward: step s+o visits block k+o (mod T)
+                                    o = blk - k;
+                                    if (o < 0) o += T;
+                                    if (o > nsub) o = 0;
+                                }
+                                tg[i] = (o >= 1) ? pend + 32 * ((s + o) & (kPendBlk - 1)) + (ce & 31) : rs + ce;
                                 const double2 *rp = reinterpret_cast<const double2 *>(tg[i]);
                                 ra[i] = rp[0];
                                 rb[i] = rp[1];
@@ -594,7 +645,7 @@ size_t rgs_smem_bytes(int max_sp) { return rgs_base_bytes(max_sp) + kNSlot * 128
 int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int max_sp, int *counter,
                const float *Adense, const double *bt, int sweeps, float *x_out, float *x_map,
                const int32_t *keep_idx, int S, int num_sms, unsigned long long *n_updates, cudaStream_t st,
-               GsLaunchInfo *info) {
+               GsLaunchInfo *info, int alt) {
     // 1/A_ii in shared memory for the whole system when a ring of >= 24 KB still fits beside it
     const int use_ivs = (rgs_base_bytes(max_sp) + (size_t)max_sp * 4 + 24 * 1024 + 1536 <= 227 * 1024) ? 1 : 0;
     const size_t base = (rgs_base_bytes(max_sp) + (use_ivs ? (size_t)max_sp * 4 : 0) + 127) / 128 * 128;
@@ -616,10 +667,11 @@ int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int m
     const int slot_floats = (int)(ring / (4 * kNSlot)) / 128 * 128;   // floats per ring slot
     if (slot_floats < 128) return -1;
     const size_t smem = base + (size_t)slot_floats * 4 * kNSlot + 512;   // + slack: a row's last chunk reads past it
-    if (cudaFuncSetAttribute(rgs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    const auto kern = alt ? rgs_kernel<true> : rgs_kernel<false>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return -1;
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rgs_kernel, kRThreads, smem) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRThreads, smem) != cudaSuccess ||
         per_sm < 1) {
         cudaGetLastError();
         per_sm = 1;
@@ -642,8 +694,8 @@ int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int m
         if (cudaMalloc(&prof, pb) != cudaSuccess) return -1;
         cudaMemsetAsync(prof, 0, pb, st);
     }
-    rgs_kernel<<<grid, kRThreads, smem, st>>>(n_bins, order_dev, lay_dev, counter, Adense, bt, sweeps, x_out, x_map,
-                                              keep_idx, S, max_sp, slot_floats, use_ivs, n_updates, prof);
+    kern<<<grid, kRThreads, smem, st>>>(n_bins, order_dev, lay_dev, counter, Adense, bt, sweeps, x_out, x_map,
+                                        keep_idx, S, max_sp, slot_floats, use_ivs, n_updates, prof);
     const cudaError_t e = cudaPeekAtLastError();
     if (profile) {
         static unsigned long long h[kProfSlots + 4 * kProfItems + 2];

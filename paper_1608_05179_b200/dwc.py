@@ -145,7 +145,7 @@ def _flags(full_grid: bool, order: int, dr: bool = False, alt: bool = False, den
         raise ValueError("order must be 1 (linear predictor) or 3 (cubic)")
     return ((DWC_FULL_GRID if full_grid else 0) | (DWC_CUBIC if order == 3 else 0) |
             (DWC_DIAG_REMOVAL if dr else 0) | (DWC_ALT_SWEEPS if alt else 0) |
-            (0 if (alt or paper) else _gs_kernel_flag(dense_stream)) | (DWC_PAPER_PSF if paper else 0))
+            (0 if paper else _gs_kernel_flag(dense_stream)) | (DWC_PAPER_PSF if paper else 0))
 
 
 def _stream(stream, device=None) -> int:
@@ -351,7 +351,7 @@ class Context:
         import torch
         n = A.shape[0]
         x = torch.empty(n, dtype=torch.float32, device=A.device)
-        fl = DWC_PAPER_PSF if general else (DWC_ALT_SWEEPS if alt else _gs_kernel_flag(dense_stream))
+        fl = DWC_PAPER_PSF if general else ((DWC_ALT_SWEEPS if alt else 0) | _gs_kernel_flag(dense_stream))
         _check(lib().dwc_gs(self._h, n, _dev(A, torch.float32, "A"), _dev(b, torch.float64, "b"), int(sweeps),
                             fl, _dev(x, torch.float32, "x"), _stream(stream, self.device)))
         return x

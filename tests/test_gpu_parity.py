@@ -233,7 +233,7 @@ def _e2e(ctx, torch, oracle_lib, band, sweeps=None, full=False, check_b=True, or
     out = ctx.solve_band(g, band.freqs, torch.from_numpy(band.csm).cuda(), cfg.epsilon, sw, cfg.eps_mode,
                          full_grid=full, want_b=True, order=order, dr=dr, alt=alt, dense_stream=dense)
     kern = ctx.stats()["gs_kernel"]
-    assert kern == (3 if alt else (4 if not dense else kern)) and kern != 0
+    assert kern == ((3 if dense else 4) if alt else (4 if not dense else kern)) and kern != 0
     nk = out["n_keep"].cpu().numpy()
     keep = out["keep_idx"].cpu().numpy()
     x = out["x_map"].cpu().numpy()
@@ -453,10 +453,14 @@ def test_e2e_cfg2_diag_removal(ctx, torch_cuda, oracle_lib):
 
 
 # ---------------------------------------------------------------------------- NEXT-4: alternating sweeps
-@pytest.mark.parametrize("nk,sweeps", [(1, 3), (31, 40), (33, 41), (130, 100), (300, 200)])
-def test_gs_alternating_parity(ctx, torch_cuda, oracle_lib, nk, sweeps):
+@pytest.mark.parametrize("dense", [False, True], ids=["residual", "alt_kernel"])
+@pytest.mark.parametrize("nk,sweeps", [(1, 3), (31, 40), (33, 41), (64, 30), (97, 31), (130, 100), (257, 61),
+                                       (300, 200)])
+def test_gs_alternating_parity(ctx, torch_cuda, oracle_lib, nk, sweeps, dense):
     """Alternating forward/backward sweeps (R21) on oracle PSF systems (odd sweep counts end on
-    a forward sweep, even ones on a backward sweep)."""
+    a forward sweep, even ones on a backward sweep): the residual kernel's visit sequence (T = 1,
+    2, 3, 4, 5, 9, 10 blocks: turns inside and beyond its 7-block carry window) and the
+    one-CTA-per-bin alternating kernel."""
     torch = torch_cuda
     g = small_geom(24, 19, 3)
     rng = np.random.default_rng(nk)
@@ -465,14 +469,33 @@ def test_gs_alternating_parity(ctx, torch_cuda, oracle_lib, nk, sweeps):
     b = A @ np.abs(rng.standard_normal(nk)) + 0.01 * rng.standard_normal(nk)
     ref = oracle_lib.gs(A, b, sweeps, alt=True)
     x = ctx.gs(torch.from_numpy(A.astype(np.float32)).cuda(), torch.from_numpy(b).cuda(), sweeps,
-               alt=True).cpu().numpy()
+               alt=True, dense_stream=dense).cpu().numpy()
+    assert ctx.stats()["gs_kernel"] == (3 if dense else 4)
     assert x.min() >= 0
     assert rel_l2(x, ref) < TOL_X
     assert abs(x.sum() - ref.sum()) < TOL_P * ref.sum()
 
 
-def test_e2e_cfg2_alternating_sweeps(ctx, torch_cuda, oracle_lib):
-    _e2e(ctx, torch_cuda, oracle_lib, synth.make_band("cfg2", bins=[0, 4, 7]), alt=True)
+@pytest.mark.parametrize("dense", [False, True], ids=["residual", "alt_kernel"])
+def test_e2e_cfg2_alternating_sweeps(ctx, torch_cuda, oracle_lib, dense):
+    _e2e(ctx, torch_cuda, oracle_lib, synth.make_band("cfg2", bins=[0, 4, 7]), alt=True, dense=dense)
+
+
+def test_e2e_cfg3_alternating_paper_mode(ctx, torch_cuda, oracle_lib):
+    """Alternating sweeps with the paper-literal PSF (both NEXT-4 variants at once) on cfg3 bins."""
+    torch = torch_cuda
+    band = synth.make_band("cfg3", bins=[40, 160, 250])
+    cfg = band.cfg
+    g = geom_of(band)
+    out = ctx.solve_band(g, band.freqs, torch.from_numpy(band.csm).cuda(), cfg.epsilon, 200, cfg.eps_mode,
+                         alt=True, paper=True)
+    assert ctx.stats()["gs_kernel"] == 4
+    rnk, rkeep, rx, _ = oracle_lib.solve_band_cfg(band, sweeps=200, alt=True, paper=True)
+    for k in range(3):
+        assert np.array_equal(out["keep_idx"][k].cpu().numpy(), rkeep[k])
+        x = out["x_map"][k].cpu().numpy()
+        assert rel_l2(x, rx[k]) < TOL_X, (k, rel_l2(x, rx[k]))
+        assert abs(x.sum() - rx[k].sum()) <= TOL_P * rx[k].sum()
 
 
 def test_errors_flags_and_new_entry_points(ctx, torch_cuda):
