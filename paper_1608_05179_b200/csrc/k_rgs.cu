@@ -18,15 +18,17 @@
 //    carried contributions of the changes of the last W = min(kRgsWin, T-1) steps, which the
 //    solver accumulates itself (fp32, for its own residuals only).  In row
 //    order, the next row whose x changes is found with one ballot over the block (the rows in
-//    between keep x exactly); its change is broadcast and applied to every row's fp32 residual
-//    and to the carries of blocks k+1..k+W.  Both use row t of A~ (= column t, symmetric) over
-//    the columns of blocks k..k+W: the "panel" of row t.  A block with q changing rows takes
-//    q + 1 ballot rounds instead of a 32-row chain.  The changes (row, dx in fp64) are published
-//    as the step's change list.
-//  * panel producer (warp 5): per step, cp.async copies of the panels of the rows PREDICTED to change:
-//    those that changed at the block's previous visit (before the first visit: the rows with
-//    b > 0, exactly the rows sweep 1 changes).  A change outside the prediction (rare: the
-//    active set of a DAMAS iteration is stable) makes the solver load that panel itself.
+//    between keep x exactly); its change is broadcast and applied to every row's fp32 update
+//    w = -r/A_ii (from the block's diagonal tile, the only load on the row-to-row chain) and to
+//    the carries of the blocks of the next W steps (from row t's "panel": row t of A~ = column t,
+//    symmetric, over the columns of those blocks; consumed one change later, off the chain).
+//    A block with q changing rows takes q + 1 ballot rounds instead of a 32-row chain.  The
+//    changes (row, x before / after) are published as the step's change list.
+//  * panel producer (warp 5): per step, cp.async copies of the block's 32x32 diagonal tile and of
+//    the panels of the rows PREDICTED to change: those that changed at the block's previous visit
+//    (before the first visit: the rows with b > 0, exactly the rows sweep 1 changes).  The carries
+//    of a change outside the prediction (rare: the active set of a DAMAS iteration is stable)
+//    are added after the block from global memory.
 //  * row producer (warp 6): bulk-copies the rows of A~ (dense row-major) of every listed change
 //    into a double-buffered shared-memory ring, whole rows or segments of them, as batches.
 //  * stream (warps 0..3, 7): apply dx_c * A[c, :] (fp64) to the stored r of every block, except that
@@ -35,9 +37,8 @@
 //    element of r has one writer and a fixed update order.  The solver of step s needs stream
 //    step s - W - 1 complete: W steps of slack for the row fetch.
 // One CTA per bin; bins are taken in descending S~ order from a global counter.
-// Numerics: the carries and the stream accumulate A~ (fp32) x dx (fp64) in fp64; A~ entries are
-// widened to fp64 exactly, except values below 2^-126 (never produced by the PSF: they would need
-// |e_i^H e_j|^2 / M^2 < 1.2e-38), which the solver's integer widening flushes to zero.
+// Numerics: the stream accumulates A~ (fp32, widened exactly) x dx (fp64) into r in fp64; the
+// solver's carries and its row recurrence are fp32.
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -51,8 +52,12 @@ namespace dwc {
 
 namespace {
 
-constexpr int kRThreads = 256;
-constexpr int kNStream = 5;          // stream warps 0..3 and 7
+#ifndef RGS_NSTREAM
+#define RGS_NSTREAM 5
+#endif
+constexpr int kNStream = RGS_NSTREAM;          // stream warps 0..3 and 7..
+constexpr int kRThreads = 32 * (kNStream + 3);
+constexpr int kRMinBlocks = kNStream > 5 ? 1 : 2;
 // warp roles: the latency-critical warps take the higher warp of each SMSP pair (w, w+4): the
 // issue arbiter prefers the higher warp id
 constexpr int kWSolver = 4, kWPanel = 5, kWRows = 6;
@@ -70,7 +75,7 @@ constexpr int kWSolver = 4, kWPanel = 5, kWRows = 6;
 #endif
 constexpr int kRStg = RGS_STG;       // panel staging depth (steps)
 constexpr int kNP = RGS_NP;          // panels staged per step (predicted rows beyond: loaded on demand)
-constexpr int kPW = (kRgsWin + 1) * 32;   // panel floats: blocks k..k+W of one row
+constexpr int kPW = kRgsWin * 32;   // panel floats: blocks of steps s+1..s+W of one row
 // pending-buffer slots: the contributions to a block wait in the slot of the step that will read
 // it, (step mod 16).  At stream step s the pending visits are those of steps s .. s + nsub; a slot is
 // written for the visit at step S + 16 from stream step S + 16 - nsub >= S + 9 on, and the stream
@@ -83,6 +88,8 @@ static_assert(kRgsWin == 7, "pending-slot reuse distance assumes a 7-block carry
 constexpr int kNList = RGS_NLIST;    // change-list ring (steps; > kRgsWin + 2)
 constexpr int kCP = 2;               // stream: chunks held in registers per pass
 constexpr int kNSlot = RGS_NSLOT;    // row ring: batches in flight
+constexpr int kRegCh = 4;            // register-resident r: 128-column chunks per stream warp
+constexpr int kRegMaxSp = 128 * kRegCh * 5;   // (5 stream warps) the largest system it holds
 
 struct __align__(16) RgsEntry {
     float xn, xo;   // x of the row after / before the change (dx = xn - xo, exact in fp64)
@@ -92,7 +99,8 @@ struct __align__(16) RgsEntry {
 __device__ __forceinline__ double entry_dx(const RgsEntry &e) { return (double)e.xn - (double)e.xo; }
 
 struct __align__(128) RgsSmem {
-    float panel[kRStg][kNP][kPW];     // staged panels (ascending row), element m = column 32k + m (mod sp)
+    float diag[kRStg][32 * 32];       // the block's diagonal tile, row t: A[32k+t][32k .. 32k+31]
+    float panel[kRStg][kNP][kPW];     // staged panels (ascending row), segment d-1: the block of step s+d
     unsigned smask[kRStg];            // rows (bits) whose panels a stage holds
     float sinv[kRStg][32];            // 1/A_ii of the stage's block (0 for padding rows)
     RgsEntry list[kNList][32];
@@ -153,14 +161,13 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
-// fp32 -> fp64 on the integer pipes (the F2F conversion unit runs ~15 lanes/clk/SM and is busy
-// with the stream's conversions): exponent rebias and mantissa shift of a normal float; zero and
-// values below 2^-126 give 0.
-__device__ __forceinline__ double widen(float f) {
-    const unsigned b = __float_as_uint(f), a = b & 0x7fffffffu;
-    const unsigned hi = (a >= 0x00800000u) ? ((a >> 3) + 0x38000000u) | (b & 0x80000000u) : 0u;
-    const unsigned lo = (a >= 0x00800000u) ? (a << 29) : 0u;
-    return __hiloint2double((int)hi, (int)lo);
+#ifndef RGS_CVT
+#define RGS_CVT 0
+#endif
+// experiment: a non-negative float's bits as a double with the exponent at its fp32 bias = f * 2^-896
+__device__ __forceinline__ double nn_scaled(float f) {
+    const unsigned u = __float_as_uint(f);
+    return __hiloint2double((int)(u >> 3), (int)(u << 29));
 }
 __device__ __forceinline__ unsigned long long clk() {
     unsigned long long t;
@@ -206,8 +213,30 @@ constexpr int kProfItems = 1024;   // then per item: start, end (globaltimer ns)
 
 // r (fp64, sp), the pending carried contributions (fp64, 16 blocks), x (fp32, sp), the prediction
 // masks (T words) and the row ring (kNSlot slots of slot_floats) follow RgsSmem.
-template <bool ALT>
-__global__ void __launch_bounds__(kRThreads, 2)
+// Register-resident stream: the rows of one ring batch applied to the NC chunks a warp owns (all
+// loads of a row issued together, independent fp64 chains per chunk element).
+template <int NC>
+__device__ __forceinline__ void apply_rows(double (&r)[kRegCh][4], const float *src, int sp, int nb, const double *dxs,
+                                           int w) {
+#pragma unroll 4
+    for (int j = 0; j < nb; j++) {
+        const double dx = dxs[j];
+        const float *rowp = src + (size_t)j * sp;
+        float4 v[NC];
+#pragma unroll
+        for (int c = 0; c < NC; c++) v[c] = *reinterpret_cast<const float4 *>(rowp + 128 * (w + kNStream * c));
+#pragma unroll
+        for (int c = 0; c < NC; c++) {
+            r[c][0] = fma((double)v[c].x, dx, r[c][0]);
+            r[c][1] = fma((double)v[c].y, dx, r[c][1]);
+            r[c][2] = fma((double)v[c].z, dx, r[c][2]);
+            r[c][3] = fma((double)v[c].w, dx, r[c][3]);
+        }
+    }
+}
+
+template <bool ALT, bool REGR>
+__global__ void __launch_bounds__(kRThreads, REGR ? 1 : kRMinBlocks)
 rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restrict__ lay, int *__restrict__ counter,
            const float *__restrict__ Adense, const double *__restrict__ bt, int sweeps, float *__restrict__ x_out,
            float *__restrict__ x_map, const int32_t *__restrict__ keep_idx, int S, int max_sp, int slot_floats,
@@ -236,7 +265,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
         const BinLayout L = lay[bin];
         const int sp = L.sp, nk = L.nk, T = sp >> 5;
         const int nsub = min(kRgsWin, T - 1);      // blocks the solver carries
-        const int pw = (nsub + 1) * 32;            // panel floats
+        const int pw = nsub * 32;                  // panel floats
         const int total = sweeps * T;
         const bool pf = prof != nullptr && item == 0;
         const unsigned long long t_item = pf ? clk() : 0ull;
@@ -256,6 +285,10 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
             if ((i & 31) == 0) pmask[i >> 5] = m;
         }
         for (int i = tid; i < kPendF; i += kRThreads) pend[i] = 0.0;
+        if (nsub < kRgsWin) {   // the panel columns beyond the window stay 0 (the solver reads all segments)
+            float *pz = &sh.panel[0][0][0];
+            for (int i = tid; i < kRStg * kNP * kPW; i += kRThreads) pz[i] = 0.f;
+        }
         if (tid == 0) {
             for (int i = 0; i < kRStg; i++) {
                 mbar_init(&sh.stg_full[i], 33);   // 32 cp.async arrivals + the mask publisher
@@ -296,10 +329,21 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                     st |= m & (0u - m);   // lowest set bit
                     m &= m - 1;
                 }
-                // panel segment d (pieces 8d .. 8d+7) holds the columns of the block of step s+d
+                // the diagonal tile: 32 rows x 128 B, 8 pieces of 16 B per lane
+                {
+                    const float *dg = Ad + (size_t)(32 * k) * sp + 32 * k + 4 * (lane & 7);
+#pragma unroll
+                    for (int i = 0; i < 8; i++) {
+                        const int r = 4 * i + (lane >> 3);
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&sh.diag[sl][32 * r + 4 * (lane & 7)])),
+                                     "l"(dg + (size_t)r * sp)
+                                     : "memory");
+                    }
+                }
+                // panel segment d-1 (pieces 8(d-1) .. 8(d-1)+7) holds the columns of the block of step s+d
                 const int q4 = pw >> 2;   // 16-byte pieces per panel
-                const int d0 = lane >> 3, d1 = d0 + 4;
-                const int cb0 = 32 * win_blk(p, pos, d0, T, alt) + 4 * (lane & 7);
+                const int d0 = 1 + (lane >> 3), d1 = d0 + 4;
+                const int cb0 = 32 * win_blk(p, pos, d0 < T ? d0 : 0, T, alt) + 4 * (lane & 7);
                 const int cb1 = 32 * win_blk(p, pos, d1 < T ? d1 : 0, T, alt) + 4 * (lane & 7);
                 unsigned mm = st;
                 for (int j = 0; mm; j++) {
@@ -343,7 +387,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 const int li = s % kNList;
                 mbar_wait(&sh.dready[li], (s / kNList) & 1);
                 const int n = sh.cnt[li];
-                if (lane < n) sh.dxs[li][lane] = entry_dx(sh.list[li][lane]);
+                if (lane < n) sh.dxs[li][lane] = entry_dx(sh.list[li][lane]) * (RGS_CVT ? 0x1p896 : 1.0);
                 __syncwarp();
                 if (lane == 0) {
                     mbar_arrive(&sh.dxready[li]);
@@ -394,14 +438,12 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 const int k = fwd ? pos : T - 1 - pos;
                 const int sl = s % kRStg, li = s % kNList;
                 const int row = 32 * k + lane;
-                float xo = xs[row];
-                // the blocks of the next nsub steps: the carry of step s + d goes to wb[d] only at its
-                // first occurrence in the window (a block visited twice in the window -- the turn of
-                // alternating sweeps -- gets the contribution committed at its first visit)
-                int wb[kRgsWin + 1];
+                const float x0 = xs[row];   // this row's x before the step (its list entry's xo)
+                float xo = x0;
+                // the carry of step s + d goes to the block of step s + d only at its first occurrence
+                // in the window (a block visited twice in the window -- the turn of alternating
+                // sweeps -- gets the contribution committed at its first visit)
                 unsigned vmask = (1u << nsub) - 1u;   // bit d-1: step s+d is the first visit of its block in the window
-#pragma unroll
-                for (int d = 0; d <= kRgsWin; d++) wb[d] = (d <= nsub) ? win_blk(p, pos, d, T, alt) : -1;
                 // alternating sweeps (the window holds at most one turn, nsub < T): step s+dt is the
                 // first of the next sweep, which walks the blocks back, so step s+d (d >= dt) revisits
                 // the block of step s+2dt-1-d: not a first occurrence for dt <= d <= 2dt-2.  Block k
@@ -415,58 +457,74 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 mbar_wait(&sh.stg_full[sl], (s / kRStg) & 1);
                 const unsigned smk = sh.smask[sl];
                 const float invd = use_ivs ? ivs[row] : sh.sinv[sl][lane];
-                // this lane's panel slot (its rank among the staged rows), -1 if not staged
-                const int myp = ((smk >> lane) & 1u) ? __popc(smk & ((1u << lane) - 1u)) : -1;
                 const unsigned long long t1 = pf ? clk() : 0ull;
                 const int sw = max(s - nsub - 1, vprev);   // the stream step the stored r of this block needs
                 if (sw >= 0) mbar_wait(&sh.sdone[sw % kNList], (sw / kNList) & 1);
                 const unsigned long long t2 = pf ? clk() : 0ull;
-                float ac = (float)rs[row] + carry[0];
+                // r of the block as of stream step sw (before any stream step: r = -b~)
+                const float ac = (float)(REGR ? (sw >= 0 ? pend[32 * (s & (kPendBlk - 1)) + lane] : -bt[L.v_off + row])
+                                              : rs[row]) + carry[0];
                 float acc[kRgsWin];
 #pragma unroll
                 for (int d = 0; d < kRgsWin; d++) acc[d] = 0.f;
                 RgsEntry *lst = sh.list[li];
                 int pos_r = fwd ? 0 : 31, q = 0;   // next row of the block in sweep order
                 unsigned chg = 0;
+                // the projected update is carried as w = -ac/A_ii: a change dv of row t moves it by
+                // -(dv/A_ii) A[row][32k+t], read from the staged diagonal tile (row t, by symmetry /
+                // the transposed store) -- the only shared-memory load on the row-to-row chain
+                float w = -ac * invd;
+                const float *dgt = sh.diag[sl] + lane;
+                // the previous change's panel values and dv: consumed one iteration later, after the
+                // next ballot, so that the chain never waits for the panel loads
+                float pvp[kRgsWin], dvp = 0.f;
+#pragma unroll
+                for (int d = 0; d < kRgsWin; d++) pvp[d] = 0.f;
                 for (;;) {
-                    const float w = -ac * invd;
                     const float xn = xo + fmaxf(w, -xo);   // = max(xo - ac/A_ii, 0)
+                    const float dl = xn - xo;              // this row's change if it is the next one
                     const unsigned m = __ballot_sync(0xffffffffu, (fwd ? lane >= pos_r : lane <= pos_r) && xn != xo);
-                    if (m == 0u) break;
-                    const int t = fwd ? __ffs(m) - 1 : 31 - __clz(m);
-                    const float xn_t = __shfl_sync(0xffffffffu, xn, t);
-                    const float xo_t = __shfl_sync(0xffffffffu, xo, t);
-                    const int pt = __shfl_sync(0xffffffffu, myp, t);
-                    const float dv = xn_t - xo_t;
-                    if (lane == t) {
-                        lst[q].xn = xn;
-                        lst[q].xo = xo;
-                        lst[q].c = row;
-                        xo = xn;
-                    }
-                    // panel of row t: element 32d + lane = A[32k+t][32 wb[d] + lane] = A[32 wb[d] + lane][32k+t]
-                    float pv[kRgsWin + 1];
-                    if (pt >= 0) {
-                        const float *pr = sh.panel[sl][pt];
-#pragma unroll
-                        for (int d = 0; d <= kRgsWin; d++) pv[d] = (d <= nsub) ? pr[32 * d + lane] : 0.f;
-                    } else {
-                        // not predicted: the panel from global memory (L2/HBM latency, rare)
-                        const float *rw = Ad + (size_t)(32 * k + t) * sp;
-#pragma unroll
-                        for (int d = 0; d <= kRgsWin; d++) pv[d] = (d <= nsub) ? __ldg(rw + 32 * wb[d] + lane) : 0.f;
-                        nmiss++;
-                    }
-                    ac = fmaf(pv[0], dv, ac);
 #pragma unroll
                     for (int d = 0; d < kRgsWin; d++)   // (forward: pv = 0 beyond nsub)
-                        if (!ALT || ((vmask >> d) & 1u)) acc[d] = fmaf(pv[d + 1], dv, acc[d]);
+                        if (!ALT || ((vmask >> d) & 1u)) acc[d] = fmaf(pvp[d], dvp, acc[d]);
+                    if (m == 0u) break;
+                    const int t = fwd ? __ffs(m) - 1 : 31 - __clz(m);
+                    const float dv = __shfl_sync(0xffffffffu, dl, t);
+                    const float a0 = dgt[32 * t];
+                    if (lane == t) xo = xn;   // (the list entry is written after the block, below)
+                    w = fmaf(-invd * dv, a0, w);
+                    // off the chain: the carries, from row t's staged panel (element 32(d-1) + lane =
+                    // A[32k+t][32 blk(s+d) + lane] = A[32 blk(s+d) + lane][32k+t]; segments beyond nsub
+                    // are zero); a row not staged is added after the block from global memory
+                    const bool stg = (smk >> t) & 1u;
+                    const float *pr = sh.panel[sl][stg ? __popc(smk & ((1u << t) - 1u)) : 0] + lane;
+                    dvp = stg ? dv : 0.f;
+#pragma unroll
+                    for (int d = 0; d < kRgsWin; d++) pvp[d] = pr[32 * d];
                     chg |= 1u << t;
                     pos_r = fwd ? t + 1 : t - 1;
                     q++;
                 }
+                // the carries of the changed rows that were not staged (rare: the prediction missed)
+                for (unsigned mm = chg & ~smk; mm; mm &= mm - 1) {
+                    const int t = __ffs(mm) - 1;
+                    const float dv = __shfl_sync(0xffffffffu, xo - x0, t);
+                    const float *rw = Ad + (size_t)(32 * k + t) * sp + lane;
+#pragma unroll
+                    for (int d = 0; d < kRgsWin; d++)
+                        if (d < nsub && (!ALT || ((vmask >> d) & 1u)))
+                            acc[d] = fmaf(__ldg(rw + 32 * win_blk(p, pos, d + 1, T, alt)), dv, acc[d]);
+                    nmiss++;
+                }
                 const unsigned long long t3 = pf ? clk() : 0ull;
                 xs[row] = xo;
+                // the block's changes in sweep order (each row changes at most once per visit)
+                if ((chg >> lane) & 1u) {
+                    const int e = fwd ? __popc(chg & ((1u << lane) - 1u)) : __popc(chg >> lane) - 1;
+                    lst[e].xn = xo;
+                    lst[e].xo = x0;
+                    lst[e].c = row;
+                }
                 if (lane == 0) {
                     sh.cnt[li] = q;
                     pmask[k] = chg;   // the prediction for the next visit
@@ -486,10 +544,89 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
             }
             if (prof && lane == 0 && item < kProfItems) prof[kProfSlots + 4 * item + 3] = nch;
             if (pf && lane == 0) { prof[0] = tt; prof[1] = tsd; prof[2] = tl; prof[3] = tr; prof[4] = total; prof[5] = nch; prof[6] = nmiss; }
+        } else if (REGR) {
+            // ================= stream warps, r in registers (sp <= kRegMaxSp, whole rows in the
+            // ring): r += dx_c A[c, :] for every change of every step.  Warp w owns the 128-column
+            // chunks q = w, w + 5, ... (at most kRegCh); lane l columns 128q + 4l .. +3.  After its
+            // step j the owner of each block publishes that block's r (8 lanes x 4 fp64) for the
+            // solver step s' whose stored residual is "r after stream step j" (s' = j + nsub + 1,
+            // or for alternating sweeps the revisit s' whose last visit was step j), in the
+            // step-indexed slot s' mod 16 (the pend buffer)
+            const int w = (wid < 4) ? wid : wid - 3;
+            const int nq = (sp + 127) >> 7;
+            const int nch = (nq - w + kNStream - 1) / kNStream;   // chunks this warp owns (<= kRegCh)
+            unsigned long long tlw = 0, tbw = 0, tap = 0, nb_all = 0;
+            double r[kRegCh][4];
+#pragma unroll
+            for (int c = 0; c < kRegCh; c++) {
+                const int col = 128 * (w + kNStream * c) + 4 * lane;
+#pragma unroll
+                for (int e = 0; e < 4; e++) r[c][e] = (col + e < sp) ? -bt[L.v_off + col + e] : 0.0;
+            }
+            // the stored r of solver step s' = s + d: r after stream step s'-nsub-1, or for a revisit
+            // whose last visit v > s'-nsub-1 (alternating sweeps; the solver carries step v's
+            // changes) r before stream step v.  `before`: called before step s's changes (d <= nsub)
+            // for the revisits with v = s, else after them for s' = s + nsub + 1
+            auto publish = [&](int s0, int p0, int pos0, int d, bool before) {
+                int q2 = pos0 + d, p2 = p0;   // step s0 + d without a division (d <= T)
+                if (q2 >= T) { q2 -= T; p2++; }
+                const int vp = (ALT && p2 >= 1 && 2 * q2 + 1 <= nsub) ? s0 + d - 2 * q2 - 1 : -1;
+                const bool rev = vp > s0 + d - nsub - 1;
+                if (before ? !(rev && vp == s0) : rev) return;
+                const int bb = sweep_fwd(p2, alt) ? q2 : T - 1 - q2;   // its block
+                const int qb = bb >> 2;
+                if ((qb % kNStream) == w && (lane >> 3) == (bb & 3)) {
+                    const int cb = qb / kNStream;
+                    double *dst = pend + 32 * ((s0 + d) & (kPendBlk - 1)) + 4 * (lane & 7);
+#pragma unroll
+                    for (int c = 0; c < kRegCh; c++)
+                        if (c == cb) {
+                            reinterpret_cast<double2 *>(dst)[0] = make_double2(r[c][0], r[c][1]);
+                            reinterpret_cast<double2 *>(dst)[1] = make_double2(r[c][2], r[c][3]);
+                        }
+                }
+            };
+            int b = 0;
+            for (int s = 0, p = 0, pos = 0; s < total; s++, pos = (pos + 1 == T) ? 0 : pos + 1, p += (pos == 0)) {
+                const int li = s % kNList;
+                const unsigned long long t0 = pf ? clk() : 0ull;
+                mbar_wait(&sh.dxready[li], (s / kNList) & 1);
+                if (pf) tlw += clk() - t0;
+                const int n = sh.cnt[li];
+                // alternating sweeps: a revisit s' = s + d of block k whose last visit is this step
+                // carries this step's changes itself, so its stored r is the one before them
+                if (ALT)
+                    for (int d = 1; d <= nsub; d++) publish(s, p, pos, d, true);
+                for (int u0 = 0; u0 < n; u0 += rg.upb, b++) {
+                    const int h = b % kNSlot;
+                    const unsigned long long t1 = pf ? clk() : 0ull;
+                    mbar_wait(&sh.rfull[h], (b / kNSlot) & 1);
+                    const unsigned long long t2 = pf ? clk() : 0ull;
+                    const int nb = min(rg.upb, n - u0);
+                    const float *src = ring + (size_t)h * slot_floats + 4 * lane;
+                    const double *dxb = &sh.dxs[li][u0];
+                    switch (nch) {   // (0: a small system leaves this warp no chunk)
+                        case 1: apply_rows<1>(r, src, sp, nb, dxb, w); break;
+                        case 2: apply_rows<2>(r, src, sp, nb, dxb, w); break;
+                        case 3: apply_rows<3>(r, src, sp, nb, dxb, w); break;
+                        case 4: apply_rows<4>(r, src, sp, nb, dxb, w); break;
+                        default: break;
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&sh.rempty[h]);
+                    if (pf) { tbw += t2 - t1; tap += clk() - t2; nb_all++; }
+                }
+                // publish the r of block blk(s + nsub + 1) after this step -- unless that visit is an
+                // alternating-sweep revisit whose last visit is inside its window (published then)
+                publish(s, p, pos, nsub + 1, false);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sh.sdone[li]);
+            }
+            if (pf && w == 0 && lane == 0) { prof[8] = tlw; prof[9] = tbw; prof[10] = tap; prof[11] = nb_all; }
         } else {
             // ================= stream warps: r += dx_c A[c, :] for every change of every step;
             // warp w owns the 128-column chunks q = w, w + 5, ...; lane l columns 128q + 4l..+3
-            const int w = (wid < 4) ? wid : 4;
+            const int w = (wid < 4) ? wid : wid - 3;
             unsigned long long tlw = 0, tbw = 0, tap = 0, nb_all = 0;
             int b = 0;
             for (int s = 0, p = 0, pos = 0; s < total; s++, pos = (pos + 1 == T) ? 0 : pos + 1, p += (pos == 0)) {
@@ -580,10 +717,22 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                                 for (int i = 0; i < kCP; i++) v[i] = *reinterpret_cast<const float4 *>(rowp + cc[i]);
 #pragma unroll
                                 for (int i = 0; i < kCP; i++) {
+#if RGS_CVT == 0
                                     ra[i].x = fma((double)v[i].x, dx, ra[i].x);
                                     ra[i].y = fma((double)v[i].y, dx, ra[i].y);
                                     rb[i].x = fma((double)v[i].z, dx, rb[i].x);
                                     rb[i].y = fma((double)v[i].w, dx, rb[i].y);
+#elif RGS_CVT == 1
+                                    ra[i].x = fma(nn_scaled(v[i].x), dx, ra[i].x);
+                                    ra[i].y = fma(nn_scaled(v[i].y), dx, ra[i].y);
+                                    rb[i].x = fma(nn_scaled(v[i].z), dx, rb[i].x);
+                                    rb[i].y = fma(nn_scaled(v[i].w), dx, rb[i].y);
+#else
+                                    ra[i].x = fma(nn_scaled(v[i].x), dx, ra[i].x);
+                                    ra[i].y = fma((double)v[i].y * 0x1p-896, dx, ra[i].y);
+                                    rb[i].x = fma(nn_scaled(v[i].z), dx, rb[i].x);
+                                    rb[i].y = fma((double)v[i].w * 0x1p-896, dx, rb[i].y);
+#endif
                                 }
                             }
 #pragma unroll
@@ -657,7 +806,8 @@ int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int m
     const size_t per2 = 114 * 1024 - 1024;
     size_t ring;
     // two per SM when the band has more bins than SMs and every ring slot still holds 2 rows
-    const bool two = per_sm_env ? per_sm_env == 2 && per2 > base + 2048
+    const bool two = kRMinBlocks < 2 ? false
+                     : per_sm_env ? per_sm_env == 2 && per2 > base + 2048
                                 : n_bins > num_sms && per2 > base && (per2 - base) / (4 * kNSlot) >= 2 * (size_t)max_sp;
     if (two)
         ring = (per2 - base - 512) / 1024 * 1024;
@@ -667,7 +817,12 @@ int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int m
     const int slot_floats = (int)(ring / (4 * kNSlot)) / 128 * 128;   // floats per ring slot
     if (slot_floats < 128) return -1;
     const size_t smem = base + (size_t)slot_floats * 4 * kNSlot + 512;   // + slack: a row's last chunk reads past it
-    const auto kern = alt ? rgs_kernel<true> : rgs_kernel<false>;
+    // r in registers (one CTA per SM: up to 255 registers) when the system fits the stream warps'
+    // chunks and a ring slot holds a whole row
+    static const bool no_regr = getenv("DWC_RGS_NO_REGR") != nullptr;   // experiment
+    const bool regr = !two && max_sp <= kRegMaxSp && slot_floats >= max_sp && kNStream == 5 && !no_regr;
+    const auto kern = alt ? (regr ? rgs_kernel<true, true> : rgs_kernel<true, false>)
+                          : (regr ? rgs_kernel<false, true> : rgs_kernel<false, false>);
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return -1;
     int per_sm = 0;
