@@ -452,7 +452,8 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
         CU(cudaMemsetAsync(ctx->upd.p, 0, 64, st));
         LAUNCH(launch_rgs(n_bins, (int *)ctx->order.p, (BinLayout *)ctx->lay.p, max_sp, (int *)ctx->counter.p,
                           (float *)ctx->Ad.p, (double *)ctx->bt.p, p->sweeps, nullptr, x_map, keep_idx,
-                          S, ctx->num_sms, (unsigned long long *)ctx->upd.p, st, &gsi, alt));
+                          S, ctx->num_sms, (unsigned long long *)ctx->upd.p, st, &gsi, alt,
+                          /*nonneg: every PSF is |.|^2 times positive scales*/ 1));
     } else if (p->flags & DWC_ALT_SWEEPS) {
         gsi.kernel = DWC_GS_KERNEL_ALT;
         gsi.ctas = n_bins;
@@ -813,6 +814,7 @@ dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int3
     CU(cudaMemcpyAsync(ctx->readback.p, ctx->flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     if (*(int *)ctx->readback.p & 2) return fail(DWC_ENUMERIC, "A has a diagonal entry <= 0 or non-finite");
+    const int nonneg = (*(int *)ctx->readback.p & 4) ? 0 : 1;   // no entry with its sign bit set, all finite
     BinLayout lay{n, sp, 0, 0, 0, gs_group_size(n), 0, 0};
     std::vector<int32_t> order{0};
     int32_t nk0 = n;
@@ -860,7 +862,7 @@ dwc_status dwc_gs(dwc_ctx *ctx, int32_t n, const float *A, const double *b, int3
         CU(cudaMemsetAsync(ctx->upd.p, 0, 64, st));
         LAUNCH(launch_rgs(1, (int *)ctx->order.p, (BinLayout *)ctx->lay.p, sp, (int *)ctx->counter.p,
                           (float *)ctx->Ad.p, (double *)ctx->gs_b.p, sweeps, x, nullptr, nullptr, 0, ctx->num_sms,
-                          (unsigned long long *)ctx->upd.p, st, &gsi, (flags & DWC_ALT_SWEEPS) ? 1 : 0));
+                          (unsigned long long *)ctx->upd.p, st, &gsi, (flags & DWC_ALT_SWEEPS) ? 1 : 0, nonneg));
         ctx->stats_upd_valid = true;
     } else {
         LAUNCH(launch_gs_prep(1, sp, (BinLayout *)ctx->lay.p, Ap, (double *)ctx->gs_b.p, ctx->packets.p, st));

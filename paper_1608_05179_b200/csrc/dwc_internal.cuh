@@ -268,7 +268,7 @@ int rgs_auto_max_sp();
 int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int max_sp, int *counter,
                const float *Adense, const double *bt, int sweeps, float *x_out, float *x_map,
                const int32_t *keep_idx, int S, int num_sms, unsigned long long *n_updates, cudaStream_t st,
-               GsLaunchInfo *info, int alt = 0);
+               GsLaunchInfo *info, int alt = 0, int nonneg = 0);
 // dwc_gs: dense row-major n x n -> padded dense sp x sp (symmetric: from the upper triangle;
 // general: transposed).
 int launch_rgs_convert(int n, int sp, const float *src, float *dense, cudaStream_t st, int general = 0);

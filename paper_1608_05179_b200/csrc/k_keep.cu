@@ -78,15 +78,24 @@ int launch_keep_unmask(int n_bins, int S, const uint32_t *mask, int32_t *n_keep,
 }
 
 // dwc_gs precondition: every A_ii > 0 and finite; sets bit 2 of *flag otherwise.
+// Bit 4: some entry has its sign bit set or is not finite (the residual kernel then widens A~
+// with F2F instead of its non-negative bit placement).
 __global__ void diag_check_kernel(int n, const float *__restrict__ A, int *__restrict__ flag) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const float v = A[(size_t)i * n + i];
         if (!(v > 0.f) || !isfinite(v)) atomicOr(flag, 2);
     }
+    bool neg = false;
+    const size_t nn = (size_t)n * n;
+    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < nn; e += (size_t)gridDim.x * blockDim.x) {
+        const float v = A[e];
+        neg |= (__float_as_uint(v) >> 31) != 0u || !isfinite(v);
+    }
+    if (__any_sync(0xffffffffu, neg) && (threadIdx.x & 31) == 0) atomicOr(flag, 4);
 }
 
 int launch_diag_check(int n, const float *A, int *flag, cudaStream_t st) {
-    diag_check_kernel<<<(n + 255) / 256 < 148 ? (n + 255) / 256 : 148, 256, 0, st>>>(n, A, flag);
+    diag_check_kernel<<<148, 256, 0, st>>>(n, A, flag);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

@@ -71,7 +71,7 @@ constexpr int kWSolver = 4, kWPanel = 5, kWRows = 6;
 #define RGS_NLIST 16
 #endif
 #ifndef RGS_NSLOT
-#define RGS_NSLOT 6
+#define RGS_NSLOT 4
 #endif
 constexpr int kRStg = RGS_STG;       // panel staging depth (steps)
 constexpr int kNP = RGS_NP;          // panels staged per step (predicted rows beyond: loaded on demand)
@@ -161,10 +161,12 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
-#ifndef RGS_CVT
-#define RGS_CVT 0
-#endif
-// experiment: a non-negative float's bits as a double with the exponent at its fp32 bias = f * 2^-896
+// fp32 -> fp64 for a non-negative float (every PSF: |.|^2 times positive scales) without the F2F
+// unit (~15 lanes/clk/SM, the stream's bottleneck): the float's bits placed in a double with the
+// exponent left at its fp32 bias, i.e. the value f * 2^-896 exactly -- zero and fp32 subnormals
+// (as fp64 subnormals) included.  One ALU shift and one FMA-pipe shift.  The stream's dx carries
+// the 2^896 (kDxScale): the DFMA forms the product D * dx * 2^896 = f * dx exactly, as before.
+constexpr double kDxScale = 0x1p896;
 __device__ __forceinline__ double nn_scaled(float f) {
     const unsigned u = __float_as_uint(f);
     return __hiloint2double((int)(u >> 3), (int)(u << 29));
@@ -215,7 +217,7 @@ constexpr int kProfItems = 1024;   // then per item: start, end (globaltimer ns)
 // masks (T words) and the row ring (kNSlot slots of slot_floats) follow RgsSmem.
 // Register-resident stream: the rows of one ring batch applied to the NC chunks a warp owns (all
 // loads of a row issued together, independent fp64 chains per chunk element).
-template <int NC>
+template <int NC, bool NN>
 __device__ __forceinline__ void apply_rows(double (&r)[kRegCh][4], const float *src, int sp, int nb, const double *dxs,
                                            int w) {
 #pragma unroll 4
@@ -227,10 +229,10 @@ __device__ __forceinline__ void apply_rows(double (&r)[kRegCh][4], const float *
         for (int c = 0; c < NC; c++) v[c] = *reinterpret_cast<const float4 *>(rowp + 128 * (w + kNStream * c));
 #pragma unroll
         for (int c = 0; c < NC; c++) {
-            r[c][0] = fma((double)v[c].x, dx, r[c][0]);
-            r[c][1] = fma((double)v[c].y, dx, r[c][1]);
-            r[c][2] = fma((double)v[c].z, dx, r[c][2]);
-            r[c][3] = fma((double)v[c].w, dx, r[c][3]);
+            r[c][0] = fma(NN ? nn_scaled(v[c].x) : (double)v[c].x, dx, r[c][0]);
+            r[c][1] = fma(NN ? nn_scaled(v[c].y) : (double)v[c].y, dx, r[c][1]);
+            r[c][2] = fma(NN ? nn_scaled(v[c].z) : (double)v[c].z, dx, r[c][2]);
+            r[c][3] = fma(NN ? nn_scaled(v[c].w) : (double)v[c].w, dx, r[c][3]);
         }
     }
 }
@@ -240,7 +242,7 @@ __global__ void __launch_bounds__(kRThreads, REGR ? 1 : kRMinBlocks)
 rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restrict__ lay, int *__restrict__ counter,
            const float *__restrict__ Adense, const double *__restrict__ bt, int sweeps, float *__restrict__ x_out,
            float *__restrict__ x_map, const int32_t *__restrict__ keep_idx, int S, int max_sp, int slot_floats,
-           int use_ivs,
+           int use_ivs, int nonneg,
            unsigned long long *__restrict__ n_updates, unsigned long long *__restrict__ prof) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     RgsSmem &sh = *reinterpret_cast<RgsSmem *>(smem_raw);
@@ -387,7 +389,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 const int li = s % kNList;
                 mbar_wait(&sh.dready[li], (s / kNList) & 1);
                 const int n = sh.cnt[li];
-                if (lane < n) sh.dxs[li][lane] = entry_dx(sh.list[li][lane]) * (RGS_CVT ? 0x1p896 : 1.0);
+                if (lane < n) sh.dxs[li][lane] = entry_dx(sh.list[li][lane]) * ((REGR && nonneg) ? kDxScale : 1.0);   // exact
                 __syncwarp();
                 if (lane == 0) {
                     mbar_arrive(&sh.dxready[li]);
@@ -605,11 +607,15 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                     const int nb = min(rg.upb, n - u0);
                     const float *src = ring + (size_t)h * slot_floats + 4 * lane;
                     const double *dxb = &sh.dxs[li][u0];
-                    switch (nch) {   // (0: a small system leaves this warp no chunk)
-                        case 1: apply_rows<1>(r, src, sp, nb, dxb, w); break;
-                        case 2: apply_rows<2>(r, src, sp, nb, dxb, w); break;
-                        case 3: apply_rows<3>(r, src, sp, nb, dxb, w); break;
-                        case 4: apply_rows<4>(r, src, sp, nb, dxb, w); break;
+                    switch (nonneg ? nch : nch + 8) {   // (0: a small system leaves this warp no chunk)
+                        case 1: apply_rows<1, true>(r, src, sp, nb, dxb, w); break;
+                        case 2: apply_rows<2, true>(r, src, sp, nb, dxb, w); break;
+                        case 3: apply_rows<3, true>(r, src, sp, nb, dxb, w); break;
+                        case 4: apply_rows<4, true>(r, src, sp, nb, dxb, w); break;
+                        case 9: apply_rows<1, false>(r, src, sp, nb, dxb, w); break;
+                        case 10: apply_rows<2, false>(r, src, sp, nb, dxb, w); break;
+                        case 11: apply_rows<3, false>(r, src, sp, nb, dxb, w); break;
+                        case 12: apply_rows<4, false>(r, src, sp, nb, dxb, w); break;
                         default: break;
                     }
                     __syncwarp();
@@ -717,22 +723,10 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                                 for (int i = 0; i < kCP; i++) v[i] = *reinterpret_cast<const float4 *>(rowp + cc[i]);
 #pragma unroll
                                 for (int i = 0; i < kCP; i++) {
-#if RGS_CVT == 0
                                     ra[i].x = fma((double)v[i].x, dx, ra[i].x);
                                     ra[i].y = fma((double)v[i].y, dx, ra[i].y);
                                     rb[i].x = fma((double)v[i].z, dx, rb[i].x);
                                     rb[i].y = fma((double)v[i].w, dx, rb[i].y);
-#elif RGS_CVT == 1
-                                    ra[i].x = fma(nn_scaled(v[i].x), dx, ra[i].x);
-                                    ra[i].y = fma(nn_scaled(v[i].y), dx, ra[i].y);
-                                    rb[i].x = fma(nn_scaled(v[i].z), dx, rb[i].x);
-                                    rb[i].y = fma(nn_scaled(v[i].w), dx, rb[i].y);
-#else
-                                    ra[i].x = fma(nn_scaled(v[i].x), dx, ra[i].x);
-                                    ra[i].y = fma((double)v[i].y * 0x1p-896, dx, ra[i].y);
-                                    rb[i].x = fma(nn_scaled(v[i].z), dx, rb[i].x);
-                                    rb[i].y = fma((double)v[i].w * 0x1p-896, dx, rb[i].y);
-#endif
                                 }
                             }
 #pragma unroll
@@ -794,7 +788,7 @@ size_t rgs_smem_bytes(int max_sp) { return rgs_base_bytes(max_sp) + kNSlot * 128
 int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int max_sp, int *counter,
                const float *Adense, const double *bt, int sweeps, float *x_out, float *x_map,
                const int32_t *keep_idx, int S, int num_sms, unsigned long long *n_updates, cudaStream_t st,
-               GsLaunchInfo *info, int alt) {
+               GsLaunchInfo *info, int alt, int nonneg) {
     // 1/A_ii in shared memory for the whole system when a ring of >= 24 KB still fits beside it
     const int use_ivs = (rgs_base_bytes(max_sp) + (size_t)max_sp * 4 + 24 * 1024 + 1536 <= 227 * 1024) ? 1 : 0;
     const size_t base = (rgs_base_bytes(max_sp) + (use_ivs ? (size_t)max_sp * 4 : 0) + 127) / 128 * 128;
@@ -850,7 +844,7 @@ int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int m
         cudaMemsetAsync(prof, 0, pb, st);
     }
     kern<<<grid, kRThreads, smem, st>>>(n_bins, order_dev, lay_dev, counter, Adense, bt, sweeps, x_out, x_map,
-                                        keep_idx, S, max_sp, slot_floats, use_ivs, n_updates, prof);
+                                        keep_idx, S, max_sp, slot_floats, use_ivs, nonneg, n_updates, prof);
     const cudaError_t e = cudaPeekAtLastError();
     if (profile) {
         static unsigned long long h[kProfSlots + 4 * kProfItems + 2];
@@ -872,10 +866,10 @@ int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int m
         }
         const double n = h[4] ? (double)h[4] : 1.0;
         fprintf(stderr,
-                "[rgs-prof] grid %d x %zu B smem (ring 6 x %d floats), steps %llu, changes %llu (%.2f/step), item %.0f cyc"
+                "[rgs-prof] grid %d x %zu B smem (ring %d x %d floats), steps %llu, changes %llu (%.2f/step), item %.0f cyc"
                 " | solver cyc/step: tiles %.0f stream %.0f loop %.0f rest %.0f | stream0: list %.0f batch %.0f apply %.0f"
                 " (%llu batches) | rowprod: ring wait %.0f issue %.0f | panel misses %llu | panelprod wait %.0f issue %.0f\n",
-                grid, smem, slot_floats, h[4], h[5], h[5] / n, (double)h[14], h[0] / n, h[1] / n, h[2] / n, h[3] / n,
+                grid, smem, kNSlot, slot_floats, h[4], h[5], h[5] / n, (double)h[14], h[0] / n, h[1] / n, h[2] / n, h[3] / n,
                 h[8] / n, h[9] / n, h[10] / n, h[11], h[12] / n, h[13] / n, h[6], h[7] / n, h[15] / n);
         cudaFree(prof);
     }

@@ -224,6 +224,47 @@ def test_gs_parity_on_oracle_system(ctx, torch_cuda, oracle_lib, nk, sweeps, den
     assert abs(x.sum() - ref.sum()) < TOL_P * ref.sum()
 
 
+@pytest.mark.parametrize("nk", [2, 300, 1086])
+def test_gs_nonneg_widening_is_bitwise_exact(ctx, torch_cuda, oracle_lib, nk):
+    """The residual kernel widens a non-negative A~ by bit placement (f * 2^-896, the 2^896 in
+    dx) instead of F2F; a -0.0 in the lower triangle (never read by the symmetric solve, but seen
+    by dwc_gs's sign scan) forces the F2F path on the same system: the iterates must be
+    bitwise identical."""
+    torch = torch_cuda
+    band = synth.make_band("cfg3", bins=[249])
+    g = geom_of(band)
+    f = band.freqs[0]
+    b = oracle_lib.das(*oracle_args(g), f, band.csm[0])
+    keep = np.sort(np.argsort(-b)[:nk]).astype(np.int32)
+    A = oracle_lib.psf(*oracle_args(g), f, keep).astype(np.float32)
+    bt = torch.from_numpy(b[keep]).cuda()
+    x_nn = ctx.gs(torch.from_numpy(A).cuda(), bt, 200, dense_stream=False).cpu().numpy()
+    A2 = A.copy()
+    A2[nk - 1, 0] = -0.0
+    x_f2f = ctx.gs(torch.from_numpy(A2).cuda(), bt, 200, dense_stream=False).cpu().numpy()
+    assert np.array_equal(x_nn, x_f2f)
+
+
+@pytest.mark.parametrize("dense", [False, True], ids=["residual", "dense_stream"])
+@pytest.mark.parametrize("n", [40, 333])
+def test_gs_signed_matrix_parity(ctx, torch_cuda, oracle_lib, n, dense):
+    """A symmetric positive-definite matrix with negative off-diagonal entries (dwc_gs accepts
+    any A with A_ii > 0): the residual kernel's F2F widening path, against the oracle."""
+    torch = torch_cuda
+    rng = np.random.default_rng(n)
+    B = rng.standard_normal((n, n // 2))
+    A = B @ B.T / n + np.diag(1.0 + rng.random(n))
+    A /= np.sqrt(np.outer(np.diag(A), np.diag(A)))   # unit diagonal, like the PSF
+    A = A.astype(np.float32).astype(np.float64)
+    assert A.min() < 0
+    bt = A @ np.abs(rng.standard_normal(n)) - 0.05
+    ref = oracle_lib.gs(A, bt, 150)
+    x = ctx.gs(torch.from_numpy(A.astype(np.float32)).cuda(), torch.from_numpy(bt).cuda(), 150,
+               dense_stream=dense).cpu().numpy()
+    assert x.min() >= 0
+    assert rel_l2(x, ref) < TOL_X, rel_l2(x, ref)
+
+
 # ---------------------------------------------------------------------------- end to end
 def _e2e(ctx, torch, oracle_lib, band, sweeps=None, full=False, check_b=True, order=1, dr=False, alt=False,
          dense=False):
