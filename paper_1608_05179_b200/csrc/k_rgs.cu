@@ -61,6 +61,9 @@ constexpr int kRMinBlocks = kNStream > 5 ? 1 : 2;
 // warp roles: the latency-critical warps take the higher warp of each SMSP pair (w, w+4): the
 // issue arbiter prefers the higher warp id
 constexpr int kWSolver = 4, kWPanel = 5, kWRows = 6;
+#ifndef RGS_REDUX
+#define RGS_REDUX 0
+#endif
 #ifndef RGS_STG
 #define RGS_STG 5
 #endif
@@ -331,34 +334,36 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                     st |= m & (0u - m);   // lowest set bit
                     m &= m - 1;
                 }
-                // the diagonal tile: 32 rows x 128 B, 8 pieces of 16 B per lane
+                // the diagonal tile: 32 rows x 128 B, 8 pieces of 16 B per lane (row offsets in 32
+                // bits from the block's row base: t * sp < 2^31)
+                const float *blk = Ad + (size_t)(32 * k) * sp;
                 {
-                    const float *dg = Ad + (size_t)(32 * k) * sp + 32 * k + 4 * (lane & 7);
+                    const float *dg = blk + 32 * k + 4 * (lane & 7);
+                    const uint32_t sd = smem_u32(&sh.diag[sl][32 * (lane >> 3) + 4 * (lane & 7)]);
 #pragma unroll
                     for (int i = 0; i < 8; i++) {
                         const int r = 4 * i + (lane >> 3);
-                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&sh.diag[sl][32 * r + 4 * (lane & 7)])),
-                                     "l"(dg + (size_t)r * sp)
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sd + 4 * 128 * i), "l"(dg + r * sp)
                                      : "memory");
                     }
                 }
                 // panel segment d-1 (pieces 8(d-1) .. 8(d-1)+7) holds the columns of the block of step s+d
                 const int q4 = pw >> 2;   // 16-byte pieces per panel
                 const int d0 = 1 + (lane >> 3), d1 = d0 + 4;
-                const int cb0 = 32 * win_blk(p, pos, d0 < T ? d0 : 0, T, alt) + 4 * (lane & 7);
-                const int cb1 = 32 * win_blk(p, pos, d1 < T ? d1 : 0, T, alt) + 4 * (lane & 7);
+                const float *pc0 = blk + 32 * win_blk(p, pos, d0 < T ? d0 : 0, T, alt) + 4 * (lane & 7);
+                const float *pc1 = blk + 32 * win_blk(p, pos, d1 < T ? d1 : 0, T, alt) + 4 * (lane & 7);
+                const uint32_t sp0 = smem_u32(&sh.panel[sl][0][4 * lane]);
+                const bool on0 = lane < q4, on1 = lane + 32 < q4;
                 unsigned mm = st;
                 for (int j = 0; mm; j++) {
                     const int t = __ffs(mm) - 1;
                     mm &= mm - 1;
-                    const float *rowp = Ad + (size_t)(32 * k + t) * sp;
-                    if (lane < q4)
-                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&sh.panel[sl][j][4 * lane])),
-                                     "l"(rowp + cb0)
+                    const int ro = t * sp;
+                    if (on0)
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sp0 + 4 * kPW * j), "l"(pc0 + ro)
                                      : "memory");
-                    if (lane + 32 < q4)
-                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&sh.panel[sl][j][4 * lane + 128])),
-                                     "l"(rowp + cb1)
+                    if (on1)
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sp0 + 4 * kPW * j + 512), "l"(pc1 + ro)
                                      : "memory");
                 }
                 // 1/A_ii of the block's rows, as the dense-stream kernel forms it (padding rows: 0);
@@ -485,12 +490,22 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 for (;;) {
                     const float xn = xo + fmaxf(w, -xo);   // = max(xo - ac/A_ii, 0)
                     const float dl = xn - xo;              // this row's change if it is the next one
+#if RGS_REDUX
+                    const bool cand = (fwd ? lane >= pos_r : lane <= pos_r) && xn != xo;
+                    const int t = fwd ? (int)__reduce_min_sync(0xffffffffu, cand ? (unsigned)lane : 32u)
+                                      : (int)__reduce_max_sync(0xffffffffu, cand ? (unsigned)lane + 1u : 0u) - 1;
+#pragma unroll
+                    for (int d = 0; d < kRgsWin; d++)   // (forward: pv = 0 beyond nsub)
+                        if (!ALT || ((vmask >> d) & 1u)) acc[d] = fmaf(pvp[d], dvp, acc[d]);
+                    if (t < 0 || t > 31) break;
+#else
                     const unsigned m = __ballot_sync(0xffffffffu, (fwd ? lane >= pos_r : lane <= pos_r) && xn != xo);
+                    const int t = fwd ? __ffs(m) - 1 : 31 - __clz(m);   // -1 when m == 0
 #pragma unroll
                     for (int d = 0; d < kRgsWin; d++)   // (forward: pv = 0 beyond nsub)
                         if (!ALT || ((vmask >> d) & 1u)) acc[d] = fmaf(pvp[d], dvp, acc[d]);
                     if (m == 0u) break;
-                    const int t = fwd ? __ffs(m) - 1 : 31 - __clz(m);
+#endif
                     const float dv = __shfl_sync(0xffffffffu, dl, t);
                     const float a0 = dgt[32 * t];
                     if (lane == t) xo = xn;   // (the list entry is written after the block, below)
