@@ -69,7 +69,7 @@ struct BinLayout {
 
 // The residual GS kernel's solver carries the contributions of each step's changes to the next
 // kRgsWin row blocks itself (k_rgs.cu); it reads them from the dense row-major A~ only.
-constexpr int kRgsWin = 7;
+constexpr int kRgsWin = 7;   // (9 and 11 measured slower: more carry work per change)
 
 // S5 + S6 on the tensor cores (k_psf.cu): int8 digit operands of the kept steering vectors
 // (opA: psf_opa_bytes, opB: psf_opb_bytes for sum rp rows; rsc: sum rp doubles), b~ = b[keep]

@@ -79,6 +79,7 @@ constexpr int kWSolver = 4, kWPanel = 5, kWRows = 6;
 constexpr int kRStg = RGS_STG;       // panel staging depth (steps)
 constexpr int kNP = RGS_NP;          // panels staged per step (predicted rows beyond: loaded on demand)
 constexpr int kPW = kRgsWin * 32;   // panel floats: blocks of steps s+1..s+W of one row
+constexpr int kPPL = (kRgsWin * 8 + 31) / 32;   // 16-byte panel pieces per producer lane
 // pending-buffer slots: the contributions to a block wait in the slot of the step that will read
 // it, (step mod 16).  At stream step s the pending visits are those of steps s .. s + nsub; a slot is
 // written for the visit at step S + 16 from stream step S + 16 - nsub >= S + 9 on, and the stream
@@ -87,8 +88,9 @@ constexpr int kPW = kRgsWin * 32;   // panel floats: blocks of steps s+1..s+W of
 // previous visit's block has committed it.
 constexpr int kPendBlk = 16;
 constexpr int kPendF = kPendBlk * 32;
-static_assert(kRgsWin == 7, "pending-slot reuse distance assumes a 7-block carry window");
+static_assert(kRgsWin + 2 <= kPendBlk, "pending / published slots are reused after kPendBlk steps");
 constexpr int kNList = RGS_NLIST;    // change-list ring (steps; > kRgsWin + 2)
+static_assert(kNList > kRgsWin + 2, "the row producer must stay within the change-list ring");
 constexpr int kCP = 2;               // stream: chunks held in registers per pass
 constexpr int kNSlot = RGS_NSLOT;    // row ring: batches in flight
 constexpr int kRegCh = 4;            // register-resident r: 128-column chunks per stream warp
@@ -349,22 +351,27 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 }
                 // panel segment d-1 (pieces 8(d-1) .. 8(d-1)+7) holds the columns of the block of step s+d
                 const int q4 = pw >> 2;   // 16-byte pieces per panel
-                const int d0 = 1 + (lane >> 3), d1 = d0 + 4;
-                const float *pc0 = blk + 32 * win_blk(p, pos, d0 < T ? d0 : 0, T, alt) + 4 * (lane & 7);
-                const float *pc1 = blk + 32 * win_blk(p, pos, d1 < T ? d1 : 0, T, alt) + 4 * (lane & 7);
+                // lane piece 32i + lane (i < kPPL) is segment 4i + (lane >> 3)
+                const float *pc[kPPL];
+                bool on[kPPL];
+#pragma unroll
+                for (int i = 0; i < kPPL; i++) {
+                    const int d = 1 + 4 * i + (lane >> 3);
+                    pc[i] = blk + 32 * win_blk(p, pos, d < T ? d : 0, T, alt) + 4 * (lane & 7);
+                    on[i] = 32 * i + lane < q4;
+                }
                 const uint32_t sp0 = smem_u32(&sh.panel[sl][0][4 * lane]);
-                const bool on0 = lane < q4, on1 = lane + 32 < q4;
                 unsigned mm = st;
                 for (int j = 0; mm; j++) {
                     const int t = __ffs(mm) - 1;
                     mm &= mm - 1;
                     const int ro = t * sp;
-                    if (on0)
-                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sp0 + 4 * kPW * j), "l"(pc0 + ro)
-                                     : "memory");
-                    if (on1)
-                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sp0 + 4 * kPW * j + 512), "l"(pc1 + ro)
-                                     : "memory");
+#pragma unroll
+                    for (int i = 0; i < kPPL; i++)
+                        if (on[i])
+                            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sp0 + 4 * kPW * j + 512 * i),
+                                         "l"(pc[i] + ro)
+                                         : "memory");
                 }
                 // 1/A_ii of the block's rows, as the dense-stream kernel forms it (padding rows: 0);
                 // the diagonal of the next step's block is loaded one step ahead
