@@ -174,7 +174,7 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 constexpr double kDxScale = 0x1p896;
 __device__ __forceinline__ double nn_scaled(float f) {
     const unsigned u = __float_as_uint(f);
-    return __hiloint2double((int)(u >> 3), (int)(u << 29));
+    return __hiloint2double((int)(u >> 3), (int)(u << 29));   // (IMAD.WIDE.U32 u * 2^29 measured slower)
 }
 __device__ __forceinline__ unsigned long long clk() {
     unsigned long long t;
@@ -439,9 +439,13 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
             }
             if (pf && lane == 0) { prof[12] = tw; prof[13] = ti; }
         } else if (wid == kWSolver) {
-            // ================= solver: lane = row 32k + lane of the current block.  Its carries are
+            // ================= solver: lane = row 32k + rl of the current block, rl = 31 - lane for
+            // forward sweeps (the next changing row in order is then the HIGHEST set ballot bit: one
+            // FLO instead of BREV + FLO on the row-to-row chain), rl = lane in the alternating
+            // kernel.  Its carries are
             // fp32 (the residual only needs fp32 for the chain); the exact fp64 contributions are
             // committed to r by the stream warps (pending buffer, see below).
+            const int rl = ALT ? lane : (lane ^ 31);   // this lane's row in the block
             float carry[kRgsWin];
 #pragma unroll
             for (int d = 0; d < kRgsWin; d++) carry[d] = 0.f;
@@ -451,7 +455,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 const bool fwd = sweep_fwd(p, alt);
                 const int k = fwd ? pos : T - 1 - pos;
                 const int sl = s % kRStg, li = s % kNList;
-                const int row = 32 * k + lane;
+                const int row = 32 * k + rl;
                 const float x0 = xs[row];   // this row's x before the step (its list entry's xo)
                 float xo = x0;
                 // the carry of step s + d goes to the block of step s + d only at its first occurrence
@@ -470,14 +474,15 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 }
                 mbar_wait(&sh.stg_full[sl], (s / kRStg) & 1);
                 const unsigned smk = sh.smask[sl];
-                const float invd = use_ivs ? ivs[row] : sh.sinv[sl][lane];
+                const float invd = use_ivs ? ivs[row] : sh.sinv[sl][rl];
                 const unsigned long long t1 = pf ? clk() : 0ull;
                 const int sw = max(s - nsub - 1, vprev);   // the stream step the stored r of this block needs
                 if (sw >= 0) mbar_wait(&sh.sdone[sw % kNList], (sw / kNList) & 1);
                 const unsigned long long t2 = pf ? clk() : 0ull;
                 // r of the block as of stream step sw (before any stream step: r = -b~)
-                const float ac = (float)(REGR ? (sw >= 0 ? pend[32 * (s & (kPendBlk - 1)) + lane] : -bt[L.v_off + row])
-                                              : rs[row]) + carry[0];
+                const float ac = (REGR ? (sw >= 0 ? reinterpret_cast<const float *>(pend)[32 * (s & (kPendBlk - 1)) + rl]
+                                                  : (float)-bt[L.v_off + row])
+                                       : (float)rs[row]) + carry[0];
                 float acc[kRgsWin];
 #pragma unroll
                 for (int d = 0; d < kRgsWin; d++) acc[d] = 0.f;
@@ -488,7 +493,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 // -(dv/A_ii) A[row][32k+t], read from the staged diagonal tile (row t, by symmetry /
                 // the transposed store) -- the only shared-memory load on the row-to-row chain
                 float w = -ac * invd;
-                const float *dgt = sh.diag[sl] + lane;
+                const float *dgt = sh.diag[sl] + rl;
                 // the previous change's panel values and dv: consumed one iteration later, after the
                 // next ballot, so that the chain never waits for the panel loads
                 float pvp[kRgsWin], dvp = 0.f;
@@ -498,30 +503,33 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                     const float xn = xo + fmaxf(w, -xo);   // = max(xo - ac/A_ii, 0)
                     const float dl = xn - xo;              // this row's change if it is the next one
 #if RGS_REDUX
-                    const bool cand = (fwd ? lane >= pos_r : lane <= pos_r) && xn != xo;
-                    const int t = fwd ? (int)__reduce_min_sync(0xffffffffu, cand ? (unsigned)lane : 32u)
-                                      : (int)__reduce_max_sync(0xffffffffu, cand ? (unsigned)lane + 1u : 0u) - 1;
+                    const bool cand = (fwd ? rl >= pos_r : rl <= pos_r) && xn != xo;
+                    const int t = fwd ? (int)__reduce_min_sync(0xffffffffu, cand ? (unsigned)rl : 32u)
+                                      : (int)__reduce_max_sync(0xffffffffu, cand ? (unsigned)rl + 1u : 0u) - 1;
 #pragma unroll
                     for (int d = 0; d < kRgsWin; d++)   // (forward: pv = 0 beyond nsub)
                         if (!ALT || ((vmask >> d) & 1u)) acc[d] = fmaf(pvp[d], dvp, acc[d]);
                     if (t < 0 || t > 31) break;
 #else
-                    const unsigned m = __ballot_sync(0xffffffffu, (fwd ? lane >= pos_r : lane <= pos_r) && xn != xo);
-                    const int t = fwd ? __ffs(m) - 1 : 31 - __clz(m);   // -1 when m == 0
+                    const unsigned m = __ballot_sync(0xffffffffu, (fwd ? rl >= pos_r : rl <= pos_r) && xn != xo);
+                    // the row (in the block) of the next change: forward sweeps take the lowest row,
+                    // i.e. (ALT = false, rl = 31 - lane) the highest ballot bit
+                    const int tl = 31 - __clz(m);   // (FLO) the highest ballot bit, -1 when m == 0
+                    const int t = !ALT ? tl ^ 31 : fwd ? __ffs(m) - 1 : tl;
 #pragma unroll
                     for (int d = 0; d < kRgsWin; d++)   // (forward: pv = 0 beyond nsub)
                         if (!ALT || ((vmask >> d) & 1u)) acc[d] = fmaf(pvp[d], dvp, acc[d]);
                     if (m == 0u) break;
 #endif
-                    const float dv = __shfl_sync(0xffffffffu, dl, t);
+                    const float dv = __shfl_sync(0xffffffffu, dl, ALT ? t : tl);
                     const float a0 = dgt[32 * t];
-                    if (lane == t) xo = xn;   // (the list entry is written after the block, below)
+                    if (rl == t) xo = xn;   // (the list entry is written after the block, below)
                     w = fmaf(-invd * dv, a0, w);
                     // off the chain: the carries, from row t's staged panel (element 32(d-1) + lane =
                     // A[32k+t][32 blk(s+d) + lane] = A[32 blk(s+d) + lane][32k+t]; segments beyond nsub
                     // are zero); a row not staged is added after the block from global memory
                     const bool stg = (smk >> t) & 1u;
-                    const float *pr = sh.panel[sl][stg ? __popc(smk & ((1u << t) - 1u)) : 0] + lane;
+                    const float *pr = sh.panel[sl][stg ? __popc(smk & ((1u << t) - 1u)) : 0] + rl;
                     dvp = stg ? dv : 0.f;
 #pragma unroll
                     for (int d = 0; d < kRgsWin; d++) pvp[d] = pr[32 * d];
@@ -532,8 +540,8 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 // the carries of the changed rows that were not staged (rare: the prediction missed)
                 for (unsigned mm = chg & ~smk; mm; mm &= mm - 1) {
                     const int t = __ffs(mm) - 1;
-                    const float dv = __shfl_sync(0xffffffffu, xo - x0, t);
-                    const float *rw = Ad + (size_t)(32 * k + t) * sp + lane;
+                    const float dv = __shfl_sync(0xffffffffu, xo - x0, ALT ? t : t ^ 31);
+                    const float *rw = Ad + (size_t)(32 * k + t) * sp + rl;
 #pragma unroll
                     for (int d = 0; d < kRgsWin; d++)
                         if (d < nsub && (!ALT || ((vmask >> d) & 1u)))
@@ -543,8 +551,8 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 const unsigned long long t3 = pf ? clk() : 0ull;
                 xs[row] = xo;
                 // the block's changes in sweep order (each row changes at most once per visit)
-                if ((chg >> lane) & 1u) {
-                    const int e = fwd ? __popc(chg & ((1u << lane) - 1u)) : __popc(chg >> lane) - 1;
+                if ((chg >> rl) & 1u) {
+                    const int e = fwd ? __popc(chg & ((1u << rl) - 1u)) : __popc(chg >> rl) - 1;
                     lst[e].xn = xo;
                     lst[e].xo = x0;
                     lst[e].c = row;
@@ -601,13 +609,13 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 const int qb = bb >> 2;
                 if ((qb % kNStream) == w && (lane >> 3) == (bb & 3)) {
                     const int cb = qb / kNStream;
-                    double *dst = pend + 32 * ((s0 + d) & (kPendBlk - 1)) + 4 * (lane & 7);
+                    // rounded to fp32 here (the solver's recurrence is fp32), off the solver's path
+                    float *dst = reinterpret_cast<float *>(pend) + 32 * ((s0 + d) & (kPendBlk - 1)) + 4 * (lane & 7);
 #pragma unroll
                     for (int c = 0; c < kRegCh; c++)
-                        if (c == cb) {
-                            reinterpret_cast<double2 *>(dst)[0] = make_double2(r[c][0], r[c][1]);
-                            reinterpret_cast<double2 *>(dst)[1] = make_double2(r[c][2], r[c][3]);
-                        }
+                        if (c == cb)
+                            *reinterpret_cast<float4 *>(dst) =
+                                make_float4((float)r[c][0], (float)r[c][1], (float)r[c][2], (float)r[c][3]);
                 }
             };
             int b = 0;
@@ -821,8 +829,12 @@ int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int m
     static const int per_sm_env = getenv("DWC_RGS_PER_SM") ? atoi(getenv("DWC_RGS_PER_SM")) : 0;   // experiment
     const size_t per2 = 114 * 1024 - 1024;
     size_t ring;
-    // two per SM when the band has more bins than SMs and every ring slot still holds 2 rows
-    const bool two = kRMinBlocks < 2 ? false
+    // r in registers (one CTA per SM: up to 255 registers) when the system fits the stream warps'
+    // chunks (and, below, a ring slot holds a whole row): measured faster than two CTAs per SM
+    static const bool no_regr = getenv("DWC_RGS_NO_REGR") != nullptr;   // experiment
+    const bool regr_fits = max_sp <= kRegMaxSp && kNStream == 5 && !no_regr;
+    // else two per SM when the band has more bins than SMs and every ring slot still holds 2 rows
+    const bool two = (kRMinBlocks < 2 || regr_fits) ? false
                      : per_sm_env ? per_sm_env == 2 && per2 > base + 2048
                                 : n_bins > num_sms && per2 > base && (per2 - base) / (4 * kNSlot) >= 2 * (size_t)max_sp;
     if (two)
@@ -833,10 +845,7 @@ int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int m
     const int slot_floats = (int)(ring / (4 * kNSlot)) / 128 * 128;   // floats per ring slot
     if (slot_floats < 128) return -1;
     const size_t smem = base + (size_t)slot_floats * 4 * kNSlot + 512;   // + slack: a row's last chunk reads past it
-    // r in registers (one CTA per SM: up to 255 registers) when the system fits the stream warps'
-    // chunks and a ring slot holds a whole row
-    static const bool no_regr = getenv("DWC_RGS_NO_REGR") != nullptr;   // experiment
-    const bool regr = !two && max_sp <= kRegMaxSp && slot_floats >= max_sp && kNStream == 5 && !no_regr;
+    const bool regr = regr_fits && slot_floats >= max_sp;
     const auto kern = alt ? (regr ? rgs_kernel<true, true> : rgs_kernel<true, false>)
                           : (regr ? rgs_kernel<false, true> : rgs_kernel<false, false>);
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)

@@ -5,7 +5,7 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 
-template <int BG>
+template <int BG, int NPV = 7>
 __global__ void chain(int iters, float *out, unsigned long long *cyc, int skip0) {
     __shared__ float diag[32 * 32];
     __shared__ float panel[8][224];
@@ -25,7 +25,7 @@ __global__ void chain(int iters, float *out, unsigned long long *cyc, int skip0)
             const unsigned m = __ballot_sync(0xffffffffu, lane >= pos_r && xn != xo);
             const int t = __ffs(m) - 1;
 #pragma unroll
-            for (int d = 0; d < 7; d++) acc[d] = fmaf(pvp[d], dvp, acc[d]);
+            for (int d = 0; d < NPV; d++) acc[d] = fmaf(pvp[d], dvp, acc[d]);
             if (m == 0u) { pos_r = 0; continue; }
             const float dv = __shfl_sync(0xffffffffu, dl, t);
             const float a0 = diag[32 * t + lane];
@@ -34,7 +34,7 @@ __global__ void chain(int iters, float *out, unsigned long long *cyc, int skip0)
             const float *pr = panel[t & 7] + lane;
             dvp = dv;
 #pragma unroll
-            for (int d = 0; d < 7; d++) pvp[d] = pr[32 * d];
+            for (int d = 0; d < NPV; d++) pvp[d] = pr[32 * d];
             pos_r = (t + 1) & 31;
         }
         const unsigned long long t1 = clock64();
@@ -83,18 +83,17 @@ int main() {
     cudaMalloc(&out, 4096 * 4);
     cudaMalloc(&cyc, 8);
     const int iters = 100000;
-    for (int mode = 0; mode <= 4; mode++) {
+    for (int mode = 0; mode <= 3; mode++) {
         for (int rep = 0; rep < 2; rep++) {
             switch (mode) {
-                case 0: chain<0><<<1, 32>>>(iters, out, cyc, 0); break;
-                case 1: chain<1><<<1, 32 * 6>>>(iters, out, cyc, 0); break;
-                case 2: chain<2><<<1, 32 * 6>>>(iters, out, cyc, 0); break;
-                case 3: chain<3><<<1, 32 * 6>>>(iters, out, cyc, 0); break;
-                case 4: chain<4><<<1, 32 * 6>>>(iters, out, cyc, 0); break;
+                case 0: chain<0, 7><<<1, 32>>>(iters, out, cyc, 0); break;
+                case 1: chain<0, 1><<<1, 32>>>(iters, out, cyc, 0); break;
+                case 2: chain<1, 7><<<1, 32 * 6>>>(iters, out, cyc, 0); break;
+                case 3: chain<1, 1><<<1, 32 * 6>>>(iters, out, cyc, 0); break;
             }
             cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
         }
-        printf("background mode %d (0 none, 1 lds+f2f+dfma, 2 lds only, 3 f2f+dfma regs, 4 lds+nn+dfma), 5 warps: %.1f cycles per change\n", mode, (double)h / iters);
+        printf("mode %d (0: alone 7 panel loads, 1: alone 1 load, 2: 5 stream warps 7 loads, 3: 5 stream warps 1 load): %.1f cycles per change\n", mode, (double)h / iters);
     }
     return 0;
 }
