@@ -1,5 +1,7 @@
 """Build the in-tree C-ABI library libdwc.so for sm_100a with nvcc (no JIT, no torch
-extension machinery): `python -m paper_1608_05179_b200.build`."""
+extension machinery): `python -m paper_1608_05179_b200.build`.  `--checked` (or build(checked=True))
+builds libdwc_checked.so with -DDWC_CHECKED: device-side invariant checks in the Gauss-Seidel
+kernels and mbarrier watchdogs (tests/test_gpu_checked.py runs it)."""
 import os
 import subprocess
 import sys
@@ -17,6 +19,7 @@ COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcom
 COMMON += os.environ.get("DWC_NVCC_EXTRA", "").split()
 LIB = os.environ.get("DWC_LIB", LIB)
 BUILD = os.environ.get("DWC_BUILD_DIR", BUILD)
+LIB_CHECKED = os.path.join(HERE, "libdwc_checked.so")
 SOURCES = {
     "dwc_api.cu": [],
     "k_das.cu": [],
@@ -30,35 +33,39 @@ SOURCES = {
 }
 
 
-def _compile(name, extra, verbose):
+def _compile(name, extra, verbose, bdir=None, defs=()):
+    bdir = bdir or BUILD
     src = os.path.join(CSRC, name)
-    obj = os.path.join(BUILD, name.replace(".cu", ".o"))
-    cmd = [NVCC, *COMMON, *extra, "-c", src, "-o", obj]
+    obj = os.path.join(bdir, name.replace(".cu", ".o"))
+    cmd = [NVCC, *COMMON, *defs, *extra, "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {name}:\n{r.stdout}\n{r.stderr}")
-    with open(os.path.join(BUILD, name + ".ptxas.txt"), "w") as f:
+    with open(os.path.join(bdir, name + ".ptxas.txt"), "w") as f:
         f.write(r.stderr)
     if verbose:
         print(r.stderr, file=sys.stderr)
     return obj
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, checked: bool = False) -> str:
+    lib = LIB_CHECKED if checked else LIB
+    bdir = BUILD + "_checked" if checked else BUILD
+    defs = ("-DDWC_CHECKED",) if checked else ()
+    os.makedirs(bdir, exist_ok=True)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(HERE, "..", "include", "dwc.h")]
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(d) for d in deps):
-        return LIB
+    if not force and os.path.exists(lib) and os.path.getmtime(lib) >= max(os.path.getmtime(d) for d in deps):
+        return lib
     with ThreadPoolExecutor(len(SOURCES)) as ex:
-        objs = list(ex.map(lambda kv: _compile(kv[0], kv[1], verbose), SOURCES.items()))
-    tmp = LIB + ".tmp%d" % os.getpid()
+        objs = list(ex.map(lambda kv: _compile(kv[0], kv[1], verbose, bdir, defs), SOURCES.items()))
+    tmp = lib + ".tmp%d" % os.getpid()
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-Xcompiler", "-fvisibility=hidden"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, checked="--checked" in sys.argv))

@@ -3,8 +3,25 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include "../../include/dwc.h"
+
+// Checked build (-DDWC_CHECKED, libdwc_checked.so, run by tests/test_gpu_checked.py): device-side
+// invariants of the Gauss-Seidel kernels' rings, slots, parities and indices report and trap;
+// mbarrier waits get a watchdog.  Compiled out of the production library.
+#ifdef DWC_CHECKED
+#define DWC_DCHECK(cond, what)                                                                          \
+    do {                                                                                                \
+        if (!(cond)) {                                                                                  \
+            printf("[dwc checked] %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, (int)blockIdx.x, \
+                   (int)threadIdx.x, what);                                                             \
+            __trap();                                                                                   \
+        }                                                                                               \
+    } while (0)
+#else
+#define DWC_DCHECK(cond, what) ((void)0)
+#endif
 
 namespace dwc {
 

@@ -142,6 +142,27 @@ __device__ __forceinline__ void mbar_init(unsigned long long *b, uint32_t count)
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
 }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+#ifdef DWC_CHECKED
+// checked build: waits that have not completed after ~2^24 polls report and trap
+template <bool kCluster>
+__device__ __forceinline__ void mbar_wait_checked(unsigned long long *b, uint32_t parity) {
+    for (unsigned it = 0;; it++) {
+        uint32_t ok;
+        if (kCluster)
+            asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+                         "selp.u32 %0, 1, 0, p;\n\t}"
+                         : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
+        else
+            asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+                         "selp.u32 %0, 1, 0, p;\n\t}"
+                         : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
+        if (ok) return;
+        DWC_DCHECK(it < (1u << 24), "gs: mbarrier wait never completes");
+    }
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *b, uint32_t parity) { mbar_wait_checked<true>(b, parity); }
+__device__ __forceinline__ void mbar_wait_cta(unsigned long long *b, uint32_t parity) { mbar_wait_checked<false>(b, parity); }
+#else
 __device__ __forceinline__ void mbar_wait(unsigned long long *b, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
@@ -164,6 +185,7 @@ __device__ __forceinline__ void mbar_wait_cta(unsigned long long *b, uint32_t pa
         "r"(parity)
         : "memory");
 }
+#endif
 __device__ __forceinline__ void mbar_arrive_local(unsigned long long *b) {
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
@@ -403,6 +425,9 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                         if (ppf) t0 = clock64();
                         mbar_wait_cta(&sh.empty[slot], ph ^ 1);
                         if (ppf) { const unsigned long long t = clock64(); p_wait += t - t0; t0 = t; }
+                        DWC_DCHECK(slot < (uint32_t)nring && nt >= 1 && nt <= chunk, "gs producer: ring slot / chunk");
+                        DWC_DCHECK(!kXtra || (int)slot < nbase || ((int)slot - nbase + 1) * chunk <= xtra_tiles,
+                                   "gs producer: extra ring slot beyond its tiles");
                         mbar_expect_tx(&sh.full[slot], (uint32_t)nt * kTile * 4);
                         if (prof) sh.issue_t[slot] = clock64();
                         bulk_g2s(slot_ptr(slot), Ab + (size_t)tt * kTile, (uint32_t)nt * kTile * 4, &sh.full[slot]);
@@ -530,6 +555,7 @@ gs_cluster_kernel(int n_items, const GsItem *__restrict__ items, const BinLayout
                             int t = first;
                             for (; t < nt; t += n_sw) {
                                 const int ord = sr.ord0 + off + t, J = ownJ[ord];
+                                DWC_DCHECK(slot < (uint32_t)nring && J >= 0 && J < T, "gs consumer: slot / owned block");
                                 const float *tile = slot_ptr(slot) + t * kTile;
                                 if (sg == 0) {
                                     tile_dot(tile, xs + 32 * J, rq, cq, acc);

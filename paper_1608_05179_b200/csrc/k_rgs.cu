@@ -122,8 +122,8 @@ __device__ __forceinline__ void mbar_init(unsigned long long *b, uint32_t count)
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
 }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
-#ifdef RGS_WATCHDOG
-// debug build: a wait that has not completed after ~2^24 polls reports itself and traps
+#if defined(RGS_WATCHDOG) || defined(DWC_CHECKED)
+// debug / checked build: a wait that has not completed after ~2^24 polls reports itself and traps
 __device__ __forceinline__ void mbar_wait(unsigned long long *b, uint32_t parity) {
     for (unsigned it = 0;; it++) {
         uint32_t ok;
@@ -331,6 +331,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 // solver may be updating it right now when the block was visited < kRStg steps
                 // ago, either value is valid)
                 unsigned m = *(volatile unsigned *)&pmask[k];
+                DWC_DCHECK(k >= 0 && k < T, "panel producer: block");
                 unsigned st = 0;
                 for (int n = 0; m && n < kNP; n++) {
                     st |= m & (0u - m);   // lowest set bit
@@ -401,6 +402,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 const int li = s % kNList;
                 mbar_wait(&sh.dready[li], (s / kNList) & 1);
                 const int n = sh.cnt[li];
+                DWC_DCHECK(n >= 0 && n <= 32, "row producer: change-list length");
                 if (lane < n) sh.dxs[li][lane] = entry_dx(sh.list[li][lane]) * ((REGR && nonneg) ? kDxScale : 1.0);   // exact
                 __syncwarp();
                 if (lane == 0) {
@@ -412,6 +414,9 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                         mbar_wait(&sh.rempty[h], ((b / kNSlot) & 1) ^ 1);
                         const unsigned long long t1 = pf ? clk() : 0ull;
                         const int nb = min(rg.upb, nu - u0);
+                        DWC_DCHECK(h < kNSlot && nb >= 1 && (rg.nseg > 1 || nb * sp <= slot_floats) &&
+                                       (rg.nseg == 1 || nb * rg.seg <= slot_floats),
+                                   "row producer: ring slot overflow");
                         float *dst = ring + (size_t)h * slot_floats;
                         if (rg.nseg == 1) {
                             mbar_expect_tx(&sh.rfull[h], (uint32_t)nb * sp * 4);
@@ -516,6 +521,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                     // i.e. (ALT = false, rl = 31 - lane) the highest ballot bit
                     const int tl = 31 - __clz(m);   // (FLO) the highest ballot bit, -1 when m == 0
                     const int t = !ALT ? tl ^ 31 : fwd ? __ffs(m) - 1 : tl;
+                    DWC_DCHECK(m == 0u || (t >= 0 && t < 32 && !((chg >> t) & 1u)), "solver: a row changes twice in one visit");
 #pragma unroll
                     for (int d = 0; d < kRgsWin; d++)   // (forward: pv = 0 beyond nsub)
                         if (!ALT || ((vmask >> d) & 1u)) acc[d] = fmaf(pvp[d], dvp, acc[d]);
@@ -550,6 +556,8 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 }
                 const unsigned long long t3 = pf ? clk() : 0ull;
                 xs[row] = xo;
+                DWC_DCHECK(q == __popc(chg) && q <= 32, "solver: change count");
+                DWC_DCHECK(sw < s && (sw < 0 || sw >= s - nsub - 1), "solver: stored-residual step");
                 // the block's changes in sweep order (each row changes at most once per visit)
                 if ((chg >> rl) & 1u) {
                     const int e = fwd ? __popc(chg & ((1u << rl) - 1u)) : __popc(chg >> rl) - 1;
@@ -587,6 +595,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
             const int w = (wid < 4) ? wid : wid - 3;
             const int nq = (sp + 127) >> 7;
             const int nch = (nq - w + kNStream - 1) / kNStream;   // chunks this warp owns (<= kRegCh)
+            DWC_DCHECK(nch >= 0 && nch <= kRegCh && rg.nseg == 1, "stream: register chunks");
             unsigned long long tlw = 0, tbw = 0, tap = 0, nb_all = 0;
             double r[kRegCh][4];
 #pragma unroll
@@ -606,6 +615,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 const bool rev = vp > s0 + d - nsub - 1;
                 if (before ? !(rev && vp == s0) : rev) return;
                 const int bb = sweep_fwd(p2, alt) ? q2 : T - 1 - q2;   // its block
+                DWC_DCHECK(bb >= 0 && bb < T && (bb >> 2) / kNStream < kRegCh, "stream: published block");
                 const int qb = bb >> 2;
                 if ((qb % kNStream) == w && (lane >> 3) == (bb & 3)) {
                     const int cb = qb / kNStream;

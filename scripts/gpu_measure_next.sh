@@ -1,0 +1,13 @@
+#!/bin/bash
+# The NEXT-row and variant bench lines (one B200): gpurun_out/next_<name>.log
+set -u
+mkdir -p gpurun_out
+run() { local name=$1; shift; timeout 900 python bench.py --no-cpu-baseline "$@" > gpurun_out/next_$name.log 2>&1; echo "$name rc=$?"; }
+run cfg3_cubic --order 3
+run cfg3_dr --dr
+run cfg3_alt --alt
+run cfg3_paper --paper
+run cfg3_snap --input snapshots
+run cfg3_dense_kernel --kernel dense
+run cfg4 --config cfg4 --steps 2 --warmup 3 --no-cvf
+run cfg5 --config cfg5 --steps 2 --warmup 3 --no-cvf

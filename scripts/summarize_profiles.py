@@ -65,18 +65,20 @@ def main():
     os.makedirs(OUT, exist_ok=True)
     launch_shares()
     summary = {}
-    for rep, name in (("gs_full.ncu-rep", "gs_sym_full"), ("psf_full.ncu-rep", "psf_tc_full"),
+    for rep, name in (("gs_full.ncu-rep", "rgs_full"), ("psf_full.ncu-rep", "psf_tc_full"),
                       ("das_full.ncu-rep", "das_full")):
         summary[name] = export(rep, name)
     print(json.dumps(summary, indent=1))
-    gs = summary.get("gs_sym_full")
+    gs = summary.get("rgs_full")
     if gs and gs["dram_read"] is not None:
-        # ncu reports bytes in the unit of the CSV's units row; raw page values are in bytes
+        # the default bench variant (bench.variant_key) on the residual kernel (gs_kernel 4)
         tp = os.path.join(ROOT, "profiles", "gs_traffic.json")
         d = json.load(open(tp)) if os.path.exists(tp) else {}
-        d["cfg3"] = gs["dram_read"] + gs["dram_write"]
-        d["_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum of one gs_cluster_kernel launch "
-                      "(symmetric-packed A~), ncu --set full, profiles/r01/gs_sym_full_raw.csv")
+        rel = os.path.relpath(os.path.join(OUT, "rgs_full_raw.csv"), ROOT)
+        d["cfg3|order1|dr0|alt0|csm|n1|g1"] = {
+            "dram_bytes": gs["dram_read"] + gs["dram_write"], "gs_kernel": 4,
+            "source": f"{rel} (rgs_kernel: dram read {gs['dram_read'] / 1e6:.1f} MB + write "
+                      f"{gs['dram_write'] / 1e6:.1f} MB per launch, L2 hit {gs['l2_hit']:.1f} %)"}
         json.dump(d, open(tp, "w"), indent=1)
 
 
