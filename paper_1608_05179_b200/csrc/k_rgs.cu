@@ -94,7 +94,7 @@ static_assert(kNList > kRgsWin + 2, "the row producer must stay within the chang
 constexpr int kCP = 2;               // stream: chunks held in registers per pass
 constexpr int kNSlot = RGS_NSLOT;    // row ring: batches in flight
 constexpr int kRegCh = 4;            // register-resident r: 128-column chunks per stream warp
-constexpr int kRegMaxSp = 128 * kRegCh * 5;   // (5 stream warps) the largest system it holds
+constexpr int kRegMaxSp = 128 * kRegCh * kNStream;   // the largest system it holds
 
 struct __align__(16) RgsEntry {
     float xn, xo;   // x of the row after / before the change (dx = xn - xo, exact in fp64)
@@ -160,6 +160,46 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned long long *b, uint32_t b
     asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
                  : "memory");
 }
+// ---- cluster mode (systems above kRegMaxSp: the residual's columns split over the CTAs of a cluster)
+__device__ __forceinline__ uint32_t cl_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cl_size() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cl_map(const void *p, uint32_t rank) {   // this smem address in CTA `rank`
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cl_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void st_cl_s32(uint32_t raddr, int v) {
+    asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(raddr), "r"(v) : "memory");
+}
+// st.async: registers -> another CTA's shared memory, the bytes completing on its mbarrier
+__device__ __forceinline__ void st_async_v4b32(uint32_t raddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d,
+                                               uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(raddr),
+                 "r"(a), "r"(b), "r"(c), "r"(d), "r"(rbar)
+                 : "memory");
+}
+__device__ __forceinline__ void st_async_b32(uint32_t raddr, uint32_t a, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(raddr), "r"(a), "r"(rbar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cl(uint32_t rbar) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rbar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx_cl(uint32_t rbar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(rbar), "r"(bytes)
+                 : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, unsigned long long *bar) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
@@ -215,7 +255,7 @@ __device__ __forceinline__ RingGeom ring_geom(int sp, int slot_floats) {
 // Profile slots (DWC_RGS_PROF=1), item 0 = the largest bin: solver [0] tile wait, [1] stream
 // wait, [2] ballot loop, [3] rest, [4] steps, [5] changes; stream warp 0 [8] list wait, [9]
 // batch wait, [10] apply, [11] batches; row producer [12] ring wait, [13] issue; [14] total.
-constexpr int kProfSlots = 16;
+constexpr int kProfSlots = 24;
 constexpr int kProfItems = 1024;   // then per item: start, end (globaltimer ns), bin, changes
 
 // r (fp64, sp), the pending carried contributions (fp64, 16 blocks), x (fp32, sp), the prediction
@@ -242,7 +282,7 @@ __device__ __forceinline__ void apply_rows(double (&r)[kRegCh][4], const float *
     }
 }
 
-template <bool ALT, bool REGR>
+template <bool ALT, bool REGR, bool CLU>
 __global__ void __launch_bounds__(kRThreads, REGR ? 1 : kRMinBlocks)
 rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restrict__ lay, int *__restrict__ counter,
            const float *__restrict__ Adense, const double *__restrict__ bt, int sweeps, float *__restrict__ x_out,
@@ -251,9 +291,11 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
            unsigned long long *__restrict__ n_updates, unsigned long long *__restrict__ prof) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     RgsSmem &sh = *reinterpret_cast<RgsSmem *>(smem_raw);
+    // r (shared-memory residual path only: registers when REGR)
     double *rs = reinterpret_cast<double *>(smem_raw + sizeof(RgsSmem));
-    // carried contributions not yet in r (the visit at step S in slot S mod kPendBlk)
-    double *pend = rs + max_sp;
+    // carried contributions not yet in r (the visit at step S in slot S mod kPendBlk); with r in
+    // registers: the published fp32 r of the block each solver step reads
+    double *pend = rs + (REGR ? 0 : max_sp);
     float *xs = reinterpret_cast<float *>(pend + kPendF);
     // 1/A_ii of every row when shared memory allows (use_ivs), else per stage from the panel producer
     float *ivs = xs + max_sp;
@@ -262,10 +304,26 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     unsigned long long my_updates = 0, my_bytes = 0;
     constexpr int alt = ALT ? 1 : 0;   // forward sweeps: the visit sequence folds to pos, pos+1, ...
+    // cluster mode: the G CTAs of a cluster solve one bin; CTA c holds r of a contiguous range of
+    // 128-column chunks (registers), fetches that slice of every changed row and applies it; the
+    // leader (rank 0) also runs the solver and the panel producer.  The change lists reach the
+    // other CTAs by st.async (completing on their dready barriers), the published r of each
+    // block reaches the leader by st.async (completing on its sdone barriers).
+    const uint32_t crank = CLU ? cl_rank() : 0u;
+    const int G = CLU ? (int)cl_size() : 1;
+    const bool leader = crank == 0;
 
     for (;;) {
-        if (tid == 0) sh.item = atomicAdd(counter, 1);
-        __syncthreads();
+        if (CLU) {
+            if (leader && tid == 0) {
+                const int it = atomicAdd(counter, 1);
+                for (int c = 0; c < G; c++) st_cl_s32(cl_map(&sh.item, c), it);
+            }
+            cl_sync();
+        } else {
+            if (tid == 0) sh.item = atomicAdd(counter, 1);
+            __syncthreads();
+        }
         const int item = sh.item;
         if (item >= n_items) break;
         const int bin = order[item];
@@ -274,9 +332,16 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
         const int nsub = min(kRgsWin, T - 1);      // blocks the solver carries
         const int pw = nsub * 32;                  // panel floats
         const int total = sweeps * T;
-        const bool pf = prof != nullptr && item == 0;
+        // this CTA's columns: chunks [q_lo, q_hi) of the nq 128-column chunks (all of them unless CLU)
+        const int nq = (sp + 127) >> 7;
+        const int nqc = CLU ? (nq + G - 1) / G : nq;
+        const int q_lo = min(nq, (int)crank * nqc), q_hi = min(nq, q_lo + nqc);
+        const int col0 = 128 * q_lo;
+        const int swid = max(0, min(sp, 128 * q_hi) - col0);   // floats of a row this CTA applies
+        const int rstride = CLU ? 128 * nqc : sp;               // floats per row in the ring
+        const bool pf = prof != nullptr && item == 0 && leader;
         const unsigned long long t_item = pf ? clk() : 0ull;
-        if (prof && tid == 0 && item < kProfItems) {
+        if (prof && leader && tid == 0 && item < kProfItems) {
             unsigned long long t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
             prof[kProfSlots + 4 * item] = t;
@@ -284,7 +349,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
         const float *Ad = Adense + L.d_off;    // dense row-major sp x sp
         for (int i = tid; i < sp; i += kRThreads) {
             const double b = bt[L.v_off + i];
-            rs[i] = -b;   // r = A x0 - b with x0 = 0 (b~ zero padded)
+            if (!REGR) rs[i] = -b;   // r = A x0 - b with x0 = 0 (b~ zero padded)
             xs[i] = 0.f;
             if (use_ivs) ivs[i] = (i < nk) ? __frcp_rn(Ad[(size_t)i * sp + i]) : 0.f;
             // sweep 1 from x0 = 0 changes exactly the rows with b~ > 0
@@ -303,7 +368,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
             }
             for (int i = 0; i < kNList; i++) {
                 mbar_init(&sh.dready[i], 1);
-                mbar_init(&sh.sdone[i], kNStream);
+                mbar_init(&sh.sdone[i], kNStream * G);   // (CLU: every CTA's stream warps, at the leader)
                 mbar_init(&sh.dxready[i], 1);
             }
             for (int h = 0; h < kNSlot; h++) {
@@ -312,10 +377,14 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
             }
             fence_mbar_init();
         }
-        __syncthreads();
-        const RingGeom rg = ring_geom(sp, slot_floats);
+        if (CLU)
+            cl_sync();   // every CTA's barriers initialised before any remote arrival
+        else
+            __syncthreads();
+        const RingGeom rg = ring_geom(rstride, slot_floats);
 
         if (wid == kWPanel) {
+            if (!CLU || leader) {   // (cluster: the leader's)
             // ================= panel producer: the panels of the rows predicted to change, as
             // 16-byte cp.async copies spread over the warp's lanes (a 1 KB panel is 2 instructions;
             // one bulk copy per panel cost ~80 cycles of issue on a single lane)
@@ -393,6 +462,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 if (pf) { pw_wait += t1 - t0; pw_issue += clk() - t1; }
             }
             if (pf && lane == 0) { prof[7] = pw_wait; prof[15] = pw_issue; }
+            }
         } else if (wid == kWRows) {
             // ================= row producer: the exact dx of every change (all lanes), then the rows
             // of every step's changes into the ring (lane 0)
@@ -407,22 +477,22 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 __syncwarp();
                 if (lane == 0) {
                     mbar_arrive(&sh.dxready[li]);
-                    const int nu = n * rg.nseg;
+                    const int nu = swid > 0 ? n * rg.nseg : 0;   // (a CTA without columns fetches nothing)
                     for (int u0 = 0; u0 < nu; u0 += rg.upb, b++) {
                         const int h = b % kNSlot;
                         const unsigned long long t0 = pf ? clk() : 0ull;
                         mbar_wait(&sh.rempty[h], ((b / kNSlot) & 1) ^ 1);
                         const unsigned long long t1 = pf ? clk() : 0ull;
                         const int nb = min(rg.upb, nu - u0);
-                        DWC_DCHECK(h < kNSlot && nb >= 1 && (rg.nseg > 1 || nb * sp <= slot_floats) &&
+                        DWC_DCHECK(h < kNSlot && nb >= 1 && (rg.nseg > 1 || nb * rstride <= slot_floats) &&
                                        (rg.nseg == 1 || nb * rg.seg <= slot_floats),
                                    "row producer: ring slot overflow");
                         float *dst = ring + (size_t)h * slot_floats;
-                        if (rg.nseg == 1) {
-                            mbar_expect_tx(&sh.rfull[h], (uint32_t)nb * sp * 4);
+                        if (rg.nseg == 1) {   // whole rows (CLU: this CTA's slice of them)
+                            mbar_expect_tx(&sh.rfull[h], (uint32_t)nb * swid * 4);
                             for (int j = 0; j < nb; j++)
-                                bulk_g2s(dst + (size_t)j * sp, Ad + (size_t)sh.list[li][u0 + j].c * sp, (uint32_t)sp * 4,
-                                         &sh.rfull[h]);
+                                bulk_g2s(dst + (size_t)j * rstride, Ad + (size_t)sh.list[li][u0 + j].c * sp + col0,
+                                         (uint32_t)swid * 4, &sh.rfull[h]);
                         } else {
                             uint32_t bytes = 0;
                             for (int j = 0; j < nb; j++) {
@@ -444,6 +514,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
             }
             if (pf && lane == 0) { prof[12] = tw; prof[13] = ti; }
         } else if (wid == kWSolver) {
+          if (!CLU || leader) {   // (cluster: the leader's)
             // ================= solver: lane = row 32k + rl of the current block, rl = 31 - lane for
             // forward sweeps (the next changing row in order is then the HIGHEST set ballot bit: one
             // FLO instead of BREV + FLO on the row-to-row chain), rl = lane in the alternating
@@ -454,7 +525,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
             float carry[kRgsWin];
 #pragma unroll
             for (int d = 0; d < kRgsWin; d++) carry[d] = 0.f;
-            unsigned long long tt = 0, tsd = 0, tl = 0, tr = 0, nch = 0, nmiss = 0;
+            unsigned long long tt = 0, tsd = 0, tl = 0, tr = 0, nch = 0, nmiss = 0, e_sd = 0, e_l = 0, e_ch = 0, nzero = 0;
             for (int s = 0, p = 0, pos = 0; s < total; s++, pos = (pos + 1 == T) ? 0 : pos + 1, p += (pos == 0)) {
                 const unsigned long long t0 = pf ? clk() : 0ull;
                 const bool fwd = sweep_fwd(p, alt);
@@ -564,26 +635,42 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                     lst[e].xn = xo;
                     lst[e].xo = x0;
                     lst[e].c = row;
+                    if (CLU)   // the other CTAs' copies, completing on their dready[li]
+                        for (int c = 1; c < G; c++)
+                            st_async_v4b32(cl_map(&lst[e], c), __float_as_uint(xo), __float_as_uint(x0), (uint32_t)row, 0u,
+                                           cl_map(&sh.dready[li], c));
                 }
                 if (lane == 0) {
                     sh.cnt[li] = q;
                     pmask[k] = chg;   // the prediction for the next visit
+                    if (CLU)
+                        for (int c = 1; c < G; c++) st_async_b32(cl_map(&sh.cnt[li], c), (uint32_t)q, cl_map(&sh.dready[li], c));
                 }
                 my_updates += (unsigned long long)q;
                 my_bytes += (unsigned long long)q * sp * 4;
                 __syncwarp();
                 if (lane == 0) {
                     mbar_arrive(&sh.dready[li]);
+                    if (CLU)   // the other CTAs' dready: one arrival plus the bytes of the list and count
+                        for (int c = 1; c < G; c++) mbar_arrive_tx_cl(cl_map(&sh.dready[li], c), 16u * (uint32_t)q + 4u);
                     mbar_arrive(&sh.stg_empty[sl]);
                 }
 #pragma unroll
                 for (int d = 0; d + 1 < kRgsWin; d++) carry[d] = carry[d + 1] + acc[d];
                 carry[kRgsWin - 1] = acc[kRgsWin - 1];
-                if (pf) { tt += t1 - t0; tsd += t2 - t1; tl += t3 - t2; tr += clk() - t3; }
+                if (pf) {
+                    tt += t1 - t0; tsd += t2 - t1; tl += t3 - t2; tr += clk() - t3;
+                    if (10 * s < total) { e_sd += t2 - t1; e_l += t3 - t2; e_ch += q; }   // the first 10 % of the steps
+                    nzero += (q == 0);
+                }
                 nch += q;
             }
+            if (CLU)   // the last steps' published-r bytes (st.async) have landed before the barriers are re-initialised
+                for (int s = max(0, total - kNList); s < total; s++) mbar_wait(&sh.sdone[s % kNList], (s / kNList) & 1);
             if (prof && lane == 0 && item < kProfItems) prof[kProfSlots + 4 * item + 3] = nch;
-            if (pf && lane == 0) { prof[0] = tt; prof[1] = tsd; prof[2] = tl; prof[3] = tr; prof[4] = total; prof[5] = nch; prof[6] = nmiss; }
+            if (pf && lane == 0) { prof[0] = tt; prof[1] = tsd; prof[2] = tl; prof[3] = tr; prof[4] = total; prof[5] = nch; prof[6] = nmiss;
+                                    prof[16] = e_sd; prof[17] = e_l; prof[18] = e_ch; prof[19] = nzero; }
+          }
         } else if (REGR) {
             // ================= stream warps, r in registers (sp <= kRegMaxSp, whole rows in the
             // ring): r += dx_c A[c, :] for every change of every step.  Warp w owns the 128-column
@@ -592,15 +679,16 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
             // solver step s' whose stored residual is "r after stream step j" (s' = j + nsub + 1,
             // or for alternating sweeps the revisit s' whose last visit was step j), in the
             // step-indexed slot s' mod 16 (the pend buffer)
+            // (CLU: the chunks of this CTA's slice, local index ql = q - q_lo)
             const int w = (wid < 4) ? wid : wid - 3;
-            const int nq = (sp + 127) >> 7;
-            const int nch = (nq - w + kNStream - 1) / kNStream;   // chunks this warp owns (<= kRegCh)
-            DWC_DCHECK(nch >= 0 && nch <= kRegCh && rg.nseg == 1, "stream: register chunks");
+            const int nch = max(0, (q_hi - q_lo - w + kNStream - 1) / kNStream);   // chunks this warp owns
+            DWC_DCHECK(nch <= kRegCh && rg.nseg == 1, "stream: register chunks");
             unsigned long long tlw = 0, tbw = 0, tap = 0, nb_all = 0;
+            uint32_t pub_bytes = 0;   // (CLU) bytes this warp published during the current step
             double r[kRegCh][4];
 #pragma unroll
             for (int c = 0; c < kRegCh; c++) {
-                const int col = 128 * (w + kNStream * c) + 4 * lane;
+                const int col = col0 + 128 * (w + kNStream * c) + 4 * lane;
 #pragma unroll
                 for (int e = 0; e < 4; e++) r[c][e] = (col + e < sp) ? -bt[L.v_off + col + e] : 0.0;
             }
@@ -615,17 +703,26 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 const bool rev = vp > s0 + d - nsub - 1;
                 if (before ? !(rev && vp == s0) : rev) return;
                 const int bb = sweep_fwd(p2, alt) ? q2 : T - 1 - q2;   // its block
-                DWC_DCHECK(bb >= 0 && bb < T && (bb >> 2) / kNStream < kRegCh, "stream: published block");
-                const int qb = bb >> 2;
-                if ((qb % kNStream) == w && (lane >> 3) == (bb & 3)) {
-                    const int cb = qb / kNStream;
-                    // rounded to fp32 here (the solver's recurrence is fp32), off the solver's path
-                    float *dst = reinterpret_cast<float *>(pend) + 32 * ((s0 + d) & (kPendBlk - 1)) + 4 * (lane & 7);
+                const int qb = bb >> 2, oc = CLU ? qb / nqc : 0, ql = qb - oc * nqc;   // owner CTA, local chunk
+                DWC_DCHECK(bb >= 0 && bb < T && ql / kNStream < kRegCh && oc < G, "stream: published block");
+                if (oc == (int)crank && (ql % kNStream) == w) {
+                    if ((lane >> 3) == (bb & 3)) {
+                        const int cb = ql / kNStream;
+                        // rounded to fp32 here (the solver's recurrence is fp32), off the solver's path
+                        float *dst = reinterpret_cast<float *>(pend) + 32 * ((s0 + d) & (kPendBlk - 1)) + 4 * (lane & 7);
 #pragma unroll
-                    for (int c = 0; c < kRegCh; c++)
-                        if (c == cb)
-                            *reinterpret_cast<float4 *>(dst) =
-                                make_float4((float)r[c][0], (float)r[c][1], (float)r[c][2], (float)r[c][3]);
+                        for (int c = 0; c < kRegCh; c++)
+                            if (c == cb) {
+                                const float4 v = make_float4((float)r[c][0], (float)r[c][1], (float)r[c][2], (float)r[c][3]);
+                                if (CLU)   // into the leader's slot, completing on its sdone of this stream step
+                                    st_async_v4b32(cl_map(dst, 0), __float_as_uint(v.x), __float_as_uint(v.y),
+                                                   __float_as_uint(v.z), __float_as_uint(v.w),
+                                                   cl_map(&sh.sdone[s0 % kNList], 0));
+                                else
+                                    *reinterpret_cast<float4 *>(dst) = v;
+                            }
+                    }
+                    pub_bytes += 128;   // (8 lanes x 16 B)
                 }
             };
             int b = 0;
@@ -639,7 +736,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 // carries this step's changes itself, so its stored r is the one before them
                 if (ALT)
                     for (int d = 1; d <= nsub; d++) publish(s, p, pos, d, true);
-                for (int u0 = 0; u0 < n; u0 += rg.upb, b++) {
+                for (int u0 = 0; u0 < (swid > 0 ? n : 0); u0 += rg.upb, b++) {
                     const int h = b % kNSlot;
                     const unsigned long long t1 = pf ? clk() : 0ull;
                     mbar_wait(&sh.rfull[h], (b / kNSlot) & 1);
@@ -648,14 +745,14 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                     const float *src = ring + (size_t)h * slot_floats + 4 * lane;
                     const double *dxb = &sh.dxs[li][u0];
                     switch (nonneg ? nch : nch + 8) {   // (0: a small system leaves this warp no chunk)
-                        case 1: apply_rows<1, true>(r, src, sp, nb, dxb, w); break;
-                        case 2: apply_rows<2, true>(r, src, sp, nb, dxb, w); break;
-                        case 3: apply_rows<3, true>(r, src, sp, nb, dxb, w); break;
-                        case 4: apply_rows<4, true>(r, src, sp, nb, dxb, w); break;
-                        case 9: apply_rows<1, false>(r, src, sp, nb, dxb, w); break;
-                        case 10: apply_rows<2, false>(r, src, sp, nb, dxb, w); break;
-                        case 11: apply_rows<3, false>(r, src, sp, nb, dxb, w); break;
-                        case 12: apply_rows<4, false>(r, src, sp, nb, dxb, w); break;
+                        case 1: apply_rows<1, true>(r, src, rstride, nb, dxb, w); break;
+                        case 2: apply_rows<2, true>(r, src, rstride, nb, dxb, w); break;
+                        case 3: apply_rows<3, true>(r, src, rstride, nb, dxb, w); break;
+                        case 4: apply_rows<4, true>(r, src, rstride, nb, dxb, w); break;
+                        case 9: apply_rows<1, false>(r, src, rstride, nb, dxb, w); break;
+                        case 10: apply_rows<2, false>(r, src, rstride, nb, dxb, w); break;
+                        case 11: apply_rows<3, false>(r, src, rstride, nb, dxb, w); break;
+                        case 12: apply_rows<4, false>(r, src, rstride, nb, dxb, w); break;
                         default: break;
                     }
                     __syncwarp();
@@ -666,7 +763,13 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 // alternating-sweep revisit whose last visit is inside its window (published then)
                 publish(s, p, pos, nsub + 1, false);
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&sh.sdone[li]);
+                if (lane == 0) {
+                    if (CLU)   // the leader's sdone: one arrival plus the bytes this warp published
+                        mbar_arrive_tx_cl(cl_map(&sh.sdone[li], 0), pub_bytes);
+                    else
+                        mbar_arrive(&sh.sdone[li]);
+                }
+                pub_bytes = 0;
             }
             if (pf && w == 0 && lane == 0) { prof[8] = tlw; prof[9] = tbw; prof[10] = tap; prof[11] = nb_all; }
         } else {
@@ -789,19 +892,23 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
         }
         __syncthreads();
         if (pf && tid == 0) prof[14] = clk() - t_item;
-        if (prof && tid == 0 && item < kProfItems) {
+        if (prof && leader && tid == 0 && item < kProfItems) {
             unsigned long long t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
             prof[kProfSlots + 4 * item + 1] = t;
             prof[kProfSlots + 4 * item + 2] = (unsigned long long)bin;
         }
         // ---- output: x~ and the embedded full-grid map (S8)
-        for (int i = tid; i < nk; i += kRThreads) {
-            const float v = xs[i];
-            if (x_out) x_out[L.v_off + i] = v;
-            if (x_map) x_map[(size_t)bin * S + keep_idx[(size_t)bin * S + i]] = v;
-        }
-        __syncthreads();
+        if (leader)
+            for (int i = tid; i < nk; i += kRThreads) {
+                const float v = xs[i];
+                if (x_out) x_out[L.v_off + i] = v;
+                if (x_map) x_map[(size_t)bin * S + keep_idx[(size_t)bin * S + i]] = v;
+            }
+        if (CLU)
+            cl_sync();   // no CTA re-initialises its barriers while another still signals them
+        else
+            __syncthreads();
     }
     if (n_updates && wid == kWSolver && lane == 0 && my_updates) {
         atomicAdd(n_updates, my_updates);        // row updates
@@ -810,7 +917,10 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
 }
 
 namespace {
-size_t rgs_base_bytes(int max_sp) { return sizeof(RgsSmem) + kPendF * 8 + (size_t)max_sp * (8 + 4) + (((size_t)max_sp / 32 + 31) & ~(size_t)31) * 4; }
+// RgsSmem, r (fp64; none when r lives in registers), the pending / published slots, x, the masks
+size_t rgs_base_bytes(int max_sp, bool regr = false) {
+    return sizeof(RgsSmem) + kPendF * 8 + (size_t)max_sp * ((regr ? 0 : 8) + 4) + (((size_t)max_sp / 32 + 31) & ~(size_t)31) * 4;
+}
 }  // namespace
 
 // The minimum ring (two halves of 128 floats); launch_rgs gives it what shared memory allows.
@@ -822,59 +932,99 @@ int rgs_auto_max_sp() {
     return v;
 }
 
-size_t rgs_smem_bytes(int max_sp) { return rgs_base_bytes(max_sp) + kNSlot * 128 * 4 + 512; }
+size_t rgs_smem_bytes(int max_sp) { return rgs_base_bytes(max_sp, max_sp <= 8 * kRegMaxSp) + kNSlot * 128 * 4 + 512; }
 
 
 int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int max_sp, int *counter,
                const float *Adense, const double *bt, int sweeps, float *x_out, float *x_map,
                const int32_t *keep_idx, int S, int num_sms, unsigned long long *n_updates, cudaStream_t st,
                GsLaunchInfo *info, int alt, int nonneg) {
-    // 1/A_ii in shared memory for the whole system when a ring of >= 24 KB still fits beside it
-    const int use_ivs = (rgs_base_bytes(max_sp) + (size_t)max_sp * 4 + 24 * 1024 + 1536 <= 227 * 1024) ? 1 : 0;
-    const size_t base = (rgs_base_bytes(max_sp) + (use_ivs ? (size_t)max_sp * 4 : 0) + 127) / 128 * 128;
-    if (base + 1536 > 227 * 1024) return -1;
-    // two CTAs per SM (2 x (smem + 1 KB reserved) <= 228 KB) when the band has the bins for it
-    // and the ring still holds a row; else one CTA per SM with the rest of the 227 KB as ring
     static const int ring_env = getenv("DWC_RGS_RING_KB") ? atoi(getenv("DWC_RGS_RING_KB")) : 0;   // experiment
     static const int per_sm_env = getenv("DWC_RGS_PER_SM") ? atoi(getenv("DWC_RGS_PER_SM")) : 0;   // experiment
-    const size_t per2 = 114 * 1024 - 1024;
-    size_t ring;
+    static const bool no_regr = getenv("DWC_RGS_NO_REGR") != nullptr;   // experiment: r in shared memory
+    static const bool no_cluster = getenv("DWC_RGS_NO_CLUSTER") != nullptr;   // experiment
     // r in registers (one CTA per SM: up to 255 registers) when the system fits the stream warps'
-    // chunks (and, below, a ring slot holds a whole row): measured faster than two CTAs per SM
-    static const bool no_regr = getenv("DWC_RGS_NO_REGR") != nullptr;   // experiment
-    const bool regr_fits = max_sp <= kRegMaxSp && kNStream == 5 && !no_regr;
-    // else two per SM when the band has more bins than SMs and every ring slot still holds 2 rows
-    const bool two = (kRMinBlocks < 2 || regr_fits) ? false
+    // chunks; above that, split over a cluster of G CTAs (<= 8, portable) -- both need a ring slot
+    // that holds a whole row (slice); else r in shared memory
+    const int nq_max = (max_sp + 127) / 128;
+    int G = 1;
+    if (!no_regr && max_sp > kRegMaxSp && !no_cluster) {
+        G = (max_sp + kRegMaxSp - 1) / kRegMaxSp;
+        if (G > 8) G = 1;
+    }
+    const bool regr_try = !no_regr && (max_sp <= kRegMaxSp || G > 1);
+    const int rstride_max = G > 1 ? 128 * ((nq_max + G - 1) / G) : max_sp;   // floats of a ring row
+    // the configuration: base shared memory, 1/A_ii copy (when a ring of >= 24 KB still fits), ring
+    auto layout = [&](bool regr, int &use_ivs, size_t &base) {
+        use_ivs = (rgs_base_bytes(max_sp, regr) + (size_t)max_sp * 4 + 24 * 1024 + 1536 <= 227 * 1024) ? 1 : 0;
+        base = (rgs_base_bytes(max_sp, regr) + (use_ivs ? (size_t)max_sp * 4 : 0) + 127) / 128 * 128;
+    };
+    int use_ivs;
+    size_t base;
+    bool regr = regr_try;
+    layout(regr, use_ivs, base);
+    auto slot_of = [&](size_t ring) { return (int)(ring / (4 * kNSlot)) / 128 * 128; };
+    size_t ring = base + 1536 <= 227 * 1024 ? (227 * 1024 - base - 512) / 1024 * 1024 : 0;
+    if (ring_env > 0 && (size_t)ring_env * 1024 < ring) ring = (size_t)ring_env * 1024;
+    if (regr && slot_of(ring) < rstride_max) {   // no whole row per slot: r in shared memory
+        regr = false;
+        G = 1;
+        layout(regr, use_ivs, base);
+    }
+    if (base + 1536 > 227 * 1024) return -1;
+    // shared-memory r: two CTAs per SM (2 x (smem + 1 KB reserved) <= 228 KB) when the band has
+    // more bins than SMs and every ring slot still holds 2 rows
+    const size_t per2 = 114 * 1024 - 1024;
+    const bool two = (regr || kRMinBlocks < 2) ? false
                      : per_sm_env ? per_sm_env == 2 && per2 > base + 2048
                                 : n_bins > num_sms && per2 > base && (per2 - base) / (4 * kNSlot) >= 2 * (size_t)max_sp;
-    if (two)
-        ring = (per2 - base - 512) / 1024 * 1024;
-    else
-        ring = (227 * 1024 - base - 512) / 1024 * 1024;
+    ring = two ? (per2 - base - 512) / 1024 * 1024 : (227 * 1024 - base - 512) / 1024 * 1024;
     if (ring_env > 0 && (size_t)ring_env * 1024 < ring) ring = (size_t)ring_env * 1024;
-    const int slot_floats = (int)(ring / (4 * kNSlot)) / 128 * 128;   // floats per ring slot
+    const int slot_floats = slot_of(ring);   // floats per ring slot
     if (slot_floats < 128) return -1;
     const size_t smem = base + (size_t)slot_floats * 4 * kNSlot + 512;   // + slack: a row's last chunk reads past it
-    const bool regr = regr_fits && slot_floats >= max_sp;
-    const auto kern = alt ? (regr ? rgs_kernel<true, true> : rgs_kernel<true, false>)
-                          : (regr ? rgs_kernel<false, true> : rgs_kernel<false, false>);
+    const bool clu = G > 1;
+    const auto kern = alt ? (clu ? rgs_kernel<true, true, true> : regr ? rgs_kernel<true, true, false> : rgs_kernel<true, false, false>)
+                          : (clu ? rgs_kernel<false, true, true> : regr ? rgs_kernel<false, true, false> : rgs_kernel<false, false, false>);
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return -1;
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRThreads, smem) != cudaSuccess ||
-        per_sm < 1) {
-        cudaGetLastError();
-        per_sm = 1;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    cfg.blockDim = dim3(kRThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    int grid;
+    if (clu) {
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = G;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cfg.gridDim = dim3(G * std::min(n_bins, std::max(1, num_sms / G)));
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) != cudaSuccess || ncl < 1) {
+            cudaGetLastError();
+            ncl = std::max(1, num_sms / G);
+        }
+        grid = G * std::min(n_bins, ncl);
+    } else {
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRThreads, smem) != cudaSuccess || per_sm < 1) {
+            cudaGetLastError();
+            per_sm = 1;
+        }
+        grid = std::min(n_bins, num_sms * per_sm);
+        static const int cta_env = getenv("DWC_RGS_CTAS") ? atoi(getenv("DWC_RGS_CTAS")) : 0;   // experiment
+        if (cta_env > 0 && cta_env < grid) grid = cta_env;
+        if (grid < 1) grid = 1;
     }
-    int grid = std::min(n_bins, num_sms * per_sm);
-    static const int cta_env = getenv("DWC_RGS_CTAS") ? atoi(getenv("DWC_RGS_CTAS")) : 0;   // experiment
-    if (cta_env > 0 && cta_env < grid) grid = cta_env;
-    if (grid < 1) grid = 1;
+    cfg.gridDim = dim3(grid);
     if (info) {
         info->kernel = DWC_GS_KERNEL_RESIDUAL;
         info->xtra_tiles = 0;
         info->ctas = grid;
-        info->max_group = 1;
+        info->max_group = G;
     }
     // DWC_RGS_PROF=1: clock64 breakdown of the largest bin (stderr)
     static const bool profile = getenv("DWC_RGS_PROF") != nullptr;
@@ -884,9 +1034,8 @@ int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int m
         if (cudaMalloc(&prof, pb) != cudaSuccess) return -1;
         cudaMemsetAsync(prof, 0, pb, st);
     }
-    kern<<<grid, kRThreads, smem, st>>>(n_bins, order_dev, lay_dev, counter, Adense, bt, sweeps, x_out, x_map,
-                                        keep_idx, S, max_sp, slot_floats, use_ivs, nonneg, n_updates, prof);
-    const cudaError_t e = cudaPeekAtLastError();
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, n_bins, order_dev, lay_dev, counter, Adense, bt, sweeps, x_out,
+                                             x_map, keep_idx, S, max_sp, slot_floats, use_ivs, nonneg, n_updates, prof);
     if (profile) {
         static unsigned long long h[kProfSlots + 4 * kProfItems + 2];
         cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, st);
@@ -912,6 +1061,9 @@ int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int m
                 " (%llu batches) | rowprod: ring wait %.0f issue %.0f | panel misses %llu | panelprod wait %.0f issue %.0f\n",
                 grid, smem, kNSlot, slot_floats, h[4], h[5], h[5] / n, (double)h[14], h[0] / n, h[1] / n, h[2] / n, h[3] / n,
                 h[8] / n, h[9] / n, h[10] / n, h[11], h[12] / n, h[13] / n, h[6], h[7] / n, h[15] / n);
+        fprintf(stderr, "[rgs-prof] first 10%% of the steps: stream wait %.0f, loop %.0f cyc/step, %.2f changes/step; "
+                        "steps without a change: %.1f %%\n",
+                h[16] / (0.1 * n), h[17] / (0.1 * n), h[18] / (0.1 * n), 100.0 * h[19] / n);
         cudaFree(prof);
     }
     return e == cudaSuccess ? 1 : -1;
