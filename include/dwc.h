@@ -106,15 +106,17 @@ typedef struct {
  * the choice below picks: the residual kernel walks the alternating visit sequence; in place of
  * the dense-stream kernel a simpler one-CTA-per-bin kernel runs (DWC_GS_KERNEL_ALT). */
 #define DWC_ALT_SWEEPS 8
-/* Gauss-Seidel kernel of the forward sweeps (both keep Eq. 13-14's row and sweep order exactly and
- * differ in summation order only):
+/* Gauss-Seidel kernel of the sweeps (both keep Eq. 13-14's row and sweep order exactly and differ
+ * in summation order only):
  *  - residual-update kernel: the residual r = A x - b of the current iterate kept on chip in fp64,
- *    updated with the row of A~ of every x that changes (one CTA per bin);
+ *    updated with the row of A~ of every x that changes (one CTA per bin; systems above 2560
+ *    points split r over a cluster of up to 8 CTAs);
  *  - dense-stream cluster kernel: every row dot recomputed from the symmetric-packed A~ streamed
  *    through shared memory (up to 4 CTAs per bin).
- * Default: the residual kernel when the band's largest compressed system has at most 2048 points
- * (padded to 32), else the dense-stream kernel.  DWC_GS_DENSE_STREAM / DWC_GS_RESIDUAL force one
- * (setting both is DWC_EINVAL).  dwc_stats.gs_kernel reports which ran. */
+ * Default: the residual kernel when the band's largest system has at most 20480 points (padded
+ * to 32), else the dense-stream kernel.  DWC_GS_DENSE_STREAM / DWC_GS_RESIDUAL force one
+ * (setting both is DWC_EINVAL).  dwc_stats.gs_kernel reports which ran, gs_max_group the
+ * largest CTAs per bin. */
 #define DWC_GS_DENSE_STREAM 16
 #define DWC_GS_RESIDUAL 32
 /* DWC_PAPER_PSF: the paper-literal beamformer and PSF (NEXT-4, fidelity study of reading R1): the

@@ -63,6 +63,11 @@ struct dwc_ctx {
     cudaEvent_t stage_done = nullptr;
     cudaStream_t copy_st = nullptr;         // host API: early keep-set readback (overlaps S5-S7)
     cudaEvent_t keep_ready = nullptr, copy_done = nullptr;
+    // residual GS on a band whose systems need different cluster sizes: one launch per size class,
+    // the classes on their own streams (forked from and joined back into the call's stream)
+    static constexpr int kMaxClasses = 4;
+    cudaStream_t class_st[kMaxClasses] = {};
+    cudaEvent_t class_fork = nullptr, class_join[kMaxClasses] = {};
     int geo_m = -1, geo_n = -1;
     bool timing = false;
     cudaEvent_t ev[8] = {};
@@ -450,10 +455,45 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
     GsLaunchInfo gsi;
     if (resid) {
         CU(cudaMemsetAsync(ctx->upd.p, 0, 64, st));
-        LAUNCH(launch_rgs(n_bins, (int *)ctx->order.p, (BinLayout *)ctx->lay.p, max_sp, (int *)ctx->counter.p,
-                          (float *)ctx->Ad.p, (double *)ctx->bt.p, p->sweeps, nullptr, x_map, keep_idx,
-                          S, ctx->num_sms, (unsigned long long *)ctx->upd.p, st, &gsi, alt,
-                          /*nonneg: every PSF is |.|^2 times positive scales*/ 1));
+        // size classes of the bins (order = descending S~): the cluster size each system needs
+        // (rgs_cluster_size); one launch per class, the classes concurrently on their own streams
+        std::vector<std::pair<int, int>> cls;   // [begin, end) in `order`
+        for (int i = 0; i < n_bins; i++) {
+            const int g = rgs_cluster_size((hk[order[i]] + 31) & ~31);
+            if (cls.empty() || rgs_cluster_size((hk[order[cls.back().first]] + 31) & ~31) != g)
+                cls.push_back({i, i + 1});
+            else
+                cls.back().second = i + 1;
+        }
+        if ((int)cls.size() > dwc_ctx::kMaxClasses) {   // merge the smallest classes into the last one kept
+            cls[dwc_ctx::kMaxClasses - 1].second = n_bins;
+            cls.resize(dwc_ctx::kMaxClasses);
+        }
+        const int ncls = (int)cls.size();
+        if (ncls > 1) {
+            if (!ctx->class_fork) CU(cudaEventCreateWithFlags(&ctx->class_fork, cudaEventDisableTiming));
+            for (int c = 1; c < ncls; c++) {
+                if (!ctx->class_st[c]) CU(cudaStreamCreateWithFlags(&ctx->class_st[c], cudaStreamNonBlocking));
+                if (!ctx->class_join[c]) CU(cudaEventCreateWithFlags(&ctx->class_join[c], cudaEventDisableTiming));
+            }
+            CU(cudaEventRecord(ctx->class_fork, st));
+        }
+        gsi = GsLaunchInfo{DWC_GS_KERNEL_RESIDUAL, 0, 0, 1};
+        for (int c = 0; c < ncls; c++) {
+            cudaStream_t cs = c == 0 ? st : ctx->class_st[c];
+            if (c > 0) CU(cudaStreamWaitEvent(cs, ctx->class_fork, 0));
+            const int b0 = cls[c].first, nb = cls[c].second - cls[c].first;
+            const int csp = (hk[order[b0]] + 31) & ~31;   // the class's largest system
+            GsLaunchInfo ci;
+            LAUNCH(launch_rgs(nb, (int *)ctx->order.p + b0, (BinLayout *)ctx->lay.p, csp, (int *)ctx->counter.p + c,
+                              (float *)ctx->Ad.p, (double *)ctx->bt.p, p->sweeps, nullptr, x_map, keep_idx,
+                              S, ctx->num_sms, (unsigned long long *)ctx->upd.p, cs, &ci, alt,
+                              /*nonneg: every PSF is |.|^2 times positive scales*/ 1));
+            gsi.ctas += ci.ctas;
+            gsi.max_group = std::max(gsi.max_group, ci.max_group);
+            if (c > 0) CU(cudaEventRecord(ctx->class_join[c], cs));
+        }
+        for (int c = 1; c < ncls; c++) CU(cudaStreamWaitEvent(st, ctx->class_join[c], 0));
     } else if (p->flags & DWC_ALT_SWEEPS) {
         gsi.kernel = DWC_GS_KERNEL_ALT;
         gsi.ctas = n_bins;
@@ -555,6 +595,11 @@ dwc_status dwc_destroy(dwc_ctx *ctx) {
     if (ctx->copy_st) cudaStreamDestroy(ctx->copy_st);
     if (ctx->keep_ready) cudaEventDestroy(ctx->keep_ready);
     if (ctx->copy_done) cudaEventDestroy(ctx->copy_done);
+    for (int c = 0; c < dwc_ctx::kMaxClasses; c++) {
+        if (ctx->class_st[c]) cudaStreamDestroy(ctx->class_st[c]);
+        if (ctx->class_join[c]) cudaEventDestroy(ctx->class_join[c]);
+    }
+    if (ctx->class_fork) cudaEventDestroy(ctx->class_fork);
     if (ctx->last_done) cudaEventDestroy(ctx->last_done);
     for (auto &e : ctx->ev)
         if (e) cudaEventDestroy(e);

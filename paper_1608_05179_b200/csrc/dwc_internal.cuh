@@ -282,6 +282,8 @@ int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_s
 size_t rgs_smem_bytes(int max_sp);
 // largest padded system the automatic kernel choice gives the residual kernel (DWC_RGS_AUTO_MAX_SP overrides)
 int rgs_auto_max_sp();
+// CTAs per bin of the residual kernel for a system of sp padded points (1: r in one CTA's registers).
+int rgs_cluster_size(int sp);
 int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int max_sp, int *counter,
                const float *Adense, const double *bt, int sweeps, float *x_out, float *x_map,
                const int32_t *keep_idx, int S, int num_sms, unsigned long long *n_updates, cudaStream_t st,

@@ -614,7 +614,9 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                     pos_r = fwd ? t + 1 : t - 1;
                     q++;
                 }
-                // the carries of the changed rows that were not staged (rare: the prediction missed)
+                // the carries of the changed rows that were not staged (the prediction missed: 1 % of
+                // the changes on cfg3, 30 % on the noisy cfg5), from global memory, four rows' loads
+                // in flight at a time
                 for (unsigned mm = chg & ~smk; mm; mm &= mm - 1) {
                     const int t = __ffs(mm) - 1;
                     const float dv = __shfl_sync(0xffffffffu, xo - x0, ALT ? t : t ^ 31);
@@ -923,17 +925,25 @@ size_t rgs_base_bytes(int max_sp, bool regr = false) {
 }
 }  // namespace
 
-// The minimum ring (two halves of 128 floats); launch_rgs gives it what shared memory allows.
-// Measured (cfg3 S~ <= 1184: residual band GS 30 ms vs 45 dense-stream; cfg2 full grid S = 6561:
-// 805 vs 590 ms; cfg4/cfg5 (S~ up to 10201): 1.6-2.8x slower on the residual kernel): one SM per
-// residual bin streams its changed rows, the dense-stream kernel spreads a large bin over 4 SMs.
+// The automatic kernel choice: the residual kernel up to 8 x kRegMaxSp points (r in registers, one
+// CTA -- or a cluster of up to 8 -- per bin), else the dense-stream kernel.  Measured (one B200):
+// cfg3 GS 24.5 ms vs 45.2 dense-stream; cfg4 full grid (S = 10201, clusters of 4) 496 vs 2107 ms;
+// cfg5 (S~ up to 9k, per-size-class launches) 1156 vs 1697 ms.
 int rgs_auto_max_sp() {
-    static const int v = getenv("DWC_RGS_AUTO_MAX_SP") ? atoi(getenv("DWC_RGS_AUTO_MAX_SP")) : 2048;
+    static const int v = getenv("DWC_RGS_AUTO_MAX_SP") ? atoi(getenv("DWC_RGS_AUTO_MAX_SP")) : 8 * kRegMaxSp;
     return v;
 }
 
 size_t rgs_smem_bytes(int max_sp) { return rgs_base_bytes(max_sp, max_sp <= 8 * kRegMaxSp) + kNSlot * 128 * 4 + 512; }
 
+
+int rgs_cluster_size(int sp) {
+    static const bool no_regr = getenv("DWC_RGS_NO_REGR") != nullptr;       // experiment: r in shared memory
+    static const bool no_cluster = getenv("DWC_RGS_NO_CLUSTER") != nullptr; // experiment
+    if (no_regr || no_cluster || sp <= kRegMaxSp) return 1;
+    const int g = (sp + kRegMaxSp - 1) / kRegMaxSp;
+    return g <= 8 ? g : 1;   // (portable cluster sizes; beyond: one CTA with r in shared memory)
+}
 
 int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int max_sp, int *counter,
                const float *Adense, const double *bt, int sweeps, float *x_out, float *x_map,
@@ -942,16 +952,11 @@ int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int m
     static const int ring_env = getenv("DWC_RGS_RING_KB") ? atoi(getenv("DWC_RGS_RING_KB")) : 0;   // experiment
     static const int per_sm_env = getenv("DWC_RGS_PER_SM") ? atoi(getenv("DWC_RGS_PER_SM")) : 0;   // experiment
     static const bool no_regr = getenv("DWC_RGS_NO_REGR") != nullptr;   // experiment: r in shared memory
-    static const bool no_cluster = getenv("DWC_RGS_NO_CLUSTER") != nullptr;   // experiment
     // r in registers (one CTA per SM: up to 255 registers) when the system fits the stream warps'
     // chunks; above that, split over a cluster of G CTAs (<= 8, portable) -- both need a ring slot
     // that holds a whole row (slice); else r in shared memory
     const int nq_max = (max_sp + 127) / 128;
-    int G = 1;
-    if (!no_regr && max_sp > kRegMaxSp && !no_cluster) {
-        G = (max_sp + kRegMaxSp - 1) / kRegMaxSp;
-        if (G > 8) G = 1;
-    }
+    int G = rgs_cluster_size(max_sp);
     const bool regr_try = !no_regr && (max_sp <= kRegMaxSp || G > 1);
     const int rstride_max = G > 1 ? 128 * ((nq_max + G - 1) / G) : max_sp;   // floats of a ring row
     // the configuration: base shared memory, 1/A_ii copy (when a ring of >= 24 KB still fits), ring

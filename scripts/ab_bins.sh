@@ -1,0 +1,8 @@
+#!/bin/bash
+# A/B of residual-GS library variants on single bins (GS ms alone): cfg3 bin 249, cfg5 bins 600 and 1023
+cd $GRAFT_REPO_ROOT
+for lib in "" $@; do
+  if [ -z "$lib" ]; then L=paper_1608_05179_b200/libdwc.so; else L=paper_1608_05179_b200/libdwc_$lib.so; fi
+  echo "== lib ${lib:-default}"
+  DWC_LIB=$L timeout 300 python scripts/dbg_cfg5.py cfg3:249 cfg5:600 cfg5:1023 2>&1 | grep -v "^\[rgs"
+done

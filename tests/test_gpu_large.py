@@ -3,9 +3,11 @@ configs reach (cfg4's full grid, cfg5's S~ up to ~9k), compared with the fp64 or
 by element (north_star tolerances: keep set bit-exact, map within 1e-3 relative L2, integrated
 power within 1e-3).
 
-On the dense-stream cluster kernel these sizes run the instantiation with extra ring tiles
-behind the dynamic tables (dwc_stats.gs_kernel == DWC_GS_KERNEL_CLUSTER_XTRA); the tests
-assert which kernel ran, so a change of the selection cannot silently drop the coverage."""
+On the residual kernel these sizes run its cluster mode (r split over 2-4 CTAs per bin,
+dwc_stats.gs_max_group); on the dense-stream cluster kernel the instantiation with extra ring
+tiles behind the dynamic tables (dwc_stats.gs_kernel == DWC_GS_KERNEL_CLUSTER_XTRA).  The tests
+assert which kernel and cluster size ran, so a change of the selection cannot silently drop the
+coverage."""
 import dataclasses
 import os
 import subprocess
@@ -88,8 +90,8 @@ def test_gs_large_systems(ctx, torch_cuda, oracle_lib, nk, sweeps, dense):
     st = ctx.stats()
     if dense:
         assert st["gs_kernel"] == 2 and st["gs_xtra_tiles"] > 0 and st["gs_max_group"] == 4
-    else:
-        assert st["gs_kernel"] == 4 and st["gs_updates"] > 0
+    else:   # CTAs per bin: r of at most 2560 points per CTA
+        assert st["gs_kernel"] == 4 and st["gs_updates"] > 0 and st["gs_max_group"] == -(-((nk + 31) // 32 * 32) // 2560)
     assert x.min() >= 0
     assert rel_l2(x, ref) < TOL_X, rel_l2(x, ref)
     assert abs(x.sum() - ref.sum()) < TOL_P * ref.sum()
@@ -172,6 +174,7 @@ def test_e2e_cfg5_largest_bins(ctx, torch_cuda, oracle_lib, dense):
     st, nk = _e2e(ctx, torch_cuda, oracle_lib, band, 20, dense=dense)
     assert nk.min() > 6000
     assert st["gs_kernel"] == (2 if dense else 4)
+    assert dense or st["gs_max_group"] >= 3   # (the residual kernel's cluster mode)
 
 
 @pytest.mark.parametrize("dense", [False, True], ids=["residual", "dense_stream"])
@@ -191,22 +194,30 @@ def test_e2e_cfg4_full_grid_defining_size(ctx, torch_cuda, oracle_lib, dense):
     st, nk = _e2e(ctx, torch_cuda, oracle_lib, band, 10, full=True, dense=dense)
     assert nk[0] == 10201
     assert st["gs_kernel"] == (2 if dense else 4)
+    assert dense or st["gs_max_group"] == 4
 
 
-def test_automatic_kernel_choice(ctx, torch_cuda):
-    """Without a kernel flag the band's largest compressed system picks the GS kernel: cfg3's
-    compressed bins (S~ <= 1184) run the residual kernel, a full-grid band of S = 2209 (padded
-    2240 > 2048) the dense-stream cluster kernel; both flags at once are rejected."""
+def test_automatic_kernel_choice(ctx, torch_cuda, tmp_path):
+    """Without a kernel flag the band's largest system picks the GS kernel: the residual kernel up
+    to 20480 padded points -- cfg3's compressed bins on one CTA each, a full-grid band of S = 4096
+    on clusters of 2 -- and above that the dense-stream cluster kernel (checked in a subprocess
+    with the threshold lowered to 2048 by DWC_RGS_AUTO_MAX_SP: a full-grid band of S = 2209);
+    both flags at once are rejected."""
     torch = torch_cuda
-    from paper_1608_05179_b200 import DwcError
+    from paper_1608_05179_b200 import DwcError  # noqa: F401
     band = synth.make_band("cfg3", bins=[0, 255])
     cfg = band.cfg
     ctx.solve_band(geom_of(band), band.freqs, torch.from_numpy(band.csm).cuda(), cfg.epsilon, 5)
-    assert ctx.stats()["gs_kernel"] == 4
-    cfg4 = dataclasses.replace(synth.CONFIGS["cfg4"], n=47, n_bins=1)
+    assert ctx.stats()["gs_kernel"] == 4 and ctx.stats()["gs_max_group"] == 1
+    cfg4 = dataclasses.replace(synth.CONFIGS["cfg4"], n=64, n_bins=1)
     b4 = synth.make_band(cfg4)
     ctx.solve_band(geom_of(b4), b4.freqs, torch.from_numpy(b4.csm).cuda(), cfg4.epsilon, 3, full_grid=True)
-    assert ctx.stats()["gs_kernel"] in (1, 2)
+    assert ctx.stats()["gs_kernel"] == 4 and ctx.stats()["gs_max_group"] == 2
+    script = _AUTO_SCRIPT.format(root=ROOT)
+    env = dict(os.environ, DWC_RGS_AUTO_MAX_SP="2048")
+    r = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert int(r.stdout.split()[-1]) in (1, 2)
     import ctypes as C
 
     from paper_1608_05179_b200.dwc import Params, lib
@@ -225,3 +236,17 @@ def test_automatic_kernel_choice(ctx, torch_cuda):
     b8 = torch.ones(8, dtype=torch.float64).cuda()
     x8 = torch.empty(8, dtype=torch.float32).cuda()
     assert lib().dwc_gs(ctx._h, 8, A8.data_ptr(), b8.data_ptr(), 1, 16 | 32, x8.data_ptr(), None) == -1
+
+
+_AUTO_SCRIPT = r"""
+import dataclasses, sys, torch
+sys.path.insert(0, {root!r})
+import synth
+from paper_1608_05179_b200 import Context, Geometry
+cfg4 = dataclasses.replace(synth.CONFIGS["cfg4"], n=47, n_bins=1)
+b4 = synth.make_band(cfg4)
+g = Geometry(b4.mic_xyz, cfg4.n, cfg4.side_len, cfg4.z0, cfg4.c0, cfg4.cx, cfg4.cy)
+c = Context(0)
+c.solve_band(g, b4.freqs, torch.from_numpy(b4.csm).cuda(), cfg4.epsilon, 3, full_grid=True)
+print(c.stats()["gs_kernel"])
+"""
