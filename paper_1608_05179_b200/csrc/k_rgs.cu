@@ -200,6 +200,12 @@ __device__ __forceinline__ void mbar_arrive_tx_cl(uint32_t rbar, uint32_t bytes)
     asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(rbar), "r"(bytes)
                  : "memory");
 }
+// relaxed: the data the waiter reads travels by st.async on the same barrier, so the arrival needs
+// no release (a release at cluster scope waits for the thread's outstanding stores)
+__device__ __forceinline__ void mbar_arrive_tx_cl_relaxed(uint32_t rbar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.relaxed.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(rbar), "r"(bytes)
+                 : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, unsigned long long *bar) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
@@ -645,16 +651,18 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 if (lane == 0) {
                     sh.cnt[li] = q;
                     pmask[k] = chg;   // the prediction for the next visit
-                    if (CLU)
-                        for (int c = 1; c < G; c++) st_async_b32(cl_map(&sh.cnt[li], c), (uint32_t)q, cl_map(&sh.dready[li], c));
+                }
+                if (CLU && lane >= 1 && lane < G) {   // lane c: CTA c's count and dready arrival (the list
+                    // bytes complete on it too; the arrival needs no release: everything CTA c reads
+                    // arrives by st.async)
+                    st_async_b32(cl_map(&sh.cnt[li], lane), (uint32_t)q, cl_map(&sh.dready[li], lane));
+                    mbar_arrive_tx_cl_relaxed(cl_map(&sh.dready[li], lane), 16u * (uint32_t)q + 4u);
                 }
                 my_updates += (unsigned long long)q;
                 my_bytes += (unsigned long long)q * sp * 4;
                 __syncwarp();
                 if (lane == 0) {
                     mbar_arrive(&sh.dready[li]);
-                    if (CLU)   // the other CTAs' dready: one arrival plus the bytes of the list and count
-                        for (int c = 1; c < G; c++) mbar_arrive_tx_cl(cl_map(&sh.dready[li], c), 16u * (uint32_t)q + 4u);
                     mbar_arrive(&sh.stg_empty[sl]);
                 }
 #pragma unroll
@@ -766,8 +774,9 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 publish(s, p, pos, nsub + 1, false);
                 __syncwarp();
                 if (lane == 0) {
-                    if (CLU)   // the leader's sdone: one arrival plus the bytes this warp published
-                        mbar_arrive_tx_cl(cl_map(&sh.sdone[li], 0), pub_bytes);
+                    if (CLU)   // the leader's sdone: one arrival plus the bytes this warp published (by
+                        // st.async: no release needed; the slots it reuses were consumed steps ago)
+                        mbar_arrive_tx_cl_relaxed(cl_map(&sh.sdone[li], 0), pub_bytes);
                     else
                         mbar_arrive(&sh.sdone[li]);
                 }
