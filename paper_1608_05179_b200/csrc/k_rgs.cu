@@ -949,6 +949,8 @@ size_t rgs_smem_bytes(int max_sp) { return rgs_base_bytes(max_sp, max_sp <= 8 * 
 int rgs_cluster_size(int sp) {
     static const bool no_regr = getenv("DWC_RGS_NO_REGR") != nullptr;       // experiment: r in shared memory
     static const bool no_cluster = getenv("DWC_RGS_NO_CLUSTER") != nullptr; // experiment
+    static const int force_g = getenv("DWC_RGS_CLUSTER_G") ? atoi(getenv("DWC_RGS_CLUSTER_G")) : 0;   // experiment
+    if (force_g > 1 && force_g <= 8 && !no_regr) return force_g;
     if (no_regr || no_cluster || sp <= kRegMaxSp) return 1;
     const int g = (sp + kRegMaxSp - 1) / kRegMaxSp;
     return g <= 8 ? g : 1;   // (portable cluster sizes; beyond: one CTA with r in shared memory)
