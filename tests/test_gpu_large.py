@@ -250,3 +250,40 @@ c = Context(0)
 c.solve_band(g, b4.freqs, torch.from_numpy(b4.csm).cuda(), cfg4.epsilon, 3, full_grid=True)
 print(c.stats()["gs_kernel"])
 """
+
+
+@pytest.mark.parametrize("dense", [False, True], ids=["residual", "alt_kernel"])
+def test_gs_large_alternating(ctx, torch_cuda, oracle_lib, dense):
+    """Alternating sweep directions (R21) on an S~ = 4500 system: the residual kernel's cluster
+    mode (2 CTAs, the alternating visit sequence across CTAs) and the one-CTA-per-bin kernel."""
+    torch = torch_cuda
+    A, bt = cfg5_system(oracle_lib, 4500)
+    ref = oracle_lib.gs(A, bt, 21, alt=True)
+    x = ctx.gs(torch.from_numpy(A.astype(np.float32)).cuda(), torch.from_numpy(bt).cuda(), 21, alt=True,
+               dense_stream=dense).cpu().numpy()
+    st = ctx.stats()
+    assert st["gs_kernel"] == (3 if dense else 4) and (dense or st["gs_max_group"] == 2)
+    assert x.min() >= 0
+    assert rel_l2(x, ref) < TOL_X, rel_l2(x, ref)
+    assert abs(x.sum() - ref.sum()) < TOL_P * ref.sum()
+
+
+def test_gs_large_general_matrix(ctx, torch_cuda, oracle_lib):
+    """The paper-literal (asymmetric) PSF of an S~ = 3000 system in cfg5's geometry: the residual
+    kernel's cluster mode on the transposed store, against the oracle's Eq. 13-14 loop."""
+    torch = torch_cuda
+    band = synth.make_band("cfg5", bins=[1023])
+    g = geom_of(band)
+    f = band.freqs[0]
+    b_full = oracle_lib.das_paper(*oracle_args(g), f, band.csm[0])
+    keep = np.sort(np.argsort(-b_full)[:3000]).astype(np.int32)
+    A = oracle_lib.psf_paper(*oracle_args(g), f, keep)
+    bt = b_full[keep]
+    ref = oracle_lib.gs(A, bt, 20)
+    x = ctx.gs(torch.from_numpy(A.astype(np.float32)).cuda(), torch.from_numpy(bt).cuda(), 20,
+               general=True).cpu().numpy()
+    st = ctx.stats()
+    assert st["gs_kernel"] == 4 and st["gs_max_group"] == 2
+    assert x.min() >= 0
+    assert rel_l2(x, ref) < TOL_X, rel_l2(x, ref)
+    assert abs(x.sum() - ref.sum()) < TOL_P * ref.sum()
