@@ -11,3 +11,7 @@ run cfg3_snap --input snapshots
 run cfg3_dense_kernel --kernel dense
 run cfg4 --config cfg4 --steps 2 --warmup 3 --no-cvf
 run cfg5 --config cfg5 --steps 2 --warmup 3 --no-cvf
+# ncu capture of the residual kernel's cluster mode on cfg4 (full grid): DRAM bytes per launch
+CMD4="python bench.py --config cfg4 --steps 1 --warmup 1 --no-cpu-baseline --no-cvf"
+timeout 900 $CMD4 > gpurun_out/plain4.log 2>&1 && \
+  timeout 1500 ncu --set full --clock-control none --import-source on -k regex:rgs_kernel -s 1 -c 1 -o gpurun_out/rgs_cfg4_full -f $CMD4 > gpurun_out/ncu_cfg4.log 2>&1; echo "ncu_cfg4 rc=$?"
