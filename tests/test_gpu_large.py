@@ -167,6 +167,30 @@ def _e2e(ctx, torch, oracle_lib, band, sweeps, full=False, dense=False):
     return st, nk
 
 
+def test_gs_residual_cluster_of_5(ctx, torch_cuda, oracle_lib):
+    """S~ = 12000 (12000 padded points: a cluster of 5 CTAs, 5 x 2400 columns of r) on the residual
+    kernel against the oracle."""
+    torch = torch_cuda
+    A, bt = cfg5_system(oracle_lib, 12000)
+    ref = oracle_lib.gs(A, bt, 12)
+    x = ctx.gs(torch.from_numpy(A.astype(np.float32)).cuda(), torch.from_numpy(bt).cuda(), 12,
+               dense_stream=False).cpu().numpy()
+    st = ctx.stats()
+    assert st["gs_kernel"] == 4 and st["gs_max_group"] == 5
+    assert x.min() >= 0
+    assert rel_l2(x, ref) < TOL_X, rel_l2(x, ref)
+    assert abs(x.sum() - ref.sum()) < TOL_P * ref.sum()
+
+
+def test_e2e_cfg5_mixed_cluster_classes(ctx, torch_cuda, oracle_lib):
+    """One cfg5 band whose systems need 1, 2 and 4 CTAs (S~ ~ 1.6k, 3.3k, 8.6k): one residual
+    launch per size class, the classes concurrently on forked streams, 20 sweeps."""
+    band = synth.make_band("cfg5", bins=[300, 600, 1023])
+    st, nk = _e2e(ctx, torch_cuda, oracle_lib, band, 20)
+    assert st["gs_kernel"] == 4 and st["gs_max_group"] == 4
+    assert sorted(-(-((int(v) + 31) // 32 * 32) // 2560) for v in nk) == [1, 2, 4]
+
+
 @pytest.mark.parametrize("dense", [False, True], ids=["residual", "dense_stream"])
 def test_e2e_cfg5_largest_bins(ctx, torch_cuda, oracle_lib, dense):
     """cfg5's three largest bins (11.2-12 kHz, S~ ~ 8-9k of 40401) at 20 sweeps, in one call."""
