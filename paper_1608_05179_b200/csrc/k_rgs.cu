@@ -576,6 +576,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 // the transposed store) -- the only shared-memory load on the row-to-row chain
                 float w = -ac * invd;
                 const float *dgt = sh.diag[sl] + rl;
+                const float *dgt_last = dgt + 32 * 31;
                 // the previous change's panel values and dv: consumed one iteration later, after the
                 // next ballot, so that the chain never waits for the panel loads
                 float pvp[kRgsWin], dvp = 0.f;
@@ -596,8 +597,10 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                     const unsigned m = __ballot_sync(0xffffffffu, (fwd ? rl >= pos_r : rl <= pos_r) && xn != xo);
                     // the row (in the block) of the next change: forward sweeps take the lowest row,
                     // i.e. (ALT = false, rl = 31 - lane) the highest ballot bit
-                    const int tl = 31 - __clz(m);   // (FLO) the highest ballot bit, -1 when m == 0
-                    const int t = !ALT ? tl ^ 31 : fwd ? __ffs(m) - 1 : tl;
+                    int tl;   // the highest ballot bit (bfind = FLO; -1 when m == 0): the lane of the next
+                    // change for forward sweeps, used as is on the chain (shuffle source, own-lane test)
+                    asm("bfind.u32 %0, %1;" : "=r"(tl) : "r"(m));
+                    const int t = !ALT ? 31 - tl : fwd ? __ffs(m) - 1 : tl;
                     DWC_DCHECK(m == 0u || (t >= 0 && t < 32 && !((chg >> t) & 1u)), "solver: a row changes twice in one visit");
 #pragma unroll
                     for (int d = 0; d < kRgsWin; d++)   // (forward: pv = 0 beyond nsub)
@@ -605,8 +608,8 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                     if (m == 0u) break;
 #endif
                     const float dv = __shfl_sync(0xffffffffu, dl, ALT ? t : tl);
-                    const float a0 = dgt[32 * t];
-                    if (rl == t) xo = xn;   // (the list entry is written after the block, below)
+                    const float a0 = ALT ? dgt[32 * t] : dgt_last[-32 * tl];   // (row t = 31 - tl: one IMAD)
+                    if (ALT ? rl == t : lane == tl) xo = xn;   // (the list entry is written after the block, below)
                     w = fmaf(-invd * dv, a0, w);
                     // off the chain: the carries, from row t's staged panel (element 32(d-1) + lane =
                     // A[32k+t][32 blk(s+d) + lane] = A[32 blk(s+d) + lane][32k+t]; segments beyond nsub
