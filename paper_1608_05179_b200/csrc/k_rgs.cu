@@ -13,30 +13,37 @@
 // are sparse (cfg2-cfg5: 5-25 % of the kept nodes change per sweep, fewer as the sweeps
 // converge), and a row whose x does not change is not read at all.
 //
-// Block formulation (B = 32 rows, T = sp/32 blocks, global step s solves block k = s mod T):
-//  * solver (warp 4, lane = row 32k + lane): the block's residuals are the stored r plus the
-//    carried contributions of the changes of the last W = min(kRgsWin, T-1) steps, which the
-//    solver accumulates itself (fp32, for its own residuals only).  In row
-//    order, the next row whose x changes is found with one ballot over the block (the rows in
-//    between keep x exactly); its change is broadcast and applied to every row's fp32 update
-//    w = -r/A_ii (from the block's diagonal tile, the only load on the row-to-row chain) and to
-//    the carries of the blocks of the next W steps (from row t's "panel": row t of A~ = column t,
-//    symmetric, over the columns of those blocks; consumed one change later, off the chain).
-//    A block with q changing rows takes q + 1 ballot rounds instead of a 32-row chain.  The
-//    changes (row, x before / after) are published as the step's change list.
+// Block formulation (B = 32 rows, T = sp/32 blocks, global step s solves block k = s mod T; for
+// alternating sweeps (reading R21) the visit sequence k = pos or T-1-pos):
+//  * solver (warp 4; forward sweeps: lane l = row 32k + 31 - l, so the next row in order is the
+//    highest ballot bit): the block's residuals are the stored r plus the carried contributions
+//    of the changes of the last W = min(kRgsWin, T-1) steps, which the solver accumulates itself
+//    (fp32, for its own residuals only).  In row order, the next row whose x changes is found
+//    with one ballot over the block (the rows in between keep x exactly); its change is broadcast
+//    and applied to every row's fp32 update w = -r/A_ii (from the block's diagonal tile, the only
+//    load on the row-to-row chain) and to the carries of the blocks of the next W steps (from
+//    row t's "panel": row t of A~ = column t, symmetric, over the columns of those blocks;
+//    consumed one change later, off the chain).  A block with q changing rows takes q + 1
+//    ballot rounds instead of a 32-row chain.  The changes (row, x before / after) are
+//    published as the step's change list.
 //  * panel producer (warp 5): per step, cp.async copies of the block's 32x32 diagonal tile and of
 //    the panels of the rows PREDICTED to change: those that changed at the block's previous visit
 //    (before the first visit: the rows with b > 0, exactly the rows sweep 1 changes).  The carries
-//    of a change outside the prediction (rare: the active set of a DAMAS iteration is stable)
-//    are added after the block from global memory.
-//  * row producer (warp 6): bulk-copies the rows of A~ (dense row-major) of every listed change
-//    into a double-buffered shared-memory ring, whole rows or segments of them, as batches.
-//  * stream (warps 0..3, 7): apply dx_c * A[c, :] (fp64) to the stored r of every block, except that
-//    the W blocks the solver carries accumulate into a pending buffer that is added to r when the
-//    solver has read the block (its own step); 128-column chunks are owned by warps (chunk mod 5), so every
-//    element of r has one writer and a fixed update order.  The solver of step s needs stream
+//    of a change outside the prediction are added after the block from global memory.
+//  * row producer (warp 6): the exact fp64 dx of every listed change; bulk copies of the rows of
+//    A~ (dense row-major) of every change into a 4-slot shared-memory ring, as batches.
+//  * stream (warps 0..3, 7; 128-column chunks owned by warps, so every element of r has one
+//    writer and a fixed update order): apply dx_c * A[c, :] (fp64) to r.  REGR (systems up to
+//    kRegMaxSp points): r in the stream warps' registers; after its step j the owner of a block
+//    publishes that block's r (fp32) for the solver step that reads "r after stream step j".
+//    Otherwise r in shared memory, and the W blocks the solver carries accumulate into a pending
+//    buffer added to r when the solver has read the block.  The solver of step s needs stream
 //    step s - W - 1 complete: W steps of slack for the row fetch.
-// One CTA per bin; bins are taken in descending S~ order from a global counter.
+//  * cluster mode (CLU, systems above kRegMaxSp up to 8 x kRegMaxSp): the G CTAs of a cluster
+//    share a bin, CTA c holding r of a contiguous range of chunks (REGR); only the leader runs
+//    the solver and the panel producer; change lists go to the other CTAs, published r back to
+//    the leader, by st.async completing on mbarriers (relaxed cross-CTA arrivals).
+// One CTA (cluster) per bin; bins are taken in descending S~ order from a global counter.
 // Numerics: the stream accumulates A~ (fp32, widened exactly) x dx (fp64) into r in fp64; the
 // solver's carries and its row recurrence are fp32.
 #include <stdint.h>
@@ -61,9 +68,6 @@ constexpr int kRMinBlocks = kNStream > 5 ? 1 : 2;
 // warp roles: the latency-critical warps take the higher warp of each SMSP pair (w, w+4): the
 // issue arbiter prefers the higher warp id
 constexpr int kWSolver = 4, kWPanel = 5, kWRows = 6;
-#ifndef RGS_REDUX
-#define RGS_REDUX 0
-#endif
 #ifndef RGS_STG
 #define RGS_STG 5
 #endif
@@ -585,15 +589,6 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 for (;;) {
                     const float xn = xo + fmaxf(w, -xo);   // = max(xo - ac/A_ii, 0)
                     const float dl = xn - xo;              // this row's change if it is the next one
-#if RGS_REDUX
-                    const bool cand = (fwd ? rl >= pos_r : rl <= pos_r) && xn != xo;
-                    const int t = fwd ? (int)__reduce_min_sync(0xffffffffu, cand ? (unsigned)rl : 32u)
-                                      : (int)__reduce_max_sync(0xffffffffu, cand ? (unsigned)rl + 1u : 0u) - 1;
-#pragma unroll
-                    for (int d = 0; d < kRgsWin; d++)   // (forward: pv = 0 beyond nsub)
-                        if (!ALT || ((vmask >> d) & 1u)) acc[d] = fmaf(pvp[d], dvp, acc[d]);
-                    if (t < 0 || t > 31) break;
-#else
                     const unsigned m = __ballot_sync(0xffffffffu, (fwd ? rl >= pos_r : rl <= pos_r) && xn != xo);
                     // the row (in the block) of the next change: forward sweeps take the lowest row,
                     // i.e. (ALT = false, rl = 31 - lane) the highest ballot bit
@@ -606,7 +601,6 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                     for (int d = 0; d < kRgsWin; d++)   // (forward: pv = 0 beyond nsub)
                         if (!ALT || ((vmask >> d) & 1u)) acc[d] = fmaf(pvp[d], dvp, acc[d]);
                     if (m == 0u) break;
-#endif
                     const float dv = __shfl_sync(0xffffffffu, dl, ALT ? t : tl);
                     const float a0 = ALT ? dgt[32 * t] : dgt_last[-32 * tl];   // (row t = 31 - tl: one IMAD)
                     if (ALT ? rl == t : lane == tl) xo = xn;   // (the list entry is written after the block, below)
