@@ -65,7 +65,7 @@ struct dwc_ctx {
     cudaEvent_t keep_ready = nullptr, copy_done = nullptr;
     // residual GS on a band whose systems need different cluster sizes: one launch per size class,
     // the classes on their own streams (forked from and joined back into the call's stream)
-    static constexpr int kMaxClasses = 4;
+    static constexpr int kMaxClasses = 8;
     cudaStream_t class_st[kMaxClasses] = {};
     cudaEvent_t class_fork = nullptr, class_join[kMaxClasses] = {};
     int geo_m = -1, geo_n = -1;
@@ -455,12 +455,15 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
     GsLaunchInfo gsi;
     if (resid) {
         CU(cudaMemsetAsync(ctx->upd.p, 0, 64, st));
-        // size classes of the bins (order = descending S~): the cluster size each system needs
-        // (rgs_cluster_size); one launch per class, the classes concurrently on their own streams
+        // size classes of the bins (order = descending S~): the CTAs and registers each system
+        // needs (rgs_size_class); one launch per class, the classes concurrently on their own streams
+        // (wide clusters -- 5120 columns per CTA -- on the compressed grid, where many rows change
+        // per sweep; narrow ones on the full grid, where few do)
+        const bool wide_cl = !(p->flags & DWC_FULL_GRID);
         std::vector<std::pair<int, int>> cls;   // [begin, end) in `order`
         for (int i = 0; i < n_bins; i++) {
-            const int g = rgs_cluster_size((hk[order[i]] + 31) & ~31);
-            if (cls.empty() || rgs_cluster_size((hk[order[cls.back().first]] + 31) & ~31) != g)
+            const int g = rgs_size_class((hk[order[i]] + 31) & ~31, wide_cl);
+            if (cls.empty() || rgs_size_class((hk[order[cls.back().first]] + 31) & ~31, wide_cl) != g)
                 cls.push_back({i, i + 1});
             else
                 cls.back().second = i + 1;
@@ -488,7 +491,7 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
             LAUNCH(launch_rgs(nb, (int *)ctx->order.p + b0, (BinLayout *)ctx->lay.p, csp, (int *)ctx->counter.p + c,
                               (float *)ctx->Ad.p, (double *)ctx->bt.p, p->sweeps, nullptr, x_map, keep_idx,
                               S, ctx->num_sms, (unsigned long long *)ctx->upd.p, cs, &ci, alt,
-                              /*nonneg: every PSF is |.|^2 times positive scales*/ 1));
+                              /*nonneg: every PSF is |.|^2 times positive scales*/ 1, wide_cl ? 1 : 0));
             gsi.ctas += ci.ctas;
             gsi.max_group = std::max(gsi.max_group, ci.max_group);
             if (c > 0) CU(cudaEventRecord(ctx->class_join[c], cs));

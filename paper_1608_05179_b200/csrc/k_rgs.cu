@@ -97,8 +97,12 @@ constexpr int kNList = RGS_NLIST;    // change-list ring (steps; > kRgsWin + 2)
 static_assert(kNList > kRgsWin + 2, "the row producer must stay within the change-list ring");
 constexpr int kCP = 2;               // stream: chunks held in registers per pass
 constexpr int kNSlot = RGS_NSLOT;    // row ring: batches in flight
-constexpr int kRegCh = 4;            // register-resident r: 128-column chunks per stream warp
-constexpr int kRegMaxSp = 128 * kRegCh * kNStream;   // the largest system it holds
+// register-resident r: 128-column chunks per stream warp -- kRegCh for systems up to kRegMaxSp
+// points (and per CTA in cluster mode), kRegChWide for a single CTA up to kRegMaxSpWide (twice
+// the registers: measured 3 % slower on cfg3's small systems, so only where it saves a cluster)
+constexpr int kRegCh = 4, kRegChWide = 8;
+constexpr int kRegMaxSp = 128 * kRegCh * kNStream;            // 2560
+constexpr int kRegMaxSpWide = 128 * kRegChWide * kNStream;    // 5120
 
 struct __align__(16) RgsEntry {
     float xn, xo;   // x of the row after / before the change (dx = xn - xo, exact in fp64)
@@ -272,8 +276,8 @@ constexpr int kProfItems = 1024;   // then per item: start, end (globaltimer ns)
 // masks (T words) and the row ring (kNSlot slots of slot_floats) follow RgsSmem.
 // Register-resident stream: the rows of one ring batch applied to the NC chunks a warp owns (all
 // loads of a row issued together, independent fp64 chains per chunk element).
-template <int NC, bool NN>
-__device__ __forceinline__ void apply_rows(double (&r)[kRegCh][4], const float *src, int sp, int nb, const double *dxs,
+template <int NC, bool NN, int RC>
+__device__ __forceinline__ void apply_rows(double (&r)[RC][4], const float *src, int sp, int nb, const double *dxs,
                                            int w) {
 #pragma unroll 4
     for (int j = 0; j < nb; j++) {
@@ -292,7 +296,30 @@ __device__ __forceinline__ void apply_rows(double (&r)[kRegCh][4], const float *
     }
 }
 
-template <bool ALT, bool REGR, bool CLU>
+// nch = the chunks a warp owns (0: a small system leaves this warp none)
+template <bool NN, int RC>
+__device__ __forceinline__ void apply_dispatch(int nch, double (&r)[RC][4], const float *src, int stride, int nb,
+                                               const double *dxb, int w) {
+    switch (nch) {
+        case 1: apply_rows<1, NN, RC>(r, src, stride, nb, dxb, w); break;
+        case 2: apply_rows<2, NN, RC>(r, src, stride, nb, dxb, w); break;
+        case 3: apply_rows<3, NN, RC>(r, src, stride, nb, dxb, w); break;
+        case 4: apply_rows<4, NN, RC>(r, src, stride, nb, dxb, w); break;
+        default:
+            if constexpr (RC > 4) {
+                switch (nch) {
+                    case 5: apply_rows<5, NN, RC>(r, src, stride, nb, dxb, w); break;
+                    case 6: apply_rows<6, NN, RC>(r, src, stride, nb, dxb, w); break;
+                    case 7: apply_rows<7, NN, RC>(r, src, stride, nb, dxb, w); break;
+                    case 8: apply_rows<8, NN, RC>(r, src, stride, nb, dxb, w); break;
+                    default: break;
+                }
+            }
+            break;
+    }
+}
+
+template <bool ALT, bool REGR, bool CLU, int RC = kRegCh>
 __global__ void __launch_bounds__(kRThreads, REGR ? 1 : kRMinBlocks)
 rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restrict__ lay, int *__restrict__ counter,
            const float *__restrict__ Adense, const double *__restrict__ bt, int sweeps, float *__restrict__ x_out,
@@ -689,12 +716,12 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
             // (CLU: the chunks of this CTA's slice, local index ql = q - q_lo)
             const int w = (wid < 4) ? wid : wid - 3;
             const int nch = max(0, (q_hi - q_lo - w + kNStream - 1) / kNStream);   // chunks this warp owns
-            DWC_DCHECK(nch <= kRegCh && rg.nseg == 1, "stream: register chunks");
+            DWC_DCHECK(nch <= RC && rg.nseg == 1, "stream: register chunks");
             unsigned long long tlw = 0, tbw = 0, tap = 0, nb_all = 0;
             uint32_t pub_bytes = 0;   // (CLU) bytes this warp published during the current step
-            double r[kRegCh][4];
+            double r[RC][4];
 #pragma unroll
-            for (int c = 0; c < kRegCh; c++) {
+            for (int c = 0; c < RC; c++) {
                 const int col = col0 + 128 * (w + kNStream * c) + 4 * lane;
 #pragma unroll
                 for (int e = 0; e < 4; e++) r[c][e] = (col + e < sp) ? -bt[L.v_off + col + e] : 0.0;
@@ -711,14 +738,14 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 if (before ? !(rev && vp == s0) : rev) return;
                 const int bb = sweep_fwd(p2, alt) ? q2 : T - 1 - q2;   // its block
                 const int qb = bb >> 2, oc = CLU ? qb / nqc : 0, ql = qb - oc * nqc;   // owner CTA, local chunk
-                DWC_DCHECK(bb >= 0 && bb < T && ql / kNStream < kRegCh && oc < G, "stream: published block");
+                DWC_DCHECK(bb >= 0 && bb < T && ql / kNStream < RC && oc < G, "stream: published block");
                 if (oc == (int)crank && (ql % kNStream) == w) {
                     if ((lane >> 3) == (bb & 3)) {
                         const int cb = ql / kNStream;
                         // rounded to fp32 here (the solver's recurrence is fp32), off the solver's path
                         float *dst = reinterpret_cast<float *>(pend) + 32 * ((s0 + d) & (kPendBlk - 1)) + 4 * (lane & 7);
 #pragma unroll
-                        for (int c = 0; c < kRegCh; c++)
+                        for (int c = 0; c < RC; c++)
                             if (c == cb) {
                                 const float4 v = make_float4((float)r[c][0], (float)r[c][1], (float)r[c][2], (float)r[c][3]);
                                 if (CLU)   // into the leader's slot, completing on its sdone of this stream step
@@ -751,17 +778,10 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                     const int nb = min(rg.upb, n - u0);
                     const float *src = ring + (size_t)h * slot_floats + 4 * lane;
                     const double *dxb = &sh.dxs[li][u0];
-                    switch (nonneg ? nch : nch + 8) {   // (0: a small system leaves this warp no chunk)
-                        case 1: apply_rows<1, true>(r, src, rstride, nb, dxb, w); break;
-                        case 2: apply_rows<2, true>(r, src, rstride, nb, dxb, w); break;
-                        case 3: apply_rows<3, true>(r, src, rstride, nb, dxb, w); break;
-                        case 4: apply_rows<4, true>(r, src, rstride, nb, dxb, w); break;
-                        case 9: apply_rows<1, false>(r, src, rstride, nb, dxb, w); break;
-                        case 10: apply_rows<2, false>(r, src, rstride, nb, dxb, w); break;
-                        case 11: apply_rows<3, false>(r, src, rstride, nb, dxb, w); break;
-                        case 12: apply_rows<4, false>(r, src, rstride, nb, dxb, w); break;
-                        default: break;
-                    }
+                    if (nonneg)
+                        apply_dispatch<true, RC>(nch, r, src, rstride, nb, dxb, w);
+                    else
+                        apply_dispatch<false, RC>(nch, r, src, rstride, nb, dxb, w);
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&sh.rempty[h]);
                     if (pf) { tbw += t2 - t1; tap += clk() - t2; nb_all++; }
@@ -943,20 +963,29 @@ int rgs_auto_max_sp() {
 size_t rgs_smem_bytes(int max_sp) { return rgs_base_bytes(max_sp, max_sp <= 8 * kRegMaxSp) + kNSlot * 128 * 4 + 512; }
 
 
-int rgs_cluster_size(int sp) {
+// wide: clusters of CTAs with 8 chunks per stream warp (5120 columns each) rather than 4 (2560):
+// fewer SMs per bin, more stream work per CTA -- better when many rows change per sweep (the
+// compressed grid: cfg5 GS 801 -> 665 ms), worse when few do (cfg4's full grid: 183 -> 200 ms)
+int rgs_cluster_size(int sp, bool wide) {
     static const bool no_regr = getenv("DWC_RGS_NO_REGR") != nullptr;       // experiment: r in shared memory
     static const bool no_cluster = getenv("DWC_RGS_NO_CLUSTER") != nullptr; // experiment
     static const int force_g = getenv("DWC_RGS_CLUSTER_G") ? atoi(getenv("DWC_RGS_CLUSTER_G")) : 0;   // experiment
     if (force_g > 1 && force_g <= 8 && !no_regr) return force_g;
-    if (no_regr || no_cluster || sp <= kRegMaxSp) return 1;
-    const int g = (sp + kRegMaxSp - 1) / kRegMaxSp;
+    if (no_regr || no_cluster || sp <= kRegMaxSpWide) return 1;   // (one CTA: r in registers, wide above kRegMaxSp)
+    const int per = wide ? kRegMaxSpWide : kRegMaxSp;
+    const int g = (sp + per - 1) / per;
     return g <= 8 ? g : 1;   // (portable cluster sizes; beyond: one CTA with r in shared memory)
+}
+
+int rgs_size_class(int sp, bool wide) {
+    const int g = rgs_cluster_size(sp, wide);
+    return g > 1 ? 1 + g : (sp > kRegMaxSp ? 1 : 0);   // 0: one CTA, 1: one CTA with wide registers, 1+G: clusters
 }
 
 int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int max_sp, int *counter,
                const float *Adense, const double *bt, int sweeps, float *x_out, float *x_map,
                const int32_t *keep_idx, int S, int num_sms, unsigned long long *n_updates, cudaStream_t st,
-               GsLaunchInfo *info, int alt, int nonneg) {
+               GsLaunchInfo *info, int alt, int nonneg, int wide_clusters) {
     static const int ring_env = getenv("DWC_RGS_RING_KB") ? atoi(getenv("DWC_RGS_RING_KB")) : 0;   // experiment
     static const int per_sm_env = getenv("DWC_RGS_PER_SM") ? atoi(getenv("DWC_RGS_PER_SM")) : 0;   // experiment
     static const bool no_regr = getenv("DWC_RGS_NO_REGR") != nullptr;   // experiment: r in shared memory
@@ -964,25 +993,32 @@ int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int m
     // chunks; above that, split over a cluster of G CTAs (<= 8, portable) -- both need a ring slot
     // that holds a whole row (slice); else r in shared memory
     const int nq_max = (max_sp + 127) / 128;
-    int G = rgs_cluster_size(max_sp);
-    const bool regr_try = !no_regr && (max_sp <= kRegMaxSp || G > 1);
+    int G = rgs_cluster_size(max_sp, wide_clusters);
+    const bool regr_try = !no_regr && (max_sp <= kRegMaxSpWide || G > 1);
+    // 8 chunks per stream warp: one CTA above kRegMaxSp, or the wide clusters
+    const bool wide = regr_try && (G == 1 ? max_sp > kRegMaxSp : (bool)wide_clusters);
     const int rstride_max = G > 1 ? 128 * ((nq_max + G - 1) / G) : max_sp;   // floats of a ring row
     // the configuration: base shared memory, 1/A_ii copy (when a ring of >= 24 KB still fits), ring
-    auto layout = [&](bool regr, int &use_ivs, size_t &base) {
-        use_ivs = (rgs_base_bytes(max_sp, regr) + (size_t)max_sp * 4 + 24 * 1024 + 1536 <= 227 * 1024) ? 1 : 0;
+    auto layout = [&](bool regr, int &use_ivs, size_t &base, bool allow_ivs) {
+        use_ivs = (allow_ivs && rgs_base_bytes(max_sp, regr) + (size_t)max_sp * 4 + 24 * 1024 + 1536 <= 227 * 1024) ? 1 : 0;
         base = (rgs_base_bytes(max_sp, regr) + (use_ivs ? (size_t)max_sp * 4 : 0) + 127) / 128 * 128;
+    };
+    auto slot_of = [&](size_t ring) { return (int)(ring / (4 * kNSlot)) / 128 * 128; };
+    auto ring_of = [&](size_t base) {
+        size_t ring = base + 1536 <= 227 * 1024 ? (227 * 1024 - base - 512) / 1024 * 1024 : 0;
+        if (ring_env > 0 && (size_t)ring_env * 1024 < ring) ring = (size_t)ring_env * 1024;
+        return ring;
     };
     int use_ivs;
     size_t base;
     bool regr = regr_try;
-    layout(regr, use_ivs, base);
-    auto slot_of = [&](size_t ring) { return (int)(ring / (4 * kNSlot)) / 128 * 128; };
-    size_t ring = base + 1536 <= 227 * 1024 ? (227 * 1024 - base - 512) / 1024 * 1024 : 0;
-    if (ring_env > 0 && (size_t)ring_env * 1024 < ring) ring = (size_t)ring_env * 1024;
-    if (regr && slot_of(ring) < rstride_max) {   // no whole row per slot: r in shared memory
+    layout(regr, use_ivs, base, true);
+    if (regr && slot_of(ring_of(base)) < rstride_max)   // a slot must hold a whole row (slice): drop the 1/A_ii copy
+        layout(regr, use_ivs, base, false);
+    if (regr && slot_of(ring_of(base)) < rstride_max) {   // still not: r in shared memory
         regr = false;
         G = 1;
-        layout(regr, use_ivs, base);
+        layout(regr, use_ivs, base, true);
     }
     if (base + 1536 > 227 * 1024) return -1;
     // shared-memory r: two CTAs per SM (2 x (smem + 1 KB reserved) <= 228 KB) when the band has
@@ -991,14 +1027,19 @@ int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int m
     const bool two = (regr || kRMinBlocks < 2) ? false
                      : per_sm_env ? per_sm_env == 2 && per2 > base + 2048
                                 : n_bins > num_sms && per2 > base && (per2 - base) / (4 * kNSlot) >= 2 * (size_t)max_sp;
-    ring = two ? (per2 - base - 512) / 1024 * 1024 : (227 * 1024 - base - 512) / 1024 * 1024;
+    size_t ring = two ? (per2 - base - 512) / 1024 * 1024 : (227 * 1024 - base - 512) / 1024 * 1024;
     if (ring_env > 0 && (size_t)ring_env * 1024 < ring) ring = (size_t)ring_env * 1024;
     const int slot_floats = slot_of(ring);   // floats per ring slot
     if (slot_floats < 128) return -1;
     const size_t smem = base + (size_t)slot_floats * 4 * kNSlot + 512;   // + slack: a row's last chunk reads past it
     const bool clu = G > 1;
-    const auto kern = alt ? (clu ? rgs_kernel<true, true, true> : regr ? rgs_kernel<true, true, false> : rgs_kernel<true, false, false>)
-                          : (clu ? rgs_kernel<false, true, true> : regr ? rgs_kernel<false, true, false> : rgs_kernel<false, false, false>);
+    const auto kern =
+        alt ? (clu ? (wide ? rgs_kernel<true, true, true, kRegChWide> : rgs_kernel<true, true, true>)
+                   : regr ? (wide ? rgs_kernel<true, true, false, kRegChWide> : rgs_kernel<true, true, false>)
+                          : rgs_kernel<true, false, false>)
+            : (clu ? (wide ? rgs_kernel<false, true, true, kRegChWide> : rgs_kernel<false, true, true>)
+                   : regr ? (wide ? rgs_kernel<false, true, false, kRegChWide> : rgs_kernel<false, true, false>)
+                          : rgs_kernel<false, false, false>);
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return -1;
     cudaLaunchConfig_t cfg = {};

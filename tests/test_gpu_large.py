@@ -62,6 +62,14 @@ _SYS = {}
 _ORACLE = {}
 
 
+def resid_ctas(nk, wide):
+    """CTAs per bin of the residual kernel: one CTA up to 5120 padded points (r in registers, 8
+    chunks per stream warp above 2560), else a cluster -- wide (5120 points per CTA, the
+    compressed grid and dwc_gs) or narrow (2560, the full grid)."""
+    sp = (int(nk) + 31) // 32 * 32
+    return 1 if sp <= 5120 else -(-sp // (5120 if wide else 2560))
+
+
 def cfg5_system(oracle_lib, nk):
     """The oracle's PSF and DAS on the nk strongest nodes of cfg5's top bin (12 kHz, M = 128,
     201x201 grid): an S~ = nk system in cfg5's own geometry."""
@@ -90,8 +98,8 @@ def test_gs_large_systems(ctx, torch_cuda, oracle_lib, nk, sweeps, dense):
     st = ctx.stats()
     if dense:
         assert st["gs_kernel"] == 2 and st["gs_xtra_tiles"] > 0 and st["gs_max_group"] == 4
-    else:   # CTAs per bin: r of at most 2560 points per CTA
-        assert st["gs_kernel"] == 4 and st["gs_updates"] > 0 and st["gs_max_group"] == -(-((nk + 31) // 32 * 32) // 2560)
+    else:   # CTAs per bin: one up to 5120 points, else wide clusters of 5120 points per CTA
+        assert st["gs_kernel"] == 4 and st["gs_updates"] > 0 and st["gs_max_group"] == resid_ctas(nk, wide=True)
     assert x.min() >= 0
     assert rel_l2(x, ref) < TOL_X, rel_l2(x, ref)
     assert abs(x.sum() - ref.sum()) < TOL_P * ref.sum()
@@ -167,28 +175,30 @@ def _e2e(ctx, torch, oracle_lib, band, sweeps, full=False, dense=False):
     return st, nk
 
 
-def test_gs_residual_cluster_of_5(ctx, torch_cuda, oracle_lib):
-    """S~ = 12000 (12000 padded points: a cluster of 5 CTAs, 5 x 2400 columns of r) on the residual
-    kernel against the oracle."""
+def test_gs_residual_cluster_of_3(ctx, torch_cuda, oracle_lib):
+    """S~ = 12000 (12000 padded points: a wide cluster of 3 CTAs, 3 x 4000 columns of r) on the
+    residual kernel against the oracle."""
     torch = torch_cuda
     A, bt = cfg5_system(oracle_lib, 12000)
     ref = oracle_lib.gs(A, bt, 12)
     x = ctx.gs(torch.from_numpy(A.astype(np.float32)).cuda(), torch.from_numpy(bt).cuda(), 12,
                dense_stream=False).cpu().numpy()
     st = ctx.stats()
-    assert st["gs_kernel"] == 4 and st["gs_max_group"] == 5
+    assert st["gs_kernel"] == 4 and st["gs_max_group"] == 3
     assert x.min() >= 0
     assert rel_l2(x, ref) < TOL_X, rel_l2(x, ref)
     assert abs(x.sum() - ref.sum()) < TOL_P * ref.sum()
 
 
 def test_e2e_cfg5_mixed_cluster_classes(ctx, torch_cuda, oracle_lib):
-    """One cfg5 band whose systems need 1, 2 and 4 CTAs (S~ ~ 1.6k, 3.3k, 8.6k): one residual
-    launch per size class, the classes concurrently on forked streams, 20 sweeps."""
+    """One cfg5 band with three residual launch classes (S~ ~ 1.6k: one CTA; 3.3k: one CTA with
+    wide registers; 8.6k: a wide cluster of 2), the classes concurrently on forked streams, 20
+    sweeps."""
     band = synth.make_band("cfg5", bins=[300, 600, 1023])
     st, nk = _e2e(ctx, torch_cuda, oracle_lib, band, 20)
-    assert st["gs_kernel"] == 4 and st["gs_max_group"] == 4
-    assert sorted(-(-((int(v) + 31) // 32 * 32) // 2560) for v in nk) == [1, 2, 4]
+    assert st["gs_kernel"] == 4 and st["gs_max_group"] == 2
+    sps = sorted((int(v) + 31) // 32 * 32 for v in nk)
+    assert sps[0] <= 2560 < sps[1] <= 5120 < sps[2] and resid_ctas(nk.max(), wide=True) == 2
 
 
 @pytest.mark.parametrize("dense", [False, True], ids=["residual", "dense_stream"])
@@ -198,7 +208,7 @@ def test_e2e_cfg5_largest_bins(ctx, torch_cuda, oracle_lib, dense):
     st, nk = _e2e(ctx, torch_cuda, oracle_lib, band, 20, dense=dense)
     assert nk.min() > 6000
     assert st["gs_kernel"] == (2 if dense else 4)
-    assert dense or st["gs_max_group"] >= 3   # (the residual kernel's cluster mode)
+    assert dense or st["gs_max_group"] == 2   # (the residual kernel's wide cluster mode)
 
 
 @pytest.mark.parametrize("dense", [False, True], ids=["residual", "dense_stream"])
@@ -223,8 +233,8 @@ def test_e2e_cfg4_full_grid_defining_size(ctx, torch_cuda, oracle_lib, dense):
 
 def test_automatic_kernel_choice(ctx, torch_cuda, tmp_path):
     """Without a kernel flag the band's largest system picks the GS kernel: the residual kernel up
-    to 20480 padded points -- cfg3's compressed bins on one CTA each, a full-grid band of S = 4096
-    on clusters of 2 -- and above that the dense-stream cluster kernel (checked in a subprocess
+    to 20480 padded points -- cfg3's compressed bins on one CTA each, a full-grid band of S = 6400
+    on (narrow) clusters of 3 -- and above that the dense-stream cluster kernel (checked in a subprocess
     with the threshold lowered to 2048 by DWC_RGS_AUTO_MAX_SP: a full-grid band of S = 2209);
     both flags at once are rejected."""
     torch = torch_cuda
@@ -233,10 +243,10 @@ def test_automatic_kernel_choice(ctx, torch_cuda, tmp_path):
     cfg = band.cfg
     ctx.solve_band(geom_of(band), band.freqs, torch.from_numpy(band.csm).cuda(), cfg.epsilon, 5)
     assert ctx.stats()["gs_kernel"] == 4 and ctx.stats()["gs_max_group"] == 1
-    cfg4 = dataclasses.replace(synth.CONFIGS["cfg4"], n=64, n_bins=1)
+    cfg4 = dataclasses.replace(synth.CONFIGS["cfg4"], n=80, n_bins=1)
     b4 = synth.make_band(cfg4)
     ctx.solve_band(geom_of(b4), b4.freqs, torch.from_numpy(b4.csm).cuda(), cfg4.epsilon, 3, full_grid=True)
-    assert ctx.stats()["gs_kernel"] == 4 and ctx.stats()["gs_max_group"] == 2
+    assert ctx.stats()["gs_kernel"] == 4 and ctx.stats()["gs_max_group"] == 3
     script = _AUTO_SCRIPT.format(root=ROOT)
     env = dict(os.environ, DWC_RGS_AUTO_MAX_SP="2048")
     r = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=600)
@@ -286,7 +296,7 @@ def test_gs_large_alternating(ctx, torch_cuda, oracle_lib, dense):
     x = ctx.gs(torch.from_numpy(A.astype(np.float32)).cuda(), torch.from_numpy(bt).cuda(), 21, alt=True,
                dense_stream=dense).cpu().numpy()
     st = ctx.stats()
-    assert st["gs_kernel"] == (3 if dense else 4) and (dense or st["gs_max_group"] == 2)
+    assert st["gs_kernel"] == (3 if dense else 4) and (dense or st["gs_max_group"] == 1)
     assert x.min() >= 0
     assert rel_l2(x, ref) < TOL_X, rel_l2(x, ref)
     assert abs(x.sum() - ref.sum()) < TOL_P * ref.sum()
@@ -307,7 +317,7 @@ def test_gs_large_general_matrix(ctx, torch_cuda, oracle_lib):
     x = ctx.gs(torch.from_numpy(A.astype(np.float32)).cuda(), torch.from_numpy(bt).cuda(), 20,
                general=True).cpu().numpy()
     st = ctx.stats()
-    assert st["gs_kernel"] == 4 and st["gs_max_group"] == 2
+    assert st["gs_kernel"] == 4 and st["gs_max_group"] == 1   # (one CTA, wide registers)
     assert x.min() >= 0
     assert rel_l2(x, ref) < TOL_X, rel_l2(x, ref)
     assert abs(x.sum() - ref.sum()) < TOL_P * ref.sum()
