@@ -31,7 +31,7 @@
 //    (before the first visit: the rows with b > 0, exactly the rows sweep 1 changes).  The carries
 //    of a change outside the prediction are added after the block from global memory.
 //  * row producer (warp 6): the exact fp64 dx of every listed change; bulk copies of the rows of
-//    A~ (dense row-major) of every change into a 4-slot shared-memory ring, as batches.
+//    A~ (dense row-major) of every change into a 3-slot shared-memory ring, as batches.
 //  * stream (warps 0..3, 7; 128-column chunks owned by warps, so every element of r has one
 //    writer and a fixed update order): apply dx_c * A[c, :] (fp64) to r.  REGR (systems up to
 //    kRegMaxSp points): r in the stream warps' registers; after its step j the owner of a block
@@ -78,7 +78,7 @@ constexpr int kWSolver = 4, kWPanel = 5, kWRows = 6;
 #define RGS_NLIST 16
 #endif
 #ifndef RGS_NSLOT
-#define RGS_NSLOT 4
+#define RGS_NSLOT 3
 #endif
 constexpr int kRStg = RGS_STG;       // panel staging depth (steps)
 constexpr int kNP = RGS_NP;          // panels staged per step (predicted rows beyond: loaded on demand)
@@ -562,7 +562,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
             float carry[kRgsWin];
 #pragma unroll
             for (int d = 0; d < kRgsWin; d++) carry[d] = 0.f;
-            unsigned long long tt = 0, tsd = 0, tl = 0, tr = 0, nch = 0, nmiss = 0, e_sd = 0, e_l = 0, e_ch = 0, nzero = 0;
+            unsigned long long tt = 0, tsd = 0, tl = 0, tr = 0, nch = 0, nmiss = 0, e_sd = 0, e_l = 0, e_ch = 0, nzero = 0, nwait = 0;
             for (int s = 0, p = 0, pos = 0; s < total; s++, pos = (pos + 1 == T) ? 0 : pos + 1, p += (pos == 0)) {
                 const unsigned long long t0 = pf ? clk() : 0ull;
                 const bool fwd = sweep_fwd(p, alt);
@@ -696,6 +696,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                     tt += t1 - t0; tsd += t2 - t1; tl += t3 - t2; tr += clk() - t3;
                     if (10 * s < total) { e_sd += t2 - t1; e_l += t3 - t2; e_ch += q; }   // the first 10 % of the steps
                     nzero += (q == 0);
+                    nwait += (t2 - t1 > 100);
                 }
                 nch += q;
             }
@@ -703,7 +704,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 for (int s = max(0, total - kNList); s < total; s++) mbar_wait(&sh.sdone[s % kNList], (s / kNList) & 1);
             if (prof && lane == 0 && item < kProfItems) prof[kProfSlots + 4 * item + 3] = nch;
             if (pf && lane == 0) { prof[0] = tt; prof[1] = tsd; prof[2] = tl; prof[3] = tr; prof[4] = total; prof[5] = nch; prof[6] = nmiss;
-                                    prof[16] = e_sd; prof[17] = e_l; prof[18] = e_ch; prof[19] = nzero; }
+                                    prof[16] = e_sd; prof[17] = e_l; prof[18] = e_ch; prof[19] = nzero; prof[20] = nwait; }
           }
         } else if (REGR) {
             // ================= stream warps, r in registers (sp <= kRegMaxSp, whole rows in the
@@ -1116,8 +1117,8 @@ int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int m
                 grid, smem, kNSlot, slot_floats, h[4], h[5], h[5] / n, (double)h[14], h[0] / n, h[1] / n, h[2] / n, h[3] / n,
                 h[8] / n, h[9] / n, h[10] / n, h[11], h[12] / n, h[13] / n, h[6], h[7] / n, h[15] / n);
         fprintf(stderr, "[rgs-prof] first 10%% of the steps: stream wait %.0f, loop %.0f cyc/step, %.2f changes/step; "
-                        "steps without a change: %.1f %%\n",
-                h[16] / (0.1 * n), h[17] / (0.1 * n), h[18] / (0.1 * n), 100.0 * h[19] / n);
+                        "steps without a change: %.1f %%; stream waits over 100 cycles: %.1f %% of the steps\n",
+                h[16] / (0.1 * n), h[17] / (0.1 * n), h[18] / (0.1 * n), 100.0 * h[19] / n, 100.0 * h[20] / n);
         cudaFree(prof);
     }
     return e == cudaSuccess ? 1 : -1;
