@@ -502,7 +502,8 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
             }
         } else if (wid == kWRows) {
             // ================= row producer: the exact dx of every change (all lanes), then the rows
-            // of every step's changes into the ring (lane 0)
+            // of every step's changes into the ring (one bulk copy per lane: issued from one lane
+            // they took ~170 cycles each)
             unsigned long long tw = 0, ti = 0;
             int b = 0;   // global batch counter (ring slot = b % kNSlot)
             for (int s = 0; s < total; s++) {
@@ -512,40 +513,41 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 DWC_DCHECK(n >= 0 && n <= 32, "row producer: change-list length");
                 if (lane < n) sh.dxs[li][lane] = entry_dx(sh.list[li][lane]) * ((REGR && nonneg) ? kDxScale : 1.0);   // exact
                 __syncwarp();
-                if (lane == 0) {
-                    mbar_arrive(&sh.dxready[li]);
-                    const int nu = swid > 0 ? n * rg.nseg : 0;   // (a CTA without columns fetches nothing)
-                    for (int u0 = 0; u0 < nu; u0 += rg.upb, b++) {
-                        const int h = b % kNSlot;
-                        const unsigned long long t0 = pf ? clk() : 0ull;
+                if (lane == 0) mbar_arrive(&sh.dxready[li]);
+                const int nu = swid > 0 ? n * rg.nseg : 0;   // (a CTA without columns fetches nothing)
+                for (int u0 = 0; u0 < nu; u0 += rg.upb, b++) {
+                    const int h = b % kNSlot;
+                    const unsigned long long t0 = pf ? clk() : 0ull;
+                    const int nb = min(rg.upb, nu - u0);
+                    float *dst = ring + (size_t)h * slot_floats;
+                    if (lane == 0) {
                         mbar_wait(&sh.rempty[h], ((b / kNSlot) & 1) ^ 1);
-                        const unsigned long long t1 = pf ? clk() : 0ull;
-                        const int nb = min(rg.upb, nu - u0);
                         DWC_DCHECK(h < kNSlot && nb >= 1 && (rg.nseg > 1 || nb * rstride <= slot_floats) &&
                                        (rg.nseg == 1 || nb * rg.seg <= slot_floats),
                                    "row producer: ring slot overflow");
-                        float *dst = ring + (size_t)h * slot_floats;
-                        if (rg.nseg == 1) {   // whole rows (CLU: this CTA's slice of them)
-                            mbar_expect_tx(&sh.rfull[h], (uint32_t)nb * swid * 4);
-                            for (int j = 0; j < nb; j++)
-                                bulk_g2s(dst + (size_t)j * rstride, Ad + (size_t)sh.list[li][u0 + j].c * sp + col0,
-                                         (uint32_t)swid * 4, &sh.rfull[h]);
-                        } else {
-                            uint32_t bytes = 0;
-                            for (int j = 0; j < nb; j++) {
-                                const int u = u0 + j, e = u / rg.nseg, g = u - e * rg.nseg;
-                                bytes += (uint32_t)min(rg.seg, sp - g * rg.seg) * 4;
-                            }
-                            mbar_expect_tx(&sh.rfull[h], bytes);
-                            for (int j = 0; j < nb; j++) {
-                                const int u = u0 + j, e = u / rg.nseg, g = u - e * rg.nseg;
-                                const int c = sh.list[li][e].c;
-                                bulk_g2s(dst + (size_t)j * rg.seg, Ad + (size_t)c * sp + (size_t)g * rg.seg,
-                                         (uint32_t)min(rg.seg, sp - g * rg.seg) * 4, &sh.rfull[h]);
-                            }
-                        }
-                        if (pf) { tw += t1 - t0; ti += clk() - t1; }
                     }
+                    const unsigned long long t1 = pf ? clk() : 0ull;
+                    if (rg.nseg == 1) {   // whole rows (CLU: this CTA's slice of them), one copy per lane
+                        if (lane == 0) mbar_expect_tx(&sh.rfull[h], (uint32_t)nb * swid * 4);
+                        __syncwarp();   // (the slot is free: every lane's copy may start)
+                        if (lane < nb)
+                            bulk_g2s(dst + (size_t)lane * rstride, Ad + (size_t)sh.list[li][u0 + lane].c * sp + col0,
+                                     (uint32_t)swid * 4, &sh.rfull[h]);
+                    } else if (lane == 0) {
+                        uint32_t bytes = 0;
+                        for (int j = 0; j < nb; j++) {
+                            const int u = u0 + j, e = u / rg.nseg, g = u - e * rg.nseg;
+                            bytes += (uint32_t)min(rg.seg, sp - g * rg.seg) * 4;
+                        }
+                        mbar_expect_tx(&sh.rfull[h], bytes);
+                        for (int j = 0; j < nb; j++) {
+                            const int u = u0 + j, e = u / rg.nseg, g = u - e * rg.nseg;
+                            const int c = sh.list[li][e].c;
+                            bulk_g2s(dst + (size_t)j * rg.seg, Ad + (size_t)c * sp + (size_t)g * rg.seg,
+                                     (uint32_t)min(rg.seg, sp - g * rg.seg) * 4, &sh.rfull[h]);
+                        }
+                    }
+                    if (pf) { tw += t1 - t0; ti += clk() - t1; }
                 }
                 __syncwarp();
             }
