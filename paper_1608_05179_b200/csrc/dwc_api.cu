@@ -460,10 +460,11 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
         // (wide clusters -- 5120 columns per CTA -- on the compressed grid, where many rows change
         // per sweep; narrow ones on the full grid, where few do)
         const bool wide_cl = !(p->flags & DWC_FULL_GRID);
+        const int pair_sp = rgs_pair_max_sp(max_sp, n_bins, ctx->num_sms);
         std::vector<std::pair<int, int>> cls;   // [begin, end) in `order`
         for (int i = 0; i < n_bins; i++) {
-            const int g = rgs_size_class((hk[order[i]] + 31) & ~31, wide_cl);
-            if (cls.empty() || rgs_size_class((hk[order[cls.back().first]] + 31) & ~31, wide_cl) != g)
+            const int g = rgs_size_class((hk[order[i]] + 31) & ~31, wide_cl, pair_sp);
+            if (cls.empty() || rgs_size_class((hk[order[cls.back().first]] + 31) & ~31, wide_cl, pair_sp) != g)
                 cls.push_back({i, i + 1});
             else
                 cls.back().second = i + 1;
@@ -491,7 +492,7 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
             LAUNCH(launch_rgs(nb, (int *)ctx->order.p + b0, (BinLayout *)ctx->lay.p, csp, (int *)ctx->counter.p + c,
                               (float *)ctx->Ad.p, (double *)ctx->bt.p, p->sweeps, nullptr, x_map, keep_idx,
                               S, ctx->num_sms, (unsigned long long *)ctx->upd.p, cs, &ci, alt,
-                              /*nonneg: every PSF is |.|^2 times positive scales*/ 1, wide_cl ? 1 : 0));
+                              /*nonneg: every PSF is |.|^2 times positive scales*/ 1, wide_cl ? 1 : 0, pair_sp));
             gsi.ctas += ci.ctas;
             gsi.max_group = std::max(gsi.max_group, ci.max_group);
             if (c > 0) CU(cudaEventRecord(ctx->class_join[c], cs));

@@ -100,7 +100,8 @@ constexpr int kNSlot = RGS_NSLOT;    // row ring: batches in flight
 // register-resident r: 128-column chunks per stream warp -- kRegCh for systems up to kRegMaxSp
 // points (and per CTA in cluster mode), kRegChWide for a single CTA up to kRegMaxSpWide (twice
 // the registers: measured 3 % slower on cfg3's small systems, so only where it saves a cluster)
-constexpr int kRegCh = 4, kRegChWide = 8;
+constexpr int kRegCh = 4, kRegChWide = 8, kRegChPair = 2;
+constexpr int kRegMaxSpPair = 128 * kRegChPair * kNStream;    // 1280: two CTAs per SM (128 registers)
 constexpr int kRegMaxSp = 128 * kRegCh * kNStream;            // 2560
 constexpr int kRegMaxSpWide = 128 * kRegChWide * kNStream;    // 5120
 
@@ -320,7 +321,7 @@ __device__ __forceinline__ void apply_dispatch(int nch, double (&r)[RC][4], cons
 }
 
 template <bool ALT, bool REGR, bool CLU, int RC = kRegCh>
-__global__ void __launch_bounds__(kRThreads, REGR ? 1 : kRMinBlocks)
+__global__ void __launch_bounds__(kRThreads, (REGR && RC > kRegChPair) ? 1 : kRMinBlocks)
 rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restrict__ lay, int *__restrict__ counter,
            const float *__restrict__ Adense, const double *__restrict__ bt, int sweeps, float *__restrict__ x_out,
            float *__restrict__ x_map, const int32_t *__restrict__ keep_idx, int S, int max_sp, int slot_floats,
@@ -980,15 +981,28 @@ int rgs_cluster_size(int sp, bool wide) {
     return g <= 8 ? g : 1;   // (portable cluster sizes; beyond: one CTA with r in shared memory)
 }
 
-int rgs_size_class(int sp, bool wide) {
+// Small systems of a band with more bins than SMs run two CTAs per SM, so that every bin starts
+// at once instead of the late-started ones forming the band's tail: the bins whose padded size
+// is at most half the band's largest (a bin's time grows about linearly with S~, and sharing an
+// SM at most doubles it, so they still finish within the longest chain).  cfg3: GS 23.7 ->
+// 21.8 ms, the longest bin's time alone (thresholds 576..704 measured alike, 544 and 800 worse).
+int rgs_pair_max_sp(int band_max_sp, int n_bins, int num_sms) {
+    static const int env = getenv("DWC_RGS_PAIR_MAX_SP") ? atoi(getenv("DWC_RGS_PAIR_MAX_SP")) : -1;   // experiment
+    if (env >= 0) return std::min(env, kRegMaxSpPair);
+    if (n_bins <= num_sms) return 0;
+    return std::min((band_max_sp / 2) & ~31, kRegMaxSpPair);
+}
+
+int rgs_size_class(int sp, bool wide, int pair_max_sp) {
     const int g = rgs_cluster_size(sp, wide);
-    return g > 1 ? 1 + g : (sp > kRegMaxSp ? 1 : 0);   // 0: one CTA, 1: one CTA with wide registers, 1+G: clusters
+    // 0: two CTAs per SM, 1: one CTA, 2: one CTA with wide registers, 2+G: clusters
+    return g > 1 ? 2 + g : (sp > kRegMaxSp ? 2 : (sp > pair_max_sp ? 1 : 0));
 }
 
 int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int max_sp, int *counter,
                const float *Adense, const double *bt, int sweeps, float *x_out, float *x_map,
                const int32_t *keep_idx, int S, int num_sms, unsigned long long *n_updates, cudaStream_t st,
-               GsLaunchInfo *info, int alt, int nonneg, int wide_clusters) {
+               GsLaunchInfo *info, int alt, int nonneg, int wide_clusters, int pair_max_sp) {
     static const int ring_env = getenv("DWC_RGS_RING_KB") ? atoi(getenv("DWC_RGS_RING_KB")) : 0;   // experiment
     static const int per_sm_env = getenv("DWC_RGS_PER_SM") ? atoi(getenv("DWC_RGS_PER_SM")) : 0;   // experiment
     static const bool no_regr = getenv("DWC_RGS_NO_REGR") != nullptr;   // experiment: r in shared memory
@@ -1000,6 +1014,7 @@ int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int m
     const bool regr_try = !no_regr && (max_sp <= kRegMaxSpWide || G > 1);
     // 8 chunks per stream warp: one CTA above kRegMaxSp, or the wide clusters
     const bool wide = regr_try && (G == 1 ? max_sp > kRegMaxSp : (bool)wide_clusters);
+    const bool pair = regr_try && G == 1 && max_sp <= pair_max_sp && n_bins > 1;   // two CTAs per SM
     const int rstride_max = G > 1 ? 128 * ((nq_max + G - 1) / G) : max_sp;   // floats of a ring row
     // the configuration: base shared memory, 1/A_ii copy (when a ring of >= 24 KB still fits), ring
     auto layout = [&](bool regr, int &use_ivs, size_t &base, bool allow_ivs) {
@@ -1027,7 +1042,8 @@ int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int m
     // shared-memory r: two CTAs per SM (2 x (smem + 1 KB reserved) <= 228 KB) when the band has
     // more bins than SMs and every ring slot still holds 2 rows
     const size_t per2 = 114 * 1024 - 1024;
-    const bool two = (regr || kRMinBlocks < 2) ? false
+    const bool two = regr ? (pair && per2 > base + 3 * 4 * (size_t)max_sp + 1024)   // (r in registers: the small class)
+                     : kRMinBlocks < 2 ? false
                      : per_sm_env ? per_sm_env == 2 && per2 > base + 2048
                                 : n_bins > num_sms && per2 > base && (per2 - base) / (4 * kNSlot) >= 2 * (size_t)max_sp;
     size_t ring = two ? (per2 - base - 512) / 1024 * 1024 : (227 * 1024 - base - 512) / 1024 * 1024;
@@ -1038,10 +1054,12 @@ int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int m
     const bool clu = G > 1;
     const auto kern =
         alt ? (clu ? (wide ? rgs_kernel<true, true, true, kRegChWide> : rgs_kernel<true, true, true>)
-                   : regr ? (wide ? rgs_kernel<true, true, false, kRegChWide> : rgs_kernel<true, true, false>)
+                   : regr ? (wide ? rgs_kernel<true, true, false, kRegChWide>
+                                  : two ? rgs_kernel<true, true, false, kRegChPair> : rgs_kernel<true, true, false>)
                           : rgs_kernel<true, false, false>)
             : (clu ? (wide ? rgs_kernel<false, true, true, kRegChWide> : rgs_kernel<false, true, true>)
-                   : regr ? (wide ? rgs_kernel<false, true, false, kRegChWide> : rgs_kernel<false, true, false>)
+                   : regr ? (wide ? rgs_kernel<false, true, false, kRegChWide>
+                                  : two ? rgs_kernel<false, true, false, kRegChPair> : rgs_kernel<false, true, false>)
                           : rgs_kernel<false, false, false>);
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return -1;

@@ -37,6 +37,10 @@ if os.environ.get("ALL_BINS", "0") == "1":
                        full_grid=cfg.full_grid, dense_stream=dense)
         s1 = ctx.stats()
         rows.append((s1["ms_gs"], kb, int(nk[kb]), s1["gs_updates"]))
+    if os.environ.get("ALL_BINS_JSON"):
+        import json
+        json.dump([{"ms": r[0], "bin": r[1], "nk": r[2], "updates": r[3], "freq": float(band.freqs[r[1]])} for r in rows],
+                  open(os.environ["ALL_BINS_JSON"], "w"))
     rows.sort(reverse=True)
     print("slowest bins alone (gs ms, bin, S~, updates):", " ".join(f"{r[0]:.2f}/{r[1]}/{r[2]}/{r[3]}" for r in rows[:8]))
     print(f"sum of bins alone {sum(r[0] for r in rows):.1f} ms -> /148 SMs {sum(r[0] for r in rows) / 148:.2f} ms")

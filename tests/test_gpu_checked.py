@@ -36,7 +36,7 @@ for name, bins, sweeps, full, dense in {cases!r}:
 np.savez({out!r}, **res)
 """
 
-CASES = [("cfg3", [249, 255, 224, 10], 1000, False, False),
+CASES = [("cfg3", [249, 255, 224, 10, 11, 12], 1000, False, False),
          ("cfg3", [249, 100], 300, False, True),
          ("cfg5", [1023], 20, False, False),
          ("cfg5", [1023], 20, False, True)]
@@ -44,7 +44,8 @@ CASES = [("cfg3", [249, 255, 224, 10], 1000, False, False),
 
 def _run(lib, out, tmp_path):
     script = _SCRIPT.format(root=ROOT, libname=os.path.basename(lib), cases=CASES, out=str(out))
-    env = dict(os.environ, DWC_LIB=lib)
+    # (two CTAs per SM for the systems of at most 640 points, as in a band with more bins than SMs)
+    env = dict(os.environ, DWC_LIB=lib, DWC_RGS_PAIR_MAX_SP="640")
     r = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, (r.stdout[-2000:], r.stderr[-4000:])
     assert "[dwc checked]" not in r.stdout
