@@ -348,6 +348,8 @@ def test_full_size_cfg3_sampled(ctx, torch_cuda, oracle_lib, dense):
     g = geom_of(band)
     out = ctx.solve_band(g, band.freqs, torch.from_numpy(band.csm).cuda(), cfg.epsilon, cfg.sweeps,
                          dense_stream=dense)
+    if not dense:   # more bins than SMs: the systems of at most half the largest size ran two per SM
+        assert ctx.stats()["gs_kernel"] == 4 and ctx.stats()["gs_ctas"] > 148
     nk = out["n_keep"].cpu().numpy()
     keep = out["keep_idx"].cpu().numpy()
     x = out["x_map"].cpu().numpy()
