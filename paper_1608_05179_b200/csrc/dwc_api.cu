@@ -483,9 +483,25 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
             CU(cudaEventRecord(ctx->class_fork, st));
         }
         gsi = GsLaunchInfo{DWC_GS_KERNEL_RESIDUAL, 0, 0, 1};
+        // every forked stream joins back into the call's stream, also when a launch fails midway
+        // (no work of this call may outlive it on a stream the caller does not see)
+        struct Join {
+            dwc_ctx *ctx;
+            cudaStream_t st;
+            int forked = 0;
+            ~Join() {
+                for (int c = 1; c <= forked; c++) {
+                    cudaEventRecord(ctx->class_join[c], ctx->class_st[c]);
+                    cudaStreamWaitEvent(st, ctx->class_join[c], 0);
+                }
+            }
+        } join{ctx, st};
         for (int c = 0; c < ncls; c++) {
             cudaStream_t cs = c == 0 ? st : ctx->class_st[c];
-            if (c > 0) CU(cudaStreamWaitEvent(cs, ctx->class_fork, 0));
+            if (c > 0) {
+                CU(cudaStreamWaitEvent(cs, ctx->class_fork, 0));
+                join.forked = c;
+            }
             const int b0 = cls[c].first, nb = cls[c].second - cls[c].first;
             const int csp = (hk[order[b0]] + 31) & ~31;   // the class's largest system
             GsLaunchInfo ci;
@@ -495,9 +511,7 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
                               /*nonneg: every PSF is |.|^2 times positive scales*/ 1, wide_cl ? 1 : 0, pair_sp));
             gsi.ctas += ci.ctas;
             gsi.max_group = std::max(gsi.max_group, ci.max_group);
-            if (c > 0) CU(cudaEventRecord(ctx->class_join[c], cs));
         }
-        for (int c = 1; c < ncls; c++) CU(cudaStreamWaitEvent(st, ctx->class_join[c], 0));
     } else if (p->flags & DWC_ALT_SWEEPS) {
         gsi.kernel = DWC_GS_KERNEL_ALT;
         gsi.ctas = n_bins;
