@@ -321,3 +321,40 @@ def test_gs_large_general_matrix(ctx, torch_cuda, oracle_lib):
     assert x.min() >= 0
     assert rel_l2(x, ref) < TOL_X, rel_l2(x, ref)
     assert abs(x.sum() - ref.sum()) < TOL_P * ref.sum()
+
+
+_SMEM_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+from paper_1608_05179_b200 import Context
+c = Context(0)
+out = {{}}
+for name, alt in (("fwd", False), ("alt", True)):
+    A = np.load({a!r}); b = np.load({b!r})
+    x = c.gs(torch.from_numpy(A).cuda(), torch.from_numpy(b).cuda(), 15, alt=alt, dense_stream=False).cpu().numpy()
+    out[name] = x
+    out[name + "_k"] = np.array([c.stats()["gs_kernel"], c.stats()["gs_max_group"]])
+np.savez({o!r}, **out)
+"""
+
+
+def test_gs_residual_shared_memory_path(oracle_lib, tmp_path):
+    """The residual kernel with r in shared memory (the path for systems whose rows do not fit a
+    ring slot; forced here by DWC_RGS_NO_REGR in a separate process): an S~ = 2100 system,
+    forward and alternating sweeps, against the oracle."""
+    A, bt = cfg5_system(oracle_lib, 2100)
+    pa, pb, po = tmp_path / "A.npy", tmp_path / "b.npy", tmp_path / "x.npz"
+    np.save(pa, A.astype(np.float32))
+    np.save(pb, bt)
+    script = _SMEM_SCRIPT.format(root=ROOT, a=str(pa), b=str(pb), o=str(po))
+    env = dict(os.environ, DWC_RGS_NO_REGR="1")
+    r = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    res = np.load(po)
+    for name, alt in (("fwd", False), ("alt", True)):
+        assert list(res[name + "_k"]) == [4, 1]
+        ref = oracle_lib.gs(A, bt, 15, alt=alt)
+        x = res[name]
+        assert x.min() >= 0
+        assert rel_l2(x, ref) < TOL_X, (name, rel_l2(x, ref))
+        assert abs(x.sum() - ref.sum()) < TOL_P * ref.sum()
