@@ -9,8 +9,8 @@ run cfg3_alt --alt
 run cfg3_paper --paper
 run cfg3_snap --input snapshots
 run cfg3_dense_kernel --kernel dense
-run cfg4 --config cfg4 --steps 2 --warmup 3 --no-cvf
-run cfg5 --config cfg5 --steps 2 --warmup 3 --no-cvf
+run cfg4 --config cfg4 --steps 2 --warmup 3 --no-cvf --no-pipeline
+run cfg5 --config cfg5 --steps 2 --warmup 3 --no-cvf --no-pipeline
 # ncu capture of the residual kernel's cluster mode on cfg4 (full grid): DRAM bytes per launch
 CMD4="python bench.py --config cfg4 --steps 1 --warmup 1 --no-cpu-baseline --no-cvf"
 timeout 900 $CMD4 > gpurun_out/plain4.log 2>&1 && \

@@ -265,7 +265,10 @@ class Band:
     bins: np.ndarray           # which bins of the config these are
 
 
-def make_band(cfg: Config | str, seed: int = 0, bins: Optional[Sequence[int]] = None) -> Band:
+def make_band(cfg: Config | str, seed: int = 0, bins: Optional[Sequence[int]] = None, block: int = 0) -> Band:
+    """The config's band of bins.  block > 0: another measurement block of the same scene (new
+    snapshot and noise draws; the exact-CSM configs have no draws, so their block is the band
+    itself)."""
     if isinstance(cfg, str):
         cfg = CONFIGS[cfg]
     mics = cfg.mics()
@@ -279,7 +282,8 @@ def make_band(cfg: Config | str, seed: int = 0, bins: Optional[Sequence[int]] = 
         if cfg.csm == "exact":
             csm[j] = csm_exact(mics, src_xyz, src_pow, f, cfg.c0)
         else:
-            rng = np.random.default_rng(np.random.SeedSequence([cfg.cfg_id, seed, int(k)]))
+            key = [cfg.cfg_id, seed, int(k)] + ([int(block)] if block else [])
+            rng = np.random.default_rng(np.random.SeedSequence(key))
             csm[j] = csm_sampled(mics, src_xyz, src_pow, f, cfg.c0, cfg.snapshots, cfg.snr_db, rng)
     return Band(cfg, mics, allf[bins].copy(), csm, src_idx, src_pow, bins)
 
