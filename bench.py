@@ -262,14 +262,25 @@ def run_pipelined(args, cfg, band, geom, ctx, dev, world, rank, strong, flush, g
             with torch.cuda.stream(sts[j]):
                 mask = ctxs[j].keep_mask(o["n_keep"], o["keep_idx"], stream=sts[j])
                 gather_band(o["x_map"], o["n_keep"], mask, cfg.n_bins)
-    def drun(first, last):   # one host thread per context (each call blocks once, for S~)
-        ths = [th.Thread(target=lambda j=j: [dstep(i) for i in range(first + j, last, 2)]) for j in (0, 1)]
+    def drun(first, last):
+        # one host thread per context, each waiting for its band before it starts its next one:
+        # at most two bands in flight, the next band's DAS / compress / PSF taking the SMs the
+        # previous band's sweeps free.  (Bands queued without that wait -- one host thread, the
+        # calls return once the sweeps are launched -- overlapped unevenly: 9.6-11.9 k bins/s
+        # from run to run against 11.9 k steady here.)
+        def worker(j):
+            for i in range(first + j, last, 2):
+                dstep(i)
+                sts[j].synchronize()
+        if strong:   # (the collectives must be issued in the same order on every rank: one thread)
+            for i in range(first, last):
+                dstep(i)
+            return
+        ths = [th.Thread(target=worker, args=(j,)) for j in (0, 1)]
         for t_ in ths:
             t_.start()
         for t_ in ths:
             t_.join()
-    if strong:   # (the collectives must be issued in the same order on every rank: one thread)
-        drun = lambda first, last: [dstep(i) for i in range(first, last)]   # noqa: E731
     drun(0, W)
     torch.cuda.synchronize(dev)
     ms_dev = timed(lambda: drun(W, n))
@@ -298,7 +309,8 @@ def run_pipelined(args, cfg, band, geom, ctx, dev, world, rank, strong, flush, g
     mb = sum(p_.csm.nbytes for p_ in pool[W:n]) / 1e6
     return {"ms_per_step": ms_dev, "e2e_ms_per_step": ms_host if ms_host is not None else float("nan"),
             "desc": ("consecutive bands (new measurement blocks of the same scene) on 2 contexts and 2 streams, one "
-                     "host thread per context: a band's DAS/compress/PSF overlap the previous band's Gauss-Seidel tail"),
+                     "host thread per context waiting for its band before the next: at most two bands in flight, a "
+                     "band's DAS/compress/PSF overlapping the previous band's Gauss-Seidel tail"),
             "l2": (f"none between steps: each of the {K} timed steps reads its own band ({mb:.0f} MB of CSMs in "
                    f"all, never re-read); 256 MiB write before the timed region")}
 
