@@ -215,8 +215,9 @@ def run_pipelined(args, cfg, band, geom, ctx, dev, world, rank, strong, flush, g
         return synth.make_band(cfg, seed=seed0 + 1000 * (j + 1) if exact else seed0, bins=band.bins, block=0 if exact else j + 1)
     with ThreadPoolExecutor(8) as ex:
         pool = list(ex.map(mk, range(2 * n)))   # device path: bands 0..n-1; host path: n..2n-1
-    ctxs = [ctx, Context(dev.index)]
-    sts = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    nc = args.contexts   # bands in flight
+    ctxs = [ctx] + [Context(dev.index) for _ in range(nc - 1)]
+    sts = [torch.cuda.Stream(dev) for _ in range(nc)]
     nb, S = len(band.freqs), cfg.S
     kw = dict(full_grid=cfg.full_grid, order=args.order, dr=args.dr, alt=args.alt, paper=args.paper,
               dense_stream=KERNEL_FLAG[args.kernel])
@@ -252,10 +253,10 @@ def run_pipelined(args, cfg, band, geom, ctx, dev, world, rank, strong, flush, g
 
     # device path: inputs resident in HBM
     csm_dev = [torch.from_numpy(pool[i].csm).to(dev) for i in range(n)]
-    dout = [outs(True), outs(True)]
+    dout = [outs(True) for _ in range(nc)]
 
     def dstep(i):
-        j = i % 2
+        j = i % nc
         o = ctxs[j].solve_band(geom, pool[i].freqs, csm_dev[i], cfg.epsilon, cfg.sweeps, cfg.eps_mode,
                                out=dout[j], stream=sts[j], **kw)
         if strong:
@@ -269,14 +270,14 @@ def run_pipelined(args, cfg, band, geom, ctx, dev, world, rank, strong, flush, g
         # calls return once the sweeps are launched -- overlapped unevenly: 9.6-11.9 k bins/s
         # from run to run against 11.9 k steady here.)
         def worker(j):
-            for i in range(first + j, last, 2):
+            for i in range(first + j, last, nc):
                 dstep(i)
                 sts[j].synchronize()
         if strong:   # (the collectives must be issued in the same order on every rank: one thread)
             for i in range(first, last):
                 dstep(i)
             return
-        ths = [th.Thread(target=worker, args=(j,)) for j in (0, 1)]
+        ths = [th.Thread(target=worker, args=(j,)) for j in range(nc)]
         for t_ in ths:
             t_.start()
         for t_ in ths:
@@ -288,16 +289,16 @@ def run_pipelined(args, cfg, band, geom, ctx, dev, world, rank, strong, flush, g
     # host path: one host thread per context (the host call returns with the outputs in host
     # memory), CSMs from pinned host memory
     csm_host = [torch.from_numpy(pool[n + i].csm).pin_memory() for i in range(n)]
-    hout = [outs(False), outs(False)]
+    hout = [outs(False) for _ in range(nc)]
 
     def hstep(i):
-        j = i % 2
+        j = i % nc
         ctxs[j].solve_band_host(geom, pool[n + i].freqs, csm_host[i], cfg.epsilon, cfg.sweeps, cfg.eps_mode,
                                 cfg.full_grid, out=hout[j], stream=sts[j], order=args.order, dr=args.dr,
                                 alt=args.alt, paper=args.paper, dense_stream=KERNEL_FLAG[args.kernel])
 
     def hrun(first, last):
-        ths = [th.Thread(target=lambda j=j: [hstep(i) for i in range(first + j, last, 2)]) for j in (0, 1)]
+        ths = [th.Thread(target=lambda j=j: [hstep(i) for i in range(first + j, last, nc)]) for j in range(nc)]
         for t_ in ths:
             t_.start()
         for t_ in ths:
@@ -305,7 +306,8 @@ def run_pipelined(args, cfg, band, geom, ctx, dev, world, rank, strong, flush, g
     hrun(0, W)
     torch.cuda.synchronize(dev)
     ms_host = timed(lambda: hrun(W, n)) if not strong else None
-    ctxs[1].close()
+    for c_ in ctxs[1:]:
+        c_.close()
     mb = sum(p_.csm.nbytes for p_ in pool[W:n]) / 1e6
     return {"ms_per_step": ms_dev, "e2e_ms_per_step": ms_host if ms_host is not None else float("nan"),
             "desc": ("consecutive bands (new measurement blocks of the same scene) on 2 contexts and 2 streams, one "
@@ -598,6 +600,7 @@ def main():
                     help="Gauss-Seidel kernel: automatic by system size (default), residual, dense-stream")
     ap.add_argument("--order", type=int, default=1, choices=[1, 3],
                     help="S3 predictor: 1 linear (reading R7, default), 3 cubic (R19)")
+    ap.add_argument("--contexts", type=int, default=2, help="pipelined: bands in flight (contexts / streams / host threads)")
     ap.add_argument("--no-pipeline", dest="pipeline", action="store_false",
                     help="time one band at a time only (default: consecutive bands on two contexts and streams)")
     args = ap.parse_args()
