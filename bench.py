@@ -255,8 +255,7 @@ def run_pipelined(args, cfg, band, geom, ctx, dev, world, rank, strong, flush, g
     csm_dev = [torch.from_numpy(pool[i].csm).to(dev) for i in range(n)]
     dout = [outs(True) for _ in range(nc)]
 
-    def dstep(i):
-        j = i % nc
+    def dstep(i, j):   # band i on context / stream j
         o = ctxs[j].solve_band(geom, pool[i].freqs, csm_dev[i], cfg.epsilon, cfg.sweeps, cfg.eps_mode,
                                out=dout[j], stream=sts[j], **kw)
         if strong:
@@ -271,34 +270,57 @@ def run_pipelined(args, cfg, band, geom, ctx, dev, world, rank, strong, flush, g
         # from run to run against 11.9 k steady here.)
         def worker(j):
             for i in range(first + j, last, nc):
-                dstep(i)
+                t0 = time.perf_counter()
+                if trace is not None:
+                    ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    ea.record(sts[j])
+                    wb = ctxs[j].workspace_bytes()
+                dstep(i, j)
+                t1 = time.perf_counter()
+                if trace is not None:
+                    eb.record(sts[j])
                 sts[j].synchronize()
+                if trace is not None:
+                    trace.append((j, i, t0, t1, time.perf_counter(), ea.elapsed_time(eb),
+                                  ctxs[j].workspace_bytes() - wb, float(dout[j]["x_map"].double().sum())))
         if strong:   # (the collectives must be issued in the same order on every rank: one thread)
             for i in range(first, last):
-                dstep(i)
+                dstep(i, (i - first) % nc)
             return
         ths = [th.Thread(target=worker, args=(j,)) for j in range(nc)]
         for t_ in ths:
             t_.start()
         for t_ in ths:
             t_.join()
+    trace = [] if os.environ.get("DWC_BENCH_TRACE") else None
     drun(0, W)
     torch.cuda.synchronize(dev)
+    if trace is not None:
+        trace.clear()
     ms_dev = timed(lambda: drun(W, n))
+    if trace:   # (diagnostic: host-side band start / call return / band done, ms from the first)
+        for i in range(W, n):
+            o = ctxs[0].solve_band(geom, pool[i].freqs, csm_dev[i], cfg.epsilon, cfg.sweeps, cfg.eps_mode, **kw)
+            torch.cuda.synchronize(dev)
+            print(f"alone band {i}: sum x {float(o['x_map'].double().sum())!r}", file=sys.stderr)
+        t00 = min(x[2] for x in trace)
+        for j, i, t0, t1, t2, dev_ms, grow, xs in sorted(trace, key=lambda x: x[2]):
+            print(f"trace ctx {j} band {i}: start {1e3 * (t0 - t00):8.2f} ret {1e3 * (t1 - t00):8.2f} "
+                  f"done {1e3 * (t2 - t00):8.2f} device {dev_ms:7.2f} ms, workspace +{grow} B, sum x {xs!r}",
+                  file=sys.stderr)
 
     # host path: one host thread per context (the host call returns with the outputs in host
     # memory), CSMs from pinned host memory
     csm_host = [torch.from_numpy(pool[n + i].csm).pin_memory() for i in range(n)]
     hout = [outs(False) for _ in range(nc)]
 
-    def hstep(i):
-        j = i % nc
+    def hstep(i, j):
         ctxs[j].solve_band_host(geom, pool[n + i].freqs, csm_host[i], cfg.epsilon, cfg.sweeps, cfg.eps_mode,
                                 cfg.full_grid, out=hout[j], stream=sts[j], order=args.order, dr=args.dr,
                                 alt=args.alt, paper=args.paper, dense_stream=KERNEL_FLAG[args.kernel])
 
     def hrun(first, last):
-        ths = [th.Thread(target=lambda j=j: [hstep(i) for i in range(first + j, last, nc)]) for j in range(nc)]
+        ths = [th.Thread(target=lambda j=j: [hstep(i, j) for i in range(first + j, last, nc)]) for j in range(nc)]
         for t_ in ths:
             t_.start()
         for t_ in ths:

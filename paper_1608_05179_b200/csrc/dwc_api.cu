@@ -7,13 +7,30 @@
 #include <string.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <numeric>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "dwc_internal.cuh"
 
 using namespace dwc;
+
+cudaError_t dwc::raise_smem_limit(const void *fn, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void *>, size_t> set;   // (device, kernel) -> limit set
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    size_t &cur = set[{dev, fn}];
+    if (bytes <= cur) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) cur = bytes;
+    return e;
+}
 
 namespace {
 
@@ -102,7 +119,10 @@ namespace {
 
 dwc_status ensure(dwc_ctx *ctx, DevBuf &b, size_t bytes) {
     if (bytes <= b.bytes) return DWC_OK;
-    bytes = std::max(bytes, b.bytes + b.bytes / 4);  // grow geometrically
+    // 25 % headroom, also on the first allocation: consecutive bands' sizes differ by a few per
+    // cent (the kept counts), and a regrowth costs a device-wide synchronisation (cudaFree), which
+    // stalls every other context's work on the device too
+    bytes = std::max(bytes + bytes / 4, b.bytes + b.bytes / 4);
     if (b.p) {
         CU(cudaDeviceSynchronize());
         CU(cudaFree(b.p));
@@ -122,7 +142,7 @@ dwc_status ensure(dwc_ctx *ctx, DevBuf &b, size_t bytes) {
 
 dwc_status ensure_pin(PinBuf &b, size_t bytes) {
     if (bytes <= b.bytes) return DWC_OK;
-    bytes = std::max(bytes, (size_t)64 << 10);
+    bytes = std::max(bytes + bytes / 4, (size_t)64 << 10);   // (headroom: see ensure)
     if (b.p) CU(cudaFreeHost(b.p));
     b.p = nullptr;
     b.bytes = 0;

@@ -25,6 +25,17 @@
 
 namespace dwc {
 
+// Raise a kernel's dynamic shared-memory limit (cudaFuncAttributeMaxDynamicSharedMemorySize) on
+// the current device to at least `bytes` (dwc_api.cu).  The attribute belongs to the function and
+// device, not to the context or stream: two host threads driving two contexts set it concurrently,
+// and a plain set to each call's own need could lower it under the other thread's launch (which
+// then fails with cudaErrorInvalidValue).  It is only ever raised, under a lock.
+cudaError_t raise_smem_limit(const void *fn, size_t bytes);
+template <typename F>
+inline cudaError_t raise_smem_limit(F *fn, size_t bytes) {
+    return raise_smem_limit((const void *)fn, bytes);
+}
+
 // Scan-grid + array geometry as the kernels see it (all fp64, device pointers).
 struct Geo {
     int m;          // microphones
@@ -86,7 +97,13 @@ struct BinLayout {
 
 // The residual GS kernel's solver carries the contributions of each step's changes to the next
 // kRgsWin row blocks itself (k_rgs.cu); it reads them from the dense row-major A~ only.
-constexpr int kRgsWin = 7;   // (9 and 11 measured slower: more carry work per change)
+#ifndef RGS_WIN
+#define RGS_WIN 3
+#endif
+// 3 measured best on B200 (cfg3 GS band -8 %, cfg4 -16 %, cfg5 -27 % against 7; 1, 2, 4, 5, 6,
+// 9 and 11 slower): each change costs the solver W panel loads + FMAs and the panel producer W
+// segments per changed row, while the stream warps keep W + 1 steps of slack.
+constexpr int kRgsWin = RGS_WIN;
 
 // S5 + S6 on the tensor cores (k_psf.cu): int8 digit operands of the kept steering vectors
 // (opA: psf_opa_bytes, opB: psf_opb_bytes for sum rp rows; rsc: sum rp doubles), b~ = b[keep]

@@ -289,7 +289,7 @@ int launch_das(const Geo &g, const double *dist, const double *amp, int n_bins,
     if (huge) {
         const size_t smem16 = (size_t)16 * Mp * 16;
         if (smem16 > 220 * 1024) return -1;
-        if (cudaFuncSetAttribute(das_kernel<1, kDasWarps, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem16) !=
+        if (raise_smem_limit(das_kernel<1, kDasWarps, 16>, smem16) !=
             cudaSuccess)
             return -1;
         dim3 grid16((g.S + 15) / 16, n_bins);
@@ -301,10 +301,10 @@ int launch_das(const Geo &g, const double *dist, const double *amp, int n_bins,
     const int NWv = (P == 64 && !big) ? 4 : kDasWarps;
     const size_t smem = (size_t)16 * Mp * (P + ((DAS_DIRECT_C && P == 64) ? 0 : 8 * NWv));
     if (smem > 220 * 1024) return -1;
-    // set on every call: the attribute is per device, and a process may drive several devices
-    const cudaError_t e = big ? cudaFuncSetAttribute(das_kernel<2, kDasWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
-                        : (P == 64) ? cudaFuncSetAttribute(das_kernel<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
-                                    : cudaFuncSetAttribute(das_kernel<1, kDasWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // (per device and kernel: a process may drive several devices)
+    const cudaError_t e = big ? raise_smem_limit(das_kernel<2, kDasWarps>, smem)
+                        : (P == 64) ? raise_smem_limit(das_kernel<2, 4>, smem)
+                                    : raise_smem_limit(das_kernel<1, kDasWarps>, smem);
     if (e != cudaSuccess) return -1;
     dim3 grid((g.S + P - 1) / P, n_bins);
     if (big)

@@ -881,7 +881,7 @@ int launch_gs(int n_items, const int *items, const BinLayout *lay_dev, int max_s
     if (xt_env >= 0 && xt_env < xtra_tiles) xtra_tiles = xt_env;
     const size_t smem = base + (size_t)xtra_tiles * kTile * 4;
     auto kern = xtra_tiles > 0 ? gs_cluster_kernel<true> : gs_cluster_kernel<false>;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    if (raise_smem_limit(kern, smem) != cudaSuccess) {
         if (prof) cudaFree(prof);
         return -1;
     }

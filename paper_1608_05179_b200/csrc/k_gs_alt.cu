@@ -156,7 +156,7 @@ int launch_gs_alt(int n_bins, const BinLayout *lay_dev, int max_sp, const float 
                   float *x_out, float *x_map, const int32_t *keep_idx, int S, cudaStream_t st) {
     const size_t smem = (size_t)max_sp * 4;
     if (smem > 48 * 1024 &&
-        cudaFuncSetAttribute(gs_alt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        raise_smem_limit(gs_alt_kernel, smem) != cudaSuccess)
         return -1;
     gs_alt_kernel<<<n_bins, kAltThreads, smem, st>>>(lay_dev, A, bt, sweeps, x_out, x_map, keep_idx, S);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;

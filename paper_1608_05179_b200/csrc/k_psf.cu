@@ -437,8 +437,7 @@ int launch_psf(const Geo &g, const double *dist, const double *amp, int n_bins, 
         cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || num_sms < 1)
         return -1;
     const int n_cta = n_tiles < num_sms ? n_tiles : num_sms;
-    if (cudaFuncSetAttribute(wt ? psf_tc_kernel<true> : psf_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
+    if (raise_smem_limit(wt ? psf_tc_kernel<true> : psf_tc_kernel<false>, smem) != cudaSuccess)
         return -1;
     if (wt)
         psf_tc_kernel<true><<<n_cta, kPsfThreads, smem, st>>>(g.m, kp, n_tiles, tiles, lay, opA, opB, rsc, wt, A, Adense,

@@ -1061,7 +1061,7 @@ int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int m
                    : regr ? (wide ? rgs_kernel<false, true, false, kRegChWide>
                                   : two ? rgs_kernel<false, true, false, kRegChPair> : rgs_kernel<false, true, false>)
                           : rgs_kernel<false, false, false>);
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    if (raise_smem_limit(kern, smem) != cudaSuccess)
         return -1;
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];

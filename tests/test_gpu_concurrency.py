@@ -1,0 +1,71 @@
+"""Two contexts driven from two host threads on two streams (bench.py's pipelined measurement):
+every band's outputs are bit-identical to the same band solved alone.
+
+Regressions this guards: a kernel's dynamic shared-memory limit is per function and device, so a
+thread setting it for a small launch lowered it under the other thread's larger launch
+(cudaErrorInvalidValue: raise_smem_limit only raises it); outputs read before the band's own
+stream finished."""
+import threading
+
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def test_two_contexts_two_threads_match_alone(torch_cuda):
+    torch = torch_cuda
+    from paper_1608_05179_b200 import Context, Geometry
+    cfg = synth.CONFIGS["cfg3"]
+    b0 = synth.make_band(cfg)
+    g = Geometry(b0.mic_xyz, cfg.n, cfg.side_len, cfg.z0, cfg.c0, cfg.cx, cfg.cy)
+    # bands of different sizes (different launch classes and shared-memory needs) on each context
+    subsets = [list(range(0, 40)), list(range(200, 256)), list(range(90, 150)), list(range(230, 256))]
+    bands = [synth.make_band(cfg, seed=0, bins=s_, block=i + 1) for i, s_ in enumerate(subsets)]
+    csm = [torch.from_numpy(b.csm).cuda() for b in bands]
+    ctxs = [Context(0), Context(0)]
+    sts = [torch.cuda.Stream(), torch.cuda.Stream()]
+    try:
+        ref = []
+        for b, c in zip(bands, csm):
+            o = ctxs[0].solve_band(g, b.freqs, c, cfg.epsilon, cfg.sweeps, cfg.eps_mode)
+            torch.cuda.synchronize()
+            ref.append({k: o[k].cpu().numpy() for k in ("n_keep", "keep_idx", "x_map")})
+        errors, got = [], {}
+
+        def worker(j):
+            try:
+                for rep in range(3):
+                    for i in range(j, len(bands), 2):
+                        o = ctxs[j].solve_band(g, bands[i].freqs, csm[i], cfg.epsilon, cfg.sweeps, cfg.eps_mode,
+                                               stream=sts[j])
+                        sts[j].synchronize()
+                        got[(rep, i)] = {k: o[k].cpu().numpy() for k in ("n_keep", "keep_idx", "x_map")}
+            except Exception as e:   # noqa: BLE001 -- reported by the main thread
+                errors.append(repr(e))
+        ths = [threading.Thread(target=worker, args=(j,)) for j in range(2)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        assert not errors, errors
+        assert len(got) == 3 * len(bands)
+        for (rep, i), o in got.items():
+            np.testing.assert_array_equal(o["n_keep"], ref[i]["n_keep"])
+            for k in range(len(bands[i].freqs)):
+                nk = int(ref[i]["n_keep"][k])
+                np.testing.assert_array_equal(o["keep_idx"][k, :nk], ref[i]["keep_idx"][k, :nk])
+            np.testing.assert_array_equal(o["x_map"], ref[i]["x_map"], err_msg=f"rep {rep} band {i}")
+    finally:
+        for c in ctxs:
+            c.close()
