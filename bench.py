@@ -215,7 +215,10 @@ def run_pipelined(args, cfg, band, geom, ctx, dev, world, rank, strong, flush, g
         return synth.make_band(cfg, seed=seed0 + 1000 * (j + 1) if exact else seed0, bins=band.bins, block=0 if exact else j + 1)
     with ThreadPoolExecutor(8) as ex:
         pool = list(ex.map(mk, range(2 * n)))   # device path: bands 0..n-1; host path: n..2n-1
-    nc = args.contexts   # bands in flight
+    # bands in flight: 2 for the whole band on one GPU; a rank's shard of a sharded band is
+    # smaller, so more shards in flight fill its SMs (profiles/r02/shard_pipeline_projection.json:
+    # best at 3 for 128-bin shards, 6 for 64- and 32-bin shards; one GPU: 2-4 alike, 8 worse)
+    nc = args.contexts or (2 if not strong else 3 if world == 2 else 6)
     ctxs = [ctx] + [Context(dev.index) for _ in range(nc - 1)]
     sts = [torch.cuda.Stream(dev) for _ in range(nc)]
     nb, S = len(band.freqs), cfg.S
@@ -332,9 +335,12 @@ def run_pipelined(args, cfg, band, geom, ctx, dev, world, rank, strong, flush, g
         c_.close()
     mb = sum(p_.csm.nbytes for p_ in pool[W:n]) / 1e6
     return {"ms_per_step": ms_dev, "e2e_ms_per_step": ms_host if ms_host is not None else float("nan"),
-            "desc": ("consecutive bands (new measurement blocks of the same scene) on 2 contexts and 2 streams, one "
-                     "host thread per context waiting for its band before the next: at most two bands in flight, a "
-                     "band's DAS/compress/PSF overlapping the previous band's Gauss-Seidel tail"),
+            "desc": (f"consecutive bands (new measurement blocks of the same scene) on {nc} contexts and {nc} streams, "
+                     + ("one host thread per context waiting for its band before the next" if not strong else
+                        "this rank's shard of each band, issued in band order from one host thread (the gathers in "
+                        "the same order on every rank), each call waiting for its context's previous band")
+                     + f": at most {nc} bands in flight, a band's DAS/compress/PSF overlapping the previous band's "
+                       "Gauss-Seidel tail"),
             "l2": (f"none between steps: each of the {K} timed steps reads its own band ({mb:.0f} MB of CSMs in "
                    f"all, never re-read); 256 MiB write before the timed region")}
 
@@ -622,7 +628,9 @@ def main():
                     help="Gauss-Seidel kernel: automatic by system size (default), residual, dense-stream")
     ap.add_argument("--order", type=int, default=1, choices=[1, 3],
                     help="S3 predictor: 1 linear (reading R7, default), 3 cubic (R19)")
-    ap.add_argument("--contexts", type=int, default=2, help="pipelined: bands in flight (contexts / streams / host threads)")
+    ap.add_argument("--contexts", type=int, default=None,
+                    help="pipelined: bands in flight (contexts / streams / host threads); default 2 on one GPU, "
+                         "3 (N = 2) or 6 (N >= 4) for a sharded band")
     ap.add_argument("--no-pipeline", dest="pipeline", action="store_false",
                     help="time one band at a time only (default: consecutive bands on two contexts and streams)")
     args = ap.parse_args()

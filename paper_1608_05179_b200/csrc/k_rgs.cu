@@ -26,13 +26,13 @@
 //    consumed one change later, off the chain).  A block with q changing rows takes q + 1
 //    ballot rounds instead of a 32-row chain.  The changes (row, x before / after) are
 //    published as the step's change list.
-//  * panel producer (warp 5): per step, cp.async copies of the block's 32x32 diagonal tile and of
+//  * panel producer (warp 0 beside the solver on its SM sub-partition; cluster mode warp 5): per step, cp.async copies of the block's 32x32 diagonal tile and of
 //    the panels of the rows PREDICTED to change: those that changed at the block's previous visit
 //    (before the first visit: the rows with b > 0, exactly the rows sweep 1 changes).  The carries
 //    of a change outside the prediction are added after the block from global memory.
 //  * row producer (warp 6): the exact fp64 dx of every listed change; bulk copies of the rows of
 //    A~ (dense row-major) of every change into a 3-slot shared-memory ring, as batches.
-//  * stream (warps 0..3, 7; 128-column chunks owned by warps, so every element of r has one
+//  * stream (warps 1..3, 5, 7; cluster mode 0..3, 7; 128-column chunks owned by warps, so every element of r has one
 //    writer and a fixed update order): apply dx_c * A[c, :] (fp64) to r.  REGR (systems up to
 //    kRegMaxSp points): r in the stream warps' registers; after its step j the owner of a block
 //    publishes that block's r (fp32) for the solver step that reads "r after stream step j".
@@ -62,12 +62,27 @@ namespace {
 #ifndef RGS_NSTREAM
 #define RGS_NSTREAM 5
 #endif
-constexpr int kNStream = RGS_NSTREAM;          // stream warps 0..3 and 7..
+constexpr int kNStream = RGS_NSTREAM;          // stream warps 1..3, 5, 7.. or 0..3, 7.. (see panel_warp)
 constexpr int kRThreads = 32 * (kNStream + 3);
 constexpr int kRMinBlocks = kNStream > 5 ? 1 : 2;
 // warp roles: the latency-critical warps take the higher warp of each SMSP pair (w, w+4): the
 // issue arbiter prefers the higher warp id
-constexpr int kWSolver = 4, kWPanel = 5, kWRows = 6;
+#ifndef RGS_PANEL_WARP
+#define RGS_PANEL_WARP 0
+#endif
+constexpr int kWSolver = 4, kWRows = 6;
+// the panel producer's warp: warps w and w + 4 share an SM sub-partition.  One CTA per bin: warp 0,
+// beside the solver instead of a stream warp (a few copies per step; cut the solver's chain by
+// 2 %: cfg3 bin 249 alone 20.85 -> 20.48 ms, band GS 20.98 -> 20.59 ms), warp 5 then streams.
+// Cluster mode: warp 5 (warp 0 measured 5 % slower on cfg4's full grid, whose non-leader CTAs
+// have no solver).  RGS_PANEL_WARP=5 keeps warp 5 everywhere (experiment).
+template <bool CLU>
+__device__ __forceinline__ constexpr int panel_warp() { return (CLU || RGS_PANEL_WARP == 5) ? 5 : 0; }
+static_assert(RGS_PANEL_WARP == 5 || RGS_PANEL_WARP == 0, "panel producer: warp 0 or warp 5");
+// stream warp index: warps 0..3, 7, 8, ... -> 0..3, 4, 5, ...; warp 5 takes index 0 when the panel
+// producer is on warp 0
+template <bool CLU>
+__device__ __forceinline__ int stream_index(int wid) { return (panel_warp<CLU>() == 0 && wid == 5) ? 0 : (wid < 4 ? wid : wid - 3); }
 #ifndef RGS_STG
 #define RGS_STG 5
 #endif
@@ -421,7 +436,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
             __syncthreads();
         const RingGeom rg = ring_geom(rstride, slot_floats);
 
-        if (wid == kWPanel) {
+        if (wid == panel_warp<CLU>()) {
             if (!CLU || leader) {   // (cluster: the leader's)
             // ================= panel producer: the panels of the rows predicted to change, as
             // 16-byte cp.async copies spread over the warp's lanes (a 1 KB panel is 2 instructions;
@@ -634,7 +649,11 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                     const float dv = __shfl_sync(0xffffffffu, dl, ALT ? t : tl);
                     const float a0 = ALT ? dgt[32 * t] : dgt_last[-32 * tl];   // (row t = 31 - tl: one IMAD)
                     if (ALT ? rl == t : lane == tl) xo = xn;   // (the list entry is written after the block, below)
+#ifdef RGS_SCALE_A0
+                    w = fmaf(dv, a0 * -invd, w);   // (the scale of the tile entry off the shuffle's path)
+#else
                     w = fmaf(-invd * dv, a0, w);
+#endif
                     // off the chain: the carries, from row t's staged panel (element 32(d-1) + lane =
                     // A[32k+t][32 blk(s+d) + lane] = A[32 blk(s+d) + lane][32k+t]; segments beyond nsub
                     // are zero); a row not staged is added after the block from global memory
@@ -718,7 +737,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
             // or for alternating sweeps the revisit s' whose last visit was step j), in the
             // step-indexed slot s' mod 16 (the pend buffer)
             // (CLU: the chunks of this CTA's slice, local index ql = q - q_lo)
-            const int w = (wid < 4) ? wid : wid - 3;
+            const int w = stream_index<CLU>(wid);
             const int nch = max(0, (q_hi - q_lo - w + kNStream - 1) / kNStream);   // chunks this warp owns
             DWC_DCHECK(nch <= RC && rg.nseg == 1, "stream: register chunks");
             unsigned long long tlw = 0, tbw = 0, tap = 0, nb_all = 0;
@@ -807,7 +826,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
         } else {
             // ================= stream warps: r += dx_c A[c, :] for every change of every step;
             // warp w owns the 128-column chunks q = w, w + 5, ...; lane l columns 128q + 4l..+3
-            const int w = (wid < 4) ? wid : wid - 3;
+            const int w = stream_index<CLU>(wid);
             unsigned long long tlw = 0, tbw = 0, tap = 0, nb_all = 0;
             int b = 0;
             for (int s = 0, p = 0, pos = 0; s < total; s++, pos = (pos + 1 == T) ? 0 : pos + 1, p += (pos == 0)) {

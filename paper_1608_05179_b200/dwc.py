@@ -155,6 +155,20 @@ def _stream(stream, device=None) -> int:
     return int(s.cuda_stream)
 
 
+def _rec(stream, *tensors):
+    """A call enqueued on `stream` reads and writes these device tensors: the caching allocator
+    allocated them on (or for) another stream -- the current one -- and would otherwise hand their
+    blocks out again as soon as the Python objects die, while the call's kernels still run on
+    `stream` (found with consecutive bands on several contexts, each on its own stream: an output
+    dropped before its stream synchronised was reallocated to another band's call).
+    record_stream delays the reuse until `stream`'s work queued at free time is done."""
+    if stream is None:
+        return
+    for t in tensors:
+        if t is not None and getattr(t, "is_cuda", False):
+            t.record_stream(stream)
+
+
 def _check_out(out: dict, K: int, S: int, want_b: bool, host: bool, device=None):
     """Caller-supplied output buffers: shape, dtype, contiguity and residency (the C call writes
     K*S elements through raw pointers)."""
@@ -232,6 +246,7 @@ class Context:
             _dev(out["keep_idx"], torch.int32, "keep_idx"), _dev(out["x_map"], torch.float32, "x_map"),
             _dev(out["b_map"], torch.float64, "b_map") if out.get("b_map") is not None else None,
             warn.ctypes.data, _stream(stream, self.device)))
+        _rec(stream, csm, out["n_keep"], out["keep_idx"], out["x_map"], out.get("b_map"))
         out["warn"] = warn
         return out
 
@@ -289,6 +304,7 @@ class Context:
             _dev(out["keep_idx"], torch.int32, "keep_idx"), _dev(out["x_map"], torch.float32, "x_map"),
             _dev(out["b_map"], torch.float64, "b_map") if out["b_map"] is not None else None,
             warn.ctypes.data, _stream(stream, self.device)))
+        _rec(stream, snap, out["n_keep"], out["keep_idx"], out["x_map"], out["b_map"])
         out["warn"] = warn
         return out
 
@@ -299,6 +315,7 @@ class Context:
         out = torch.empty((K, M, M), dtype=torch.complex128, device=snap.device)
         _check(lib().dwc_csm(self._h, M, K, I, _dev(snap, torch.complex128, "snap"),
                              _dev(out, torch.complex128, "csm"), _stream(stream, self.device)))
+        _rec(stream, snap, out)
         return out
 
     def steer(self, geom: Geometry, freq: float, idx, stream=None):
@@ -308,6 +325,7 @@ class Context:
         arr, grid = geom.c_array(), geom.c_grid()
         _check(lib().dwc_steer(self._h, C.byref(arr), C.byref(grid), float(freq), idx.numel(),
                                _dev(idx, torch.int32, "idx"), _dev(E, torch.complex128, "E"), _stream(stream, self.device)))
+        _rec(stream, idx, E)
         return E
 
     def das(self, geom: Geometry, freqs, csm, stream=None, dr: bool = False, paper: bool = False):
@@ -319,6 +337,7 @@ class Context:
                              _dev(csm, torch.complex128, "csm"),
                              (DWC_DIAG_REMOVAL if dr else 0) | (DWC_PAPER_PSF if paper else 0),
                              _dev(b, torch.float64, "b"), _stream(stream, self.device)))
+        _rec(stream, csm, b)
         return b
 
     def compress(self, geom: Geometry, b_map, epsilon: float, eps_mode: int = 0, full_grid: bool = False, order: int = 1,
@@ -333,6 +352,7 @@ class Context:
         _check(lib().dwc_compress(self._h, C.byref(grid), C.byref(prm), K, _dev(b_map, torch.float64, "b_map"),
                                   _dev(nk, torch.int32, "n_keep"), _dev(keep, torch.int32, "keep_idx"),
                                   _dev(lev, torch.uint8, "level") if lev is not None else None, _stream(stream, self.device)))
+        _rec(stream, b_map, nk, keep, lev)
         return nk, keep, lev
 
     def psf(self, geom: Geometry, freq: float, keep_idx, stream=None, dr: bool = False, paper: bool = False):
@@ -345,6 +365,7 @@ class Context:
                              _dev(keep_idx, torch.int32, "keep_idx"),
                              (DWC_DIAG_REMOVAL if dr else 0) | (DWC_PAPER_PSF if paper else 0),
                              _dev(A, torch.float32, "A"), _stream(stream, self.device)))
+        _rec(stream, keep_idx, A)
         return A
 
     def gs(self, A, b, sweeps: int, stream=None, alt: bool = False, dense_stream=None, general: bool = False):
@@ -354,6 +375,7 @@ class Context:
         fl = DWC_PAPER_PSF if general else ((DWC_ALT_SWEEPS if alt else 0) | _gs_kernel_flag(dense_stream))
         _check(lib().dwc_gs(self._h, n, _dev(A, torch.float32, "A"), _dev(b, torch.float64, "b"), int(sweeps),
                             fl, _dev(x, torch.float32, "x"), _stream(stream, self.device)))
+        _rec(stream, A, b, x)
         return x
 
     # ---- multi-GPU gather helpers ----------------------------------------------------------
@@ -366,6 +388,7 @@ class Context:
         _check(lib().dwc_keep_mask(self._h, K, S, _dev(n_keep, torch.int32, "n_keep"),
                                    _dev(keep_idx, torch.int32, "keep_idx"), _dev(mask, torch.int32, "mask"),
                                    _stream(stream, self.device)))
+        _rec(stream, n_keep, keep_idx, mask)
         return mask
 
     def keep_unmask(self, mask, S: int, stream=None):
@@ -377,6 +400,7 @@ class Context:
         _check(lib().dwc_keep_unmask(self._h, K, int(S), _dev(mask, torch.int32, "mask"),
                                      _dev(n_keep, torch.int32, "n_keep"), _dev(keep_idx, torch.int32, "keep_idx"),
                                      _stream(stream, self.device)))
+        _rec(stream, mask, n_keep, keep_idx)
         return n_keep, keep_idx
 
     # ---- diagnostics --------------------------------------------------------------------

@@ -69,3 +69,57 @@ def test_two_contexts_two_threads_match_alone(torch_cuda):
     finally:
         for c in ctxs:
             c.close()
+
+
+def test_four_contexts_dropped_outputs_on_side_streams(torch_cuda):
+    """Four contexts on four threads and streams, each call's outputs allocated by the binding and
+    dropped before the stream synchronises (every other call's kept): the binding records the
+    call's stream on every tensor it hands the library, so the caching allocator does not give a
+    dropped output's block to another thread's allocation while the kernels still write it.
+    (Regression: consecutive shard-sized bands on four contexts faulted with illegal-address and
+    invalid-address-space errors; CUDA_LAUNCH_BLOCKING=1 hid it.)"""
+    torch = torch_cuda
+    from paper_1608_05179_b200 import Context, Geometry
+    cfg = synth.CONFIGS["cfg3"]
+    bins = list(range(1, 256, 8))   # a 32-bin strided shard (8-way sharding)
+    bands = [synth.make_band(cfg, seed=0, bins=bins, block=i + 1) for i in range(4)]
+    g = Geometry(bands[0].mic_xyz, cfg.n, cfg.side_len, cfg.z0, cfg.c0, cfg.cx, cfg.cy)
+    csm = [torch.from_numpy(b.csm).cuda() for b in bands]
+    nc = 4
+    ctxs = [Context(0) for _ in range(nc)]
+    sts = [torch.cuda.Stream() for _ in range(nc)]
+    sweeps = 300
+    try:
+        ref = []
+        for b, c in zip(bands, csm):
+            o = ctxs[0].solve_band(g, b.freqs, c, cfg.epsilon, sweeps, cfg.eps_mode)
+            torch.cuda.synchronize()
+            ref.append({k: o[k].cpu().numpy() for k in ("n_keep", "x_map")})
+        errors, got = [], {}
+
+        def worker(j):
+            try:
+                for rep in range(4):
+                    i = (j + rep) % len(bands)
+                    ctxs[j].solve_band(g, bands[i].freqs, csm[i], cfg.epsilon, sweeps, cfg.eps_mode, stream=sts[j])
+                    junk = [torch.full((len(bins), cfg.S), -7, dtype=torch.int32, device="cuda") for _ in range(3)]
+                    o = ctxs[j].solve_band(g, bands[i].freqs, csm[i], cfg.epsilon, sweeps, cfg.eps_mode, stream=sts[j])
+                    junk += [torch.full((len(bins), cfg.S), 1e30, dtype=torch.float32, device="cuda") for _ in range(3)]
+                    sts[j].synchronize()
+                    got[(j, rep)] = (i, {k: o[k].cpu().numpy() for k in ("n_keep", "x_map")})
+                    del junk
+            except Exception as e:   # noqa: BLE001 -- reported by the main thread
+                errors.append(repr(e))
+        ths = [threading.Thread(target=worker, args=(j,)) for j in range(nc)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        torch.cuda.synchronize()
+        assert not errors, errors
+        for (j, rep), (i, o) in got.items():
+            np.testing.assert_array_equal(o["n_keep"], ref[i]["n_keep"])
+            np.testing.assert_array_equal(o["x_map"], ref[i]["x_map"], err_msg=f"context {j} rep {rep} band {i}")
+    finally:
+        for c in ctxs:
+            c.close()
