@@ -205,7 +205,15 @@ def run_pipelined(args, cfg, band, geom, ctx, dev, world, rank, strong, flush, g
     import torch.distributed as dist
 
     from paper_1608_05179_b200 import Context
-    W, K = args.warmup, args.steps
+    K = args.steps
+    # bands in flight: 3 for the whole band on one GPU (with the DWC_THROUGHPUT hint: 16.9 k
+    # bins/s against 16.0 k with 2 and 16.6 k with 4); a rank's shard of a sharded band is smaller,
+    # so more shards in flight fill its SMs (profiles/r02/shard_pipeline_projection.json: 8 best
+    # for 128-, 64- and 32-bin shards)
+    nc = args.contexts or (3 if not strong else 8)
+    # warm-up: W steps, and at least one band per context (its workspace and first launches are
+    # set up untimed)
+    W = max(args.warmup, nc)
     n = W + K
     # exact-CSM configs have no measurement noise: their consecutive "blocks" are new scenes
     exact = cfg.csm == "exact"
@@ -215,15 +223,11 @@ def run_pipelined(args, cfg, band, geom, ctx, dev, world, rank, strong, flush, g
         return synth.make_band(cfg, seed=seed0 + 1000 * (j + 1) if exact else seed0, bins=band.bins, block=0 if exact else j + 1)
     with ThreadPoolExecutor(8) as ex:
         pool = list(ex.map(mk, range(2 * n)))   # device path: bands 0..n-1; host path: n..2n-1
-    # bands in flight: 2 for the whole band on one GPU; a rank's shard of a sharded band is
-    # smaller, so more shards in flight fill its SMs (profiles/r02/shard_pipeline_projection.json:
-    # best at 3 for 128-bin shards, 6 for 64- and 32-bin shards; one GPU: 2-4 alike, 8 worse)
-    nc = args.contexts or (2 if not strong else 3 if world == 2 else 6)
     ctxs = [ctx] + [Context(dev.index) for _ in range(nc - 1)]
     sts = [torch.cuda.Stream(dev) for _ in range(nc)]
     nb, S = len(band.freqs), cfg.S
     kw = dict(full_grid=cfg.full_grid, order=args.order, dr=args.dr, alt=args.alt, paper=args.paper,
-              dense_stream=KERNEL_FLAG[args.kernel])
+              dense_stream=KERNEL_FLAG[args.kernel], throughput=args.throughput)
 
     def outs(device):
         mk_ = (lambda shape, dt: torch.empty(shape, dtype=dt, device=dev)) if device else \
@@ -320,7 +324,8 @@ def run_pipelined(args, cfg, band, geom, ctx, dev, world, rank, strong, flush, g
     def hstep(i, j):
         ctxs[j].solve_band_host(geom, pool[n + i].freqs, csm_host[i], cfg.epsilon, cfg.sweeps, cfg.eps_mode,
                                 cfg.full_grid, out=hout[j], stream=sts[j], order=args.order, dr=args.dr,
-                                alt=args.alt, paper=args.paper, dense_stream=KERNEL_FLAG[args.kernel])
+                                alt=args.alt, paper=args.paper, dense_stream=KERNEL_FLAG[args.kernel],
+                                throughput=args.throughput)
 
     def hrun(first, last):
         ths = [th.Thread(target=lambda j=j: [hstep(i, j) for i in range(first + j, last, nc)]) for j in range(nc)]
@@ -560,6 +565,7 @@ def run_ours(args, cfg):
                        "parallelism": f"bins-dp{world}",
                        "l2_flush": (pipe["l2"] if pipe else "256 MiB write between timed steps"),
                        "pipeline": (pipe["desc"] if pipe else "none: one band at a time"),
+                       "throughput_hint": bool(pipe) and args.throughput,
                        "inputs": ("snapshot spectra resident in HBM, CSM formed on device (Eq. 1)" if snapshots
                                   else "CSMs resident in HBM")},
             "psf_stream_gbs": achieved,
@@ -629,8 +635,10 @@ def main():
     ap.add_argument("--order", type=int, default=1, choices=[1, 3],
                     help="S3 predictor: 1 linear (reading R7, default), 3 cubic (R19)")
     ap.add_argument("--contexts", type=int, default=None,
-                    help="pipelined: bands in flight (contexts / streams / host threads); default 2 on one GPU, "
-                         "3 (N = 2) or 6 (N >= 4) for a sharded band")
+                    help="pipelined: bands in flight (contexts / streams / host threads); default 3 on one GPU, "
+                         "8 for a sharded band")
+    ap.add_argument("--no-throughput-hint", dest="throughput", action="store_false",
+                    help="pipelined: do not pass DWC_THROUGHPUT (bands in flight) to the library")
     ap.add_argument("--no-pipeline", dest="pipeline", action="store_false",
                     help="time one band at a time only (default: consecutive bands on two contexts and streams)")
     args = ap.parse_args()

@@ -87,7 +87,8 @@ typedef struct {
     int32_t eps_mode; /* 0 = relative, 1 = absolute (reading R6) */
     int32_t sweeps;   /* Gauss-Seidel sweeps >= 1 from x0 = 0 */
     int32_t flags;    /* DWC_FULL_GRID: keep every node (the paper's "original grid"); DWC_CUBIC;
-                         DWC_DIAG_REMOVAL; DWC_ALT_SWEEPS */
+                         DWC_DIAG_REMOVAL; DWC_ALT_SWEEPS; DWC_GS_DENSE_STREAM / DWC_GS_RESIDUAL;
+                         DWC_PAPER_PSF; DWC_THROUGHPUT (each documented below) */
 } dwc_params;
 
 #define DWC_FULL_GRID 1
@@ -127,6 +128,15 @@ typedef struct {
  * transposed.  Not with DWC_DIAG_REMOVAL or DWC_GS_DENSE_STREAM (DWC_EINVAL); with DWC_ALT_SWEEPS.
  * The sweeps' convergence is not guaranteed (A_P has an indefinite symmetric part). */
 #define DWC_PAPER_PSF 64
+/* DWC_THROUGHPUT: a hint that this band is one of several in flight (bands streamed in, on other
+ * contexts / streams): the residual kernel then runs every system of up to 1280 points two CTAs
+ * per SM (half the registers and shared memory each), so overlapping bands share
+ * the SMs; without it only the systems of at most 2/3 of the band's largest size do, and only
+ * when the band has more bins than SMs.  The iterates are bitwise identical either way (the
+ * kernel's arithmetic and order do not depend on the class).  Measured on cfg3 (one B200): one
+ * band alone 24.0 -> 28.6 ms, bands in flight 14.2 k -> 16.7 k bins/s.  Ignored by the
+ * dense-stream kernel. */
+#define DWC_THROUGHPUT 128
 #define DWC_MAX_MICS 512
 
 /* Create / destroy a context on CUDA device `device`.  The device must be sm_100

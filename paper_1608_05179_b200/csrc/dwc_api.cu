@@ -234,7 +234,7 @@ dwc_status check_params(const dwc_params *p) {
     if (p->eps_mode != 0 && p->eps_mode != 1) return fail(DWC_EINVAL, "eps_mode must be 0 or 1");
     if (p->sweeps < 1) return fail(DWC_EINVAL, "sweeps must be >= 1");
     if (p->flags & ~(DWC_FULL_GRID | DWC_CUBIC | DWC_DIAG_REMOVAL | DWC_ALT_SWEEPS | DWC_GS_DENSE_STREAM | DWC_GS_RESIDUAL |
-                     DWC_PAPER_PSF))
+                     DWC_PAPER_PSF | DWC_THROUGHPUT))
         return fail(DWC_EINVAL, "unknown flags 0x%x", p->flags);
     if ((p->flags & DWC_GS_DENSE_STREAM) && (p->flags & DWC_GS_RESIDUAL))
         return fail(DWC_EINVAL, "DWC_GS_DENSE_STREAM and DWC_GS_RESIDUAL exclude each other");
@@ -480,7 +480,7 @@ dwc_status solve_band_dev(dwc_ctx *ctx, const dwc_array *arr, const dwc_grid *gr
         // (wide clusters -- 5120 columns per CTA -- on the compressed grid, where many rows change
         // per sweep; narrow ones on the full grid, where few do)
         const bool wide_cl = !(p->flags & DWC_FULL_GRID);
-        const int pair_sp = rgs_pair_max_sp(max_sp, n_bins, ctx->num_sms);
+        const int pair_sp = rgs_pair_max_sp(max_sp, n_bins, ctx->num_sms, (p->flags & DWC_THROUGHPUT) != 0);
         std::vector<std::pair<int, int>> cls;   // [begin, end) in `order`
         for (int i = 0; i < n_bins; i++) {
             const int g = rgs_size_class((hk[order[i]] + 31) & ~31, wide_cl, pair_sp);

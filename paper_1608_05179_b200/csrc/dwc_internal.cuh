@@ -304,7 +304,7 @@ int rgs_cluster_size(int sp, bool wide);
 // Launch class of a system of sp padded points (bins of one class share a residual-kernel launch).
 int rgs_size_class(int sp, bool wide, int pair_max_sp = 0);
 // Systems of at most this many padded points run two CTAs per SM (0: none).
-int rgs_pair_max_sp(int band_max_sp, int n_bins, int num_sms);
+int rgs_pair_max_sp(int band_max_sp, int n_bins, int num_sms, bool throughput);
 int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int max_sp, int *counter,
                const float *Adense, const double *bt, int sweeps, float *x_out, float *x_map,
                const int32_t *keep_idx, int S, int num_sms, unsigned long long *n_updates, cudaStream_t st,

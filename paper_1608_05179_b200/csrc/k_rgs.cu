@@ -84,7 +84,7 @@ static_assert(RGS_PANEL_WARP == 5 || RGS_PANEL_WARP == 0, "panel producer: warp 
 template <bool CLU>
 __device__ __forceinline__ int stream_index(int wid) { return (panel_warp<CLU>() == 0 && wid == 5) ? 0 : (wid < 4 ? wid : wid - 3); }
 #ifndef RGS_STG
-#define RGS_STG 5
+#define RGS_STG 4
 #endif
 #ifndef RGS_NP
 #define RGS_NP 8
@@ -336,7 +336,10 @@ __device__ __forceinline__ void apply_dispatch(int nch, double (&r)[RC][4], cons
 }
 
 template <bool ALT, bool REGR, bool CLU, int RC = kRegCh>
-__global__ void __launch_bounds__(kRThreads, (REGR && RC > kRegChPair) ? 1 : kRMinBlocks)
+#ifndef RGS_PAIR_MINB
+#define RGS_PAIR_MINB kRMinBlocks
+#endif
+__global__ void __launch_bounds__(kRThreads, (REGR && RC > kRegChPair) ? 1 : (REGR ? RGS_PAIR_MINB : kRMinBlocks))
 rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restrict__ lay, int *__restrict__ counter,
            const float *__restrict__ Adense, const double *__restrict__ bt, int sweeps, float *__restrict__ x_out,
            float *__restrict__ x_map, const int32_t *__restrict__ keep_idx, int S, int max_sp, int slot_floats,
@@ -1002,14 +1005,17 @@ int rgs_cluster_size(int sp, bool wide) {
 
 // Small systems of a band with more bins than SMs run two CTAs per SM, so that every bin starts
 // at once instead of the late-started ones forming the band's tail: the bins whose padded size
-// is at most half the band's largest (a bin's time grows about linearly with S~, and sharing an
-// SM at most doubles it, so they still finish within the longest chain).  cfg3: GS 23.7 ->
-// 21.8 ms, the longest bin's time alone (thresholds 576..704 measured alike, 544 and 800 worse).
-int rgs_pair_max_sp(int band_max_sp, int n_bins, int num_sms) {
+// is at most 2/3 of the band's largest (a bin's time grows about linearly with S~, and sharing an
+// SM at most doubles it).  cfg3 (largest 1344): one band alone 24.0 ms at 2/3 (896) as at 1/2
+// (672), bands in flight 14.2 -> 15.6 k bins/s; 1024 and 1280 gain more in flight (16.0 k) but
+// lose alone (25.9, 28.6 ms).  throughput (DWC_THROUGHPUT: bands in flight): every system up to
+// kRegMaxSpPair, whatever the band's size.
+int rgs_pair_max_sp(int band_max_sp, int n_bins, int num_sms, bool throughput) {
     static const int env = getenv("DWC_RGS_PAIR_MAX_SP") ? atoi(getenv("DWC_RGS_PAIR_MAX_SP")) : -1;   // experiment
     if (env >= 0) return std::min(env, kRegMaxSpPair);
+    if (throughput) return kRegMaxSpPair;
     if (n_bins <= num_sms) return 0;
-    return std::min((band_max_sp / 2) & ~31, kRegMaxSpPair);
+    return std::min((2 * band_max_sp / 3) & ~31, kRegMaxSpPair);
 }
 
 int rgs_size_class(int sp, bool wide, int pair_max_sp) {
@@ -1060,12 +1066,18 @@ int launch_rgs(int n_bins, const int *order_dev, const BinLayout *lay_dev, int m
     if (base + 1536 > 227 * 1024) return -1;
     // shared-memory r: two CTAs per SM (2 x (smem + 1 KB reserved) <= 228 KB) when the band has
     // more bins than SMs and every ring slot still holds 2 rows
+#ifndef RGS_PAIR_PER_SM
+#define RGS_PAIR_PER_SM 2
+#endif
     const size_t per2 = 114 * 1024 - 1024;
-    const bool two = regr ? (pair && per2 > base + 3 * 4 * (size_t)max_sp + 1024)   // (r in registers: the small class)
+    // the small register class: RGS_PAIR_PER_SM CTAs per SM (shared memory split that many ways;
+    // 3, with RGS_PAIR_MINB=3 for 80 registers, measured 31 % slower for bands in flight)
+    const size_t perp = 228 * 1024 / RGS_PAIR_PER_SM - 1024;
+    const bool two = regr ? (pair && perp > base + 3 * 4 * (size_t)max_sp + 1024)   // (r in registers: the small class)
                      : kRMinBlocks < 2 ? false
                      : per_sm_env ? per_sm_env == 2 && per2 > base + 2048
                                 : n_bins > num_sms && per2 > base && (per2 - base) / (4 * kNSlot) >= 2 * (size_t)max_sp;
-    size_t ring = two ? (per2 - base - 512) / 1024 * 1024 : (227 * 1024 - base - 512) / 1024 * 1024;
+    size_t ring = two ? ((regr ? perp : per2) - base - 512) / 1024 * 1024 : (227 * 1024 - base - 512) / 1024 * 1024;
     if (ring_env > 0 && (size_t)ring_env * 1024 < ring) ring = (size_t)ring_env * 1024;
     const int slot_floats = slot_of(ring);   // floats per ring slot
     if (slot_floats < 128) return -1;

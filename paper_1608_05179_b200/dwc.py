@@ -21,6 +21,7 @@ DWC_ALT_SWEEPS = 8
 DWC_GS_DENSE_STREAM = 16
 DWC_GS_RESIDUAL = 32
 DWC_PAPER_PSF = 64
+DWC_THROUGHPUT = 128
 GS_KERNELS = {0: "none", 1: "cluster", 2: "cluster_xtra", 3: "alternating", 4: "residual"}
 STATUS = {0: "DWC_OK", -1: "DWC_EINVAL", -2: "DWC_ESINGULAR", -3: "DWC_ENUMERIC",
           -4: "DWC_ENOMEM", -5: "DWC_ECUDA", -6: "DWC_ESTATE"}
@@ -140,12 +141,13 @@ def _gs_kernel_flag(dense_stream) -> int:
 
 
 def _flags(full_grid: bool, order: int, dr: bool = False, alt: bool = False, dense_stream=None,
-           paper: bool = False) -> int:
+           paper: bool = False, throughput: bool = False) -> int:
     if order not in (1, 3):
         raise ValueError("order must be 1 (linear predictor) or 3 (cubic)")
     return ((DWC_FULL_GRID if full_grid else 0) | (DWC_CUBIC if order == 3 else 0) |
             (DWC_DIAG_REMOVAL if dr else 0) | (DWC_ALT_SWEEPS if alt else 0) |
-            (0 if paper else _gs_kernel_flag(dense_stream)) | (DWC_PAPER_PSF if paper else 0))
+            (0 if paper else _gs_kernel_flag(dense_stream)) | (DWC_PAPER_PSF if paper else 0) |
+            (DWC_THROUGHPUT if throughput else 0))
 
 
 def _stream(stream, device=None) -> int:
@@ -221,7 +223,8 @@ class Context:
     # ---- hot path ---------------------------------------------------------------
     def solve_band(self, geom: Geometry, freqs: Sequence[float], csm, epsilon: float, sweeps: int,
                    eps_mode: int = 0, full_grid: bool = False, want_b: bool = False, out=None, order: int = 1,
-                   stream=None, dr: bool = False, alt: bool = False, dense_stream=None, paper: bool = False):
+                   stream=None, dr: bool = False, alt: bool = False, dense_stream=None, paper: bool = False,
+                   throughput: bool = False):
         """Batched S0..S8 on device tensors.  csm: cuda complex128 [K,M,M].
         Returns dict(n_keep int32[K], keep_idx int32[K,S], x_map float32[K,S], b_map, warn)."""
         import torch
@@ -239,7 +242,7 @@ class Context:
             _check_out(out, K, S, want_b, host=False, device=dev)
         warn = np.zeros(K, dtype=np.uint32)
         arr, grid = geom.c_array(), geom.c_grid()
-        prm = Params(float(epsilon), int(eps_mode), int(sweeps), _flags(full_grid, order, dr, alt, dense_stream, paper))
+        prm = Params(float(epsilon), int(eps_mode), int(sweeps), _flags(full_grid, order, dr, alt, dense_stream, paper, throughput))
         _check(lib().dwc_solve_band(
             self._h, C.byref(arr), C.byref(grid), C.byref(prm), K, freqs.ctypes.data,
             _dev(csm, torch.complex128, "csm"), _dev(out["n_keep"], torch.int32, "n_keep"),
@@ -252,7 +255,8 @@ class Context:
 
     def solve_band_host(self, geom: Geometry, freqs, csm, epsilon: float, sweeps: int, eps_mode: int = 0,
                         full_grid: bool = False, want_b: bool = False, out=None, stream=None, order: int = 1,
-                        dr: bool = False, alt: bool = False, dense_stream=None, paper: bool = False):
+                        dr: bool = False, alt: bool = False, dense_stream=None, paper: bool = False,
+                   throughput: bool = False):
         """Same as solve_band with host buffers (numpy or CPU tensors, pinned or not); the
         host<->device copies happen inside the C call, which returns when results are on the host."""
         import torch
@@ -270,7 +274,7 @@ class Context:
             _check_out(out, K, S, want_b, host=True)
         warn = np.zeros(K, dtype=np.uint32)
         arr, grid = geom.c_array(), geom.c_grid()
-        prm = Params(float(epsilon), int(eps_mode), int(sweeps), _flags(full_grid, order, dr, alt, dense_stream, paper))
+        prm = Params(float(epsilon), int(eps_mode), int(sweeps), _flags(full_grid, order, dr, alt, dense_stream, paper, throughput))
         csm = csm.contiguous()
         _check(lib().dwc_solve_band_host(
             self._h, C.byref(arr), C.byref(grid), C.byref(prm), K, freqs.ctypes.data, csm.data_ptr(),
@@ -283,7 +287,8 @@ class Context:
     # ---- stage entry points ---------------------------------------------------------
     def solve_band_snapshots(self, geom: Geometry, freqs: Sequence[float], snap, epsilon: float, sweeps: int,
                              eps_mode: int = 0, full_grid: bool = False, want_b: bool = False, order: int = 1,
-                             stream=None, dr: bool = False, alt: bool = False, dense_stream=None, paper: bool = False):
+                             stream=None, dr: bool = False, alt: bool = False, dense_stream=None, paper: bool = False,
+                   throughput: bool = False):
         """The path from snapshot spectra (Eq. 1 on the device).  snap: cuda complex128 [K,M,I]."""
         import torch
         freqs = np.ascontiguousarray(freqs, dtype=np.float64)
@@ -297,7 +302,7 @@ class Context:
                "b_map": torch.empty((K, S), dtype=torch.float64, device=dev) if want_b else None}
         warn = np.zeros(K, dtype=np.uint32)
         arr, grid = geom.c_array(), geom.c_grid()
-        prm = Params(float(epsilon), int(eps_mode), int(sweeps), _flags(full_grid, order, dr, alt, dense_stream, paper))
+        prm = Params(float(epsilon), int(eps_mode), int(sweeps), _flags(full_grid, order, dr, alt, dense_stream, paper, throughput))
         _check(lib().dwc_solve_band_snapshots(
             self._h, C.byref(arr), C.byref(grid), C.byref(prm), K, freqs.ctypes.data, int(snap.shape[2]),
             _dev(snap, torch.complex128, "snap"), _dev(out["n_keep"], torch.int32, "n_keep"),

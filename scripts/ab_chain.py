@@ -1,5 +1,6 @@
 """A/B helper (library chosen by DWC_LIB): the cfg3 band's GS time (median of 5 calls) and the
 chain-floor bin alone (ALONE_BIN, default 249; median of 3), one line per library."""
+import hashlib
 import os
 import sys
 
@@ -30,4 +31,4 @@ for rep in range(3):
     ctx.solve_band(g, band.freqs[kb:kb + 1], csm[kb:kb + 1], cfg.epsilon, cfg.sweeps, cfg.eps_mode, **kw)
     al.append(ctx.stats()["ms_gs"])
 print(f"{os.path.basename(os.environ.get('DWC_LIB', 'libdwc.so'))} {cfgname}: band gs median {np.median(gs):.2f} "
-      f"(min {min(gs):.2f} max {max(gs):.2f}) | bin {kb} alone {np.median(al):.2f} ms | sum x {xs.sum():.6e}", flush=True)
+      f"(min {min(gs):.2f} max {max(gs):.2f}) | bin {kb} alone {np.median(al):.2f} ms | sum x {xs.sum():.6e} md5 {hashlib.md5(xs.tobytes()).hexdigest()[:12]}", flush=True)

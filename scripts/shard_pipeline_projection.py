@@ -23,9 +23,10 @@ from paper_1608_05179_b200 import Context, Geometry  # noqa: E402
 from paper_1608_05179_b200.band_parallel import shard_bins  # noqa: E402
 
 cfg = synth.CONFIGS["cfg3"]
-W, K = 3, int(os.environ.get("PROJ_STEPS", "16"))
+W0, K = 3, int(os.environ.get("PROJ_STEPS", "16"))
 GS = [int(x) for x in os.environ.get("PROJ_G", "1,2,4,8").split(",")]
 CS = [int(x) for x in os.environ.get("PROJ_C", "2,3,4,6,8").split(",")]
+TP = os.environ.get("PROJ_THROUGHPUT", "1") == "1"   # the DWC_THROUGHPUT hint (bench.py's pipelined default)
 band0 = synth.make_band(cfg, bins=[0])
 g = Geometry(band0.mic_xyz, cfg.n, cfg.side_len, cfg.z0, cfg.c0, cfg.cx, cfg.cy)
 dev = torch.device("cuda", 0)
@@ -33,11 +34,13 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 ctxs = [Context(0) for _ in range(max(CS))]
 sts = [torch.cuda.Stream(dev) for _ in range(max(CS))]
 cur = torch.cuda.current_stream(dev)
-res = {"workload": "cfg3 (256 bins, 1000 sweeps), consecutive bands (blocks 1..W+K)", "warmup": W, "steps": K,
+res = {"workload": "cfg3 (256 bins, 1000 sweeps), consecutive bands (blocks 1..W+K)", "warmup": "max(3, bands in flight)", "steps": K,
+       "throughput_hint": TP,
        "shards": {}}
 
 
 def run(bins, nc):
+    W = max(W0, nc)
     with ThreadPoolExecutor(8) as ex:
         pool = list(ex.map(lambda j: synth.make_band(cfg, bins=bins, block=j + 1), range(W + K)))
     csm = [torch.from_numpy(b.csm).to(dev) for b in pool]
@@ -46,14 +49,15 @@ def run(bins, nc):
     def drun(first, last):
         def worker(j):
             for i in range(first + j, last, nc):
-                ctxs[j].solve_band(g, freqs, csm[i], cfg.epsilon, cfg.sweeps, cfg.eps_mode, stream=sts[j])
+                ctxs[j].solve_band(g, freqs, csm[i], cfg.epsilon, cfg.sweeps, cfg.eps_mode, stream=sts[j],
+                                   throughput=TP)
                 sts[j].synchronize()
         ths = [threading.Thread(target=worker, args=(j,)) for j in range(nc)]
         for t in ths:
             t.start()
         for t in ths:
             t.join()
-    drun(0, W)
+    drun(0, W)   # (W >= nc: every context warmed)
     torch.cuda.synchronize()
     flush.zero_()
     torch.cuda.synchronize()

@@ -123,3 +123,27 @@ def test_four_contexts_dropped_outputs_on_side_streams(torch_cuda):
     finally:
         for c in ctxs:
             c.close()
+
+
+def test_throughput_hint_is_bitwise_neutral(torch_cuda):
+    """DWC_THROUGHPUT only moves systems into the two-CTAs-per-SM class: the full cfg3 band's
+    outputs are bitwise identical with and without it (also on a 32-bin shard, where the hint
+    pairs bins the default leaves one per SM)."""
+    torch = torch_cuda
+    from paper_1608_05179_b200 import Context, Geometry
+    cfg = synth.CONFIGS["cfg3"]
+    ctx = Context(0)
+    try:
+        for bins in (None, list(range(1, 256, 8))):
+            band = synth.make_band(cfg, bins=bins)
+            g = Geometry(band.mic_xyz, cfg.n, cfg.side_len, cfg.z0, cfg.c0, cfg.cx, cfg.cy)
+            csm = torch.from_numpy(band.csm).cuda()
+            outs = []
+            for tp in (False, True):
+                o = ctx.solve_band(g, band.freqs, csm, cfg.epsilon, cfg.sweeps, cfg.eps_mode, throughput=tp)
+                torch.cuda.synchronize()
+                outs.append({k: o[k].cpu().numpy() for k in ("n_keep", "keep_idx", "x_map")})
+            for k in ("n_keep", "keep_idx", "x_map"):
+                np.testing.assert_array_equal(outs[0][k], outs[1][k], err_msg=k)
+    finally:
+        ctx.close()

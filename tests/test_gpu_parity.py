@@ -556,7 +556,7 @@ def test_errors_flags_and_new_entry_points(ctx, torch_cuda):
     keep = torch.empty((1, g.S), dtype=torch.int32, device="cuda")
     x = torch.empty((1, g.S), dtype=torch.float32, device="cuda")
     f = np.array(band.freqs, dtype=np.float64)
-    prm = Params(0.1, 0, 5, 128)   # unknown flag bit
+    prm = Params(0.1, 0, 5, 1 << 20)   # unknown flag bit
     rc = lib().dwc_solve_band(ctx._h, C.byref(arr), C.byref(grid), C.byref(prm), 1, f.ctypes.data,
                               csm.data_ptr(), nk.data_ptr(), keep.data_ptr(), x.data_ptr(), None, None,
                               torch.cuda.current_stream().cuda_stream)
