@@ -89,3 +89,20 @@ def test_output_buffer_checks():
         _check_out(ok, K, S, want_b=True, host=True)        # b_map wanted but missing
     with pytest.raises(ValueError):
         _check_out(ok, K, S, want_b=False, host=False)      # host tensors for the device path
+
+
+def test_binding_flag_constants_match_header():
+    """Every DWC_* flag / kernel id the binding names has the header's value (the binding passes
+    them as raw bits through dwc_params.flags), and _flags composes them."""
+    import re
+
+    from paper_1608_05179_b200 import dwc
+    hdr = open(os.path.join(ROOT, "include", "dwc.h")).read()
+    defs = {k: int(v) for k, v in re.findall(r"#define\s+(DWC_[A-Z0-9_]+)\s+(\d+)\b", hdr)}
+    names = [n for n in dir(dwc) if n.startswith("DWC_") and isinstance(getattr(dwc, n), int)]
+    assert "DWC_THROUGHPUT" in names and len(names) >= 8
+    for n in names:
+        assert n in defs and defs[n] == getattr(dwc, n), n
+    f = dwc._flags(True, 3, dr=True, alt=True, dense_stream=False, throughput=True)
+    assert f == (defs["DWC_FULL_GRID"] | defs["DWC_CUBIC"] | defs["DWC_DIAG_REMOVAL"] | defs["DWC_ALT_SWEEPS"] |
+                 defs["DWC_GS_RESIDUAL"] | defs["DWC_THROUGHPUT"])
