@@ -452,10 +452,15 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 const unsigned long long t0 = pf ? clk() : 0ull;
                 mbar_wait(&sh.stg_empty[sl], ((s / kRStg) & 1) ^ 1);
                 const unsigned long long t1 = pf ? clk() : 0ull;
-                // the mask of block k as the solver left it at the previous visit (a hint: the
-                // solver may be updating it right now when the block was visited < kRStg steps
-                // ago, either value is valid)
-                unsigned m = *(volatile unsigned *)&pmask[k];
+                // the mask of block k as the solver left it at its previous visit, when that visit
+                // is certainly complete (>= kRStg steps ago: this stage slot was released by the
+                // solver's step s - kRStg); a visit closer than that (systems of T < kRStg blocks,
+                // the turn of alternating sweeps) may still be running, and which value a racing read
+                // saw would decide which carries take the panel path and which the miss path -- a
+                // different fp32 summation order, so results would depend on timing.  Those steps
+                // stage the block's first kNP rows instead (deterministic).
+                const int dprev = alt ? 2 * pos + 1 : T;   // steps since block k's previous visit
+                unsigned m = (p == 0 || dprev >= kRStg) ? *(volatile unsigned *)&pmask[k] : ~0u;
                 DWC_DCHECK(k >= 0 && k < T, "panel producer: block");
                 unsigned st = 0;
                 for (int n = 0; m && n < kNP; n++) {
