@@ -108,7 +108,7 @@ constexpr int kRgsWin = RGS_WIN;
 // S5 + S6 on the tensor cores (k_psf.cu): int8 digit operands of the kept steering vectors
 // (opA: psf_opa_bytes, opB: psf_opb_bytes for sum rp rows; rsc: sum rp doubles), b~ = b[keep]
 // into bt (fp64, zero padded to sp; skipped when b is NULL), then A~_k over the (bin, I, J)
-// list of 128x64 output tiles touching the upper triangle, both triangles written.
+// list of 128x32 output tiles touching the upper triangle, both triangles written.
 // wt != NULL: diagonal removal (R20) -- the slice kernel writes |e_mr|^2 there (M doubles per
 // padded row, layout wt[r_off*M + m*rp + r]) and the epilogue forms the DR PSF.
 int psf_kp(int m);

@@ -459,7 +459,7 @@ rgs_kernel(int n_items, const int *__restrict__ order, const BinLayout *__restri
                 // saw would decide which carries take the panel path and which the miss path -- a
                 // different fp32 summation order, so results would depend on timing.  Those steps
                 // stage the block's first kNP rows instead (deterministic).
-                const int dprev = alt ? 2 * pos + 1 : T;   // steps since block k's previous visit
+                const int dprev = ALT ? 2 * pos + 1 : T;   // steps since block k's previous visit
                 unsigned m = (p == 0 || dprev >= kRStg) ? *(volatile unsigned *)&pmask[k] : ~0u;
                 DWC_DCHECK(k >= 0 && k < T, "panel producer: block");
                 unsigned st = 0;
