@@ -1,7 +1,7 @@
 """The device-checked library (libdwc_checked.so: -DDWC_CHECKED, device-side invariant checks on
 the Gauss-Seidel kernels' ring slots, parities, change lists and indices, plus mbarrier
-watchdogs that trap) runs the cfg3 band's longest-chain bins and cfg4/cfg5-shaped large systems
-on both GS kernels in a separate process.  It must finish without a trap and give results
+watchdogs that trap) runs the cfg3 band's longest-chain bins, its smallest systems with
+alternating sweeps, and cfg5-shaped large systems on both GS kernels in a separate process.  It must finish without a trap and give results
 bitwise identical to the production library's (the checks only observe)."""
 import os
 import subprocess
@@ -25,21 +25,22 @@ import paper_1608_05179_b200.dwc as D
 assert D.LIB_PATH.endswith({libname!r}), D.LIB_PATH
 c = Context(0)
 res = {{}}
-for name, bins, sweeps, full, dense in {cases!r}:
+for name, bins, sweeps, full, dense, alt in {cases!r}:
     band = synth.make_band(name, bins=bins)
     cfg = band.cfg
     g = Geometry(band.mic_xyz, cfg.n, cfg.side_len, cfg.z0, cfg.c0, cfg.cx, cfg.cy)
     out = c.solve_band(g, band.freqs, torch.from_numpy(band.csm).cuda(), cfg.epsilon, sweeps, cfg.eps_mode,
-                       full_grid=full, dense_stream=dense)
-    res[f"{{name}}_{{dense}}"] = out["x_map"].cpu().numpy()
-    res[f"{{name}}_{{dense}}_k"] = np.array([c.stats()["gs_kernel"]])
+                       full_grid=full, dense_stream=dense, alt=alt)
+    res[f"{{name}}_{{dense}}_{{alt}}"] = out["x_map"].cpu().numpy()
+    res[f"{{name}}_{{dense}}_{{alt}}_k"] = np.array([c.stats()["gs_kernel"]])
 np.savez({out!r}, **res)
 """
 
-CASES = [("cfg3", [249, 255, 224, 10, 11, 12], 1000, False, False),
-         ("cfg3", [249, 100], 300, False, True),
-         ("cfg5", [1023], 20, False, False),
-         ("cfg5", [1023], 20, False, True)]
+CASES = [("cfg3", [249, 255, 224, 10, 11, 12], 1000, False, False, False),
+         ("cfg3", [249, 100], 300, False, True, False),
+         ("cfg3", [0, 1, 2, 249], 300, False, False, True),   # systems of < 4 blocks, alternating sweeps
+         ("cfg5", [1023], 20, False, False, False),
+         ("cfg5", [1023], 20, False, True, False)]
 
 
 def _run(lib, out, tmp_path):
