@@ -14,8 +14,9 @@ Two measurements, both bracketed by barrier + cuda.synchronize and timed with CU
     each step timed alone with the L2 flushed (256 MiB write) between steps;
   * pipelined (the line's `value`, default; --no-pipeline keeps the sequential one): K
     consecutive bands -- new measurement blocks of the same scene, as a stream of acoustic
-    data delivers them -- on two contexts and two streams, so that a band's DAS / compress / PSF
-    run in the tail of the previous band's Gauss-Seidel sweeps; one event pair around the K
+    data delivers them -- on several contexts and streams (3 on one GPU, 8 for a rank's shard of
+    a sharded band; --contexts), each call with the DWC_THROUGHPUT hint, so that a band's DAS /
+    compress / PSF and sweeps run beside the previous bands' sweeps; one event pair around the K
     steps, every step reading a band no earlier step read (no L2 reuse; the L2 is flushed
     once before).  e2e likewise, one host thread per context (the host call returns with
     its outputs in host memory).
@@ -195,7 +196,7 @@ def variant_key(cfg, args) -> str:
 
 
 def run_pipelined(args, cfg, band, geom, ctx, dev, world, rank, strong, flush, gather_band):
-    """Consecutive bands on two contexts / streams (see run_ours).  Returns the per-step times of
+    """Consecutive bands on several contexts / streams (see run_ours).  Returns the per-step times of
     the device path and of the host path (CSMs from pinned host memory, outputs to pinned host
     memory, one host thread per context)."""
     import threading as th
@@ -530,9 +531,9 @@ def run_ours(args, cfg):
     d2h = K * 4 + K * S * 4 + K * S * 4
     seq = {"value": value, "ms_per_step": ms, "e2e_value": e2e_value, "e2e_ms_per_step": ems}
 
-    # pipelined: consecutive bands (new measurement blocks of the same scene) on two contexts and
-    # two streams, so that a band's DAS / compress / PSF run in the tail of the previous band's
-    # Gauss-Seidel sweeps.  Every timed step reads a band no earlier step read (no L2 reuse).
+    # pipelined: consecutive bands (new measurement blocks of the same scene) on several contexts
+    # and streams, so that a band's DAS / compress / PSF and sweeps run beside the previous bands'
+    # sweeps.  Every timed step reads a band no earlier step read (no L2 reuse).
     pipe = None
     if args.pipeline and not snapshots:
         pipe = run_pipelined(args, cfg, band, geom, ctx, dev, world, rank, strong, flush, gather_band)
@@ -640,7 +641,7 @@ def main():
     ap.add_argument("--no-throughput-hint", dest="throughput", action="store_false",
                     help="pipelined: do not pass DWC_THROUGHPUT (bands in flight) to the library")
     ap.add_argument("--no-pipeline", dest="pipeline", action="store_false",
-                    help="time one band at a time only (default: consecutive bands on two contexts and streams)")
+                    help="time one band at a time only (default: consecutive bands on several contexts and streams)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
